@@ -1,0 +1,239 @@
+// abi.cpp -- the extern "C" boundary (include/sdb.h): argument validation with
+// the reference's error taxonomy, context/workspace management, dispatch to
+// the sm_100a kernels.  No compute happens on the host.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/sdb.h"
+#include "ctx.h"
+#include "sdb_internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+int cuda_status(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return SDB_OK;
+    return fail(SDB_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+cudaStream_t pick(sdb_ctx* ctx, void* stream) {
+    return stream ? static_cast<cudaStream_t>(stream) : (ctx ? ctx->stream : nullptr);
+}
+
+int check_dtype(int d) { return (d == SDB_F32 || d == SDB_F16) ? SDB_OK : fail(SDB_PARAM, "unknown dtype"); }
+
+// conv2d_out_shape's checks, src/tensor.cpp:157-167
+int check_conv(int N, int H, int W, int C, int K, int R, int S, int stride, int pad) {
+    if (N < 1 || H < 1 || W < 1 || C < 1 || K < 1 || R < 1 || S < 1)
+        return fail(SDB_SHAPE, "conv2d: dims must be >= 1");
+    if (stride < 1 || pad < 0) return fail(SDB_SHAPE, "conv2d: stride >= 1, pad >= 0 required");
+    if (H + 2 * pad < R || W + 2 * pad < S) return fail(SDB_SHAPE, "conv2d: kernel larger than padded input");
+    return SDB_OK;
+}
+
+}  // namespace
+
+void* sdb_ctx::scratch(size_t bytes) {
+    if (bytes <= ws_bytes) return ws;
+    if (ws) {
+        cudaStreamSynchronize(stream);
+        cudaFree(ws);
+    }
+    ws_bytes = std::max(bytes, ws_bytes * 2);
+    if (cudaMalloc(&ws, ws_bytes) != cudaSuccess) {
+        ws = nullptr;
+        ws_bytes = 0;
+    }
+    return ws;
+}
+
+extern "C" {
+
+const char* sdb_last_error(void) { return g_err.c_str(); }
+int sdb_version(void) { return 1; }
+
+int sdb_ctx_create(int device, int rank, int world, const void* nccl_id, sdb_ctx** out) {
+    if (!out) return fail(SDB_PARAM, "null out");
+    if (world < 1 || rank < 0 || rank >= world) return fail(SDB_PARAM, "invalid rank/world");
+    if (int rc = cuda_status(cudaSetDevice(device), "cudaSetDevice")) return rc;
+    auto* c = new sdb_ctx();
+    c->device = device;
+    c->rank = rank;
+    c->world = world;
+    if (int rc = cuda_status(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream")) {
+        delete c;
+        return rc;
+    }
+    if (world > 1) {
+        if (!nccl_id) {
+            delete c;
+            return fail(SDB_PARAM, "world > 1 requires an nccl unique id");
+        }
+        if (int rc = sdb::comm_init(c, nccl_id)) {
+            delete c;
+            return rc;
+        }
+    }
+    *out = c;
+    return SDB_OK;
+}
+
+int sdb_ctx_destroy(sdb_ctx* ctx) {
+    if (!ctx) return SDB_OK;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    sdb::comm_destroy(ctx);
+    if (ctx->ws) cudaFree(ctx->ws);
+    cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    return SDB_OK;
+}
+
+void* sdb_ctx_stream(sdb_ctx* ctx) { return ctx ? ctx->stream : nullptr; }
+
+int sdb_synchronize(sdb_ctx* ctx) {
+    if (!ctx) return fail(SDB_PARAM, "null ctx");
+    return cuda_status(cudaStreamSynchronize(ctx->stream), "synchronize");
+}
+
+int sdb_get_nccl_unique_id(void* out128) { return sdb::comm_unique_id(out128); }
+
+int sdb_conv_fprop(sdb_ctx* ctx, int dtype, const void* x, const void* w, void* y, int N, int H, int W, int C, int K,
+                   int R, int S, int stride, int pad, void* stream) {
+    if (int rc = check_dtype(dtype)) return rc;
+    if (int rc = check_conv(N, H, W, C, K, R, S, stride, pad)) return rc;
+    const sdb::ConvShape g{N, H, W, C, K, R, S, stride, pad};
+    return cuda_status(sdb::conv_fprop(g, dtype, x, w, y, pick(ctx, stream)), "conv_fprop");
+}
+
+int sdb_conv_dgrad(sdb_ctx* ctx, int dtype, const void* dy, const void* w, void* dx, int N, int H, int W, int C, int K,
+                   int R, int S, int stride, int pad, int accumulate, void* stream) {
+    if (int rc = check_dtype(dtype)) return rc;
+    if (int rc = check_conv(N, H, W, C, K, R, S, stride, pad)) return rc;
+    const sdb::ConvShape g{N, H, W, C, K, R, S, stride, pad};
+    return cuda_status(sdb::conv_dgrad(g, dtype, dy, w, dx, accumulate, pick(ctx, stream)), "conv_dgrad");
+}
+
+int sdb_conv_wgrad(sdb_ctx* ctx, int dtype, const void* x, const void* dy, void* dw, int N, int H, int W, int C, int K,
+                   int R, int S, int stride, int pad, void* stream) {
+    if (!ctx) return fail(SDB_PARAM, "conv_wgrad needs a context (workspace)");
+    if (int rc = check_dtype(dtype)) return rc;
+    if (int rc = check_conv(N, H, W, C, K, R, S, stride, pad)) return rc;
+    const sdb::ConvShape g{N, H, W, C, K, R, S, stride, pad};
+    const size_t wsb = sdb::conv_wgrad_workspace(g, dtype);
+    void* ws = ctx->scratch(wsb);
+    if (!ws) return fail(SDB_CUDA, "workspace allocation failed");
+    return cuda_status(sdb::conv_wgrad(g, dtype, x, dy, dw, ws, wsb, pick(ctx, stream)), "conv_wgrad");
+}
+
+static int check_norm(int dtype, int64_t rows, int C) {
+    if (int rc = check_dtype(dtype)) return rc;
+    if (rows < 2) return fail(SDB_DEGENERATE, "batch norm needs at least 2 values per channel");
+    if (!sdb::norm_channels_ok(C)) return fail(SDB_UNSUPPORTED, "norm kernels need C % 8 == 0, C <= 2048, C | 2048");
+    return SDB_OK;
+}
+
+int sdb_bn_fwd(sdb_ctx* ctx, int dtype, const void* x, const float* gamma, const float* beta, void* y, float* mean,
+               float* invstd, int64_t rows, int C, float eps, int relu, void* stream) {
+    if (!ctx) return fail(SDB_PARAM, "null ctx");
+    if (int rc = check_norm(dtype, rows, C)) return rc;
+    void* ws = ctx->scratch(sdb::norm_workspace_bytes(rows, C));
+    return cuda_status(sdb::bn_forward(dtype, x, gamma, beta, y, mean, invstd, rows, C, eps, relu ? 1 : 0, 1.0f, ws,
+                                       pick(ctx, stream)),
+                       "bn_fwd");
+}
+
+int sdb_bn_bwd(sdb_ctx* ctx, int dtype, const void* dy, const void* x, const void* y_relu, const float* gamma,
+               const float* mean, const float* invstd, void* dx, float* dgamma, float* dbeta, int64_t rows, int C,
+               void* stream) {
+    if (!ctx) return fail(SDB_PARAM, "null ctx");
+    if (int rc = check_norm(dtype, rows, C)) return rc;
+    void* ws = ctx->scratch(sdb::norm_workspace_bytes(rows, C));
+    return cuda_status(sdb::bn_backward(dtype, dy, x, y_relu, gamma, mean, invstd, dx, dgamma, dbeta, rows, C, ws,
+                                        pick(ctx, stream)),
+                       "bn_bwd");
+}
+
+// iabn_forward's contract checks, src/memopt.cpp:229-235
+static int check_iabn_params(sdb_ctx* ctx, const float* gamma, int C, float slope, cudaStream_t st) {
+    if (!(slope > 0.0f)) return fail(SDB_NONINVERTIBLE, "iabn requires a strictly positive leaky slope");
+    std::vector<float> g(static_cast<size_t>(C));
+    if (int rc = cuda_status(cudaMemcpyAsync(g.data(), gamma, C * sizeof(float), cudaMemcpyDeviceToHost, st), "gamma"))
+        return rc;
+    if (int rc = cuda_status(cudaStreamSynchronize(st), "gamma sync")) return rc;
+    for (float v : g)
+        if (v == 0.0f) return fail(SDB_NONINVERTIBLE, "iabn requires gamma != 0 in every channel");
+    (void)ctx;
+    return SDB_OK;
+}
+
+int sdb_iabn_fwd(sdb_ctx* ctx, int dtype, const void* x, const float* gamma, const float* beta, void* y, float* mean,
+                 float* invstd, int64_t rows, int C, float eps, float slope, void* stream) {
+    if (!ctx) return fail(SDB_PARAM, "null ctx");
+    if (int rc = check_norm(dtype, rows, C)) return rc;
+    if (int rc = check_iabn_params(ctx, gamma, C, slope, pick(ctx, stream))) return rc;
+    void* ws = ctx->scratch(sdb::norm_workspace_bytes(rows, C));
+    return cuda_status(
+        sdb::bn_forward(dtype, x, gamma, beta, y, mean, invstd, rows, C, eps, 2, slope, ws, pick(ctx, stream)),
+        "iabn_fwd");
+}
+
+int sdb_iabn_bwd(sdb_ctx* ctx, int dtype, const void* dy, const void* y, const float* gamma, const float* beta,
+                 const float* mean, const float* invstd, void* dx, float* dgamma, float* dbeta, int64_t rows, int C,
+                 float slope, void* stream) {
+    if (!ctx) return fail(SDB_PARAM, "null ctx");
+    if (int rc = check_norm(dtype, rows, C)) return rc;
+    if (!(slope > 0.0f)) return fail(SDB_NONINVERTIBLE, "iabn requires a strictly positive leaky slope");
+    void* ws = ctx->scratch(sdb::norm_workspace_bytes(rows, C));
+    return cuda_status(sdb::iabn_backward(dtype, dy, y, gamma, beta, mean, invstd, dx, dgamma, dbeta, rows, C, slope,
+                                          ws, pick(ctx, stream)),
+                       "iabn_bwd");
+}
+
+int sdb_nonfinite(sdb_ctx* ctx, int dtype, const void* g, int64_t n, int* flag, void* stream) {
+    if (int rc = check_dtype(dtype)) return rc;
+    return cuda_status(sdb::nonfinite_check(dtype, g, n, flag, pick(ctx, stream)), "nonfinite");
+}
+
+int sdb_fused_sgd(sdb_ctx* ctx, int gdtype, const void* gsum, float* w, float* v, void* w16, int64_t n, float lr,
+                  float momentum, const double* scale, double denom_mult, const int* flag, void* stream) {
+    if (int rc = check_dtype(gdtype)) return rc;
+    if (n < 0) return fail(SDB_CONTRACT, "negative parameter count");
+    return cuda_status(sdb::fused_sgd(gdtype, gsum, w, v, static_cast<__half*>(w16), n, lr, momentum, scale,
+                                      denom_mult, flag, pick(ctx, stream)),
+                       "fused_sgd");
+}
+
+int sdb_update_scale(sdb_ctx* ctx, double* scale, int64_t* good_steps, const int* flag, int dynamic,
+                     int64_t growth_interval, double growth, double backoff, double min_scale, double max_scale,
+                     void* stream) {
+    // LossScaleState::validate's policy checks, src/precision.cpp:20-30
+    if (growth_interval < 1 || growth <= 1.0 || backoff <= 0.0 || backoff >= 1.0)
+        return fail(SDB_CONTRACT, "invalid loss scale policy parameters");
+    return cuda_status(sdb::update_scale_device(scale, good_steps, flag, dynamic, growth_interval, growth, backoff,
+                                                min_scale, max_scale, pick(ctx, stream)),
+                       "update_scale");
+}
+
+int sdb_cast(sdb_ctx* ctx, int src_dtype, const void* src, int dst_dtype, void* dst, int64_t n, void* stream) {
+    cudaStream_t st = pick(ctx, stream);
+    if (src_dtype == SDB_F32 && dst_dtype == SDB_F16)
+        return cuda_status(sdb::cast_f32_f16(static_cast<const float*>(src), static_cast<__half*>(dst), n, st), "cast");
+    if (src_dtype == SDB_F16 && dst_dtype == SDB_F32)
+        return cuda_status(sdb::cast_f16_f32(static_cast<const __half*>(src), static_cast<float*>(dst), n, st), "cast");
+    return fail(SDB_PARAM, "unsupported cast");
+}
+
+}  // extern "C"

@@ -1,0 +1,624 @@
+// conv.cu -- convolution (reference K1/K2: src/tensor.cpp:157-196 forward,
+// src/autograd.cpp:290-320 backward) as implicit GEMM on the sm_100a tensor
+// cores (tcgen05.mma kind::f16, fp32 accumulators in TMEM).
+//
+// Layouts: activations NHWC, filters KRSC ([out][kh][kw][in]), fp16 storage,
+// fp32 accumulation, outputs rounded RNE (the reference's fp16 contract,
+// src/tensor.cpp:79-82 + 195).
+//
+//   fprop : Y[m=(n,oh,ow)][k]     = sum_{(r,s,c)} X[n,oh*st-p+r,ow*st-p+s,c] * W[k,r,s,c]
+//   dgrad : DX[m=(n,h,w)][c]      = sum_{(r,s,k)} DY[n,(h+p-r)/st,(w+p-s)/st,k] * W[k,r,s,c]
+//           (sub-pixel phases: each stride phase (h%st,w%st) is its own GEMM over
+//            the taps that land on it, so stride-2 layers waste no MACs)
+//   wgrad : DW[k][(r,s,c)]        = sum_{m=(n,oh,ow)} DY[m][k] * X[n,oh*st-p+r,ow*st-p+s,c]
+//           (deterministic split-K over m: fp32 partials reduced in fixed order)
+//
+// Mainloop: 4 producer warps gather the implicit-im2col tiles with 16-byte
+// cp.async (zero-fill gives the padding) straight into the UMMA SWIZZLE_128B
+// canonical layouts (K-major or MN-major, so no transposes are ever
+// materialised), completion is published through mbarriers after a
+// fence.proxy.async; one elected thread issues tcgen05.mma into TMEM and
+// releases stages with tcgen05.commit; the same 4 warps then drain TMEM with
+// tcgen05.ld and write the epilogue.  A CUDA-core variant of the same GEMM
+// views serves fp32 mode (config C1: reference-precision) and odd channel
+// counts.
+#include <algorithm>
+#include <cstdio>
+
+#include "common.cuh"
+#include "sdb_internal.h"
+
+namespace sdb {
+
+enum ConvMode { FPROP = 0, DGRAD = 1, WGRAD = 2 };
+
+struct ConvArgs {
+    const void* x;   // fprop/wgrad: input activation; dgrad: DY
+    const void* w;   // fprop/dgrad: filter; wgrad: DY
+    void* out;       // fprop: Y, dgrad: DX, wgrad: DW or fp32 partials
+    int N, H, W, C, K, R, S, stride, pad, Ho, Wo;
+    int M, NG, KG;   // GEMM extents
+    // dgrad phase
+    int ph, pw, Hp, Wp, r0, nr, q0, nq;
+    // wgrad split-K
+    int kb_per_split;
+    int accumulate;  // dgrad: out += result
+};
+
+// ============================================================ tcgen05 kernel
+constexpr int kBM = 128, kBK = 64;
+
+template <int MODE, int BN, int ST>
+struct TcCfg {
+    static constexpr int kABytes = kBM * kBK * 2;
+    static constexpr int kBBytes = BN * kBK * 2;
+    static constexpr int kStage = kABytes + kBBytes;
+    static constexpr int kSmem = ST * kStage + 1024 + 256;
+    static constexpr bool kAMN = MODE == WGRAD;                  // A MN-major?
+    static constexpr bool kBMN = MODE == DGRAD || MODE == WGRAD; // B MN-major?
+    static constexpr int kLag = ST - 1;
+};
+
+// byte offset of 16B chunk inside a K-major SW128 tile: (row, chunk of 8 k)
+SDB_DEV uint32_t kmaj_off(int row, int chunk) {
+    return static_cast<uint32_t>((row >> 3) * 1024 + (row & 7) * 128 + (((chunk ^ row) & 7) << 4));
+}
+// byte offset of 16B chunk inside an MN-major SW128 tile of MN extent E:
+// (mn chunk index mc = mn/8, k row)
+SDB_DEV uint32_t mnmaj_off(int mc, int k, int E) {
+    return static_cast<uint32_t>((k >> 3) * (E / 64) * 1024 + (mc >> 3) * 1024 + (k & 7) * 128 +
+                                 (((mc ^ k) & 7) << 4));
+}
+
+template <int MODE, int BN, int ST>
+__global__ void __launch_bounds__(160, 1) conv_tc_kernel(ConvArgs a) {
+    using Cfg = TcCfg<MODE, BN, ST>;
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    uint8_t* gbase = smem_raw + (base - raw);
+    uint64_t* full = reinterpret_cast<uint64_t*>(gbase + ST * Cfg::kStage);
+    uint64_t* empty = full + ST;
+    uint64_t* done = empty + ST;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int m0 = blockIdx.x * kBM, n0 = blockIdx.y * BN;
+    const int nkb_total = (a.KG + kBK - 1) / kBK;
+    const int kb0 = MODE == WGRAD ? blockIdx.z * a.kb_per_split : 0;
+    const int nk = MODE == WGRAD ? max(0, min(a.kb_per_split, nkb_total - kb0)) : nkb_total;
+
+    if (tid == 0) {
+        for (int s = 0; s < ST; ++s) {
+            mbar_init(&full[s], 128);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(done, 1);
+        mbar_fence_init();
+    }
+    if (warp == 4) tmem_alloc(tmem_slot, BN);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp < 4) {
+        // ------------------------------------------------ producers
+        const __half* X = static_cast<const __half*>(a.x);
+        const __half* Wt = static_cast<const __half*>(a.w);
+        const int HoWo = a.Ho * a.Wo;
+        // per-thread precomputation for the gathered operand rows
+        int rowN[8], rowY[8], rowX[8];  // A rows (fprop/dgrad): image, base y, base x
+        if (MODE == FPROP || MODE == DGRAD) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int m = m0 + (tid >> 3) + 16 * i;
+                if (m < a.M) {
+                    if (MODE == FPROP) {
+                        const int n = m / HoWo, rem = m - n * HoWo, oh = rem / a.Wo, ow = rem - oh * a.Wo;
+                        rowN[i] = n;
+                        rowY[i] = oh * a.stride - a.pad;
+                        rowX[i] = ow * a.stride - a.pad;
+                    } else {
+                        const int HpWp = a.Hp * a.Wp;
+                        const int n = m / HpWp, rem = m - n * HpWp, i2 = rem / a.Wp, j2 = rem - i2 * a.Wp;
+                        rowN[i] = n;
+                        rowY[i] = a.ph + a.stride * i2 + a.pad;  // h + p
+                        rowX[i] = a.pw + a.stride * j2 + a.pad;
+                    }
+                } else {
+                    rowN[i] = -1;
+                    rowY[i] = rowX[i] = 0;
+                }
+            }
+        }
+        // wgrad B: the thread's fixed column chunk (tap, c)
+        constexpr int kBChunksPerRow = BN / 8;           // MN-major B: chunks per k row
+        constexpr int kBRowStep = 128 / kBChunksPerRow;  // k rows advanced per i
+        int wg_r = 0, wg_s = 0, wg_c = 0;
+        bool wg_ok = false;
+        if (MODE == WGRAD) {
+            const int col = n0 + (tid % kBChunksPerRow) * 8;
+            wg_ok = col < a.NG;
+            const int tap = col / a.C;
+            wg_c = col - tap * a.C;
+            wg_r = tap / a.S;
+            wg_s = tap - wg_r * a.S;
+        }
+
+        for (int it = 0; it < nk; ++it) {
+            const int s = it % ST;
+            if (it >= ST) mbar_wait(&empty[s], ((it / ST) - 1) & 1);
+            const uint32_t sa = base + s * Cfg::kStage;
+            const uint32_t sb = sa + Cfg::kABytes;
+            const int kb = kb0 + it;
+            if (MODE == FPROP) {
+                // A: rows m, chunk = tid&7 -> kg = kb*64 + 8*(tid&7)
+                const int kg = kb * kBK + 8 * (tid & 7);
+                const bool kok = kg < a.KG;
+                const int tap = kg / a.C, c = kg - tap * a.C;
+                const int r = tap / a.S, q = tap - r * a.S;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int row = (tid >> 3) + 16 * i;
+                    const int ih = rowY[i] + r, iw = rowX[i] + q;
+                    const bool ok = kok && rowN[i] >= 0 && ih >= 0 && ih < a.H && iw >= 0 && iw < a.W;
+                    const __half* src = ok ? X + ((static_cast<int64_t>(rowN[i]) * a.H + ih) * a.W + iw) * a.C + c : X;
+                    cp_async16(sa + kmaj_off(row, tid & 7), src, ok ? 16u : 0u);
+                }
+                // B: filter rows (k-major): rows = out channels
+#pragma unroll
+                for (int i = 0; i < BN / 16; ++i) {
+                    const int row = (tid >> 3) + 16 * i;
+                    const int j = n0 + row;
+                    const bool ok = kok && j < a.NG;
+                    const __half* src = ok ? Wt + static_cast<int64_t>(j) * a.KG + kg : Wt;
+                    cp_async16(sb + kmaj_off(row, tid & 7), src, ok ? 16u : 0u);
+                }
+            } else if (MODE == DGRAD) {
+                // A: DY gather, k-major over kg = tap*K + kout
+                const int kg = kb * kBK + 8 * (tid & 7);
+                const bool kok = kg < a.KG;
+                const int t = kg / a.K, kout = kg - t * a.K;
+                const int r = a.r0 + a.stride * (t / a.nq), q = a.q0 + a.stride * (t % a.nq);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int row = (tid >> 3) + 16 * i;
+                    const int yy = rowY[i] - r, xx = rowX[i] - q;  // (h+p-r), (w+p-q), multiples of stride
+                    const int oh = yy / a.stride, ow = xx / a.stride;
+                    const bool ok = kok && rowN[i] >= 0 && yy >= 0 && xx >= 0 && oh < a.Ho && ow < a.Wo;
+                    const __half* src =
+                        ok ? X + ((static_cast<int64_t>(rowN[i]) * a.Ho + oh) * a.Wo + ow) * a.K + kout : X;
+                    cp_async16(sa + kmaj_off(row, tid & 7), src, ok ? 16u : 0u);
+                }
+                // B: filter as MN-major [c][kg]: chunk = 8 consecutive c at one kg row
+#pragma unroll
+                for (int i = 0; i < BN / 16; ++i) {
+                    const int krow = tid / kBChunksPerRow + kBRowStep * i;
+                    const int mc = tid % kBChunksPerRow;
+                    const int kg2 = kb * kBK + krow;
+                    const int c = n0 + mc * 8;
+                    const bool ok = kg2 < a.KG && c < a.NG;
+                    const int t2 = kg2 / a.K, ko2 = kg2 - t2 * a.K;
+                    const int r2 = a.r0 + a.stride * (t2 / a.nq), q2 = a.q0 + a.stride * (t2 % a.nq);
+                    const __half* src = ok ? Wt + ((static_cast<int64_t>(ko2) * a.R + r2) * a.S + q2) * a.C + c : Wt;
+                    cp_async16(sb + mnmaj_off(mc, krow, BN), src, ok ? 16u : 0u);
+                }
+            } else {
+                // WGRAD. A = DY^T as MN-major [kout][m]: chunk = 8 kout at one pixel row
+                const __half* DY = static_cast<const __half*>(a.w);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int krow = (tid >> 4) + 8 * i;
+                    const int mc = tid & 15;
+                    const int m = kb * kBK + krow;
+                    const int ko = m0 + mc * 8;
+                    const bool ok = m < a.KG && ko < a.M;
+                    const __half* src = ok ? DY + static_cast<int64_t>(m) * a.K + ko : DY;
+                    cp_async16(sa + mnmaj_off(mc, krow, kBM), src, ok ? 16u : 0u);
+                }
+                // B = im2col(X)^T as MN-major [(r,s,c)][m]
+#pragma unroll
+                for (int i = 0; i < BN / 16; ++i) {
+                    const int krow = tid / kBChunksPerRow + kBRowStep * i;
+                    const int mc = tid % kBChunksPerRow;
+                    const int m = kb * kBK + krow;
+                    bool ok = wg_ok && m < a.KG;
+                    const __half* src = X;
+                    if (ok) {
+                        const int n = m / HoWo, rem = m - n * HoWo, oh = rem / a.Wo, ow = rem - oh * a.Wo;
+                        const int ih = oh * a.stride - a.pad + wg_r, iw = ow * a.stride - a.pad + wg_s;
+                        ok = ih >= 0 && ih < a.H && iw >= 0 && iw < a.W;
+                        if (ok) src = X + ((static_cast<int64_t>(n) * a.H + ih) * a.W + iw) * a.C + wg_c;
+                    }
+                    cp_async16(sb + mnmaj_off(mc, krow, BN), src, ok ? 16u : 0u);
+                }
+            }
+            cp_async_commit();
+            if (it >= Cfg::kLag) {
+                cp_async_wait<Cfg::kLag>();
+                fence_proxy_async();
+                mbar_arrive(&full[(it - Cfg::kLag) % ST]);
+            }
+        }
+        cp_async_wait<0>();
+        fence_proxy_async();
+        for (int it = max(0, nk - Cfg::kLag); it < nk; ++it) mbar_arrive(&full[it % ST]);
+
+        // ------------------------------------------------ epilogue
+        const int row_local = warp * 32 + (tid & 31);
+        const int grow = m0 + row_local;
+        if (nk > 0) {
+            mbar_wait(done, 0);
+            tc_fence_after();
+        }
+        // output row pointer
+        int64_t out_row = -1;
+        if (grow < a.M) {
+            if (MODE == FPROP) {
+                out_row = static_cast<int64_t>(grow) * a.NG;
+            } else if (MODE == DGRAD) {
+                const int HpWp = a.Hp * a.Wp;
+                const int n = grow / HpWp, rem = grow - n * HpWp, i2 = rem / a.Wp, j2 = rem - i2 * a.Wp;
+                const int h = a.ph + a.stride * i2, w = a.pw + a.stride * j2;
+                out_row = ((static_cast<int64_t>(n) * a.H + h) * a.W + w) * a.C;
+            } else {
+                out_row = (static_cast<int64_t>(blockIdx.z) * a.M + grow) * a.NG;
+            }
+        }
+#pragma unroll 1
+        for (int cb = 0; cb < BN; cb += 32) {
+            uint32_t v[32];
+            if (nk > 0) {
+                tmem_ld32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + cb, v);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = 0u;
+            }
+            if (out_row < 0) continue;
+            const int col0 = n0 + cb;
+            if (MODE == WGRAD) {
+                float* o = static_cast<float*>(a.out) + out_row + col0;
+                if (col0 + 32 <= a.NG && (a.NG & 3) == 0) {
+#pragma unroll
+                    for (int j = 0; j < 32; j += 4)
+                        *reinterpret_cast<float4*>(o + j) = make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]),
+                                                                        __uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
+                } else {
+                    for (int j = 0; j < 32 && col0 + j < a.NG; ++j) o[j] = __uint_as_float(v[j]);
+                }
+            } else {
+                __half* o = static_cast<__half*>(a.out) + out_row + col0;
+                const int lim = MODE == FPROP ? a.NG : a.C;
+                if (col0 + 32 <= lim && (lim & 7) == 0) {
+#pragma unroll
+                    for (int j = 0; j < 32; j += 8) {
+                        float f[8];
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(v[j + e]);
+                        if (MODE == DGRAD && a.accumulate) {
+                            const uint4 old = *reinterpret_cast<const uint4*>(o + j);
+                            const __half* oh = reinterpret_cast<const __half*>(&old);
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) f[e] += __half2float(oh[e]);
+                        }
+                        uint4 pk;
+                        __half2* p2 = reinterpret_cast<__half2*>(&pk);
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) p2[e] = __floats2half2_rn(f[2 * e], f[2 * e + 1]);
+                        *reinterpret_cast<uint4*>(o + j) = pk;
+                    }
+                } else {
+                    for (int j = 0; j < 32 && col0 + j < lim; ++j) {
+                        float f = __uint_as_float(v[j]);
+                        if (MODE == DGRAD && a.accumulate) f += __half2float(o[j]);
+                        o[j] = __float2half_rn(f);
+                    }
+                }
+            }
+        }
+    } else if (tid == 128) {
+        // ------------------------------------------------ MMA issuer (one thread)
+        constexpr uint32_t idesc = umma_idesc_f16(kBM, BN, Cfg::kAMN ? 1 : 0, Cfg::kBMN ? 1 : 0);
+        for (int it = 0; it < nk; ++it) {
+            const int s = it % ST;
+            mbar_wait(&full[s], (it / ST) & 1);
+            tc_fence_after();
+            const uint32_t sa = base + s * Cfg::kStage;
+            const uint32_t sb = sa + Cfg::kABytes;
+#pragma unroll
+            for (int kk = 0; kk < kBK / 16; ++kk) {
+                const uint64_t ad = Cfg::kAMN ? umma_desc_sw128(sa + kk * 2 * 2048, 1024, 2048)
+                                              : umma_desc_sw128(sa + kk * 32, 16, 1024);
+                const uint64_t bd = Cfg::kBMN ? umma_desc_sw128(sb + kk * 2 * (BN / 64) * 1024, 1024, (BN / 64) * 1024)
+                                              : umma_desc_sw128(sb + kk * 32, 16, 1024);
+                umma_f16(tmem, ad, bd, idesc, (it > 0 || kk > 0) ? 1u : 0u);
+            }
+            umma_commit(&empty[s]);
+        }
+        if (nk > 0) umma_commit(done);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 4) {
+        tc_fence_after();
+        tmem_dealloc(tmem, BN);
+    }
+}
+
+// ============================================================ CUDA-core kernel
+// Same GEMM views, scalar gathers, 64x64x16 tiles; fp32 or fp16 storage.
+template <class T>
+SDB_DEV float a_elem(const ConvArgs& a, int mode, int m, int kg) {
+    const T* X = static_cast<const T*>(a.x);
+    if (m >= a.M || kg >= a.KG) return 0.f;
+    if (mode == FPROP) {
+        const int HoWo = a.Ho * a.Wo;
+        const int n = m / HoWo, rem = m - n * HoWo, oh = rem / a.Wo, ow = rem - oh * a.Wo;
+        const int tap = kg / a.C, c = kg - tap * a.C, r = tap / a.S, q = tap - r * a.S;
+        const int ih = oh * a.stride - a.pad + r, iw = ow * a.stride - a.pad + q;
+        if (ih < 0 || ih >= a.H || iw < 0 || iw >= a.W) return 0.f;
+        return to_f<T>(X[((static_cast<int64_t>(n) * a.H + ih) * a.W + iw) * a.C + c]);
+    } else if (mode == DGRAD) {
+        const int HpWp = a.Hp * a.Wp;
+        const int n = m / HpWp, rem = m - n * HpWp, i2 = rem / a.Wp, j2 = rem - i2 * a.Wp;
+        const int t = kg / a.K, kout = kg - t * a.K;
+        const int r = a.r0 + a.stride * (t / a.nq), q = a.q0 + a.stride * (t % a.nq);
+        const int yy = a.ph + a.stride * i2 + a.pad - r, xx = a.pw + a.stride * j2 + a.pad - q;
+        if (yy < 0 || xx < 0) return 0.f;
+        const int oh = yy / a.stride, ow = xx / a.stride;
+        if (oh >= a.Ho || ow >= a.Wo) return 0.f;
+        return to_f<T>(X[((static_cast<int64_t>(n) * a.Ho + oh) * a.Wo + ow) * a.K + kout]);
+    } else {
+        const T* DY = static_cast<const T*>(a.w);
+        return to_f<T>(DY[static_cast<int64_t>(kg) * a.K + m]);  // A[kout][pixel]
+    }
+}
+
+template <class T>
+SDB_DEV float b_elem(const ConvArgs& a, int mode, int j, int kg) {
+    if (j >= a.NG || kg >= a.KG) return 0.f;
+    if (mode == FPROP) {
+        return to_f<T>(static_cast<const T*>(a.w)[static_cast<int64_t>(j) * a.KG + kg]);
+    } else if (mode == DGRAD) {
+        const int t = kg / a.K, kout = kg - t * a.K;
+        const int r = a.r0 + a.stride * (t / a.nq), q = a.q0 + a.stride * (t % a.nq);
+        return to_f<T>(static_cast<const T*>(a.w)[((static_cast<int64_t>(kout) * a.R + r) * a.S + q) * a.C + j]);
+    } else {
+        const T* X = static_cast<const T*>(a.x);
+        const int HoWo = a.Ho * a.Wo;
+        const int m = kg;
+        const int n = m / HoWo, rem = m - n * HoWo, oh = rem / a.Wo, ow = rem - oh * a.Wo;
+        const int tap = j / a.C, c = j - tap * a.C, r = tap / a.S, q = tap - r * a.S;
+        const int ih = oh * a.stride - a.pad + r, iw = ow * a.stride - a.pad + q;
+        if (ih < 0 || ih >= a.H || iw < 0 || iw >= a.W) return 0.f;
+        return to_f<T>(X[((static_cast<int64_t>(n) * a.H + ih) * a.W + iw) * a.C + c]);
+    }
+}
+
+template <class T, int MODE>
+__global__ void __launch_bounds__(256) conv_simt_kernel(ConvArgs a) {
+    __shared__ float As[16][64 + 4];
+    __shared__ float Bs[16][64 + 4];
+    const int tid = threadIdx.x;
+    const int m0 = blockIdx.x * 64, n0 = blockIdx.y * 64;
+    const int tx = tid & 15, ty = tid >> 4;
+    const int nkb_total = (a.KG + 15) / 16;
+    int kb0 = 0, kb1 = nkb_total;
+    if (MODE == WGRAD) {
+        kb0 = blockIdx.z * a.kb_per_split;
+        kb1 = min(nkb_total, kb0 + a.kb_per_split);
+    }
+    float acc[4][4] = {};
+    for (int kb = kb0; kb < kb1; ++kb) {
+        for (int e = tid; e < 16 * 64; e += 256) {
+            const int kk = e / 64, mm = e % 64;
+            As[kk][mm] = a_elem<T>(a, MODE, m0 + mm, kb * 16 + kk);
+            Bs[kk][mm] = b_elem<T>(a, MODE, n0 + mm, kb * 16 + kk);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) {
+            float av[4], bv[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) av[i] = As[kk][ty * 4 + i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bv[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] += av[i] * bv[j];
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int m = m0 + ty * 4 + i;
+        if (m >= a.M) continue;
+        int64_t row;
+        if (MODE == FPROP) {
+            row = static_cast<int64_t>(m) * a.NG;
+        } else if (MODE == DGRAD) {
+            const int HpWp = a.Hp * a.Wp;
+            const int n = m / HpWp, rem = m - n * HpWp, i2 = rem / a.Wp, j2 = rem - i2 * a.Wp;
+            row = ((static_cast<int64_t>(n) * a.H + a.ph + a.stride * i2) * a.W + a.pw + a.stride * j2) * a.C;
+        } else {
+            row = (static_cast<int64_t>(blockIdx.z) * a.M + m) * a.NG;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int n = n0 + tx * 4 + j;
+            if (n >= a.NG) continue;
+            if (MODE == WGRAD) {
+                static_cast<float*>(a.out)[row + n] = acc[i][j];
+            } else {
+                T* o = static_cast<T*>(a.out) + row + n;
+                float f = acc[i][j];
+                if (MODE == DGRAD && a.accumulate) f += to_f<T>(*o);
+                *o = from_f<T>(f);
+            }
+        }
+    }
+}
+
+// deterministic split-K reduction: dw[i] = sum_s ws[s][i] (fixed order), cast
+template <class T>
+__global__ void wgrad_reduce_kernel(const float* __restrict__ ws, int splits, int64_t n, T* __restrict__ dw) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        float s = 0.f;
+        for (int k = 0; k < splits; ++k) s += ws[k * n + i];
+        dw[i] = from_f<T>(s);
+    }
+}
+
+// zero the dgrad output positions of a phase with no taps
+template <class T>
+__global__ void dgrad_zero_phase_kernel(ConvArgs a) {
+    const int64_t total = static_cast<int64_t>(a.M) * a.C;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int m = static_cast<int>(e / a.C), c = static_cast<int>(e % a.C);
+        const int HpWp = a.Hp * a.Wp;
+        const int n = m / HpWp, rem = m - n * HpWp, i2 = rem / a.Wp, j2 = rem - i2 * a.Wp;
+        T* o = static_cast<T*>(a.out) +
+               ((static_cast<int64_t>(n) * a.H + a.ph + a.stride * i2) * a.W + a.pw + a.stride * j2) * a.C + c;
+        if (!a.accumulate) *o = from_f<T>(0.f);
+    }
+}
+
+// ============================================================ launchers
+template <int MODE, int BN, int ST>
+static cudaError_t launch_tc(const ConvArgs& a, int splits, cudaStream_t st) {
+    using Cfg = TcCfg<MODE, BN, ST>;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(conv_tc_kernel<MODE, BN, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
+        configured = true;
+    }
+    dim3 grid((a.M + kBM - 1) / kBM, (a.NG + BN - 1) / BN, splits);
+    conv_tc_kernel<MODE, BN, ST><<<grid, 160, Cfg::kSmem, st>>>(a);
+    return cudaGetLastError();
+}
+
+template <int MODE>
+static cudaError_t launch_tc_pick(const ConvArgs& a, int splits, cudaStream_t st) {
+    if (a.NG <= 64) return launch_tc<MODE, 64, 4>(a, splits, st);
+    const int64_t tiles128 = static_cast<int64_t>((a.M + 127) / 128) * ((a.NG + 127) / 128) * splits;
+    if (a.NG >= 256 && tiles128 >= 2 * kNumSMs) return launch_tc<MODE, 256, 4>(a, splits, st);
+    return launch_tc<MODE, 128, 3>(a, splits, st);
+}
+
+template <class T, int MODE>
+static cudaError_t launch_simt(const ConvArgs& a, int splits, cudaStream_t st) {
+    dim3 grid((a.M + 63) / 64, (a.NG + 63) / 64, splits);
+    conv_simt_kernel<T, MODE><<<grid, 256, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+static ConvArgs make_args(const ConvShape& g) {
+    ConvArgs a{};
+    a.N = g.N; a.H = g.H; a.W = g.W; a.C = g.C; a.K = g.K; a.R = g.R; a.S = g.S;
+    a.stride = g.stride; a.pad = g.pad;
+    a.Ho = (g.H + 2 * g.pad - g.R) / g.stride + 1;
+    a.Wo = (g.W + 2 * g.pad - g.S) / g.stride + 1;
+    return a;
+}
+
+static bool tc_ok(const ConvShape& g, int dtype) {
+    return dtype == kF16 && (g.C % 8) == 0 && (g.K % 8) == 0 && !conv_force_simt();
+}
+
+static bool& force_simt_flag() {
+    static bool f = false;
+    return f;
+}
+bool conv_force_simt() { return force_simt_flag(); }
+void conv_set_force_simt(bool v) { force_simt_flag() = v; }
+
+cudaError_t conv_fprop(const ConvShape& g, int dtype, const void* x, const void* w, void* y, cudaStream_t st) {
+    ConvArgs a = make_args(g);
+    a.x = x; a.w = w; a.out = y;
+    a.M = g.N * a.Ho * a.Wo;
+    a.NG = g.K;
+    a.KG = g.R * g.S * g.C;
+    if (tc_ok(g, dtype)) return launch_tc_pick<FPROP>(a, 1, st);
+    return dtype == kF16 ? launch_simt<__half, FPROP>(a, 1, st) : launch_simt<float, FPROP>(a, 1, st);
+}
+
+cudaError_t conv_dgrad(const ConvShape& g, int dtype, const void* dy, const void* w, void* dx, int accumulate,
+                       cudaStream_t st) {
+    ConvArgs base = make_args(g);
+    base.x = dy; base.w = w; base.out = dx; base.accumulate = accumulate;
+    base.NG = g.C;
+    const int sd = g.stride;
+    for (int ph = 0; ph < sd; ++ph)
+        for (int pw = 0; pw < sd; ++pw) {
+            ConvArgs a = base;
+            a.ph = ph; a.pw = pw;
+            a.Hp = ph < g.H ? (g.H - ph + sd - 1) / sd : 0;
+            a.Wp = pw < g.W ? (g.W - pw + sd - 1) / sd : 0;
+            if (a.Hp == 0 || a.Wp == 0) continue;
+            a.r0 = (ph + g.pad) % sd;
+            a.q0 = (pw + g.pad) % sd;
+            a.nr = a.r0 < g.R ? (g.R - a.r0 + sd - 1) / sd : 0;
+            a.nq = a.q0 < g.S ? (g.S - a.q0 + sd - 1) / sd : 0;
+            a.M = g.N * a.Hp * a.Wp;
+            a.KG = a.nr * a.nq * g.K;
+            cudaError_t e;
+            if (a.KG == 0) {
+                const int64_t total = static_cast<int64_t>(a.M) * a.C;
+                const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 8 * kNumSMs));
+                if (dtype == kF16) dgrad_zero_phase_kernel<__half><<<blocks, 256, 0, st>>>(a);
+                else dgrad_zero_phase_kernel<float><<<blocks, 256, 0, st>>>(a);
+                e = cudaGetLastError();
+            } else if (tc_ok(g, dtype)) {
+                e = launch_tc_pick<DGRAD>(a, 1, st);
+            } else {
+                e = dtype == kF16 ? launch_simt<__half, DGRAD>(a, 1, st) : launch_simt<float, DGRAD>(a, 1, st);
+            }
+            if (e != cudaSuccess) return e;
+        }
+    return cudaSuccess;
+}
+
+size_t conv_wgrad_workspace(const ConvShape& g, int dtype) {
+    ConvArgs a = make_args(g);
+    const int64_t M = g.K, NG = static_cast<int64_t>(g.R) * g.S * g.C, KG = static_cast<int64_t>(g.N) * a.Ho * a.Wo;
+    const bool tc = tc_ok(g, dtype);
+    const int bk = tc ? kBK : 16;
+    const int64_t nkb = (KG + bk - 1) / bk;
+    const int64_t tiles = tc ? ((M + 127) / 128) * ((NG + 127) / 128) : ((M + 63) / 64) * ((NG + 63) / 64);
+    int64_t splits = std::max<int64_t>(1, std::min<int64_t>(nkb / 4, (2 * kNumSMs + tiles - 1) / tiles));
+    splits = std::min<int64_t>(splits, 64);
+    return static_cast<size_t>(splits) * M * NG * sizeof(float);
+}
+
+cudaError_t conv_wgrad(const ConvShape& g, int dtype, const void* x, const void* dy, void* dw, void* ws,
+                       size_t ws_bytes, cudaStream_t st) {
+    ConvArgs a = make_args(g);
+    a.x = x; a.w = dy;
+    a.M = g.K;
+    a.NG = g.R * g.S * g.C;
+    a.KG = g.N * a.Ho * a.Wo;
+    const bool tc = tc_ok(g, dtype);
+    const int bk = tc ? kBK : 16;
+    const int nkb = (a.KG + bk - 1) / bk;
+    const int64_t per = static_cast<int64_t>(a.M) * a.NG;
+    int splits = static_cast<int>(ws_bytes / (per * sizeof(float)));
+    splits = std::max(1, std::min(splits, nkb));
+    a.kb_per_split = (nkb + splits - 1) / splits;
+    splits = (nkb + a.kb_per_split - 1) / a.kb_per_split;
+    if (ws == nullptr || ws_bytes < static_cast<size_t>(per) * sizeof(float) * splits) return cudaErrorInvalidValue;
+    a.out = ws;
+    cudaError_t e;
+    if (tc) e = launch_tc_pick<WGRAD>(a, splits, st);
+    else e = dtype == kF16 ? launch_simt<__half, WGRAD>(a, splits, st) : launch_simt<float, WGRAD>(a, splits, st);
+    if (e != cudaSuccess) return e;
+    const int blocks = static_cast<int>(std::min<int64_t>((per + 255) / 256, 8 * kNumSMs));
+    if (dtype == kF16) wgrad_reduce_kernel<__half><<<blocks, 256, 0, st>>>(static_cast<float*>(ws), splits, per, static_cast<__half*>(dw));
+    else wgrad_reduce_kernel<float><<<blocks, 256, 0, st>>>(static_cast<float*>(ws), splits, per, static_cast<float*>(dw));
+    return cudaGetLastError();
+}
+
+}  // namespace sdb

@@ -1,0 +1,387 @@
+// norm.cu -- BatchNorm and InPlace-ABN forward/backward on NHWC tensors.
+//
+// Reference semantics (all under /root/reference/proj/src):
+//   BN fwd   syncbn.cpp:21-70  FP64 per-channel sum/sumsq, sums rounded to
+//            float (agg buffer), mean = sum/count, biased var clamped >= 0,
+//            invstd = 1/sqrt(var+eps), y = gamma*(x-mean)*invstd + beta.
+//   BN bwd   syncbn.cpp:72-117 FP64 sum(dy), sum(dy*xhat) (rounded to float),
+//            dx = gamma*invstd*(dy - s1/m - xhat*s2/m), dgamma = s2, dbeta = s1.
+//   IABN fwd memopt.cpp:226-276 same statistics kept in double, y = leaky(z).
+//   IABN bwd memopt.cpp:278-327 recompute z and xhat from the OUTPUT y
+//            (z = y>=0 ? y : y/slope; xhat = (z-beta)/gamma), dz = dy*(y>0?1:slope).
+// The optional fused ReLU of the BN path (C1: BN followed by relu,
+// model.cpp:238-245) keeps its mask in the stored output (y>0 <=> z>0).
+//
+// Kernels: (1) per-block partial statistics, 8 channels per thread with
+// 128-bit loads, fp32 runs of <=16 rows folded into fp64 registers, fp64
+// block reduction in smem -> partial[block][2C]; (2) fixed-order fp64
+// finalize per channel (deterministic, no atomics); (3) vectorised apply.
+// The second read of x in (3) mostly hits the 126 MB L2.
+#include <algorithm>
+
+#include "common.cuh"
+#include "sdb_internal.h"
+
+namespace sdb {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kMaxBlocks = 2 * kNumSMs;
+
+template <class T>
+SDB_DEV void load8(const T* p, float (&v)[8]);
+template <>
+SDB_DEV void load8<__half>(const __half* p, float (&v)[8]) {
+    const uint4 u = *reinterpret_cast<const uint4*>(p);
+    const __half2* h = reinterpret_cast<const __half2*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float2 f = __half22float2(h[i]);
+        v[2 * i] = f.x;
+        v[2 * i + 1] = f.y;
+    }
+}
+template <>
+SDB_DEV void load8<float>(const float* p, float (&v)[8]) {
+    const float4 a = *reinterpret_cast<const float4*>(p);
+    const float4 b = *reinterpret_cast<const float4*>(p + 4);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+template <class T>
+SDB_DEV void store8(T* p, const float (&v)[8]);
+template <>
+SDB_DEV void store8<__half>(__half* p, const float (&v)[8]) {
+    uint4 u;
+    __half2* h = reinterpret_cast<__half2*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) h[i] = __floats2half2_rn(v[2 * i], v[2 * i + 1]);
+    *reinterpret_cast<uint4*>(p) = u;
+}
+template <>
+SDB_DEV void store8<float>(float* p, const float (&v)[8]) {
+    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    *reinterpret_cast<float4*>(p + 4) = make_float4(v[4], v[5], v[6], v[7]);
+}
+
+// ---------------------------------------------------------------- statistics
+// KIND 0: (x, x^2)             forward statistics
+// KIND 1: (dz, dz*xhat) BN     xhat = (x-mean)*invstd (float), dz = relu mask ? dy : 0
+// KIND 2: (dz, dz*xhat) IABN   recompute from y
+struct StatArgs {
+    const void* a;  // x (KIND 0/1) or y (KIND 2)
+    const void* dy;
+    const void* y;  // BN relu mask source (may be null)
+    const float *gamma, *beta, *mean, *invstd;
+    float slope;
+    int64_t rows;
+    int C;
+    int64_t rows_per_block;
+    double* partial;
+};
+
+template <class T, int KIND>
+__global__ void __launch_bounds__(kThreads) stats_kernel(StatArgs p) {
+    extern __shared__ double red[];  // [kThreads][16]
+    const int tpr = p.C / 8;
+    const int rpi = kThreads / tpr;
+    const int cg = threadIdx.x % tpr, rg = threadIdx.x / tpr;
+    const int c0 = cg * 8;
+    const int64_t r_begin = blockIdx.x * p.rows_per_block;
+    const int64_t r_end = min(p.rows, r_begin + p.rows_per_block);
+    double S[8] = {}, Q[8] = {};
+    float s[8] = {}, q[8] = {};
+    float g[8], b[8], mu[8], is[8];
+    if (KIND != 0) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            g[j] = p.gamma[c0 + j];
+            is[j] = p.invstd[c0 + j];
+            mu[j] = KIND == 1 ? p.mean[c0 + j] : 0.f;
+            b[j] = KIND == 2 ? p.beta[c0 + j] : 0.f;
+        }
+    }
+    int run = 0;
+    for (int64_t r = r_begin + rg; r < r_end; r += rpi) {
+        const int64_t off = r * p.C + c0;
+        float v[8];
+        load8<T>(static_cast<const T*>(p.a) + off, v);
+        if (KIND == 0) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                s[j] += v[j];
+                q[j] += v[j] * v[j];
+            }
+        } else {
+            float d[8];
+            load8<T>(static_cast<const T*>(p.dy) + off, d);
+            if (KIND == 1) {
+                if (p.y) {
+                    float yv[8];
+                    load8<T>(static_cast<const T*>(p.y) + off, yv);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) d[j] = yv[j] > 0.f ? d[j] : 0.f;
+                }
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const float xh = (v[j] - mu[j]) * is[j];
+                    s[j] += d[j];
+                    q[j] += d[j] * xh;
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const float yv = v[j];
+                    const float z = yv >= 0.f ? yv : yv / p.slope;
+                    const float dz = d[j] * (yv > 0.f ? 1.f : p.slope);
+                    const float xh = (z - b[j]) / g[j];
+                    s[j] += dz;
+                    q[j] += dz * xh;
+                }
+            }
+        }
+        if (++run == 16) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                S[j] += s[j];
+                Q[j] += q[j];
+                s[j] = q[j] = 0.f;
+            }
+            run = 0;
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        S[j] += s[j];
+        Q[j] += q[j];
+        red[threadIdx.x * 16 + j] = S[j];
+        red[threadIdx.x * 16 + 8 + j] = Q[j];
+    }
+    __syncthreads();
+    if (rg == 0) {
+        for (int k = 1; k < rpi; ++k) {
+            const int t = k * tpr + cg;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                S[j] += red[t * 16 + j];
+                Q[j] += red[t * 16 + 8 + j];
+            }
+        }
+        double* out = p.partial + static_cast<int64_t>(blockIdx.x) * 2 * p.C;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            out[c0 + j] = S[j];
+            out[p.C + c0 + j] = Q[j];
+        }
+    }
+}
+
+// MODE 0: BN fwd (sums rounded to float first), 1: IABN fwd (double)
+// MODE 2: BN bwd, 3: IABN bwd  -> coef[0..C) = s1/m, coef[C..2C) = s2/m
+__global__ void finalize_kernel(const double* partial, int nblocks, int C, int64_t count, float eps, int mode,
+                                float* mean, float* invstd, float* dgamma, float* dbeta, float* coef) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= C) return;
+    double S = 0.0, Q = 0.0;
+    for (int b = 0; b < nblocks; ++b) {
+        S += partial[static_cast<int64_t>(b) * 2 * C + c];
+        Q += partial[static_cast<int64_t>(b) * 2 * C + C + c];
+    }
+    if (mode == 0 || mode == 1) {
+        double mu, var;
+        if (mode == 0) {
+            const float sf = static_cast<float>(S), qf = static_cast<float>(Q);
+            mu = static_cast<double>(sf) / static_cast<double>(count);
+            var = static_cast<double>(qf) / static_cast<double>(count) - mu * mu;
+        } else {
+            mu = S / static_cast<double>(count);
+            var = Q / static_cast<double>(count) - mu * mu;
+        }
+        if (var < 0.0) var = 0.0;
+        mean[c] = static_cast<float>(mu);
+        invstd[c] = static_cast<float>(1.0 / sqrt(var + static_cast<double>(eps)));
+    } else {
+        const float s1 = static_cast<float>(S), s2 = static_cast<float>(Q);
+        dgamma[c] = s2;
+        dbeta[c] = s1;
+        if (mode == 2) {
+            const float m = static_cast<float>(count);
+            coef[c] = s1 / m;
+            coef[C + c] = s2 / m;
+        } else {
+            coef[c] = static_cast<float>(S / static_cast<double>(count));
+            coef[C + c] = static_cast<float>(Q / static_cast<double>(count));
+        }
+    }
+}
+
+// ---------------------------------------------------------------- apply
+// KIND 0: BN fwd (+act relu when act==1), 1: IABN fwd, 2: BN bwd, 3: IABN bwd
+struct ApplyArgs {
+    const void* a;   // x or y
+    const void* dy;
+    const void* y;   // relu mask (BN bwd)
+    void* out;
+    const float *gamma, *beta, *mean, *invstd, *coef;
+    float slope;
+    int act;
+    int64_t n8;  // number of 8-element groups
+    int C;
+};
+
+template <class T, int KIND>
+__global__ void __launch_bounds__(kThreads) apply_kernel(ApplyArgs p) {
+    for (int64_t gi = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; gi < p.n8;
+         gi += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t off = gi * 8;
+        const int c0 = static_cast<int>(off % p.C);
+        float v[8], o[8];
+        load8<T>(static_cast<const T*>(p.a) + off, v);
+        if (KIND == 0 || KIND == 1) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int c = c0 + j;
+                const float z = p.gamma[c] * (v[j] - p.mean[c]) * p.invstd[c] + p.beta[c];
+                if (KIND == 0) o[j] = (p.act && !(z > 0.f)) ? 0.f : z;
+                else o[j] = z > 0.f ? z : p.slope * z;
+            }
+        } else {
+            float d[8];
+            load8<T>(static_cast<const T*>(p.dy) + off, d);
+            if (KIND == 2) {
+                if (p.y) {
+                    float yv[8];
+                    load8<T>(static_cast<const T*>(p.y) + off, yv);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) d[j] = yv[j] > 0.f ? d[j] : 0.f;
+                }
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const int c = c0 + j;
+                    const float gis = p.gamma[c] * p.invstd[c];
+                    const float xh = (v[j] - p.mean[c]) * p.invstd[c];
+                    o[j] = gis * (d[j] - p.coef[c] - xh * p.coef[p.C + c]);
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const int c = c0 + j;
+                    const float yv = v[j];
+                    const float z = yv >= 0.f ? yv : yv / p.slope;
+                    const float dz = d[j] * (yv > 0.f ? 1.f : p.slope);
+                    const float xh = (z - p.beta[c]) / p.gamma[c];
+                    const float gis = p.gamma[c] * p.invstd[c];
+                    o[j] = gis * (dz - p.coef[c] - xh * p.coef[p.C + c]);
+                }
+            }
+        }
+        store8<T>(static_cast<T*>(p.out) + off, o);
+    }
+}
+
+struct Plan {
+    int nblocks;
+    int64_t rpb;
+};
+
+Plan plan_for(int64_t rows, int C) {
+    const int rpi = kThreads / (C / 8);
+    // at least 16 rows per thread-iteration group, at most kMaxBlocks blocks
+    int64_t nb = (rows + static_cast<int64_t>(rpi) * 16 - 1) / (static_cast<int64_t>(rpi) * 16);
+    nb = std::max<int64_t>(1, std::min<int64_t>(nb, kMaxBlocks));
+    Plan p;
+    p.nblocks = static_cast<int>(nb);
+    p.rpb = (rows + nb - 1) / nb;
+    return p;
+}
+
+int apply_blocks(int64_t n8) { return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n8 + kThreads - 1) / kThreads, 16 * kNumSMs))); }
+
+template <class T, int KIND>
+cudaError_t run_stats(const StatArgs& a0, const Plan& pl, cudaStream_t st) {
+    StatArgs a = a0;
+    a.rows_per_block = pl.rpb;
+    stats_kernel<T, KIND><<<pl.nblocks, kThreads, kThreads * 16 * sizeof(double), st>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+bool norm_channels_ok(int C) { return C >= 8 && C <= 2048 && (C % 8) == 0 && (2048 % C) == 0; }
+
+size_t norm_workspace_bytes(int64_t rows, int C) {
+    const Plan p = plan_for(std::max<int64_t>(rows, 1), C);
+    return static_cast<size_t>(p.nblocks) * 2 * C * sizeof(double) + 2 * C * sizeof(float) + 256;
+}
+
+cudaError_t bn_forward(int dtype, const void* x, const float* gamma, const float* beta, void* y, float* mean,
+                       float* invstd, int64_t rows, int C, float eps, int act, float slope, void* ws, cudaStream_t st) {
+    // act: 0 none, 1 relu (BN mode);  act 2 = IABN with `slope`
+    const Plan pl = plan_for(rows, C);
+    double* partial = static_cast<double*>(ws);
+    StatArgs sa{};
+    sa.a = x; sa.rows = rows; sa.C = C; sa.partial = partial;
+    cudaError_t e = dtype == kF16 ? run_stats<__half, 0>(sa, pl, st) : run_stats<float, 0>(sa, pl, st);
+    if (e != cudaSuccess) return e;
+    finalize_kernel<<<(C + 127) / 128, 128, 0, st>>>(partial, pl.nblocks, C, rows, eps, act == 2 ? 1 : 0, mean, invstd,
+                                                     nullptr, nullptr, nullptr);
+    ApplyArgs aa{};
+    aa.a = x; aa.out = y; aa.gamma = gamma; aa.beta = beta; aa.mean = mean; aa.invstd = invstd;
+    aa.slope = slope; aa.act = act; aa.n8 = rows * C / 8; aa.C = C;
+    const int nb = apply_blocks(aa.n8);
+    if (act == 2) {
+        if (dtype == kF16) apply_kernel<__half, 1><<<nb, kThreads, 0, st>>>(aa);
+        else apply_kernel<float, 1><<<nb, kThreads, 0, st>>>(aa);
+    } else {
+        if (dtype == kF16) apply_kernel<__half, 0><<<nb, kThreads, 0, st>>>(aa);
+        else apply_kernel<float, 0><<<nb, kThreads, 0, st>>>(aa);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t bn_backward(int dtype, const void* dy, const void* x, const void* y_mask, const float* gamma,
+                        const float* mean, const float* invstd, void* dx, float* dgamma, float* dbeta, int64_t rows,
+                        int C, void* ws, cudaStream_t st) {
+    const Plan pl = plan_for(rows, C);
+    double* partial = static_cast<double*>(ws);
+    float* coef = reinterpret_cast<float*>(partial + static_cast<int64_t>(pl.nblocks) * 2 * C);
+    StatArgs sa{};
+    sa.a = x; sa.dy = dy; sa.y = y_mask; sa.gamma = gamma; sa.mean = mean; sa.invstd = invstd;
+    sa.rows = rows; sa.C = C; sa.partial = partial;
+    cudaError_t e = dtype == kF16 ? run_stats<__half, 1>(sa, pl, st) : run_stats<float, 1>(sa, pl, st);
+    if (e != cudaSuccess) return e;
+    finalize_kernel<<<(C + 127) / 128, 128, 0, st>>>(partial, pl.nblocks, C, rows, 0.f, 2, nullptr, nullptr, dgamma,
+                                                     dbeta, coef);
+    ApplyArgs aa{};
+    aa.a = x; aa.dy = dy; aa.y = y_mask; aa.out = dx; aa.gamma = gamma; aa.mean = mean; aa.invstd = invstd;
+    aa.coef = coef; aa.n8 = rows * C / 8; aa.C = C;
+    const int nb = apply_blocks(aa.n8);
+    if (dtype == kF16) apply_kernel<__half, 2><<<nb, kThreads, 0, st>>>(aa);
+    else apply_kernel<float, 2><<<nb, kThreads, 0, st>>>(aa);
+    return cudaGetLastError();
+}
+
+cudaError_t iabn_backward(int dtype, const void* dy, const void* y, const float* gamma, const float* beta,
+                          const float* mean, const float* invstd, void* dx, float* dgamma, float* dbeta, int64_t rows,
+                          int C, float slope, void* ws, cudaStream_t st) {
+    (void)mean;
+    const Plan pl = plan_for(rows, C);
+    double* partial = static_cast<double*>(ws);
+    float* coef = reinterpret_cast<float*>(partial + static_cast<int64_t>(pl.nblocks) * 2 * C);
+    StatArgs sa{};
+    sa.a = y; sa.dy = dy; sa.gamma = gamma; sa.beta = beta; sa.invstd = invstd; sa.slope = slope;
+    sa.rows = rows; sa.C = C; sa.partial = partial;
+    cudaError_t e = dtype == kF16 ? run_stats<__half, 2>(sa, pl, st) : run_stats<float, 2>(sa, pl, st);
+    if (e != cudaSuccess) return e;
+    finalize_kernel<<<(C + 127) / 128, 128, 0, st>>>(partial, pl.nblocks, C, rows, 0.f, 3, nullptr, nullptr, dgamma,
+                                                     dbeta, coef);
+    ApplyArgs aa{};
+    aa.a = y; aa.dy = dy; aa.out = dx; aa.gamma = gamma; aa.beta = beta; aa.invstd = invstd; aa.coef = coef;
+    aa.slope = slope; aa.n8 = rows * C / 8; aa.C = C;
+    const int nb = apply_blocks(aa.n8);
+    if (dtype == kF16) apply_kernel<__half, 3><<<nb, kThreads, 0, st>>>(aa);
+    else apply_kernel<float, 3><<<nb, kThreads, 0, st>>>(aa);
+    return cudaGetLastError();
+}
+
+}  // namespace sdb

@@ -1,0 +1,57 @@
+// sdb_internal.h -- internal host-side declarations shared by the kernel
+// translation units, the C ABI (abi.cpp) and the step driver (detector.cpp).
+#pragma once
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace sdb {
+
+enum DType { kF32 = 0, kF16 = 1 };
+
+struct ConvShape {
+    int N, H, W, C;  // input activation (NHWC)
+    int K, R, S;     // filter KRSC
+    int stride, pad;
+    int Ho() const { return (H + 2 * pad - R) / stride + 1; }
+    int Wo() const { return (W + 2 * pad - S) / stride + 1; }
+};
+
+// ---- conv.cu
+cudaError_t conv_fprop(const ConvShape& g, int dtype, const void* x, const void* w, void* y, cudaStream_t st);
+cudaError_t conv_dgrad(const ConvShape& g, int dtype, const void* dy, const void* w, void* dx, int accumulate,
+                       cudaStream_t st);
+size_t conv_wgrad_workspace(const ConvShape& g, int dtype);
+cudaError_t conv_wgrad(const ConvShape& g, int dtype, const void* x, const void* dy, void* dw, void* ws,
+                       size_t ws_bytes, cudaStream_t st);
+bool conv_force_simt();
+void conv_set_force_simt(bool v);
+
+// ---- norm.cu  (rows = N*H*W, channels innermost)
+// workspace: norm_workspace_bytes(rows, C)
+size_t norm_workspace_bytes(int64_t rows, int C);
+// act: 0 = BN, 1 = BN + ReLU, 2 = IABN (leaky `slope`; slope == 1 -> identity)
+cudaError_t bn_forward(int dtype, const void* x, const float* gamma, const float* beta, void* y, float* mean,
+                       float* invstd, int64_t rows, int C, float eps, int act, float slope, void* ws,
+                       cudaStream_t st);
+// y_mask: stored BN+ReLU output (relu mask) or null for plain BN
+cudaError_t bn_backward(int dtype, const void* dy, const void* x, const void* y_mask, const float* gamma,
+                        const float* mean, const float* invstd, void* dx, float* dgamma, float* dbeta, int64_t rows,
+                        int C, void* ws, cudaStream_t st);
+bool norm_channels_ok(int C);
+cudaError_t iabn_backward(int dtype, const void* dy, const void* y, const float* gamma, const float* beta,
+                          const float* mean, const float* invstd, void* dx, float* dgamma, float* dbeta,
+                          int64_t rows, int C, float slope, void* ws, cudaStream_t st);
+
+// ---- optim.cu
+cudaError_t nonfinite_check(int gdtype, const void* g, int64_t n, int* flag, cudaStream_t st);
+cudaError_t fused_sgd(int gdtype, const void* gsum, float* w, float* v, __half* w16, int64_t n, float lr, float mu,
+                      const double* scale, double denom_mult, const int* flag, cudaStream_t st);
+cudaError_t update_scale_device(double* scale, int64_t* good_steps, const int* flag, int dynamic,
+                                int64_t growth_interval, double growth, double backoff, double min_scale,
+                                double max_scale, cudaStream_t st);
+cudaError_t cast_f32_f16(const float* in, __half* out, int64_t n, cudaStream_t st);
+cudaError_t cast_f16_f32(const __half* in, float* out, int64_t n, cudaStream_t st);
+
+}  // namespace sdb

@@ -1,0 +1,229 @@
+"""Host mirror of the reference operator API (namespace ``simdet``) on top of
+the libsdb C ABI.  Same names, argument meaning and error behaviour as the
+reference's C++ functions, so parity tests read like the reference's own
+tests; tensors are torch CUDA tensors in the reference layout (NCHW / OIHW),
+converted to the library's NHWC / KRSC layout at this boundary (the "parity
+shim" of SURVEY.md §8(b)).  torch is plumbing only (allocation, streams);
+every arithmetic op runs in libsdb's sm_100a kernels.
+
+Reference entry points mirrored (file:line under /root/reference/proj):
+  conv2d                      src/tensor.cpp:169-196
+  conv2d_backward             src/autograd.cpp:290-320  (Tape conv2d rule)
+  syncbn_forward / _backward  src/syncbn.cpp:21-117     (group == nullptr)
+  iabn_forward / _backward    src/memopt.cpp:226-327
+  apply_sgd / has_nonfinite   src/trainer.cpp:78-94
+  update_scale                src/precision.cpp:45-56
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import F16, F32, check, lib
+
+_P, _I, _L, _F, _D = C.c_void_p, C.c_int, C.c_int64, C.c_float, C.c_double
+
+_SIGS = {
+    "sdb_ctx_create": [_I, _I, _I, _P, C.POINTER(_P)],
+    "sdb_ctx_destroy": [_P],
+    "sdb_synchronize": [_P],
+    "sdb_get_nccl_unique_id": [_P],
+    "sdb_conv_fprop": [_P, _I, _P, _P, _P] + [_I] * 9 + [_P],
+    "sdb_conv_dgrad": [_P, _I, _P, _P, _P] + [_I] * 10 + [_P],
+    "sdb_conv_wgrad": [_P, _I, _P, _P, _P] + [_I] * 9 + [_P],
+    "sdb_bn_fwd": [_P, _I, _P, _P, _P, _P, _P, _P, _L, _I, _F, _I, _P],
+    "sdb_bn_bwd": [_P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _L, _I, _P],
+    "sdb_iabn_fwd": [_P, _I, _P, _P, _P, _P, _P, _P, _L, _I, _F, _F, _P],
+    "sdb_iabn_bwd": [_P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _L, _I, _F, _P],
+    "sdb_nonfinite": [_P, _I, _P, _L, _P, _P],
+    "sdb_fused_sgd": [_P, _I, _P, _P, _P, _P, _L, _F, _F, _P, _D, _P, _P],
+    "sdb_update_scale": [_P, _P, _P, _P, _I, _L, _D, _D, _D, _D, _P],
+    "sdb_cast": [_P, _I, _P, _I, _P, _L, _P],
+}
+
+_configured = False
+_ctx = {}
+
+
+def L():
+    global _configured
+    lb = lib()
+    if not _configured:
+        for name, args in _SIGS.items():
+            fn = getattr(lb, name)
+            fn.argtypes = args
+            fn.restype = C.c_int
+        _configured = True
+    return lb
+
+
+def _require_cuda(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise RuntimeError("libsdb ops need CUDA tensors (no CPU fallback)")
+
+
+def ctx(device: int | None = None):
+    """Per-device default context (single rank)."""
+    if device is None:
+        device = torch.cuda.current_device()
+    if device not in _ctx:
+        h = _P()
+        check(L().sdb_ctx_create(device, 0, 1, None, C.byref(h)))
+        _ctx[device] = h
+    return _ctx[device]
+
+
+def stream():
+    return _P(torch.cuda.current_stream().cuda_stream)
+
+
+def ptr(t):
+    return None if t is None else _P(t.data_ptr())
+
+
+def dt(t) -> int:
+    if t.dtype == torch.float16:
+        return F16
+    if t.dtype == torch.float32:
+        return F32
+    raise TypeError(f"unsupported dtype {t.dtype}")
+
+
+def nchw_to_nhwc(t):
+    return t.permute(0, 2, 3, 1).contiguous()
+
+
+def nhwc_to_nchw(t):
+    return t.permute(0, 3, 1, 2).contiguous()
+
+
+# ------------------------------------------------------------------ NHWC primitives
+def conv_fprop_nhwc(x, w, stride, pad):
+    _require_cuda(x, w)
+    N, H, W, Cc = x.shape
+    K, R, S, C2 = w.shape
+    Ho = (H + 2 * pad - R) // stride + 1 if H + 2 * pad >= R else 0
+    Wo = (W + 2 * pad - S) // stride + 1 if W + 2 * pad >= S else 0
+    y = torch.empty((N, max(Ho, 1), max(Wo, 1), K), device=x.device, dtype=x.dtype)
+    check(L().sdb_conv_fprop(ctx(), dt(x), ptr(x), ptr(w), ptr(y), N, H, W, Cc, K, R, S, stride, pad, stream()))
+    return y
+
+
+def conv_dgrad_nhwc(dy, w, x_shape, stride, pad, out=None, accumulate=False):
+    N, H, W, Cc = x_shape
+    K, R, S, _ = w.shape
+    dx = out if out is not None else torch.empty((N, H, W, Cc), device=dy.device, dtype=dy.dtype)
+    check(L().sdb_conv_dgrad(ctx(), dt(dy), ptr(dy), ptr(w), ptr(dx), N, H, W, Cc, K, R, S, stride, pad,
+                             1 if accumulate else 0, stream()))
+    return dx
+
+
+def conv_wgrad_nhwc(x, dy, w_shape, stride, pad):
+    N, H, W, Cc = x.shape
+    K, R, S, _ = w_shape
+    dw = torch.empty((K, R, S, Cc), device=x.device, dtype=x.dtype)
+    check(L().sdb_conv_wgrad(ctx(), dt(x), ptr(x), ptr(dy), ptr(dw), N, H, W, Cc, K, R, S, stride, pad, stream()))
+    return dw
+
+
+# ------------------------------------------------------------------ reference-shaped API
+def conv2d(x, k, stride: int, pad: int):
+    """simdet::conv2d (src/tensor.cpp:169): x [N,C,H,W], k [O,C,kh,kw]."""
+    from . import ShapeError
+    if x.dim() != 4 or k.dim() != 4:
+        raise ShapeError("conv2d: rank-4 operands required")
+    if x.dtype != k.dtype:
+        raise ShapeError("conv2d: dtype mismatch")
+    if x.shape[1] != k.shape[1]:
+        raise ShapeError("conv2d: channel mismatch")
+    y = conv_fprop_nhwc(nchw_to_nhwc(x), nchw_to_nhwc(k), stride, pad)
+    return nhwc_to_nchw(y)
+
+
+def conv2d_backward(x, k, dy, stride: int, pad: int):
+    """Tape conv2d backward rule (src/autograd.cpp:290-320) + leaf-dtype finalisation."""
+    dy = dy.to(x.dtype)
+    xn, kn, dyn = nchw_to_nhwc(x), nchw_to_nhwc(k), nchw_to_nhwc(dy)
+    dx = conv_dgrad_nhwc(dyn, kn, tuple(xn.shape), stride, pad)
+    dk = conv_wgrad_nhwc(xn, dyn, tuple(kn.shape), stride, pad)
+    return nhwc_to_nchw(dx), nhwc_to_nchw(dk)
+
+
+def _bn_io(x):
+    xn = nchw_to_nhwc(x)
+    N, H, W, Cc = xn.shape
+    return xn, N * H * W, Cc
+
+
+def syncbn_forward(x, gamma, beta, eps: float, relu: bool = False):
+    """syncbn_forward with group == nullptr (src/syncbn.cpp:21-70)."""
+    xn, rows, Cc = _bn_io(x)
+    y = torch.empty_like(xn)
+    mean = torch.empty(Cc, device=x.device, dtype=torch.float32)
+    invstd = torch.empty_like(mean)
+    check(L().sdb_bn_fwd(ctx(), dt(x), ptr(xn), ptr(gamma), ptr(beta), ptr(y), ptr(mean), ptr(invstd), rows, Cc, eps,
+                         1 if relu else 0, stream()))
+    return nhwc_to_nchw(y), mean, invstd
+
+
+def syncbn_backward(dy, x, mean, invstd, gamma, y_relu=None):
+    """syncbn_backward with group == nullptr (src/syncbn.cpp:72-117)."""
+    xn, rows, Cc = _bn_io(x)
+    dyn = nchw_to_nhwc(dy.to(x.dtype))
+    yr = nchw_to_nhwc(y_relu) if y_relu is not None else None
+    dx = torch.empty_like(xn)
+    dgamma = torch.empty(Cc, device=x.device, dtype=torch.float32)
+    dbeta = torch.empty_like(dgamma)
+    check(L().sdb_bn_bwd(ctx(), dt(x), ptr(dyn), ptr(xn), ptr(yr), ptr(gamma), ptr(mean), ptr(invstd), ptr(dx),
+                         ptr(dgamma), ptr(dbeta), rows, Cc, stream()))
+    return nhwc_to_nchw(dx), dgamma, dbeta
+
+
+def iabn_forward(x, gamma, beta, eps: float, slope: float):
+    """iabn_forward (src/memopt.cpp:226-276): y = leaky(BN(x)); saves y only."""
+    xn, rows, Cc = _bn_io(x)
+    y = torch.empty_like(xn)
+    mean = torch.empty(Cc, device=x.device, dtype=torch.float32)
+    invstd = torch.empty_like(mean)
+    check(L().sdb_iabn_fwd(ctx(), dt(x), ptr(xn), ptr(gamma), ptr(beta), ptr(y), ptr(mean), ptr(invstd), rows, Cc,
+                           eps, slope, stream()))
+    return nhwc_to_nchw(y), mean, invstd
+
+
+def iabn_backward(dy, y, mean, invstd, gamma, beta, slope: float):
+    """iabn_backward (src/memopt.cpp:278-327): recompute from the output."""
+    yn, rows, Cc = _bn_io(y)
+    dyn = nchw_to_nhwc(dy.to(y.dtype))
+    dx = torch.empty_like(yn)
+    dgamma = torch.empty(Cc, device=y.device, dtype=torch.float32)
+    dbeta = torch.empty_like(dgamma)
+    check(L().sdb_iabn_bwd(ctx(), dt(y), ptr(dyn), ptr(yn), ptr(gamma), ptr(beta), ptr(mean), ptr(invstd), ptr(dx),
+                           ptr(dgamma), ptr(dbeta), rows, Cc, slope, stream()))
+    return nhwc_to_nchw(dx), dgamma, dbeta
+
+
+def has_nonfinite(g) -> bool:
+    """has_nonfinite (src/trainer.cpp:78-82)."""
+    flag = torch.zeros(1, device=g.device, dtype=torch.int32)
+    check(L().sdb_nonfinite(ctx(), dt(g), ptr(g), g.numel(), ptr(flag), stream()))
+    return bool(flag.item())
+
+
+def apply_sgd(w, v, gsum, lr: float, momentum: float, denom: float, w16=None, flag=None, scale=None):
+    """apply_sgd (src/trainer.cpp:86-94), in place on fp32 w and v; optional fp16 shadow.
+    denom = scale * K; pass `scale` (device double) to read the live loss scale."""
+    if scale is None:
+        mult = denom
+    else:
+        mult = denom  # caller passes K when the scale is on device
+    check(L().sdb_fused_sgd(ctx(), dt(gsum), ptr(gsum), ptr(w), ptr(v), ptr(w16), w.numel(), lr, momentum,
+                            ptr(scale), mult, ptr(flag), stream()))
+
+
+def update_scale(scale_dev, good_dev, flag_dev, dynamic: bool, growth_interval=2000, growth=2.0, backoff=0.5,
+                 min_scale=1.0, max_scale=16777216.0):
+    """update_scale (src/precision.cpp:45-56) on device-resident state."""
+    check(L().sdb_update_scale(ctx(), ptr(scale_dev), ptr(good_dev), ptr(flag_dev), 1 if dynamic else 0,
+                               growth_interval, growth, backoff, min_scale, max_scale, stream()))

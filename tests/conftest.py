@@ -1,0 +1,26 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
+
+
+@pytest.fixture(scope="session")
+def orc():
+    import oracle
+    return oracle.orc()
+
+
+@pytest.fixture(scope="session")
+def ref():
+    import oracle
+    if not oracle.ref_available():
+        pytest.skip("reference oracle library not built")
+    return oracle.ref()

@@ -1,0 +1,238 @@
+"""GPU parity: libsdb conv / BN / IABN / optimizer kernels vs the compiled
+reference engine (oracle/_ref) on identical seeded inputs.  Runs through the
+C ABI (paper_1903_05831_b200.simdet mirrors the reference signatures)."""
+import numpy as np
+import pytest
+
+import oracle
+from tests.util import assert_close
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+CONV_CASES = [
+    # (N, C, H, W, K, R, S, stride, pad)
+    (2, 16, 12, 10, 32, 3, 3, 1, 1),
+    (2, 64, 9, 11, 64, 1, 1, 1, 0),
+    (2, 32, 10, 10, 64, 1, 1, 2, 0),
+    (2, 8, 32, 32, 64, 7, 7, 2, 3),
+    (1, 16, 9, 9, 16, 3, 3, 2, 1),
+    (1, 24, 7, 5, 40, 3, 3, 1, 1),
+    (2, 64, 20, 24, 256, 3, 3, 1, 1),
+    (1, 3, 11, 13, 8, 3, 3, 1, 1),
+]
+
+
+def _rand(rng, shape, fp16, scale=1.0):
+    a = (rng.standard_normal(shape) * scale).astype(np.float32)
+    if fp16:
+        a = a.astype(np.float16).astype(np.float32)
+    return a
+
+
+def _ref_conv(x, k, stride, pad, fp16):
+    N, C, H, W = x.shape
+    O, _, kh, kw = k.shape
+    Ho, Wo = (H + 2 * pad - kh) // stride + 1, (W + 2 * pad - kw) // stride + 1
+    y = np.zeros((N, O, Ho, Wo), np.float32)
+    rc = oracle.ref().ref_conv2d(oracle.p(x), N, C, H, W, oracle.p(k), O, kh, kw, stride, pad, int(fp16), oracle.p(y))
+    assert rc == 0
+    return y
+
+
+def _ref_conv_bwd(x, k, dy, stride, pad, fp16):
+    N, C, H, W = x.shape
+    O, _, kh, kw = k.shape
+    dx = np.zeros_like(x)
+    dk = np.zeros_like(k)
+    rc = oracle.ref().ref_conv2d_backward(oracle.p(x), N, C, H, W, oracle.p(k), O, kh, kw, stride, pad, int(fp16),
+                                          oracle.p(dy), oracle.p(dx), oracle.p(dk))
+    assert rc == 0
+    return dx, dk
+
+
+@pytest.mark.parametrize("fp16", [False, True])
+@pytest.mark.parametrize("case", CONV_CASES)
+def test_conv_fwd_bwd(ref, case, fp16):
+    from paper_1903_05831_b200 import simdet as sd
+    N, C, H, W, K, R, S, st, pd = case
+    rng = np.random.default_rng(hash(case) % 2**32)
+    x = _rand(rng, (N, C, H, W), fp16)
+    k = _rand(rng, (K, C, R, S), fp16, 1.0 / np.sqrt(C * R * S))
+    y_ref = _ref_conv(x, k, st, pd, fp16)
+    dy = _rand(rng, y_ref.shape, fp16)
+    dx_ref, dk_ref = _ref_conv_bwd(x, k, dy, st, pd, fp16)
+    tdt = torch.float16 if fp16 else torch.float32
+    xt, kt, dyt = (torch.from_numpy(a).to("cuda", tdt) for a in (x, k, dy))
+    y = sd.conv2d(xt, kt, st, pd)
+    dx, dk = sd.conv2d_backward(xt, kt, dyt, st, pd)
+    torch.cuda.synchronize()
+    tol = 2e-3 if fp16 else 1e-5
+    assert_close(y, y_ref, tol, "y")
+    assert_close(dx, dx_ref, tol, "dx")
+    assert_close(dk, dk_ref, tol, "dk")
+
+
+def test_conv_large_tile_path(ref):
+    """exercises the 128x256 tensor-core tile (enough tiles to pick BN=256)."""
+    from paper_1903_05831_b200 import simdet as sd
+    rng = np.random.default_rng(7)
+    N, C, H, W, K = 8, 64, 56, 56, 512
+    x = _rand(rng, (N, C, H, W), True)
+    k = _rand(rng, (K, C, 1, 1), True, 0.125)
+    y_ref = _ref_conv(x, k, 1, 0, True)
+    y = sd.conv2d(torch.from_numpy(x).cuda().half(), torch.from_numpy(k).cuda().half(), 1, 0)
+    assert_close(y, y_ref, 2e-3, "y")
+
+
+BN_SHAPES = [(2, 64, 7, 9), (4, 256, 5, 5), (2, 2048, 3, 3), (1, 8, 4, 4), (2, 512, 16, 12)]
+
+
+@pytest.mark.parametrize("fp16", [False, True])
+@pytest.mark.parametrize("shape", BN_SHAPES)
+def test_bn_fwd_bwd(ref, shape, fp16):
+    from paper_1903_05831_b200 import simdet as sd
+    N, C, H, W = shape
+    rng = np.random.default_rng(C + H)
+    x = _rand(rng, shape, fp16, 2.0) + 0.5
+    x = x.astype(np.float16).astype(np.float32) if fp16 else x
+    g = (1.0 + 0.2 * rng.standard_normal(C)).astype(np.float32)
+    b = (0.1 * rng.standard_normal(C)).astype(np.float32)
+    y_ref = np.zeros_like(x)
+    mean_ref = np.zeros(C, np.float32)
+    inv_ref = np.zeros(C, np.float32)
+    assert ref.ref_bn_forward(oracle.p(x), N, C, H, W, oracle.p(g), oracle.p(b), 1e-5, int(fp16), oracle.p(y_ref),
+                              oracle.p(mean_ref), oracle.p(inv_ref)) == 0
+    dy = _rand(rng, shape, fp16)
+    dx_ref = np.zeros_like(x)
+    dg_ref = np.zeros(C, np.float32)
+    db_ref = np.zeros(C, np.float32)
+    assert ref.ref_bn_backward(oracle.p(dy), oracle.p(x), N, C, H, W, oracle.p(g), oracle.p(mean_ref),
+                               oracle.p(inv_ref), int(fp16), oracle.p(dx_ref), oracle.p(dg_ref), oracle.p(db_ref)) == 0
+    tdt = torch.float16 if fp16 else torch.float32
+    xt = torch.from_numpy(x).to("cuda", tdt)
+    gt, bt = torch.from_numpy(g).cuda(), torch.from_numpy(b).cuda()
+    y, mean, inv = sd.syncbn_forward(xt, gt, bt, 1e-5)
+    dx, dg, db = sd.syncbn_backward(torch.from_numpy(dy).to("cuda", tdt), xt, mean, inv, gt)
+    torch.cuda.synchronize()
+    tol = 1e-2 if fp16 else 1e-3
+    assert_close(mean, mean_ref, 1e-5, "mean")
+    assert_close(inv, inv_ref, 1e-5, "invstd")
+    assert_close(y, y_ref, tol, "y")
+    assert_close(dx, dx_ref, tol, "dx")
+    assert_close(dg, dg_ref, tol, "dgamma")
+    assert_close(db, db_ref, tol, "dbeta")
+
+
+@pytest.mark.parametrize("fp16", [False, True])
+@pytest.mark.parametrize("slope", [0.1, 1.0])
+@pytest.mark.parametrize("shape", BN_SHAPES)
+def test_iabn_fwd_bwd(ref, shape, fp16, slope):
+    from paper_1903_05831_b200 import simdet as sd
+    N, C, H, W = shape
+    rng = np.random.default_rng(3 * C + W)
+    x = _rand(rng, shape, fp16, 1.5) - 0.25
+    x = x.astype(np.float16).astype(np.float32) if fp16 else x
+    g = (1.0 + 0.2 * rng.standard_normal(C)).astype(np.float32)
+    g[np.abs(g) < 0.05] = 0.5
+    b = (0.1 * rng.standard_normal(C)).astype(np.float32)
+    y_ref = np.zeros_like(x)
+    mean_ref = np.zeros(C, np.float32)
+    inv_ref = np.zeros(C, np.float32)
+    assert ref.ref_iabn_forward(oracle.p(x), N, C, H, W, oracle.p(g), oracle.p(b), 1e-5, slope, int(fp16),
+                                oracle.p(y_ref), oracle.p(mean_ref), oracle.p(inv_ref)) == 0
+    dy = _rand(rng, shape, fp16)
+    dx_ref = np.zeros_like(x)
+    dg_ref = np.zeros(C, np.float32)
+    db_ref = np.zeros(C, np.float32)
+    assert ref.ref_iabn_backward(oracle.p(dy), oracle.p(y_ref), N, C, H, W, oracle.p(g), oracle.p(b),
+                                 oracle.p(mean_ref), oracle.p(inv_ref), 1e-5, slope, int(fp16), oracle.p(dx_ref),
+                                 oracle.p(dg_ref), oracle.p(db_ref)) == 0
+    tdt = torch.float16 if fp16 else torch.float32
+    gt, bt = torch.from_numpy(g).cuda(), torch.from_numpy(b).cuda()
+    y, mean, inv = sd.iabn_forward(torch.from_numpy(x).to("cuda", tdt), gt, bt, 1e-5, slope)
+    dx, dg, db = sd.iabn_backward(torch.from_numpy(dy).to("cuda", tdt), y, mean, inv, gt, bt, slope)
+    torch.cuda.synchronize()
+    tol = 1e-2 if fp16 else 1e-3
+    assert_close(y, y_ref, tol, "y")
+    assert_close(dx, dx_ref, tol, "dx")
+    assert_close(dg, dg_ref, tol, "dgamma")
+    assert_close(db, db_ref, tol, "dbeta")
+
+
+def test_iabn_errors():
+    """NonInvertibleError / DegenerateBatchError, src/memopt.cpp:229-235."""
+    import paper_1903_05831_b200 as pkg
+    from paper_1903_05831_b200 import simdet as sd
+    x = torch.randn(2, 8, 3, 3, device="cuda")
+    g = torch.ones(8, device="cuda")
+    b = torch.zeros(8, device="cuda")
+    with pytest.raises(pkg.NonInvertibleError):
+        sd.iabn_forward(x, g, b, 1e-5, 0.0)
+    g0 = g.clone()
+    g0[3] = 0
+    with pytest.raises(pkg.NonInvertibleError):
+        sd.iabn_forward(x, g0, b, 1e-5, 0.1)
+    with pytest.raises(pkg.DegenerateBatchError):
+        sd.iabn_forward(torch.randn(1, 8, 1, 1, device="cuda"), g, b, 1e-5, 0.1)
+
+
+@pytest.mark.parametrize("gfp16", [False, True])
+def test_fused_sgd_bitwise(orc, gfp16):
+    """apply_sgd (src/trainer.cpp:86-94) is FP32 elementwise: compare bit for bit."""
+    from paper_1903_05831_b200 import simdet as sd
+    rng = np.random.default_rng(11)
+    n = 1 << 20 | 77
+    w = rng.standard_normal(n).astype(np.float32)
+    v = (0.01 * rng.standard_normal(n)).astype(np.float32)
+    g = (300 * rng.standard_normal(n)).astype(np.float32)
+    if gfp16:
+        g = g.astype(np.float16).astype(np.float32)
+    scale, K = 128.0, 4
+    w_o, v_o = w.copy(), v.copy()
+    orc.orc_apply_sgd(oracle.p(w_o), oracle.p(v_o), oracle.p(g), n, 0.01, 0.9, scale * K)
+    wt, vt = torch.from_numpy(w).cuda(), torch.from_numpy(v).cuda()
+    gt = torch.from_numpy(g).cuda().to(torch.float16 if gfp16 else torch.float32)
+    w16 = torch.empty(n, device="cuda", dtype=torch.float16)
+    sc = torch.tensor([scale], dtype=torch.float64, device="cuda")
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    sd.apply_sgd(wt, vt, gt, 0.01, 0.9, float(K), w16=w16, flag=flag, scale=sc)
+    torch.cuda.synchronize()
+    assert np.array_equal(wt.cpu().numpy().view(np.uint32), w_o.view(np.uint32))
+    assert np.array_equal(vt.cpu().numpy().view(np.uint32), v_o.view(np.uint32))
+    assert np.array_equal(w16.cpu().numpy(), w_o.astype(np.float16))
+    # overflow flag set -> untouched (src/trainer.cpp:253)
+    flag.fill_(1)
+    before = wt.clone()
+    sd.apply_sgd(wt, vt, gt, 0.01, 0.9, float(K), flag=flag, scale=sc)
+    torch.cuda.synchronize()
+    assert torch.equal(before, wt)
+
+
+def test_nonfinite():
+    from paper_1903_05831_b200 import simdet as sd
+    for dtp in (torch.float32, torch.float16):
+        g = torch.randn(100003, device="cuda").to(dtp)
+        assert not sd.has_nonfinite(g)
+        g[77777] = float("inf")
+        assert sd.has_nonfinite(g)
+        g[77777] = float("nan")
+        assert sd.has_nonfinite(g)
+
+
+def test_update_scale_matches_reference(ref):
+    """device update_scale vs the reference's (src/precision.cpp:45-56)."""
+    from paper_1903_05831_b200 import simdet as sd
+    import ctypes as C
+    rng = np.random.default_rng(5)
+    pattern = (rng.random(400) < 0.1).astype(np.int32)
+    s_ref, g_ref = C.c_double(32768.0), C.c_int64(0)
+    sc = torch.tensor([32768.0], dtype=torch.float64, device="cuda")
+    good = torch.zeros(1, dtype=torch.int64, device="cuda")
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for ov in pattern:
+        ref.ref_update_scale(C.byref(s_ref), C.byref(g_ref), 1, 7, 2.0, 0.5, 1.0, 2.0**24, int(ov))
+        flag.fill_(int(ov))
+        sd.update_scale(sc, good, flag, True, growth_interval=7)
+        torch.cuda.synchronize()
+        assert sc.item() == s_ref.value and good.item() == g_ref.value
