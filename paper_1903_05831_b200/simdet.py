@@ -76,7 +76,11 @@ def ctx(device: int | None = None):
 
 
 def stream():
-    return _P(torch.cuda.current_stream().cuda_stream)
+    """torch's current stream; the legacy default stream (handle 0) is passed
+    as cudaStreamLegacy (0x1) because a NULL stream means "the context's own
+    stream" at the C ABI."""
+    h = torch.cuda.current_stream().cuda_stream
+    return _P(h if h else 1)
 
 
 def ptr(t):
