@@ -100,6 +100,95 @@ int sdb_update_scale(sdb_ctx* ctx, double* scale, int64_t* good_steps, const int
 /* binary16 RNE round trip / casts (src/half.cpp:9-71) */
 int sdb_cast(sdb_ctx* ctx, int src_dtype, const void* src, int dst_dtype, void* dst, int64_t n, void* stream);
 
+/* ---- detection operators (no reference implementation exists; semantics of
+ * the restated oracle, boxes/IoU/ordering per src/postproc.cpp:20-63). ---- */
+/* RPN proposal layer per image: top pre_k by (score desc, index asc), decode,
+ * clip, greedy bitmask NMS (IoU > iou in FP64), first post_k kept.
+ * logits [n_img][n_loc][A_pad], deltas [n_img][n_loc][4*A_pad] (dtype),
+ * anchors [n_loc*A][4] fp32; outputs rois [n_img][post_k][4], count [n_img]. */
+int sdb_rpn_proposal(sdb_ctx* ctx, int dtype, const void* logits, const void* deltas, const float* anchors, int n_img,
+                     int n_loc, int A, int A_pad, int pre_k, double iou, int post_k, float img_h, float img_w,
+                     float* rois, float* roi_scores, int32_t* count, int32_t* topk_order, void* stream);
+/* anchors [H*W*A][4] for scales x ratios (anchor a = ratio_i * n_scales + scale_j) */
+int sdb_make_anchors(sdb_ctx* ctx, int H, int W, float stride, const float* scales, int n_scales,
+                     const float* ratios, int n_ratios, float* out, void* stream);
+/* RoIAlign (aligned, fixed sampling ratio): feat [N,H,W,C], rois [R][5] =
+ * (batch, x1, y1, x2, y2); out [R,P,P,C].  Backward is an atomics-free gather. */
+int sdb_roialign_fwd(sdb_ctx* ctx, int dtype, const void* feat, int N, int H, int W, int C, const float* rois, int R,
+                     int P, float spatial_scale, int sampling_ratio, void* out, void* stream);
+int sdb_roialign_bwd(sdb_ctx* ctx, int dtype, const void* dy, int N, int H, int W, int C, const float* rois, int R,
+                     int P, float spatial_scale, int sampling_ratio, void* dfeat, void* stream);
+/* softmax cross-entropy, the reference CE op (src/model.cpp:101-151): mean over
+ * rows with label >= 0, backward scaled by *grad_scale (device double or NULL).
+ * logits/dlogits [R][ld] (first ncls columns valid); loss written to *loss. */
+int sdb_softmax_ce(sdb_ctx* ctx, int dtype, const void* logits, int R, int ncls, int ld, const int32_t* labels,
+                   const double* grad_scale, double* loss, void* dlogits, void* stream);
+
+/* ---- the data-parallel Faster R-CNN C4 training step (src/trainer.cpp:217-271) ---- */
+typedef struct {
+    int mode;            /* 0: fp32 + BN+ReLU (config C1); 1: fp16 + InPlace-ABN, fp32 masters */
+    int batch;           /* images per GPU */
+    int img_h, img_w;
+    int blocks[4];       /* bottlenecks in res2..res5 (res5 == 0: RoIAlign -> avgpool -> fc head) */
+    int num_classes;     /* foreground classes (background added) */
+    int rpn_channels;
+    int n_scales, n_ratios;
+    float scales[8], ratios[8];
+    int pre_nms, post_nms;
+    double nms_iou;
+    int rpn_batch;
+    double rpn_fg_frac, rpn_fg_thr, rpn_bg_thr;
+    int roi_batch;
+    double roi_fg_frac, roi_fg_thr, roi_bg_hi, roi_bg_lo;
+    int pool, sampling_ratio;
+    float lr, momentum, eps, slope;
+    int dynamic_scale;
+    double scale_init;
+    int64_t growth_interval;
+    double growth, backoff, min_scale, max_scale;
+    uint64_t seed;
+    int max_gt;
+    double bucket_mb;    /* fp16 gradient bucket size for the NCCL allreduce */
+} sdb_det_config;
+
+typedef struct sdb_det sdb_det;
+
+int sdb_det_create(sdb_ctx* ctx, const sdb_det_config* cfg, sdb_det** out);
+int sdb_det_destroy(sdb_det* det);
+/* parameter registry, in the reference's flat pack order (src/model.cpp:155-167 style) */
+int sdb_det_num_params(sdb_det* det, int* n_tensors, int64_t* n_conv_fc, int64_t* n_bn);
+/* kind: 0 conv [O,C,kh,kw], 1 fc [in,out], 2 bn gamma [C], 3 bn beta [C] (reference layouts) */
+int sdb_det_param_info(sdb_det* det, int idx, char* name, int name_len, int64_t* shape4, int* ndim, int* kind);
+int sdb_det_get_param(sdb_det* det, int idx, float* host);  /* fp32 master, reference layout */
+int sdb_det_set_param(sdb_det* det, int idx, const float* host);
+int sdb_det_get_grad(sdb_det* det, int idx, float* host);   /* last step's summed gradient (scaled) */
+/* feed one batch: images NHWC with C padded to 8 (dtype of the mode), on host
+ * (pinned, copied H2D on the step stream) or device; GT arrays on host
+ * ([batch][max_gt][4], [batch][max_gt], [batch]); slots = global batch slots
+ * (src/dataset.cpp:94) keying the sampling RNG. */
+int sdb_det_set_batch(sdb_det* det, const void* images, int images_on_host, const float* gt_boxes,
+                      const int32_t* gt_cls, const int32_t* gt_count, const int64_t* slots);
+/* synthesize the batch's images on device from the slots (N(0,1) pixels) */
+int sdb_det_synth_images(sdb_det* det, const int64_t* slots);
+int sdb_det_step(sdb_det* det);
+/* blocks until the step finished; losses[0..3] = rpn_cls, rpn_box, rcnn_cls,
+ * rcnn_box (allreduced /K), losses[4] = total; scale_used; overflow flag */
+int sdb_det_read_losses(sdb_det* det, double* losses5, double* scale_used, int* overflow);
+/* end-to-end call with HOST buffers: H2D of images+GT, the step, D2H of losses */
+int sdb_det_train_step_host(sdb_det* det, const void* images_host, const float* gt_boxes, const int32_t* gt_cls,
+                            const int32_t* gt_count, const int64_t* slots, double* losses5);
+/* debug/parity exports of the last step's discrete decisions & intermediates.
+ * what: 0 anchor labels (int8 [batch][nA]), 1 anchor targets (f32 [batch][nA][4]),
+ * 2 proposals (f32 [batch][post][4]), 3 proposal counts (i32 [batch]),
+ * 4 sampled rois (f32 [batch*roi_batch][5]), 5 roi labels (i32), 6 roi targets (f32 [..][4]),
+ * 7 rpn logits (dtype [batch][n_loc][A_pad]), 8 rpn deltas (dtype [batch][n_loc][4*A_pad]),
+ * 9 anchors (f32 [nA][4]), 10 C4 feature (dtype NHWC), 11 images (dtype NHWC8),
+ * 12 loss-scale state (f64 scale, then i64 good_steps). Returns bytes in *bytes. */
+int sdb_det_export(sdb_det* det, int what, void* host, int64_t capacity, int64_t* bytes);
+int sdb_det_dims(sdb_det* det, int* feat_h, int* feat_w, int* n_anchor_per_loc, int* a_pad);
+/* launches of libsdb kernels per step (counted at the first step) */
+int sdb_det_kernel_launches(sdb_det* det, int64_t* n);
+
 #ifdef __cplusplus
 }
 #endif

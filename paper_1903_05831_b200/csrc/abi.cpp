@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -12,6 +13,7 @@
 
 #include "../../include/sdb.h"
 #include "ctx.h"
+#include "detect.h"
 #include "sdb_internal.h"
 
 namespace {
@@ -44,6 +46,10 @@ int check_conv(int N, int H, int W, int C, int K, int R, int S, int stride, int 
 }
 
 }  // namespace
+
+namespace sdb {
+int set_error(int code, const char* msg) { return fail(code, msg); }
+}  // namespace sdb
 
 void* sdb_ctx::scratch(size_t bytes) {
     if (bytes <= ws_bytes) return ws;
@@ -225,6 +231,72 @@ int sdb_update_scale(sdb_ctx* ctx, double* scale, int64_t* good_steps, const int
     return cuda_status(sdb::update_scale_device(scale, good_steps, flag, dynamic, growth_interval, growth, backoff,
                                                 min_scale, max_scale, pick(ctx, stream)),
                        "update_scale");
+}
+
+int sdb_make_anchors(sdb_ctx* ctx, int H, int W, float stride, const float* scales, int n_scales, const float* ratios,
+                     int n_ratios, float* out, void* stream) {
+    if (H < 1 || W < 1 || n_scales < 1 || n_scales > 8 || n_ratios < 1 || n_ratios > 8)
+        return fail(SDB_PARAM, "anchors: bad grid or scale/ratio count (1..8)");
+    sdb::AnchorCfg c{};
+    c.H = H; c.W = W; c.stride = stride; c.ns = n_scales; c.nr = n_ratios;
+    for (int i = 0; i < n_scales; ++i) c.scales[i] = scales[i];
+    for (int i = 0; i < n_ratios; ++i) c.ratios[i] = ratios[i];
+    return cuda_status(sdb::make_anchors(c, out, pick(ctx, stream)), "make_anchors");
+}
+
+int sdb_rpn_proposal(sdb_ctx* ctx, int dtype, const void* logits, const void* deltas, const float* anchors, int n_img,
+                     int n_loc, int A, int A_pad, int pre_k, double iou, int post_k, float img_h, float img_w,
+                     float* rois, float* roi_scores, int32_t* count, int32_t* topk_order, void* stream) {
+    if (!ctx) return fail(SDB_PARAM, "null ctx");
+    if (int rc = check_dtype(dtype)) return rc;
+    if (iou < 0.0 || iou > 1.0) return fail(SDB_PARAM, "iou threshold outside [0,1]");  // postproc.cpp:48
+    if (n_img < 1 || n_loc < 1 || A < 1 || A_pad < A || pre_k < 1 || post_k < 1)
+        return fail(SDB_SHAPE, "rpn_proposal: bad sizes");
+    if (std::min<int64_t>(pre_k, static_cast<int64_t>(n_loc) * A) > 16384)
+        return fail(SDB_UNSUPPORTED, "rpn_proposal: pre_k > 16384");
+    const size_t wsb = sdb::proposal_workspace_bytes(n_img, n_loc * A, pre_k);
+    void* ws = ctx->scratch(wsb);
+    if (!ws) return fail(SDB_CUDA, "workspace allocation failed");
+    std::vector<int32_t> dummy;
+    int32_t* keep = static_cast<int32_t*>(ctx->scratch(0)) ;
+    (void)keep;
+    // keep positions live in a second scratch region after the proposal workspace
+    void* ws2 = ctx->scratch(wsb + static_cast<size_t>(n_img) * post_k * 4 + 256);
+    sdb::ProposalArgs p{};
+    p.logits = logits; p.deltas = deltas; p.dtype = dtype; p.anchors = anchors;
+    p.n_img = n_img; p.n_loc = n_loc; p.A = A; p.A_pad = A_pad; p.pre_k = pre_k; p.post_k = post_k;
+    p.iou_thr = iou; p.img_h = img_h; p.img_w = img_w; p.clip_dw = static_cast<float>(std::log(1000.0 / 16.0));
+    p.rois = rois; p.roi_scores = roi_scores; p.count = count; p.topk_order_out = topk_order;
+    p.keep_pos = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(ws2) + ((wsb + 255) & ~size_t(255)));
+    return cuda_status(sdb::rpn_proposals(p, ws2, pick(ctx, stream)), "rpn_proposal");
+}
+
+int sdb_roialign_fwd(sdb_ctx* ctx, int dtype, const void* feat, int N, int H, int W, int C, const float* rois, int R,
+                     int P, float spatial_scale, int sampling_ratio, void* out, void* stream) {
+    if (int rc = check_dtype(dtype)) return rc;
+    if (C % 8 || P < 1 || sampling_ratio < 1 || R < 0) return fail(SDB_UNSUPPORTED, "roialign: C % 8, P, ratio");
+    return cuda_status(sdb::roialign_fwd(dtype, feat, N, H, W, C, rois, R, P, spatial_scale, sampling_ratio, out,
+                                         pick(ctx, stream)),
+                       "roialign_fwd");
+}
+
+int sdb_roialign_bwd(sdb_ctx* ctx, int dtype, const void* dy, int N, int H, int W, int C, const float* rois, int R,
+                     int P, float spatial_scale, int sampling_ratio, void* dfeat, void* stream) {
+    if (int rc = check_dtype(dtype)) return rc;
+    if (C % 8 || P < 1 || P > 16 || sampling_ratio < 1 || R < 0)
+        return fail(SDB_UNSUPPORTED, "roialign: C % 8, P <= 16, ratio");
+    return cuda_status(sdb::roialign_bwd(dtype, dy, N, H, W, C, rois, R, P, spatial_scale, sampling_ratio, dfeat,
+                                         pick(ctx, stream)),
+                       "roialign_bwd");
+}
+
+int sdb_softmax_ce(sdb_ctx* ctx, int dtype, const void* logits, int R, int ncls, int ld, const int32_t* labels,
+                   const double* grad_scale, double* loss, void* dlogits, void* stream) {
+    if (int rc = check_dtype(dtype)) return rc;
+    if (R < 1 || ncls < 1 || ld < ncls) return fail(SDB_SHAPE, "cross-entropy expects [batch, classes] logits");
+    sdb::LossArgs la{grad_scale, loss, 0};
+    return cuda_status(sdb::softmax_ce(dtype, logits, R, ncls, ld, labels, dlogits, la, nullptr, pick(ctx, stream)),
+                       "softmax_ce");
 }
 
 int sdb_cast(sdb_ctx* ctx, int src_dtype, const void* src, int dst_dtype, void* dst, int64_t n, void* stream) {

@@ -39,7 +39,10 @@ void comm_destroy(Ctx* c) {
 // in-place SUM allreduce (the reference's allreduce_sum contract)
 cudaError_t comm_allreduce_sum(Ctx* c, void* buf, int64_t n, int dtype, cudaStream_t st) {
     if (c->world == 1 || n == 0) return cudaSuccess;
-    const ncclDataType_t t = dtype == kF16 ? ncclFloat16 : (dtype == kF32 ? ncclFloat32 : ncclInt32);
+    // dtype: kF32, kF16, 2 = int32, 3 = float64
+    const ncclDataType_t t = dtype == kF16 ? ncclFloat16
+                             : dtype == kF32 ? ncclFloat32
+                             : dtype == 3 ? ncclFloat64 : ncclInt32;
     const ncclResult_t r =
         ncclAllReduce(buf, buf, static_cast<size_t>(n), t, ncclSum, static_cast<ncclComm_t>(c->nccl), st);
     return r == ncclSuccess ? cudaSuccess : cudaErrorUnknown;

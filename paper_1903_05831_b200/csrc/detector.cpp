@@ -1,0 +1,1023 @@
+// detector.cpp -- the B200 step driver: one data-parallel Faster R-CNN ResNet-C4
+// training step as a static C++ schedule over the sm_100a kernels.
+//
+// Mirrors the reference step body (src/trainer.cpp:217-271, order in
+// SURVEY.md Appendix B):
+//   fp16 shadows of conv/fc weights, BN params fp32      trainer.cpp:222-227
+//   forward (every fp16 op output rounded RNE)            tensor.cpp:79-82
+//   losses with the loss scale folded into backward      model.cpp:132-150
+//   backward, grads finalised in the leaf dtype           autograd.cpp:437-485
+//   loss allreduce /K; gradient allreduce (fp16 buckets,  trainer.cpp:240-251
+//     issued as each bucket's last wgrad completes, overlapped with backward)
+//   overflow = nonfinite(summed grads); fused unscale+SGD trainer.cpp:252-254,86-94
+//   update_scale                                          precision.cpp:45-56
+// The reference's Tape/CustomOp machinery (autograd.cpp) is replaced by this
+// fixed schedule; all activations live in HBM buffers allocated once, and the
+// whole step is captured into a CUDA graph after the first (eager) step.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/sdb.h"
+#include "ctx.h"
+#include "detect.h"
+#include "sdb_internal.h"
+
+namespace sdb {
+cudaError_t comm_allreduce_sum(Ctx* c, void* buf, int64_t n, int dtype, cudaStream_t st);
+}
+
+using namespace sdb;
+
+namespace {
+
+int det_fail(int code, const std::string& m) { return sdb::set_error(code, m.c_str()); }
+
+#define CK(expr)                                                                          \
+    do {                                                                                  \
+        cudaError_t e_ = (expr);                                                          \
+        if (e_ != cudaSuccess) throw std::runtime_error(std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+uint64_t mix64(uint64_t a, uint64_t b) {
+    uint64_t z = a ^ (b + 0x9e3779b97f4a7c15ull);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+
+// splitmix64 Rng of the reference (src/tensor.cpp:38-49), for bit-identical init
+struct Rng {
+    uint64_t s;
+    uint64_t next() {
+        uint64_t z = (s += 0x9e3779b97f4a7c15ull);
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+        return z ^ (z >> 31);
+    }
+    float uniform(float lo, float hi) {
+        const float u = static_cast<float>(next() >> 40) * 0x1.0p-24f;
+        return lo + (hi - lo) * u;
+    }
+};
+
+int round_up(int v, int m) { return (v + m - 1) / m * m; }
+
+struct Act {
+    void* p = nullptr;
+    int n = 0, h = 0, w = 0, c = 0;
+    int64_t numel() const { return static_cast<int64_t>(n) * h * w * c; }
+};
+
+struct Param {
+    std::string name;
+    std::vector<int64_t> ref_shape;
+    int kind = 0;  // 0 conv, 1 fc, 2 gamma, 3 beta
+    int64_t off = 0, numel = 0;  // in the conv/fc flat or the bn flat
+    int K = 0, R = 1, S = 1, C = 0;  // device KRSC dims (conv/fc)
+};
+
+struct ConvL {
+    int p = -1;  // param index
+    ConvShape g{};
+};
+
+struct NormL {
+    int pg = -1, pb = -1;  // gamma/beta param index
+    int C = 0;
+    float* mean = nullptr;
+    float* invstd = nullptr;
+    int act = 0;  // mode 0: 0 none / 1 relu; mode 1: 2 (iabn)
+    float slope = 1.0f;
+};
+
+struct Block {
+    ConvL c1, c2, c3, down;
+    NormL n1, n2, n3, nd;
+    bool has_down = false;
+    Act in, z1, a1, z2, a2, z3, b3, zd, d, out;
+};
+
+}  // namespace
+
+struct sdb_det {
+    sdb_ctx* ctx = nullptr;
+    sdb_det_config cfg{};
+    int dt = kF16;
+    int es = 2;
+    std::vector<Param> params;
+    int64_t n_w = 0, n_bn = 0;
+    // flat parameter state
+    float *w32 = nullptr, *v32 = nullptr, *bn32 = nullptr, *bnv = nullptr, *bng = nullptr;
+    void* wdev = nullptr;  // weights used by the kernels: fp16 shadow (mode 1) or w32 (mode 0)
+    void* g = nullptr;     // conv/fc grads (dtype)
+    // loss-scale state + outputs
+    double* scale = nullptr;
+    int64_t* good = nullptr;
+    int* flag = nullptr;
+    double* losses = nullptr;      // [8]: 4 losses, (reduced copy)
+    double* scale_used = nullptr;  // snapshot of the scale used by the step
+    // layers
+    ConvL stem;
+    NormL stem_n;
+    Act img, stem_z, stem_a, pool;
+    uint8_t* pool_arg = nullptr;
+    std::vector<Block> backbone, head;
+    ConvL rpn_conv, rpn_cls, rpn_bbox, fc_cls, fc_bbox;
+    Act c4, rpn_z, rpn_a, rpn_logits, rpn_deltas, roi_feat, head_out, pooled, cls_logits, bbox_pred;
+    int A = 0, A_pad = 0, n_loc = 0, nA = 0, fh = 0, fw = 0, ncls = 0, ncls_pad = 0, nbox_pad = 0;
+    int R = 0, P = 0, head_hw = 0, feat_c = 0;
+    float* anchors = nullptr;
+    // targets
+    float* gt = nullptr;
+    int32_t *gt_cls = nullptr, *gt_count = nullptr;
+    uint64_t* keys = nullptr;  // [2*batch]: rpn keys then rcnn keys
+    int8_t* a_labels = nullptr;
+    float* a_targets = nullptr;
+    float* props = nullptr;
+    int32_t *prop_count = nullptr, *keep_pos = nullptr;
+    int8_t* pt_flag = nullptr;
+    int32_t* pt_arg = nullptr;
+    float* rois = nullptr;
+    int32_t *roi_labels = nullptr, *roi_count = nullptr;
+    float* roi_targets = nullptr;
+    // grad scratch
+    void* gbuf[5] = {};
+    void *d_rpn_logits = nullptr, *d_rpn_deltas = nullptr, *d_cls = nullptr, *d_bbox = nullptr;
+    int64_t gbuf_elems = 0;
+    void* ws = nullptr;
+    size_t ws_bytes = 0;
+    // host staging
+    float* h_gt = nullptr;
+    int32_t *h_cls = nullptr, *h_cnt = nullptr;
+    uint64_t* h_keys = nullptr;
+    double* h_losses = nullptr;
+    // comm
+    cudaStream_t comm = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    std::vector<cudaEvent_t> bucket_ev;
+    std::vector<std::pair<int64_t, int64_t>> buckets;  // [lo, hi) element ranges of g, issued from the end
+    // graph
+    cudaGraphExec_t gexec = nullptr;
+    bool use_graph = true;
+    int steps_done = 0;
+    int64_t launches = 0;
+    std::vector<void*> allocs;
+
+    void* alloc(size_t bytes) {
+        void* p = nullptr;
+        CK(cudaMalloc(&p, std::max<size_t>(bytes, 256)));
+        allocs.push_back(p);
+        return p;
+    }
+    Act act(int n, int h, int w, int c) {
+        Act a;
+        a.n = n; a.h = h; a.w = w; a.c = c;
+        a.p = alloc(static_cast<size_t>(a.numel()) * es);
+        return a;
+    }
+    float* wptr(int pi) { return w32 + params[pi].off; }
+    void* wdev_ptr(int pi) { return static_cast<uint8_t*>(wdev) + params[pi].off * (dt == kF16 ? 2 : 4); }
+    void* gptr(int pi) { return static_cast<uint8_t*>(g) + params[pi].off * es; }
+    float* bnp(int pi) { return bn32 + params[pi].off; }
+    float* bngp(int pi) { return bng + params[pi].off; }
+
+    int add_param(const std::string& name, std::vector<int64_t> shape, int kind, int K = 0, int R = 1, int S = 1,
+                  int C = 0) {
+        Param p;
+        p.name = name;
+        p.ref_shape = std::move(shape);
+        p.kind = kind;
+        if (kind <= 1) {
+            p.K = K; p.R = R; p.S = S; p.C = C;
+            p.numel = static_cast<int64_t>(K) * R * S * C;
+            p.off = n_w;
+            n_w += round_up(static_cast<int>(p.numel), 8);  // 16B alignment of every slice
+        } else {
+            p.numel = p.ref_shape[0];
+            p.off = n_bn;
+            n_bn += p.numel;
+        }
+        params.push_back(p);
+        return static_cast<int>(params.size()) - 1;
+    }
+
+    ConvL conv(const std::string& name, int cin, int cout, int k, int stride, int pad) {
+        ConvL c;
+        c.p = add_param(name, {cout, cin, k, k}, 0, cout, k, k, cin);
+        c.g.K = cout; c.g.R = k; c.g.S = k; c.g.C = cin; c.g.stride = stride; c.g.pad = pad;
+        return c;
+    }
+    NormL norm(const std::string& name, int C, bool relu_or_leaky, bool identity) {
+        NormL nl;
+        nl.C = C;
+        nl.pg = add_param(name + ".gamma", {C}, 2);
+        nl.pb = add_param(name + ".beta", {C}, 3);
+        nl.mean = static_cast<float*>(alloc(C * 4));
+        nl.invstd = static_cast<float*>(alloc(C * 4));
+        if (cfg.mode == 0) {
+            nl.act = relu_or_leaky ? 1 : 0;
+        } else {
+            nl.act = 2;
+            nl.slope = identity ? 1.0f : cfg.slope;
+        }
+        return nl;
+    }
+};
+
+namespace {
+
+// ------------------------------------------------------------------ build
+void build_stage(sdb_det* d, std::vector<Block>& out, const std::string& pref, int nblocks, int cin, int width,
+                 int cout, int stride) {
+    for (int b = 0; b < nblocks; ++b) {
+        Block bl;
+        const std::string p = pref + "." + std::to_string(b);
+        const int s = b == 0 ? stride : 1;
+        const int ci = b == 0 ? cin : cout;
+        bl.c1 = d->conv(p + ".conv1", ci, width, 1, s, 0);
+        bl.n1 = d->norm(p + ".bn1", width, true, false);
+        bl.c2 = d->conv(p + ".conv2", width, width, 3, 1, 1);
+        bl.n2 = d->norm(p + ".bn2", width, true, false);
+        bl.c3 = d->conv(p + ".conv3", width, cout, 1, 1, 0);
+        bl.n3 = d->norm(p + ".bn3", cout, false, true);
+        if (b == 0) {
+            bl.has_down = true;
+            bl.down = d->conv(p + ".down", ci, cout, 1, s, 0);
+            bl.nd = d->norm(p + ".down_bn", cout, false, true);
+        }
+        out.push_back(bl);
+    }
+}
+
+void alloc_stage(sdb_det* d, std::vector<Block>& st, Act in) {
+    for (auto& bl : st) {
+        bl.in = in;
+        auto set = [&](ConvL& c, const Act& x) {
+            c.g.N = x.n; c.g.H = x.h; c.g.W = x.w;
+        };
+        set(bl.c1, in);
+        bl.z1 = d->act(in.n, bl.c1.g.Ho(), bl.c1.g.Wo(), bl.c1.g.K);
+        bl.a1 = d->cfg.mode == 0 ? d->act(bl.z1.n, bl.z1.h, bl.z1.w, bl.z1.c) : bl.z1;
+        set(bl.c2, bl.a1);
+        bl.z2 = d->act(in.n, bl.c2.g.Ho(), bl.c2.g.Wo(), bl.c2.g.K);
+        bl.a2 = d->cfg.mode == 0 ? d->act(bl.z2.n, bl.z2.h, bl.z2.w, bl.z2.c) : bl.z2;
+        set(bl.c3, bl.a2);
+        bl.z3 = d->act(in.n, bl.c3.g.Ho(), bl.c3.g.Wo(), bl.c3.g.K);
+        bl.b3 = d->cfg.mode == 0 ? d->act(bl.z3.n, bl.z3.h, bl.z3.w, bl.z3.c) : bl.z3;
+        if (bl.has_down) {
+            set(bl.down, in);
+            bl.zd = d->act(in.n, bl.down.g.Ho(), bl.down.g.Wo(), bl.down.g.K);
+            bl.d = d->cfg.mode == 0 ? d->act(bl.zd.n, bl.zd.h, bl.zd.w, bl.zd.c) : bl.zd;
+        }
+        bl.out = d->act(bl.z3.n, bl.z3.h, bl.z3.w, bl.z3.c);
+        d->gbuf_elems = std::max({d->gbuf_elems, in.numel(), bl.z1.numel(), bl.z2.numel(), bl.z3.numel()});
+        in = bl.out;
+    }
+}
+
+void init_params(sdb_det* d) {
+    // init_model_params semantics (src/model.cpp:175-195): U(+-sqrt(1/fan_in)),
+    // gamma 1, beta 0; seed per tensor = seed*0x9e37 + i*0x85eb (1-based i)
+    std::vector<float> wh(static_cast<size_t>(d->n_w), 0.0f), bh(static_cast<size_t>(d->n_bn), 0.0f);
+    uint64_t i = 0;
+    for (auto& p : d->params) {
+        ++i;
+        if (p.kind == 2) {
+            std::fill(bh.begin() + p.off, bh.begin() + p.off + p.numel, 1.0f);
+            continue;
+        }
+        if (p.kind == 3) continue;
+        int64_t fan, n = 1;
+        for (int64_t s : p.ref_shape) n *= s;
+        if (p.kind == 0) fan = p.ref_shape[1] * p.ref_shape[2] * p.ref_shape[3];
+        else fan = p.ref_shape[0];
+        const float s = static_cast<float>(std::sqrt(1.0 / static_cast<double>(fan)));
+        Rng rng{d->cfg.seed * 0x9e37ull + i * 0x85ebull};
+        std::vector<float> ref(static_cast<size_t>(n));
+        for (auto& x : ref) x = rng.uniform(-s, s);
+        // scatter the reference layout into the device layout
+        float* dst = wh.data() + p.off;
+        if (p.kind == 0) {
+            const int64_t O = p.ref_shape[0], Ci = p.ref_shape[1], kh = p.ref_shape[2], kw = p.ref_shape[3];
+            for (int64_t o = 0; o < O; ++o)
+                for (int64_t c = 0; c < Ci; ++c)
+                    for (int64_t r = 0; r < kh; ++r)
+                        for (int64_t q = 0; q < kw; ++q)
+                            dst[((o * p.R + r) * p.S + q) * p.C + c] = ref[((o * Ci + c) * kh + r) * kw + q];
+        } else {
+            const int64_t in = p.ref_shape[0], outc = p.ref_shape[1];
+            for (int64_t ii = 0; ii < in; ++ii)
+                for (int64_t o = 0; o < outc; ++o) dst[o * p.C + ii] = ref[ii * outc + o];
+        }
+    }
+    CK(cudaMemcpy(d->w32, wh.data(), wh.size() * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d->bn32, bh.data(), bh.size() * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemset(d->v32, 0, wh.size() * 4));
+    CK(cudaMemset(d->bnv, 0, bh.size() * 4));
+    if (d->dt == kF16) CK(cast_f32_f16(d->w32, static_cast<__half*>(d->wdev), d->n_w, d->ctx->stream));
+    CK(cudaStreamSynchronize(d->ctx->stream));
+}
+
+size_t max_ws(sdb_det* d) {
+    size_t m = 1 << 20;
+    auto conv_ws = [&](const ConvL& c) { m = std::max(m, conv_wgrad_workspace(c.g, d->dt)); };
+    auto norm_ws = [&](const NormL& n, int64_t rows) { m = std::max(m, norm_workspace_bytes(rows, n.C)); };
+    conv_ws(d->stem);
+    norm_ws(d->stem_n, static_cast<int64_t>(d->stem_z.n) * d->stem_z.h * d->stem_z.w);
+    for (auto* st : {&d->backbone, &d->head})
+        for (auto& b : *st) {
+            conv_ws(b.c1); conv_ws(b.c2); conv_ws(b.c3);
+            norm_ws(b.n1, static_cast<int64_t>(b.z1.n) * b.z1.h * b.z1.w);
+            norm_ws(b.n2, static_cast<int64_t>(b.z2.n) * b.z2.h * b.z2.w);
+            norm_ws(b.n3, static_cast<int64_t>(b.z3.n) * b.z3.h * b.z3.w);
+            if (b.has_down) conv_ws(b.down);
+        }
+    conv_ws(d->rpn_conv); conv_ws(d->rpn_cls); conv_ws(d->rpn_bbox); conv_ws(d->fc_cls); conv_ws(d->fc_bbox);
+    m = std::max(m, proposal_workspace_bytes(d->cfg.batch, d->nA, d->cfg.pre_nms));
+    m = std::max(m, anchor_target_workspace_bytes(d->cfg.batch, d->nA, d->cfg.max_gt));
+    return m;
+}
+
+// ------------------------------------------------------------------ forward helpers
+void conv_fwd(sdb_det* d, const ConvL& c, const Act& x, const Act& y) {
+    CK(conv_fprop(c.g, d->dt, x.p, d->wdev_ptr(c.p), y.p, d->ctx->stream));
+}
+
+void norm_fwd(sdb_det* d, const NormL& n, const Act& z, const Act& a) {
+    const int64_t rows = static_cast<int64_t>(z.n) * z.h * z.w;
+    CK(bn_forward(d->dt, z.p, d->bnp(n.pg), d->bnp(n.pb), a.p, n.mean, n.invstd, rows, n.C, d->cfg.eps, n.act,
+                  n.slope, d->ws, d->ctx->stream));
+}
+
+// dz from da for a norm layer; y = a (stored output), x = z (pre-norm, mode 0 only)
+void norm_bwd(sdb_det* d, const NormL& n, const Act& z, const Act& a, const void* da, void* dz) {
+    const int64_t rows = static_cast<int64_t>(z.n) * z.h * z.w;
+    if (d->cfg.mode == 0) {
+        CK(bn_backward(d->dt, da, z.p, n.act == 1 ? a.p : nullptr, d->bnp(n.pg), n.mean, n.invstd, dz,
+                       d->bngp(n.pg), d->bngp(n.pb), rows, n.C, d->ws, d->ctx->stream));
+    } else {
+        CK(iabn_backward(d->dt, da, a.p, d->bnp(n.pg), d->bnp(n.pb), n.mean, n.invstd, dz, d->bngp(n.pg),
+                         d->bngp(n.pb), rows, n.C, n.slope, d->ws, d->ctx->stream));
+    }
+}
+
+void block_fwd(sdb_det* d, Block& b) {
+    conv_fwd(d, b.c1, b.in, b.z1);
+    norm_fwd(d, b.n1, b.z1, b.a1);
+    conv_fwd(d, b.c2, b.a1, b.z2);
+    norm_fwd(d, b.n2, b.z2, b.a2);
+    conv_fwd(d, b.c3, b.a2, b.z3);
+    norm_fwd(d, b.n3, b.z3, b.b3);
+    const Act* sc = &b.in;
+    if (b.has_down) {
+        conv_fwd(d, b.down, b.in, b.zd);
+        norm_fwd(d, b.nd, b.zd, b.d);
+        sc = &b.d;
+    }
+    CK(add_act(d->dt, b.b3.p, sc->p, b.out.p, b.out.numel(), d->cfg.mode == 0 ? 1 : 2, d->cfg.slope, d->ctx->stream));
+}
+
+// ------------------------------------------------------------------ backward helpers
+struct Bwd {
+    sdb_det* d;
+    int64_t issued_lo;  // lowest g offset whose bucket has been issued
+    size_t next_bucket = 0;
+};
+
+void grads_ready(Bwd& B, int pi) {
+    sdb_det* d = B.d;
+    if (d->ctx->world == 1) return;
+    const int64_t off = d->params[pi].off;
+    while (B.next_bucket < d->buckets.size() && off <= d->buckets[B.next_bucket].first) {
+        const auto [lo, hi] = d->buckets[B.next_bucket];
+        cudaEvent_t ev = d->bucket_ev[B.next_bucket];
+        CK(cudaEventRecord(ev, d->ctx->stream));
+        CK(cudaStreamWaitEvent(d->comm, ev, 0));
+        CK(comm_allreduce_sum(d->ctx, static_cast<uint8_t*>(d->g) + lo * d->es, hi - lo, d->dt, d->comm));
+        ++B.next_bucket;
+    }
+}
+
+void conv_wgrad_to(Bwd& B, const ConvL& c, const Act& x, const void* dy) {
+    sdb_det* d = B.d;
+    CK(conv_wgrad(c.g, d->dt, x.p, dy, d->gptr(c.p), d->ws, d->ws_bytes, d->ctx->stream));
+    grads_ready(B, c.p);
+}
+
+// backward of a bottleneck; dout = grad wrt b.out (buffer may be clobbered);
+// writes grad wrt b.in into dx.  Uses scratch buffers s0..s2.
+void block_bwd(Bwd& B, Block& b, void* dout, void* dx, void* s0, void* s1, void* s2) {
+    sdb_det* d = B.d;
+    cudaStream_t st = d->ctx->stream;
+    const float neg = d->cfg.mode == 0 ? 0.0f : d->cfg.slope;
+    // add + activation: dS = act'(out) * dout   (rounded at the add node)
+    void* dS = s0;
+    CK(act_bwd(d->dt, dout, b.out.p, dS, b.out.numel(), neg, st));
+    // shortcut first (its params come last in the block's pack order)
+    if (b.has_down) {
+        norm_bwd(d, b.nd, b.zd, b.d, dS, s1);
+        conv_wgrad_to(B, b.down, b.in, s1);
+        CK(conv_dgrad(b.down.g, d->dt, s1, d->wdev_ptr(b.down.p), dx, 0, st));
+    } else {
+        CK(cudaMemcpyAsync(dx, dS, b.in.numel() * d->es, cudaMemcpyDeviceToDevice, st));
+    }
+    norm_bwd(d, b.n3, b.z3, b.b3, dS, s1);
+    conv_wgrad_to(B, b.c3, b.a2, s1);
+    CK(conv_dgrad(b.c3.g, d->dt, s1, d->wdev_ptr(b.c3.p), s2, 0, st));
+    norm_bwd(d, b.n2, b.z2, b.a2, s2, s1);
+    conv_wgrad_to(B, b.c2, b.a1, s1);
+    CK(conv_dgrad(b.c2.g, d->dt, s1, d->wdev_ptr(b.c2.p), s2, 0, st));
+    norm_bwd(d, b.n1, b.z1, b.a1, s2, s1);
+    conv_wgrad_to(B, b.c1, b.in, s1);
+    CK(conv_dgrad(b.c1.g, d->dt, s1, d->wdev_ptr(b.c1.p), dx, 1, st));
+}
+
+// ------------------------------------------------------------------ the step
+void run_step(sdb_det* d) {
+    cudaStream_t st = d->ctx->stream;
+    const auto& cf = d->cfg;
+    // ---- forward: backbone
+    conv_fwd(d, d->stem, d->img, d->stem_z);
+    norm_fwd(d, d->stem_n, d->stem_z, d->stem_a);
+    CK(maxpool_fwd(d->dt, d->stem_a.p, d->stem_a.n, d->stem_a.h, d->stem_a.w, d->stem_a.c, 3, 2, 1, d->pool.p,
+                   d->pool_arg, st));
+    for (auto& b : d->backbone) block_fwd(d, b);
+    // ---- RPN head
+    conv_fwd(d, d->rpn_conv, d->c4, d->rpn_z);
+    CK(relu_fwd(d->dt, d->rpn_z.p, d->rpn_a.p, d->rpn_a.numel(), st));
+    conv_fwd(d, d->rpn_cls, d->rpn_a, d->rpn_logits);
+    conv_fwd(d, d->rpn_bbox, d->rpn_a, d->rpn_deltas);
+    // ---- targets and proposals (no gradient)
+    AnchorTargetArgs at{};
+    at.anchors = d->anchors; at.nA = d->nA; at.n_img = cf.batch; at.gt = d->gt; at.gt_stride = cf.max_gt;
+    at.gt_count = d->gt_count; at.img_h = static_cast<float>(cf.img_h); at.img_w = static_cast<float>(cf.img_w);
+    at.keys = d->keys; at.fg_thr = cf.rpn_fg_thr; at.bg_thr = cf.rpn_bg_thr; at.batch = cf.rpn_batch;
+    at.fg_cap = static_cast<int>(cf.rpn_fg_frac * cf.rpn_batch); at.labels = d->a_labels; at.targets = d->a_targets;
+    CK(anchor_targets(at, d->ws, st));
+    ProposalArgs pa{};
+    pa.logits = d->rpn_logits.p; pa.deltas = d->rpn_deltas.p; pa.dtype = d->dt; pa.anchors = d->anchors;
+    pa.n_img = cf.batch; pa.n_loc = d->n_loc; pa.A = d->A; pa.A_pad = d->A_pad; pa.pre_k = cf.pre_nms;
+    pa.post_k = cf.post_nms; pa.iou_thr = cf.nms_iou; pa.img_h = static_cast<float>(cf.img_h);
+    pa.img_w = static_cast<float>(cf.img_w); pa.clip_dw = static_cast<float>(std::log(1000.0 / 16.0));
+    pa.rois = d->props; pa.roi_scores = nullptr; pa.keep_pos = d->keep_pos; pa.count = d->prop_count;
+    CK(rpn_proposals(pa, d->ws, st));
+    ProposalTargetArgs pt{};
+    pt.proposals = d->props; pt.prop_stride = cf.post_nms; pt.prop_count = d->prop_count; pt.gt = d->gt;
+    pt.gt_cls = d->gt_cls; pt.gt_stride = cf.max_gt; pt.gt_count = d->gt_count; pt.keys = d->keys + cf.batch;
+    pt.fg_thr = cf.roi_fg_thr; pt.bg_hi = cf.roi_bg_hi; pt.bg_lo = cf.roi_bg_lo; pt.batch = cf.roi_batch;
+    pt.fg_cap = static_cast<int>(std::llround(cf.roi_fg_frac * cf.roi_batch)); pt.n_img = cf.batch;
+    pt.work_flag = d->pt_flag; pt.work_arg = d->pt_arg; pt.work_stride = cf.post_nms + cf.max_gt;
+    pt.out_rois = d->rois; pt.out_labels = d->roi_labels; pt.out_targets = d->roi_targets; pt.out_src = nullptr;
+    pt.out_count = d->roi_count;
+    CK(proposal_targets(pt, st));
+    // ---- RoI head
+    const float sscale = 1.0f / 16.0f;
+    CK(roialign_fwd(d->dt, d->c4.p, d->c4.n, d->c4.h, d->c4.w, d->c4.c, d->rois, d->R, d->P, sscale,
+                    cf.sampling_ratio, d->roi_feat.p, st));
+    for (auto& b : d->head) block_fwd(d, b);
+    CK(avgpool_fwd(d->dt, d->head_out.p, d->R, d->head_out.h * d->head_out.w, d->feat_c, d->pooled.p, st));
+    conv_fwd(d, d->fc_cls, d->pooled, d->cls_logits);
+    conv_fwd(d, d->fc_bbox, d->pooled, d->bbox_pred);
+    // ---- losses (scale folded into backward)
+    CK(cudaMemcpyAsync(d->scale_used, d->scale, 8, cudaMemcpyDeviceToDevice, st));
+    void* g0 = d->d_cls;
+    void* g1 = d->d_bbox;
+    LossArgs la{d->scale, d->losses, 0};
+    CK(sigmoid_bce(d->dt, d->rpn_logits.p, static_cast<int64_t>(d->n_loc) * cf.batch, d->A, d->A_pad, d->a_labels,
+                   d->d_rpn_logits, la, nullptr, st));
+    la.slot = 1;
+    CK(rpn_smooth_l1(d->dt, d->rpn_deltas.p, static_cast<int64_t>(d->n_loc) * cf.batch, d->A, d->A_pad, d->a_labels,
+                     d->a_targets, 1.0 / 9.0, static_cast<double>(cf.rpn_batch) * cf.batch, d->d_rpn_deltas, la,
+                     nullptr, st));
+    la.slot = 2;
+    CK(softmax_ce(d->dt, d->cls_logits.p, d->R, d->ncls, d->ncls_pad, d->roi_labels, g0, la, nullptr, st));
+    la.slot = 3;
+    CK(rcnn_smooth_l1(d->dt, d->bbox_pred.p, d->R, d->nbox_pad, d->roi_labels, d->roi_targets, 1.0, g1, la, nullptr,
+                      st));
+
+    // ---- backward
+    Bwd B{d, 0, 0};
+    // fc layers (bbox then cls: reverse pack order)
+    void* dpool = d->gbuf[2];
+    conv_wgrad_to(B, d->fc_bbox, d->pooled, g1);
+    CK(conv_dgrad(d->fc_bbox.g, d->dt, g1, d->wdev_ptr(d->fc_bbox.p), dpool, 0, st));
+    conv_wgrad_to(B, d->fc_cls, d->pooled, g0);
+    CK(conv_dgrad(d->fc_cls.g, d->dt, g0, d->wdev_ptr(d->fc_cls.p), dpool, 1, st));
+    // avgpool, then the res5 head
+    void* dhead = d->gbuf[3];
+    CK(avgpool_bwd(d->dt, dpool, d->R, d->head_out.h * d->head_out.w, d->feat_c, dhead, st));
+    void* cur = dhead;
+    void* spare = d->gbuf[2];
+    for (int i = static_cast<int>(d->head.size()) - 1; i >= 0; --i) {
+        block_bwd(B, d->head[i], cur, spare, d->gbuf[0], d->gbuf[1], d->gbuf[4]);
+        std::swap(cur, spare);
+    }
+    (void)spare;
+    // cur = d roi_feat
+    void* dc4 = d->gbuf[(cur == d->gbuf[2]) ? 3 : 2];
+    CK(roialign_bwd(d->dt, cur, d->c4.n, d->c4.h, d->c4.w, d->c4.c, d->rois, d->R, d->P, sscale, cf.sampling_ratio,
+                    dc4, st));
+    // RPN head backward (bbox, cls, conv)
+    void* drpn = d->gbuf[0];
+    conv_wgrad_to(B, d->rpn_bbox, d->rpn_a, d->d_rpn_deltas);
+    CK(conv_dgrad(d->rpn_bbox.g, d->dt, d->d_rpn_deltas, d->wdev_ptr(d->rpn_bbox.p), drpn, 0, st));
+    conv_wgrad_to(B, d->rpn_cls, d->rpn_a, d->d_rpn_logits);
+    CK(conv_dgrad(d->rpn_cls.g, d->dt, d->d_rpn_logits, d->wdev_ptr(d->rpn_cls.p), drpn, 1, st));
+    CK(act_bwd(d->dt, drpn, d->rpn_a.p, drpn, d->rpn_a.numel(), 0.0f, st));
+    conv_wgrad_to(B, d->rpn_conv, d->c4, drpn);
+    CK(conv_dgrad(d->rpn_conv.g, d->dt, drpn, d->wdev_ptr(d->rpn_conv.p), dc4, 1, st));
+    // backbone
+    cur = dc4;
+    spare = dc4 == d->gbuf[2] ? d->gbuf[3] : d->gbuf[2];
+    for (int i = static_cast<int>(d->backbone.size()) - 1; i >= 0; --i) {
+        block_bwd(B, d->backbone[i], cur, spare, d->gbuf[0], d->gbuf[1], d->gbuf[4]);
+        std::swap(cur, spare);
+    }
+    // maxpool, stem norm, stem wgrad (the image gradient is not needed)
+    CK(maxpool_bwd(d->dt, cur, d->pool_arg, d->stem_a.n, d->stem_a.h, d->stem_a.w, d->stem_a.c, 3, 2, 1, spare, st));
+    norm_bwd(d, d->stem_n, d->stem_z, d->stem_a, spare, d->gbuf[0]);
+    conv_wgrad_to(B, d->stem, d->img, d->gbuf[0]);
+
+    // ---- data-parallel reduction, overflow check, update
+    if (d->ctx->world > 1) {
+        grads_ready(B, 0);  // flush any remaining bucket
+        CK(cudaEventRecord(d->ev_fork, st));
+        CK(cudaStreamWaitEvent(d->comm, d->ev_fork, 0));
+        CK(comm_allreduce_sum(d->ctx, d->bng, d->n_bn, kF32, d->comm));
+        CK(comm_allreduce_sum(d->ctx, d->losses, 4, 3 /* f64 */, d->comm));
+        CK(cudaEventRecord(d->ev_join, d->comm));
+        CK(cudaStreamWaitEvent(st, d->ev_join, 0));
+    }
+    CK(cudaMemsetAsync(d->flag, 0, sizeof(int), st));
+    CK(nonfinite_check(d->dt, d->g, d->n_w, d->flag, st));
+    CK(nonfinite_check(kF32, d->bng, d->n_bn, d->flag, st));
+    const double K = static_cast<double>(d->ctx->world);
+    CK(fused_sgd(d->dt, d->g, d->w32, d->v32, d->dt == kF16 ? static_cast<__half*>(d->wdev) : nullptr, d->n_w, cf.lr,
+                 cf.momentum, d->scale, K, d->flag, st));
+    CK(fused_sgd(kF32, d->bng, d->bn32, d->bnv, nullptr, d->n_bn, cf.lr, cf.momentum, d->scale, K, d->flag, st));
+    CK(update_scale_device(d->scale, d->good, d->flag, cf.dynamic_scale, cf.growth_interval, cf.growth, cf.backoff,
+                           cf.min_scale, cf.max_scale, st));
+}
+
+}  // namespace
+
+// ====================================================================== ABI
+extern "C" {
+
+int sdb_det_create(sdb_ctx* ctx, const sdb_det_config* cfgp, sdb_det** out) {
+    if (!ctx || !cfgp || !out) return det_fail(SDB_PARAM, "null argument");
+    const sdb_det_config& cf = *cfgp;
+    if (cf.batch < 1 || cf.img_h < 32 || cf.img_w < 32) return det_fail(SDB_SHAPE, "bad batch/image size");
+    if (cf.mode != 0 && cf.mode != 1) return det_fail(SDB_PARAM, "mode must be 0 (fp32/BN) or 1 (fp16/IABN)");
+    if (cf.n_scales < 1 || cf.n_scales > 8 || cf.n_ratios < 1 || cf.n_ratios > 8) return det_fail(SDB_PARAM, "anchors");
+    if (cf.nms_iou < 0.0 || cf.nms_iou > 1.0) return det_fail(SDB_PARAM, "iou threshold outside [0,1]");
+    if (cf.mode == 1 && !(cf.slope > 0.0f)) return det_fail(SDB_NONINVERTIBLE, "iabn requires slope > 0");
+    auto* d = new sdb_det();
+    try {
+        d->ctx = ctx;
+        d->cfg = cf;
+        d->dt = cf.mode == 1 ? kF16 : kF32;
+        d->es = cf.mode == 1 ? 2 : 4;
+        d->use_graph = std::getenv("SDB_NO_GRAPH") == nullptr;
+        CK(cudaSetDevice(ctx->device));
+        const int b = cf.batch;
+        // ---- parameters (reference pack order)
+        d->stem = d->conv("stem.conv", 3, 64, 7, 2, 3);
+        d->params[d->stem.p].C = 8;  // input channels padded 3 -> 8 on device (16-byte rows)
+        d->n_w = d->params[d->stem.p].off + 64 * 7 * 7 * 8;
+        d->params[d->stem.p].numel = 64 * 7 * 7 * 8;
+        d->stem.g.C = 8;
+        d->stem_n = d->norm("stem.bn", 64, true, false);
+        build_stage(d, d->backbone, "res2", cf.blocks[0], 64, 64, 256, 1);
+        build_stage(d, d->backbone, "res3", cf.blocks[1], 256, 128, 512, 2);
+        build_stage(d, d->backbone, "res4", cf.blocks[2], 512, 256, 1024, 2);
+        d->A = cf.n_scales * cf.n_ratios;
+        d->A_pad = round_up(d->A, 8);
+        d->rpn_conv = d->conv("rpn.conv", 1024, cf.rpn_channels, 3, 1, 1);
+        {
+            const int pc = d->add_param("rpn.cls", {d->A, cf.rpn_channels, 1, 1}, 0, d->A_pad, 1, 1, cf.rpn_channels);
+            d->rpn_cls.p = pc;
+            d->rpn_cls.g = ConvShape{0, 0, 0, cf.rpn_channels, d->A_pad, 1, 1, 1, 0};
+            const int pb = d->add_param("rpn.bbox", {4 * d->A, cf.rpn_channels, 1, 1}, 0, 4 * d->A_pad, 1, 1,
+                                        cf.rpn_channels);
+            d->rpn_bbox.p = pb;
+            d->rpn_bbox.g = ConvShape{0, 0, 0, cf.rpn_channels, 4 * d->A_pad, 1, 1, 1, 0};
+        }
+        d->feat_c = 1024;
+        if (cf.blocks[3] > 0) {
+            build_stage(d, d->head, "res5", cf.blocks[3], 1024, 512, 2048, 2);
+            d->feat_c = 2048;
+        }
+        d->ncls = cf.num_classes + 1;
+        d->ncls_pad = round_up(d->ncls, 8);
+        d->nbox_pad = round_up(4 * d->ncls, 8);
+        d->fc_cls.p = d->add_param("fc.cls", {d->feat_c, d->ncls}, 1, d->ncls_pad, 1, 1, d->feat_c);
+        d->fc_bbox.p = d->add_param("fc.bbox", {d->feat_c, 4 * d->ncls}, 1, d->nbox_pad, 1, 1, d->feat_c);
+
+        // ---- activations
+        d->img = d->act(b, cf.img_h, cf.img_w, 8);
+        d->stem.g.N = b; d->stem.g.H = cf.img_h; d->stem.g.W = cf.img_w;
+        d->stem_z = d->act(b, d->stem.g.Ho(), d->stem.g.Wo(), 64);
+        d->stem_a = cf.mode == 0 ? d->act(b, d->stem_z.h, d->stem_z.w, 64) : d->stem_z;
+        const int ph = (d->stem_a.h + 2 - 3) / 2 + 1, pw = (d->stem_a.w + 2 - 3) / 2 + 1;
+        d->pool = d->act(b, ph, pw, 64);
+        d->pool_arg = static_cast<uint8_t*>(d->alloc(static_cast<size_t>(d->pool.numel())));
+        d->gbuf_elems = std::max(d->stem_z.numel(), d->pool.numel());
+        alloc_stage(d, d->backbone, d->pool);
+        d->c4 = d->backbone.back().out;
+        d->fh = d->c4.h;
+        d->fw = d->c4.w;
+        d->n_loc = d->fh * d->fw;
+        d->nA = d->n_loc * d->A;
+        auto setg = [](ConvL& c, const Act& x) { c.g.N = x.n; c.g.H = x.h; c.g.W = x.w; };
+        setg(d->rpn_conv, d->c4);
+        d->rpn_z = d->act(b, d->fh, d->fw, cf.rpn_channels);
+        d->rpn_a = d->act(b, d->fh, d->fw, cf.rpn_channels);
+        setg(d->rpn_cls, d->rpn_a);
+        setg(d->rpn_bbox, d->rpn_a);
+        d->rpn_logits = d->act(b, d->fh, d->fw, d->A_pad);
+        d->rpn_deltas = d->act(b, d->fh, d->fw, 4 * d->A_pad);
+        d->R = b * cf.roi_batch;
+        d->P = cf.pool;
+        d->roi_feat = d->act(d->R, d->P, d->P, 1024);
+        d->gbuf_elems = std::max({d->gbuf_elems, d->c4.numel(), d->rpn_z.numel(), d->roi_feat.numel(),
+                                  d->rpn_deltas.numel()});
+        if (!d->head.empty()) {
+            alloc_stage(d, d->head, d->roi_feat);
+            d->head_out = d->head.back().out;
+        } else {
+            d->head_out = d->roi_feat;
+        }
+        d->pooled = d->act(d->R, 1, 1, d->feat_c);
+        setg(d->fc_cls, d->pooled);
+        setg(d->fc_bbox, d->pooled);
+        d->fc_cls.g.C = d->feat_c; d->fc_cls.g.K = d->ncls_pad; d->fc_cls.g.R = d->fc_cls.g.S = 1;
+        d->fc_cls.g.stride = 1; d->fc_cls.g.pad = 0;
+        d->fc_bbox.g = d->fc_cls.g;
+        d->fc_bbox.g.K = d->nbox_pad;
+        d->cls_logits = d->act(d->R, 1, 1, d->ncls_pad);
+        d->bbox_pred = d->act(d->R, 1, 1, d->nbox_pad);
+        d->gbuf_elems = std::max({d->gbuf_elems, d->head_out.numel(), d->bbox_pred.numel()});
+        for (auto& gb : d->gbuf) gb = d->alloc(static_cast<size_t>(d->gbuf_elems) * d->es);
+        d->d_rpn_logits = d->alloc(static_cast<size_t>(d->rpn_logits.numel()) * d->es);
+        d->d_rpn_deltas = d->alloc(static_cast<size_t>(d->rpn_deltas.numel()) * d->es);
+        d->d_cls = d->alloc(static_cast<size_t>(d->cls_logits.numel()) * d->es);
+        d->d_bbox = d->alloc(static_cast<size_t>(d->bbox_pred.numel()) * d->es);
+
+        // ---- parameter state
+        d->w32 = static_cast<float*>(d->alloc(d->n_w * 4));
+        d->v32 = static_cast<float*>(d->alloc(d->n_w * 4));
+        d->wdev = cf.mode == 1 ? d->alloc(d->n_w * 2) : d->w32;
+        d->g = d->alloc(d->n_w * d->es);
+        CK(cudaMemset(d->g, 0, d->n_w * d->es));
+        d->bn32 = static_cast<float*>(d->alloc(d->n_bn * 4));
+        d->bnv = static_cast<float*>(d->alloc(d->n_bn * 4));
+        d->bng = static_cast<float*>(d->alloc(d->n_bn * 4));
+        d->scale = static_cast<double*>(d->alloc(8));
+        d->good = static_cast<int64_t*>(d->alloc(8));
+        d->flag = static_cast<int*>(d->alloc(4));
+        d->losses = static_cast<double*>(d->alloc(8 * 8));
+        d->scale_used = static_cast<double*>(d->alloc(8));
+        const double s0 = cf.mode == 1 ? cf.scale_init : 1.0;
+        const int64_t zero = 0;
+        CK(cudaMemcpy(d->scale, &s0, 8, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(d->good, &zero, 8, cudaMemcpyHostToDevice));
+        CK(cudaMemset(d->losses, 0, 64));
+
+        // ---- targets / proposals buffers
+        d->anchors = static_cast<float*>(d->alloc(static_cast<size_t>(d->nA) * 16));
+        AnchorCfg ac{};
+        ac.H = d->fh; ac.W = d->fw; ac.stride = 16.0f; ac.ns = cf.n_scales; ac.nr = cf.n_ratios;
+        for (int i = 0; i < cf.n_scales; ++i) ac.scales[i] = cf.scales[i];
+        for (int i = 0; i < cf.n_ratios; ++i) ac.ratios[i] = cf.ratios[i];
+        CK(make_anchors(ac, d->anchors, ctx->stream));
+        d->gt = static_cast<float*>(d->alloc(static_cast<size_t>(b) * cf.max_gt * 16));
+        d->gt_cls = static_cast<int32_t*>(d->alloc(static_cast<size_t>(b) * cf.max_gt * 4));
+        d->gt_count = static_cast<int32_t*>(d->alloc(b * 4));
+        d->keys = static_cast<uint64_t*>(d->alloc(2 * b * 8));
+        d->a_labels = static_cast<int8_t*>(d->alloc(static_cast<size_t>(b) * d->nA));
+        d->a_targets = static_cast<float*>(d->alloc(static_cast<size_t>(b) * d->nA * 16));
+        d->props = static_cast<float*>(d->alloc(static_cast<size_t>(b) * cf.post_nms * 16));
+        d->prop_count = static_cast<int32_t*>(d->alloc(b * 4));
+        d->keep_pos = static_cast<int32_t*>(d->alloc(static_cast<size_t>(b) * cf.post_nms * 4));
+        const int ws_stride = cf.post_nms + cf.max_gt;
+        d->pt_flag = static_cast<int8_t*>(d->alloc(static_cast<size_t>(b) * ws_stride));
+        d->pt_arg = static_cast<int32_t*>(d->alloc(static_cast<size_t>(b) * ws_stride * 4));
+        d->rois = static_cast<float*>(d->alloc(static_cast<size_t>(d->R) * 20));
+        d->roi_labels = static_cast<int32_t*>(d->alloc(static_cast<size_t>(d->R) * 4));
+        d->roi_targets = static_cast<float*>(d->alloc(static_cast<size_t>(d->R) * 16));
+        d->roi_count = static_cast<int32_t*>(d->alloc(b * 4));
+        d->ws_bytes = max_ws(d);
+        d->ws = d->alloc(d->ws_bytes);
+        CK(cudaMallocHost(&d->h_gt, static_cast<size_t>(b) * cf.max_gt * 16));
+        CK(cudaMallocHost(&d->h_cls, static_cast<size_t>(b) * cf.max_gt * 4));
+        CK(cudaMallocHost(&d->h_cnt, b * 4));
+        CK(cudaMallocHost(&d->h_keys, 2 * b * 8));
+        CK(cudaMallocHost(&d->h_losses, 16 * 8));
+
+        // ---- comm: fp16 buckets from the end of the flat gradient (backward order)
+        if (ctx->world > 1) {
+            CK(cudaStreamCreateWithPriority(&d->comm, cudaStreamNonBlocking, -1));
+            CK(cudaEventCreateWithFlags(&d->ev_fork, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&d->ev_join, cudaEventDisableTiming));
+            const int64_t cap = static_cast<int64_t>(cf.bucket_mb * 1024 * 1024 / d->es);
+            int64_t hi = d->n_w;
+            for (int pi = static_cast<int>(d->params.size()) - 1; pi >= 0; --pi) {
+                const Param& p = d->params[pi];
+                if (p.kind > 1) continue;
+                if (hi - p.off >= cap || pi == d->stem.p) {
+                    d->buckets.push_back({p.off, hi});
+                    hi = p.off;
+                }
+            }
+            if (hi > 0) d->buckets.push_back({0, hi});
+            for (size_t i = 0; i < d->buckets.size(); ++i) {
+                cudaEvent_t e;
+                CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                d->bucket_ev.push_back(e);
+            }
+        }
+        init_params(d);
+    } catch (const std::exception& e) {
+        for (void* p : d->allocs) cudaFree(p);
+        delete d;
+        return det_fail(SDB_CUDA, e.what());
+    }
+    *out = d;
+    return SDB_OK;
+}
+
+int sdb_det_destroy(sdb_det* d) {
+    if (!d) return SDB_OK;
+    cudaStreamSynchronize(d->ctx->stream);
+    if (d->gexec) cudaGraphExecDestroy(d->gexec);
+    for (void* p : d->allocs) cudaFree(p);
+    cudaFreeHost(d->h_gt);
+    cudaFreeHost(d->h_cls);
+    cudaFreeHost(d->h_cnt);
+    cudaFreeHost(d->h_keys);
+    cudaFreeHost(d->h_losses);
+    for (auto e : d->bucket_ev) cudaEventDestroy(e);
+    if (d->comm) {
+        cudaEventDestroy(d->ev_fork);
+        cudaEventDestroy(d->ev_join);
+        cudaStreamDestroy(d->comm);
+    }
+    delete d;
+    return SDB_OK;
+}
+
+int sdb_det_num_params(sdb_det* d, int* n_tensors, int64_t* n_w, int64_t* n_bn) {
+    if (n_tensors) *n_tensors = static_cast<int>(d->params.size());
+    if (n_w) *n_w = d->n_w;
+    if (n_bn) *n_bn = d->n_bn;
+    return SDB_OK;
+}
+
+int sdb_det_param_info(sdb_det* d, int idx, char* name, int name_len, int64_t* shape4, int* ndim, int* kind) {
+    if (idx < 0 || idx >= static_cast<int>(d->params.size())) return det_fail(SDB_PARAM, "param index");
+    const Param& p = d->params[idx];
+    if (name && name_len > 0) {
+        std::strncpy(name, p.name.c_str(), name_len - 1);
+        name[name_len - 1] = 0;
+    }
+    if (ndim) *ndim = static_cast<int>(p.ref_shape.size());
+    if (shape4)
+        for (size_t i = 0; i < 4; ++i) shape4[i] = i < p.ref_shape.size() ? p.ref_shape[i] : 1;
+    if (kind) *kind = p.kind;
+    return SDB_OK;
+}
+
+static int param_xfer(sdb_det* d, int idx, float* host, int which /*0 get w, 1 set w, 2 get grad*/) {
+    if (idx < 0 || idx >= static_cast<int>(d->params.size())) return det_fail(SDB_PARAM, "param index");
+    const Param& p = d->params[idx];
+    cudaStream_t st = d->ctx->stream;
+    try {
+        CK(cudaStreamSynchronize(st));
+        if (p.kind >= 2) {
+            float* src = (which == 2 ? d->bng : d->bn32) + p.off;
+            if (which == 1) CK(cudaMemcpy(src, host, p.numel * 4, cudaMemcpyHostToDevice));
+            else CK(cudaMemcpy(host, src, p.numel * 4, cudaMemcpyDeviceToHost));
+            return SDB_OK;
+        }
+        std::vector<float> dev(static_cast<size_t>(p.numel));
+        if (which == 2) {
+            if (d->dt == kF16) {
+                std::vector<__half> h(static_cast<size_t>(p.numel));
+                CK(cudaMemcpy(h.data(), d->gptr(idx), p.numel * 2, cudaMemcpyDeviceToHost));
+                for (size_t i = 0; i < h.size(); ++i) dev[i] = __half2float(h[i]);
+            } else {
+                CK(cudaMemcpy(dev.data(), d->gptr(idx), p.numel * 4, cudaMemcpyDeviceToHost));
+            }
+        } else {
+            CK(cudaMemcpy(dev.data(), d->wptr(idx), p.numel * 4, cudaMemcpyDeviceToHost));
+        }
+        int64_t n = 1;
+        for (int64_t s : p.ref_shape) n *= s;
+        std::vector<float> ref(static_cast<size_t>(n));
+        auto map = [&](auto fn) {
+            if (p.kind == 0) {
+                const int64_t O = p.ref_shape[0], Ci = p.ref_shape[1], kh = p.ref_shape[2], kw = p.ref_shape[3];
+                for (int64_t o = 0; o < O; ++o)
+                    for (int64_t c = 0; c < Ci; ++c)
+                        for (int64_t r = 0; r < kh; ++r)
+                            for (int64_t q = 0; q < kw; ++q)
+                                fn(((o * Ci + c) * kh + r) * kw + q, ((o * p.R + r) * p.S + q) * p.C + c);
+            } else {
+                const int64_t in = p.ref_shape[0], outc = p.ref_shape[1];
+                for (int64_t i = 0; i < in; ++i)
+                    for (int64_t o = 0; o < outc; ++o) fn(i * outc + o, o * p.C + i);
+            }
+        };
+        if (which == 1) {
+            map([&](int64_t ri, int64_t di) { dev[di] = host[ri]; });
+            CK(cudaMemcpy(d->wptr(idx), dev.data(), p.numel * 4, cudaMemcpyHostToDevice));
+            if (d->dt == kF16) CK(cast_f32_f16(d->wptr(idx), static_cast<__half*>(d->wdev_ptr(idx)), p.numel, st));
+            CK(cudaStreamSynchronize(st));
+        } else {
+            map([&](int64_t ri, int64_t di) { host[ri] = dev[di]; });
+        }
+    } catch (const std::exception& e) {
+        return det_fail(SDB_CUDA, e.what());
+    }
+    return SDB_OK;
+}
+
+int sdb_det_get_param(sdb_det* d, int idx, float* host) { return param_xfer(d, idx, host, 0); }
+int sdb_det_set_param(sdb_det* d, int idx, const float* host) { return param_xfer(d, idx, const_cast<float*>(host), 1); }
+int sdb_det_get_grad(sdb_det* d, int idx, float* host) { return param_xfer(d, idx, host, 2); }
+
+static void stage_gt(sdb_det* d, const float* gt_boxes, const int32_t* gt_cls, const int32_t* gt_count,
+                     const int64_t* slots) {
+    const auto& cf = d->cfg;
+    const int b = cf.batch;
+    std::memcpy(d->h_gt, gt_boxes, static_cast<size_t>(b) * cf.max_gt * 16);
+    std::memcpy(d->h_cls, gt_cls, static_cast<size_t>(b) * cf.max_gt * 4);
+    for (int j = 0; j < b; ++j) d->h_cnt[j] = std::min(std::max(gt_count[j], 0), cf.max_gt);
+    for (int j = 0; j < b; ++j) {
+        d->h_keys[j] = mix64(cf.seed ^ 0xA11C0000ull, static_cast<uint64_t>(slots[j]));
+        d->h_keys[b + j] = mix64(cf.seed ^ 0x5A3B0000ull, static_cast<uint64_t>(slots[j]));
+    }
+    cudaStream_t st = d->ctx->stream;
+    CK(cudaMemcpyAsync(d->gt, d->h_gt, static_cast<size_t>(b) * cf.max_gt * 16, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d->gt_cls, d->h_cls, static_cast<size_t>(b) * cf.max_gt * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d->gt_count, d->h_cnt, b * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d->keys, d->h_keys, 2 * b * 8, cudaMemcpyHostToDevice, st));
+}
+
+int sdb_det_set_batch(sdb_det* d, const void* images, int on_host, const float* gt_boxes, const int32_t* gt_cls,
+                      const int32_t* gt_count, const int64_t* slots) {
+    try {
+        cudaStream_t st = d->ctx->stream;
+        if (images)
+            CK(cudaMemcpyAsync(d->img.p, images, d->img.numel() * d->es,
+                               on_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st));
+        stage_gt(d, gt_boxes, gt_cls, gt_count, slots);
+        // the pinned staging buffers are reused next call: wait for the copies
+        CK(cudaStreamSynchronize(st));
+    } catch (const std::exception& e) {
+        return det_fail(SDB_CUDA, e.what());
+    }
+    return SDB_OK;
+}
+
+int sdb_det_synth_images(sdb_det* d, const int64_t* slots) {
+    try {
+        int64_t* ds = static_cast<int64_t*>(d->ws);
+        CK(cudaMemcpy(ds, slots, d->cfg.batch * 8, cudaMemcpyHostToDevice));
+        CK(synth_images(d->dt, d->img.p, d->cfg.batch, d->cfg.img_h, d->cfg.img_w, 8, d->cfg.seed, ds, 0,
+                        d->ctx->stream));
+        CK(cudaStreamSynchronize(d->ctx->stream));
+    } catch (const std::exception& e) {
+        return det_fail(SDB_CUDA, e.what());
+    }
+    return SDB_OK;
+}
+
+int sdb_det_step(sdb_det* d) {
+    try {
+        cudaStream_t st = d->ctx->stream;
+        if (!d->use_graph || d->steps_done == 0) {
+            run_step(d);
+        } else {
+            if (!d->gexec) {
+                cudaGraph_t graph;
+                CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+                run_step(d);
+                CK(cudaStreamEndCapture(st, &graph));
+                size_t n = 0;
+                CK(cudaGraphGetNodes(graph, nullptr, &n));
+                std::vector<cudaGraphNode_t> nodes(n);
+                CK(cudaGraphGetNodes(graph, nodes.data(), &n));
+                int64_t k = 0;
+                for (auto nd : nodes) {
+                    cudaGraphNodeType t;
+                    CK(cudaGraphNodeGetType(nd, &t));
+                    k += t == cudaGraphNodeTypeKernel;
+                }
+                d->launches = k;
+                CK(cudaGraphInstantiate(&d->gexec, graph, 0));
+                CK(cudaGraphDestroy(graph));
+            }
+            CK(cudaGraphLaunch(d->gexec, st));
+        }
+        ++d->steps_done;
+    } catch (const std::exception& e) {
+        return det_fail(SDB_CUDA, e.what());
+    }
+    return SDB_OK;
+}
+
+int sdb_det_read_losses(sdb_det* d, double* losses5, double* scale_used, int* overflow) {
+    try {
+        cudaStream_t st = d->ctx->stream;
+        CK(cudaMemcpyAsync(d->h_losses, d->losses, 4 * 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(d->h_losses + 8, d->scale_used, 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(d->h_losses + 9, d->flag, 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        const double K = d->ctx->world;
+        double tot = 0;
+        for (int i = 0; i < 4; ++i) {
+            if (losses5) losses5[i] = d->h_losses[i] / K;
+            tot += d->h_losses[i];
+        }
+        if (losses5) losses5[4] = tot / K;
+        if (scale_used) *scale_used = d->h_losses[8];
+        if (overflow) *overflow = *reinterpret_cast<int*>(d->h_losses + 9);
+    } catch (const std::exception& e) {
+        return det_fail(SDB_CUDA, e.what());
+    }
+    return SDB_OK;
+}
+
+int sdb_det_train_step_host(sdb_det* d, const void* images_host, const float* gt_boxes, const int32_t* gt_cls,
+                            const int32_t* gt_count, const int64_t* slots, double* losses5) {
+    try {
+        cudaStream_t st = d->ctx->stream;
+        CK(cudaMemcpyAsync(d->img.p, images_host, d->img.numel() * d->es, cudaMemcpyHostToDevice, st));
+        stage_gt(d, gt_boxes, gt_cls, gt_count, slots);
+    } catch (const std::exception& e) {
+        return det_fail(SDB_CUDA, e.what());
+    }
+    if (int rc = sdb_det_step(d)) return rc;
+    return sdb_det_read_losses(d, losses5, nullptr, nullptr);
+}
+
+int sdb_det_export(sdb_det* d, int what, void* host, int64_t cap, int64_t* bytes) {
+    const auto& cf = d->cfg;
+    const void* src = nullptr;
+    int64_t n = 0;
+    double tmp_state[2];
+    switch (what) {
+        case 0: src = d->a_labels; n = static_cast<int64_t>(cf.batch) * d->nA; break;
+        case 1: src = d->a_targets; n = static_cast<int64_t>(cf.batch) * d->nA * 16; break;
+        case 2: src = d->props; n = static_cast<int64_t>(cf.batch) * cf.post_nms * 16; break;
+        case 3: src = d->prop_count; n = cf.batch * 4; break;
+        case 4: src = d->rois; n = static_cast<int64_t>(d->R) * 20; break;
+        case 5: src = d->roi_labels; n = static_cast<int64_t>(d->R) * 4; break;
+        case 6: src = d->roi_targets; n = static_cast<int64_t>(d->R) * 16; break;
+        case 7: src = d->rpn_logits.p; n = d->rpn_logits.numel() * d->es; break;
+        case 8: src = d->rpn_deltas.p; n = d->rpn_deltas.numel() * d->es; break;
+        case 9: src = d->anchors; n = static_cast<int64_t>(d->nA) * 16; break;
+        case 10: src = d->c4.p; n = d->c4.numel() * d->es; break;
+        case 11: src = d->img.p; n = d->img.numel() * d->es; break;
+        case 12: {
+            cudaStreamSynchronize(d->ctx->stream);
+            cudaMemcpy(&tmp_state[0], d->scale, 8, cudaMemcpyDeviceToHost);
+            cudaMemcpy(&tmp_state[1], d->good, 8, cudaMemcpyDeviceToHost);
+            if (bytes) *bytes = 16;
+            if (host && cap >= 16) std::memcpy(host, tmp_state, 16);
+            return SDB_OK;
+        }
+        default: return det_fail(SDB_PARAM, "unknown export id");
+    }
+    if (bytes) *bytes = n;
+    if (!host) return SDB_OK;
+    if (cap < n) return det_fail(SDB_PARAM, "export buffer too small");
+    if (cudaStreamSynchronize(d->ctx->stream) != cudaSuccess || cudaMemcpy(host, src, n, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return det_fail(SDB_CUDA, "export copy failed");
+    return SDB_OK;
+}
+
+int sdb_det_dims(sdb_det* d, int* fh, int* fw, int* A, int* A_pad) {
+    if (fh) *fh = d->fh;
+    if (fw) *fw = d->fw;
+    if (A) *A = d->A;
+    if (A_pad) *A_pad = d->A_pad;
+    return SDB_OK;
+}
+
+int sdb_det_kernel_launches(sdb_det* d, int64_t* n) {
+    *n = d->launches;
+    return SDB_OK;
+}
+
+}  // extern "C"

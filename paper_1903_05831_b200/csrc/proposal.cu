@@ -1,0 +1,732 @@
+// proposal.cu -- RPN proposal layer and target assignment (north-star item 3).
+//
+// The reference has no proposal layer; its only box semantics are
+// iou()/nms_greedy() (src/postproc.cpp:20-63): continuous corners (no +1),
+// FP64 IoU, 0 when the union is 0, (score desc, index asc) order, suppression
+// iff IoU > t.  The restated CPU oracle (oracle/restate.cpp) defines the rest;
+// every discrete output here (top-k order, NMS keep list, anchor labels,
+// sampled RoIs) is BIT-EXACT against it given identical fp32 inputs.  This TU
+// is compiled with -fmad=false so no float/double FMA contraction occurs.
+//
+//   topk      one CTA per image: 64-bit radix select over the composite key
+//             (~orderable(score) << 32 | index) -> bitonic sort in smem
+//   decode    anchors + deltas -> clipped boxes, portable exp (bit-identical to
+//             orc_expf)
+//   nms mask  64x64 IoU tiles -> upper-triangular bitmask (fp64, -fmad=false)
+//   nms scan  one CTA per image: chunked keep scan, diagonal words in smem,
+//             parallel OR of kept rows, early exit at post_k
+//   targets   fp64 IoU vs ground truth, Detectron-style labels, counter-RNG
+//             (mix64, src/dataset.cpp:11-17) priority sampling via radix select
+#include <algorithm>
+#include <cfloat>
+
+#include "common.cuh"
+#include "detect.h"
+#include "sdb_internal.h"
+
+namespace sdb {
+
+namespace {
+
+SDB_DEV uint64_t mix64(uint64_t a, uint64_t b) {
+    uint64_t z = a ^ (b + 0x9e3779b97f4a7c15ull);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+
+// bit-identical to orc_expf (oracle/restate.cpp)
+SDB_DEV float portable_expf(float xf) {
+    const double x = xf;
+    if (!(x == x)) return xf;
+    if (x > 88.8) return __int_as_float(0x7f800000);
+    if (x < -104.0) return 0.0f;
+    const double kd = floor(__dadd_rn(__dmul_rn(x, 1.4426950408889634), 0.5));
+    const double r = __dsub_rn(__dsub_rn(x, __dmul_rn(kd, 0.693147180369123816490)), __dmul_rn(kd, 1.90821492927058770002e-10));
+    double p = 1.0 / 39916800.0;
+    p = __dadd_rn(__dmul_rn(p, r), 1.0 / 3628800.0);
+    p = __dadd_rn(__dmul_rn(p, r), 1.0 / 362880.0);
+    p = __dadd_rn(__dmul_rn(p, r), 1.0 / 40320.0);
+    p = __dadd_rn(__dmul_rn(p, r), 1.0 / 5040.0);
+    p = __dadd_rn(__dmul_rn(p, r), 1.0 / 720.0);
+    p = __dadd_rn(__dmul_rn(p, r), 1.0 / 120.0);
+    p = __dadd_rn(__dmul_rn(p, r), 1.0 / 24.0);
+    p = __dadd_rn(__dmul_rn(p, r), 1.0 / 6.0);
+    p = __dadd_rn(__dmul_rn(p, r), 0.5);
+    p = __dadd_rn(__dmul_rn(p, r), 1.0);
+    p = __dadd_rn(__dmul_rn(p, r), 1.0);
+    const long long k = static_cast<long long>(kd);
+    const double two_k = __longlong_as_double((k + 1023) << 52);
+    return __double2float_rn(__dmul_rn(p, two_k));
+}
+
+// src/postproc.cpp:20-26
+SDB_DEV double iou_d(double ax1, double ay1, double ax2, double ay2, double bx1, double by1, double bx2, double by2) {
+    const double ix = fmax(0.0, __dsub_rn(fmin(ax2, bx2), fmax(ax1, bx1)));
+    const double iy = fmax(0.0, __dsub_rn(fmin(ay2, by2), fmax(ay1, by1)));
+    const double inter = __dmul_rn(ix, iy);
+    const double aa = __dmul_rn(__dsub_rn(ax2, ax1), __dsub_rn(ay2, ay1));
+    const double ab = __dmul_rn(__dsub_rn(bx2, bx1), __dsub_rn(by2, by1));
+    const double uni = __dsub_rn(__dadd_rn(aa, ab), inter);
+    return uni > 0.0 ? __ddiv_rn(inter, uni) : 0.0;
+}
+SDB_DEV double iou_f4(const float* a, const float* b) {
+    return iou_d(a[0], a[1], a[2], a[3], b[0], b[1], b[2], b[3]);
+}
+
+SDB_DEV uint32_t desc_key(float s) {
+    // ascending order of the returned key == (score desc); NaN ranks last
+    const uint32_t u = __float_as_uint(s);
+    if ((u & 0x7fffffffu) > 0x7f800000u) return 0xffffffffu;
+    const uint32_t ord = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+    return ~ord;
+}
+
+// ---------------------------------------------------------------- block utils
+template <int NT>
+SDB_DEV int block_sum_int(int v, int* sh) {
+    v += __shfl_xor_sync(0xffffffffu, v, 16);
+    v += __shfl_xor_sync(0xffffffffu, v, 8);
+    v += __shfl_xor_sync(0xffffffffu, v, 4);
+    v += __shfl_xor_sync(0xffffffffu, v, 2);
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+    __syncthreads();
+    int t = 0;
+    for (int w = 0; w < NT / 32; ++w) t += sh[w];
+    __syncthreads();
+    return t;
+}
+
+// exclusive block scan of an int flag in thread order; returns prefix, total in *tot
+template <int NT>
+SDB_DEV int block_excl_scan(int v, int* sh, int* tot) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    __syncthreads();
+    if (lane == 31) sh[wid] = x;
+    __syncthreads();
+    int base = 0, total = 0;
+    for (int w = 0; w < NT / 32; ++w) {
+        if (w < wid) base += sh[w];
+        total += sh[w];
+    }
+    __syncthreads();
+    *tot = total;
+    return base + x - v;
+}
+
+// Radix select (8 x 8-bit passes) of the k-th smallest 64-bit key among the
+// flagged elements [0, n).  KeyFn(i, &flag) -> key.  Returns the key T such
+// that count(key < T) < k <= count(key <= T); also *n_lt = count(key < T).
+// If the flagged count <= k, returns UINT64_MAX and *n_lt = flagged count.
+template <int NT, class KeyFn>
+SDB_DEV uint64_t block_radix_select(int n, int k, KeyFn keyfn, int* hist /*256*/, int* sh, int* n_lt_out) {
+    int cnt = 0;
+    for (int i = threadIdx.x; i < n; i += NT) {
+        bool f;
+        keyfn(i, f);
+        cnt += f;
+    }
+    const int total = block_sum_int<NT>(cnt, sh);
+    if (total <= k || k <= 0) {
+        *n_lt_out = k <= 0 ? 0 : total;
+        return k <= 0 ? 0ull : ~0ull;
+    }
+    uint64_t prefix = 0, mask = 0;
+    int kk = k;  // rank (1-based) within the current prefix class
+    int below = 0;
+    for (int pass = 0; pass < 8; ++pass) {
+        const int shift = 56 - 8 * pass;
+        for (int b = threadIdx.x; b < 256; b += NT) hist[b] = 0;
+        __syncthreads();
+        for (int i = threadIdx.x; i < n; i += NT) {
+            bool f;
+            const uint64_t key = keyfn(i, f);
+            if (f && (key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255], 1);
+        }
+        __syncthreads();
+        // find the digit where the cumulative count reaches kk (single thread; 256 bins)
+        if (threadIdx.x == 0) {
+            int acc = 0, d = 0;
+            for (d = 0; d < 256; ++d) {
+                if (acc + hist[d] >= kk) break;
+                acc += hist[d];
+            }
+            sh[0] = d;
+            sh[1] = acc;
+        }
+        __syncthreads();
+        const int d = sh[0], acc = sh[1];
+        __syncthreads();
+        kk -= acc;
+        below += acc;
+        prefix |= static_cast<uint64_t>(d) << shift;
+        mask |= 0xffull << shift;
+    }
+    *n_lt_out = below;
+    return prefix;
+}
+
+// ---------------------------------------------------------------- anchors
+__global__ void anchors_kernel(AnchorCfg a, float* __restrict__ out) {
+    const int A = a.ns * a.nr;
+    const int64_t total = static_cast<int64_t>(a.H) * a.W * A;
+    for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int j = static_cast<int>(idx % a.ns);
+        const int i = static_cast<int>((idx / a.ns) % a.nr);
+        const int64_t loc = idx / A;
+        const int x = static_cast<int>(loc % a.W), y = static_cast<int>(loc / a.W);
+        const float cx = __fmul_rn(__fadd_rn(static_cast<float>(x), 0.5f), a.stride);
+        const float cy = __fmul_rn(__fadd_rn(static_cast<float>(y), 0.5f), a.stride);
+        const double sr = __dsqrt_rn(static_cast<double>(a.ratios[i]));
+        const float w = __double2float_rn(__ddiv_rn(static_cast<double>(a.scales[j]), sr));
+        const float h = __double2float_rn(__dmul_rn(static_cast<double>(a.scales[j]), sr));
+        out[idx * 4 + 0] = __fsub_rn(cx, __fmul_rn(0.5f, w));
+        out[idx * 4 + 1] = __fsub_rn(cy, __fmul_rn(0.5f, h));
+        out[idx * 4 + 2] = __fadd_rn(cx, __fmul_rn(0.5f, w));
+        out[idx * 4 + 3] = __fadd_rn(cy, __fmul_rn(0.5f, h));
+    }
+}
+
+// ---------------------------------------------------------------- top-k + decode
+constexpr int kTopkThreads = 1024;
+
+// logits: [img][loc][A_pad] (fp16 or fp32), valid anchors a < A; anchor index = loc*A + a
+struct TopkArgs {
+    const void* logits;
+    int dtype;
+    const void* deltas;  // [img][loc][4*A_pad]
+    const float* anchors;
+    int n_loc, A, A_pad;
+    int k;       // min(pre_k, n_anchors)
+    int k_pow2;  // next power of two >= k
+    float img_h, img_w, clip_dw;
+    float* boxes;       // [img][k][4]
+    int32_t* order;     // [img][k] anchor indices
+    float* scores;      // [img][k]
+};
+
+SDB_DEV float load_val(const void* p, int dtype, int64_t i) {
+    return dtype == kF16 ? __half2float(static_cast<const __half*>(p)[i]) : static_cast<const float*>(p)[i];
+}
+
+__global__ void __launch_bounds__(kTopkThreads) topk_decode_kernel(TopkArgs a) {
+    extern __shared__ uint64_t keys[];  // k_pow2
+    __shared__ int hist[256];
+    __shared__ int sh[64];
+    __shared__ int n_sel;
+    const int img = blockIdx.x;
+    const int n = a.n_loc * a.A;
+    auto keyfn = [&](int i, bool& f) -> uint64_t {
+        f = true;
+        const int loc = i / a.A, an = i - loc * a.A;
+        const float s = load_val(a.logits, a.dtype, (static_cast<int64_t>(img) * a.n_loc + loc) * a.A_pad + an);
+        return (static_cast<uint64_t>(desc_key(s)) << 32) | static_cast<uint32_t>(i);
+    };
+    int n_lt;
+    const uint64_t T = block_radix_select<kTopkThreads>(n, a.k, keyfn, hist, sh, &n_lt);
+    if (threadIdx.x == 0) n_sel = 0;
+    for (int i = threadIdx.x; i < a.k_pow2; i += kTopkThreads) keys[i] = ~0ull;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += kTopkThreads) {
+        bool f;
+        const uint64_t key = keyfn(i, f);
+        if (key <= T) {
+            const int slot = atomicAdd(&n_sel, 1);
+            if (slot < a.k_pow2) keys[slot] = key;
+        }
+    }
+    __syncthreads();
+    // bitonic sort ascending (keys are unique)
+    for (int size = 2; size <= a.k_pow2; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int t = threadIdx.x; t < a.k_pow2 / 2; t += kTopkThreads) {
+                const int lo = 2 * t - (t & (stride - 1));
+                const int hi = lo + stride;
+                const bool up = (lo & size) == 0;
+                const uint64_t x = keys[lo], y = keys[hi];
+                if ((x > y) == up) {
+                    keys[lo] = y;
+                    keys[hi] = x;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    // decode the sorted candidates (orc_decode with unit weights)
+    for (int r = threadIdx.x; r < a.k; r += kTopkThreads) {
+        const int i = static_cast<int>(keys[r] & 0xffffffffu);
+        const int loc = i / a.A, an = i - loc * a.A;
+        const float* an4 = a.anchors + static_cast<int64_t>(i) * 4;
+        const int64_t dbase = (static_cast<int64_t>(img) * a.n_loc + loc) * 4 * a.A_pad + 4 * an;
+        const float dx = load_val(a.deltas, a.dtype, dbase + 0), dy = load_val(a.deltas, a.dtype, dbase + 1);
+        const float dw = fminf(load_val(a.deltas, a.dtype, dbase + 2), a.clip_dw);
+        const float dh = fminf(load_val(a.deltas, a.dtype, dbase + 3), a.clip_dw);
+        const float aw = __fsub_rn(an4[2], an4[0]), ah = __fsub_rn(an4[3], an4[1]);
+        const float acx = __fadd_rn(an4[0], __fmul_rn(0.5f, aw)), acy = __fadd_rn(an4[1], __fmul_rn(0.5f, ah));
+        const float pcx = __fadd_rn(__fmul_rn(dx, aw), acx), pcy = __fadd_rn(__fmul_rn(dy, ah), acy);
+        const float pw = __fmul_rn(portable_expf(dw), aw), ph = __fmul_rn(portable_expf(dh), ah);
+        float* o = a.boxes + (static_cast<int64_t>(img) * a.k + r) * 4;
+        o[0] = fminf(fmaxf(__fsub_rn(pcx, __fmul_rn(0.5f, pw)), 0.0f), a.img_w);
+        o[1] = fminf(fmaxf(__fsub_rn(pcy, __fmul_rn(0.5f, ph)), 0.0f), a.img_h);
+        o[2] = fminf(fmaxf(__fadd_rn(pcx, __fmul_rn(0.5f, pw)), 0.0f), a.img_w);
+        o[3] = fminf(fmaxf(__fadd_rn(pcy, __fmul_rn(0.5f, ph)), 0.0f), a.img_h);
+        a.order[static_cast<int64_t>(img) * a.k + r] = i;
+        a.scores[static_cast<int64_t>(img) * a.k + r] =
+            load_val(a.logits, a.dtype, (static_cast<int64_t>(img) * a.n_loc + loc) * a.A_pad + an);
+    }
+}
+
+// ---------------------------------------------------------------- NMS
+__global__ void __launch_bounds__(64) nms_mask_kernel(const float* __restrict__ boxes, int k, int nwords, double thr,
+                                                      uint64_t* __restrict__ mask) {
+    const int img = blockIdx.z, rb = blockIdx.y, cb = blockIdx.x;
+    if (cb < rb) return;
+    __shared__ float cbx[64][4];
+    const float* B = boxes + static_cast<int64_t>(img) * k * 4;
+    const int j0 = cb * 64;
+    const int t = threadIdx.x;
+    if (j0 + t < k) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) cbx[t][c] = B[(j0 + t) * 4 + c];
+    }
+    __syncthreads();
+    const int i = rb * 64 + t;
+    if (i >= k) return;
+    const float* bi = B + static_cast<int64_t>(i) * 4;
+    const double x1 = bi[0], y1 = bi[1], x2 = bi[2], y2 = bi[3];
+    uint64_t bits = 0;
+    const int jn = min(64, k - j0);
+    for (int jj = 0; jj < jn; ++jj) {
+        const int j = j0 + jj;
+        if (j <= i) continue;
+        // cheap exact reject: no overlap -> IoU is 0, never > thr (thr >= 0)
+        if (cbx[jj][0] >= bi[2] || cbx[jj][2] <= bi[0] || cbx[jj][1] >= bi[3] || cbx[jj][3] <= bi[1]) continue;
+        if (iou_d(x1, y1, x2, y2, cbx[jj][0], cbx[jj][1], cbx[jj][2], cbx[jj][3]) > thr) bits |= 1ull << jj;
+    }
+    mask[(static_cast<int64_t>(img) * k + i) * nwords + cb] = bits;
+}
+
+constexpr int kScanThreads = 256;
+
+__global__ void __launch_bounds__(kScanThreads) nms_scan_kernel(const float* __restrict__ boxes,
+                                                                const uint64_t* __restrict__ mask,
+                                                                const float* __restrict__ scores, int k, int nwords,
+                                                                int post_k, float* __restrict__ rois,
+                                                                float* __restrict__ roi_scores,
+                                                                int32_t* __restrict__ keep_pos,
+                                                                int32_t* __restrict__ count) {
+    extern __shared__ uint64_t removed[];  // nwords
+    __shared__ uint64_t diag[64];
+    __shared__ uint64_t chunk_keep;
+    __shared__ int kept, done;
+    const int img = blockIdx.x;
+    const uint64_t* M = mask + static_cast<int64_t>(img) * k * nwords;
+    for (int w = threadIdx.x; w < nwords; w += kScanThreads) removed[w] = 0;
+    if (threadIdx.x == 0) {
+        kept = 0;
+        done = 0;
+    }
+    __syncthreads();
+    for (int c = 0; c < nwords && !done; ++c) {
+        if (threadIdx.x < 64) {
+            const int i = c * 64 + threadIdx.x;
+            diag[threadIdx.x] = i < k ? M[static_cast<int64_t>(i) * nwords + c] : 0ull;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint64_t w = removed[c], km = 0;
+            int kc = kept;
+            for (int b = 0; b < 64; ++b) {
+                const int i = c * 64 + b;
+                if (i >= k) break;
+                if ((w >> b) & 1ull) continue;
+                if (kc >= post_k) {
+                    done = 1;
+                    break;
+                }
+                km |= 1ull << b;
+                keep_pos[static_cast<int64_t>(img) * post_k + kc] = i;
+                ++kc;
+                w |= diag[b];
+            }
+            if (kc >= post_k) done = 1;
+            removed[c] = w;
+            chunk_keep = km;
+            kept = kc;
+        }
+        __syncthreads();
+        const uint64_t km = chunk_keep;
+        if (km) {
+            for (int w = c + 1 + threadIdx.x; w < nwords; w += kScanThreads) {
+                uint64_t acc = 0;
+                uint64_t bits = km;
+                while (bits) {
+                    const int b = __ffsll(static_cast<long long>(bits)) - 1;
+                    bits &= bits - 1;
+                    acc |= M[static_cast<int64_t>(c * 64 + b) * nwords + w];
+                }
+                removed[w] |= acc;
+            }
+        }
+        __syncthreads();
+    }
+    const int nk = kept;
+    for (int j = threadIdx.x; j < post_k; j += kScanThreads) {
+        float* o = rois + (static_cast<int64_t>(img) * post_k + j) * 4;
+        if (j < nk) {
+            const int i = keep_pos[static_cast<int64_t>(img) * post_k + j];
+            const float* b = boxes + (static_cast<int64_t>(img) * k + i) * 4;
+            o[0] = b[0]; o[1] = b[1]; o[2] = b[2]; o[3] = b[3];
+            if (roi_scores) roi_scores[static_cast<int64_t>(img) * post_k + j] = scores[static_cast<int64_t>(img) * k + i];
+        } else {
+            o[0] = o[1] = o[2] = o[3] = 0.0f;
+        }
+    }
+    if (threadIdx.x == 0) count[img] = nk;
+}
+
+// ---------------------------------------------------------------- anchor targets
+// per anchor: inside flag, max IoU, argmax; per gt: max IoU over inside anchors
+__global__ void anchor_iou_kernel(const float* __restrict__ anchors, int nA, const float* __restrict__ gt, int gt_stride,
+                                  const int32_t* __restrict__ gt_count, float img_h, float img_w,
+                                  double* __restrict__ max_iou, int32_t* __restrict__ argmax,
+                                  unsigned long long* __restrict__ gt_max) {
+    const int img = blockIdx.y;
+    const int G = gt_count[img];
+    const float* g = gt + static_cast<int64_t>(img) * gt_stride * 4;
+    for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < nA; a += gridDim.x * blockDim.x) {
+        const float* b = anchors + static_cast<int64_t>(a) * 4;
+        const bool inside = b[0] >= 0.0f && b[1] >= 0.0f && b[2] <= img_w && b[3] <= img_h;
+        double best = -1.0;
+        int bi = 0;
+        if (inside) {
+            best = 0.0;
+            for (int j = 0; j < G; ++j) {
+                const double v = iou_f4(b, g + j * 4);
+                if (v > best) {
+                    best = v;
+                    bi = j;
+                }
+                if (v > 0.0) atomicMax(&gt_max[static_cast<int64_t>(img) * gt_stride + j],
+                                       static_cast<unsigned long long>(__double_as_longlong(v)));
+            }
+        }
+        max_iou[static_cast<int64_t>(img) * nA + a] = best;
+        argmax[static_cast<int64_t>(img) * nA + a] = bi;
+    }
+}
+
+__global__ void anchor_label_kernel(const float* __restrict__ anchors, int nA, const float* __restrict__ gt,
+                                    int gt_stride, const int32_t* __restrict__ gt_count,
+                                    const double* __restrict__ max_iou, const unsigned long long* __restrict__ gt_max,
+                                    double fg_thr, double bg_thr, int8_t* __restrict__ labels) {
+    const int img = blockIdx.y;
+    const int G = gt_count[img];
+    const float* g = gt + static_cast<int64_t>(img) * gt_stride * 4;
+    for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < nA; a += gridDim.x * blockDim.x) {
+        const double m = max_iou[static_cast<int64_t>(img) * nA + a];
+        int8_t lab = -1;
+        if (m >= 0.0) {  // inside
+            if (m < bg_thr) lab = 0;
+            const float* b = anchors + static_cast<int64_t>(a) * 4;
+            for (int j = 0; j < G; ++j) {
+                const double gm = __longlong_as_double(static_cast<long long>(gt_max[static_cast<int64_t>(img) * gt_stride + j]));
+                if (gm > 0.0 && iou_f4(b, g + j * 4) == gm) {
+                    lab = 1;
+                    break;
+                }
+            }
+            if (m >= fg_thr) lab = 1;
+        }
+        labels[static_cast<int64_t>(img) * nA + a] = lab;
+    }
+}
+
+constexpr int kSampleThreads = 1024;
+
+// one CTA per image: keep <= cap fg by smallest mix64(key, a), then bg to fill `batch`
+__global__ void __launch_bounds__(kSampleThreads) anchor_sample_kernel(int nA, const uint64_t* __restrict__ keys,
+                                                                       int batch, int fg_cap,
+                                                                       int8_t* __restrict__ labels) {
+    __shared__ int hist[256];
+    __shared__ int sh[64];
+    __shared__ int tie_list[64];
+    const int img = blockIdx.x;
+    int8_t* L = labels + static_cast<int64_t>(img) * nA;
+    const uint64_t kfg = keys[img];
+    const uint64_t kbg = mix64(kfg, 0xb9ull);
+    int n_fg_kept = 0;
+    for (int pass = 0; pass < 2; ++pass) {
+        const int want = pass == 0 ? 1 : 0;
+        const uint64_t key = pass == 0 ? kfg : kbg;
+        const int k = pass == 0 ? fg_cap : batch - n_fg_kept;
+        auto keyfn = [&](int i, bool& f) -> uint64_t {
+            f = L[i] == want;
+            return f ? mix64(key, static_cast<uint64_t>(i)) : 0ull;
+        };
+        int n_lt;
+        const uint64_t T = block_radix_select<kSampleThreads>(nA, k, keyfn, hist, sh, &n_lt);
+        int kept_here;
+        if (T == ~0ull) {
+            kept_here = n_lt;  // all flagged kept
+        } else {
+            // ties at T: keep the lowest indices (rare); single-thread scan
+            const int need = k - n_lt;
+            if (threadIdx.x == 0) {
+                int got = 0;
+                for (int i = 0; i < nA && got < need && got < 64; ++i)
+                    if (L[i] == want && mix64(key, static_cast<uint64_t>(i)) == T) tie_list[got++] = i;
+                sh[32] = got;
+            }
+            __syncthreads();
+            const int ntie = sh[32];
+            __syncthreads();
+            for (int i = threadIdx.x; i < nA; i += kSampleThreads) {
+                if (L[i] != want) continue;
+                const uint64_t pk = mix64(key, static_cast<uint64_t>(i));
+                bool keep = pk < T;
+                if (pk == T)
+                    for (int t = 0; t < ntie; ++t) keep |= tie_list[t] == i;
+                if (!keep) L[i] = -1;
+            }
+            kept_here = k;
+        }
+        __syncthreads();
+        if (pass == 0) n_fg_kept = kept_here;
+    }
+}
+
+__global__ void anchor_bbox_target_kernel(const float* __restrict__ anchors, int nA, const float* __restrict__ gt,
+                                          int gt_stride, const int32_t* __restrict__ argmax,
+                                          const int8_t* __restrict__ labels, float* __restrict__ targets) {
+    const int img = blockIdx.y;
+    const float* g = gt + static_cast<int64_t>(img) * gt_stride * 4;
+    for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < nA; a += gridDim.x * blockDim.x) {
+        float* t = targets + (static_cast<int64_t>(img) * nA + a) * 4;
+        if (labels[static_cast<int64_t>(img) * nA + a] != 1) {
+            t[0] = t[1] = t[2] = t[3] = 0.0f;
+            continue;
+        }
+        encode_box(anchors + static_cast<int64_t>(a) * 4, g + argmax[static_cast<int64_t>(img) * nA + a] * 4, 1.f, 1.f,
+                   1.f, 1.f, t);
+    }
+}
+
+// ---------------------------------------------------------------- proposal targets
+constexpr int kPtThreads = 1024;
+
+__global__ void __launch_bounds__(kPtThreads) proposal_target_kernel(ProposalTargetArgs a) {
+    __shared__ int hist[256];
+    __shared__ int sh[64];
+    __shared__ int tie_list[64];
+    const int img = blockIdx.x;
+    const int R = a.prop_count[img];
+    const int G = a.gt_count[img];
+    const int T = R + G;
+    const float* props = a.proposals + static_cast<int64_t>(img) * a.prop_stride * 4;
+    const float* g = a.gt + static_cast<int64_t>(img) * a.gt_stride * 4;
+    const int32_t* gcls = a.gt_cls + static_cast<int64_t>(img) * a.gt_stride;
+    int8_t* cls = a.work_flag + static_cast<int64_t>(img) * a.work_stride;    // 1 fg, 0 bg, -1 neither
+    int32_t* arg = a.work_arg + static_cast<int64_t>(img) * a.work_stride;
+    for (int i = threadIdx.x; i < T; i += kPtThreads) {
+        const float* b = i < R ? props + i * 4 : g + (i - R) * 4;
+        double best = 0.0;
+        int bi = 0;
+        for (int j = 0; j < G; ++j) {
+            const double v = iou_f4(b, g + j * 4);
+            if (v > best) {
+                best = v;
+                bi = j;
+            }
+        }
+        int8_t f = -1;
+        if (G > 0 && best >= a.fg_thr) f = 1;
+        else if (best < a.bg_hi && best >= a.bg_lo) f = 0;
+        cls[i] = f;
+        arg[i] = bi;
+    }
+    __syncthreads();
+    const uint64_t kfg = a.keys[img], kbg = mix64(a.keys[img], 0xb9ull);
+    int n_fg = 0;
+    for (int pass = 0; pass < 2; ++pass) {
+        const int want = pass == 0 ? 1 : 0;
+        const uint64_t key = pass == 0 ? kfg : kbg;
+        const int k = pass == 0 ? a.fg_cap : a.batch - n_fg;
+        auto keyfn = [&](int i, bool& f) -> uint64_t {
+            f = cls[i] == want;
+            return f ? mix64(key, static_cast<uint64_t>(i)) : 0ull;
+        };
+        int n_lt;
+        const uint64_t Tk = block_radix_select<kPtThreads>(T, k, keyfn, hist, sh, &n_lt);
+        int kept_here;
+        if (Tk == ~0ull) {
+            kept_here = n_lt;
+            // mark kept as 2 (fg) / 3 (bg) for compaction
+            for (int i = threadIdx.x; i < T; i += kPtThreads)
+                if (cls[i] == want) cls[i] = static_cast<int8_t>(want + 2);
+        } else {
+            const int need = k - n_lt;
+            if (threadIdx.x == 0) {
+                int got = 0;
+                for (int i = 0; i < T && got < need && got < 64; ++i)
+                    if (cls[i] == want && mix64(key, static_cast<uint64_t>(i)) == Tk) tie_list[got++] = i;
+                sh[32] = got;
+            }
+            __syncthreads();
+            const int ntie = sh[32];
+            __syncthreads();
+            for (int i = threadIdx.x; i < T; i += kPtThreads) {
+                if (cls[i] != want) continue;
+                const uint64_t pk = mix64(key, static_cast<uint64_t>(i));
+                bool keep = pk < Tk;
+                if (pk == Tk)
+                    for (int t = 0; t < ntie; ++t) keep |= tie_list[t] == i;
+                if (keep) cls[i] = static_cast<int8_t>(want + 2);
+            }
+            kept_here = k;
+        }
+        __syncthreads();
+        if (pass == 0) n_fg = kept_here;
+    }
+    // compaction: kept fg (value 3) in index order, then kept bg (value 2) in index order
+    const int chunks = (T + kPtThreads - 1) / kPtThreads;
+    int base_fg = 0, base_bg = n_fg;
+    for (int ch = 0; ch < chunks; ++ch) {
+        const int i = ch * kPtThreads + threadIdx.x;
+        const int8_t f = i < T ? cls[i] : -1;
+        int tot_fg, tot_bg;
+        const int pf = block_excl_scan<kPtThreads>(f == 3, sh, &tot_fg);
+        const int pb = block_excl_scan<kPtThreads>(f == 2, sh, &tot_bg);
+        if (f == 3 || f == 2) {
+            const int s = f == 3 ? base_fg + pf : base_bg + pb;
+            const float* b = i < R ? props + i * 4 : g + (i - R) * 4;
+            const int64_t o = static_cast<int64_t>(img) * a.batch + s;
+            float* r5 = a.out_rois + o * 5;
+            r5[0] = static_cast<float>(img);
+            r5[1] = b[0]; r5[2] = b[1]; r5[3] = b[2]; r5[4] = b[3];
+            a.out_labels[o] = f == 3 ? gcls[arg[i]] : 0;
+            float* t = a.out_targets + o * 4;
+            if (f == 3) encode_box(b, g + arg[i] * 4, 10.f, 10.f, 5.f, 5.f, t);
+            else t[0] = t[1] = t[2] = t[3] = 0.0f;
+            if (a.out_src) a.out_src[o] = i;
+        }
+        base_fg += tot_fg;
+        base_bg += tot_bg;
+    }
+    __syncthreads();
+    // pad the unused slots (ignored by every loss: label -1, batch index -1)
+    const int S = base_bg;
+    for (int s = S + threadIdx.x; s < a.batch; s += kPtThreads) {
+        const int64_t o = static_cast<int64_t>(img) * a.batch + s;
+        float* r5 = a.out_rois + o * 5;
+        r5[0] = -1.0f;
+        r5[1] = r5[2] = r5[3] = r5[4] = 0.0f;
+        a.out_labels[o] = -1;
+        float* t = a.out_targets + o * 4;
+        t[0] = t[1] = t[2] = t[3] = 0.0f;
+        if (a.out_src) a.out_src[o] = -1;
+    }
+    if (threadIdx.x == 0) a.out_count[img] = S;
+}
+
+__global__ void u64_fill_kernel(unsigned long long* p, int64_t n, unsigned long long v) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        p[i] = v;
+}
+
+}  // namespace
+
+// ================================================================ host launchers
+cudaError_t make_anchors(const AnchorCfg& cfg, float* out, cudaStream_t st) {
+    const int64_t total = static_cast<int64_t>(cfg.H) * cfg.W * cfg.ns * cfg.nr;
+    const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 4 * kNumSMs));
+    anchors_kernel<<<blocks, 256, 0, st>>>(cfg, out);
+    return cudaGetLastError();
+}
+
+static int next_pow2(int v) {
+    int p = 1;
+    while (p < v) p <<= 1;
+    return p;
+}
+
+size_t proposal_workspace_bytes(int n_img, int n_anchors, int pre_k) {
+    const int k = std::min(pre_k, n_anchors);
+    const int nwords = (k + 63) / 64;
+    return static_cast<size_t>(n_img) * k * (16 + 4 + 4) + static_cast<size_t>(n_img) * k * nwords * 8 + 1024;
+}
+
+cudaError_t rpn_proposals(const ProposalArgs& p, void* ws, cudaStream_t st) {
+    const int nA = p.n_loc * p.A;
+    const int k = std::min(p.pre_k, nA);
+    if (k <= 0) return cudaErrorInvalidValue;
+    const int kp2 = next_pow2(k);
+    if (kp2 > 16384) return cudaErrorInvalidValue;
+    const int nwords = (k + 63) / 64;
+    uint8_t* w = static_cast<uint8_t*>(ws);
+    float* boxes = reinterpret_cast<float*>(w);
+    w += static_cast<size_t>(p.n_img) * k * 16;
+    int32_t* order = reinterpret_cast<int32_t*>(w);
+    w += static_cast<size_t>(p.n_img) * k * 4;
+    float* scores = reinterpret_cast<float*>(w);
+    w += static_cast<size_t>(p.n_img) * k * 4;
+    w = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(w) + 255) & ~uintptr_t(255));
+    uint64_t* mask = reinterpret_cast<uint64_t*>(w);
+
+    TopkArgs t{};
+    t.logits = p.logits; t.dtype = p.dtype; t.deltas = p.deltas; t.anchors = p.anchors;
+    t.n_loc = p.n_loc; t.A = p.A; t.A_pad = p.A_pad; t.k = k; t.k_pow2 = kp2;
+    t.img_h = p.img_h; t.img_w = p.img_w; t.clip_dw = p.clip_dw;
+    t.boxes = boxes; t.order = order; t.scores = scores;
+    const size_t smem = static_cast<size_t>(kp2) * 8;
+    cudaFuncSetAttribute(topk_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384 * 8);
+    topk_decode_kernel<<<p.n_img, kTopkThreads, smem, st>>>(t);
+    if (p.topk_order_out) {
+        cudaMemcpyAsync(p.topk_order_out, order, static_cast<size_t>(p.n_img) * k * 4, cudaMemcpyDeviceToDevice, st);
+    }
+    dim3 mg(nwords, nwords, p.n_img);
+    nms_mask_kernel<<<mg, 64, 0, st>>>(boxes, k, nwords, p.iou_thr, mask);
+    nms_scan_kernel<<<p.n_img, kScanThreads, static_cast<size_t>(nwords) * 8, st>>>(
+        boxes, mask, scores, k, nwords, p.post_k, p.rois, p.roi_scores, p.keep_pos, p.count);
+    return cudaGetLastError();
+}
+
+cudaError_t anchor_targets(const AnchorTargetArgs& a, void* ws, cudaStream_t st) {
+    uint8_t* w = static_cast<uint8_t*>(ws);
+    double* max_iou = reinterpret_cast<double*>(w);
+    w += static_cast<size_t>(a.n_img) * a.nA * 8;
+    int32_t* argmax = reinterpret_cast<int32_t*>(w);
+    w += static_cast<size_t>(a.n_img) * a.nA * 4;
+    w = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(w) + 255) & ~uintptr_t(255));
+    unsigned long long* gt_max = reinterpret_cast<unsigned long long*>(w);
+    const int64_t ng = static_cast<int64_t>(a.n_img) * a.gt_stride;
+    u64_fill_kernel<<<1, 256, 0, st>>>(gt_max, ng, 0ull);
+    dim3 grid(std::min((a.nA + 255) / 256, 2 * kNumSMs), a.n_img);
+    anchor_iou_kernel<<<grid, 256, 0, st>>>(a.anchors, a.nA, a.gt, a.gt_stride, a.gt_count, a.img_h, a.img_w, max_iou,
+                                            argmax, gt_max);
+    anchor_label_kernel<<<grid, 256, 0, st>>>(a.anchors, a.nA, a.gt, a.gt_stride, a.gt_count, max_iou, gt_max,
+                                              a.fg_thr, a.bg_thr, a.labels);
+    anchor_sample_kernel<<<a.n_img, kSampleThreads, 0, st>>>(a.nA, a.keys, a.batch, a.fg_cap, a.labels);
+    anchor_bbox_target_kernel<<<grid, 256, 0, st>>>(a.anchors, a.nA, a.gt, a.gt_stride, argmax, a.labels, a.targets);
+    return cudaGetLastError();
+}
+
+size_t anchor_target_workspace_bytes(int n_img, int nA, int gt_stride) {
+    return static_cast<size_t>(n_img) * nA * 12 + static_cast<size_t>(n_img) * gt_stride * 8 + 512;
+}
+
+cudaError_t proposal_targets(const ProposalTargetArgs& a, cudaStream_t st) {
+    proposal_target_kernel<<<a.n_img, kPtThreads, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace sdb

@@ -1,0 +1,810 @@
+// roi.cu -- RoIAlign forward/backward, pooling, residual activations, detection
+// losses and the synthetic input generator.
+//
+// RoIAlign: aligned (half-pixel) corners, fixed sampling ratio, average of the
+// bilinear samples; the restated oracle is orc_roialign_fwd/bwd (numerically
+// identical to torchvision.ops.roi_align(aligned=True)).  Forward: one thread
+// per (RoI, bin, 8 channels), 128-bit loads of the 4 corners of each sample.
+// Backward is a deterministic GATHER (no atomics): one CTA owns an 8x8 pixel
+// tile x 256-channel slab of dX in registers, walks the RoIs of its image
+// that reach the tile in index order and, using the separable bilinear
+// weights WY[ph][h] x WX[pw][w] staged in smem, accumulates every dY
+// contribution in a fixed order -- bitwise reproducible run to run.
+//
+// Losses fold the loss scale into backward exactly like the reference CE op
+// (src/model.cpp:132-150): forward returns the unscaled loss, backward
+// multiplies by grad_scale.  Reductions are fixed-order (deterministic).
+// Compiled with -fmad=false (no contraction) so float expressions evaluate
+// as written in the oracle.
+#include <algorithm>
+
+#include "common.cuh"
+#include "detect.h"
+#include "sdb_internal.h"
+
+namespace sdb {
+
+namespace {
+
+template <class T>
+SDB_DEV void ld8(const T* p, float (&v)[8]);
+template <>
+SDB_DEV void ld8<__half>(const __half* p, float (&v)[8]) {
+    const uint4 u = *reinterpret_cast<const uint4*>(p);
+    const __half2* h = reinterpret_cast<const __half2*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float2 f = __half22float2(h[i]);
+        v[2 * i] = f.x;
+        v[2 * i + 1] = f.y;
+    }
+}
+template <>
+SDB_DEV void ld8<float>(const float* p, float (&v)[8]) {
+    const float4 a = *reinterpret_cast<const float4*>(p);
+    const float4 b = *reinterpret_cast<const float4*>(p + 4);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+template <class T>
+SDB_DEV void st8(T* p, const float (&v)[8]);
+template <>
+SDB_DEV void st8<__half>(__half* p, const float (&v)[8]) {
+    uint4 u;
+    __half2* h = reinterpret_cast<__half2*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) h[i] = __floats2half2_rn(v[2 * i], v[2 * i + 1]);
+    *reinterpret_cast<uint4*>(p) = u;
+}
+template <>
+SDB_DEV void st8<float>(float* p, const float (&v)[8]) {
+    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    *reinterpret_cast<float4*>(p + 4) = make_float4(v[4], v[5], v[6], v[7]);
+}
+
+struct Geom {
+    int b;
+    float sw, sh, bw, bh;
+};
+
+// orc roi_geom (aligned=1): corner * scale - 0.5, bins = extent / P
+SDB_DEV Geom roi_geom(const float* r, int P, float scale) {
+    Geom g;
+    g.b = static_cast<int>(r[0]);
+    g.sw = r[1] * scale - 0.5f;
+    g.sh = r[2] * scale - 0.5f;
+    const float ew = r[3] * scale - 0.5f, eh = r[4] * scale - 0.5f;
+    g.bw = (ew - g.sw) / static_cast<float>(P);
+    g.bh = (eh - g.sh) / static_cast<float>(P);
+    return g;
+}
+
+SDB_DEV float sample_coord(float start, int p, float bin, int i, int sr) {
+    return start + static_cast<float>(p) * bin + (static_cast<float>(i) + 0.5f) * bin / static_cast<float>(sr);
+}
+
+// ---------------------------------------------------------------- RoIAlign fwd
+template <class T>
+__global__ void roialign_fwd_kernel(const T* __restrict__ feat, int H, int W, int C, const float* __restrict__ rois,
+                                    int R, int P, float scale, int sr, T* __restrict__ out) {
+    const int C8 = C / 8;
+    const int64_t total = static_cast<int64_t>(R) * P * P * C8;
+    const float count = static_cast<float>(max(sr * sr, 1));
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int c8 = static_cast<int>(e % C8);
+        const int64_t bin = e / C8;
+        const int pw = static_cast<int>(bin % P), ph = static_cast<int>((bin / P) % P);
+        const int r = static_cast<int>(bin / (P * P));
+        const Geom g = roi_geom(rois + static_cast<int64_t>(r) * 5, P, scale);
+        float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        if (g.b >= 0) {
+            const T* f = feat + static_cast<int64_t>(g.b) * H * W * C + c8 * 8;
+            for (int iy = 0; iy < sr; ++iy) {
+                float y = sample_coord(g.sh, ph, g.bh, iy, sr);
+                for (int ix = 0; ix < sr; ++ix) {
+                    float x = sample_coord(g.sw, pw, g.bw, ix, sr);
+                    if (y < -1.0f || y > static_cast<float>(H) || x < -1.0f || x > static_cast<float>(W)) continue;
+                    float yy = y <= 0.f ? 0.f : y, xx = x <= 0.f ? 0.f : x;
+                    int yl = static_cast<int>(yy), xl = static_cast<int>(xx), yh, xh;
+                    if (yl >= H - 1) { yh = yl = H - 1; yy = static_cast<float>(yl); } else yh = yl + 1;
+                    if (xl >= W - 1) { xh = xl = W - 1; xx = static_cast<float>(xl); } else xh = xl + 1;
+                    const float ly = yy - static_cast<float>(yl), lx = xx - static_cast<float>(xl);
+                    const float hy = 1.f - ly, hx = 1.f - lx;
+                    const float w1 = hy * hx, w2 = hy * lx, w3 = ly * hx, w4 = ly * lx;
+                    float v1[8], v2[8], v3[8], v4[8];
+                    ld8<T>(f + (static_cast<int64_t>(yl) * W + xl) * C, v1);
+                    ld8<T>(f + (static_cast<int64_t>(yl) * W + xh) * C, v2);
+                    ld8<T>(f + (static_cast<int64_t>(yh) * W + xl) * C, v3);
+                    ld8<T>(f + (static_cast<int64_t>(yh) * W + xh) * C, v4);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) acc[j] += w1 * v1[j] + w2 * v2[j] + w3 * v3[j] + w4 * v4[j];
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[j] = acc[j] / count;
+        }
+        st8<T>(out + e * 8, acc);
+    }
+}
+
+// ---------------------------------------------------------------- RoIAlign bwd (gather)
+constexpr int kTile = 8;        // 8x8 pixel tile
+constexpr int kSlab = 256;      // channels per CTA
+constexpr int kBwdThreads = 256;
+constexpr int kMaxP = 16;
+
+template <class T>
+__global__ void __launch_bounds__(kBwdThreads) roialign_bwd_kernel(const T* __restrict__ dy, int H, int W, int C,
+                                                                   const float* __restrict__ rois, int R, int P,
+                                                                   float scale, int sr, T* __restrict__ dfeat) {
+    __shared__ float WY[kMaxP][kTile];
+    __shared__ float WX[kMaxP][kTile];
+    __shared__ int list[1024];
+    __shared__ int sh[40];
+    const int n = blockIdx.z;
+    const int tiles_x = (W + kTile - 1) / kTile;
+    const int ty = blockIdx.x / tiles_x, tx = blockIdx.x % tiles_x;
+    const int y0 = ty * kTile, x0 = tx * kTile;
+    const int c_base = blockIdx.y * kSlab;
+    const int chunk = threadIdx.x & 31;         // 8-channel chunk within the slab
+    const int pix0 = threadIdx.x >> 5;          // pixels pix0 + 8*i
+    const int c = c_base + chunk * 8;
+    const bool c_ok = c < C;
+    const float inv_count = 1.0f / static_cast<float>(max(sr * sr, 1));
+    float acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+
+    for (int base = 0; base < R; base += 1024) {
+        // compact (in index order) the RoIs of image n that reach this tile
+        int cnt_local = 0;
+        int mine[4];
+        for (int q = 0; q < 4; ++q) {
+            const int r = base + threadIdx.x * 4 + q;
+            mine[q] = 0;
+            if (r >= R) continue;
+            const float* rr = rois + static_cast<int64_t>(r) * 5;
+            if (static_cast<int>(rr[0]) != n) continue;
+            const Geom g = roi_geom(rr, P, scale);
+            const float ylo = g.sh - 1.0f, yhi = g.sh + g.bh * P + 1.0f;
+            const float xlo = g.sw - 1.0f, xhi = g.sw + g.bw * P + 1.0f;
+            if (yhi < static_cast<float>(y0) || ylo > static_cast<float>(y0 + kTile) || xhi < static_cast<float>(x0) ||
+                xlo > static_cast<float>(x0 + kTile))
+                continue;
+            mine[q] = 1;
+            ++cnt_local;
+        }
+        // exclusive scan of cnt_local
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        int xs = cnt_local;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int yv = __shfl_up_sync(0xffffffffu, xs, o);
+            if (lane >= o) xs += yv;
+        }
+        if (lane == 31) sh[wid] = xs;
+        __syncthreads();
+        int wbase = 0, total = 0;
+        for (int w2 = 0; w2 < kBwdThreads / 32; ++w2) {
+            if (w2 < wid) wbase += sh[w2];
+            total += sh[w2];
+        }
+        int pos = wbase + xs - cnt_local;
+        for (int q = 0; q < 4; ++q)
+            if (mine[q]) list[pos++] = base + threadIdx.x * 4 + q;
+        __syncthreads();
+
+        for (int li = 0; li < total; ++li) {
+            const int r = list[li];
+            const Geom g = roi_geom(rois + static_cast<int64_t>(r) * 5, P, scale);
+            // separable weights for this tile
+            for (int t = threadIdx.x; t < 2 * P * kTile; t += kBwdThreads) {
+                const bool isx = t >= P * kTile;
+                const int tt = isx ? t - P * kTile : t;
+                const int pb = tt / kTile, lo = tt % kTile;
+                const int pix = (isx ? x0 : y0) + lo;
+                const int lim = isx ? W : H;
+                float wsum = 0.f;
+                for (int is = 0; is < sr; ++is) {
+                    float v = isx ? sample_coord(g.sw, pb, g.bw, is, sr) : sample_coord(g.sh, pb, g.bh, is, sr);
+                    if (v < -1.0f || v > static_cast<float>(lim)) continue;
+                    if (v <= 0.f) v = 0.f;
+                    int lo_i = static_cast<int>(v), hi_i;
+                    if (lo_i >= lim - 1) { hi_i = lo_i = lim - 1; v = static_cast<float>(lo_i); } else hi_i = lo_i + 1;
+                    const float l = v - static_cast<float>(lo_i), h = 1.f - l;
+                    if (lo_i == pix) wsum += h;
+                    if (hi_i == pix) wsum += l;
+                }
+                if (isx) WX[pb][lo] = wsum;
+                else WY[pb][lo] = wsum;
+            }
+            __syncthreads();
+            if (c_ok) {
+                const T* d = dy + static_cast<int64_t>(r) * P * P * C + c;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int p = pix0 + 8 * i;
+                    const int ly = p >> 3, lx = p & 7;
+                    if (y0 + ly >= H || x0 + lx >= W) continue;
+                    for (int ph = 0; ph < P; ++ph) {
+                        const float wy = WY[ph][ly];
+                        if (wy == 0.f) continue;
+                        for (int pw = 0; pw < P; ++pw) {
+                            const float wx = WX[pw][lx];
+                            if (wx == 0.f) continue;
+                            const float wgt = wy * wx * inv_count;
+                            float v[8];
+                            ld8<T>(d + (static_cast<int64_t>(ph) * P + pw) * C, v);
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) acc[i][j] += wgt * v[j];
+                        }
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    if (!c_ok) return;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int p = pix0 + 8 * i;
+        const int yy = y0 + (p >> 3), xx = x0 + (p & 7);
+        if (yy >= H || xx >= W) continue;
+        st8<T>(dfeat + ((static_cast<int64_t>(n) * H + yy) * W + xx) * C + c, acc[i]);
+    }
+}
+
+// ---------------------------------------------------------------- pooling
+template <class T>
+__global__ void maxpool_fwd_kernel(const T* __restrict__ x, int N, int H, int W, int C, int k, int s, int p,
+                                   int Ho, int Wo, T* __restrict__ y, uint8_t* __restrict__ am) {
+    const int C8 = C / 8;
+    const int64_t total = static_cast<int64_t>(N) * Ho * Wo * C8;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int c8 = static_cast<int>(e % C8);
+        const int64_t pix = e / C8;
+        const int ow = static_cast<int>(pix % Wo), oh = static_cast<int>((pix / Wo) % Ho);
+        const int n = static_cast<int>(pix / (static_cast<int64_t>(Wo) * Ho));
+        float m[8];
+        int at[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) { m[j] = -INFINITY; at[j] = -1; }
+        for (int r = 0; r < k; ++r)
+            for (int q = 0; q < k; ++q) {
+                const int ih = oh * s - p + r, iw = ow * s - p + q;
+                if (ih < 0 || ih >= H || iw < 0 || iw >= W) continue;
+                float v[8];
+                ld8<T>(x + ((static_cast<int64_t>(n) * H + ih) * W + iw) * C + c8 * 8, v);
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (at[j] < 0 || v[j] > m[j]) { m[j] = v[j]; at[j] = r * k + q; }
+            }
+        st8<T>(y + e * 8, m);
+        uint64_t pk = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) pk |= static_cast<uint64_t>(at[j] & 0xff) << (8 * j);
+        reinterpret_cast<uint64_t*>(am)[e] = pk;
+    }
+}
+
+template <class T>
+__global__ void maxpool_bwd_kernel(const T* __restrict__ dy, const uint8_t* __restrict__ am, int N, int H, int W, int C,
+                                   int k, int s, int p, int Ho, int Wo, T* __restrict__ dx) {
+    const int C8 = C / 8;
+    const int64_t total = static_cast<int64_t>(N) * H * W * C8;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int c8 = static_cast<int>(e % C8);
+        const int64_t pix = e / C8;
+        const int iw = static_cast<int>(pix % W), ih = static_cast<int>((pix / W) % H);
+        const int n = static_cast<int>(pix / (static_cast<int64_t>(W) * H));
+        float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        const int oh_lo = max(0, (ih + p - k + s) / s), oh_hi = min(Ho - 1, (ih + p) / s);
+        const int ow_lo = max(0, (iw + p - k + s) / s), ow_hi = min(Wo - 1, (iw + p) / s);
+        for (int oh = oh_lo; oh <= oh_hi; ++oh)
+            for (int ow = ow_lo; ow <= ow_hi; ++ow) {
+                const int r = ih - (oh * s - p), q = iw - (ow * s - p);
+                if (r < 0 || r >= k || q < 0 || q >= k) continue;
+                const int64_t oe = ((static_cast<int64_t>(n) * Ho + oh) * Wo + ow) * C8 + c8;
+                const uint64_t pk = reinterpret_cast<const uint64_t*>(am)[oe];
+                float g[8];
+                ld8<T>(dy + oe * 8, g);
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (static_cast<int>((pk >> (8 * j)) & 0xff) == r * k + q) acc[j] += g[j];
+            }
+        st8<T>(dx + e * 8, acc);
+    }
+}
+
+template <class T>
+__global__ void avgpool_fwd_kernel(const T* __restrict__ x, int N, int HW, int C, T* __restrict__ y) {
+    const int C8 = C / 8;
+    const int64_t total = static_cast<int64_t>(N) * C8;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int c8 = static_cast<int>(e % C8);
+        const int64_t n = e / C8;
+        float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int i = 0; i < HW; ++i) {
+            float v[8];
+            ld8<T>(x + (n * HW + i) * C + c8 * 8, v);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[j] += v[j];
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = acc[j] / static_cast<float>(HW);
+        st8<T>(y + e * 8, acc);
+    }
+}
+
+template <class T>
+__global__ void avgpool_bwd_kernel(const T* __restrict__ dy, int N, int HW, int C, float inv, T* __restrict__ dx) {
+    const int C8 = C / 8;
+    const int64_t total = static_cast<int64_t>(N) * HW * C8;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int c8 = static_cast<int>(e % C8);
+        const int64_t n = e / (static_cast<int64_t>(HW) * C8);
+        float g[8];
+        ld8<T>(dy + (n * C8 + c8) * 8, g);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) g[j] = g[j] * inv;
+        st8<T>(dx + e * 8, g);
+    }
+}
+
+// ---------------------------------------------------------------- elementwise
+template <class T>
+SDB_DEV float rnd(float v) {
+    return to_f<T>(from_f<T>(v));
+}
+
+template <class T>
+__global__ void add_act_kernel(const T* __restrict__ a, const T* __restrict__ b, T* __restrict__ out, int64_t n8,
+                               int act, float slope) {
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n8;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        float va[8], vb[8], o[8];
+        ld8<T>(a + e * 8, va);
+        ld8<T>(b + e * 8, vb);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const float s = rnd<T>(va[j] + vb[j]);  // add node output (src/tensor.cpp:125)
+            o[j] = act == 0 ? s : (s > 0.f ? s : (act == 1 ? 0.f : slope * s));
+        }
+        st8<T>(out + e * 8, o);
+    }
+}
+
+template <class T>
+__global__ void act_bwd_kernel(const T* __restrict__ dy, const T* __restrict__ y, T* __restrict__ dx, int64_t n8,
+                               float neg) {
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n8;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        float g[8], v[8];
+        ld8<T>(dy + e * 8, g);
+        ld8<T>(y + e * 8, v);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) g[j] = v[j] > 0.f ? g[j] : neg * g[j];  // src/autograd.cpp:340-351
+        st8<T>(dx + e * 8, g);
+    }
+}
+
+template <class T>
+__global__ void relu_kernel(const T* __restrict__ x, T* __restrict__ y, int64_t n8) {
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n8;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        float v[8];
+        ld8<T>(x + e * 8, v);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = v[j] > 0.f ? v[j] : 0.f;
+        st8<T>(y + e * 8, v);
+    }
+}
+
+template <class T>
+__global__ void add_inplace_kernel(T* __restrict__ acc, const T* __restrict__ b, int64_t n8) {
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n8;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        float va[8], vb[8];
+        ld8<T>(acc + e * 8, va);
+        ld8<T>(b + e * 8, vb);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) va[j] += vb[j];
+        st8<T>(acc + e * 8, va);
+    }
+}
+
+// ---------------------------------------------------------------- losses
+constexpr int kLossThreads = 1024;
+
+SDB_DEV double block_sum_d(double v, double* sh) {
+    v = warp_sum(v);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double t = 0.0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += sh[w];
+    __syncthreads();
+    return t;
+}
+
+template <class T>
+SDB_DEV float ldv(const T* p, int64_t i) { return to_f<T>(p[i]); }
+
+// reference softmax-CE (src/model.cpp:106-150) over rows with label >= 0
+template <class T>
+__global__ void __launch_bounds__(kLossThreads) softmax_ce_kernel(const T* __restrict__ logits, int R, int ncls, int ld,
+                                                                  const int32_t* __restrict__ labels,
+                                                                  T* __restrict__ dlogits, const double* scale,
+                                                                  double* loss_out, int slot) {
+    __shared__ double sh[32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    int cnt = 0;
+    for (int r = threadIdx.x; r < R; r += blockDim.x) cnt += labels[r] >= 0;
+    const double B = block_sum_d(static_cast<double>(cnt), sh);
+    const double gs = scale ? *scale : 1.0;
+    const float g = B > 0 ? static_cast<float>(1.0 * gs / B) : 0.f;
+    double wl = 0.0;
+    for (int r = wid; r < R; r += nw) {
+        const int y = labels[r];
+        const T* x = logits + static_cast<int64_t>(r) * ld;
+        T* dx = dlogits + static_cast<int64_t>(r) * ld;
+        if (y < 0) {
+            for (int j = lane; j < ld; j += 32) dx[j] = from_f<T>(0.f);
+            continue;
+        }
+        double mx = -INFINITY;
+        for (int j = lane; j < ncls; j += 32) mx = fmax(mx, static_cast<double>(ldv(x, j)));
+        for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        double z = 0.0;
+        for (int j = lane; j < ncls; j += 32) z += exp(static_cast<double>(ldv(x, j)) - mx);
+        z = warp_sum(z);
+        float py = 0.f;
+        for (int j = lane; j < ld; j += 32) {
+            if (j < ncls) {
+                const float pj = static_cast<float>(exp(static_cast<double>(ldv(x, j)) - mx) / z);
+                if (j == y) py = pj;
+                dx[j] = from_f<T>((pj - (j == y ? 1.0f : 0.0f)) * g);
+            } else {
+                dx[j] = from_f<T>(0.f);
+            }
+        }
+        py = __shfl_sync(0xffffffffu, py, y & 31);
+        if (lane == 0) wl += -log(fmax(1e-30, static_cast<double>(py)));
+    }
+    if (lane == 0) sh[wid] = wl;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < nw; ++w) t += sh[w];
+        loss_out[slot] = B > 0 ? t / B : 0.0;
+    }
+}
+
+// sigmoid BCE over anchors with label >= 0, normalised by their count
+template <class T>
+__global__ void __launch_bounds__(kLossThreads) sigmoid_bce_kernel(const T* __restrict__ logits, int64_t n_loc, int A,
+                                                                   int A_pad, const int8_t* __restrict__ labels,
+                                                                   T* __restrict__ dlogits, const double* scale,
+                                                                   double* loss_out, int slot) {
+    __shared__ double sh[32];
+    const int64_t n = n_loc * A_pad;
+    int cnt = 0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const int a = static_cast<int>(i % A_pad);
+        if (a < A) cnt += labels[(i / A_pad) * A + a] >= 0;
+    }
+    const double norm = block_sum_d(static_cast<double>(cnt), sh);
+    const double gs = (scale ? *scale : 1.0) / (norm > 0 ? norm : 1.0);
+    double acc = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const int a = static_cast<int>(i % A_pad);
+        float gout = 0.f;
+        if (a < A) {
+            const int t = labels[(i / A_pad) * A + a];
+            if (t >= 0) {
+                const double v = ldv(logits, i);
+                acc += fmax(v, 0.0) - v * t + log1p(exp(-fabs(v)));
+                gout = static_cast<float>((1.0 / (1.0 + exp(-v)) - t) * gs);
+            }
+        }
+        dlogits[i] = from_f<T>(gout);
+    }
+    const double tot = block_sum_d(acc, sh);
+    if (threadIdx.x == 0) loss_out[slot] = norm > 0 ? tot / norm : 0.0;
+}
+
+SDB_DEV void sl1(double d, double beta, double& l, double& g) {
+    const double ad = fabs(d);
+    if (ad < beta) {
+        l = 0.5 * d * d / beta;
+        g = d / beta;
+    } else {
+        l = ad - 0.5 * beta;
+        g = d > 0 ? 1.0 : -1.0;
+    }
+}
+
+template <class T>
+__global__ void __launch_bounds__(kLossThreads) rpn_sl1_kernel(const T* __restrict__ deltas, int64_t n_loc, int A,
+                                                               int A_pad, const int8_t* __restrict__ labels,
+                                                               const float* __restrict__ targets, double beta,
+                                                               double norm, T* __restrict__ dd, const double* scale,
+                                                               double* loss_out, int slot) {
+    __shared__ double sh[32];
+    const int64_t n = n_loc * 4 * A_pad;
+    const double gs = (scale ? *scale : 1.0) / norm;
+    double acc = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const int64_t loc = i / (4 * A_pad);
+        const int rem = static_cast<int>(i % (4 * A_pad));
+        const int a = rem / 4, k = rem % 4;
+        float gout = 0.f;
+        if (a < A && labels[loc * A + a] == 1) {
+            const double d = static_cast<double>(ldv(deltas, i)) - static_cast<double>(targets[(loc * A + a) * 4 + k]);
+            double l, g;
+            sl1(d, beta, l, g);
+            acc += l;
+            gout = static_cast<float>(g * gs);
+        }
+        dd[i] = from_f<T>(gout);
+    }
+    const double tot = block_sum_d(acc, sh);
+    if (threadIdx.x == 0) loss_out[slot] = tot / norm;
+}
+
+template <class T>
+__global__ void __launch_bounds__(kLossThreads) rcnn_sl1_kernel(const T* __restrict__ pred, int R, int ld,
+                                                                const int32_t* __restrict__ labels,
+                                                                const float* __restrict__ targets, double beta,
+                                                                T* __restrict__ dp, const double* scale,
+                                                                double* loss_out, int slot) {
+    __shared__ double sh[32];
+    int cnt = 0;
+    for (int r = threadIdx.x; r < R; r += blockDim.x) cnt += labels[r] >= 0;
+    const double norm = block_sum_d(static_cast<double>(cnt), sh);
+    const double gs = (scale ? *scale : 1.0) / (norm > 0 ? norm : 1.0);
+    double acc = 0.0;
+    const int64_t n = static_cast<int64_t>(R) * ld;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const int r = static_cast<int>(i / ld), col = static_cast<int>(i % ld);
+        const int lab = labels[r];
+        float gout = 0.f;
+        if (lab > 0 && col >= 4 * lab && col < 4 * lab + 4) {
+            const double d = static_cast<double>(ldv(pred, i)) - static_cast<double>(targets[r * 4 + (col - 4 * lab)]);
+            double l, g;
+            sl1(d, beta, l, g);
+            acc += l;
+            gout = static_cast<float>(g * gs);
+        }
+        dp[i] = from_f<T>(gout);
+    }
+    const double tot = block_sum_d(acc, sh);
+    if (threadIdx.x == 0) loss_out[slot] = norm > 0 ? tot / norm : 0.0;
+}
+
+// ---------------------------------------------------------------- synthetic images
+SDB_DEV uint64_t mix64d(uint64_t a, uint64_t b) {
+    uint64_t z = a ^ (b + 0x9e3779b97f4a7c15ull);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+
+template <class T>
+__global__ void synth_kernel(T* __restrict__ out, int n, int H, int W, int Cp, uint64_t seed,
+                             const int64_t* __restrict__ slots, int64_t slot0) {
+    const int64_t total = static_cast<int64_t>(n) * H * W;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int img = static_cast<int>(e / (static_cast<int64_t>(H) * W));
+        const int64_t hw = e % (static_cast<int64_t>(H) * W);
+        const int64_t slot = slots ? slots[img] : slot0 + img;
+        const uint64_t key = mix64d(seed ^ 0x1a2b3c4d5e6f7788ull, static_cast<uint64_t>(slot));
+        T* o = out + e * Cp;
+        for (int c = 0; c < Cp; ++c) {
+            float v = 0.f;
+            if (c < 3) {
+                const uint64_t el = static_cast<uint64_t>(c) * H * W + hw;
+                const uint64_t r1 = mix64d(key, 2 * el), r2 = mix64d(key, 2 * el + 1);
+                const float u1 = (static_cast<float>(r1 >> 40) + 0.5f) * 0x1.0p-24f;
+                const float u2 = static_cast<float>(r2 >> 40) * 0x1.0p-24f;
+                v = sqrtf(-2.0f * logf(u1)) * cospif(2.0f * u2);
+            }
+            o[c] = from_f<T>(v);
+        }
+    }
+}
+
+int grid_for(int64_t n) {
+    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 16 * kNumSMs)));
+}
+
+}  // namespace
+
+#define SDB_DISPATCH(dtype, KERNEL, GRID, BLOCK, SMEM, ST, ...)                         \
+    do {                                                                                \
+        if ((dtype) == kF16) KERNEL<__half><<<GRID, BLOCK, SMEM, ST>>>(__VA_ARGS__);    \
+        else KERNEL<float><<<GRID, BLOCK, SMEM, ST>>>(__VA_ARGS__);                     \
+    } while (0)
+
+template <class T>
+static inline const T* cp(const void* p) { return static_cast<const T*>(p); }
+
+cudaError_t roialign_fwd(int dtype, const void* feat, int N, int H, int W, int C, const float* rois, int R, int P,
+                         float scale, int sr, void* out, cudaStream_t st) {
+    (void)N;
+    const int64_t total = static_cast<int64_t>(R) * P * P * (C / 8);
+    if (dtype == kF16)
+        roialign_fwd_kernel<__half><<<grid_for(total), 256, 0, st>>>(cp<__half>(feat), H, W, C, rois, R, P, scale, sr,
+                                                                    static_cast<__half*>(out));
+    else
+        roialign_fwd_kernel<float><<<grid_for(total), 256, 0, st>>>(cp<float>(feat), H, W, C, rois, R, P, scale, sr,
+                                                                   static_cast<float*>(out));
+    return cudaGetLastError();
+}
+
+cudaError_t roialign_bwd(int dtype, const void* dy, int N, int H, int W, int C, const float* rois, int R, int P,
+                         float scale, int sr, void* dfeat, cudaStream_t st) {
+    if (P > kMaxP) return cudaErrorInvalidValue;
+    dim3 grid(((H + kTile - 1) / kTile) * ((W + kTile - 1) / kTile), (C + kSlab - 1) / kSlab, N);
+    if (dtype == kF16)
+        roialign_bwd_kernel<__half><<<grid, kBwdThreads, 0, st>>>(cp<__half>(dy), H, W, C, rois, R, P, scale, sr,
+                                                                  static_cast<__half*>(dfeat));
+    else
+        roialign_bwd_kernel<float><<<grid, kBwdThreads, 0, st>>>(cp<float>(dy), H, W, C, rois, R, P, scale, sr,
+                                                                 static_cast<float*>(dfeat));
+    return cudaGetLastError();
+}
+
+cudaError_t maxpool_fwd(int dtype, const void* x, int N, int H, int W, int C, int k, int s, int p, void* y,
+                        uint8_t* argmax, cudaStream_t st) {
+    const int Ho = (H + 2 * p - k) / s + 1, Wo = (W + 2 * p - k) / s + 1;
+    const int64_t total = static_cast<int64_t>(N) * Ho * Wo * (C / 8);
+    if (dtype == kF16)
+        maxpool_fwd_kernel<__half><<<grid_for(total), 256, 0, st>>>(cp<__half>(x), N, H, W, C, k, s, p, Ho, Wo,
+                                                                    static_cast<__half*>(y), argmax);
+    else
+        maxpool_fwd_kernel<float><<<grid_for(total), 256, 0, st>>>(cp<float>(x), N, H, W, C, k, s, p, Ho, Wo,
+                                                                   static_cast<float*>(y), argmax);
+    return cudaGetLastError();
+}
+
+cudaError_t maxpool_bwd(int dtype, const void* dy, const uint8_t* argmax, int N, int H, int W, int C, int k, int s,
+                        int p, void* dx, cudaStream_t st) {
+    const int Ho = (H + 2 * p - k) / s + 1, Wo = (W + 2 * p - k) / s + 1;
+    const int64_t total = static_cast<int64_t>(N) * H * W * (C / 8);
+    if (dtype == kF16)
+        maxpool_bwd_kernel<__half><<<grid_for(total), 256, 0, st>>>(cp<__half>(dy), argmax, N, H, W, C, k, s, p, Ho, Wo,
+                                                                    static_cast<__half*>(dx));
+    else
+        maxpool_bwd_kernel<float><<<grid_for(total), 256, 0, st>>>(cp<float>(dy), argmax, N, H, W, C, k, s, p, Ho, Wo,
+                                                                   static_cast<float*>(dx));
+    return cudaGetLastError();
+}
+
+cudaError_t avgpool_fwd(int dtype, const void* x, int N, int HW, int C, void* y, cudaStream_t st) {
+    const int64_t total = static_cast<int64_t>(N) * (C / 8);
+    if (dtype == kF16)
+        avgpool_fwd_kernel<__half><<<grid_for(total), 256, 0, st>>>(cp<__half>(x), N, HW, C, static_cast<__half*>(y));
+    else
+        avgpool_fwd_kernel<float><<<grid_for(total), 256, 0, st>>>(cp<float>(x), N, HW, C, static_cast<float*>(y));
+    return cudaGetLastError();
+}
+
+cudaError_t avgpool_bwd(int dtype, const void* dy, int N, int HW, int C, void* dx, cudaStream_t st) {
+    const int64_t total = static_cast<int64_t>(N) * HW * (C / 8);
+    const float inv = static_cast<float>(1.0 / static_cast<double>(HW));  // src/autograd.cpp:381-384
+    if (dtype == kF16)
+        avgpool_bwd_kernel<__half><<<grid_for(total), 256, 0, st>>>(cp<__half>(dy), N, HW, C, inv,
+                                                                    static_cast<__half*>(dx));
+    else
+        avgpool_bwd_kernel<float><<<grid_for(total), 256, 0, st>>>(cp<float>(dy), N, HW, C, inv, static_cast<float*>(dx));
+    return cudaGetLastError();
+}
+
+cudaError_t add_act(int dtype, const void* a, const void* b, void* out, int64_t n, int act, float slope,
+                    cudaStream_t st) {
+    const int64_t n8 = n / 8;
+    if (dtype == kF16)
+        add_act_kernel<__half><<<grid_for(n8), 256, 0, st>>>(cp<__half>(a), cp<__half>(b), static_cast<__half*>(out),
+                                                             n8, act, slope);
+    else
+        add_act_kernel<float><<<grid_for(n8), 256, 0, st>>>(cp<float>(a), cp<float>(b), static_cast<float*>(out), n8,
+                                                            act, slope);
+    return cudaGetLastError();
+}
+
+cudaError_t act_bwd(int dtype, const void* dy, const void* y, void* dx, int64_t n, float neg, cudaStream_t st) {
+    const int64_t n8 = n / 8;
+    if (dtype == kF16)
+        act_bwd_kernel<__half><<<grid_for(n8), 256, 0, st>>>(cp<__half>(dy), cp<__half>(y), static_cast<__half*>(dx),
+                                                             n8, neg);
+    else
+        act_bwd_kernel<float><<<grid_for(n8), 256, 0, st>>>(cp<float>(dy), cp<float>(y), static_cast<float*>(dx), n8,
+                                                            neg);
+    return cudaGetLastError();
+}
+
+cudaError_t relu_fwd(int dtype, const void* x, void* y, int64_t n, cudaStream_t st) {
+    const int64_t n8 = n / 8;
+    if (dtype == kF16) relu_kernel<__half><<<grid_for(n8), 256, 0, st>>>(cp<__half>(x), static_cast<__half*>(y), n8);
+    else relu_kernel<float><<<grid_for(n8), 256, 0, st>>>(cp<float>(x), static_cast<float*>(y), n8);
+    return cudaGetLastError();
+}
+
+cudaError_t add_inplace(int dtype, void* acc, const void* b, int64_t n, cudaStream_t st) {
+    const int64_t n8 = n / 8;
+    if (dtype == kF16)
+        add_inplace_kernel<__half><<<grid_for(n8), 256, 0, st>>>(static_cast<__half*>(acc), cp<__half>(b), n8);
+    else
+        add_inplace_kernel<float><<<grid_for(n8), 256, 0, st>>>(static_cast<float*>(acc), cp<float>(b), n8);
+    return cudaGetLastError();
+}
+
+size_t loss_workspace_bytes(int64_t) { return 0; }
+
+cudaError_t softmax_ce(int dtype, const void* logits, int R, int ncls, int ld, const int32_t* labels, void* dlogits,
+                       const LossArgs& la, void*, cudaStream_t st) {
+    if (dtype == kF16)
+        softmax_ce_kernel<__half><<<1, kLossThreads, 0, st>>>(cp<__half>(logits), R, ncls, ld, labels,
+                                                             static_cast<__half*>(dlogits), la.scale, la.loss_out,
+                                                             la.slot);
+    else
+        softmax_ce_kernel<float><<<1, kLossThreads, 0, st>>>(cp<float>(logits), R, ncls, ld, labels,
+                                                            static_cast<float*>(dlogits), la.scale, la.loss_out, la.slot);
+    return cudaGetLastError();
+}
+
+cudaError_t sigmoid_bce(int dtype, const void* logits, int64_t n_loc, int A, int A_pad, const int8_t* labels,
+                        void* dlogits, const LossArgs& la, void*, cudaStream_t st) {
+    if (dtype == kF16)
+        sigmoid_bce_kernel<__half><<<1, kLossThreads, 0, st>>>(cp<__half>(logits), n_loc, A, A_pad, labels,
+                                                              static_cast<__half*>(dlogits), la.scale, la.loss_out,
+                                                              la.slot);
+    else
+        sigmoid_bce_kernel<float><<<1, kLossThreads, 0, st>>>(cp<float>(logits), n_loc, A, A_pad, labels,
+                                                             static_cast<float*>(dlogits), la.scale, la.loss_out,
+                                                             la.slot);
+    return cudaGetLastError();
+}
+
+cudaError_t rpn_smooth_l1(int dtype, const void* deltas, int64_t n_loc, int A, int A_pad, const int8_t* labels,
+                          const float* targets, double beta, double norm, void* dd, const LossArgs& la, void*,
+                          cudaStream_t st) {
+    if (dtype == kF16)
+        rpn_sl1_kernel<__half><<<1, kLossThreads, 0, st>>>(cp<__half>(deltas), n_loc, A, A_pad, labels, targets, beta,
+                                                          norm, static_cast<__half*>(dd), la.scale, la.loss_out,
+                                                          la.slot);
+    else
+        rpn_sl1_kernel<float><<<1, kLossThreads, 0, st>>>(cp<float>(deltas), n_loc, A, A_pad, labels, targets, beta,
+                                                         norm, static_cast<float*>(dd), la.scale, la.loss_out, la.slot);
+    return cudaGetLastError();
+}
+
+cudaError_t rcnn_smooth_l1(int dtype, const void* pred, int R, int ld, const int32_t* labels, const float* targets,
+                           double beta, void* dp, const LossArgs& la, void*, cudaStream_t st) {
+    if (dtype == kF16)
+        rcnn_sl1_kernel<__half><<<1, kLossThreads, 0, st>>>(cp<__half>(pred), R, ld, labels, targets, beta,
+                                                           static_cast<__half*>(dp), la.scale, la.loss_out, la.slot);
+    else
+        rcnn_sl1_kernel<float><<<1, kLossThreads, 0, st>>>(cp<float>(pred), R, ld, labels, targets, beta,
+                                                          static_cast<float*>(dp), la.scale, la.loss_out, la.slot);
+    return cudaGetLastError();
+}
+
+cudaError_t synth_images(int dtype, void* out, int n, int H, int W, int Cp, uint64_t seed, const int64_t* slots,
+                         int64_t slot0, cudaStream_t st) {
+    const int64_t total = static_cast<int64_t>(n) * H * W;
+    if (dtype == kF16)
+        synth_kernel<__half><<<grid_for(total), 256, 0, st>>>(static_cast<__half*>(out), n, H, W, Cp, seed, slots, slot0);
+    else
+        synth_kernel<float><<<grid_for(total), 256, 0, st>>>(static_cast<float*>(out), n, H, W, Cp, seed, slots, slot0);
+    return cudaGetLastError();
+}
+
+}  // namespace sdb

@@ -10,6 +10,9 @@ namespace sdb {
 
 enum DType { kF32 = 0, kF16 = 1 };
 
+// records the thread-local message returned by sdb_last_error(); returns code
+int set_error(int code, const char* msg);
+
 struct ConvShape {
     int N, H, W, C;  // input activation (NHWC)
     int K, R, S;     // filter KRSC
