@@ -188,6 +188,11 @@ int sdb_det_export(sdb_det* det, int what, void* host, int64_t capacity, int64_t
 int sdb_det_dims(sdb_det* det, int* feat_h, int* feat_w, int* n_anchor_per_loc, int* a_pad);
 /* launches of libsdb kernels per step (counted at the first step) */
 int sdb_det_kernel_launches(sdb_det* det, int64_t* n);
+/* one eager, CUDA-event-instrumented step on the current batch: per category
+ * (0 conv fprop, 1 dgrad, 2 wgrad, 3 norm fwd, 4 norm bwd, 5 elementwise,
+ * 6 pooling, 7 targets, 8 proposal, 9 roialign fwd, 10 roialign bwd, 11 losses,
+ * 12 optimizer, 13 comm) device ms, algorithmic FLOPs, algorithmic bytes, launches */
+int sdb_det_profile(sdb_det* det, double* ms, double* flops, double* bytes, int64_t* launches, int ncat);
 
 #ifdef __cplusplus
 }

@@ -105,6 +105,29 @@ struct Block {
     Act in, z1, a1, z2, a2, z3, b3, zd, d, out;
 };
 
+enum ProfCat {
+    P_FPROP = 0, P_DGRAD, P_WGRAD, P_NORM_F, P_NORM_B, P_ELEM, P_POOL, P_TARGETS, P_PROPOSAL, P_ROI_F, P_ROI_B,
+    P_LOSS, P_OPTIM, P_COMM, P_NCAT
+};
+
+// per-category CUDA-event timing of one eager step (sdb_det_profile)
+struct Prof {
+    bool on = false;
+    std::vector<cudaEvent_t> pool;
+    size_t used = 0;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> recs;
+    double flops[P_NCAT] = {}, bytes[P_NCAT] = {};
+    int64_t launches[P_NCAT] = {};
+    cudaEvent_t get() {
+        if (used == pool.size()) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            pool.push_back(e);
+        }
+        return pool[used++];
+    }
+};
+
 }  // namespace
 
 struct sdb_det {
@@ -170,6 +193,7 @@ struct sdb_det {
     int steps_done = 0;
     int64_t launches = 0;
     std::vector<void*> allocs;
+    Prof prof;
 
     void* alloc(size_t bytes) {
         void* p = nullptr;
@@ -233,6 +257,30 @@ struct sdb_det {
 };
 
 namespace {
+
+struct PScope {
+    sdb_det* d;
+    int cat;
+    cudaEvent_t e0 = nullptr;
+    PScope(sdb_det* dd, int c, double flops = 0, double bytes = 0, int nlaunch = 1) : d(dd), cat(c) {
+        if (!d->prof.on) return;
+        d->prof.flops[c] += flops;
+        d->prof.bytes[c] += bytes;
+        d->prof.launches[c] += nlaunch;
+        e0 = d->prof.get();
+        cudaEventRecord(e0, d->ctx->stream);
+    }
+    ~PScope() {
+        if (!e0) return;
+        cudaEvent_t e1 = d->prof.get();
+        cudaEventRecord(e1, d->ctx->stream);
+        d->prof.recs.push_back({cat, {e0, e1}});
+    }
+};
+
+double conv_flops(const ConvShape& g) {
+    return 2.0 * g.N * g.Ho() * g.Wo() * static_cast<double>(g.K) * g.C * g.R * g.S;
+}
 
 // ------------------------------------------------------------------ build
 void build_stage(sdb_det* d, std::vector<Block>& out, const std::string& pref, int nblocks, int cin, int width,
@@ -348,11 +396,13 @@ size_t max_ws(sdb_det* d) {
 
 // ------------------------------------------------------------------ forward helpers
 void conv_fwd(sdb_det* d, const ConvL& c, const Act& x, const Act& y) {
+    PScope ps(d, P_FPROP, conv_flops(c.g));
     CK(conv_fprop(c.g, d->dt, x.p, d->wdev_ptr(c.p), y.p, d->ctx->stream));
 }
 
 void norm_fwd(sdb_det* d, const NormL& n, const Act& z, const Act& a) {
     const int64_t rows = static_cast<int64_t>(z.n) * z.h * z.w;
+    PScope ps(d, P_NORM_F, 0, 2.0 * d->es * z.numel(), 3);
     CK(bn_forward(d->dt, z.p, d->bnp(n.pg), d->bnp(n.pb), a.p, n.mean, n.invstd, rows, n.C, d->cfg.eps, n.act,
                   n.slope, d->ws, d->ctx->stream));
 }
@@ -360,6 +410,7 @@ void norm_fwd(sdb_det* d, const NormL& n, const Act& z, const Act& a) {
 // dz from da for a norm layer; y = a (stored output), x = z (pre-norm, mode 0 only)
 void norm_bwd(sdb_det* d, const NormL& n, const Act& z, const Act& a, const void* da, void* dz) {
     const int64_t rows = static_cast<int64_t>(z.n) * z.h * z.w;
+    PScope ps(d, P_NORM_B, 0, 3.0 * d->es * z.numel(), 3);
     if (d->cfg.mode == 0) {
         CK(bn_backward(d->dt, da, z.p, n.act == 1 ? a.p : nullptr, d->bnp(n.pg), n.mean, n.invstd, dz,
                        d->bngp(n.pg), d->bngp(n.pb), rows, n.C, d->ws, d->ctx->stream));
@@ -382,10 +433,16 @@ void block_fwd(sdb_det* d, Block& b) {
         norm_fwd(d, b.nd, b.zd, b.d);
         sc = &b.d;
     }
+    PScope ps(d, P_ELEM, 0, 3.0 * d->es * b.out.numel());
     CK(add_act(d->dt, b.b3.p, sc->p, b.out.p, b.out.numel(), d->cfg.mode == 0 ? 1 : 2, d->cfg.slope, d->ctx->stream));
 }
 
 // ------------------------------------------------------------------ backward helpers
+void dgrad(sdb_det* d, const ConvL& c, const void* dy, void* dx, int accumulate) {
+    PScope ps(d, P_DGRAD, conv_flops(c.g), 0, c.g.stride * c.g.stride);
+    CK(conv_dgrad(c.g, d->dt, dy, d->wdev_ptr(c.p), dx, accumulate, d->ctx->stream));
+}
+
 struct Bwd {
     sdb_det* d;
     int64_t issued_lo;  // lowest g offset whose bucket has been issued
@@ -399,6 +456,7 @@ void grads_ready(Bwd& B, int pi) {
     while (B.next_bucket < d->buckets.size() && off <= d->buckets[B.next_bucket].first) {
         const auto [lo, hi] = d->buckets[B.next_bucket];
         cudaEvent_t ev = d->bucket_ev[B.next_bucket];
+        PScope ps(d, P_COMM, 0, static_cast<double>(hi - lo) * d->es);
         CK(cudaEventRecord(ev, d->ctx->stream));
         CK(cudaStreamWaitEvent(d->comm, ev, 0));
         CK(comm_allreduce_sum(d->ctx, static_cast<uint8_t*>(d->g) + lo * d->es, hi - lo, d->dt, d->comm));
@@ -408,7 +466,10 @@ void grads_ready(Bwd& B, int pi) {
 
 void conv_wgrad_to(Bwd& B, const ConvL& c, const Act& x, const void* dy) {
     sdb_det* d = B.d;
+    {
+    PScope ps(d, P_WGRAD, conv_flops(c.g), 0, 2);
     CK(conv_wgrad(c.g, d->dt, x.p, dy, d->gptr(c.p), d->ws, d->ws_bytes, d->ctx->stream));
+    }
     grads_ready(B, c.p);
 }
 
@@ -420,24 +481,28 @@ void block_bwd(Bwd& B, Block& b, void* dout, void* dx, void* s0, void* s1, void*
     const float neg = d->cfg.mode == 0 ? 0.0f : d->cfg.slope;
     // add + activation: dS = act'(out) * dout   (rounded at the add node)
     void* dS = s0;
-    CK(act_bwd(d->dt, dout, b.out.p, dS, b.out.numel(), neg, st));
+    {
+        PScope ps(d, P_ELEM, 0, 3.0 * d->es * b.out.numel());
+        CK(act_bwd(d->dt, dout, b.out.p, dS, b.out.numel(), neg, st));
+    }
     // shortcut first (its params come last in the block's pack order)
     if (b.has_down) {
         norm_bwd(d, b.nd, b.zd, b.d, dS, s1);
         conv_wgrad_to(B, b.down, b.in, s1);
-        CK(conv_dgrad(b.down.g, d->dt, s1, d->wdev_ptr(b.down.p), dx, 0, st));
+        dgrad(d, b.down, s1, dx, 0);
     } else {
+        PScope ps(d, P_ELEM, 0, 2.0 * d->es * b.in.numel(), 0);
         CK(cudaMemcpyAsync(dx, dS, b.in.numel() * d->es, cudaMemcpyDeviceToDevice, st));
     }
     norm_bwd(d, b.n3, b.z3, b.b3, dS, s1);
     conv_wgrad_to(B, b.c3, b.a2, s1);
-    CK(conv_dgrad(b.c3.g, d->dt, s1, d->wdev_ptr(b.c3.p), s2, 0, st));
+    dgrad(d, b.c3, s1, s2, 0);
     norm_bwd(d, b.n2, b.z2, b.a2, s2, s1);
     conv_wgrad_to(B, b.c2, b.a1, s1);
-    CK(conv_dgrad(b.c2.g, d->dt, s1, d->wdev_ptr(b.c2.p), s2, 0, st));
+    dgrad(d, b.c2, s1, s2, 0);
     norm_bwd(d, b.n1, b.z1, b.a1, s2, s1);
     conv_wgrad_to(B, b.c1, b.in, s1);
-    CK(conv_dgrad(b.c1.g, d->dt, s1, d->wdev_ptr(b.c1.p), dx, 1, st));
+    dgrad(d, b.c1, s1, dx, 1);
 }
 
 // ------------------------------------------------------------------ the step
@@ -447,12 +512,14 @@ void run_step(sdb_det* d) {
     // ---- forward: backbone
     conv_fwd(d, d->stem, d->img, d->stem_z);
     norm_fwd(d, d->stem_n, d->stem_z, d->stem_a);
+    { PScope ps(d, P_POOL, 0, d->es * (d->stem_a.numel() + d->pool.numel()));
     CK(maxpool_fwd(d->dt, d->stem_a.p, d->stem_a.n, d->stem_a.h, d->stem_a.w, d->stem_a.c, 3, 2, 1, d->pool.p,
-                   d->pool_arg, st));
+                   d->pool_arg, st)); }
     for (auto& b : d->backbone) block_fwd(d, b);
     // ---- RPN head
     conv_fwd(d, d->rpn_conv, d->c4, d->rpn_z);
-    CK(relu_fwd(d->dt, d->rpn_z.p, d->rpn_a.p, d->rpn_a.numel(), st));
+    { PScope ps(d, P_ELEM, 0, 2.0 * d->es * d->rpn_z.numel());
+    CK(relu_fwd(d->dt, d->rpn_z.p, d->rpn_a.p, d->rpn_a.numel(), st)); }
     conv_fwd(d, d->rpn_cls, d->rpn_a, d->rpn_logits);
     conv_fwd(d, d->rpn_bbox, d->rpn_a, d->rpn_deltas);
     // ---- targets and proposals (no gradient)
@@ -461,14 +528,14 @@ void run_step(sdb_det* d) {
     at.gt_count = d->gt_count; at.img_h = static_cast<float>(cf.img_h); at.img_w = static_cast<float>(cf.img_w);
     at.keys = d->keys; at.fg_thr = cf.rpn_fg_thr; at.bg_thr = cf.rpn_bg_thr; at.batch = cf.rpn_batch;
     at.fg_cap = static_cast<int>(cf.rpn_fg_frac * cf.rpn_batch); at.labels = d->a_labels; at.targets = d->a_targets;
-    CK(anchor_targets(at, d->ws, st));
+    { PScope ps(d, P_TARGETS, 0, 0, 5); CK(anchor_targets(at, d->ws, st)); }
     ProposalArgs pa{};
     pa.logits = d->rpn_logits.p; pa.deltas = d->rpn_deltas.p; pa.dtype = d->dt; pa.anchors = d->anchors;
     pa.n_img = cf.batch; pa.n_loc = d->n_loc; pa.A = d->A; pa.A_pad = d->A_pad; pa.pre_k = cf.pre_nms;
     pa.post_k = cf.post_nms; pa.iou_thr = cf.nms_iou; pa.img_h = static_cast<float>(cf.img_h);
     pa.img_w = static_cast<float>(cf.img_w); pa.clip_dw = static_cast<float>(std::log(1000.0 / 16.0));
     pa.rois = d->props; pa.roi_scores = nullptr; pa.keep_pos = d->keep_pos; pa.count = d->prop_count;
-    CK(rpn_proposals(pa, d->ws, st));
+    { PScope ps(d, P_PROPOSAL, 0, 0, 3); CK(rpn_proposals(pa, d->ws, st)); }
     ProposalTargetArgs pt{};
     pt.proposals = d->props; pt.prop_stride = cf.post_nms; pt.prop_count = d->prop_count; pt.gt = d->gt;
     pt.gt_cls = d->gt_cls; pt.gt_stride = cf.max_gt; pt.gt_count = d->gt_count; pt.keys = d->keys + cf.batch;
@@ -477,19 +544,22 @@ void run_step(sdb_det* d) {
     pt.work_flag = d->pt_flag; pt.work_arg = d->pt_arg; pt.work_stride = cf.post_nms + cf.max_gt;
     pt.out_rois = d->rois; pt.out_labels = d->roi_labels; pt.out_targets = d->roi_targets; pt.out_src = nullptr;
     pt.out_count = d->roi_count;
-    CK(proposal_targets(pt, st));
+    { PScope ps(d, P_TARGETS, 0, 0, 1); CK(proposal_targets(pt, st)); }
     // ---- RoI head
     const float sscale = 1.0f / 16.0f;
+    { PScope ps(d, P_ROI_F, 0, static_cast<double>(d->es) * (d->roi_feat.numel() + d->c4.numel()));
     CK(roialign_fwd(d->dt, d->c4.p, d->c4.n, d->c4.h, d->c4.w, d->c4.c, d->rois, d->R, d->P, sscale,
-                    cf.sampling_ratio, d->roi_feat.p, st));
+                    cf.sampling_ratio, d->roi_feat.p, st)); }
     for (auto& b : d->head) block_fwd(d, b);
-    CK(avgpool_fwd(d->dt, d->head_out.p, d->R, d->head_out.h * d->head_out.w, d->feat_c, d->pooled.p, st));
+    { PScope ps(d, P_POOL, 0, static_cast<double>(d->es) * d->head_out.numel());
+    CK(avgpool_fwd(d->dt, d->head_out.p, d->R, d->head_out.h * d->head_out.w, d->feat_c, d->pooled.p, st)); }
     conv_fwd(d, d->fc_cls, d->pooled, d->cls_logits);
     conv_fwd(d, d->fc_bbox, d->pooled, d->bbox_pred);
     // ---- losses (scale folded into backward)
     CK(cudaMemcpyAsync(d->scale_used, d->scale, 8, cudaMemcpyDeviceToDevice, st));
     void* g0 = d->d_cls;
     void* g1 = d->d_bbox;
+    PScope ps_loss(d, P_LOSS, 0, 0, 4);
     LossArgs la{d->scale, d->losses, 0};
     CK(sigmoid_bce(d->dt, d->rpn_logits.p, static_cast<int64_t>(d->n_loc) * cf.batch, d->A, d->A_pad, d->a_labels,
                    d->d_rpn_logits, la, nullptr, st));
@@ -508,12 +578,13 @@ void run_step(sdb_det* d) {
     // fc layers (bbox then cls: reverse pack order)
     void* dpool = d->gbuf[2];
     conv_wgrad_to(B, d->fc_bbox, d->pooled, g1);
-    CK(conv_dgrad(d->fc_bbox.g, d->dt, g1, d->wdev_ptr(d->fc_bbox.p), dpool, 0, st));
+    dgrad(d, d->fc_bbox, g1, dpool, 0);
     conv_wgrad_to(B, d->fc_cls, d->pooled, g0);
-    CK(conv_dgrad(d->fc_cls.g, d->dt, g0, d->wdev_ptr(d->fc_cls.p), dpool, 1, st));
+    dgrad(d, d->fc_cls, g0, dpool, 1);
     // avgpool, then the res5 head
     void* dhead = d->gbuf[3];
-    CK(avgpool_bwd(d->dt, dpool, d->R, d->head_out.h * d->head_out.w, d->feat_c, dhead, st));
+    { PScope ps(d, P_POOL, 0, static_cast<double>(d->es) * d->head_out.numel());
+    CK(avgpool_bwd(d->dt, dpool, d->R, d->head_out.h * d->head_out.w, d->feat_c, dhead, st)); }
     void* cur = dhead;
     void* spare = d->gbuf[2];
     for (int i = static_cast<int>(d->head.size()) - 1; i >= 0; --i) {
@@ -523,17 +594,19 @@ void run_step(sdb_det* d) {
     (void)spare;
     // cur = d roi_feat
     void* dc4 = d->gbuf[(cur == d->gbuf[2]) ? 3 : 2];
+    { PScope ps(d, P_ROI_B, 0, static_cast<double>(d->es) * (d->roi_feat.numel() + d->c4.numel()));
     CK(roialign_bwd(d->dt, cur, d->c4.n, d->c4.h, d->c4.w, d->c4.c, d->rois, d->R, d->P, sscale, cf.sampling_ratio,
-                    dc4, st));
+                    dc4, st)); }
     // RPN head backward (bbox, cls, conv)
     void* drpn = d->gbuf[0];
     conv_wgrad_to(B, d->rpn_bbox, d->rpn_a, d->d_rpn_deltas);
-    CK(conv_dgrad(d->rpn_bbox.g, d->dt, d->d_rpn_deltas, d->wdev_ptr(d->rpn_bbox.p), drpn, 0, st));
+    dgrad(d, d->rpn_bbox, d->d_rpn_deltas, drpn, 0);
     conv_wgrad_to(B, d->rpn_cls, d->rpn_a, d->d_rpn_logits);
-    CK(conv_dgrad(d->rpn_cls.g, d->dt, d->d_rpn_logits, d->wdev_ptr(d->rpn_cls.p), drpn, 1, st));
-    CK(act_bwd(d->dt, drpn, d->rpn_a.p, drpn, d->rpn_a.numel(), 0.0f, st));
+    dgrad(d, d->rpn_cls, d->d_rpn_logits, drpn, 1);
+    { PScope ps(d, P_ELEM, 0, 3.0 * d->es * d->rpn_a.numel());
+    CK(act_bwd(d->dt, drpn, d->rpn_a.p, drpn, d->rpn_a.numel(), 0.0f, st)); }
     conv_wgrad_to(B, d->rpn_conv, d->c4, drpn);
-    CK(conv_dgrad(d->rpn_conv.g, d->dt, drpn, d->wdev_ptr(d->rpn_conv.p), dc4, 1, st));
+    dgrad(d, d->rpn_conv, drpn, dc4, 1);
     // backbone
     cur = dc4;
     spare = dc4 == d->gbuf[2] ? d->gbuf[3] : d->gbuf[2];
@@ -542,7 +615,8 @@ void run_step(sdb_det* d) {
         std::swap(cur, spare);
     }
     // maxpool, stem norm, stem wgrad (the image gradient is not needed)
-    CK(maxpool_bwd(d->dt, cur, d->pool_arg, d->stem_a.n, d->stem_a.h, d->stem_a.w, d->stem_a.c, 3, 2, 1, spare, st));
+    { PScope ps(d, P_POOL, 0, d->es * (2.0 * d->stem_a.numel() + d->pool.numel()));
+    CK(maxpool_bwd(d->dt, cur, d->pool_arg, d->stem_a.n, d->stem_a.h, d->stem_a.w, d->stem_a.c, 3, 2, 1, spare, st)); }
     norm_bwd(d, d->stem_n, d->stem_z, d->stem_a, spare, d->gbuf[0]);
     conv_wgrad_to(B, d->stem, d->img, d->gbuf[0]);
 
@@ -556,6 +630,7 @@ void run_step(sdb_det* d) {
         CK(cudaEventRecord(d->ev_join, d->comm));
         CK(cudaStreamWaitEvent(st, d->ev_join, 0));
     }
+    PScope ps_opt(d, P_OPTIM, 0, (d->es + 12.0 + (d->dt == kF16 ? 2.0 : 0.0)) * d->n_w + 16.0 * d->n_bn, 5);
     CK(cudaMemsetAsync(d->flag, 0, sizeof(int), st));
     CK(nonfinite_check(d->dt, d->g, d->n_w, d->flag, st));
     CK(nonfinite_check(kF32, d->bng, d->n_bn, d->flag, st));
@@ -1012,6 +1087,38 @@ int sdb_det_dims(sdb_det* d, int* fh, int* fw, int* A, int* A_pad) {
     if (fw) *fw = d->fw;
     if (A) *A = d->A;
     if (A_pad) *A_pad = d->A_pad;
+    return SDB_OK;
+}
+
+int sdb_det_profile(sdb_det* d, double* ms, double* flops, double* bytes, int64_t* launches, int ncat) {
+    try {
+        Prof& p = d->prof;
+        p.used = 0;
+        p.recs.clear();
+        std::fill(p.flops, p.flops + P_NCAT, 0.0);
+        std::fill(p.bytes, p.bytes + P_NCAT, 0.0);
+        std::fill(p.launches, p.launches + P_NCAT, 0);
+        p.on = true;
+        run_step(d);
+        p.on = false;
+        CK(cudaStreamSynchronize(d->ctx->stream));
+        std::vector<double> acc(P_NCAT, 0.0);
+        for (auto& r : p.recs) {
+            float t = 0;
+            CK(cudaEventElapsedTime(&t, r.second.first, r.second.second));
+            acc[r.first] += t;
+        }
+        for (int i = 0; i < ncat && i < P_NCAT; ++i) {
+            if (ms) ms[i] = acc[i];
+            if (flops) flops[i] = p.flops[i];
+            if (bytes) bytes[i] = p.bytes[i];
+            if (launches) launches[i] = p.launches[i];
+        }
+        ++d->steps_done;
+    } catch (const std::exception& e) {
+        d->prof.on = false;
+        return det_fail(SDB_CUDA, e.what());
+    }
     return SDB_OK;
 }
 

@@ -119,6 +119,7 @@ _SIGS = {
     "sdb_det_export": [_P, _I, _P, _L, C.POINTER(_L)],
     "sdb_det_dims": [_P, C.POINTER(_I), C.POINTER(_I), C.POINTER(_I), C.POINTER(_I)],
     "sdb_det_kernel_launches": [_P, C.POINTER(_L)],
+    "sdb_det_profile": [_P, _P, _P, _P, _P, _I],
     "sdb_ctx_create": [_I, _I, _I, _P, C.POINTER(_P)],
     "sdb_ctx_destroy": [_P],
     "sdb_get_nccl_unique_id": [_P],
@@ -265,6 +266,17 @@ class Detector:
         buf = np.zeros(n.value, np.uint8)
         check(L().sdb_det_export(self.h, what, buf.ctypes.data_as(_P), n.value, C.byref(n)))
         return buf.view(dtype)
+
+    PROFILE_CATS = ["conv_fprop", "conv_dgrad", "conv_wgrad", "norm_fwd", "norm_bwd", "elementwise", "pooling",
+                    "targets", "proposal", "roialign_fwd", "roialign_bwd", "losses", "optimizer", "comm"]
+
+    def profile(self):
+        """one eager CUDA-event-instrumented step: {category: (ms, flops, bytes, launches)}"""
+        n = len(self.PROFILE_CATS)
+        ms, fl, by = (_D * n)(), (_D * n)(), (_D * n)()
+        la = (_L * n)()
+        check(L().sdb_det_profile(self.h, ms, fl, by, la, n))
+        return {c: (ms[i], fl[i], by[i], la[i]) for i, c in enumerate(self.PROFILE_CATS)}
 
     def kernel_launches(self) -> int:
         n = _L()
