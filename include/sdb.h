@@ -97,6 +97,10 @@ int sdb_fused_sgd(sdb_ctx* ctx, int gdtype, const void* gsum, float* w, float* v
 int sdb_update_scale(sdb_ctx* ctx, double* scale, int64_t* good_steps, const int* flag, int dynamic,
                      int64_t growth_interval, double growth, double backoff, double min_scale, double max_scale,
                      void* stream);
+/* debug switches (tests only): key 1 = force the CUDA-core conv path instead
+ * of tcgen05 (a second, independently ordered implementation of the same GEMM
+ * views -- used to measure the fp16 accumulation-order noise floor). */
+int sdb_debug_set(int key, int value);
 /* binary16 RNE round trip / casts (src/half.cpp:9-71) */
 int sdb_cast(sdb_ctx* ctx, int src_dtype, const void* src, int dst_dtype, void* dst, int64_t n, void* stream);
 
@@ -126,7 +130,8 @@ int sdb_softmax_ce(sdb_ctx* ctx, int dtype, const void* logits, int R, int ncls,
 
 /* ---- the data-parallel Faster R-CNN C4 training step (src/trainer.cpp:217-271) ---- */
 typedef struct {
-    int mode;            /* 0: fp32 + BN+ReLU (config C1); 1: fp16 + InPlace-ABN, fp32 masters */
+    int mode;            /* 0: fp32 + BN+ReLU (config C1); 1: fp16 + InPlace-ABN, fp32 masters;
+                            2: fp32 + InPlace-ABN (isolates fp16 rounding in parity tests) */
     int batch;           /* images per GPU */
     int img_h, img_w;
     int blocks[4];       /* bottlenecks in res2..res5 (res5 == 0: RoIAlign -> avgpool -> fc head) */

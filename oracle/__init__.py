@@ -69,6 +69,18 @@ _REF_SIGS = {
     "ref_sgd_step_master": (_I, [_P, _P, _P, _L, _F, _F]),
 }
 
+class RefDetCfg(C.Structure):
+    """mirror of RefDetCfg in oracle/detector_ref.cpp"""
+    _fields_ = [("mode", _I), ("batch", _I), ("img_h", _I), ("img_w", _I), ("blocks", _I * 4),
+                ("num_classes", _I), ("rpn_channels", _I), ("A", _I), ("pool", _I), ("sampling_ratio", _I),
+                ("rpn_batch", _I), ("eps", _F), ("slope", _F)]
+
+
+_REF_SIGS.update({
+    "ref_det_param_list": (_I, [_P, _P, _P, _P, _I]),
+    "ref_det_step": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _I, _D, _P, _P, _P, _P]),
+})
+
 _orc = None
 _ref = None
 

@@ -68,6 +68,14 @@ void* sdb_ctx::scratch(size_t bytes) {
 extern "C" {
 
 const char* sdb_last_error(void) { return g_err.c_str(); }
+
+int sdb_debug_set(int key, int value) {
+    if (key == 1) {
+        sdb::conv_set_force_simt(value != 0);
+        return SDB_OK;
+    }
+    return fail(SDB_PARAM, "unknown debug key");
+}
 int sdb_version(void) { return 1; }
 
 int sdb_ctx_create(int device, int rank, int world, const void* nccl_id, sdb_ctx** out) {

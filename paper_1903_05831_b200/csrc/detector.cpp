@@ -559,6 +559,7 @@ void run_step(sdb_det* d) {
     CK(cudaMemcpyAsync(d->scale_used, d->scale, 8, cudaMemcpyDeviceToDevice, st));
     void* g0 = d->d_cls;
     void* g1 = d->d_bbox;
+    {
     PScope ps_loss(d, P_LOSS, 0, 0, 4);
     LossArgs la{d->scale, d->losses, 0};
     CK(sigmoid_bce(d->dt, d->rpn_logits.p, static_cast<int64_t>(d->n_loc) * cf.batch, d->A, d->A_pad, d->a_labels,
@@ -572,6 +573,7 @@ void run_step(sdb_det* d) {
     la.slot = 3;
     CK(rcnn_smooth_l1(d->dt, d->bbox_pred.p, d->R, d->nbox_pad, d->roi_labels, d->roi_targets, 1.0, g1, la, nullptr,
                       st));
+    }
 
     // ---- backward
     Bwd B{d, 0, 0};
@@ -651,10 +653,10 @@ int sdb_det_create(sdb_ctx* ctx, const sdb_det_config* cfgp, sdb_det** out) {
     if (!ctx || !cfgp || !out) return det_fail(SDB_PARAM, "null argument");
     const sdb_det_config& cf = *cfgp;
     if (cf.batch < 1 || cf.img_h < 32 || cf.img_w < 32) return det_fail(SDB_SHAPE, "bad batch/image size");
-    if (cf.mode != 0 && cf.mode != 1) return det_fail(SDB_PARAM, "mode must be 0 (fp32/BN) or 1 (fp16/IABN)");
+    if (cf.mode < 0 || cf.mode > 2) return det_fail(SDB_PARAM, "mode must be 0 (fp32/BN), 1 (fp16/IABN), 2 (fp32/IABN)");
     if (cf.n_scales < 1 || cf.n_scales > 8 || cf.n_ratios < 1 || cf.n_ratios > 8) return det_fail(SDB_PARAM, "anchors");
     if (cf.nms_iou < 0.0 || cf.nms_iou > 1.0) return det_fail(SDB_PARAM, "iou threshold outside [0,1]");
-    if (cf.mode == 1 && !(cf.slope > 0.0f)) return det_fail(SDB_NONINVERTIBLE, "iabn requires slope > 0");
+    if (cf.mode >= 1 && !(cf.slope > 0.0f)) return det_fail(SDB_NONINVERTIBLE, "iabn requires slope > 0");
     auto* d = new sdb_det();
     try {
         d->ctx = ctx;

@@ -1,0 +1,173 @@
+"""End-to-end parity of the libsdb Faster R-CNN C4 training step against the
+oracle (reference Tape + restated detection ops), through the C ABI.
+
+Bars (BASELINE.json north star):
+  * bit-exact anchor labels, top-k/NMS proposals and sampled RoIs (every step);
+  * losses within 1e-3 relative (fp32) / 1e-2 (fp16); RPN outputs likewise;
+  * per-step parameter deltas within 1e-2 relative, per tensor, over 10 steps
+    in fp32 (C1 = BN+ReLU, and the C2 graph in fp32 = IABN, mode 2);
+  * fp16 (C2): the reference's own fp16 contract rounds every gradient to
+    binary16, which by itself moves per-tensor gradients by up to ~10% versus
+    the same graph in fp32 (several BN beta gradients are exact zeros in real
+    arithmetic -- e.g. bn2 beta, because a 1x1 conv followed by BN backward sums
+    to zero per channel -- so what remains is pure rounding noise).  The fp16
+    gradient bar is therefore measured, not assumed: per tensor,
+        err(GPU16, ref16) <= max(1e-2, 1.5 * err(ref16, ref32))
+    on the same weights, inputs and targets, with the global (all-parameter)
+    step delta held to the same rule.  DESIGN.md ("fp16 noise floor") has the
+    numbers.
+Sizes are reduced where the single-threaded CPU oracle would take minutes
+(C2 runs 10 steps at 128x128; C1 one step at its full 256x256)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import p as ptr
+from tests import det_parity as dp
+from tests.util import norm_rel
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def _step(det, slots):
+    det.feed(slots)
+    det.step()
+    losses, scale, ov = det.losses()
+    assert ov == 0
+    s = dp.gpu_state(det)
+    dp.check_discrete(det, s, slots)
+    return losses, scale, s
+
+
+def _losses_close(lg, lr, tol):
+    for i in range(4):
+        rel = abs(lg[i] - lr[i]) / max(abs(lr[i]), 1e-12)
+        assert rel <= tol, (i, lg[i], lr[i], rel)
+
+
+def test_c1_one_step_fp32(ref, orc):
+    from paper_1903_05831_b200 import detector as D
+    det = D.Detector(D.preset("c1"))
+    cfg = dp.ref_cfg(det)
+    dp.check_param_order(det, cfg)
+    w0 = dp.flat_params(det)
+    slots = D.batch_slots(1, 0, 1, det.p.batch)
+    lg, scale, s = _step(det, slots)
+    lr, g_ref, lg_ref, dl_ref = dp.oracle_step(det, cfg, w0, s, scale)
+    _losses_close(lg, lr, 1e-3)
+    A = det.A
+    assert norm_rel(s["logits"][..., :A].transpose(0, 3, 1, 2), lg_ref) <= 1e-3
+    g = dp.flat_grads(det)
+    for (name, _, _), a, b in zip(det.params, dp.split(det, g), dp.split(det, g_ref)):
+        assert norm_rel(a, b) <= 1e-3, (name, norm_rel(a, b))
+    w_ref, v_ref = w0.copy(), np.zeros_like(w0)
+    orc.orc_apply_sgd(ptr(w_ref), ptr(v_ref), ptr(g_ref), w0.size, det.p.lr, det.p.momentum, scale)
+    w1 = dp.flat_params(det)
+    for (name, _, _), a, b in zip(det.params, dp.split(det, w1 - w0), dp.split(det, w_ref - w0)):
+        assert norm_rel(a, b) <= 1e-3, (name, norm_rel(a, b))
+    det.close()
+
+
+def test_c2_graph_fp32_ten_steps(ref, orc):
+    """the C2 network (InPlace-ABN everywhere) in fp32: 10 independent-trajectory steps"""
+    from paper_1903_05831_b200 import detector as D
+    det = D.Detector(D.preset("c2", img_h=128, img_w=128, mode=2, scale_init=1.0))
+    cfg = dp.ref_cfg(det)
+    w_ref = dp.flat_params(det)
+    v_ref = np.zeros_like(w_ref)
+    for step in range(1, 11):
+        slots = D.batch_slots(step, 0, 1, det.p.batch)
+        w_gpu0 = dp.flat_params(det)
+        lg, scale, s = _step(det, slots)
+        lr, g_ref, _, _ = dp.oracle_step(det, cfg, w_ref, s, scale)
+        _losses_close(lg, lr, 1e-3)
+        w_ref0 = w_ref.copy()
+        orc.orc_apply_sgd(ptr(w_ref), ptr(v_ref), ptr(g_ref), w_ref.size, det.p.lr, det.p.momentum, scale)
+        w_gpu1 = dp.flat_params(det)
+        for (name, _, _), a, b in zip(det.params, dp.split(det, w_gpu1 - w_gpu0), dp.split(det, w_ref - w_ref0)):
+            assert norm_rel(a, b) <= 1e-2, (step, name, norm_rel(a, b))
+    det.close()
+
+
+def _ref16_vs_ref32(det, cfg16, w, s, scale):
+    """the reference's own fp16-rounding deviation on this step (same inputs/targets)"""
+    cfg32 = dp.ref_cfg(det)
+    cfg32.mode = 2
+    _, g16, _, _ = dp.oracle_step(det, cfg16, w, s, scale)
+    _, g32, _, _ = dp.oracle_step(det, cfg32, w, s, scale)
+    return g16, g32
+
+
+def test_c2_fp16_ten_steps(ref, orc):
+    from paper_1903_05831_b200 import detector as D
+    det = D.Detector(D.preset("c2", img_h=128, img_w=128))
+    cfg = dp.ref_cfg(det)
+    dp.check_param_order(det, cfg)
+    w_ref = dp.flat_params(det)
+    v_ref = np.zeros_like(w_ref)
+    for step in range(1, 11):
+        slots = D.batch_slots(step, 0, 1, det.p.batch)
+        w_gpu0 = dp.flat_params(det)
+        lg, scale, s = _step(det, slots)
+        assert scale == 128.0  # static loss scale (config C2)
+        lr, g16, lg_ref, dl_ref = dp.oracle_step(det, cfg, w_ref, s, scale)
+        _losses_close(lg, lr, 1e-2)
+        assert norm_rel(s["logits"][..., :det.A].astype(np.float32).transpose(0, 3, 1, 2), lg_ref) <= 1e-2
+        g16b, g32 = _ref16_vs_ref32(det, cfg, w_ref, s, scale)
+        assert np.array_equal(g16, g16b)  # the oracle is deterministic
+        g = dp.flat_grads(det)
+        for (name, _, _), a, b, c in zip(det.params, dp.split(det, g), dp.split(det, g16), dp.split(det, g32)):
+            floor = norm_rel(b, c)
+            assert norm_rel(a, b) <= max(1e-2, 1.5 * floor), (step, name, norm_rel(a, b), floor)
+        assert norm_rel(g, g16) <= max(1e-2, 1.5 * norm_rel(g16, g32))
+        w_ref0 = w_ref.copy()
+        assert orc.orc_has_nonfinite(ptr(g16), g16.size) == 0
+        orc.orc_apply_sgd(ptr(w_ref), ptr(v_ref), ptr(g16), w_ref.size, det.p.lr, det.p.momentum, scale)
+        w_gpu1 = dp.flat_params(det)
+        dg, dr = w_gpu1 - w_gpu0, w_ref - w_ref0
+        assert norm_rel(dg, dr) <= max(1e-2, 1.5 * norm_rel(g16, g32)), (step, norm_rel(dg, dr))
+    det.close()
+
+
+def test_step_is_deterministic():
+    """two identical runs produce bit-identical weights (atomics-free kernels)"""
+    from paper_1903_05831_b200 import detector as D
+    ws = []
+    for _ in range(2):
+        det = D.Detector(D.preset("c2", img_h=128, img_w=128))
+        for step in range(1, 4):
+            det.feed(D.batch_slots(step, 0, 1, 2))
+            det.step()
+        det.losses()
+        ws.append(dp.flat_params(det))
+        det.close()
+    assert np.array_equal(ws[0].view(np.uint32), ws[1].view(np.uint32))
+
+
+def test_injected_overflow_skips_step_and_backs_off():
+    """tests/test_trainer.cpp:292-321 analogue: a non-finite gradient skips the
+    update and halves a dynamic scale (src/trainer.cpp:238,252-257)."""
+    from paper_1903_05831_b200 import detector as D
+    det = D.Detector(D.preset("c2", img_h=128, img_w=128, dynamic_scale=1, scale_init=2.0**15))
+    det.feed(D.batch_slots(1, 0, 1, 2))
+    det.step()
+    _, sc1, ov1 = det.losses()
+    assert ov1 == 0 and sc1 == 2.0**15
+    # poison one weight -> the forward produces inf/nan -> every gradient non-finite
+    w = det.get_param(0)
+    w_bad = w.copy()
+    w_bad.flat[0] = np.inf
+    det.set_param(0, w_bad)
+    before = dp.flat_params(det)
+    det.feed(D.batch_slots(2, 0, 1, 2))
+    det.step()
+    _, sc2, ov2 = det.losses()
+    assert ov2 == 1 and sc2 == 2.0**15
+    after = dp.flat_params(det)
+    assert np.array_equal(np.nan_to_num(before), np.nan_to_num(after))  # untouched
+    state = det.export(12, np.uint8)
+    assert state[:8].view(np.float64)[0] == 2.0**14  # halved for the next step
+    det.close()
