@@ -167,6 +167,8 @@ int sdb_det_param_info(sdb_det* det, int idx, char* name, int name_len, int64_t*
 int sdb_det_get_param(sdb_det* det, int idx, float* host);  /* fp32 master, reference layout */
 int sdb_det_set_param(sdb_det* det, int idx, const float* host);
 int sdb_det_get_grad(sdb_det* det, int idx, float* host);   /* last step's summed gradient (scaled) */
+int sdb_det_get_velocity(sdb_det* det, int idx, float* host);       /* SGD momentum buffer */
+int sdb_det_set_velocity(sdb_det* det, int idx, const float* host);
 /* feed one batch: images NHWC with C padded to 8 (dtype of the mode), on host
  * (pinned, copied H2D on the step stream) or device; GT arrays on host
  * ([batch][max_gt][4], [batch][max_gt], [batch]); slots = global batch slots

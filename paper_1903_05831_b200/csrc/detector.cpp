@@ -873,15 +873,16 @@ int sdb_det_param_info(sdb_det* d, int idx, char* name, int name_len, int64_t* s
     return SDB_OK;
 }
 
-static int param_xfer(sdb_det* d, int idx, float* host, int which /*0 get w, 1 set w, 2 get grad*/) {
+// which: 0 get w, 1 set w, 2 get grad, 3 get velocity, 4 set velocity
+static int param_xfer(sdb_det* d, int idx, float* host, int which) {
     if (idx < 0 || idx >= static_cast<int>(d->params.size())) return det_fail(SDB_PARAM, "param index");
     const Param& p = d->params[idx];
     cudaStream_t st = d->ctx->stream;
     try {
         CK(cudaStreamSynchronize(st));
         if (p.kind >= 2) {
-            float* src = (which == 2 ? d->bng : d->bn32) + p.off;
-            if (which == 1) CK(cudaMemcpy(src, host, p.numel * 4, cudaMemcpyHostToDevice));
+            float* src = (which == 2 ? d->bng : (which >= 3 ? d->bnv : d->bn32)) + p.off;
+            if (which == 1 || which == 4) CK(cudaMemcpy(src, host, p.numel * 4, cudaMemcpyHostToDevice));
             else CK(cudaMemcpy(host, src, p.numel * 4, cudaMemcpyDeviceToHost));
             return SDB_OK;
         }
@@ -895,7 +896,8 @@ static int param_xfer(sdb_det* d, int idx, float* host, int which /*0 get w, 1 s
                 CK(cudaMemcpy(dev.data(), d->gptr(idx), p.numel * 4, cudaMemcpyDeviceToHost));
             }
         } else {
-            CK(cudaMemcpy(dev.data(), d->wptr(idx), p.numel * 4, cudaMemcpyDeviceToHost));
+            const float* src = which >= 3 ? d->v32 + p.off : d->wptr(idx);
+            CK(cudaMemcpy(dev.data(), src, p.numel * 4, cudaMemcpyDeviceToHost));
         }
         int64_t n = 1;
         for (int64_t s : p.ref_shape) n *= s;
@@ -914,10 +916,10 @@ static int param_xfer(sdb_det* d, int idx, float* host, int which /*0 get w, 1 s
                     for (int64_t o = 0; o < outc; ++o) fn(i * outc + o, o * p.C + i);
             }
         };
-        if (which == 1) {
+        if (which == 1 || which == 4) {
             map([&](int64_t ri, int64_t di) { dev[di] = host[ri]; });
-            CK(cudaMemcpy(d->wptr(idx), dev.data(), p.numel * 4, cudaMemcpyHostToDevice));
-            if (d->dt == kF16) CK(cast_f32_f16(d->wptr(idx), static_cast<__half*>(d->wdev_ptr(idx)), p.numel, st));
+            CK(cudaMemcpy(which == 4 ? d->v32 + p.off : d->wptr(idx), dev.data(), p.numel * 4, cudaMemcpyHostToDevice));
+            if (which == 1 && d->dt == kF16) CK(cast_f32_f16(d->wptr(idx), static_cast<__half*>(d->wdev_ptr(idx)), p.numel, st));
             CK(cudaStreamSynchronize(st));
         } else {
             map([&](int64_t ri, int64_t di) { host[ri] = dev[di]; });
@@ -931,6 +933,10 @@ static int param_xfer(sdb_det* d, int idx, float* host, int which /*0 get w, 1 s
 int sdb_det_get_param(sdb_det* d, int idx, float* host) { return param_xfer(d, idx, host, 0); }
 int sdb_det_set_param(sdb_det* d, int idx, const float* host) { return param_xfer(d, idx, const_cast<float*>(host), 1); }
 int sdb_det_get_grad(sdb_det* d, int idx, float* host) { return param_xfer(d, idx, host, 2); }
+int sdb_det_get_velocity(sdb_det* d, int idx, float* host) { return param_xfer(d, idx, host, 3); }
+int sdb_det_set_velocity(sdb_det* d, int idx, const float* host) {
+    return param_xfer(d, idx, const_cast<float*>(host), 4);
+}
 
 static void stage_gt(sdb_det* d, const float* gt_boxes, const int32_t* gt_cls, const int32_t* gt_count,
                      const int64_t* slots) {

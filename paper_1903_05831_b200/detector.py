@@ -111,6 +111,8 @@ _SIGS = {
     "sdb_det_get_param": [_P, _I, _P],
     "sdb_det_set_param": [_P, _I, _P],
     "sdb_det_get_grad": [_P, _I, _P],
+    "sdb_det_get_velocity": [_P, _I, _P],
+    "sdb_det_set_velocity": [_P, _I, _P],
     "sdb_det_set_batch": [_P, _P, _I, _P, _P, _P, _P],
     "sdb_det_synth_images": [_P, _P],
     "sdb_det_step": [_P],
@@ -213,6 +215,12 @@ class Detector:
         _, shape, _ = self.params[i]
         out = np.zeros(shape, np.float32)
         check(L().sdb_det_get_grad(self.h, i, out.ctypes.data_as(_P)))
+        return out
+
+    def get_velocity(self, i) -> np.ndarray:
+        _, shape, _ = self.params[i]
+        out = np.zeros(shape, np.float32)
+        check(L().sdb_det_get_velocity(self.h, i, out.ctypes.data_as(_P)))
         return out
 
     def gt_batch(self, slots):

@@ -53,6 +53,10 @@ def flat_params(det):
     return np.concatenate([det.get_param(i).ravel() for i in range(det.n_tensors)]).astype(np.float32)
 
 
+def flat_velocity(det):
+    return np.concatenate([det.get_velocity(i).ravel() for i in range(det.n_tensors)]).astype(np.float32)
+
+
 def flat_grads(det):
     return np.concatenate([det.get_grad(i).ravel() for i in range(det.n_tensors)]).astype(np.float32)
 

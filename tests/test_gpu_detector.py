@@ -76,18 +76,17 @@ def test_c2_graph_fp32_ten_steps(ref, orc):
     from paper_1903_05831_b200 import detector as D
     det = D.Detector(D.preset("c2", img_h=128, img_w=128, mode=2, scale_init=1.0))
     cfg = dp.ref_cfg(det)
-    w_ref = dp.flat_params(det)
-    v_ref = np.zeros_like(w_ref)
     for step in range(1, 11):
+        # per-step comparison from the same state (weights + momentum)
         slots = D.batch_slots(step, 0, 1, det.p.batch)
-        w_gpu0 = dp.flat_params(det)
+        w_gpu0, v_ref = dp.flat_params(det), dp.flat_velocity(det)
+        w_ref = w_gpu0.copy()
         lg, scale, s = _step(det, slots)
         lr, g_ref, _, _ = dp.oracle_step(det, cfg, w_ref, s, scale)
         _losses_close(lg, lr, 1e-3)
-        w_ref0 = w_ref.copy()
         orc.orc_apply_sgd(ptr(w_ref), ptr(v_ref), ptr(g_ref), w_ref.size, det.p.lr, det.p.momentum, scale)
         w_gpu1 = dp.flat_params(det)
-        for (name, _, _), a, b in zip(det.params, dp.split(det, w_gpu1 - w_gpu0), dp.split(det, w_ref - w_ref0)):
+        for (name, _, _), a, b in zip(det.params, dp.split(det, w_gpu1 - w_gpu0), dp.split(det, w_ref - w_gpu0)):
             assert norm_rel(a, b) <= 1e-2, (step, name, norm_rel(a, b))
     det.close()
 
@@ -106,11 +105,10 @@ def test_c2_fp16_ten_steps(ref, orc):
     det = D.Detector(D.preset("c2", img_h=128, img_w=128))
     cfg = dp.ref_cfg(det)
     dp.check_param_order(det, cfg)
-    w_ref = dp.flat_params(det)
-    v_ref = np.zeros_like(w_ref)
     for step in range(1, 11):
         slots = D.batch_slots(step, 0, 1, det.p.batch)
-        w_gpu0 = dp.flat_params(det)
+        w_gpu0, v_ref = dp.flat_params(det), dp.flat_velocity(det)
+        w_ref = w_gpu0.copy()
         lg, scale, s = _step(det, slots)
         assert scale == 128.0  # static loss scale (config C2)
         lr, g16, lg_ref, dl_ref = dp.oracle_step(det, cfg, w_ref, s, scale)
