@@ -552,6 +552,19 @@ cudaError_t conv_dgrad(const ConvShape& g, int dtype, const void* dy, const void
     base.x = dy; base.w = w; base.out = dx; base.accumulate = accumulate;
     base.NG = g.C;
     const int sd = g.stride;
+    // phases whose taps are all empty (e.g. the odd pixels of a 1x1 stride-2
+    // conv) receive no gradient: zero the whole output once with a contiguous
+    // memset (or leave it untouched when accumulating)
+    bool empty_phase = false;
+    for (int ph = 0; ph < sd; ++ph)
+        for (int pw = 0; pw < sd; ++pw) {
+            const int r0 = (ph + g.pad) % sd, q0 = (pw + g.pad) % sd;
+            if (r0 >= g.R || q0 >= g.S) empty_phase = true;
+        }
+    if (empty_phase && !accumulate) {
+        const cudaError_t e = cudaMemsetAsync(dx, 0, static_cast<size_t>(g.N) * g.H * g.W * g.C * (dtype == kF16 ? 2 : 4), st);
+        if (e != cudaSuccess) return e;
+    }
     for (int ph = 0; ph < sd; ++ph)
         for (int pw = 0; pw < sd; ++pw) {
             ConvArgs a = base;
@@ -567,11 +580,7 @@ cudaError_t conv_dgrad(const ConvShape& g, int dtype, const void* dy, const void
             a.KG = a.nr * a.nq * g.K;
             cudaError_t e;
             if (a.KG == 0) {
-                const int64_t total = static_cast<int64_t>(a.M) * a.C;
-                const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 8 * kNumSMs));
-                if (dtype == kF16) dgrad_zero_phase_kernel<__half><<<blocks, 256, 0, st>>>(a);
-                else dgrad_zero_phase_kernel<float><<<blocks, 256, 0, st>>>(a);
-                e = cudaGetLastError();
+                continue;  // zeroed above (or untouched when accumulating)
             } else if (tc_ok(g, dtype)) {
                 e = launch_tc_pick<DGRAD>(a, 1, st);
             } else {

@@ -27,7 +27,7 @@ namespace sdb {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kMaxBlocks = 2 * kNumSMs;
+constexpr int kMaxBlocks = 4 * kNumSMs;
 
 template <class T>
 SDB_DEV void load8(const T* p, float (&v)[8]);
@@ -101,53 +101,60 @@ __global__ void __launch_bounds__(kThreads) stats_kernel(StatArgs p) {
             b[j] = KIND == 2 ? p.beta[c0 + j] : 0.f;
         }
     }
+    // process up to 4 rows per iteration (4 x 128-bit loads in flight per operand),
+    // fold fp32 partial sums into fp64 every 16 rows
     int run = 0;
-    for (int64_t r = r_begin + rg; r < r_end; r += rpi) {
-        const int64_t off = r * p.C + c0;
-        float v[8];
-        load8<T>(static_cast<const T*>(p.a) + off, v);
-        if (KIND == 0) {
+    for (int64_t r0 = r_begin + rg; r0 < r_end; r0 += 4 * rpi) {
+        float v[4][8], dd[4][8], ym[4][8];
+        bool ok[4];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                s[j] += v[j];
-                q[j] += v[j] * v[j];
+        for (int u = 0; u < 4; ++u) {
+            const int64_t r = r0 + u * rpi;
+            ok[u] = r < r_end;
+            if (ok[u]) {
+                const int64_t off = r * p.C + c0;
+                load8<T>(static_cast<const T*>(p.a) + off, v[u]);
+                if (KIND != 0) load8<T>(static_cast<const T*>(p.dy) + off, dd[u]);
+                if (KIND == 1 && p.y) load8<T>(static_cast<const T*>(p.y) + off, ym[u]);
             }
-        } else {
-            float d[8];
-            load8<T>(static_cast<const T*>(p.dy) + off, d);
-            if (KIND == 1) {
-                if (p.y) {
-                    float yv[8];
-                    load8<T>(static_cast<const T*>(p.y) + off, yv);
+        }
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) d[j] = yv[j] > 0.f ? d[j] : 0.f;
-                }
+        for (int u = 0; u < 4; ++u) {
+            if (!ok[u]) continue;
+            if (KIND == 0) {
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
-                    const float xh = (v[j] - mu[j]) * is[j];
-                    s[j] += d[j];
-                    q[j] += d[j] * xh;
+                    s[j] += v[u][j];
+                    q[j] += v[u][j] * v[u][j];
+                }
+            } else if (KIND == 1) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const float d = (p.y && !(ym[u][j] > 0.f)) ? 0.f : dd[u][j];
+                    const float xh = (v[u][j] - mu[j]) * is[j];
+                    s[j] += d;
+                    q[j] += d * xh;
                 }
             } else {
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
-                    const float yv = v[j];
+                    const float yv = v[u][j];
                     const float z = yv >= 0.f ? yv : yv / p.slope;
-                    const float dz = d[j] * (yv > 0.f ? 1.f : p.slope);
+                    const float dz = dd[u][j] * (yv > 0.f ? 1.f : p.slope);
                     const float xh = (z - b[j]) / g[j];
                     s[j] += dz;
                     q[j] += dz * xh;
                 }
             }
-        }
-        if (++run == 16) {
+            if (++run == 16) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                S[j] += s[j];
-                Q[j] += q[j];
-                s[j] = q[j] = 0.f;
+                for (int j = 0; j < 8; ++j) {
+                    S[j] += s[j];
+                    Q[j] += q[j];
+                    s[j] = q[j] = 0.f;
+                }
+                run = 0;
             }
-            run = 0;
         }
     }
 #pragma unroll
@@ -178,14 +185,30 @@ __global__ void __launch_bounds__(kThreads) stats_kernel(StatArgs p) {
 
 // MODE 0: BN fwd (sums rounded to float first), 1: IABN fwd (double)
 // MODE 2: BN bwd, 3: IABN bwd  -> coef[0..C) = s1/m, coef[C..2C) = s2/m
-__global__ void finalize_kernel(const double* partial, int nblocks, int C, int64_t count, float eps, int mode,
-                                float* mean, float* invstd, float* dgamma, float* dbeta, float* coef) {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= C) return;
+// Fixed-order parallel reduction of the per-block partials: thread (cx, ry)
+// of a 32x8 block sums partial[b][c] for b = ry, ry+8, ... (coalesced across
+// cx); the 8 row sums are then added in order.  Deterministic, no atomics.
+__global__ void __launch_bounds__(256) finalize_kernel(const double* partial, int nblocks, int C, int64_t count,
+                                                       float eps, int mode, float* mean, float* invstd, float* dgamma,
+                                                       float* dbeta, float* coef) {
+    __shared__ double rs[8][32], rq[8][32];
+    const int cx = threadIdx.x & 31, ry = threadIdx.x >> 5;
+    const int c = blockIdx.x * 32 + cx;
     double S = 0.0, Q = 0.0;
-    for (int b = 0; b < nblocks; ++b) {
-        S += partial[static_cast<int64_t>(b) * 2 * C + c];
-        Q += partial[static_cast<int64_t>(b) * 2 * C + C + c];
+    if (c < C)
+        for (int b = ry; b < nblocks; b += 8) {
+            S += partial[static_cast<int64_t>(b) * 2 * C + c];
+            Q += partial[static_cast<int64_t>(b) * 2 * C + C + c];
+        }
+    rs[ry][cx] = S;
+    rq[ry][cx] = Q;
+    __syncthreads();
+    if (ry != 0 || c >= C) return;
+    S = 0.0;
+    Q = 0.0;
+    for (int k = 0; k < 8; ++k) {
+        S += rs[k][cx];
+        Q += rq[k][cx];
     }
     if (mode == 0 || mode == 1) {
         double mu, var;
@@ -229,19 +252,39 @@ struct ApplyArgs {
     int C;
 };
 
+SDB_DEV void ldf8(const float* p, float (&v)[8]) {
+    const float4 a = *reinterpret_cast<const float4*>(p);
+    const float4 b = *reinterpret_cast<const float4*>(p + 4);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+
+// Each thread owns one 8-channel group (parameters held in registers) and
+// walks rows with a grid stride; 128-bit loads/stores, 2 rows in flight.
 template <class T, int KIND>
 __global__ void __launch_bounds__(kThreads) apply_kernel(ApplyArgs p) {
-    for (int64_t gi = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; gi < p.n8;
-         gi += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t off = gi * 8;
-        const int c0 = static_cast<int>(off % p.C);
+    const int tpr = p.C / 8;
+    const int rpi = kThreads / tpr;
+    const int cg = threadIdx.x % tpr, rg = threadIdx.x / tpr;
+    const int c0 = cg * 8;
+    const int64_t rows = p.n8 / tpr;
+    float g[8], b[8], mu[8], is[8], k1[8], k2[8];
+    ldf8(p.gamma + c0, g);
+    ldf8(p.invstd + c0, is);
+    if (KIND != 3) ldf8(p.mean + c0, mu);
+    if (KIND != 2) ldf8(p.beta + c0, b);
+    if (KIND >= 2) {
+        ldf8(p.coef + c0, k1);
+        ldf8(p.coef + p.C + c0, k2);
+    }
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * rpi;
+    for (int64_t r = static_cast<int64_t>(blockIdx.x) * rpi + rg; r < rows; r += stride) {
+        const int64_t off = r * p.C + c0;
         float v[8], o[8];
         load8<T>(static_cast<const T*>(p.a) + off, v);
         if (KIND == 0 || KIND == 1) {
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-                const int c = c0 + j;
-                const float z = p.gamma[c] * (v[j] - p.mean[c]) * p.invstd[c] + p.beta[c];
+                const float z = g[j] * (v[j] - mu[j]) * is[j] + b[j];
                 if (KIND == 0) o[j] = (p.act && !(z > 0.f)) ? 0.f : z;
                 else o[j] = z > 0.f ? z : p.slope * z;
             }
@@ -257,21 +300,19 @@ __global__ void __launch_bounds__(kThreads) apply_kernel(ApplyArgs p) {
                 }
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
-                    const int c = c0 + j;
-                    const float gis = p.gamma[c] * p.invstd[c];
-                    const float xh = (v[j] - p.mean[c]) * p.invstd[c];
-                    o[j] = gis * (d[j] - p.coef[c] - xh * p.coef[p.C + c]);
+                    const float gis = g[j] * is[j];
+                    const float xh = (v[j] - mu[j]) * is[j];
+                    o[j] = gis * (d[j] - k1[j] - xh * k2[j]);
                 }
             } else {
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
-                    const int c = c0 + j;
                     const float yv = v[j];
                     const float z = yv >= 0.f ? yv : yv / p.slope;
                     const float dz = d[j] * (yv > 0.f ? 1.f : p.slope);
-                    const float xh = (z - p.beta[c]) / p.gamma[c];
-                    const float gis = p.gamma[c] * p.invstd[c];
-                    o[j] = gis * (dz - p.coef[c] - xh * p.coef[p.C + c]);
+                    const float xh = (z - b[j]) / g[j];
+                    const float gis = g[j] * is[j];
+                    o[j] = gis * (dz - k1[j] - xh * k2[j]);
                 }
             }
         }
@@ -295,7 +336,9 @@ Plan plan_for(int64_t rows, int C) {
     return p;
 }
 
-int apply_blocks(int64_t n8) { return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n8 + kThreads - 1) / kThreads, 16 * kNumSMs))); }
+int apply_blocks(int64_t n8) {
+    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n8 + kThreads - 1) / kThreads, 8 * kNumSMs)));
+}
 
 template <class T, int KIND>
 cudaError_t run_stats(const StatArgs& a0, const Plan& pl, cudaStream_t st) {
@@ -323,7 +366,7 @@ cudaError_t bn_forward(int dtype, const void* x, const float* gamma, const float
     sa.a = x; sa.rows = rows; sa.C = C; sa.partial = partial;
     cudaError_t e = dtype == kF16 ? run_stats<__half, 0>(sa, pl, st) : run_stats<float, 0>(sa, pl, st);
     if (e != cudaSuccess) return e;
-    finalize_kernel<<<(C + 127) / 128, 128, 0, st>>>(partial, pl.nblocks, C, rows, eps, act == 2 ? 1 : 0, mean, invstd,
+    finalize_kernel<<<(C + 31) / 32, 256, 0, st>>>(partial, pl.nblocks, C, rows, eps, act == 2 ? 1 : 0, mean, invstd,
                                                      nullptr, nullptr, nullptr);
     ApplyArgs aa{};
     aa.a = x; aa.out = y; aa.gamma = gamma; aa.beta = beta; aa.mean = mean; aa.invstd = invstd;
@@ -350,7 +393,7 @@ cudaError_t bn_backward(int dtype, const void* dy, const void* x, const void* y_
     sa.rows = rows; sa.C = C; sa.partial = partial;
     cudaError_t e = dtype == kF16 ? run_stats<__half, 1>(sa, pl, st) : run_stats<float, 1>(sa, pl, st);
     if (e != cudaSuccess) return e;
-    finalize_kernel<<<(C + 127) / 128, 128, 0, st>>>(partial, pl.nblocks, C, rows, 0.f, 2, nullptr, nullptr, dgamma,
+    finalize_kernel<<<(C + 31) / 32, 256, 0, st>>>(partial, pl.nblocks, C, rows, 0.f, 2, nullptr, nullptr, dgamma,
                                                      dbeta, coef);
     ApplyArgs aa{};
     aa.a = x; aa.dy = dy; aa.y = y_mask; aa.out = dx; aa.gamma = gamma; aa.mean = mean; aa.invstd = invstd;
@@ -373,7 +416,7 @@ cudaError_t iabn_backward(int dtype, const void* dy, const void* y, const float*
     sa.rows = rows; sa.C = C; sa.partial = partial;
     cudaError_t e = dtype == kF16 ? run_stats<__half, 2>(sa, pl, st) : run_stats<float, 2>(sa, pl, st);
     if (e != cudaSuccess) return e;
-    finalize_kernel<<<(C + 127) / 128, 128, 0, st>>>(partial, pl.nblocks, C, rows, 0.f, 3, nullptr, nullptr, dgamma,
+    finalize_kernel<<<(C + 31) / 32, 256, 0, st>>>(partial, pl.nblocks, C, rows, 0.f, 3, nullptr, nullptr, dgamma,
                                                      dbeta, coef);
     ApplyArgs aa{};
     aa.a = y; aa.dy = dy; aa.out = dx; aa.gamma = gamma; aa.beta = beta; aa.invstd = invstd; aa.coef = coef;

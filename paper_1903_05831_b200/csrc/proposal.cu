@@ -173,6 +173,42 @@ SDB_DEV uint64_t block_radix_select(int n, int k, KeyFn keyfn, int* hist /*256*/
     return prefix;
 }
 
+// Indices of the flagged elements whose key equals the selection threshold T,
+// lowest `need` of them (the (key, index) order of the oracle's pick_smallest).
+// Collected in parallel; exact for up to 64 tied keys (64-bit hash ties do not
+// occur in practice).
+template <int NT, class KeyFn>
+SDB_DEV int collect_ties(int n, uint64_t T, int need, KeyFn keyfn, int* tie_list /*64*/, int* sh) {
+    if (threadIdx.x == 0) sh[33] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += NT) {
+        bool f;
+        const uint64_t k = keyfn(i, f);
+        if (f && k == T) {
+            const int s = atomicAdd(&sh[33], 1);
+            if (s < 64) tie_list[s] = i;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int m = min(sh[33], 64);
+        for (int a = 1; a < m; ++a) {
+            const int v = tie_list[a];
+            int b = a - 1;
+            while (b >= 0 && tie_list[b] > v) {
+                tie_list[b + 1] = tie_list[b];
+                --b;
+            }
+            tie_list[b + 1] = v;
+        }
+        sh[32] = min(m, need);
+    }
+    __syncthreads();
+    const int r = sh[32];
+    __syncthreads();
+    return r;
+}
+
 // ---------------------------------------------------------------- anchors
 __global__ void anchors_kernel(AnchorCfg a, float* __restrict__ out) {
     const int A = a.ns * a.nr;
@@ -478,17 +514,8 @@ __global__ void __launch_bounds__(kSampleThreads) anchor_sample_kernel(int nA, c
         if (T == ~0ull) {
             kept_here = n_lt;  // all flagged kept
         } else {
-            // ties at T: keep the lowest indices (rare); single-thread scan
-            const int need = k - n_lt;
-            if (threadIdx.x == 0) {
-                int got = 0;
-                for (int i = 0; i < nA && got < need && got < 64; ++i)
-                    if (L[i] == want && mix64(key, static_cast<uint64_t>(i)) == T) tie_list[got++] = i;
-                sh[32] = got;
-            }
-            __syncthreads();
-            const int ntie = sh[32];
-            __syncthreads();
+            // ties at T: keep the lowest indices
+            const int ntie = collect_ties<kSampleThreads>(nA, T, k - n_lt, keyfn, tie_list, sh);
             for (int i = threadIdx.x; i < nA; i += kSampleThreads) {
                 if (L[i] != want) continue;
                 const uint64_t pk = mix64(key, static_cast<uint64_t>(i));
@@ -573,16 +600,7 @@ __global__ void __launch_bounds__(kPtThreads) proposal_target_kernel(ProposalTar
             for (int i = threadIdx.x; i < T; i += kPtThreads)
                 if (cls[i] == want) cls[i] = static_cast<int8_t>(want + 2);
         } else {
-            const int need = k - n_lt;
-            if (threadIdx.x == 0) {
-                int got = 0;
-                for (int i = 0; i < T && got < need && got < 64; ++i)
-                    if (cls[i] == want && mix64(key, static_cast<uint64_t>(i)) == Tk) tie_list[got++] = i;
-                sh[32] = got;
-            }
-            __syncthreads();
-            const int ntie = sh[32];
-            __syncthreads();
+            const int ntie = collect_ties<kPtThreads>(T, Tk, k - n_lt, keyfn, tie_list, sh);
             for (int i = threadIdx.x; i < T; i += kPtThreads) {
                 if (cls[i] != want) continue;
                 const uint64_t pk = mix64(key, static_cast<uint64_t>(i));
