@@ -104,11 +104,17 @@ __global__ void __launch_bounds__(160, 1) conv_tc_kernel(ConvArgs a) {
 
     if (warp < 4) {
         // ------------------------------------------------ producers
+        // All per-row / per-column address arithmetic is hoisted out of the
+        // k loop: per k-block each thread does at most one tap decomposition,
+        // and every chunk is a pointer add + bounds test (the instruction
+        // budget per k-block must stay below the MMA time of the k-block).
         const __half* X = static_cast<const __half*>(a.x);
         const __half* Wt = static_cast<const __half*>(a.w);
         const int HoWo = a.Ho * a.Wo;
-        // per-thread precomputation for the gathered operand rows
-        int rowN[8], rowY[8], rowX[8];  // A rows (fprop/dgrad): image, base y, base x
+        constexpr int kBChunksPerRow = BN / 8;           // MN-major B: chunks per k row
+        constexpr int kBRowStep = 128 / kBChunksPerRow;  // k rows advanced per i
+        // A rows (fprop/dgrad): per-row image/base coordinates
+        int rowN[8], rowY[8], rowX[8];
         if (MODE == FPROP || MODE == DGRAD) {
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
@@ -123,22 +129,34 @@ __global__ void __launch_bounds__(160, 1) conv_tc_kernel(ConvArgs a) {
                         const int HpWp = a.Hp * a.Wp;
                         const int n = m / HpWp, rem = m - n * HpWp, i2 = rem / a.Wp, j2 = rem - i2 * a.Wp;
                         rowN[i] = n;
-                        rowY[i] = a.ph + a.stride * i2 + a.pad;  // h + p
-                        rowX[i] = a.pw + a.stride * j2 + a.pad;
+                        // (h + p - r0) / st is exact: h = ph + st*i2 and r0 = (ph + p) mod st
+                        rowY[i] = (a.ph + a.stride * i2 + a.pad - a.r0) / a.stride;
+                        rowX[i] = (a.pw + a.stride * j2 + a.pad - a.q0) / a.stride;
                     }
                 } else {
                     rowN[i] = -1;
-                    rowY[i] = rowX[i] = 0;
+                    rowY[i] = rowX[i] = -(1 << 28);
                 }
             }
         }
-        // wgrad B: the thread's fixed column chunk (tap, c)
-        constexpr int kBChunksPerRow = BN / 8;           // MN-major B: chunks per k row
-        constexpr int kBRowStep = 128 / kBChunksPerRow;  // k rows advanced per i
+        // fprop B: filter row offsets
+        int64_t brow[BN / 16];
+        if (MODE == FPROP) {
+#pragma unroll
+            for (int i = 0; i < BN / 16; ++i) {
+                const int j = n0 + (tid >> 3) + 16 * i;
+                brow[i] = j < a.NG ? static_cast<int64_t>(j) * a.KG : -1;
+            }
+        }
+        // dgrad B (MN-major filter [c][(tap,kout)]) and wgrad A/B: fixed column chunk
+        const int mcB = tid % kBChunksPerRow;
+        const int krowB = tid / kBChunksPerRow;
+        const int64_t RSC = static_cast<int64_t>(a.R) * a.S * a.C;
+        const bool dg_fast = (a.K % kBK) == 0;
         int wg_r = 0, wg_s = 0, wg_c = 0;
         bool wg_ok = false;
         if (MODE == WGRAD) {
-            const int col = n0 + (tid % kBChunksPerRow) * 8;
+            const int col = n0 + mcB * 8;
             wg_ok = col < a.NG;
             const int tap = col / a.C;
             wg_c = col - tap * a.C;
@@ -153,7 +171,6 @@ __global__ void __launch_bounds__(160, 1) conv_tc_kernel(ConvArgs a) {
             const uint32_t sb = sa + Cfg::kABytes;
             const int kb = kb0 + it;
             if (MODE == FPROP) {
-                // A: rows m, chunk = tid&7 -> kg = kb*64 + 8*(tid&7)
                 const int kg = kb * kBK + 8 * (tid & 7);
                 const bool kok = kg < a.KG;
                 const int tap = kg / a.C, c = kg - tap * a.C;
@@ -162,76 +179,100 @@ __global__ void __launch_bounds__(160, 1) conv_tc_kernel(ConvArgs a) {
                 for (int i = 0; i < 8; ++i) {
                     const int row = (tid >> 3) + 16 * i;
                     const int ih = rowY[i] + r, iw = rowX[i] + q;
-                    const bool ok = kok && rowN[i] >= 0 && ih >= 0 && ih < a.H && iw >= 0 && iw < a.W;
+                    const bool ok = kok && static_cast<unsigned>(ih) < static_cast<unsigned>(a.H) &&
+                                    static_cast<unsigned>(iw) < static_cast<unsigned>(a.W);
                     const __half* src = ok ? X + ((static_cast<int64_t>(rowN[i]) * a.H + ih) * a.W + iw) * a.C + c : X;
                     cp_async16(sa + kmaj_off(row, tid & 7), src, ok ? 16u : 0u);
                 }
-                // B: filter rows (k-major): rows = out channels
 #pragma unroll
                 for (int i = 0; i < BN / 16; ++i) {
                     const int row = (tid >> 3) + 16 * i;
-                    const int j = n0 + row;
-                    const bool ok = kok && j < a.NG;
-                    const __half* src = ok ? Wt + static_cast<int64_t>(j) * a.KG + kg : Wt;
-                    cp_async16(sb + kmaj_off(row, tid & 7), src, ok ? 16u : 0u);
+                    const bool ok = kok && brow[i] >= 0;
+                    cp_async16(sb + kmaj_off(row, tid & 7), ok ? Wt + brow[i] + kg : Wt, ok ? 16u : 0u);
                 }
             } else if (MODE == DGRAD) {
                 // A: DY gather, k-major over kg = tap*K + kout
                 const int kg = kb * kBK + 8 * (tid & 7);
                 const bool kok = kg < a.KG;
                 const int t = kg / a.K, kout = kg - t * a.K;
-                const int r = a.r0 + a.stride * (t / a.nq), q = a.q0 + a.stride * (t % a.nq);
+                const int ti = t / a.nq, tq = t - ti * a.nq;
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
                     const int row = (tid >> 3) + 16 * i;
-                    const int yy = rowY[i] - r, xx = rowX[i] - q;  // (h+p-r), (w+p-q), multiples of stride
-                    const int oh = yy / a.stride, ow = xx / a.stride;
-                    const bool ok = kok && rowN[i] >= 0 && yy >= 0 && xx >= 0 && oh < a.Ho && ow < a.Wo;
+                    const int oh = rowY[i] - ti, ow = rowX[i] - tq;
+                    const bool ok = kok && rowN[i] >= 0 && static_cast<unsigned>(oh) < static_cast<unsigned>(a.Ho) &&
+                                    static_cast<unsigned>(ow) < static_cast<unsigned>(a.Wo);
                     const __half* src =
                         ok ? X + ((static_cast<int64_t>(rowN[i]) * a.Ho + oh) * a.Wo + ow) * a.K + kout : X;
                     cp_async16(sa + kmaj_off(row, tid & 7), src, ok ? 16u : 0u);
                 }
-                // B: filter as MN-major [c][kg]: chunk = 8 consecutive c at one kg row
-#pragma unroll
-                for (int i = 0; i < BN / 16; ++i) {
-                    const int krow = tid / kBChunksPerRow + kBRowStep * i;
-                    const int mc = tid % kBChunksPerRow;
-                    const int kg2 = kb * kBK + krow;
-                    const int c = n0 + mc * 8;
-                    const bool ok = kg2 < a.KG && c < a.NG;
-                    const int t2 = kg2 / a.K, ko2 = kg2 - t2 * a.K;
+                // B: filter as MN-major [c][kg]
+                const int c = n0 + mcB * 8;
+                const bool cok = c < a.NG;
+                if (dg_fast) {
+                    // the whole k-block lies in one tap: kout = kbk + krow
+                    const int kg0 = kb * kBK;
+                    const int t2 = kg0 / a.K, kbk = kg0 - t2 * a.K;
                     const int r2 = a.r0 + a.stride * (t2 / a.nq), q2 = a.q0 + a.stride * (t2 % a.nq);
-                    const __half* src = ok ? Wt + ((static_cast<int64_t>(ko2) * a.R + r2) * a.S + q2) * a.C + c : Wt;
-                    cp_async16(sb + mnmaj_off(mc, krow, BN), src, ok ? 16u : 0u);
+                    const bool tok = kg0 < a.KG && cok;
+                    const __half* bsrc = Wt + static_cast<int64_t>(kbk + krowB) * RSC + (r2 * a.S + q2) * a.C + c;
+#pragma unroll
+                    for (int i = 0; i < BN / 16; ++i) {
+                        const int krow = krowB + kBRowStep * i;
+                        cp_async16(sb + mnmaj_off(mcB, krow, BN), tok ? bsrc + kBRowStep * i * RSC : Wt, tok ? 16u : 0u);
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < BN / 16; ++i) {
+                        const int krow = krowB + kBRowStep * i;
+                        const int kg2 = kb * kBK + krow;
+                        const bool ok = kg2 < a.KG && cok;
+                        const int t2 = kg2 / a.K, ko2 = kg2 - t2 * a.K;
+                        const int r2 = a.r0 + a.stride * (t2 / a.nq), q2 = a.q0 + a.stride * (t2 % a.nq);
+                        const __half* src = ok ? Wt + ((static_cast<int64_t>(ko2) * a.R + r2) * a.S + q2) * a.C + c : Wt;
+                        cp_async16(sb + mnmaj_off(mcB, krow, BN), src, ok ? 16u : 0u);
+                    }
                 }
             } else {
                 // WGRAD. A = DY^T as MN-major [kout][m]: chunk = 8 kout at one pixel row
                 const __half* DY = static_cast<const __half*>(a.w);
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    const int krow = (tid >> 4) + 8 * i;
+                {
                     const int mc = tid & 15;
-                    const int m = kb * kBK + krow;
                     const int ko = m0 + mc * 8;
-                    const bool ok = m < a.KG && ko < a.M;
-                    const __half* src = ok ? DY + static_cast<int64_t>(m) * a.K + ko : DY;
-                    cp_async16(sa + mnmaj_off(mc, krow, kBM), src, ok ? 16u : 0u);
-                }
-                // B = im2col(X)^T as MN-major [(r,s,c)][m]
+                    const int mrow0 = kb * kBK + (tid >> 4);
+                    const __half* asrc = DY + static_cast<int64_t>(mrow0) * a.K + ko;
 #pragma unroll
-                for (int i = 0; i < BN / 16; ++i) {
-                    const int krow = tid / kBChunksPerRow + kBRowStep * i;
-                    const int mc = tid % kBChunksPerRow;
-                    const int m = kb * kBK + krow;
-                    bool ok = wg_ok && m < a.KG;
-                    const __half* src = X;
-                    if (ok) {
-                        const int n = m / HoWo, rem = m - n * HoWo, oh = rem / a.Wo, ow = rem - oh * a.Wo;
-                        const int ih = oh * a.stride - a.pad + wg_r, iw = ow * a.stride - a.pad + wg_s;
-                        ok = ih >= 0 && ih < a.H && iw >= 0 && iw < a.W;
-                        if (ok) src = X + ((static_cast<int64_t>(n) * a.H + ih) * a.W + iw) * a.C + wg_c;
+                    for (int i = 0; i < 8; ++i) {
+                        const int krow = (tid >> 4) + 8 * i;
+                        const bool ok = mrow0 + 8 * i < a.KG && ko < a.M;
+                        cp_async16(sa + mnmaj_off(mc, krow, kBM), ok ? asrc + static_cast<int64_t>(8 * i) * a.K : DY,
+                                   ok ? 16u : 0u);
                     }
-                    cp_async16(sb + mnmaj_off(mc, krow, BN), src, ok ? 16u : 0u);
+                }
+                // B = im2col(X)^T as MN-major [(r,s,c)][m]; pixel walk is incremental
+                {
+                    int m = kb * kBK + krowB;
+                    int n = m / HoWo;
+                    int rem = m - n * HoWo;
+                    int oh = rem / a.Wo, ow = rem - oh * a.Wo;
+#pragma unroll
+                    for (int i = 0; i < BN / 16; ++i) {
+                        const int krow = krowB + kBRowStep * i;
+                        const int ih = oh * a.stride - a.pad + wg_r, iw = ow * a.stride - a.pad + wg_s;
+                        const bool ok = wg_ok && m < a.KG && static_cast<unsigned>(ih) < static_cast<unsigned>(a.H) &&
+                                        static_cast<unsigned>(iw) < static_cast<unsigned>(a.W);
+                        const __half* src = ok ? X + ((static_cast<int64_t>(n) * a.H + ih) * a.W + iw) * a.C + wg_c : X;
+                        cp_async16(sb + mnmaj_off(mcB, krow, BN), src, ok ? 16u : 0u);
+                        m += kBRowStep;
+                        ow += kBRowStep;
+                        while (ow >= a.Wo) {
+                            ow -= a.Wo;
+                            if (++oh == a.Ho) {
+                                oh = 0;
+                                ++n;
+                            }
+                        }
+                    }
                 }
             }
             cp_async_commit();
@@ -591,16 +632,33 @@ cudaError_t conv_dgrad(const ConvShape& g, int dtype, const void* dy, const void
     return cudaSuccess;
 }
 
-size_t conv_wgrad_workspace(const ConvShape& g, int dtype) {
+// Deterministic split-K plan for wgrad (shared by workspace sizing and launch):
+// fill one wave of the tensor-core kernel (1 CTA/SM at BN=256, 2 at BN<=128)
+// with >= 8 k-blocks per split.
+static int wgrad_splits(const ConvShape& g, int dtype) {
     ConvArgs a = make_args(g);
     const int64_t M = g.K, NG = static_cast<int64_t>(g.R) * g.S * g.C, KG = static_cast<int64_t>(g.N) * a.Ho * a.Wo;
     const bool tc = tc_ok(g, dtype);
     const int bk = tc ? kBK : 16;
     const int64_t nkb = (KG + bk - 1) / bk;
-    const int64_t tiles = tc ? ((M + 127) / 128) * ((NG + 127) / 128) : ((M + 63) / 64) * ((NG + 63) / 64);
-    int64_t splits = std::max<int64_t>(1, std::min<int64_t>(nkb / 4, (2 * kNumSMs + tiles - 1) / tiles));
-    splits = std::min<int64_t>(splits, 64);
-    return static_cast<size_t>(splits) * M * NG * sizeof(float);
+    int64_t tiles, per_sm;
+    if (tc) {
+        const int bn = NG <= 64 ? 64 : 128;  // split-K launches never pick BN=256 unless tiles are plentiful
+        tiles = ((M + 127) / 128) * ((NG + bn - 1) / bn);
+        per_sm = 2;
+    } else {
+        tiles = ((M + 63) / 64) * ((NG + 63) / 64);
+        per_sm = 4;
+    }
+    const int64_t target = per_sm * kNumSMs;
+    int64_t splits = target / std::max<int64_t>(tiles, 1);
+    splits = std::max<int64_t>(1, std::min<int64_t>(splits, nkb / 8));
+    return static_cast<int>(std::min<int64_t>(splits, 64));
+}
+
+size_t conv_wgrad_workspace(const ConvShape& g, int dtype) {
+    const int64_t M = g.K, NG = static_cast<int64_t>(g.R) * g.S * g.C;
+    return static_cast<size_t>(wgrad_splits(g, dtype)) * M * NG * sizeof(float);
 }
 
 cudaError_t conv_wgrad(const ConvShape& g, int dtype, const void* x, const void* dy, void* dw, void* ws,
@@ -614,8 +672,7 @@ cudaError_t conv_wgrad(const ConvShape& g, int dtype, const void* x, const void*
     const int bk = tc ? kBK : 16;
     const int nkb = (a.KG + bk - 1) / bk;
     const int64_t per = static_cast<int64_t>(a.M) * a.NG;
-    int splits = static_cast<int>(ws_bytes / (per * sizeof(float)));
-    splits = std::max(1, std::min(splits, nkb));
+    int splits = wgrad_splits(g, dtype);
     a.kb_per_split = (nkb + splits - 1) / splits;
     splits = (nkb + a.kb_per_split - 1) / a.kb_per_split;
     if (ws == nullptr || ws_bytes < static_cast<size_t>(per) * sizeof(float) * splits) return cudaErrorInvalidValue;
