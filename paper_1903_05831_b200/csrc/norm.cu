@@ -27,7 +27,7 @@ namespace sdb {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kMaxBlocks = 4 * kNumSMs;
+constexpr int kMaxBlocks = 2 * kNumSMs;
 
 template <class T>
 SDB_DEV void load8(const T* p, float (&v)[8]);
@@ -81,7 +81,7 @@ struct StatArgs {
 };
 
 template <class T, int KIND>
-__global__ void __launch_bounds__(kThreads) stats_kernel(StatArgs p) {
+__global__ void __launch_bounds__(kThreads, 2) stats_kernel(StatArgs p) {
     extern __shared__ double red[];  // [kThreads][16]
     const int tpr = p.C / 8;
     const int rpi = kThreads / tpr;
@@ -99,16 +99,18 @@ __global__ void __launch_bounds__(kThreads) stats_kernel(StatArgs p) {
             is[j] = p.invstd[c0 + j];
             mu[j] = KIND == 1 ? p.mean[c0 + j] : 0.f;
             b[j] = KIND == 2 ? p.beta[c0 + j] : 0.f;
+            if (KIND == 2) g[j] = 1.0f / g[j];  // xhat = (z - beta) * (1/gamma)
         }
     }
-    // process up to 4 rows per iteration (4 x 128-bit loads in flight per operand),
-    // fold fp32 partial sums into fp64 every 16 rows
+    const float inv_slope = 1.0f / p.slope;
+    // process up to 2 rows per iteration (2 x 128-bit loads in flight per operand,
+    // <= 85 registers so 3 CTAs fit per SM), fold fp32 partials into fp64 every 16 rows
     int run = 0;
-    for (int64_t r0 = r_begin + rg; r0 < r_end; r0 += 4 * rpi) {
-        float v[4][8], dd[4][8], ym[4][8];
-        bool ok[4];
+    for (int64_t r0 = r_begin + rg; r0 < r_end; r0 += 2 * rpi) {
+        float v[2][8], dd[2][8], ym[2][8];
+        bool ok[2];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 2; ++u) {
             const int64_t r = r0 + u * rpi;
             ok[u] = r < r_end;
             if (ok[u]) {
@@ -119,7 +121,7 @@ __global__ void __launch_bounds__(kThreads) stats_kernel(StatArgs p) {
             }
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 2; ++u) {
             if (!ok[u]) continue;
             if (KIND == 0) {
 #pragma unroll
@@ -139,9 +141,9 @@ __global__ void __launch_bounds__(kThreads) stats_kernel(StatArgs p) {
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     const float yv = v[u][j];
-                    const float z = yv >= 0.f ? yv : yv / p.slope;
+                    const float z = yv >= 0.f ? yv : yv * inv_slope;
                     const float dz = dd[u][j] * (yv > 0.f ? 1.f : p.slope);
-                    const float xh = (z - b[j]) / g[j];
+                    const float xh = (z - b[j]) * g[j];
                     s[j] += dz;
                     q[j] += dz * xh;
                 }
@@ -261,7 +263,7 @@ SDB_DEV void ldf8(const float* p, float (&v)[8]) {
 // Each thread owns one 8-channel group (parameters held in registers) and
 // walks rows with a grid stride; 128-bit loads/stores, 2 rows in flight.
 template <class T, int KIND>
-__global__ void __launch_bounds__(kThreads) apply_kernel(ApplyArgs p) {
+__global__ void __launch_bounds__(kThreads, 2) apply_kernel(ApplyArgs p) {
     const int tpr = p.C / 8;
     const int rpi = kThreads / tpr;
     const int cg = threadIdx.x % tpr, rg = threadIdx.x / tpr;
@@ -276,6 +278,13 @@ __global__ void __launch_bounds__(kThreads) apply_kernel(ApplyArgs p) {
         ldf8(p.coef + c0, k1);
         ldf8(p.coef + p.C + c0, k2);
     }
+    float ig[8], gis[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        ig[j] = 1.0f / g[j];
+        gis[j] = g[j] * is[j];
+    }
+    const float inv_slope = 1.0f / p.slope;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * rpi;
     for (int64_t r = static_cast<int64_t>(blockIdx.x) * rpi + rg; r < rows; r += stride) {
         const int64_t off = r * p.C + c0;
@@ -308,11 +317,10 @@ __global__ void __launch_bounds__(kThreads) apply_kernel(ApplyArgs p) {
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     const float yv = v[j];
-                    const float z = yv >= 0.f ? yv : yv / p.slope;
+                    const float z = yv >= 0.f ? yv : yv * inv_slope;
                     const float dz = d[j] * (yv > 0.f ? 1.f : p.slope);
-                    const float xh = (z - b[j]) / g[j];
-                    const float gis = g[j] * is[j];
-                    o[j] = gis * (dz - k1[j] - xh * k2[j]);
+                    const float xh = (z - b[j]) * ig[j];
+                    o[j] = gis[j] * (dz - k1[j] - xh * k2[j]);
                 }
             }
         }
