@@ -23,18 +23,18 @@ SDB_DEV void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.clust
 SDB_DEV void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// try_wait with a suspend-time hint: the waiting warp sleeps in hardware until
+// the phase flips (or the hint expires) instead of spinning on issue slots the
+// producer warps need.
 SDB_DEV void mbar_wait(uint64_t* bar, uint32_t phase) {
     const uint32_t addr = smem_u32(bar);
-    uint32_t done = 0;
-    do {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(done)
-            : "r"(addr), "r"(phase)
-            : "memory");
-    } while (!done);
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(addr),
+        "r"(phase), "r"(0x989680u)
+        : "memory");
 }
 
 // ---------------------------------------------------------------- cp.async
@@ -46,6 +46,11 @@ SDB_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memo
 template <int N>
 SDB_DEV void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+// arrive on `bar` once all prior cp.async of this thread have completed
+// (counts as one of the barrier's expected arrivals)
+SDB_DEV void cp_async_mbar_arrive_noinc(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 SDB_DEV void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 

@@ -275,16 +275,12 @@ __global__ void __launch_bounds__(160, 1) conv_tc_kernel(ConvArgs a) {
                     }
                 }
             }
-            cp_async_commit();
-            if (it >= Cfg::kLag) {
-                cp_async_wait<Cfg::kLag>();
-                fence_proxy_async();
-                mbar_arrive(&full[(it - Cfg::kLag) % ST]);
-            }
+            // the mbarrier arrival fires when THIS thread's copies of the stage
+            // land; the producer never blocks on its own loads and runs ST
+            // stages ahead of the MMA (limited only by the empty barriers)
+            cp_async_mbar_arrive_noinc(&full[s]);
         }
         cp_async_wait<0>();
-        fence_proxy_async();
-        for (int it = max(0, nk - Cfg::kLag); it < nk; ++it) mbar_arrive(&full[it % ST]);
 
         // ------------------------------------------------ epilogue
         const int row_local = warp * 32 + (tid & 31);
