@@ -139,8 +139,14 @@ __global__ void __launch_bounds__(kBwdThreads) roialign_bwd_kernel(const T* __re
                                                                    float scale, int sr, T* __restrict__ dfeat) {
     __shared__ float WY[kMaxP][kTile];
     __shared__ float WX[kMaxP][kTile];
+    __shared__ int rng[2][4][kTile];  // double-buffered [row lo, row hi, col lo, col hi] of nonzero bins
     __shared__ int list[1024];
     __shared__ int sh[40];
+    if (threadIdx.x < 64) {
+        const int t = threadIdx.x & 31;
+        rng[threadIdx.x >> 5][t >> 3][t & 7] = ((t >> 3) & 1) ? -1 : P;
+    }
+    int it_count = 0;
     const int n = blockIdx.z;
     const int tiles_x = (W + kTile - 1) / kTile;
     const int ty = blockIdx.x / tiles_x, tx = blockIdx.x % tiles_x;
@@ -195,9 +201,15 @@ __global__ void __launch_bounds__(kBwdThreads) roialign_bwd_kernel(const T* __re
             if (mine[q]) list[pos++] = base + threadIdx.x * 4 + q;
         __syncthreads();
 
-        for (int li = 0; li < total; ++li) {
+        for (int li = 0; li < total; ++li, ++it_count) {
             const int r = list[li];
+            const int buf = it_count & 1;
             const Geom g = roi_geom(rois + static_cast<int64_t>(r) * 5, P, scale);
+            // reset the other range buffer (last read two RoIs ago, before a barrier)
+            if (threadIdx.x < 32) {
+                const int t = threadIdx.x;
+                rng[buf ^ 1][t >> 3][t & 7] = ((t >> 3) & 1) ? -1 : P;
+            }
             // separable weights for this tile
             for (int t = threadIdx.x; t < 2 * P * kTile; t += kBwdThreads) {
                 const bool isx = t >= P * kTile;
@@ -218,6 +230,10 @@ __global__ void __launch_bounds__(kBwdThreads) roialign_bwd_kernel(const T* __re
                 }
                 if (isx) WX[pb][lo] = wsum;
                 else WY[pb][lo] = wsum;
+                if (wsum != 0.f) {
+                    atomicMin(&rng[buf][isx ? 2 : 0][lo], pb);
+                    atomicMax(&rng[buf][isx ? 3 : 1][lo], pb);
+                }
             }
             __syncthreads();
             if (c_ok) {
@@ -227,10 +243,11 @@ __global__ void __launch_bounds__(kBwdThreads) roialign_bwd_kernel(const T* __re
                     const int p = pix0 + 8 * i;
                     const int ly = p >> 3, lx = p & 7;
                     if (y0 + ly >= H || x0 + lx >= W) continue;
-                    for (int ph = 0; ph < P; ++ph) {
+                    const int phe = rng[buf][1][ly], pwb = rng[buf][2][lx], pwe = rng[buf][3][lx];
+                    for (int ph = rng[buf][0][ly]; ph <= phe; ++ph) {
                         const float wy = WY[ph][ly];
                         if (wy == 0.f) continue;
-                        for (int pw = 0; pw < P; ++pw) {
+                        for (int pw = pwb; pw <= pwe; ++pw) {
                             const float wx = WX[pw][lx];
                             if (wx == 0.f) continue;
                             const float wgt = wy * wx * inv_count;

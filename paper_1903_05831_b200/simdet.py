@@ -40,6 +40,12 @@ _SIGS = {
     "sdb_fused_sgd": [_P, _I, _P, _P, _P, _P, _L, _F, _F, _P, _D, _P, _P],
     "sdb_update_scale": [_P, _P, _P, _P, _I, _L, _D, _D, _D, _D, _P],
     "sdb_cast": [_P, _I, _P, _I, _P, _L, _P],
+    "sdb_make_anchors": [_P, _I, _I, _F, _P, _I, _P, _I, _P, _P],
+    "sdb_rpn_proposal": [_P, _I, _P, _P, _P, _I, _I, _I, _I, _I, _D, _I, _F, _F, _P, _P, _P, _P, _P],
+    "sdb_roialign_fwd": [_P, _I, _P, _I, _I, _I, _I, _P, _I, _I, _F, _I, _P, _P],
+    "sdb_roialign_bwd": [_P, _I, _P, _I, _I, _I, _I, _P, _I, _I, _F, _I, _P, _P],
+    "sdb_softmax_ce": [_P, _I, _P, _I, _I, _I, _P, _P, _P, _P, _P],
+    "sdb_debug_set": [_I, _I],
 }
 
 _configured = False
@@ -224,6 +230,60 @@ def apply_sgd(w, v, gsum, lr: float, momentum: float, denom: float, w16=None, fl
         mult = denom  # caller passes K when the scale is on device
     check(L().sdb_fused_sgd(ctx(), dt(gsum), ptr(gsum), ptr(w), ptr(v), ptr(w16), w.numel(), lr, momentum,
                             ptr(scale), mult, ptr(flag), stream()))
+
+
+def make_anchors(H, W, stride, scales, ratios):
+    """anchors [H*W*A, 4] fp32, anchor a = ratio_i * n_scales + scale_j (restated, no reference op)"""
+    sc = torch.tensor(scales, dtype=torch.float32)
+    ra = torch.tensor(ratios, dtype=torch.float32)
+    out = torch.empty((H * W * len(scales) * len(ratios), 4), device="cuda", dtype=torch.float32)
+    check(L().sdb_make_anchors(ctx(), H, W, stride, C.c_void_p(sc.data_ptr()), len(scales), C.c_void_p(ra.data_ptr()),
+                               len(ratios), ptr(out), stream()))
+    return out
+
+
+def rpn_proposal(logits, deltas, anchors, A, pre_k, iou, post_k, img_h, img_w):
+    """RPN proposal layer: logits [n, n_loc, A_pad], deltas [n, n_loc, 4*A_pad] (NHWC-flat)."""
+    n, n_loc, A_pad = logits.shape
+    rois = torch.empty((n, post_k, 4), device=logits.device, dtype=torch.float32)
+    scores = torch.empty((n, post_k), device=logits.device, dtype=torch.float32)
+    count = torch.empty(n, device=logits.device, dtype=torch.int32)
+    k = min(pre_k, n_loc * A)
+    order = torch.empty((n, k), device=logits.device, dtype=torch.int32)
+    check(L().sdb_rpn_proposal(ctx(), dt(logits), ptr(logits), ptr(deltas), ptr(anchors), n, n_loc, A, A_pad, pre_k,
+                               iou, post_k, img_h, img_w, ptr(rois), ptr(scores), ptr(count), ptr(order), stream()))
+    return rois, scores, count, order
+
+
+def roialign_forward(feat, rois, P, spatial_scale, sampling_ratio):
+    """RoIAlign (aligned) forward, reference layout: feat [N,C,H,W] -> [R,C,P,P]."""
+    fn = nchw_to_nhwc(feat)
+    N, H, W, Cc = fn.shape
+    R = rois.shape[0]
+    out = torch.empty((R, P, P, Cc), device=feat.device, dtype=feat.dtype)
+    check(L().sdb_roialign_fwd(ctx(), dt(feat), ptr(fn), N, H, W, Cc, ptr(rois), R, P, spatial_scale, sampling_ratio,
+                               ptr(out), stream()))
+    return nhwc_to_nchw(out)
+
+
+def roialign_backward(dy, feat_shape, rois, P, spatial_scale, sampling_ratio):
+    """RoIAlign backward (atomics-free gather): dy [R,C,P,P] -> dfeat [N,C,H,W]."""
+    N, Cc, H, W = feat_shape
+    dyn = nchw_to_nhwc(dy)
+    dx = torch.empty((N, H, W, Cc), device=dy.device, dtype=dy.dtype)
+    check(L().sdb_roialign_bwd(ctx(), dt(dy), ptr(dyn), N, H, W, Cc, ptr(rois), rois.shape[0], P, spatial_scale,
+                               sampling_ratio, ptr(dx), stream()))
+    return nhwc_to_nchw(dx)
+
+
+def softmax_ce(logits, labels, grad_scale=None):
+    """the reference CE op (src/model.cpp:101-151): returns (loss, dlogits)"""
+    R, ncls = logits.shape
+    loss = torch.zeros(1, device=logits.device, dtype=torch.float64)
+    dx = torch.empty_like(logits)
+    check(L().sdb_softmax_ce(ctx(), dt(logits), ptr(logits), R, ncls, ncls, ptr(labels), ptr(grad_scale), ptr(loss),
+                             ptr(dx), stream()))
+    return loss, dx
 
 
 def update_scale(scale_dev, good_dev, flag_dev, dynamic: bool, growth_interval=2000, growth=2.0, backoff=0.5,
