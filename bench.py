@@ -217,22 +217,22 @@ def run_ours(args):
 
     from paper_1903_05831_b200 import detector as D
 
+    from paper_1903_05831_b200 import dist as dp
+
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     dist = None
     nccl_id = None
     if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("gloo")
-        from paper_1903_05831_b200 import lib
+        dist = dp.init("gloo")
         import ctypes as C
-        obj = [None]
-        if rank == 0:
+
+        def make_id():
             buf = C.create_string_buffer(128)
             D.L().sdb_get_nccl_unique_id(buf)
-            obj = [bytes(buf.raw)]
-        dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
+            return bytes(buf.raw)
+
+        nccl_id = dp.share_nccl_id(dist, rank, make_id)
     p = D.preset(args.config)
     det = D.Detector(p, device=local, rank=rank, world=world, nccl_id=nccl_id)
     import ctypes as C
@@ -281,11 +281,7 @@ def run_ours(args):
         barrier()
     ms = e0.elapsed_time(e1)
     losses, scale_used, overflow = det.losses()
-    ms_max = ms
-    if dist is not None:
-        t = torch.tensor([ms], dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_max = float(t.item())
+    ms_max = dp.max_over_ranks(dist, ms) if dist is not None else ms
     value = world * B * K / (ms_max / 1e3)
 
     # ---------------- end to end through the host C-ABI call
@@ -306,9 +302,7 @@ def run_ours(args):
     barrier()
     ms_e2e = e2.elapsed_time(e3)
     if dist is not None:
-        t = torch.tensor([ms_e2e], dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_e2e = float(t.item())
+        ms_e2e = dp.max_over_ranks(dist, ms_e2e)
     e2e_value = world * B * K / (ms_e2e / 1e3)
 
     # ---------------- instrumented step: roofline of the dominant kernel family

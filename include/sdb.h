@@ -195,6 +195,11 @@ int sdb_det_export(sdb_det* det, int what, void* host, int64_t capacity, int64_t
 int sdb_det_dims(sdb_det* det, int* feat_h, int* feat_w, int* n_anchor_per_loc, int* a_pad);
 /* launches of libsdb kernels per step (counted at the first step) */
 int sdb_det_kernel_launches(sdb_det* det, int64_t* n);
+/* the gradient-bucket plan of the data-parallel allreduce (host logic, no GPU):
+ * offsets = start of every conv/fc gradient slice in the flat buffer (pack
+ * order), total = buffer length; buckets are emitted in issue order (from the
+ * end).  Returns the bucket count; out_lo_hi gets [lo, hi) pairs. */
+int sdb_plan_buckets(const int64_t* offsets, int n, int64_t total, int64_t cap_elems, int64_t* out_lo_hi, int cap_out);
 /* one eager, CUDA-event-instrumented step on the current batch: per category
  * (0 conv fprop, 1 dgrad, 2 wgrad, 3 norm fwd, 4 norm bwd, 5 elementwise,
  * 6 pooling, 7 targets, 8 proposal, 9 roialign fwd, 10 roialign bwd, 11 losses,

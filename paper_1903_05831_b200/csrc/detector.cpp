@@ -649,6 +649,33 @@ void run_step(sdb_det* d) {
 // ====================================================================== ABI
 extern "C" {
 
+int sdb_plan_buckets(const int64_t* offsets, int n, int64_t total, int64_t cap_elems, int64_t* out_lo_hi, int cap_out) {
+    // gradient buckets over the flat buffer, formed from the END because the
+    // backward pass completes the last layers first; a bucket closes at the
+    // first parameter boundary where it reaches cap_elems (the first
+    // parameter always closes the last bucket)
+    int nb = 0;
+    int64_t hi = total;
+    for (int i = n - 1; i >= 0; --i) {
+        if (hi - offsets[i] >= cap_elems || i == 0) {
+            if (nb < cap_out) {
+                out_lo_hi[2 * nb] = offsets[i];
+                out_lo_hi[2 * nb + 1] = hi;
+            }
+            ++nb;
+            hi = offsets[i];
+        }
+    }
+    if (hi > 0) {
+        if (nb < cap_out) {
+            out_lo_hi[2 * nb] = 0;
+            out_lo_hi[2 * nb + 1] = hi;
+        }
+        ++nb;
+    }
+    return nb;
+}
+
 int sdb_det_create(sdb_ctx* ctx, const sdb_det_config* cfgp, sdb_det** out) {
     if (!ctx || !cfgp || !out) return det_fail(SDB_PARAM, "null argument");
     const sdb_det_config& cf = *cfgp;
@@ -806,16 +833,13 @@ int sdb_det_create(sdb_ctx* ctx, const sdb_det_config* cfgp, sdb_det** out) {
             CK(cudaEventCreateWithFlags(&d->ev_fork, cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&d->ev_join, cudaEventDisableTiming));
             const int64_t cap = static_cast<int64_t>(cf.bucket_mb * 1024 * 1024 / d->es);
-            int64_t hi = d->n_w;
-            for (int pi = static_cast<int>(d->params.size()) - 1; pi >= 0; --pi) {
-                const Param& p = d->params[pi];
-                if (p.kind > 1) continue;
-                if (hi - p.off >= cap || pi == d->stem.p) {
-                    d->buckets.push_back({p.off, hi});
-                    hi = p.off;
-                }
-            }
-            if (hi > 0) d->buckets.push_back({0, hi});
+            std::vector<int64_t> offs;
+            for (const Param& p : d->params)
+                if (p.kind <= 1) offs.push_back(p.off);
+            std::vector<int64_t> lohi(2 * offs.size() + 2);
+            const int nb = sdb_plan_buckets(offs.data(), static_cast<int>(offs.size()), d->n_w, cap, lohi.data(),
+                                            static_cast<int>(offs.size()) + 1);
+            for (int i = 0; i < nb; ++i) d->buckets.push_back({lohi[2 * i], lohi[2 * i + 1]});
             for (size_t i = 0; i < d->buckets.size(); ++i) {
                 cudaEvent_t e;
                 CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));

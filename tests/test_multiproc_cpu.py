@@ -1,0 +1,92 @@
+"""Data-parallel host logic on CPU (no GPU): world-size-2 gloo processes run
+the control plane bench.py uses (NCCL-id broadcast, max-over-ranks timing,
+barriers), the global batch sharding of src/dataset.cpp:82-103, and the
+gradient-bucket plan of the C++ step driver."""
+import ctypes as C
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+import torch.multiprocessing as mp  # noqa: E402
+
+from paper_1903_05831_b200 import dist as dp  # noqa: E402
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    fake_id = bytes(range(128))
+    nid = dp.share_nccl_id(dist, rank, lambda: fake_id)
+    t = dp.max_over_ranks(dist, 10.0 + rank)
+    dist.barrier()
+    # GT / slots each rank would feed at step 3 with b = 2
+    slots = dp.global_slots(3, rank, world, 2)
+    from paper_1903_05831_b200 import detector as D
+    p = D.preset("c4")
+    gts = [D.make_gt(p, s) for s in slots]
+    q.put((rank, nid == fake_id, t, slots, [g[0].tolist() for g in gts]))
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_control_plane_and_sharding():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = sorted(q.get(timeout=120) for _ in range(2))
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    assert all(r[1] for r in res)                 # every rank received rank 0's communicator id
+    assert all(r[2] == 11.0 for r in res)          # max over ranks
+    # union of the two ranks' shards == the single-rank global batch of b = 4
+    union = res[0][3] + res[1][3]
+    assert union == dp.global_slots(3, 0, 1, 4)
+    from paper_1903_05831_b200 import detector as D
+    p = D.preset("c4")
+    single = [D.make_gt(p, s)[0].tolist() for s in union]
+    assert res[0][4] + res[1][4] == single         # identical ground truth regardless of K
+
+
+@pytest.mark.parametrize("world,b", [(1, 8), (2, 4), (4, 2), (8, 1)])
+def test_global_batch_identity(world, b):
+    """tests/test_trainer.cpp:116-126 analogue: K x b shards cover the same slots"""
+    for step in (1, 2, 7):
+        allslots = sorted(s for r in range(world) for s in dp.global_slots(step, r, world, b))
+        assert allslots == list(range((step - 1) * 8, step * 8))
+
+
+def test_bucket_plan_r50():
+    """the C++ driver's bucket plan on the R50-C4 gradient layout (fp16, 25 MB)"""
+    import paper_1903_05831_b200 as pkg
+    lb = pkg.lib()
+    # conv/fc slice sizes of R50-C4 in pack order (multiples of 8, as the driver aligns them)
+    rng = np.random.default_rng(0)
+    sizes = [64 * 7 * 7 * 8] + [int(s) * 8 for s in rng.integers(512, 300000, 60)]
+    offs = np.cumsum([0] + sizes[:-1]).astype(np.int64)
+    total = int(sum(sizes))
+    cap = 25 * 1024 * 1024 // 2
+    out = np.zeros(2 * (len(offs) + 1), np.int64)
+    fn = lb.sdb_plan_buckets
+    fn.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_int64, C.c_void_p, C.c_int]
+    nb = fn(offs.ctypes.data_as(C.c_void_p), len(offs), total, cap, out.ctypes.data_as(C.c_void_p), len(offs) + 1)
+    b = out[: 2 * nb].reshape(nb, 2)
+    assert b[0, 1] == total and b[-1, 0] == 0              # covers the buffer, last layers first
+    assert all(b[i, 0] == b[i + 1, 1] for i in range(nb - 1))  # contiguous, descending
+    assert set(b[:, 0]).issubset(set(offs.tolist()))        # boundaries at parameter starts
+    assert all((hi - lo) >= cap for lo, hi in b[:-1])       # every bucket but the last reaches the cap
+    assert nb == -(-total // cap) or nb == total // cap + 1 or nb <= total // cap + 1
