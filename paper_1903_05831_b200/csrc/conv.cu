@@ -48,17 +48,6 @@ struct ConvArgs {
 // ============================================================ tcgen05 kernel
 constexpr int kBM = 128, kBK = 64;
 
-template <int MODE, int BN, int ST>
-struct TcCfg {
-    static constexpr int kABytes = kBM * kBK * 2;
-    static constexpr int kBBytes = BN * kBK * 2;
-    static constexpr int kStage = kABytes + kBBytes;
-    static constexpr int kSmem = ST * kStage + 1024 + 256;
-    static constexpr bool kAMN = MODE == WGRAD;                  // A MN-major?
-    static constexpr bool kBMN = MODE == DGRAD || MODE == WGRAD; // B MN-major?
-    static constexpr int kLag = ST - 1;
-};
-
 // byte offset of 16B chunk inside a K-major SW128 tile: (row, chunk of 8 k)
 SDB_DEV uint32_t kmaj_off(int row, int chunk) {
     return static_cast<uint32_t>((row >> 3) * 1024 + (row & 7) * 128 + (((chunk ^ row) & 7) << 4));
@@ -70,316 +59,393 @@ SDB_DEV uint32_t mnmaj_off(int mc, int k, int E) {
                                  (((mc ^ k) & 7) << 4));
 }
 
+// Persistent, warp-specialised tcgen05 implicit GEMM.
+//   warps 0-3 : producers (implicit-im2col gathers with cp.async, 16 B chunks)
+//   warp  4   : MMA issuer (one elected lane) + TMEM owner
+//   warps 5-8 : epilogue (tcgen05.ld -> regs -> swizzled smem staging -> coalesced stores)
+// Two TMEM accumulators (2 x BN columns): the epilogue of tile i drains one
+// while the MMA of tile i+1 fills the other, so stores overlap the mainloop.
+// Tiles are strided over a grid of (SMs x CTAs/SM), m fastest (CTAs resident
+// together share the same filter tile in L2).
 template <int MODE, int BN, int ST>
-__global__ void __launch_bounds__(160, 1) conv_tc_kernel(ConvArgs a) {
-    using Cfg = TcCfg<MODE, BN, ST>;
+struct TcPCfg {
+    static constexpr int kABytes = kBM * kBK * 2;
+    static constexpr int kBBytes = BN * kBK * 2;
+    static constexpr int kStage = kABytes + kBBytes;
+    static constexpr int kStaging = 4 * 32 * 16 * 4;  // 4 epilogue warps x 32 rows x 16 fp32
+    static constexpr int kSmem = ST * kStage + kStaging + 1024 + 512;
+    static constexpr bool kAMN = MODE == WGRAD;
+    static constexpr bool kBMN = MODE == DGRAD || MODE == WGRAD;
+    static constexpr int kThreads = 288;
+};
+
+template <int MODE, int BN, int ST>
+__global__ void __launch_bounds__(288, (BN <= 128) ? 2 : 1) conv_tc_kernel(ConvArgs a, int tiles_m, int tiles_n, int n_tiles) {
+    using Cfg = TcPCfg<MODE, BN, ST>;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
     uint8_t* gbase = smem_raw + (base - raw);
-    uint64_t* full = reinterpret_cast<uint64_t*>(gbase + ST * Cfg::kStage);
+    float* staging = reinterpret_cast<float*>(gbase + ST * Cfg::kStage);
+    uint64_t* full = reinterpret_cast<uint64_t*>(gbase + ST * Cfg::kStage + Cfg::kStaging);
     uint64_t* empty = full + ST;
-    uint64_t* done = empty + ST;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+    uint64_t* tfull = empty + ST;   // [2]
+    uint64_t* tempty = tfull + 2;   // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
-    const int tid = threadIdx.x, warp = tid >> 5;
-    const int m0 = blockIdx.x * kBM, n0 = blockIdx.y * BN;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int nkb_total = (a.KG + kBK - 1) / kBK;
-    const int kb0 = MODE == WGRAD ? blockIdx.z * a.kb_per_split : 0;
-    const int nk = MODE == WGRAD ? max(0, min(a.kb_per_split, nkb_total - kb0)) : nkb_total;
 
     if (tid == 0) {
         for (int s = 0; s < ST; ++s) {
             mbar_init(&full[s], 128);
             mbar_init(&empty[s], 1);
         }
-        mbar_init(done, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 4);
+        }
         mbar_fence_init();
     }
-    if (warp == 4) tmem_alloc(tmem_slot, BN);
+    if (warp == 4) tmem_alloc(tmem_slot, 2 * BN);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    if (warp < 4) {
-        // ------------------------------------------------ producers
-        // All per-row / per-column address arithmetic is hoisted out of the
-        // k loop: per k-block each thread does at most one tap decomposition,
-        // and every chunk is a pointer add + bounds test (the instruction
-        // budget per k-block must stay below the MMA time of the k-block).
-        const __half* X = static_cast<const __half*>(a.x);
-        const __half* Wt = static_cast<const __half*>(a.w);
-        const int HoWo = a.Ho * a.Wo;
-        constexpr int kBChunksPerRow = BN / 8;           // MN-major B: chunks per k row
-        constexpr int kBRowStep = 128 / kBChunksPerRow;  // k rows advanced per i
-        // A rows (fprop/dgrad): per-row image/base coordinates
-        int rowN[8], rowY[8], rowX[8];
-        if (MODE == FPROP || MODE == DGRAD) {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const int m = m0 + (tid >> 3) + 16 * i;
-                if (m < a.M) {
-                    if (MODE == FPROP) {
-                        const int n = m / HoWo, rem = m - n * HoWo, oh = rem / a.Wo, ow = rem - oh * a.Wo;
-                        rowN[i] = n;
-                        rowY[i] = oh * a.stride - a.pad;
-                        rowX[i] = ow * a.stride - a.pad;
-                    } else {
-                        const int HpWp = a.Hp * a.Wp;
-                        const int n = m / HpWp, rem = m - n * HpWp, i2 = rem / a.Wp, j2 = rem - i2 * a.Wp;
-                        rowN[i] = n;
-                        // (h + p - r0) / st is exact: h = ph + st*i2 and r0 = (ph + p) mod st
-                        rowY[i] = (a.ph + a.stride * i2 + a.pad - a.r0) / a.stride;
-                        rowX[i] = (a.pw + a.stride * j2 + a.pad - a.q0) / a.stride;
-                    }
-                } else {
-                    rowN[i] = -1;
-                    rowY[i] = rowX[i] = -(1 << 28);
-                }
-            }
-        }
-        // fprop B: filter row offsets
-        int64_t brow[BN / 16];
-        if (MODE == FPROP) {
-#pragma unroll
-            for (int i = 0; i < BN / 16; ++i) {
-                const int j = n0 + (tid >> 3) + 16 * i;
-                brow[i] = j < a.NG ? static_cast<int64_t>(j) * a.KG : -1;
-            }
-        }
-        // dgrad B (MN-major filter [c][(tap,kout)]) and wgrad A/B: fixed column chunk
-        const int mcB = tid % kBChunksPerRow;
-        const int krowB = tid / kBChunksPerRow;
-        const int64_t RSC = static_cast<int64_t>(a.R) * a.S * a.C;
-        const bool dg_fast = (a.K % kBK) == 0;
-        int wg_r = 0, wg_s = 0, wg_c = 0;
-        bool wg_ok = false;
-        if (MODE == WGRAD) {
-            const int col = n0 + mcB * 8;
-            wg_ok = col < a.NG;
-            const int tap = col / a.C;
-            wg_c = col - tap * a.C;
-            wg_r = tap / a.S;
-            wg_s = tap - wg_r * a.S;
-        }
+    auto tile_coords = [&](int t, int& m0, int& n0, int& kb0, int& nk) {
+        const int tm = t % tiles_m;
+        const int rest = t / tiles_m;
+        const int tn = rest % tiles_n;
+        const int split = rest / tiles_n;
+        m0 = tm * kBM;
+        n0 = tn * BN;
+        kb0 = MODE == WGRAD ? split * a.kb_per_split : 0;
+        nk = MODE == WGRAD ? max(0, min(a.kb_per_split, nkb_total - kb0)) : nkb_total;
+    };
 
-        for (int it = 0; it < nk; ++it) {
-            const int s = it % ST;
-            if (it >= ST) mbar_wait(&empty[s], ((it / ST) - 1) & 1);
-            const uint32_t sa = base + s * Cfg::kStage;
-            const uint32_t sb = sa + Cfg::kABytes;
-            const int kb = kb0 + it;
+    if (warp < 4) {
+        int it = 0;  // global k-block counter (stage/phase continue across tiles)
+        for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+            int m0, n0, kb0, nk;
+            tile_coords(t, m0, n0, kb0, nk);
+// ------------------------------------------------ producers
+            // All per-row / per-column address arithmetic is hoisted out of the
+            // k loop: per k-block each thread does at most one tap decomposition,
+            // and every chunk is a pointer add + bounds test (the instruction
+            // budget per k-block must stay below the MMA time of the k-block).
+            const __half* X = static_cast<const __half*>(a.x);
+            const __half* Wt = static_cast<const __half*>(a.w);
+            const int HoWo = a.Ho * a.Wo;
+            constexpr int kBChunksPerRow = BN / 8;           // MN-major B: chunks per k row
+            constexpr int kBRowStep = 128 / kBChunksPerRow;  // k rows advanced per i
+            // A rows (fprop/dgrad): per-row image/base coordinates
+            int rowN[8], rowY[8], rowX[8];
+            if (MODE == FPROP || MODE == DGRAD) {
+    #pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int m = m0 + (tid >> 3) + 16 * i;
+                    if (m < a.M) {
+                        if (MODE == FPROP) {
+                            const int n = m / HoWo, rem = m - n * HoWo, oh = rem / a.Wo, ow = rem - oh * a.Wo;
+                            rowN[i] = n;
+                            rowY[i] = oh * a.stride - a.pad;
+                            rowX[i] = ow * a.stride - a.pad;
+                        } else {
+                            const int HpWp = a.Hp * a.Wp;
+                            const int n = m / HpWp, rem = m - n * HpWp, i2 = rem / a.Wp, j2 = rem - i2 * a.Wp;
+                            rowN[i] = n;
+                            // (h + p - r0) / st is exact: h = ph + st*i2 and r0 = (ph + p) mod st
+                            rowY[i] = (a.ph + a.stride * i2 + a.pad - a.r0) / a.stride;
+                            rowX[i] = (a.pw + a.stride * j2 + a.pad - a.q0) / a.stride;
+                        }
+                    } else {
+                        rowN[i] = -1;
+                        rowY[i] = rowX[i] = -(1 << 28);
+                    }
+                }
+            }
+            // fprop B: filter row offsets
+            int64_t brow[BN / 16];
             if (MODE == FPROP) {
-                const int kg = kb * kBK + 8 * (tid & 7);
-                const bool kok = kg < a.KG;
-                const int tap = kg / a.C, c = kg - tap * a.C;
-                const int r = tap / a.S, q = tap - r * a.S;
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    const int row = (tid >> 3) + 16 * i;
-                    const int ih = rowY[i] + r, iw = rowX[i] + q;
-                    const bool ok = kok && static_cast<unsigned>(ih) < static_cast<unsigned>(a.H) &&
-                                    static_cast<unsigned>(iw) < static_cast<unsigned>(a.W);
-                    const __half* src = ok ? X + ((static_cast<int64_t>(rowN[i]) * a.H + ih) * a.W + iw) * a.C + c : X;
-                    cp_async16(sa + kmaj_off(row, tid & 7), src, ok ? 16u : 0u);
-                }
-#pragma unroll
+    #pragma unroll
                 for (int i = 0; i < BN / 16; ++i) {
-                    const int row = (tid >> 3) + 16 * i;
-                    const bool ok = kok && brow[i] >= 0;
-                    cp_async16(sb + kmaj_off(row, tid & 7), ok ? Wt + brow[i] + kg : Wt, ok ? 16u : 0u);
+                    const int j = n0 + (tid >> 3) + 16 * i;
+                    brow[i] = j < a.NG ? static_cast<int64_t>(j) * a.KG : -1;
                 }
-            } else if (MODE == DGRAD) {
-                // A: DY gather, k-major over kg = tap*K + kout
-                const int kg = kb * kBK + 8 * (tid & 7);
-                const bool kok = kg < a.KG;
-                const int t = kg / a.K, kout = kg - t * a.K;
-                const int ti = t / a.nq, tq = t - ti * a.nq;
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    const int row = (tid >> 3) + 16 * i;
-                    const int oh = rowY[i] - ti, ow = rowX[i] - tq;
-                    const bool ok = kok && rowN[i] >= 0 && static_cast<unsigned>(oh) < static_cast<unsigned>(a.Ho) &&
-                                    static_cast<unsigned>(ow) < static_cast<unsigned>(a.Wo);
-                    const __half* src =
-                        ok ? X + ((static_cast<int64_t>(rowN[i]) * a.Ho + oh) * a.Wo + ow) * a.K + kout : X;
-                    cp_async16(sa + kmaj_off(row, tid & 7), src, ok ? 16u : 0u);
-                }
-                // B: filter as MN-major [c][kg]
-                const int c = n0 + mcB * 8;
-                const bool cok = c < a.NG;
-                if (dg_fast) {
-                    // the whole k-block lies in one tap: kout = kbk + krow
-                    const int kg0 = kb * kBK;
-                    const int t2 = kg0 / a.K, kbk = kg0 - t2 * a.K;
-                    const int r2 = a.r0 + a.stride * (t2 / a.nq), q2 = a.q0 + a.stride * (t2 % a.nq);
-                    const bool tok = kg0 < a.KG && cok;
-                    const __half* bsrc = Wt + static_cast<int64_t>(kbk + krowB) * RSC + (r2 * a.S + q2) * a.C + c;
-#pragma unroll
+            }
+            // dgrad B (MN-major filter [c][(tap,kout)]) and wgrad A/B: fixed column chunk
+            const int mcB = tid % kBChunksPerRow;
+            const int krowB = tid / kBChunksPerRow;
+            const int64_t RSC = static_cast<int64_t>(a.R) * a.S * a.C;
+            const bool dg_fast = (a.K % kBK) == 0;
+            int wg_r = 0, wg_s = 0, wg_c = 0;
+            bool wg_ok = false;
+            if (MODE == WGRAD) {
+                const int col = n0 + mcB * 8;
+                wg_ok = col < a.NG;
+                const int tap = col / a.C;
+                wg_c = col - tap * a.C;
+                wg_r = tap / a.S;
+                wg_s = tap - wg_r * a.S;
+            }
+
+            for (int k = 0; k < nk; ++k, ++it) {
+                const int s = it % ST;
+                if (it >= ST) mbar_wait(&empty[s], ((it / ST) - 1) & 1);
+                const uint32_t sa = base + s * Cfg::kStage;
+                const uint32_t sb = sa + Cfg::kABytes;
+                const int kb = kb0 + k;
+                if (MODE == FPROP) {
+                    const int kg = kb * kBK + 8 * (tid & 7);
+                    const bool kok = kg < a.KG;
+                    const int tap = kg / a.C, c = kg - tap * a.C;
+                    const int r = tap / a.S, q = tap - r * a.S;
+    #pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const int row = (tid >> 3) + 16 * i;
+                        const int ih = rowY[i] + r, iw = rowX[i] + q;
+                        const bool ok = kok && static_cast<unsigned>(ih) < static_cast<unsigned>(a.H) &&
+                                        static_cast<unsigned>(iw) < static_cast<unsigned>(a.W);
+                        const __half* src = ok ? X + ((static_cast<int64_t>(rowN[i]) * a.H + ih) * a.W + iw) * a.C + c : X;
+                        cp_async16(sa + kmaj_off(row, tid & 7), src, ok ? 16u : 0u);
+                    }
+    #pragma unroll
                     for (int i = 0; i < BN / 16; ++i) {
-                        const int krow = krowB + kBRowStep * i;
-                        cp_async16(sb + mnmaj_off(mcB, krow, BN), tok ? bsrc + kBRowStep * i * RSC : Wt, tok ? 16u : 0u);
+                        const int row = (tid >> 3) + 16 * i;
+                        const bool ok = kok && brow[i] >= 0;
+                        cp_async16(sb + kmaj_off(row, tid & 7), ok ? Wt + brow[i] + kg : Wt, ok ? 16u : 0u);
+                    }
+                } else if (MODE == DGRAD) {
+                    // A: DY gather, k-major over kg = tap*K + kout
+                    const int kg = kb * kBK + 8 * (tid & 7);
+                    const bool kok = kg < a.KG;
+                    const int t = kg / a.K, kout = kg - t * a.K;
+                    const int ti = t / a.nq, tq = t - ti * a.nq;
+    #pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const int row = (tid >> 3) + 16 * i;
+                        const int oh = rowY[i] - ti, ow = rowX[i] - tq;
+                        const bool ok = kok && rowN[i] >= 0 && static_cast<unsigned>(oh) < static_cast<unsigned>(a.Ho) &&
+                                        static_cast<unsigned>(ow) < static_cast<unsigned>(a.Wo);
+                        const __half* src =
+                            ok ? X + ((static_cast<int64_t>(rowN[i]) * a.Ho + oh) * a.Wo + ow) * a.K + kout : X;
+                        cp_async16(sa + kmaj_off(row, tid & 7), src, ok ? 16u : 0u);
+                    }
+                    // B: filter as MN-major [c][kg]
+                    const int c = n0 + mcB * 8;
+                    const bool cok = c < a.NG;
+                    if (dg_fast) {
+                        // the whole k-block lies in one tap: kout = kbk + krow
+                        const int kg0 = kb * kBK;
+                        const int t2 = kg0 / a.K, kbk = kg0 - t2 * a.K;
+                        const int r2 = a.r0 + a.stride * (t2 / a.nq), q2 = a.q0 + a.stride * (t2 % a.nq);
+                        const bool tok = kg0 < a.KG && cok;
+                        const __half* bsrc = Wt + static_cast<int64_t>(kbk + krowB) * RSC + (r2 * a.S + q2) * a.C + c;
+    #pragma unroll
+                        for (int i = 0; i < BN / 16; ++i) {
+                            const int krow = krowB + kBRowStep * i;
+                            cp_async16(sb + mnmaj_off(mcB, krow, BN), tok ? bsrc + kBRowStep * i * RSC : Wt, tok ? 16u : 0u);
+                        }
+                    } else {
+    #pragma unroll
+                        for (int i = 0; i < BN / 16; ++i) {
+                            const int krow = krowB + kBRowStep * i;
+                            const int kg2 = kb * kBK + krow;
+                            const bool ok = kg2 < a.KG && cok;
+                            const int t2 = kg2 / a.K, ko2 = kg2 - t2 * a.K;
+                            const int r2 = a.r0 + a.stride * (t2 / a.nq), q2 = a.q0 + a.stride * (t2 % a.nq);
+                            const __half* src = ok ? Wt + ((static_cast<int64_t>(ko2) * a.R + r2) * a.S + q2) * a.C + c : Wt;
+                            cp_async16(sb + mnmaj_off(mcB, krow, BN), src, ok ? 16u : 0u);
+                        }
                     }
                 } else {
-#pragma unroll
-                    for (int i = 0; i < BN / 16; ++i) {
-                        const int krow = krowB + kBRowStep * i;
-                        const int kg2 = kb * kBK + krow;
-                        const bool ok = kg2 < a.KG && cok;
-                        const int t2 = kg2 / a.K, ko2 = kg2 - t2 * a.K;
-                        const int r2 = a.r0 + a.stride * (t2 / a.nq), q2 = a.q0 + a.stride * (t2 % a.nq);
-                        const __half* src = ok ? Wt + ((static_cast<int64_t>(ko2) * a.R + r2) * a.S + q2) * a.C + c : Wt;
-                        cp_async16(sb + mnmaj_off(mcB, krow, BN), src, ok ? 16u : 0u);
+                    // WGRAD. A = DY^T as MN-major [kout][m]: chunk = 8 kout at one pixel row
+                    const __half* DY = static_cast<const __half*>(a.w);
+                    {
+                        const int mc = tid & 15;
+                        const int ko = m0 + mc * 8;
+                        const int mrow0 = kb * kBK + (tid >> 4);
+                        const __half* asrc = DY + static_cast<int64_t>(mrow0) * a.K + ko;
+    #pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            const int krow = (tid >> 4) + 8 * i;
+                            const bool ok = mrow0 + 8 * i < a.KG && ko < a.M;
+                            cp_async16(sa + mnmaj_off(mc, krow, kBM), ok ? asrc + static_cast<int64_t>(8 * i) * a.K : DY,
+                                       ok ? 16u : 0u);
+                        }
                     }
-                }
-            } else {
-                // WGRAD. A = DY^T as MN-major [kout][m]: chunk = 8 kout at one pixel row
-                const __half* DY = static_cast<const __half*>(a.w);
-                {
-                    const int mc = tid & 15;
-                    const int ko = m0 + mc * 8;
-                    const int mrow0 = kb * kBK + (tid >> 4);
-                    const __half* asrc = DY + static_cast<int64_t>(mrow0) * a.K + ko;
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        const int krow = (tid >> 4) + 8 * i;
-                        const bool ok = mrow0 + 8 * i < a.KG && ko < a.M;
-                        cp_async16(sa + mnmaj_off(mc, krow, kBM), ok ? asrc + static_cast<int64_t>(8 * i) * a.K : DY,
-                                   ok ? 16u : 0u);
-                    }
-                }
-                // B = im2col(X)^T as MN-major [(r,s,c)][m]; pixel walk is incremental
-                {
-                    int m = kb * kBK + krowB;
-                    int n = m / HoWo;
-                    int rem = m - n * HoWo;
-                    int oh = rem / a.Wo, ow = rem - oh * a.Wo;
-#pragma unroll
-                    for (int i = 0; i < BN / 16; ++i) {
-                        const int krow = krowB + kBRowStep * i;
-                        const int ih = oh * a.stride - a.pad + wg_r, iw = ow * a.stride - a.pad + wg_s;
-                        const bool ok = wg_ok && m < a.KG && static_cast<unsigned>(ih) < static_cast<unsigned>(a.H) &&
-                                        static_cast<unsigned>(iw) < static_cast<unsigned>(a.W);
-                        const __half* src = ok ? X + ((static_cast<int64_t>(n) * a.H + ih) * a.W + iw) * a.C + wg_c : X;
-                        cp_async16(sb + mnmaj_off(mcB, krow, BN), src, ok ? 16u : 0u);
-                        m += kBRowStep;
-                        ow += kBRowStep;
-                        while (ow >= a.Wo) {
-                            ow -= a.Wo;
-                            if (++oh == a.Ho) {
-                                oh = 0;
-                                ++n;
+                    // B = im2col(X)^T as MN-major [(r,s,c)][m]; pixel walk is incremental
+                    {
+                        int m = kb * kBK + krowB;
+                        int n = m / HoWo;
+                        int rem = m - n * HoWo;
+                        int oh = rem / a.Wo, ow = rem - oh * a.Wo;
+    #pragma unroll
+                        for (int i = 0; i < BN / 16; ++i) {
+                            const int krow = krowB + kBRowStep * i;
+                            const int ih = oh * a.stride - a.pad + wg_r, iw = ow * a.stride - a.pad + wg_s;
+                            const bool ok = wg_ok && m < a.KG && static_cast<unsigned>(ih) < static_cast<unsigned>(a.H) &&
+                                            static_cast<unsigned>(iw) < static_cast<unsigned>(a.W);
+                            const __half* src = ok ? X + ((static_cast<int64_t>(n) * a.H + ih) * a.W + iw) * a.C + wg_c : X;
+                            cp_async16(sb + mnmaj_off(mcB, krow, BN), src, ok ? 16u : 0u);
+                            m += kBRowStep;
+                            ow += kBRowStep;
+                            while (ow >= a.Wo) {
+                                ow -= a.Wo;
+                                if (++oh == a.Ho) {
+                                    oh = 0;
+                                    ++n;
+                                }
                             }
                         }
                     }
                 }
+                // the mbarrier arrival fires when THIS thread's copies of the stage
+                // land; the producer never blocks on its own loads
+                cp_async_mbar_arrive_noinc(&full[s]);
             }
-            // the mbarrier arrival fires when THIS thread's copies of the stage
-            // land; the producer never blocks on its own loads and runs ST
-            // stages ahead of the MMA (limited only by the empty barriers)
-            cp_async_mbar_arrive_noinc(&full[s]);
         }
         cp_async_wait<0>();
-
-        // ------------------------------------------------ epilogue
-        const int row_local = warp * 32 + (tid & 31);
-        const int grow = m0 + row_local;
-        if (nk > 0) {
-            mbar_wait(done, 0);
-            tc_fence_after();
-        }
-        // output row pointer
-        int64_t out_row = -1;
-        if (grow < a.M) {
-            if (MODE == FPROP) {
-                out_row = static_cast<int64_t>(grow) * a.NG;
-            } else if (MODE == DGRAD) {
-                const int HpWp = a.Hp * a.Wp;
-                const int n = grow / HpWp, rem = grow - n * HpWp, i2 = rem / a.Wp, j2 = rem - i2 * a.Wp;
-                const int h = a.ph + a.stride * i2, w = a.pw + a.stride * j2;
-                out_row = ((static_cast<int64_t>(n) * a.H + h) * a.W + w) * a.C;
-            } else {
-                out_row = (static_cast<int64_t>(blockIdx.z) * a.M + grow) * a.NG;
+    } else if (warp == 4) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = umma_idesc_f16(kBM, BN, Cfg::kAMN ? 1 : 0, Cfg::kBMN ? 1 : 0);
+            int it = 0, lt = 0;
+            for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++lt) {
+                int m0, n0, kb0, nk;
+                tile_coords(t, m0, n0, kb0, nk);
+                const int acc = lt & 1;
+                mbar_wait(&tempty[acc], ((lt >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t dcol = tmem + acc * BN;
+                for (int k = 0; k < nk; ++k, ++it) {
+                    const int s = it % ST;
+                    mbar_wait(&full[s], (it / ST) & 1);
+                    tc_fence_after();
+                    const uint32_t sa = base + s * Cfg::kStage;
+                    const uint32_t sb = sa + Cfg::kABytes;
+#pragma unroll
+                    for (int kk = 0; kk < kBK / 16; ++kk) {
+                        const uint64_t ad = Cfg::kAMN ? umma_desc_sw128(sa + kk * 2 * 2048, 1024, 2048)
+                                                      : umma_desc_sw128(sa + kk * 32, 16, 1024);
+                        const uint64_t bd = Cfg::kBMN
+                                                ? umma_desc_sw128(sb + kk * 2 * (BN / 64) * 1024, 1024, (BN / 64) * 1024)
+                                                : umma_desc_sw128(sb + kk * 32, 16, 1024);
+                        umma_f16(dcol, ad, bd, idesc, (k > 0 || kk > 0) ? 1u : 0u);
+                    }
+                    umma_commit(&empty[s]);
+                }
+                umma_commit(&tfull[acc]);
             }
         }
+        __syncwarp();
+    } else {
+        // ------------------------------------------------ epilogue warps 5..8
+        const int q = warp & 3;  // TMEM lane quadrant this warp may access
+        float* stg = staging + (warp - 5) * 32 * 16;
+        int lt = 0;
+        for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++lt) {
+            int m0, n0, kb0, nk;
+            tile_coords(t, m0, n0, kb0, nk);
+            const int acc = lt & 1;
+            mbar_wait(&tfull[acc], (lt >> 1) & 1);
+            tc_fence_after();
+            // row pointers of the 2 rows each lane stores in the coalesced phase
+            int64_t rowp[2];
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const int r = (k * 32 + lane) >> 1;  // 0..31
+                const int grow = m0 + q * 32 + r;
+                int64_t o = -1;
+                if (grow < a.M) {
+                    if (MODE == FPROP) {
+                        o = static_cast<int64_t>(grow) * a.NG;
+                    } else if (MODE == DGRAD) {
+                        const int HpWp = a.Hp * a.Wp;
+                        const int n = grow / HpWp, rem = grow - n * HpWp, i2 = rem / a.Wp, j2 = rem - i2 * a.Wp;
+                        o = ((static_cast<int64_t>(n) * a.H + a.ph + a.stride * i2) * a.W + a.pw + a.stride * j2) * a.C;
+                    } else {
+                        const int split = t / (tiles_m * tiles_n);
+                        o = (static_cast<int64_t>(split) * a.M + grow) * a.NG;
+                    }
+                }
+                rowp[k] = o;
+            }
+            const int lim = MODE == DGRAD ? a.C : a.NG;
 #pragma unroll 1
-        for (int cb = 0; cb < BN; cb += 32) {
-            uint32_t v[32];
-            if (nk > 0) {
-                tmem_ld32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + cb, v);
-            } else {
-#pragma unroll
-                for (int j = 0; j < 32; ++j) v[j] = 0u;
-            }
-            if (out_row < 0) continue;
-            const int col0 = n0 + cb;
-            if (MODE == WGRAD) {
-                float* o = static_cast<float*>(a.out) + out_row + col0;
-                if (col0 + 32 <= a.NG && (a.NG & 3) == 0) {
-#pragma unroll
-                    for (int j = 0; j < 32; j += 4)
-                        *reinterpret_cast<float4*>(o + j) = make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]),
-                                                                        __uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
-                } else {
-                    for (int j = 0; j < 32 && col0 + j < a.NG; ++j) o[j] = __uint_as_float(v[j]);
+            for (int cb = 0; cb < BN; cb += 16) {
+                uint32_t v[16];
+                tmem_ld16(tmem + acc * BN + (static_cast<uint32_t>(q * 32) << 16) + cb, v);
+                if (cb + 16 >= BN) {
+                    // accumulator fully drained into registers: hand it back to the MMA
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tempty[acc]);
                 }
-            } else {
-                __half* o = static_cast<__half*>(a.out) + out_row + col0;
-                const int lim = MODE == FPROP ? a.NG : a.C;
-                if (col0 + 32 <= lim && (lim & 7) == 0) {
+                if (nk == 0) {
 #pragma unroll
-                    for (int j = 0; j < 32; j += 8) {
-                        float f[8];
+                    for (int j = 0; j < 16; ++j) v[j] = 0u;
+                }
+                // stage row `lane` (16 fp32 = 4 x 16 B slots, XOR-swizzled: conflict-free)
 #pragma unroll
-                        for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(v[j + e]);
-                        if (MODE == DGRAD && a.accumulate) {
-                            const uint4 old = *reinterpret_cast<const uint4*>(o + j);
-                            const __half* oh = reinterpret_cast<const __half*>(&old);
+                for (int j = 0; j < 4; ++j) {
+                    const int slot = j ^ ((lane >> 1) & 3);
+                    *reinterpret_cast<float4*>(stg + lane * 16 + slot * 4) =
+                        make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                    __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+                }
+                __syncwarp();
+                const int col0 = n0 + cb;
 #pragma unroll
-                            for (int e = 0; e < 8; ++e) f[e] += __half2float(oh[e]);
+                for (int k = 0; k < 2; ++k) {
+                    const int idx = k * 32 + lane;
+                    const int r = idx >> 1, c8 = idx & 1;  // row, 8-column chunk
+                    const int j0 = 2 * c8, sw = (r >> 1) & 3;
+                    const float4 f0 = *reinterpret_cast<const float4*>(stg + r * 16 + ((j0 ^ sw) * 4));
+                    const float4 f1 = *reinterpret_cast<const float4*>(stg + r * 16 + (((j0 + 1) ^ sw) * 4));
+                    const int col = col0 + c8 * 8;
+                    if (rowp[k] < 0 || col >= lim) continue;
+                    float f[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
+                    if (MODE == WGRAD) {
+                        float* o = static_cast<float*>(a.out) + rowp[k] + col;
+                        if (col + 8 <= lim && (lim & 3) == 0) {
+                            *reinterpret_cast<float4*>(o) = f0;
+                            *reinterpret_cast<float4*>(o + 4) = f1;
+                        } else {
+                            for (int e = 0; e < 8 && col + e < lim; ++e) o[e] = f[e];
                         }
-                        uint4 pk;
-                        __half2* p2 = reinterpret_cast<__half2*>(&pk);
+                    } else {
+                        __half* o = static_cast<__half*>(a.out) + rowp[k] + col;
+                        if (col + 8 <= lim && (lim & 7) == 0) {
+                            if (MODE == DGRAD && a.accumulate) {
+                                const uint4 old = *reinterpret_cast<const uint4*>(o);
+                                const __half* oh = reinterpret_cast<const __half*>(&old);
 #pragma unroll
-                        for (int e = 0; e < 4; ++e) p2[e] = __floats2half2_rn(f[2 * e], f[2 * e + 1]);
-                        *reinterpret_cast<uint4*>(o + j) = pk;
-                    }
-                } else {
-                    for (int j = 0; j < 32 && col0 + j < lim; ++j) {
-                        float f = __uint_as_float(v[j]);
-                        if (MODE == DGRAD && a.accumulate) f += __half2float(o[j]);
-                        o[j] = __float2half_rn(f);
+                                for (int e = 0; e < 8; ++e) f[e] += __half2float(oh[e]);
+                            }
+                            uint4 pk;
+                            __half2* p2 = reinterpret_cast<__half2*>(&pk);
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) p2[e] = __floats2half2_rn(f[2 * e], f[2 * e + 1]);
+                            *reinterpret_cast<uint4*>(o) = pk;
+                        } else {
+                            for (int e = 0; e < 8 && col + e < lim; ++e) {
+                                float x = f[e];
+                                if (MODE == DGRAD && a.accumulate) x += __half2float(o[e]);
+                                o[e] = __float2half_rn(x);
+                            }
+                        }
                     }
                 }
+                __syncwarp();
             }
         }
-    } else if (tid == 128) {
-        // ------------------------------------------------ MMA issuer (one thread)
-        constexpr uint32_t idesc = umma_idesc_f16(kBM, BN, Cfg::kAMN ? 1 : 0, Cfg::kBMN ? 1 : 0);
-        for (int it = 0; it < nk; ++it) {
-            const int s = it % ST;
-            mbar_wait(&full[s], (it / ST) & 1);
-            tc_fence_after();
-            const uint32_t sa = base + s * Cfg::kStage;
-            const uint32_t sb = sa + Cfg::kABytes;
-#pragma unroll
-            for (int kk = 0; kk < kBK / 16; ++kk) {
-                const uint64_t ad = Cfg::kAMN ? umma_desc_sw128(sa + kk * 2 * 2048, 1024, 2048)
-                                              : umma_desc_sw128(sa + kk * 32, 16, 1024);
-                const uint64_t bd = Cfg::kBMN ? umma_desc_sw128(sb + kk * 2 * (BN / 64) * 1024, 1024, (BN / 64) * 1024)
-                                              : umma_desc_sw128(sb + kk * 32, 16, 1024);
-                umma_f16(tmem, ad, bd, idesc, (it > 0 || kk > 0) ? 1u : 0u);
-            }
-            umma_commit(&empty[s]);
-        }
-        if (nk > 0) umma_commit(done);
     }
     tc_fence_before();
     __syncthreads();
     if (warp == 4) {
         tc_fence_after();
-        tmem_dealloc(tmem, BN);
+        tmem_dealloc(tmem, 2 * BN);
     }
 }
 
@@ -527,14 +593,19 @@ __global__ void dgrad_zero_phase_kernel(ConvArgs a) {
 // ============================================================ launchers
 template <int MODE, int BN, int ST>
 static cudaError_t launch_tc(const ConvArgs& a, int splits, cudaStream_t st) {
-    using Cfg = TcCfg<MODE, BN, ST>;
+    using Cfg = TcPCfg<MODE, BN, ST>;
     static bool configured = false;
     if (!configured) {
         cudaFuncSetAttribute(conv_tc_kernel<MODE, BN, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
         configured = true;
     }
-    dim3 grid((a.M + kBM - 1) / kBM, (a.NG + BN - 1) / BN, splits);
-    conv_tc_kernel<MODE, BN, ST><<<grid, 160, Cfg::kSmem, st>>>(a);
+    const int tiles_m = (a.M + kBM - 1) / kBM, tiles_n = (a.NG + BN - 1) / BN;
+    const int n_tiles = tiles_m * tiles_n * splits;
+    // resident CTAs per SM: TMEM holds 512 columns (2 accumulators of BN each) and
+    // 227 KB of shared memory
+    const int per_sm = (4 * BN <= 512 && 2 * (Cfg::kSmem + 1024) <= 228 * 1024) ? 2 : 1;
+    const int grid = std::min(n_tiles, per_sm * kNumSMs);
+    conv_tc_kernel<MODE, BN, ST><<<grid, Cfg::kThreads, Cfg::kSmem, st>>>(a, tiles_m, tiles_n, n_tiles);
     return cudaGetLastError();
 }
 
