@@ -24,6 +24,9 @@
 // counts.
 #include <algorithm>
 #include <cstdio>
+#include <cstring>
+
+#include <cuda.h>
 
 #include "common.cuh"
 #include "sdb_internal.h"
@@ -43,6 +46,12 @@ struct ConvArgs {
     // wgrad split-K
     int kb_per_split;
     int accumulate;  // dgrad: out += result
+    int tma_b;       // dgrad: filter operand loaded by TMA (needs K % 64 == 0)
+};
+
+// TMA descriptors of the dense GEMM operand (filter for fprop/dgrad, DY for wgrad)
+struct alignas(64) TmaDesc {
+    CUtensorMap m;
 };
 
 // ============================================================ tcgen05 kernel
@@ -80,7 +89,8 @@ struct TcPCfg {
 };
 
 template <int MODE, int BN, int ST>
-__global__ void __launch_bounds__(288, (BN <= 128) ? 2 : 1) conv_tc_kernel(ConvArgs a, int tiles_m, int tiles_n, int n_tiles) {
+__global__ void __launch_bounds__(288, (BN <= 128) ? 2 : 1)
+    conv_tc_kernel(ConvArgs a, int tiles_m, int tiles_n, int n_tiles, const __grid_constant__ TmaDesc tma) {
     using Cfg = TcPCfg<MODE, BN, ST>;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
@@ -96,9 +106,13 @@ __global__ void __launch_bounds__(288, (BN <= 128) ? 2 : 1) conv_tc_kernel(ConvA
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int nkb_total = (a.KG + kBK - 1) / kBK;
 
+    // the dense operand arrives by TMA (fprop B, wgrad A, dgrad B when K % 64 == 0):
+    // one extra arrive.expect_tx per stage on top of the 128 cp.async arrivals
+    const bool use_tma = MODE == FPROP || MODE == WGRAD || (MODE == DGRAD && a.tma_b);
     if (tid == 0) {
+        prefetch_tmap(&tma.m);
         for (int s = 0; s < ST; ++s) {
-            mbar_init(&full[s], 128);
+            mbar_init(&full[s], use_tma ? 129 : 128);
             mbar_init(&empty[s], 1);
         }
         for (int i = 0; i < 2; ++i) {
@@ -210,11 +224,10 @@ __global__ void __launch_bounds__(288, (BN <= 128) ? 2 : 1) conv_tc_kernel(ConvA
                         const __half* src = ok ? X + ((static_cast<int64_t>(rowN[i]) * a.H + ih) * a.W + iw) * a.C + c : X;
                         cp_async16(sa + kmaj_off(row, tid & 7), src, ok ? 16u : 0u);
                     }
-    #pragma unroll
-                    for (int i = 0; i < BN / 16; ++i) {
-                        const int row = (tid >> 3) + 16 * i;
-                        const bool ok = kok && brow[i] >= 0;
-                        cp_async16(sb + kmaj_off(row, tid & 7), ok ? Wt + brow[i] + kg : Wt, ok ? 16u : 0u);
+                    // B: the filter tile [BN rows][64 k] in one TMA box (zero-filled out of range)
+                    if (tid == 0) {
+                        mbar_arrive_expect_tx(&full[s], BN * kBK * 2);
+                        tma_load_2d(sb, &tma.m, &full[s], kb * kBK, n0);
                     }
                 } else if (MODE == DGRAD) {
                     // A: DY gather, k-major over kg = tap*K + kout
@@ -235,7 +248,18 @@ __global__ void __launch_bounds__(288, (BN <= 128) ? 2 : 1) conv_tc_kernel(ConvA
                     // B: filter as MN-major [c][kg]
                     const int c = n0 + mcB * 8;
                     const bool cok = c < a.NG;
-                    if (dg_fast) {
+                    if (a.tma_b) {
+                        // one 3-D box [64 kout][1 tap][64 c] per 64-channel MN atom
+                        if (tid == 0) {
+                            const int kg0 = kb * kBK;
+                            const int t2 = kg0 / a.K, kbk = kg0 - t2 * a.K;
+                            const int r2 = a.r0 + a.stride * (t2 / a.nq), q2 = a.q0 + a.stride * (t2 % a.nq);
+                            mbar_arrive_expect_tx(&full[s], BN * kBK * 2);
+#pragma unroll
+                            for (int g = 0; g < BN / 64; ++g)
+                                tma_load_3d(sb + g * 8192, &tma.m, &full[s], n0 + 64 * g, r2 * a.S + q2, kbk);
+                        }
+                    } else if (dg_fast) {
                         // the whole k-block lies in one tap: kout = kbk + krow
                         const int kg0 = kb * kBK;
                         const int t2 = kg0 / a.K, kbk = kg0 - t2 * a.K;
@@ -260,20 +284,11 @@ __global__ void __launch_bounds__(288, (BN <= 128) ? 2 : 1) conv_tc_kernel(ConvA
                         }
                     }
                 } else {
-                    // WGRAD. A = DY^T as MN-major [kout][m]: chunk = 8 kout at one pixel row
-                    const __half* DY = static_cast<const __half*>(a.w);
-                    {
-                        const int mc = tid & 15;
-                        const int ko = m0 + mc * 8;
-                        const int mrow0 = kb * kBK + (tid >> 4);
-                        const __half* asrc = DY + static_cast<int64_t>(mrow0) * a.K + ko;
-    #pragma unroll
-                        for (int i = 0; i < 8; ++i) {
-                            const int krow = (tid >> 4) + 8 * i;
-                            const bool ok = mrow0 + 8 * i < a.KG && ko < a.M;
-                            cp_async16(sa + mnmaj_off(mc, krow, kBM), ok ? asrc + static_cast<int64_t>(8 * i) * a.K : DY,
-                                       ok ? 16u : 0u);
-                        }
+                    // WGRAD. A = DY^T as MN-major [kout][m]: two TMA boxes [64 pixels][64 kout]
+                    if (tid == 0) {
+                        mbar_arrive_expect_tx(&full[s], kBM * kBK * 2);
+                        tma_load_2d(sa, &tma.m, &full[s], m0, kb * kBK);
+                        tma_load_2d(sa + 8192, &tma.m, &full[s], m0 + 64, kb * kBK);
                     }
                     // B = im2col(X)^T as MN-major [(r,s,c)][m]; pixel walk is incremental
                     {
@@ -326,11 +341,15 @@ __global__ void __launch_bounds__(288, (BN <= 128) ? 2 : 1) conv_tc_kernel(ConvA
                     const uint32_t sb = sa + Cfg::kABytes;
 #pragma unroll
                     for (int kk = 0; kk < kBK / 16; ++kk) {
-                        const uint64_t ad = Cfg::kAMN ? umma_desc_sw128(sa + kk * 2 * 2048, 1024, 2048)
+                        // TMA-loaded MN-major operands: 8 KB per 64-element MN atom (LBO),
+                        // 1 KB per 8 k-rows (SBO); cp.async MN-major B interleaves the atoms
+                        const uint64_t ad = Cfg::kAMN ? umma_desc_sw128(sa + kk * 2048, 8192, 1024)
                                                       : umma_desc_sw128(sa + kk * 32, 16, 1024);
-                        const uint64_t bd = Cfg::kBMN
-                                                ? umma_desc_sw128(sb + kk * 2 * (BN / 64) * 1024, 1024, (BN / 64) * 1024)
-                                                : umma_desc_sw128(sb + kk * 32, 16, 1024);
+                        const uint64_t bd =
+                            !Cfg::kBMN ? umma_desc_sw128(sb + kk * 32, 16, 1024)
+                            : (MODE == DGRAD && a.tma_b)
+                                ? umma_desc_sw128(sb + kk * 2048, 8192, 1024)
+                                : umma_desc_sw128(sb + kk * 2 * (BN / 64) * 1024, 1024, (BN / 64) * 1024);
                         umma_f16(dcol, ad, bd, idesc, (k > 0 || kk > 0) ? 1u : 0u);
                     }
                     umma_commit(&empty[s]);
@@ -591,6 +610,34 @@ __global__ void dgrad_zero_phase_kernel(ConvArgs a) {
 }
 
 // ============================================================ launchers
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static bool make_tmap(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
+                      const uint32_t* box) {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&fn), cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return false;
+    }
+    cuuint64_t d[5], st[4];
+    cuuint32_t b[5], es[5];
+    for (int i = 0; i < rank; ++i) {
+        d[i] = dims[i];
+        b[i] = box[i];
+        es[i] = 1;
+        if (i + 1 < rank) st[i] = strides[i];
+    }
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, rank, const_cast<void*>(base), d, st, b, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int MODE, int BN, int ST>
 static cudaError_t launch_tc(const ConvArgs& a, int splits, cudaStream_t st) {
     using Cfg = TcPCfg<MODE, BN, ST>;
@@ -605,7 +652,30 @@ static cudaError_t launch_tc(const ConvArgs& a, int splits, cudaStream_t st) {
     // 227 KB of shared memory
     const int per_sm = (4 * BN <= 512 && 2 * (Cfg::kSmem + 1024) <= 228 * 1024) ? 2 : 1;
     const int grid = std::min(n_tiles, per_sm * kNumSMs);
-    conv_tc_kernel<MODE, BN, ST><<<grid, Cfg::kThreads, Cfg::kSmem, st>>>(a, tiles_m, tiles_n, n_tiles);
+    TmaDesc tma;
+    std::memset(&tma, 0, sizeof(tma));
+    bool ok = true;
+    if (MODE == FPROP) {
+        // filter [K][R*S*C] fp16, box [BN rows][64 k]
+        const uint64_t dims[2] = {static_cast<uint64_t>(a.KG), static_cast<uint64_t>(a.NG)};
+        const uint64_t strides[1] = {static_cast<uint64_t>(a.KG) * 2};
+        const uint32_t box[2] = {64, static_cast<uint32_t>(BN)};
+        ok = make_tmap(&tma.m, a.w, 2, dims, strides, box);
+    } else if (MODE == DGRAD && a.tma_b) {
+        // filter [K][R*S][C] fp16, box [64 kout][1 tap][64 c]
+        const uint64_t dims[3] = {static_cast<uint64_t>(a.C), static_cast<uint64_t>(a.R) * a.S, static_cast<uint64_t>(a.K)};
+        const uint64_t strides[2] = {static_cast<uint64_t>(a.C) * 2, static_cast<uint64_t>(a.R) * a.S * a.C * 2};
+        const uint32_t box[3] = {64, 1, 64};
+        ok = make_tmap(&tma.m, a.w, 3, dims, strides, box);
+    } else if (MODE == WGRAD) {
+        // DY [pixels][K] fp16, box [64 pixels][64 kout]
+        const uint64_t dims[2] = {static_cast<uint64_t>(a.M), static_cast<uint64_t>(a.KG)};
+        const uint64_t strides[1] = {static_cast<uint64_t>(a.M) * 2};
+        const uint32_t box[2] = {64, 64};
+        ok = make_tmap(&tma.m, a.w, 2, dims, strides, box);
+    }
+    if (!ok) return cudaErrorInvalidValue;
+    conv_tc_kernel<MODE, BN, ST><<<grid, Cfg::kThreads, Cfg::kSmem, st>>>(a, tiles_m, tiles_n, n_tiles, tma);
     return cudaGetLastError();
 }
 
@@ -690,6 +760,7 @@ cudaError_t conv_dgrad(const ConvShape& g, int dtype, const void* dy, const void
             if (a.KG == 0) {
                 continue;  // zeroed above (or untouched when accumulating)
             } else if (tc_ok(g, dtype)) {
+                a.tma_b = (g.K % kBK) == 0 ? 1 : 0;
                 e = launch_tc_pick<DGRAD>(a, 1, st);
             } else {
                 e = dtype == kF16 ? launch_simt<__half, DGRAD>(a, 1, st) : launch_simt<float, DGRAD>(a, 1, st);
