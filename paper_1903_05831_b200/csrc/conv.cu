@@ -45,7 +45,8 @@ struct ConvArgs {
     int ph, pw, Hp, Wp, r0, nr, q0, nq;
     // wgrad split-K
     int kb_per_split;
-    int accumulate;  // dgrad: out += result
+    int accumulate;  // dgrad: out = result + addend
+    const void* addend;  // dgrad accumulate source (may alias out)
     int tma_b;       // dgrad: filter operand loaded by TMA (needs K % 64 == 0)
 };
 
@@ -393,6 +394,16 @@ __global__ void __launch_bounds__(288, (BN <= 128) ? 2 : 1)
             const int lim = MODE == DGRAD ? a.C : a.NG;
 #pragma unroll 1
             for (int cb = 0; cb < BN; cb += 16) {
+                // residual fan-in: fetch the addend first so its latency overlaps the TMEM drain
+                uint4 addv[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+                if (MODE == DGRAD && a.accumulate) {
+#pragma unroll
+                    for (int k = 0; k < 2; ++k) {
+                        const int col = n0 + cb + (((k * 32 + lane) & 1) * 8);
+                        if (rowp[k] >= 0 && col + 8 <= lim && (lim & 7) == 0)
+                            addv[k] = *reinterpret_cast<const uint4*>(static_cast<const __half*>(a.addend) + rowp[k] + col);
+                    }
+                }
                 uint32_t v[16];
                 tmem_ld16(tmem + acc * BN + (static_cast<uint32_t>(q * 32) << 16) + cb, v);
                 if (cb + 16 >= BN) {
@@ -437,8 +448,7 @@ __global__ void __launch_bounds__(288, (BN <= 128) ? 2 : 1)
                         __half* o = static_cast<__half*>(a.out) + rowp[k] + col;
                         if (col + 8 <= lim && (lim & 7) == 0) {
                             if (MODE == DGRAD && a.accumulate) {
-                                const uint4 old = *reinterpret_cast<const uint4*>(o);
-                                const __half* oh = reinterpret_cast<const __half*>(&old);
+                                const __half* oh = reinterpret_cast<const __half*>(&addv[k]);
 #pragma unroll
                                 for (int e = 0; e < 8; ++e) f[e] += __half2float(oh[e]);
                             }
@@ -450,7 +460,8 @@ __global__ void __launch_bounds__(288, (BN <= 128) ? 2 : 1)
                         } else {
                             for (int e = 0; e < 8 && col + e < lim; ++e) {
                                 float x = f[e];
-                                if (MODE == DGRAD && a.accumulate) x += __half2float(o[e]);
+                                if (MODE == DGRAD && a.accumulate)
+                                    x += __half2float(static_cast<const __half*>(a.addend)[rowp[k] + col + e]);
                                 o[e] = __float2half_rn(x);
                             }
                         }
@@ -576,7 +587,7 @@ __global__ void __launch_bounds__(256) conv_simt_kernel(ConvArgs a) {
             } else {
                 T* o = static_cast<T*>(a.out) + row + n;
                 float f = acc[i][j];
-                if (MODE == DGRAD && a.accumulate) f += to_f<T>(*o);
+                if (MODE == DGRAD && a.accumulate) f += to_f<T>(static_cast<const T*>(a.addend)[o - static_cast<T*>(a.out)]);
                 *o = from_f<T>(f);
             }
         }
@@ -725,9 +736,10 @@ cudaError_t conv_fprop(const ConvShape& g, int dtype, const void* x, const void*
 }
 
 cudaError_t conv_dgrad(const ConvShape& g, int dtype, const void* dy, const void* w, void* dx, int accumulate,
-                       cudaStream_t st) {
+                       cudaStream_t st, const void* addend) {
     ConvArgs base = make_args(g);
-    base.x = dy; base.w = w; base.out = dx; base.accumulate = accumulate;
+    base.x = dy; base.w = w; base.out = dx; base.accumulate = accumulate || addend != nullptr;
+    base.addend = addend ? addend : dx;
     base.NG = g.C;
     const int sd = g.stride;
     // phases whose taps are all empty (e.g. the odd pixels of a 1x1 stride-2
@@ -739,7 +751,15 @@ cudaError_t conv_dgrad(const ConvShape& g, int dtype, const void* dy, const void
             const int r0 = (ph + g.pad) % sd, q0 = (pw + g.pad) % sd;
             if (r0 >= g.R || q0 >= g.S) empty_phase = true;
         }
-    if (empty_phase && !accumulate) {
+    if (empty_phase && base.accumulate && base.addend != dx) {
+        // taps never reach some output phases: those positions take the addend as is
+        const cudaError_t e = cudaMemcpyAsync(dx, base.addend,
+                                              static_cast<size_t>(g.N) * g.H * g.W * g.C * (dtype == kF16 ? 2 : 4),
+                                              cudaMemcpyDeviceToDevice, st);
+        if (e != cudaSuccess) return e;
+        base.addend = dx;
+    }
+    if (empty_phase && !base.accumulate) {
         const cudaError_t e = cudaMemsetAsync(dx, 0, static_cast<size_t>(g.N) * g.H * g.W * g.C * (dtype == kF16 ? 2 : 4), st);
         if (e != cudaSuccess) return e;
     }

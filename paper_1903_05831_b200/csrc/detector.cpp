@@ -116,6 +116,8 @@ struct Prof {
     std::vector<cudaEvent_t> pool;
     size_t used = 0;
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> recs;
+    std::vector<std::string> labels;
+    std::vector<double> rec_flops;
     double flops[P_NCAT] = {}, bytes[P_NCAT] = {};
     int64_t launches[P_NCAT] = {};
     cudaEvent_t get() {
@@ -181,6 +183,8 @@ struct sdb_det {
     float* h_gt = nullptr;
     int32_t *h_cls = nullptr, *h_cnt = nullptr;
     uint64_t* h_keys = nullptr;
+    int64_t* h_slots = nullptr;
+    int64_t* slots_dev = nullptr;
     double* h_losses = nullptr;
     // comm
     cudaStream_t comm = nullptr;
@@ -275,8 +279,19 @@ struct PScope {
         cudaEvent_t e1 = d->prof.get();
         cudaEventRecord(e1, d->ctx->stream);
         d->prof.recs.push_back({cat, {e0, e1}});
+        d->prof.labels.push_back(label);
+        d->prof.rec_flops.push_back(flops_);
     }
+    std::string label;
+    double flops_ = 0;
 };
+
+std::string shape_label(const char* what, const ConvShape& g) {
+    char buf[160];
+    std::snprintf(buf, sizeof buf, "%s N%d H%d W%d C%d K%d R%d S%d st%d", what, g.N, g.H, g.W, g.C, g.K, g.R, g.S,
+                  g.stride);
+    return buf;
+}
 
 double conv_flops(const ConvShape& g) {
     return 2.0 * g.N * g.Ho() * g.Wo() * static_cast<double>(g.K) * g.C * g.R * g.S;
@@ -397,6 +412,7 @@ size_t max_ws(sdb_det* d) {
 // ------------------------------------------------------------------ forward helpers
 void conv_fwd(sdb_det* d, const ConvL& c, const Act& x, const Act& y) {
     PScope ps(d, P_FPROP, conv_flops(c.g));
+    if (d->prof.on) { ps.label = shape_label("fprop", c.g); ps.flops_ = conv_flops(c.g); }
     CK(conv_fprop(c.g, d->dt, x.p, d->wdev_ptr(c.p), y.p, d->ctx->stream));
 }
 
@@ -438,9 +454,10 @@ void block_fwd(sdb_det* d, Block& b) {
 }
 
 // ------------------------------------------------------------------ backward helpers
-void dgrad(sdb_det* d, const ConvL& c, const void* dy, void* dx, int accumulate) {
+void dgrad(sdb_det* d, const ConvL& c, const void* dy, void* dx, int accumulate, const void* addend = nullptr) {
     PScope ps(d, P_DGRAD, conv_flops(c.g), 0, c.g.stride * c.g.stride);
-    CK(conv_dgrad(c.g, d->dt, dy, d->wdev_ptr(c.p), dx, accumulate, d->ctx->stream));
+    if (d->prof.on) { ps.label = shape_label("dgrad", c.g); ps.flops_ = conv_flops(c.g); }
+    CK(conv_dgrad(c.g, d->dt, dy, d->wdev_ptr(c.p), dx, accumulate, d->ctx->stream, addend));
 }
 
 struct Bwd {
@@ -468,6 +485,7 @@ void conv_wgrad_to(Bwd& B, const ConvL& c, const Act& x, const void* dy) {
     sdb_det* d = B.d;
     {
     PScope ps(d, P_WGRAD, conv_flops(c.g), 0, 2);
+    if (d->prof.on) { ps.label = shape_label("wgrad", c.g); ps.flops_ = conv_flops(c.g); }
     CK(conv_wgrad(c.g, d->dt, x.p, dy, d->gptr(c.p), d->ws, d->ws_bytes, d->ctx->stream));
     }
     grads_ready(B, c.p);
@@ -490,9 +508,6 @@ void block_bwd(Bwd& B, Block& b, void* dout, void* dx, void* s0, void* s1, void*
         norm_bwd(d, b.nd, b.zd, b.d, dS, s1);
         conv_wgrad_to(B, b.down, b.in, s1);
         dgrad(d, b.down, s1, dx, 0);
-    } else {
-        PScope ps(d, P_ELEM, 0, 2.0 * d->es * b.in.numel(), 0);
-        CK(cudaMemcpyAsync(dx, dS, b.in.numel() * d->es, cudaMemcpyDeviceToDevice, st));
     }
     norm_bwd(d, b.n3, b.z3, b.b3, dS, s1);
     conv_wgrad_to(B, b.c3, b.a2, s1);
@@ -502,7 +517,9 @@ void block_bwd(Bwd& B, Block& b, void* dout, void* dx, void* s0, void* s1, void*
     dgrad(d, b.c2, s1, s2, 0);
     norm_bwd(d, b.n1, b.z1, b.a1, s2, s1);
     conv_wgrad_to(B, b.c1, b.in, s1);
-    dgrad(d, b.c1, s1, dx, 1);
+    // residual fan-in in the dgrad epilogue: dx = conv1^T(dz1) + (down-path dx | identity dS)
+    if (b.has_down) dgrad(d, b.c1, s1, dx, 1);
+    else dgrad(d, b.c1, s1, dx, 1, dS);
 }
 
 // ------------------------------------------------------------------ the step
@@ -825,6 +842,8 @@ int sdb_det_create(sdb_ctx* ctx, const sdb_det_config* cfgp, sdb_det** out) {
         CK(cudaMallocHost(&d->h_cls, static_cast<size_t>(b) * cf.max_gt * 4));
         CK(cudaMallocHost(&d->h_cnt, b * 4));
         CK(cudaMallocHost(&d->h_keys, 2 * b * 8));
+        CK(cudaMallocHost(&d->h_slots, b * 8));
+        d->slots_dev = static_cast<int64_t*>(d->alloc(b * 8));
         CK(cudaMallocHost(&d->h_losses, 16 * 8));
 
         // ---- comm: fp16 buckets from the end of the flat gradient (backward order)
@@ -865,6 +884,7 @@ int sdb_det_destroy(sdb_det* d) {
     cudaFreeHost(d->h_cls);
     cudaFreeHost(d->h_cnt);
     cudaFreeHost(d->h_keys);
+    cudaFreeHost(d->h_slots);
     cudaFreeHost(d->h_losses);
     for (auto e : d->bucket_ev) cudaEventDestroy(e);
     if (d->comm) {
@@ -998,11 +1018,13 @@ int sdb_det_set_batch(sdb_det* d, const void* images, int on_host, const float* 
 
 int sdb_det_synth_images(sdb_det* d, const int64_t* slots) {
     try {
-        int64_t* ds = static_cast<int64_t*>(d->ws);
-        CK(cudaMemcpy(ds, slots, d->cfg.batch * 8, cudaMemcpyHostToDevice));
-        CK(synth_images(d->dt, d->img.p, d->cfg.batch, d->cfg.img_h, d->cfg.img_w, 8, d->cfg.seed, ds, 0,
-                        d->ctx->stream));
-        CK(cudaStreamSynchronize(d->ctx->stream));
+        // stream-ordered after the previous step (never touch the step workspace:
+        // the previous step may still be running on the context stream)
+        cudaStream_t st = d->ctx->stream;
+        CK(cudaStreamSynchronize(st));
+        std::memcpy(d->h_slots, slots, d->cfg.batch * 8);
+        CK(cudaMemcpyAsync(d->slots_dev, d->h_slots, d->cfg.batch * 8, cudaMemcpyHostToDevice, st));
+        CK(synth_images(d->dt, d->img.p, d->cfg.batch, d->cfg.img_h, d->cfg.img_w, 8, d->cfg.seed, d->slots_dev, 0, st));
     } catch (const std::exception& e) {
         return det_fail(SDB_CUDA, e.what());
     }
@@ -1127,6 +1149,8 @@ int sdb_det_profile(sdb_det* d, double* ms, double* flops, double* bytes, int64_
         Prof& p = d->prof;
         p.used = 0;
         p.recs.clear();
+        p.labels.clear();
+        p.rec_flops.clear();
         std::fill(p.flops, p.flops + P_NCAT, 0.0);
         std::fill(p.bytes, p.bytes + P_NCAT, 0.0);
         std::fill(p.launches, p.launches + P_NCAT, 0);
@@ -1135,11 +1159,18 @@ int sdb_det_profile(sdb_det* d, double* ms, double* flops, double* bytes, int64_
         p.on = false;
         CK(cudaStreamSynchronize(d->ctx->stream));
         std::vector<double> acc(P_NCAT, 0.0);
-        for (auto& r : p.recs) {
+        const bool verbose = std::getenv("SDB_PROFILE_VERBOSE") != nullptr;
+        for (size_t k = 0; k < p.recs.size(); ++k) {
+            auto& r = p.recs[k];
             float t = 0;
             CK(cudaEventElapsedTime(&t, r.second.first, r.second.second));
             acc[r.first] += t;
+            if (verbose && !p.labels[k].empty())
+                std::fprintf(stderr, "[sdb-prof] %-60s %8.1f us %7.0f TF/s\n", p.labels[k].c_str(), t * 1e3,
+                             p.rec_flops[k] / (t * 1e-3) / 1e12);
         }
+        p.labels.clear();
+        p.rec_flops.clear();
         for (int i = 0; i < ncat && i < P_NCAT; ++i) {
             if (ms) ms[i] = acc[i];
             if (flops) flops[i] = p.flops[i];
