@@ -89,7 +89,11 @@ __global__ void __launch_bounds__(kThreads, 2) stats_kernel(StatArgs p) {
     const int c0 = cg * 8;
     const int64_t r_begin = blockIdx.x * p.rows_per_block;
     const int64_t r_end = min(p.rows, r_begin + p.rows_per_block);
-    double S[8] = {}, Q[8] = {};
+    // fp64 running sums live in this thread's smem slot (frees 32 registers for
+    // a deeper load pipeline); fp32 partials are folded in every 16 rows
+    double* mine = red + threadIdx.x * 16;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) mine[j] = 0.0;
     float s[8] = {}, q[8] = {};
     float g[8], b[8], mu[8], is[8];
     if (KIND != 0) {
@@ -103,14 +107,13 @@ __global__ void __launch_bounds__(kThreads, 2) stats_kernel(StatArgs p) {
         }
     }
     const float inv_slope = 1.0f / p.slope;
-    // process up to 2 rows per iteration (2 x 128-bit loads in flight per operand,
-    // <= 85 registers so 3 CTAs fit per SM), fold fp32 partials into fp64 every 16 rows
+    constexpr int U = KIND == 0 ? 4 : (KIND == 1 ? 2 : 3);  // rows in flight per thread
     int run = 0;
-    for (int64_t r0 = r_begin + rg; r0 < r_end; r0 += 2 * rpi) {
-        float v[2][8], dd[2][8], ym[2][8];
-        bool ok[2];
+    for (int64_t r0 = r_begin + rg; r0 < r_end; r0 += U * rpi) {
+        float v[U][8], dd[U][8], ym[U][8];
+        bool ok[U];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < U; ++u) {
             const int64_t r = r0 + u * rpi;
             ok[u] = r < r_end;
             if (ok[u]) {
@@ -121,7 +124,7 @@ __global__ void __launch_bounds__(kThreads, 2) stats_kernel(StatArgs p) {
             }
         }
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < U; ++u) {
             if (!ok[u]) continue;
             if (KIND == 0) {
 #pragma unroll
@@ -151,20 +154,21 @@ __global__ void __launch_bounds__(kThreads, 2) stats_kernel(StatArgs p) {
             if (++run == 16) {
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
-                    S[j] += s[j];
-                    Q[j] += q[j];
+                    mine[j] += s[j];
+                    mine[8 + j] += q[j];
                     s[j] = q[j] = 0.f;
                 }
                 run = 0;
             }
         }
     }
+    double S[8], Q[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-        S[j] += s[j];
-        Q[j] += q[j];
-        red[threadIdx.x * 16 + j] = S[j];
-        red[threadIdx.x * 16 + 8 + j] = Q[j];
+        S[j] = mine[j] + s[j];
+        Q[j] = mine[8 + j] + q[j];
+        mine[j] = S[j];
+        mine[8 + j] = Q[j];
     }
     __syncthreads();
     if (rg == 0) {
