@@ -580,11 +580,11 @@ void run_step(sdb_det* d) {
     PScope ps_loss(d, P_LOSS, 0, 0, 4);
     LossArgs la{d->scale, d->losses, 0};
     CK(sigmoid_bce(d->dt, d->rpn_logits.p, static_cast<int64_t>(d->n_loc) * cf.batch, d->A, d->A_pad, d->a_labels,
-                   d->d_rpn_logits, la, nullptr, st));
+                   d->d_rpn_logits, la, d->ws, st));
     la.slot = 1;
     CK(rpn_smooth_l1(d->dt, d->rpn_deltas.p, static_cast<int64_t>(d->n_loc) * cf.batch, d->A, d->A_pad, d->a_labels,
                      d->a_targets, 1.0 / 9.0, static_cast<double>(cf.rpn_batch) * cf.batch, d->d_rpn_deltas, la,
-                     nullptr, st));
+                     d->ws, st));
     la.slot = 2;
     CK(softmax_ce(d->dt, d->cls_logits.p, d->R, d->ncls, d->ncls_pad, d->roi_labels, g0, la, nullptr, st));
     la.slot = 3;

@@ -360,56 +360,72 @@ __global__ void __launch_bounds__(kScanThreads) nms_scan_kernel(const float* __r
                                                                 int32_t* __restrict__ keep_pos,
                                                                 int32_t* __restrict__ count) {
     extern __shared__ uint64_t removed[];  // nwords
-    __shared__ uint64_t diag[64];
-    __shared__ uint64_t chunk_keep;
-    __shared__ int kept, done;
+    __shared__ uint64_t diag[2][64];
+    __shared__ int rows[64];
+    __shared__ int nrows, kept, done;
     const int img = blockIdx.x;
     const uint64_t* M = mask + static_cast<int64_t>(img) * k * nwords;
     for (int w = threadIdx.x; w < nwords; w += kScanThreads) removed[w] = 0;
+    if (threadIdx.x < 64) diag[0][threadIdx.x] = threadIdx.x < k ? M[static_cast<int64_t>(threadIdx.x) * nwords] : 0ull;
     if (threadIdx.x == 0) {
         kept = 0;
         done = 0;
     }
     __syncthreads();
     for (int c = 0; c < nwords && !done; ++c) {
-        if (threadIdx.x < 64) {
-            const int i = c * 64 + threadIdx.x;
-            diag[threadIdx.x] = i < k ? M[static_cast<int64_t>(i) * nwords + c] : 0ull;
-        }
-        __syncthreads();
+        const int cur = c & 1;
         if (threadIdx.x == 0) {
-            uint64_t w = removed[c], km = 0;
-            int kc = kept;
-            for (int b = 0; b < 64; ++b) {
-                const int i = c * 64 + b;
-                if (i >= k) break;
-                if ((w >> b) & 1ull) continue;
-                if (kc >= post_k) {
-                    done = 1;
-                    break;
-                }
-                km |= 1ull << b;
-                keep_pos[static_cast<int64_t>(img) * post_k + kc] = i;
+            // greedy keep within the 64-box chunk: visit only surviving candidates
+            // (ffs over ~removed), each kept box suppresses its diagonal row word
+            const int lim = min(64, k - c * 64);
+            const uint64_t valid = lim >= 64 ? ~0ull : ((1ull << lim) - 1ull);
+            uint64_t w = removed[c];
+            int kc = kept, nr = 0;
+            uint64_t cand = ~w & valid;
+            while (cand) {
+                const int b = __ffsll(static_cast<long long>(cand)) - 1;
+                if (kc >= post_k) break;
+                keep_pos[static_cast<int64_t>(img) * post_k + kc] = c * 64 + b;
                 ++kc;
-                w |= diag[b];
+                rows[nr++] = c * 64 + b;
+                w |= diag[cur][b];
+                cand = ~w & valid & ~((2ull << b) - 1ull);
             }
             if (kc >= post_k) done = 1;
             removed[c] = w;
-            chunk_keep = km;
+            nrows = nr;
             kept = kc;
         }
         __syncthreads();
-        const uint64_t km = chunk_keep;
-        if (km) {
-            for (int w = c + 1 + threadIdx.x; w < nwords; w += kScanThreads) {
-                uint64_t acc = 0;
-                uint64_t bits = km;
-                while (bits) {
-                    const int b = __ffsll(static_cast<long long>(bits)) - 1;
-                    bits &= bits - 1;
-                    acc |= M[static_cast<int64_t>(c * 64 + b) * nwords + w];
+        // prefetch the next chunk's diagonal words (independent of `removed`)
+        if (threadIdx.x < 64 && c + 1 < nwords) {
+            const int i = (c + 1) * 64 + threadIdx.x;
+            diag[cur ^ 1][threadIdx.x] = i < k ? M[static_cast<int64_t>(i) * nwords + c + 1] : 0ull;
+        }
+        // OR every kept row's remaining words into `removed`: the (row, word)
+        // loads are independent -- flatten them over the block, 4 loads in flight
+        // per thread, reduce with shared atomicOr (order-independent -> deterministic)
+        const int nrem = nwords - c - 1, nr = nrows;
+        if (!done && nr > 0 && nrem > 0) {
+            const int total = nr * nrem;
+            for (int e0 = threadIdx.x; e0 < total; e0 += 4 * kScanThreads) {
+                uint64_t v[4];
+                int wi[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int e = e0 + u * kScanThreads;
+                    v[u] = 0;
+                    wi[u] = -1;
+                    if (e < total) {
+                        const int r = e / nrem;
+                        wi[u] = c + 1 + (e - r * nrem);
+                        v[u] = __ldg(M + static_cast<int64_t>(rows[r]) * nwords + wi[u]);
+                    }
                 }
-                removed[w] |= acc;
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (v[u]) atomicOr(reinterpret_cast<unsigned long long*>(&removed[wi[u]]),
+                                       static_cast<unsigned long long>(v[u]));
             }
         }
         __syncthreads();

@@ -502,23 +502,57 @@ __global__ void __launch_bounds__(kLossThreads) softmax_ce_kernel(const T* __res
     }
 }
 
+// RPN losses run on many blocks with fixed-order partial sums (deterministic):
+// per-block partials -> one tiny in-order reduction.
+constexpr int kLossBlocks = 2 * kNumSMs;
+constexpr int kLossBlockThreads = 256;
+
+SDB_DEV double block_sum_d256(double v, double* sh) {
+    v = warp_sum(v);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double t = 0.0;
+    for (int w = 0; w < kLossBlockThreads / 32; ++w) t += sh[w];
+    __syncthreads();
+    return t;
+}
+
+// number of sampled anchors (label >= 0) per block
+__global__ void __launch_bounds__(kLossBlockThreads) label_count_kernel(const int8_t* __restrict__ labels, int64_t n,
+                                                                        double* __restrict__ partial) {
+    __shared__ double sh[8];
+    double c = 0.0;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        c += labels[i] >= 0;
+    const double t = block_sum_d256(c, sh);
+    if (threadIdx.x == 0) partial[blockIdx.x] = t;
+}
+
+SDB_DEV double sum_partials(const double* p, int n) {
+    double t = 0.0;
+    for (int i = 0; i < n; ++i) t += p[i];
+    return t;
+}
+
 // sigmoid BCE over anchors with label >= 0, normalised by their count
 template <class T>
-__global__ void __launch_bounds__(kLossThreads) sigmoid_bce_kernel(const T* __restrict__ logits, int64_t n_loc, int A,
-                                                                   int A_pad, const int8_t* __restrict__ labels,
-                                                                   T* __restrict__ dlogits, const double* scale,
-                                                                   double* loss_out, int slot) {
-    __shared__ double sh[32];
-    const int64_t n = n_loc * A_pad;
-    int cnt = 0;
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-        const int a = static_cast<int>(i % A_pad);
-        if (a < A) cnt += labels[(i / A_pad) * A + a] >= 0;
-    }
-    const double norm = block_sum_d(static_cast<double>(cnt), sh);
+__global__ void __launch_bounds__(kLossBlockThreads) sigmoid_bce_kernel(const T* __restrict__ logits, int64_t n_loc,
+                                                                        int A, int A_pad,
+                                                                        const int8_t* __restrict__ labels,
+                                                                        T* __restrict__ dlogits, const double* scale,
+                                                                        const double* __restrict__ counts,
+                                                                        double* __restrict__ partial) {
+    __shared__ double sh[8];
+    __shared__ double norm_s;
+    if (threadIdx.x == 0) norm_s = sum_partials(counts, gridDim.x);
+    __syncthreads();
+    const double norm = norm_s;
     const double gs = (scale ? *scale : 1.0) / (norm > 0 ? norm : 1.0);
+    const int64_t n = n_loc * A_pad;
     double acc = 0.0;
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int a = static_cast<int>(i % A_pad);
         float gout = 0.f;
         if (a < A) {
@@ -531,8 +565,17 @@ __global__ void __launch_bounds__(kLossThreads) sigmoid_bce_kernel(const T* __re
         }
         dlogits[i] = from_f<T>(gout);
     }
-    const double tot = block_sum_d(acc, sh);
-    if (threadIdx.x == 0) loss_out[slot] = norm > 0 ? tot / norm : 0.0;
+    const double tot = block_sum_d256(acc, sh);
+    if (threadIdx.x == 0) partial[blockIdx.x] = tot;
+}
+
+// loss = sum(partial) / (norm or sum(counts))
+__global__ void loss_finalize_kernel(const double* __restrict__ partial, int n, const double* __restrict__ counts,
+                                     double norm, double* loss_out, int slot) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const double d = counts ? sum_partials(counts, n) : norm;
+    const double t = sum_partials(partial, n);
+    loss_out[slot] = d > 0 ? t / d : 0.0;
 }
 
 SDB_DEV void sl1(double d, double beta, double& l, double& g) {
@@ -547,16 +590,17 @@ SDB_DEV void sl1(double d, double beta, double& l, double& g) {
 }
 
 template <class T>
-__global__ void __launch_bounds__(kLossThreads) rpn_sl1_kernel(const T* __restrict__ deltas, int64_t n_loc, int A,
-                                                               int A_pad, const int8_t* __restrict__ labels,
-                                                               const float* __restrict__ targets, double beta,
-                                                               double norm, T* __restrict__ dd, const double* scale,
-                                                               double* loss_out, int slot) {
-    __shared__ double sh[32];
+__global__ void __launch_bounds__(kLossBlockThreads) rpn_sl1_kernel(const T* __restrict__ deltas, int64_t n_loc, int A,
+                                                                    int A_pad, const int8_t* __restrict__ labels,
+                                                                    const float* __restrict__ targets, double beta,
+                                                                    double norm, T* __restrict__ dd, const double* scale,
+                                                                    double* __restrict__ partial) {
+    __shared__ double sh[8];
     const int64_t n = n_loc * 4 * A_pad;
     const double gs = (scale ? *scale : 1.0) / norm;
     double acc = 0.0;
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t loc = i / (4 * A_pad);
         const int rem = static_cast<int>(i % (4 * A_pad));
         const int a = rem / 4, k = rem % 4;
@@ -570,8 +614,8 @@ __global__ void __launch_bounds__(kLossThreads) rpn_sl1_kernel(const T* __restri
         }
         dd[i] = from_f<T>(gout);
     }
-    const double tot = block_sum_d(acc, sh);
-    if (threadIdx.x == 0) loss_out[slot] = tot / norm;
+    const double tot = block_sum_d256(acc, sh);
+    if (threadIdx.x == 0) partial[blockIdx.x] = tot;
 }
 
 template <class T>
@@ -763,7 +807,7 @@ cudaError_t add_inplace(int dtype, void* acc, const void* b, int64_t n, cudaStre
     return cudaGetLastError();
 }
 
-size_t loss_workspace_bytes(int64_t) { return 0; }
+size_t loss_workspace_bytes(int64_t) { return 3 * kLossBlocks * sizeof(double); }
 
 cudaError_t softmax_ce(int dtype, const void* logits, int R, int ncls, int ld, const int32_t* labels, void* dlogits,
                        const LossArgs& la, void*, cudaStream_t st) {
@@ -778,28 +822,33 @@ cudaError_t softmax_ce(int dtype, const void* logits, int R, int ncls, int ld, c
 }
 
 cudaError_t sigmoid_bce(int dtype, const void* logits, int64_t n_loc, int A, int A_pad, const int8_t* labels,
-                        void* dlogits, const LossArgs& la, void*, cudaStream_t st) {
+                        void* dlogits, const LossArgs& la, void* ws, cudaStream_t st) {
+    double* counts = static_cast<double*>(ws);
+    double* partial = counts + kLossBlocks;
+    label_count_kernel<<<kLossBlocks, kLossBlockThreads, 0, st>>>(labels, n_loc * A, counts);
     if (dtype == kF16)
-        sigmoid_bce_kernel<__half><<<1, kLossThreads, 0, st>>>(cp<__half>(logits), n_loc, A, A_pad, labels,
-                                                              static_cast<__half*>(dlogits), la.scale, la.loss_out,
-                                                              la.slot);
+        sigmoid_bce_kernel<__half><<<kLossBlocks, kLossBlockThreads, 0, st>>>(
+            cp<__half>(logits), n_loc, A, A_pad, labels, static_cast<__half*>(dlogits), la.scale, counts, partial);
     else
-        sigmoid_bce_kernel<float><<<1, kLossThreads, 0, st>>>(cp<float>(logits), n_loc, A, A_pad, labels,
-                                                             static_cast<float*>(dlogits), la.scale, la.loss_out,
-                                                             la.slot);
+        sigmoid_bce_kernel<float><<<kLossBlocks, kLossBlockThreads, 0, st>>>(
+            cp<float>(logits), n_loc, A, A_pad, labels, static_cast<float*>(dlogits), la.scale, counts, partial);
+    loss_finalize_kernel<<<1, 32, 0, st>>>(partial, kLossBlocks, counts, 0.0, la.loss_out, la.slot);
     return cudaGetLastError();
 }
 
 cudaError_t rpn_smooth_l1(int dtype, const void* deltas, int64_t n_loc, int A, int A_pad, const int8_t* labels,
-                          const float* targets, double beta, double norm, void* dd, const LossArgs& la, void*,
+                          const float* targets, double beta, double norm, void* dd, const LossArgs& la, void* ws,
                           cudaStream_t st) {
+    double* partial = static_cast<double*>(ws) + 2 * kLossBlocks;
     if (dtype == kF16)
-        rpn_sl1_kernel<__half><<<1, kLossThreads, 0, st>>>(cp<__half>(deltas), n_loc, A, A_pad, labels, targets, beta,
-                                                          norm, static_cast<__half*>(dd), la.scale, la.loss_out,
-                                                          la.slot);
+        rpn_sl1_kernel<__half><<<kLossBlocks, kLossBlockThreads, 0, st>>>(cp<__half>(deltas), n_loc, A, A_pad, labels,
+                                                                         targets, beta, norm, static_cast<__half*>(dd),
+                                                                         la.scale, partial);
     else
-        rpn_sl1_kernel<float><<<1, kLossThreads, 0, st>>>(cp<float>(deltas), n_loc, A, A_pad, labels, targets, beta,
-                                                         norm, static_cast<float*>(dd), la.scale, la.loss_out, la.slot);
+        rpn_sl1_kernel<float><<<kLossBlocks, kLossBlockThreads, 0, st>>>(cp<float>(deltas), n_loc, A, A_pad, labels,
+                                                                        targets, beta, norm, static_cast<float*>(dd),
+                                                                        la.scale, partial);
+    loss_finalize_kernel<<<1, 32, 0, st>>>(partial, kLossBlocks, nullptr, norm, la.loss_out, la.slot);
     return cudaGetLastError();
 }
 
