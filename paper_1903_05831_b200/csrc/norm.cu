@@ -80,98 +80,159 @@ struct StatArgs {
     double* partial;
 };
 
-template <class T, int KIND>
-__global__ void __launch_bounds__(kThreads, 2) stats_kernel(StatArgs p) {
-    extern __shared__ double red[];  // [kThreads][16]
-    const int tpr = p.C / 8;
-    const int rpi = kThreads / tpr;
-    const int cg = threadIdx.x % tpr, rg = threadIdx.x / tpr;
-    const int c0 = cg * 8;
+// Bulk-copy pipeline: a producer lane streams contiguous row tiles (16 KB per
+// operand) into a ring of shared-memory stages with cp.async.bulk (completion
+// by transaction bytes on an mbarrier); 8 consumer warps reduce each tile from
+// shared memory.  Memory-level parallelism is ST x NIN x 16 KB per CTA
+// (~96 KB), independent of registers, which is what keeps HBM busy: the
+// previous register-pipelined version sat at 25% occupancy and ~2.7 TB/s.
+constexpr int kTileBytes = 16384;
+constexpr int kStatThreads = kThreads + 32;  // + producer warp
+
+template <int NIN>
+struct StatPipe {
+    static constexpr int kStages = NIN == 1 ? 6 : (NIN == 2 ? 3 : 2);
+    static constexpr int kSmem = kStages * NIN * kTileBytes + 2 * kStages * 8;
+};
+
+// rows per tile for channel count C
+template <class T>
+SDB_DEV int tile_rows_for(int C) {
+    return kTileBytes / (C * static_cast<int>(sizeof(T)));
+}
+
+template <class T, int KIND, int NIN>
+__global__ void __launch_bounds__(kStatThreads, 2) stats_kernel(StatArgs p) {
+    constexpr int ST = StatPipe<NIN>::kStages;
+    extern __shared__ __align__(128) uint8_t sm[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + ST * NIN * kTileBytes);
+    uint64_t* empty = full + ST;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int C = p.C;
+    const int TR = tile_rows_for<T>(C);
     const int64_t r_begin = blockIdx.x * p.rows_per_block;
     const int64_t r_end = min(p.rows, r_begin + p.rows_per_block);
-    // fp64 running sums live in this thread's smem slot (frees 32 registers for
-    // a deeper load pipeline); fp32 partials are folded in every 16 rows
-    double* mine = red + threadIdx.x * 16;
-#pragma unroll
-    for (int j = 0; j < 16; ++j) mine[j] = 0.0;
-    float s[8] = {}, q[8] = {};
-    float g[8], b[8], mu[8], is[8];
-    if (KIND != 0) {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            g[j] = p.gamma[c0 + j];
-            is[j] = p.invstd[c0 + j];
-            mu[j] = KIND == 1 ? p.mean[c0 + j] : 0.f;
-            b[j] = KIND == 2 ? p.beta[c0 + j] : 0.f;
-            if (KIND == 2) g[j] = 1.0f / g[j];  // xhat = (z - beta) * (1/gamma)
+    const int ntiles = r_end > r_begin ? static_cast<int>((r_end - r_begin + TR - 1) / TR) : 0;
+    if (tid == 0) {
+        for (int s = 0; s < ST; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kThreads / 32);
         }
-    }
-    const float inv_slope = 1.0f / p.slope;
-    constexpr int U = KIND == 0 ? 4 : (KIND == 1 ? 2 : 3);  // rows in flight per thread
-    int run = 0;
-    for (int64_t r0 = r_begin + rg; r0 < r_end; r0 += U * rpi) {
-        float v[U][8], dd[U][8], ym[U][8];
-        bool ok[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int64_t r = r0 + u * rpi;
-            ok[u] = r < r_end;
-            if (ok[u]) {
-                const int64_t off = r * p.C + c0;
-                load8<T>(static_cast<const T*>(p.a) + off, v[u]);
-                if (KIND != 0) load8<T>(static_cast<const T*>(p.dy) + off, dd[u]);
-                if (KIND == 1 && p.y) load8<T>(static_cast<const T*>(p.y) + off, ym[u]);
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            if (!ok[u]) continue;
-            if (KIND == 0) {
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    s[j] += v[u][j];
-                    q[j] += v[u][j] * v[u][j];
-                }
-            } else if (KIND == 1) {
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const float d = (p.y && !(ym[u][j] > 0.f)) ? 0.f : dd[u][j];
-                    const float xh = (v[u][j] - mu[j]) * is[j];
-                    s[j] += d;
-                    q[j] += d * xh;
-                }
-            } else {
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const float yv = v[u][j];
-                    const float z = yv >= 0.f ? yv : yv * inv_slope;
-                    const float dz = dd[u][j] * (yv > 0.f ? 1.f : p.slope);
-                    const float xh = (z - b[j]) * g[j];
-                    s[j] += dz;
-                    q[j] += dz * xh;
-                }
-            }
-            if (++run == 16) {
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    mine[j] += s[j];
-                    mine[8 + j] += q[j];
-                    s[j] = q[j] = 0.f;
-                }
-                run = 0;
-            }
-        }
-    }
-    double S[8], Q[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        S[j] = mine[j] + s[j];
-        Q[j] = mine[8 + j] + q[j];
-        mine[j] = S[j];
-        mine[8 + j] = Q[j];
+        mbar_fence_init();
     }
     __syncthreads();
-    if (rg == 0) {
+    const uint32_t sbase = smem_u32(sm);
+    const int tpr = C / 8;
+    const int rpi = kThreads / tpr;
+    const int cg = tid % tpr, rg = tid / tpr;
+    const int c0 = cg * 8;
+    double S[8], Q[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) S[j] = Q[j] = 0.0;
+    if (warp == kThreads / 32) {
+        // ------------------------------------------------ producer
+        if (lane == 0) {
+            const T* src[3] = {static_cast<const T*>(p.a), static_cast<const T*>(p.dy), static_cast<const T*>(p.y)};
+            for (int i = 0; i < ntiles; ++i) {
+                const int s = i % ST;
+                if (i >= ST) mbar_wait(&empty[s], ((i / ST) - 1) & 1);
+                const int64_t r0 = r_begin + static_cast<int64_t>(i) * TR;
+                const int nr = static_cast<int>(min(static_cast<int64_t>(TR), r_end - r0));
+                const uint32_t bytes = static_cast<uint32_t>(nr) * C * sizeof(T);
+                mbar_arrive_expect_tx(&full[s], bytes * NIN);
+#pragma unroll
+                for (int j = 0; j < NIN; ++j)
+                    bulk_load(sbase + (s * NIN + j) * kTileBytes, src[j] + r0 * C, bytes, &full[s]);
+            }
+        }
+    } else {
+        // ------------------------------------------------ consumers
+        float g[8], b[8], mu[8], is[8];
+        if (KIND != 0) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                g[j] = p.gamma[c0 + j];
+                is[j] = p.invstd[c0 + j];
+                mu[j] = KIND == 1 ? p.mean[c0 + j] : 0.f;
+                b[j] = KIND == 2 ? p.beta[c0 + j] : 0.f;
+                if (KIND == 2) g[j] = 1.0f / g[j];  // xhat = (z - beta) * (1/gamma)
+            }
+        }
+        const float inv_slope = 1.0f / p.slope;
+        float s[8] = {}, q[8] = {};
+        int run = 0;
+        for (int i = 0; i < ntiles; ++i) {
+            const int st = i % ST;
+            mbar_wait(&full[st], (i / ST) & 1);
+            const int64_t r0 = r_begin + static_cast<int64_t>(i) * TR;
+            const int nr = static_cast<int>(min(static_cast<int64_t>(TR), r_end - r0));
+            const T* ta = reinterpret_cast<const T*>(sm + (st * NIN) * kTileBytes);
+            const T* td = reinterpret_cast<const T*>(sm + (st * NIN + 1) * kTileBytes);
+            const T* tm = reinterpret_cast<const T*>(sm + (st * NIN + 2) * kTileBytes);
+            for (int rr = rg; rr < nr; rr += rpi) {
+                const int off = rr * C + c0;
+                float v[8], dd[8], ym[8];
+                load8<T>(ta + off, v);
+                if (KIND != 0) load8<T>(td + off, dd);
+                if (NIN == 3) load8<T>(tm + off, ym);
+                if (KIND == 0) {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        s[j] += v[j];
+                        q[j] += v[j] * v[j];
+                    }
+                } else if (KIND == 1) {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const float d = (NIN == 3 && !(ym[j] > 0.f)) ? 0.f : dd[j];
+                        const float xh = (v[j] - mu[j]) * is[j];
+                        s[j] += d;
+                        q[j] += d * xh;
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const float yv = v[j];
+                        const float z = yv >= 0.f ? yv : yv * inv_slope;
+                        const float dz = dd[j] * (yv > 0.f ? 1.f : p.slope);
+                        const float xh = (z - b[j]) * g[j];
+                        s[j] += dz;
+                        q[j] += dz * xh;
+                    }
+                }
+                // fp32 runs of <= 16 rows, folded into fp64
+                if (++run == 16) {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        S[j] += s[j];
+                        Q[j] += q[j];
+                        s[j] = q[j] = 0.f;
+                    }
+                    run = 0;
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[st]);
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            S[j] += s[j];
+            Q[j] += q[j];
+        }
+    }
+    // every stage has been consumed (all bulk copies landed): reuse the ring
+    // as the fixed-order block reduction buffer
+    __syncthreads();
+    double* red = reinterpret_cast<double*>(sm);
+    if (tid < kThreads) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            red[tid * 16 + j] = S[j];
+            red[tid * 16 + 8 + j] = Q[j];
+        }
+    }
+    __syncthreads();
+    if (tid < kThreads && rg == 0) {
         for (int k = 1; k < rpi; ++k) {
             const int t = k * tpr + cg;
 #pragma unroll
@@ -180,11 +241,11 @@ __global__ void __launch_bounds__(kThreads, 2) stats_kernel(StatArgs p) {
                 Q[j] += red[t * 16 + 8 + j];
             }
         }
-        double* out = p.partial + static_cast<int64_t>(blockIdx.x) * 2 * p.C;
+        double* out = p.partial + static_cast<int64_t>(blockIdx.x) * 2 * C;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             out[c0 + j] = S[j];
-            out[p.C + c0 + j] = Q[j];
+            out[C + c0 + j] = Q[j];
         }
     }
 }
@@ -192,27 +253,38 @@ __global__ void __launch_bounds__(kThreads, 2) stats_kernel(StatArgs p) {
 // MODE 0: BN fwd (sums rounded to float first), 1: IABN fwd (double)
 // MODE 2: BN bwd, 3: IABN bwd  -> coef[0..C) = s1/m, coef[C..2C) = s2/m
 // Fixed-order parallel reduction of the per-block partials: thread (cx, ry)
-// of a 32x8 block sums partial[b][c] for b = ry, ry+8, ... (coalesced across
-// cx); the 8 row sums are then added in order.  Deterministic, no atomics.
-__global__ void __launch_bounds__(256) finalize_kernel(const double* partial, int nblocks, int C, int64_t count,
-                                                       float eps, int mode, float* mean, float* invstd, float* dgamma,
-                                                       float* dbeta, float* coef) {
-    __shared__ double rs[8][32], rq[8][32];
+// of a 32x32 block sums partial[b][c] for b = ry, ry+32, ... (coalesced across
+// cx, 4 independent loads in flight); the 32 row sums are then added in order.
+// Deterministic, no atomics.
+__global__ void __launch_bounds__(1024) finalize_kernel(const double* __restrict__ partial, int nblocks, int C,
+                                                        int64_t count, float eps, int mode, float* mean, float* invstd,
+                                                        float* dgamma, float* dbeta, float* coef) {
+    __shared__ double rs[32][33], rq[32][33];
     const int cx = threadIdx.x & 31, ry = threadIdx.x >> 5;
     const int c = blockIdx.x * 32 + cx;
     double S = 0.0, Q = 0.0;
-    if (c < C)
-        for (int b = ry; b < nblocks; b += 8) {
-            S += partial[static_cast<int64_t>(b) * 2 * C + c];
-            Q += partial[static_cast<int64_t>(b) * 2 * C + C + c];
+    if (c < C) {
+        const int64_t stride = 2 * static_cast<int64_t>(C);
+        int b = ry;
+        for (; b + 96 < nblocks; b += 128) {
+            const double* p0 = partial + b * stride + c;
+            const double s0 = p0[0], s1 = p0[32 * stride], s2 = p0[64 * stride], s3 = p0[96 * stride];
+            const double q0 = p0[C], q1 = p0[32 * stride + C], q2 = p0[64 * stride + C], q3 = p0[96 * stride + C];
+            S += s0; S += s1; S += s2; S += s3;
+            Q += q0; Q += q1; Q += q2; Q += q3;
         }
+        for (; b < nblocks; b += 32) {
+            S += partial[b * stride + c];
+            Q += partial[b * stride + C + c];
+        }
+    }
     rs[ry][cx] = S;
     rq[ry][cx] = Q;
     __syncthreads();
     if (ry != 0 || c >= C) return;
     S = 0.0;
     Q = 0.0;
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < 32; ++k) {
         S += rs[k][cx];
         Q += rq[k][cx];
     }
@@ -337,14 +409,16 @@ struct Plan {
     int64_t rpb;
 };
 
-Plan plan_for(int64_t rows, int C) {
-    const int rpi = kThreads / (C / 8);
-    // at least 16 rows per thread-iteration group, at most kMaxBlocks blocks
-    int64_t nb = (rows + static_cast<int64_t>(rpi) * 16 - 1) / (static_cast<int64_t>(rpi) * 16);
-    nb = std::max<int64_t>(1, std::min<int64_t>(nb, kMaxBlocks));
+// Rows are split into at most 2 CTAs per SM, each a whole number of tiles.
+Plan plan_for(int64_t rows, int C, int elem_bytes) {
+    const int64_t tr = kTileBytes / (static_cast<int64_t>(C) * elem_bytes);
+    const int64_t tiles = std::max<int64_t>(1, (rows + tr - 1) / tr);
+    const int64_t nb = std::min<int64_t>(tiles, kMaxBlocks);
+    const int64_t tpb = (tiles + nb - 1) / nb;
     Plan p;
-    p.nblocks = static_cast<int>(nb);
-    p.rpb = (rows + nb - 1) / nb;
+    p.rpb = tpb * tr;
+    p.nblocks = static_cast<int>((rows + p.rpb - 1) / p.rpb);
+    if (p.nblocks < 1) p.nblocks = 1;
     return p;
 }
 
@@ -352,12 +426,24 @@ int apply_blocks(int64_t n8) {
     return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n8 + kThreads - 1) / kThreads, 8 * kNumSMs)));
 }
 
-template <class T, int KIND>
+template <class T, int KIND, int NIN>
 cudaError_t run_stats(const StatArgs& a0, const Plan& pl, cudaStream_t st) {
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(stats_kernel<T, KIND, NIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             StatPipe<NIN>::kSmem);
+        configured = true;
+    }
     StatArgs a = a0;
     a.rows_per_block = pl.rpb;
-    stats_kernel<T, KIND><<<pl.nblocks, kThreads, kThreads * 16 * sizeof(double), st>>>(a);
+    stats_kernel<T, KIND, NIN><<<pl.nblocks, kStatThreads, StatPipe<NIN>::kSmem, st>>>(a);
     return cudaGetLastError();
+}
+
+void finalize(const double* partial, const Plan& pl, int C, int64_t rows, float eps, int mode, float* mean,
+              float* invstd, float* dgamma, float* dbeta, float* coef, cudaStream_t st) {
+    finalize_kernel<<<(C + 31) / 32, 1024, 0, st>>>(partial, pl.nblocks, C, rows, eps, mode, mean, invstd, dgamma,
+                                                      dbeta, coef);
 }
 
 }  // namespace
@@ -365,21 +451,23 @@ cudaError_t run_stats(const StatArgs& a0, const Plan& pl, cudaStream_t st) {
 bool norm_channels_ok(int C) { return C >= 8 && C <= 2048 && (C % 8) == 0 && (2048 % C) == 0; }
 
 size_t norm_workspace_bytes(int64_t rows, int C) {
-    const Plan p = plan_for(std::max<int64_t>(rows, 1), C);
-    return static_cast<size_t>(p.nblocks) * 2 * C * sizeof(double) + 2 * C * sizeof(float) + 256;
+    // the fp16 plan has the most blocks (fewest rows per tile)... take the max of both
+    const Plan p16 = plan_for(std::max<int64_t>(rows, 1), C, 2);
+    const Plan p32 = plan_for(std::max<int64_t>(rows, 1), C, 4);
+    const int nb = std::max(p16.nblocks, p32.nblocks);
+    return static_cast<size_t>(nb) * 2 * C * sizeof(double) + 2 * C * sizeof(float) + 256;
 }
 
 cudaError_t bn_forward(int dtype, const void* x, const float* gamma, const float* beta, void* y, float* mean,
                        float* invstd, int64_t rows, int C, float eps, int act, float slope, void* ws, cudaStream_t st) {
     // act: 0 none, 1 relu (BN mode);  act 2 = IABN with `slope`
-    const Plan pl = plan_for(rows, C);
+    const Plan pl = plan_for(rows, C, dtype == kF16 ? 2 : 4);
     double* partial = static_cast<double*>(ws);
     StatArgs sa{};
-    sa.a = x; sa.rows = rows; sa.C = C; sa.partial = partial;
-    cudaError_t e = dtype == kF16 ? run_stats<__half, 0>(sa, pl, st) : run_stats<float, 0>(sa, pl, st);
+    sa.a = x; sa.rows = rows; sa.C = C; sa.partial = partial; sa.slope = 1.f;
+    cudaError_t e = dtype == kF16 ? run_stats<__half, 0, 1>(sa, pl, st) : run_stats<float, 0, 1>(sa, pl, st);
     if (e != cudaSuccess) return e;
-    finalize_kernel<<<(C + 31) / 32, 256, 0, st>>>(partial, pl.nblocks, C, rows, eps, act == 2 ? 1 : 0, mean, invstd,
-                                                     nullptr, nullptr, nullptr);
+    finalize(partial, pl, C, rows, eps, act == 2 ? 1 : 0, mean, invstd, nullptr, nullptr, nullptr, st);
     ApplyArgs aa{};
     aa.a = x; aa.out = y; aa.gamma = gamma; aa.beta = beta; aa.mean = mean; aa.invstd = invstd;
     aa.slope = slope; aa.act = act; aa.n8 = rows * C / 8; aa.C = C;
@@ -397,16 +485,17 @@ cudaError_t bn_forward(int dtype, const void* x, const float* gamma, const float
 cudaError_t bn_backward(int dtype, const void* dy, const void* x, const void* y_mask, const float* gamma,
                         const float* mean, const float* invstd, void* dx, float* dgamma, float* dbeta, int64_t rows,
                         int C, void* ws, cudaStream_t st) {
-    const Plan pl = plan_for(rows, C);
+    const Plan pl = plan_for(rows, C, dtype == kF16 ? 2 : 4);
     double* partial = static_cast<double*>(ws);
     float* coef = reinterpret_cast<float*>(partial + static_cast<int64_t>(pl.nblocks) * 2 * C);
     StatArgs sa{};
     sa.a = x; sa.dy = dy; sa.y = y_mask; sa.gamma = gamma; sa.mean = mean; sa.invstd = invstd;
-    sa.rows = rows; sa.C = C; sa.partial = partial;
-    cudaError_t e = dtype == kF16 ? run_stats<__half, 1>(sa, pl, st) : run_stats<float, 1>(sa, pl, st);
+    sa.rows = rows; sa.C = C; sa.partial = partial; sa.slope = 1.f;
+    cudaError_t e;
+    if (y_mask) e = dtype == kF16 ? run_stats<__half, 1, 3>(sa, pl, st) : run_stats<float, 1, 3>(sa, pl, st);
+    else e = dtype == kF16 ? run_stats<__half, 1, 2>(sa, pl, st) : run_stats<float, 1, 2>(sa, pl, st);
     if (e != cudaSuccess) return e;
-    finalize_kernel<<<(C + 31) / 32, 256, 0, st>>>(partial, pl.nblocks, C, rows, 0.f, 2, nullptr, nullptr, dgamma,
-                                                     dbeta, coef);
+    finalize(partial, pl, C, rows, 0.f, 2, nullptr, nullptr, dgamma, dbeta, coef, st);
     ApplyArgs aa{};
     aa.a = x; aa.dy = dy; aa.y = y_mask; aa.out = dx; aa.gamma = gamma; aa.mean = mean; aa.invstd = invstd;
     aa.coef = coef; aa.n8 = rows * C / 8; aa.C = C;
@@ -420,16 +509,15 @@ cudaError_t iabn_backward(int dtype, const void* dy, const void* y, const float*
                           const float* mean, const float* invstd, void* dx, float* dgamma, float* dbeta, int64_t rows,
                           int C, float slope, void* ws, cudaStream_t st) {
     (void)mean;
-    const Plan pl = plan_for(rows, C);
+    const Plan pl = plan_for(rows, C, dtype == kF16 ? 2 : 4);
     double* partial = static_cast<double*>(ws);
     float* coef = reinterpret_cast<float*>(partial + static_cast<int64_t>(pl.nblocks) * 2 * C);
     StatArgs sa{};
     sa.a = y; sa.dy = dy; sa.gamma = gamma; sa.beta = beta; sa.invstd = invstd; sa.slope = slope;
     sa.rows = rows; sa.C = C; sa.partial = partial;
-    cudaError_t e = dtype == kF16 ? run_stats<__half, 2>(sa, pl, st) : run_stats<float, 2>(sa, pl, st);
+    cudaError_t e = dtype == kF16 ? run_stats<__half, 2, 2>(sa, pl, st) : run_stats<float, 2, 2>(sa, pl, st);
     if (e != cudaSuccess) return e;
-    finalize_kernel<<<(C + 31) / 32, 256, 0, st>>>(partial, pl.nblocks, C, rows, 0.f, 3, nullptr, nullptr, dgamma,
-                                                     dbeta, coef);
+    finalize(partial, pl, C, rows, 0.f, 3, nullptr, nullptr, dgamma, dbeta, coef, st);
     ApplyArgs aa{};
     aa.a = y; aa.dy = dy; aa.out = dx; aa.gamma = gamma; aa.beta = beta; aa.invstd = invstd; aa.coef = coef;
     aa.slope = slope; aa.n8 = rows * C / 8; aa.C = C;

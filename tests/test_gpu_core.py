@@ -85,7 +85,10 @@ def test_conv_large_tile_path(ref):
     assert_close(y, y_ref, 2e-3, "y")
 
 
-BN_SHAPES = [(2, 64, 7, 9), (4, 256, 5, 5), (2, 2048, 3, 3), (1, 8, 4, 4), (2, 512, 16, 12)]
+# the last two are large enough that every CTA of the bulk-copy statistics
+# pipeline streams more tiles than it has stages (ring wrap-around)
+BN_SHAPES = [(2, 64, 7, 9), (4, 256, 5, 5), (2, 2048, 3, 3), (1, 8, 4, 4), (2, 512, 16, 12), (6, 128, 150, 160),
+             (2, 1024, 41, 37)]
 
 
 @pytest.mark.parametrize("fp16", [False, True])
