@@ -101,6 +101,24 @@ SDB_DEV int tile_rows_for(int C) {
     return kTileBytes / (C * static_cast<int>(sizeof(T)));
 }
 
+// producer lane: stream row tiles [r_begin, r_end) of up to three operands
+// into the stage ring
+template <class T, int NIN, int ST>
+SDB_DEV void stream_tiles(uint32_t sbase, uint64_t* full, uint64_t* empty, const void* a, const void* b,
+                          const void* c, int64_t r_begin, int64_t r_end, int ntiles, int TR, int C) {
+    const T* src[3] = {static_cast<const T*>(a), static_cast<const T*>(b), static_cast<const T*>(c)};
+    for (int i = 0; i < ntiles; ++i) {
+        const int s = i % ST;
+        if (i >= ST) mbar_wait(&empty[s], ((i / ST) - 1) & 1);
+        const int64_t r0 = r_begin + static_cast<int64_t>(i) * TR;
+        const int nr = static_cast<int>(min(static_cast<int64_t>(TR), r_end - r0));
+        const uint32_t bytes = static_cast<uint32_t>(nr) * C * sizeof(T);
+        mbar_arrive_expect_tx(&full[s], bytes * NIN);
+#pragma unroll
+        for (int j = 0; j < NIN; ++j) bulk_load(sbase + (s * NIN + j) * kTileBytes, src[j] + r0 * C, bytes, &full[s]);
+    }
+}
+
 template <class T, int KIND, int NIN>
 __global__ void __launch_bounds__(kStatThreads, 2) stats_kernel(StatArgs p) {
     constexpr int ST = StatPipe<NIN>::kStages;
@@ -131,20 +149,8 @@ __global__ void __launch_bounds__(kStatThreads, 2) stats_kernel(StatArgs p) {
     for (int j = 0; j < 8; ++j) S[j] = Q[j] = 0.0;
     if (warp == kThreads / 32) {
         // ------------------------------------------------ producer
-        if (lane == 0) {
-            const T* src[3] = {static_cast<const T*>(p.a), static_cast<const T*>(p.dy), static_cast<const T*>(p.y)};
-            for (int i = 0; i < ntiles; ++i) {
-                const int s = i % ST;
-                if (i >= ST) mbar_wait(&empty[s], ((i / ST) - 1) & 1);
-                const int64_t r0 = r_begin + static_cast<int64_t>(i) * TR;
-                const int nr = static_cast<int>(min(static_cast<int64_t>(TR), r_end - r0));
-                const uint32_t bytes = static_cast<uint32_t>(nr) * C * sizeof(T);
-                mbar_arrive_expect_tx(&full[s], bytes * NIN);
-#pragma unroll
-                for (int j = 0; j < NIN; ++j)
-                    bulk_load(sbase + (s * NIN + j) * kTileBytes, src[j] + r0 * C, bytes, &full[s]);
-            }
-        }
+        if (lane == 0)
+            stream_tiles<T, NIN, ST>(sbase, full, empty, p.a, p.dy, p.y, r_begin, r_end, ntiles, TR, C);
     } else {
         // ------------------------------------------------ consumers
         float g[8], b[8], mu[8], is[8];
@@ -336,15 +342,41 @@ SDB_DEV void ldf8(const float* p, float (&v)[8]) {
     v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
 }
 
-// Each thread owns one 8-channel group (parameters held in registers) and
-// walks rows with a grid stride; 128-bit loads/stores, 2 rows in flight.
-template <class T, int KIND>
-__global__ void __launch_bounds__(kThreads, 2) apply_kernel(ApplyArgs p) {
-    const int tpr = p.C / 8;
+// Same bulk-copy pipeline as the statistics pass: the producer lane streams
+// the operand row tiles into shared memory, the 8 consumer warps (one 8-channel
+// group per thread, parameters in registers) normalise from shared memory and
+// store 128-bit rows straight to HBM.  Safe in place (out == a or out == dy):
+// a tile is read into shared memory before any of its rows is written, and
+// only this CTA touches its rows.
+template <class T, int KIND, int NIN>
+__global__ void __launch_bounds__(kStatThreads, 2) apply_kernel(ApplyArgs p, int64_t rows, int64_t rpb) {
+    constexpr int ST = StatPipe<NIN>::kStages;
+    extern __shared__ __align__(128) uint8_t sm[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + ST * NIN * kTileBytes);
+    uint64_t* empty = full + ST;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int C = p.C;
+    const int TR = tile_rows_for<T>(C);
+    const int64_t r_begin = blockIdx.x * rpb;
+    const int64_t r_end = min(rows, r_begin + rpb);
+    const int ntiles = r_end > r_begin ? static_cast<int>((r_end - r_begin + TR - 1) / TR) : 0;
+    if (tid == 0) {
+        for (int s = 0; s < ST; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kThreads / 32);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    if (warp == kThreads / 32) {
+        if (lane == 0)
+            stream_tiles<T, NIN, ST>(smem_u32(sm), full, empty, p.a, p.dy, p.y, r_begin, r_end, ntiles, TR, C);
+        return;
+    }
+    const int tpr = C / 8;
     const int rpi = kThreads / tpr;
-    const int cg = threadIdx.x % tpr, rg = threadIdx.x / tpr;
+    const int cg = tid % tpr, rg = tid / tpr;
     const int c0 = cg * 8;
-    const int64_t rows = p.n8 / tpr;
     float g[8], b[8], mu[8], is[8], k1[8], k2[8];
     ldf8(p.gamma + c0, g);
     ldf8(p.invstd + c0, is);
@@ -352,7 +384,7 @@ __global__ void __launch_bounds__(kThreads, 2) apply_kernel(ApplyArgs p) {
     if (KIND != 2) ldf8(p.beta + c0, b);
     if (KIND >= 2) {
         ldf8(p.coef + c0, k1);
-        ldf8(p.coef + p.C + c0, k2);
+        ldf8(p.coef + C + c0, k2);
     }
     float ig[8], gis[8];
 #pragma unroll
@@ -361,46 +393,56 @@ __global__ void __launch_bounds__(kThreads, 2) apply_kernel(ApplyArgs p) {
         gis[j] = g[j] * is[j];
     }
     const float inv_slope = 1.0f / p.slope;
-    const int64_t stride = static_cast<int64_t>(gridDim.x) * rpi;
-    for (int64_t r = static_cast<int64_t>(blockIdx.x) * rpi + rg; r < rows; r += stride) {
-        const int64_t off = r * p.C + c0;
-        float v[8], o[8];
-        load8<T>(static_cast<const T*>(p.a) + off, v);
-        if (KIND == 0 || KIND == 1) {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const float z = g[j] * (v[j] - mu[j]) * is[j] + b[j];
-                if (KIND == 0) o[j] = (p.act && !(z > 0.f)) ? 0.f : z;
-                else o[j] = z > 0.f ? z : p.slope * z;
-            }
-        } else {
-            float d[8];
-            load8<T>(static_cast<const T*>(p.dy) + off, d);
-            if (KIND == 2) {
-                if (p.y) {
-                    float yv[8];
-                    load8<T>(static_cast<const T*>(p.y) + off, yv);
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) d[j] = yv[j] > 0.f ? d[j] : 0.f;
-                }
+    T* out = static_cast<T*>(p.out);
+    for (int i = 0; i < ntiles; ++i) {
+        const int st = i % ST;
+        mbar_wait(&full[st], (i / ST) & 1);
+        const int64_t r0 = r_begin + static_cast<int64_t>(i) * TR;
+        const int nr = static_cast<int>(min(static_cast<int64_t>(TR), r_end - r0));
+        const T* ta = reinterpret_cast<const T*>(sm + (st * NIN) * kTileBytes);
+        const T* td = reinterpret_cast<const T*>(sm + (st * NIN + 1) * kTileBytes);
+        const T* tm = reinterpret_cast<const T*>(sm + (st * NIN + 2) * kTileBytes);
+        for (int rr = rg; rr < nr; rr += rpi) {
+            const int off = rr * C + c0;
+            float v[8], o[8];
+            load8<T>(ta + off, v);
+            if (KIND == 0 || KIND == 1) {
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
-                    const float gis = g[j] * is[j];
-                    const float xh = (v[j] - mu[j]) * is[j];
-                    o[j] = gis * (d[j] - k1[j] - xh * k2[j]);
+                    const float z = g[j] * (v[j] - mu[j]) * is[j] + b[j];
+                    if (KIND == 0) o[j] = (p.act && !(z > 0.f)) ? 0.f : z;
+                    else o[j] = z > 0.f ? z : p.slope * z;
                 }
             } else {
+                float d[8];
+                load8<T>(td + off, d);
+                if (KIND == 2) {
+                    if (NIN == 3) {
+                        float yv[8];
+                        load8<T>(tm + off, yv);
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const float yv = v[j];
-                    const float z = yv >= 0.f ? yv : yv * inv_slope;
-                    const float dz = d[j] * (yv > 0.f ? 1.f : p.slope);
-                    const float xh = (z - b[j]) * ig[j];
-                    o[j] = gis[j] * (dz - k1[j] - xh * k2[j]);
+                        for (int j = 0; j < 8; ++j) d[j] = yv[j] > 0.f ? d[j] : 0.f;
+                    }
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const float xh = (v[j] - mu[j]) * is[j];
+                        o[j] = gis[j] * (d[j] - k1[j] - xh * k2[j]);
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const float yv = v[j];
+                        const float z = yv >= 0.f ? yv : yv * inv_slope;
+                        const float dz = d[j] * (yv > 0.f ? 1.f : p.slope);
+                        const float xh = (z - b[j]) * ig[j];
+                        o[j] = gis[j] * (dz - k1[j] - xh * k2[j]);
+                    }
                 }
             }
+            store8<T>(out + (r0 + rr) * C + c0, o);
         }
-        store8<T>(static_cast<T*>(p.out) + off, o);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
     }
 }
 
@@ -422,10 +464,6 @@ Plan plan_for(int64_t rows, int C, int elem_bytes) {
     return p;
 }
 
-int apply_blocks(int64_t n8) {
-    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n8 + kThreads - 1) / kThreads, 8 * kNumSMs)));
-}
-
 template <class T, int KIND, int NIN>
 cudaError_t run_stats(const StatArgs& a0, const Plan& pl, cudaStream_t st) {
     static bool configured = false;
@@ -437,6 +475,18 @@ cudaError_t run_stats(const StatArgs& a0, const Plan& pl, cudaStream_t st) {
     StatArgs a = a0;
     a.rows_per_block = pl.rpb;
     stats_kernel<T, KIND, NIN><<<pl.nblocks, kStatThreads, StatPipe<NIN>::kSmem, st>>>(a);
+    return cudaGetLastError();
+}
+
+template <class T, int KIND, int NIN>
+cudaError_t run_apply(const ApplyArgs& aa, int64_t rows, const Plan& pl, cudaStream_t st) {
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(apply_kernel<T, KIND, NIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             StatPipe<NIN>::kSmem);
+        configured = true;
+    }
+    apply_kernel<T, KIND, NIN><<<pl.nblocks, kStatThreads, StatPipe<NIN>::kSmem, st>>>(aa, rows, pl.rpb);
     return cudaGetLastError();
 }
 
@@ -471,15 +521,8 @@ cudaError_t bn_forward(int dtype, const void* x, const float* gamma, const float
     ApplyArgs aa{};
     aa.a = x; aa.out = y; aa.gamma = gamma; aa.beta = beta; aa.mean = mean; aa.invstd = invstd;
     aa.slope = slope; aa.act = act; aa.n8 = rows * C / 8; aa.C = C;
-    const int nb = apply_blocks(aa.n8);
-    if (act == 2) {
-        if (dtype == kF16) apply_kernel<__half, 1><<<nb, kThreads, 0, st>>>(aa);
-        else apply_kernel<float, 1><<<nb, kThreads, 0, st>>>(aa);
-    } else {
-        if (dtype == kF16) apply_kernel<__half, 0><<<nb, kThreads, 0, st>>>(aa);
-        else apply_kernel<float, 0><<<nb, kThreads, 0, st>>>(aa);
-    }
-    return cudaGetLastError();
+    if (act == 2) return dtype == kF16 ? run_apply<__half, 1, 1>(aa, rows, pl, st) : run_apply<float, 1, 1>(aa, rows, pl, st);
+    return dtype == kF16 ? run_apply<__half, 0, 1>(aa, rows, pl, st) : run_apply<float, 0, 1>(aa, rows, pl, st);
 }
 
 cudaError_t bn_backward(int dtype, const void* dy, const void* x, const void* y_mask, const float* gamma,
@@ -499,10 +542,9 @@ cudaError_t bn_backward(int dtype, const void* dy, const void* x, const void* y_
     ApplyArgs aa{};
     aa.a = x; aa.dy = dy; aa.y = y_mask; aa.out = dx; aa.gamma = gamma; aa.mean = mean; aa.invstd = invstd;
     aa.coef = coef; aa.n8 = rows * C / 8; aa.C = C;
-    const int nb = apply_blocks(aa.n8);
-    if (dtype == kF16) apply_kernel<__half, 2><<<nb, kThreads, 0, st>>>(aa);
-    else apply_kernel<float, 2><<<nb, kThreads, 0, st>>>(aa);
-    return cudaGetLastError();
+    if (y_mask)
+        return dtype == kF16 ? run_apply<__half, 2, 3>(aa, rows, pl, st) : run_apply<float, 2, 3>(aa, rows, pl, st);
+    return dtype == kF16 ? run_apply<__half, 2, 2>(aa, rows, pl, st) : run_apply<float, 2, 2>(aa, rows, pl, st);
 }
 
 cudaError_t iabn_backward(int dtype, const void* dy, const void* y, const float* gamma, const float* beta,
@@ -521,10 +563,7 @@ cudaError_t iabn_backward(int dtype, const void* dy, const void* y, const float*
     ApplyArgs aa{};
     aa.a = y; aa.dy = dy; aa.out = dx; aa.gamma = gamma; aa.beta = beta; aa.invstd = invstd; aa.coef = coef;
     aa.slope = slope; aa.n8 = rows * C / 8; aa.C = C;
-    const int nb = apply_blocks(aa.n8);
-    if (dtype == kF16) apply_kernel<__half, 3><<<nb, kThreads, 0, st>>>(aa);
-    else apply_kernel<float, 3><<<nb, kThreads, 0, st>>>(aa);
-    return cudaGetLastError();
+    return dtype == kF16 ? run_apply<__half, 3, 2>(aa, rows, pl, st) : run_apply<float, 3, 2>(aa, rows, pl, st);
 }
 
 }  // namespace sdb
