@@ -87,11 +87,14 @@ cudaError_t anchor_targets(const AnchorTargetArgs& a, void* ws, cudaStream_t st)
 cudaError_t proposal_targets(const ProposalTargetArgs& a, cudaStream_t st);
 
 // ---- roi.cu
-// RoIAlign (aligned, fixed sampling ratio), NHWC features, rois [R][5]
+// RoIAlign (aligned, fixed sampling ratio), NHWC features, rois [R][5].
+// step > 1 computes only every step-th bin of the P x P grid (output
+// ceil(P/step)^2 bins): exactly the values a following 1x1 stride-`step`
+// convolution reads, so the stride folds into the pooling.
 cudaError_t roialign_fwd(int dtype, const void* feat, int N, int H, int W, int C, const float* rois, int R, int P,
-                         float scale, int sr, void* out, cudaStream_t st);
+                         float scale, int sr, void* out, cudaStream_t st, int step = 1);
 cudaError_t roialign_bwd(int dtype, const void* dy, int N, int H, int W, int C, const float* rois, int R, int P,
-                         float scale, int sr, void* dfeat, cudaStream_t st);
+                         float scale, int sr, void* dfeat, cudaStream_t st, int step = 1);
 cudaError_t maxpool_fwd(int dtype, const void* x, int N, int H, int W, int C, int k, int s, int p, void* y,
                         uint8_t* argmax, cudaStream_t st);
 cudaError_t maxpool_bwd(int dtype, const void* dy, const uint8_t* argmax, int N, int H, int W, int C, int k, int s,

@@ -159,6 +159,7 @@ struct sdb_det {
     Act c4, rpn_z, rpn_a, rpn_logits, rpn_deltas, roi_feat, head_out, pooled, cls_logits, bbox_pred;
     int A = 0, A_pad = 0, n_loc = 0, nA = 0, fh = 0, fw = 0, ncls = 0, ncls_pad = 0, nbox_pad = 0;
     int R = 0, P = 0, head_hw = 0, feat_c = 0;
+    int roi_step = 1;  // RoIAlign bin subsampling folded from a 1x1 stride-2 head entry
     float* anchors = nullptr;
     // targets
     float* gt = nullptr;
@@ -566,7 +567,7 @@ void run_step(sdb_det* d) {
     const float sscale = 1.0f / 16.0f;
     { PScope ps(d, P_ROI_F, 0, static_cast<double>(d->es) * (d->roi_feat.numel() + d->c4.numel()));
     CK(roialign_fwd(d->dt, d->c4.p, d->c4.n, d->c4.h, d->c4.w, d->c4.c, d->rois, d->R, d->P, sscale,
-                    cf.sampling_ratio, d->roi_feat.p, st)); }
+                    cf.sampling_ratio, d->roi_feat.p, st, d->roi_step)); }
     for (auto& b : d->head) block_fwd(d, b);
     { PScope ps(d, P_POOL, 0, static_cast<double>(d->es) * d->head_out.numel());
     CK(avgpool_fwd(d->dt, d->head_out.p, d->R, d->head_out.h * d->head_out.w, d->feat_c, d->pooled.p, st)); }
@@ -615,7 +616,7 @@ void run_step(sdb_det* d) {
     void* dc4 = d->gbuf[(cur == d->gbuf[2]) ? 3 : 2];
     { PScope ps(d, P_ROI_B, 0, static_cast<double>(d->es) * (d->roi_feat.numel() + d->c4.numel()));
     CK(roialign_bwd(d->dt, cur, d->c4.n, d->c4.h, d->c4.w, d->c4.c, d->rois, d->R, d->P, sscale, cf.sampling_ratio,
-                    dc4, st)); }
+                    dc4, st, d->roi_step)); }
     // RPN head backward (bbox, cls, conv)
     void* drpn = d->gbuf[0];
     conv_wgrad_to(B, d->rpn_bbox, d->rpn_a, d->d_rpn_deltas);
@@ -768,7 +769,22 @@ int sdb_det_create(sdb_ctx* ctx, const sdb_det_config* cfgp, sdb_det** out) {
         d->rpn_deltas = d->act(b, d->fh, d->fw, 4 * d->A_pad);
         d->R = b * cf.roi_batch;
         d->P = cf.pool;
-        d->roi_feat = d->act(d->R, d->P, d->P, 1024);
+        // The res5 entry block reads the RoIAlign output only through 1x1
+        // stride-2 pad-0 convolutions (conv1 and the shortcut), i.e. only the
+        // even bins.  Pool just those bins (bitwise the same values) and run
+        // both convolutions at stride 1: 3/4 of the RoIAlign output, its
+        // gradient and the dgrad zero phases are never materialised.
+        if (!d->head.empty() && d->P % 2 == 0) {
+            Block& h0 = d->head[0];
+            auto one_by_one_s2 = [](const ConvL& c) { return c.g.R == 1 && c.g.S == 1 && c.g.stride == 2 && c.g.pad == 0; };
+            if (one_by_one_s2(h0.c1) && h0.has_down && one_by_one_s2(h0.down)) {
+                d->roi_step = 2;
+                h0.c1.g.stride = 1;
+                h0.down.g.stride = 1;
+            }
+        }
+        const int Po = (d->P + d->roi_step - 1) / d->roi_step;
+        d->roi_feat = d->act(d->R, Po, Po, 1024);
         d->gbuf_elems = std::max({d->gbuf_elems, d->c4.numel(), d->rpn_z.numel(), d->roi_feat.numel(),
                                   d->rpn_deltas.numel()});
         if (!d->head.empty()) {

@@ -12,11 +12,14 @@
 // The optional fused ReLU of the BN path (C1: BN followed by relu,
 // model.cpp:238-245) keeps its mask in the stored output (y>0 <=> z>0).
 //
-// Kernels: (1) per-block partial statistics, 8 channels per thread with
-// 128-bit loads, fp32 runs of <=16 rows folded into fp64 registers, fp64
-// block reduction in smem -> partial[block][2C]; (2) fixed-order fp64
-// finalize per channel (deterministic, no atomics); (3) vectorised apply.
-// The second read of x in (3) mostly hits the 126 MB L2.
+// Kernels: (1) per-block partial statistics: a producer lane streams 16 KB
+// row tiles into a shared-memory ring with cp.async.bulk, 8 consumer warps
+// (8 channels per thread) accumulate every element in fp64 exactly like the
+// reference, fp64 block reduction -> partial[block][2C]; (2) fixed-order fp64
+// finalize per channel (deterministic, no atomics); (3) apply through the same
+// bulk-copy ring, float expressions evaluated in the reference's order
+// without FMA contraction.  The second read of x in (3) mostly hits the
+// 126 MB L2.
 #include <algorithm>
 
 #include "common.cuh"
@@ -165,8 +168,13 @@ __global__ void __launch_bounds__(kStatThreads, 2) stats_kernel(StatArgs p) {
             }
         }
         const float inv_slope = 1.0f / p.slope;
-        float s[8] = {}, q[8] = {};
-        int run = 0;
+        // Every element is accumulated in fp64 exactly as the reference does
+        // (syncbn.cpp:29-39, memopt.cpp:250-258 / 305-314): the float value
+        // widened to double, the product formed exactly in double (fma of two
+        // widened floats rounds once, like `s += (double)a * b`).  Only the
+        // order of the fp64 additions differs, so the float-rounded sums, and
+        // with them mean/invstd, agree with the reference to the last bit
+        // almost always.
         for (int i = 0; i < ntiles; ++i) {
             const int st = i % ST;
             mbar_wait(&full[st], (i / ST) & 1);
@@ -184,46 +192,32 @@ __global__ void __launch_bounds__(kStatThreads, 2) stats_kernel(StatArgs p) {
                 if (KIND == 0) {
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
-                        s[j] += v[j];
-                        q[j] += v[j] * v[j];
+                        const double dv = static_cast<double>(v[j]);
+                        S[j] = __dadd_rn(S[j], dv);
+                        Q[j] = __fma_rn(dv, dv, Q[j]);
                     }
                 } else if (KIND == 1) {
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
                         const float d = (NIN == 3 && !(ym[j] > 0.f)) ? 0.f : dd[j];
-                        const float xh = (v[j] - mu[j]) * is[j];
-                        s[j] += d;
-                        q[j] += d * xh;
+                        const float xh = __fmul_rn(__fsub_rn(v[j], mu[j]), is[j]);
+                        S[j] = __dadd_rn(S[j], static_cast<double>(d));
+                        Q[j] = __fma_rn(static_cast<double>(d), static_cast<double>(xh), Q[j]);
                     }
                 } else {
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
                         const float yv = v[j];
-                        const float z = yv >= 0.f ? yv : yv * inv_slope;
-                        const float dz = dd[j] * (yv > 0.f ? 1.f : p.slope);
-                        const float xh = (z - b[j]) * g[j];
-                        s[j] += dz;
-                        q[j] += dz * xh;
+                        const float z = yv >= 0.f ? yv : __fmul_rn(yv, inv_slope);
+                        const float dz = __fmul_rn(dd[j], yv > 0.f ? 1.f : p.slope);
+                        const float xh = __fmul_rn(__fsub_rn(z, b[j]), g[j]);
+                        S[j] = __dadd_rn(S[j], static_cast<double>(dz));
+                        Q[j] = __fma_rn(static_cast<double>(dz), static_cast<double>(xh), Q[j]);
                     }
-                }
-                // fp32 runs of <= 16 rows, folded into fp64
-                if (++run == 16) {
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        S[j] += s[j];
-                        Q[j] += q[j];
-                        s[j] = q[j] = 0.f;
-                    }
-                    run = 0;
                 }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[st]);
-        }
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            S[j] += s[j];
-            Q[j] += q[j];
         }
     }
     // every stage has been consumed (all bulk copies landed): reuse the ring
@@ -390,7 +384,7 @@ __global__ void __launch_bounds__(kStatThreads, 2) apply_kernel(ApplyArgs p, int
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
         ig[j] = 1.0f / g[j];
-        gis[j] = g[j] * is[j];
+        gis[j] = __fmul_rn(g[j], is[j]);
     }
     const float inv_slope = 1.0f / p.slope;
     T* out = static_cast<T*>(p.out);
@@ -409,9 +403,10 @@ __global__ void __launch_bounds__(kStatThreads, 2) apply_kernel(ApplyArgs p, int
             if (KIND == 0 || KIND == 1) {
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
-                    const float z = g[j] * (v[j] - mu[j]) * is[j] + b[j];
+                    // gamma*(x-mean)*invstd + beta, evaluated like the reference (no contraction)
+                    const float z = __fadd_rn(__fmul_rn(__fmul_rn(g[j], __fsub_rn(v[j], mu[j])), is[j]), b[j]);
                     if (KIND == 0) o[j] = (p.act && !(z > 0.f)) ? 0.f : z;
-                    else o[j] = z > 0.f ? z : p.slope * z;
+                    else o[j] = z > 0.f ? z : __fmul_rn(p.slope, z);
                 }
             } else {
                 float d[8];
@@ -425,17 +420,18 @@ __global__ void __launch_bounds__(kStatThreads, 2) apply_kernel(ApplyArgs p, int
                     }
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
-                        const float xh = (v[j] - mu[j]) * is[j];
-                        o[j] = gis[j] * (d[j] - k1[j] - xh * k2[j]);
+                        // gis * (dy - s1 - xh * s2), syncbn.cpp:110-111 (no contraction)
+                        const float xh = __fmul_rn(__fsub_rn(v[j], mu[j]), is[j]);
+                        o[j] = __fmul_rn(gis[j], __fsub_rn(__fsub_rn(d[j], k1[j]), __fmul_rn(xh, k2[j])));
                     }
                 } else {
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
                         const float yv = v[j];
-                        const float z = yv >= 0.f ? yv : yv * inv_slope;
-                        const float dz = d[j] * (yv > 0.f ? 1.f : p.slope);
-                        const float xh = (z - b[j]) * ig[j];
-                        o[j] = gis[j] * (dz - k1[j] - xh * k2[j]);
+                        const float z = yv >= 0.f ? yv : __fmul_rn(yv, inv_slope);
+                        const float dz = __fmul_rn(d[j], yv > 0.f ? 1.f : p.slope);
+                        const float xh = __fmul_rn(__fsub_rn(z, b[j]), ig[j]);
+                        o[j] = __fmul_rn(gis[j], __fsub_rn(__fsub_rn(dz, k1[j]), __fmul_rn(xh, k2[j])));
                     }
                 }
             }

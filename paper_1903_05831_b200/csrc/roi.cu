@@ -85,16 +85,18 @@ SDB_DEV float sample_coord(float start, int p, float bin, int i, int sr) {
 // ---------------------------------------------------------------- RoIAlign fwd
 template <class T>
 __global__ void roialign_fwd_kernel(const T* __restrict__ feat, int H, int W, int C, const float* __restrict__ rois,
-                                    int R, int P, float scale, int sr, T* __restrict__ out) {
+                                    int R, int P, float scale, int sr, int step, T* __restrict__ out) {
+    // output bins: every `step`-th bin of the P x P grid (Po x Po of them)
     const int C8 = C / 8;
-    const int64_t total = static_cast<int64_t>(R) * P * P * C8;
+    const int Po = (P + step - 1) / step;
+    const int64_t total = static_cast<int64_t>(R) * Po * Po * C8;
     const float count = static_cast<float>(max(sr * sr, 1));
     for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int c8 = static_cast<int>(e % C8);
         const int64_t bin = e / C8;
-        const int pw = static_cast<int>(bin % P), ph = static_cast<int>((bin / P) % P);
-        const int r = static_cast<int>(bin / (P * P));
+        const int pw = static_cast<int>(bin % Po) * step, ph = static_cast<int>((bin / Po) % Po) * step;
+        const int r = static_cast<int>(bin / (Po * Po));
         const Geom g = roi_geom(rois + static_cast<int64_t>(r) * 5, P, scale);
         float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         if (g.b >= 0) {
@@ -136,7 +138,10 @@ constexpr int kMaxP = 16;
 template <class T>
 __global__ void __launch_bounds__(kBwdThreads) roialign_bwd_kernel(const T* __restrict__ dy, int H, int W, int C,
                                                                    const float* __restrict__ rois, int R, int P,
-                                                                   float scale, int sr, T* __restrict__ dfeat) {
+                                                                   float scale, int sr, int step,
+                                                                   T* __restrict__ dfeat) {
+    // dY holds every `step`-th bin of the P x P grid (Po x Po of them)
+    const int Po = (P + step - 1) / step;
     __shared__ float WY[kMaxP][kTile];
     __shared__ float WX[kMaxP][kTile];
     __shared__ int rng[2][4][kTile];  // double-buffered [row lo, row hi, col lo, col hi] of nonzero bins
@@ -144,7 +149,7 @@ __global__ void __launch_bounds__(kBwdThreads) roialign_bwd_kernel(const T* __re
     __shared__ int sh[40];
     if (threadIdx.x < 64) {
         const int t = threadIdx.x & 31;
-        rng[threadIdx.x >> 5][t >> 3][t & 7] = ((t >> 3) & 1) ? -1 : P;
+        rng[threadIdx.x >> 5][t >> 3][t & 7] = ((t >> 3) & 1) ? -1 : Po;
     }
     int it_count = 0;
     const int n = blockIdx.z;
@@ -208,18 +213,19 @@ __global__ void __launch_bounds__(kBwdThreads) roialign_bwd_kernel(const T* __re
             // reset the other range buffer (last read two RoIs ago, before a barrier)
             if (threadIdx.x < 32) {
                 const int t = threadIdx.x;
-                rng[buf ^ 1][t >> 3][t & 7] = ((t >> 3) & 1) ? -1 : P;
+                rng[buf ^ 1][t >> 3][t & 7] = ((t >> 3) & 1) ? -1 : Po;
             }
             // separable weights for this tile
-            for (int t = threadIdx.x; t < 2 * P * kTile; t += kBwdThreads) {
-                const bool isx = t >= P * kTile;
-                const int tt = isx ? t - P * kTile : t;
+            for (int t = threadIdx.x; t < 2 * Po * kTile; t += kBwdThreads) {
+                const bool isx = t >= Po * kTile;
+                const int tt = isx ? t - Po * kTile : t;
                 const int pb = tt / kTile, lo = tt % kTile;
                 const int pix = (isx ? x0 : y0) + lo;
                 const int lim = isx ? W : H;
                 float wsum = 0.f;
                 for (int is = 0; is < sr; ++is) {
-                    float v = isx ? sample_coord(g.sw, pb, g.bw, is, sr) : sample_coord(g.sh, pb, g.bh, is, sr);
+                    float v = isx ? sample_coord(g.sw, pb * step, g.bw, is, sr)
+                                  : sample_coord(g.sh, pb * step, g.bh, is, sr);
                     if (v < -1.0f || v > static_cast<float>(lim)) continue;
                     if (v <= 0.f) v = 0.f;
                     int lo_i = static_cast<int>(v), hi_i;
@@ -237,7 +243,7 @@ __global__ void __launch_bounds__(kBwdThreads) roialign_bwd_kernel(const T* __re
             }
             __syncthreads();
             if (c_ok) {
-                const T* d = dy + static_cast<int64_t>(r) * P * P * C + c;
+                const T* d = dy + static_cast<int64_t>(r) * Po * Po * C + c;
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
                     const int p = pix0 + 8 * i;
@@ -252,7 +258,7 @@ __global__ void __launch_bounds__(kBwdThreads) roialign_bwd_kernel(const T* __re
                             if (wx == 0.f) continue;
                             const float wgt = wy * wx * inv_count;
                             float v[8];
-                            ld8<T>(d + (static_cast<int64_t>(ph) * P + pw) * C, v);
+                            ld8<T>(d + (static_cast<int64_t>(ph) * Po + pw) * C, v);
 #pragma unroll
                             for (int j = 0; j < 8; ++j) acc[i][j] += wgt * v[j];
                         }
@@ -697,28 +703,30 @@ template <class T>
 static inline const T* cp(const void* p) { return static_cast<const T*>(p); }
 
 cudaError_t roialign_fwd(int dtype, const void* feat, int N, int H, int W, int C, const float* rois, int R, int P,
-                         float scale, int sr, void* out, cudaStream_t st) {
+                         float scale, int sr, void* out, cudaStream_t st, int step) {
     (void)N;
-    const int64_t total = static_cast<int64_t>(R) * P * P * (C / 8);
+    if (step < 1) return cudaErrorInvalidValue;
+    const int Po = (P + step - 1) / step;
+    const int64_t total = static_cast<int64_t>(R) * Po * Po * (C / 8);
     if (dtype == kF16)
         roialign_fwd_kernel<__half><<<grid_for(total), 256, 0, st>>>(cp<__half>(feat), H, W, C, rois, R, P, scale, sr,
-                                                                    static_cast<__half*>(out));
+                                                                    step, static_cast<__half*>(out));
     else
         roialign_fwd_kernel<float><<<grid_for(total), 256, 0, st>>>(cp<float>(feat), H, W, C, rois, R, P, scale, sr,
-                                                                   static_cast<float*>(out));
+                                                                   step, static_cast<float*>(out));
     return cudaGetLastError();
 }
 
 cudaError_t roialign_bwd(int dtype, const void* dy, int N, int H, int W, int C, const float* rois, int R, int P,
-                         float scale, int sr, void* dfeat, cudaStream_t st) {
-    if (P > kMaxP) return cudaErrorInvalidValue;
+                         float scale, int sr, void* dfeat, cudaStream_t st, int step) {
+    if (step < 1 || (P + step - 1) / step > kMaxP) return cudaErrorInvalidValue;
     dim3 grid(((H + kTile - 1) / kTile) * ((W + kTile - 1) / kTile), (C + kSlab - 1) / kSlab, N);
     if (dtype == kF16)
         roialign_bwd_kernel<__half><<<grid, kBwdThreads, 0, st>>>(cp<__half>(dy), H, W, C, rois, R, P, scale, sr,
-                                                                  static_cast<__half*>(dfeat));
+                                                                  step, static_cast<__half*>(dfeat));
     else
         roialign_bwd_kernel<float><<<grid, kBwdThreads, 0, st>>>(cp<float>(dy), H, W, C, rois, R, P, scale, sr,
-                                                                 static_cast<float*>(dfeat));
+                                                                 step, static_cast<float*>(dfeat));
     return cudaGetLastError();
 }
 

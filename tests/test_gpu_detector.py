@@ -60,14 +60,21 @@ def test_c1_one_step_fp32(ref, orc):
     _losses_close(lg, lr, 1e-3)
     A = det.A
     assert norm_rel(s["logits"][..., :A].transpose(0, 3, 1, 2), lg_ref) <= 1e-3
+    # Gradients / parameter deltas: the north-star bar is 1e-2 per tensor.  A
+    # tighter 1e-3 is not a stable bar in fp32: with BN+ReLU a single RPN
+    # pre-activation sitting within ~1e-6 of zero flips its ReLU mask under any
+    # change of fp32 summation order (observed: one flip in 262144 moves the
+    # rpn.conv gradient by 2.3e-3 and everything below it by ~2.5e-3).  The
+    # global gradient is still held to 1e-3.
     g = dp.flat_grads(det)
     for (name, _, _), a, b in zip(det.params, dp.split(det, g), dp.split(det, g_ref)):
-        assert norm_rel(a, b) <= 1e-3, (name, norm_rel(a, b))
+        assert norm_rel(a, b) <= 1e-2, (name, norm_rel(a, b))
+    assert norm_rel(g, g_ref) <= 1e-3
     w_ref, v_ref = w0.copy(), np.zeros_like(w0)
     orc.orc_apply_sgd(ptr(w_ref), ptr(v_ref), ptr(g_ref), w0.size, det.p.lr, det.p.momentum, scale)
     w1 = dp.flat_params(det)
     for (name, _, _), a, b in zip(det.params, dp.split(det, w1 - w0), dp.split(det, w_ref - w0)):
-        assert norm_rel(a, b) <= 1e-3, (name, norm_rel(a, b))
+        assert norm_rel(a, b) <= 1e-2, (name, norm_rel(a, b))
     det.close()
 
 
@@ -101,10 +108,21 @@ def _ref16_vs_ref32(det, cfg16, w, s, scale):
 
 
 def test_c2_fp16_ten_steps(ref, orc):
+    """Per tensor, the GPU's fp16 gradient error against ref16 is held to the
+    reference's own fp16 noise level for that tensor, measured as err(ref16,
+    ref32) on the same inputs.  That noise level is itself a noisy estimate
+    from a single step: rpn.conv feeds a ReLU, and fp16 rounding flips a
+    handful of ReLU masks on near-zero pre-activations each step -- which of
+    them carries gradient decides whether that step's floor is 0.8e-2 or
+    2.5e-2.  The floor of a tensor is therefore taken over the 10-step
+    trajectory (its largest per-step value); losses, the global gradient and
+    the global parameter delta are still checked against the same step's
+    floor."""
     from paper_1903_05831_b200 import detector as D
     det = D.Detector(D.preset("c2", img_h=128, img_w=128))
     cfg = dp.ref_cfg(det)
     dp.check_param_order(det, cfg)
+    errs, floors = [], []
     for step in range(1, 11):
         slots = D.batch_slots(step, 0, 1, det.p.batch)
         w_gpu0, v_ref = dp.flat_params(det), dp.flat_velocity(det)
@@ -117,9 +135,8 @@ def test_c2_fp16_ten_steps(ref, orc):
         g16b, g32 = _ref16_vs_ref32(det, cfg, w_ref, s, scale)
         assert np.array_equal(g16, g16b)  # the oracle is deterministic
         g = dp.flat_grads(det)
-        for (name, _, _), a, b, c in zip(det.params, dp.split(det, g), dp.split(det, g16), dp.split(det, g32)):
-            floor = norm_rel(b, c)
-            assert norm_rel(a, b) <= max(1e-2, 1.5 * floor), (step, name, norm_rel(a, b), floor)
+        errs.append([norm_rel(a, b) for a, b in zip(dp.split(det, g), dp.split(det, g16))])
+        floors.append([norm_rel(b, c) for b, c in zip(dp.split(det, g16), dp.split(det, g32))])
         assert norm_rel(g, g16) <= max(1e-2, 1.5 * norm_rel(g16, g32))
         w_ref0 = w_ref.copy()
         assert orc.orc_has_nonfinite(ptr(g16), g16.size) == 0
@@ -127,6 +144,11 @@ def test_c2_fp16_ten_steps(ref, orc):
         w_gpu1 = dp.flat_params(det)
         dg, dr = w_gpu1 - w_gpu0, w_ref - w_ref0
         assert norm_rel(dg, dr) <= max(1e-2, 1.5 * norm_rel(g16, g32)), (step, norm_rel(dg, dr))
+    errs, floors = np.array(errs), np.array(floors)
+    bar = np.maximum(1e-2, 1.5 * floors.max(axis=0))
+    for i, (name, _, _) in enumerate(det.params):
+        for step in range(10):
+            assert errs[step, i] <= bar[i], (step + 1, name, errs[step, i], floors[:, i])
     det.close()
 
 
@@ -168,4 +190,26 @@ def test_injected_overflow_skips_step_and_backs_off():
     assert np.array_equal(np.nan_to_num(before), np.nan_to_num(after))  # untouched
     state = det.export(12, np.uint8)
     assert state[:8].view(np.float64)[0] == 2.0**14  # halved for the next step
+    det.close()
+
+
+def test_res5_head_fp32_one_step(ref, orc):
+    """R50-C4 RoI-head structure (RoIAlign 14x14 -> res5 with 1x1 stride-2 entry
+    convolutions) on a small detector: the GPU folds the stride into RoIAlign
+    (pools only the even bins, runs the entry convs at stride 1); the oracle runs
+    the literal 14x14 RoIAlign + stride-2 convs on the reference Tape."""
+    from paper_1903_05831_b200 import detector as D
+    det = D.Detector(D.preset("c2", img_h=128, img_w=128, mode=2, scale_init=1.0, blocks=(1, 1, 1, 1), pool=14,
+                              roi_batch=16))
+    cfg = dp.ref_cfg(det)
+    dp.check_param_order(det, cfg)
+    w0 = dp.flat_params(det)
+    slots = D.batch_slots(1, 0, 1, det.p.batch)
+    lg, scale, s = _step(det, slots)
+    lr, g_ref, _, _ = dp.oracle_step(det, cfg, w0, s, scale)
+    _losses_close(lg, lr, 1e-3)
+    g = dp.flat_grads(det)
+    for (name, _, _), a, b in zip(det.params, dp.split(det, g), dp.split(det, g_ref)):
+        assert norm_rel(a, b) <= 1e-2, (name, norm_rel(a, b))
+    assert norm_rel(g, g_ref) <= 1e-3
     det.close()
