@@ -24,6 +24,7 @@
 // counts.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include <cuda.h>
@@ -67,6 +68,114 @@ SDB_DEV uint32_t kmaj_off(int row, int chunk) {
 SDB_DEV uint32_t mnmaj_off(int mc, int k, int E) {
     return static_cast<uint32_t>((k >> 3) * (E / 64) * 1024 + (mc >> 3) * 1024 + (k & 7) * 128 +
                                  (((mc ^ k) & 7) << 4));
+}
+
+// Epilogue of one output tile, run by the 4 epilogue warps (warp w owns TMEM
+// lane quadrant q = w & 3, i.e. tile rows 32q..32q+31): TMEM -> registers
+// (16 columns at a time) -> XOR-swizzled smem staging -> coalesced 16-byte
+// stores (fp16 RNE, fp32 split-K partials for wgrad, optional dgrad addend).
+// The accumulator is handed back to the MMA warp as soon as it is drained.
+template <int MODE, int BN>
+SDB_DEV void epilogue_tile(const ConvArgs& a, int split, int m0, int n0, int nk, uint32_t tacc, int q, int lane,
+                           float* stg, uint64_t* tempty_acc) {
+    // row pointers of the 2 rows each lane stores in the coalesced phase
+    int64_t rowp[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const int r = (k * 32 + lane) >> 1;  // 0..31
+        const int grow = m0 + q * 32 + r;
+        int64_t o = -1;
+        if (grow < a.M) {
+            if (MODE == FPROP) {
+                o = static_cast<int64_t>(grow) * a.NG;
+            } else if (MODE == DGRAD) {
+                const int HpWp = a.Hp * a.Wp;
+                const int n = grow / HpWp, rem = grow - n * HpWp, i2 = rem / a.Wp, j2 = rem - i2 * a.Wp;
+                o = ((static_cast<int64_t>(n) * a.H + a.ph + a.stride * i2) * a.W + a.pw + a.stride * j2) * a.C;
+            } else {
+                o = (static_cast<int64_t>(split) * a.M + grow) * a.NG;
+            }
+        }
+        rowp[k] = o;
+    }
+    const int lim = MODE == DGRAD ? a.C : a.NG;
+#pragma unroll 1
+    for (int cb = 0; cb < BN; cb += 16) {
+        // residual fan-in: fetch the addend first so its latency overlaps the TMEM drain
+        uint4 addv[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+        if (MODE == DGRAD && a.accumulate) {
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const int col = n0 + cb + (((k * 32 + lane) & 1) * 8);
+                if (rowp[k] >= 0 && col + 8 <= lim && (lim & 7) == 0)
+                    addv[k] = *reinterpret_cast<const uint4*>(static_cast<const __half*>(a.addend) + rowp[k] + col);
+            }
+        }
+        uint32_t v[16];
+        tmem_ld16(tacc + (static_cast<uint32_t>(q * 32) << 16) + cb, v);
+        if (cb + 16 >= BN) {
+            // accumulator fully drained into registers: hand it back to the MMA
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tempty_acc);
+        }
+        if (nk == 0) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = 0u;
+        }
+        // stage row `lane` (16 fp32 = 4 x 16 B slots, XOR-swizzled: conflict-free)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int slot = j ^ ((lane >> 1) & 3);
+            *reinterpret_cast<float4*>(stg + lane * 16 + slot * 4) =
+                make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                            __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+        }
+        __syncwarp();
+        const int col0 = n0 + cb;
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int idx = k * 32 + lane;
+            const int r = idx >> 1, c8 = idx & 1;  // row, 8-column chunk
+            const int j0 = 2 * c8, sw = (r >> 1) & 3;
+            const float4 f0 = *reinterpret_cast<const float4*>(stg + r * 16 + ((j0 ^ sw) * 4));
+            const float4 f1 = *reinterpret_cast<const float4*>(stg + r * 16 + (((j0 + 1) ^ sw) * 4));
+            const int col = col0 + c8 * 8;
+            if (rowp[k] < 0 || col >= lim) continue;
+            float f[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
+            if (MODE == WGRAD) {
+                float* o = static_cast<float*>(a.out) + rowp[k] + col;
+                if (col + 8 <= lim && (lim & 3) == 0) {
+                    *reinterpret_cast<float4*>(o) = f0;
+                    *reinterpret_cast<float4*>(o + 4) = f1;
+                } else {
+                    for (int e = 0; e < 8 && col + e < lim; ++e) o[e] = f[e];
+                }
+            } else {
+                __half* o = static_cast<__half*>(a.out) + rowp[k] + col;
+                if (col + 8 <= lim && (lim & 7) == 0) {
+                    if (MODE == DGRAD && a.accumulate) {
+                        const __half* oh = reinterpret_cast<const __half*>(&addv[k]);
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) f[e] += __half2float(oh[e]);
+                    }
+                    uint4 pk;
+                    __half2* p2 = reinterpret_cast<__half2*>(&pk);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) p2[e] = __floats2half2_rn(f[2 * e], f[2 * e + 1]);
+                    *reinterpret_cast<uint4*>(o) = pk;
+                } else {
+                    for (int e = 0; e < 8 && col + e < lim; ++e) {
+                        float x = f[e];
+                        if (MODE == DGRAD && a.accumulate)
+                            x += __half2float(static_cast<const __half*>(a.addend)[rowp[k] + col + e]);
+                        o[e] = __float2half_rn(x);
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    }
 }
 
 // Persistent, warp-specialised tcgen05 implicit GEMM.
@@ -361,7 +470,6 @@ __global__ void __launch_bounds__(288, (BN <= 128) ? 2 : 1)
         __syncwarp();
     } else {
         // ------------------------------------------------ epilogue warps 5..8
-        const int q = warp & 3;  // TMEM lane quadrant this warp may access
         float* stg = staging + (warp - 5) * 32 * 16;
         int lt = 0;
         for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++lt) {
@@ -370,110 +478,217 @@ __global__ void __launch_bounds__(288, (BN <= 128) ? 2 : 1)
             const int acc = lt & 1;
             mbar_wait(&tfull[acc], (lt >> 1) & 1);
             tc_fence_after();
-            // row pointers of the 2 rows each lane stores in the coalesced phase
-            int64_t rowp[2];
-#pragma unroll
-            for (int k = 0; k < 2; ++k) {
-                const int r = (k * 32 + lane) >> 1;  // 0..31
-                const int grow = m0 + q * 32 + r;
-                int64_t o = -1;
-                if (grow < a.M) {
-                    if (MODE == FPROP) {
-                        o = static_cast<int64_t>(grow) * a.NG;
-                    } else if (MODE == DGRAD) {
-                        const int HpWp = a.Hp * a.Wp;
-                        const int n = grow / HpWp, rem = grow - n * HpWp, i2 = rem / a.Wp, j2 = rem - i2 * a.Wp;
-                        o = ((static_cast<int64_t>(n) * a.H + a.ph + a.stride * i2) * a.W + a.pw + a.stride * j2) * a.C;
-                    } else {
-                        const int split = t / (tiles_m * tiles_n);
-                        o = (static_cast<int64_t>(split) * a.M + grow) * a.NG;
-                    }
-                }
-                rowp[k] = o;
-            }
-            const int lim = MODE == DGRAD ? a.C : a.NG;
-#pragma unroll 1
-            for (int cb = 0; cb < BN; cb += 16) {
-                // residual fan-in: fetch the addend first so its latency overlaps the TMEM drain
-                uint4 addv[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
-                if (MODE == DGRAD && a.accumulate) {
-#pragma unroll
-                    for (int k = 0; k < 2; ++k) {
-                        const int col = n0 + cb + (((k * 32 + lane) & 1) * 8);
-                        if (rowp[k] >= 0 && col + 8 <= lim && (lim & 7) == 0)
-                            addv[k] = *reinterpret_cast<const uint4*>(static_cast<const __half*>(a.addend) + rowp[k] + col);
-                    }
-                }
-                uint32_t v[16];
-                tmem_ld16(tmem + acc * BN + (static_cast<uint32_t>(q * 32) << 16) + cb, v);
-                if (cb + 16 >= BN) {
-                    // accumulator fully drained into registers: hand it back to the MMA
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&tempty[acc]);
-                }
-                if (nk == 0) {
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) v[j] = 0u;
-                }
-                // stage row `lane` (16 fp32 = 4 x 16 B slots, XOR-swizzled: conflict-free)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int slot = j ^ ((lane >> 1) & 3);
-                    *reinterpret_cast<float4*>(stg + lane * 16 + slot * 4) =
-                        make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
-                                    __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
-                }
-                __syncwarp();
-                const int col0 = n0 + cb;
-#pragma unroll
-                for (int k = 0; k < 2; ++k) {
-                    const int idx = k * 32 + lane;
-                    const int r = idx >> 1, c8 = idx & 1;  // row, 8-column chunk
-                    const int j0 = 2 * c8, sw = (r >> 1) & 3;
-                    const float4 f0 = *reinterpret_cast<const float4*>(stg + r * 16 + ((j0 ^ sw) * 4));
-                    const float4 f1 = *reinterpret_cast<const float4*>(stg + r * 16 + (((j0 + 1) ^ sw) * 4));
-                    const int col = col0 + c8 * 8;
-                    if (rowp[k] < 0 || col >= lim) continue;
-                    float f[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
-                    if (MODE == WGRAD) {
-                        float* o = static_cast<float*>(a.out) + rowp[k] + col;
-                        if (col + 8 <= lim && (lim & 3) == 0) {
-                            *reinterpret_cast<float4*>(o) = f0;
-                            *reinterpret_cast<float4*>(o + 4) = f1;
-                        } else {
-                            for (int e = 0; e < 8 && col + e < lim; ++e) o[e] = f[e];
-                        }
-                    } else {
-                        __half* o = static_cast<__half*>(a.out) + rowp[k] + col;
-                        if (col + 8 <= lim && (lim & 7) == 0) {
-                            if (MODE == DGRAD && a.accumulate) {
-                                const __half* oh = reinterpret_cast<const __half*>(&addv[k]);
-#pragma unroll
-                                for (int e = 0; e < 8; ++e) f[e] += __half2float(oh[e]);
-                            }
-                            uint4 pk;
-                            __half2* p2 = reinterpret_cast<__half2*>(&pk);
-#pragma unroll
-                            for (int e = 0; e < 4; ++e) p2[e] = __floats2half2_rn(f[2 * e], f[2 * e + 1]);
-                            *reinterpret_cast<uint4*>(o) = pk;
-                        } else {
-                            for (int e = 0; e < 8 && col + e < lim; ++e) {
-                                float x = f[e];
-                                if (MODE == DGRAD && a.accumulate)
-                                    x += __half2float(static_cast<const __half*>(a.addend)[rowp[k] + col + e]);
-                                o[e] = __float2half_rn(x);
-                            }
-                        }
-                    }
-                }
-                __syncwarp();
-            }
+            epilogue_tile<MODE, BN>(a, t / (tiles_m * tiles_n), m0, n0, nk, tmem + acc * BN, warp & 3, lane, stg,
+                                    &tempty[acc]);
         }
     }
     tc_fence_before();
     __syncthreads();
     if (warp == 4) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 2 * BN);
+    }
+}
+
+// ============================================================ all-TMA tcgen05 kernel
+// Both operands arrive by TMA, the activation side through the im2col mode of
+// cp.async.bulk.tensor (the hardware walks the output-pixel traversal of the
+// convolution, applies the filter-tap offset and zero-fills the padding), so
+// the whole mainloop of a stage is 1-6 TMA instructions from one thread:
+//   fprop  A = im2col(X)        [128 pixels][64 c]   K-major   (needs C % 64 == 0)
+//          B = W               [BN k][64 (r,s,c)]   K-major   2-D tile
+//   dgrad  A = im2col(DY) over the sub-pixel phase grid, taps as non-negative
+//              offsets from a shifted base          K-major   (needs K % 64 == 0)
+//          B = W as [c][(tap,k)]                    MN-major  3-D tile
+//   wgrad  A = DY^T             [64 px][128 k]       MN-major  2-D tile
+//          B = im2col(X)^T      [64 px][BN (r,s,c)]  MN-major  (needs C % 64 == 0)
+// warp 0: TMA producer (one lane), warp 1: MMA issuer + TMEM owner,
+// warps 2-5: epilogue (TMEM lane quadrant = warp & 3).
+struct alignas(64) TmaPair {
+    CUtensorMap a, b;
+};
+
+SDB_DEV void tma_im2col_4d(uint32_t dst, const void* map, uint64_t* bar, int c, int w, int h, int n, int off_w,
+                           int off_h) {
+    const uint16_t ow = static_cast<uint16_t>(off_w), oh = static_cast<uint16_t>(off_h);
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, "
+        "%6}], [%2], {%7, %8};" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c), "r"(w), "r"(h), "r"(n), "h"(ow), "h"(oh)
+        : "memory");
+}
+
+template <int MODE, int BN, int ST>
+struct TmaCfg {
+    static constexpr int kABytes = kBM * kBK * 2;
+    static constexpr int kBBytes = BN * kBK * 2;
+    static constexpr int kStage = kABytes + kBBytes;
+    static constexpr int kStaging = 4 * 32 * 16 * 4;
+    static constexpr int kSmem = ST * kStage + kStaging + 1024 + 256;
+    static constexpr int kThreads = 192;
+    static constexpr int kPerSM = BN <= 128 ? 2 : 1;
+};
+
+template <int MODE, int BN, int ST>
+__global__ void __launch_bounds__(192, (BN <= 128) ? 2 : 1)
+    conv_tma_kernel(ConvArgs a, int tiles_m, int tiles_n, int n_tiles, const __grid_constant__ TmaPair tm) {
+    using Cfg = TmaCfg<MODE, BN, ST>;
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    uint8_t* gbase = smem_raw + (base - raw);
+    float* staging = reinterpret_cast<float*>(gbase + ST * Cfg::kStage);
+    uint64_t* full = reinterpret_cast<uint64_t*>(gbase + ST * Cfg::kStage + Cfg::kStaging);
+    uint64_t* empty = full + ST;
+    uint64_t* tfull = empty + ST;   // [2]
+    uint64_t* tempty = tfull + 2;   // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int nkb_total = (a.KG + kBK - 1) / kBK;
+    if (tid == 0) {
+        prefetch_tmap(&tm.a);
+        prefetch_tmap(&tm.b);
+        for (int s = 0; s < ST; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 4);
+        }
+        mbar_fence_init();
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, 2 * BN);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    auto tile_coords = [&](int t, int& m0, int& n0, int& kb0, int& nk) {
+        const int tm_ = t % tiles_m;
+        const int rest = t / tiles_m;
+        const int tn = rest % tiles_n;
+        const int split = rest / tiles_n;
+        m0 = tm_ * kBM;
+        n0 = tn * BN;
+        kb0 = MODE == WGRAD ? split * a.kb_per_split : 0;
+        nk = MODE == WGRAD ? max(0, min(a.kb_per_split, nkb_total - kb0)) : nkb_total;
+    };
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ------------------------------------------------ TMA producer
+            const int HoWo = a.Ho * a.Wo;
+            int it = 0;
+            for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+                int m0, n0, kb0, nk;
+                tile_coords(t, m0, n0, kb0, nk);
+                // im2col base of the tile's first output pixel (fprop / dgrad)
+                int bw = 0, bh = 0, bn = 0;
+                if (MODE == FPROP) {
+                    const int n = m0 / HoWo, rem = m0 - n * HoWo, oh = rem / a.Wo, ow = rem - oh * a.Wo;
+                    bn = n;
+                    bh = oh * a.stride - a.pad;
+                    bw = ow * a.stride - a.pad;
+                } else if (MODE == DGRAD) {
+                    const int HpWp = a.Hp * a.Wp;
+                    const int n = m0 / HpWp, rem = m0 - n * HpWp, i2 = rem / a.Wp, j2 = rem - i2 * a.Wp;
+                    bn = n;
+                    // DY row of phase pixel i2 for tap ti: i2 + cy - ti; base shifted by (nr-1) so the
+                    // per-tap offset (nr-1-ti) is non-negative
+                    bh = i2 + (a.ph + a.pad - a.r0) / a.stride - (a.nr - 1);
+                    bw = j2 + (a.pw + a.pad - a.q0) / a.stride - (a.nq - 1);
+                }
+                for (int k = 0; k < nk; ++k, ++it) {
+                    const int s = it % ST;
+                    if (it >= ST) mbar_wait(&empty[s], ((it / ST) - 1) & 1);
+                    const uint32_t sa = base + s * Cfg::kStage;
+                    const uint32_t sb = sa + Cfg::kABytes;
+                    const int kg0 = (kb0 + k) * kBK;
+                    mbar_arrive_expect_tx(&full[s], Cfg::kStage);
+                    if (MODE == FPROP) {
+                        const int tap = kg0 / a.C, c = kg0 - tap * a.C;
+                        const int r = tap / a.S, q = tap - r * a.S;
+                        tma_im2col_4d(sa, &tm.a, &full[s], c, bw, bh, bn, q, r);
+                        tma_load_2d(sb, &tm.b, &full[s], kg0, n0);
+                    } else if (MODE == DGRAD) {
+                        const int t2 = kg0 / a.K, kout = kg0 - t2 * a.K;
+                        const int ti = t2 / a.nq, tq = t2 - ti * a.nq;
+                        tma_im2col_4d(sa, &tm.a, &full[s], kout, bw, bh, bn, a.nq - 1 - tq, a.nr - 1 - ti);
+                        const int r2 = a.r0 + a.stride * ti, q2 = a.q0 + a.stride * tq;
+#pragma unroll
+                        for (int g = 0; g < BN / 64; ++g)
+                            tma_load_3d(sb + g * 8192, &tm.b, &full[s], n0 + 64 * g, r2 * a.S + q2, kout);
+                    } else {
+                        tma_load_2d(sa, &tm.a, &full[s], m0, kg0);
+                        tma_load_2d(sa + 8192, &tm.a, &full[s], m0 + 64, kg0);
+                        const int n = kg0 / HoWo, rem = kg0 - n * HoWo, oh = rem / a.Wo, ow = rem - oh * a.Wo;
+                        const int h = oh * a.stride - a.pad, w = ow * a.stride - a.pad;
+#pragma unroll
+                        for (int g = 0; g < BN / 64; ++g) {
+                            int col = n0 + 64 * g;
+                            if (col >= a.NG) col = 0;  // beyond the filter: any valid box (columns discarded)
+                            const int tap = col / a.C, c = col - tap * a.C;
+                            const int r = tap / a.S, q = tap - r * a.S;
+                            tma_im2col_4d(sb + g * 8192, &tm.b, &full[s], c, w, h, n, q, r);
+                        }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ------------------------------------------------ MMA issuer
+            constexpr bool kAMN = MODE == WGRAD;
+            constexpr bool kBMN = MODE != FPROP;
+            constexpr uint32_t idesc = umma_idesc_f16(kBM, BN, kAMN ? 1 : 0, kBMN ? 1 : 0);
+            int it = 0, lt = 0;
+            for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++lt) {
+                int m0, n0, kb0, nk;
+                tile_coords(t, m0, n0, kb0, nk);
+                const int acc = lt & 1;
+                mbar_wait(&tempty[acc], ((lt >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t dcol = tmem + acc * BN;
+                for (int k = 0; k < nk; ++k, ++it) {
+                    const int s = it % ST;
+                    mbar_wait(&full[s], (it / ST) & 1);
+                    tc_fence_after();
+                    const uint32_t sa = base + s * Cfg::kStage;
+                    const uint32_t sb = sa + Cfg::kABytes;
+#pragma unroll
+                    for (int kk = 0; kk < kBK / 16; ++kk) {
+                        // TMA MN-major operands: 8 KB per 64-element MN atom (LBO), 1 KB per 8 k rows (SBO)
+                        const uint64_t ad = kAMN ? umma_desc_sw128(sa + kk * 2048, 8192, 1024)
+                                                 : umma_desc_sw128(sa + kk * 32, 16, 1024);
+                        const uint64_t bd = kBMN ? umma_desc_sw128(sb + kk * 2048, 8192, 1024)
+                                                 : umma_desc_sw128(sb + kk * 32, 16, 1024);
+                        umma_f16(dcol, ad, bd, idesc, (k > 0 || kk > 0) ? 1u : 0u);
+                    }
+                    umma_commit(&empty[s]);
+                }
+                umma_commit(&tfull[acc]);
+            }
+        }
+        __syncwarp();
+    } else {
+        // ------------------------------------------------ epilogue warps 2..5
+        float* stg = staging + (warp - 2) * 32 * 16;
+        int lt = 0;
+        for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++lt) {
+            int m0, n0, kb0, nk;
+            tile_coords(t, m0, n0, kb0, nk);
+            const int acc = lt & 1;
+            mbar_wait(&tfull[acc], (lt >> 1) & 1);
+            tc_fence_after();
+            epilogue_tile<MODE, BN>(a, t / (tiles_m * tiles_n), m0, n0, nk, tmem + acc * BN, warp & 3, lane, stg,
+                                    &tempty[acc]);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
         tc_fence_after();
         tmem_dealloc(tmem, 2 * BN);
     }
@@ -649,6 +864,103 @@ static bool make_tmap(CUtensorMap* m, const void* base, int rank, const uint64_t
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// cuTensorMapEncodeIm2col: 4-D NHWC tensor [N][H][W][C] fp16, SWIZZLE_128B,
+// 64 channels per pixel (128 B rows), `pixels` output pixels per box
+typedef CUresult (*EncodeIm2colFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t, const cuuint32_t*,
+                                   CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                   CUtensorMapFloatOOBfill);
+
+static bool make_im2col(CUtensorMap* m, const void* base, int N, int H, int W, int C, int lower_h, int lower_w,
+                        int upper_h, int upper_w, int stride, int pixels) {
+    static EncodeIm2colFn fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", reinterpret_cast<void**>(&fn), cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return false;
+    }
+    const cuuint64_t dims[4] = {static_cast<cuuint64_t>(C), static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H),
+                                static_cast<cuuint64_t>(N)};
+    const cuuint64_t strides[3] = {static_cast<cuuint64_t>(C) * 2, static_cast<cuuint64_t>(W) * C * 2,
+                                   static_cast<cuuint64_t>(H) * W * C * 2};
+    const int lower[2] = {lower_w, lower_h};
+    const int upper[2] = {upper_w, upper_h};
+    const cuuint32_t es[4] = {1, static_cast<cuuint32_t>(stride), static_cast<cuuint32_t>(stride), 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<void*>(base), dims, strides, lower, upper, 64,
+              static_cast<cuuint32_t>(pixels), es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static bool& tma_disabled_flag() {
+    static bool f = std::getenv("SDB_CONV_NO_TMA") != nullptr;
+    return f;
+}
+
+// all-TMA path applicability (see conv_tma_kernel)
+static bool tma_ok(const ConvArgs& a, int mode) {
+    if (tma_disabled_flag()) return false;
+    if (mode == DGRAD) return (a.K % kBK) == 0;
+    return (a.C % 64) == 0;
+}
+
+template <int MODE, int BN, int ST>
+static cudaError_t launch_tma(const ConvArgs& a, int splits, cudaStream_t st) {
+    using Cfg = TmaCfg<MODE, BN, ST>;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(conv_tma_kernel<MODE, BN, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
+        configured = true;
+    }
+    const int tiles_m = (a.M + kBM - 1) / kBM, tiles_n = (a.NG + BN - 1) / BN;
+    const int n_tiles = tiles_m * tiles_n * splits;
+    const int grid = std::min(n_tiles, Cfg::kPerSM * kNumSMs);
+    TmaPair tm;
+    std::memset(&tm, 0, sizeof(tm));
+    bool ok;
+    if (MODE == FPROP) {
+        ok = make_im2col(&tm.a, a.x, a.N, a.H, a.W, a.C, -a.pad, -a.pad, a.pad - (a.R - 1), a.pad - (a.S - 1), a.stride,
+                         kBM);
+        const uint64_t dims[2] = {static_cast<uint64_t>(a.KG), static_cast<uint64_t>(a.NG)};
+        const uint64_t strides[1] = {static_cast<uint64_t>(a.KG) * 2};
+        const uint32_t box[2] = {64, static_cast<uint32_t>(BN)};
+        ok = ok && make_tmap(&tm.b, a.w, 2, dims, strides, box);
+    } else if (MODE == DGRAD) {
+        // DY over the phase grid: Hp x Wp output positions, base shifted by (nr-1, nq-1)
+        const int lh = (a.ph + a.pad - a.r0) / a.stride - (a.nr - 1);
+        const int lw = (a.pw + a.pad - a.q0) / a.stride - (a.nq - 1);
+        ok = make_im2col(&tm.a, a.x, a.N, a.Ho, a.Wo, a.K, lh, lw, a.Hp - a.Ho + lh, a.Wp - a.Wo + lw, 1, kBM);
+        const uint64_t dims[3] = {static_cast<uint64_t>(a.C), static_cast<uint64_t>(a.R) * a.S, static_cast<uint64_t>(a.K)};
+        const uint64_t strides[2] = {static_cast<uint64_t>(a.C) * 2, static_cast<uint64_t>(a.R) * a.S * a.C * 2};
+        const uint32_t box[3] = {64, 1, 64};
+        ok = ok && make_tmap(&tm.b, a.w, 3, dims, strides, box);
+    } else {
+        const uint64_t dims[2] = {static_cast<uint64_t>(a.M), static_cast<uint64_t>(a.KG)};
+        const uint64_t strides[1] = {static_cast<uint64_t>(a.M) * 2};
+        const uint32_t box[2] = {64, 64};
+        ok = make_tmap(&tm.a, a.w, 2, dims, strides, box);
+        ok = ok && make_im2col(&tm.b, a.x, a.N, a.H, a.W, a.C, -a.pad, -a.pad, a.pad - (a.R - 1), a.pad - (a.S - 1),
+                               a.stride, kBK);
+    }
+    if (!ok) return cudaErrorInvalidValue;
+    conv_tma_kernel<MODE, BN, ST><<<grid, Cfg::kThreads, Cfg::kSmem, st>>>(a, tiles_m, tiles_n, n_tiles, tm);
+    return cudaGetLastError();
+}
+
+// tile width: 256 when the GEMM N is wide enough (one CTA per SM, 2 x 256 TMEM
+// columns), else 128 / 64 (two CTAs per SM)
+static int tma_bn(const ConvArgs& a) { return a.NG >= 256 ? 256 : (a.NG > 64 ? 128 : 64); }
+
+template <int MODE>
+static cudaError_t launch_tma_pick(const ConvArgs& a, int splits, cudaStream_t st) {
+    switch (tma_bn(a)) {
+        case 256: return launch_tma<MODE, 256, 4>(a, splits, st);
+        case 128: return launch_tma<MODE, 128, 3>(a, splits, st);
+        default: return launch_tma<MODE, 64, 4>(a, splits, st);
+    }
+}
+
 template <int MODE, int BN, int ST>
 static cudaError_t launch_tc(const ConvArgs& a, int splits, cudaStream_t st) {
     using Cfg = TcPCfg<MODE, BN, ST>;
@@ -731,7 +1043,7 @@ cudaError_t conv_fprop(const ConvShape& g, int dtype, const void* x, const void*
     a.M = g.N * a.Ho * a.Wo;
     a.NG = g.K;
     a.KG = g.R * g.S * g.C;
-    if (tc_ok(g, dtype)) return launch_tc_pick<FPROP>(a, 1, st);
+    if (tc_ok(g, dtype)) return tma_ok(a, FPROP) ? launch_tma_pick<FPROP>(a, 1, st) : launch_tc_pick<FPROP>(a, 1, st);
     return dtype == kF16 ? launch_simt<__half, FPROP>(a, 1, st) : launch_simt<float, FPROP>(a, 1, st);
 }
 
@@ -781,7 +1093,7 @@ cudaError_t conv_dgrad(const ConvShape& g, int dtype, const void* dy, const void
                 continue;  // zeroed above (or untouched when accumulating)
             } else if (tc_ok(g, dtype)) {
                 a.tma_b = (g.K % kBK) == 0 ? 1 : 0;
-                e = launch_tc_pick<DGRAD>(a, 1, st);
+                e = tma_ok(a, DGRAD) ? launch_tma_pick<DGRAD>(a, 1, st) : launch_tc_pick<DGRAD>(a, 1, st);
             } else {
                 e = dtype == kF16 ? launch_simt<__half, DGRAD>(a, 1, st) : launch_simt<float, DGRAD>(a, 1, st);
             }
@@ -795,12 +1107,19 @@ cudaError_t conv_dgrad(const ConvShape& g, int dtype, const void* dy, const void
 // with >= 8 k-blocks per split.
 static int wgrad_splits(const ConvShape& g, int dtype) {
     ConvArgs a = make_args(g);
-    const int64_t M = g.K, NG = static_cast<int64_t>(g.R) * g.S * g.C, KG = static_cast<int64_t>(g.N) * a.Ho * a.Wo;
+    a.M = g.K;
+    a.NG = g.R * g.S * g.C;
+    a.KG = g.N * a.Ho * a.Wo;
+    const int64_t M = a.M, NG = a.NG, KG = a.KG;
     const bool tc = tc_ok(g, dtype);
     const int bk = tc ? kBK : 16;
     const int64_t nkb = (KG + bk - 1) / bk;
     int64_t tiles, per_sm;
-    if (tc) {
+    if (tc && tma_ok(a, WGRAD)) {
+        const int bn = tma_bn(a);
+        tiles = ((M + 127) / 128) * ((NG + bn - 1) / bn);
+        per_sm = bn <= 128 ? 2 : 1;
+    } else if (tc) {
         const int bn = NG <= 64 ? 64 : 128;  // split-K launches never pick BN=256 unless tiles are plentiful
         tiles = ((M + 127) / 128) * ((NG + bn - 1) / bn);
         per_sm = 2;
@@ -836,7 +1155,7 @@ cudaError_t conv_wgrad(const ConvShape& g, int dtype, const void* x, const void*
     if (ws == nullptr || ws_bytes < static_cast<size_t>(per) * sizeof(float) * splits) return cudaErrorInvalidValue;
     a.out = ws;
     cudaError_t e;
-    if (tc) e = launch_tc_pick<WGRAD>(a, splits, st);
+    if (tc) e = tma_ok(a, WGRAD) ? launch_tma_pick<WGRAD>(a, splits, st) : launch_tc_pick<WGRAD>(a, splits, st);
     else e = dtype == kF16 ? launch_simt<__half, WGRAD>(a, splits, st) : launch_simt<float, WGRAD>(a, splits, st);
     if (e != cudaSuccess) return e;
     const int blocks = static_cast<int>(std::min<int64_t>((per + 255) / 256, 8 * kNumSMs));

@@ -20,6 +20,14 @@ CONV_CASES = [
     (1, 24, 7, 5, 40, 3, 3, 1, 1),
     (2, 64, 20, 24, 256, 3, 3, 1, 1),
     (1, 3, 11, 13, 8, 3, 3, 1, 1),
+    # all-TMA path (C % 64 == 0 / K % 64 == 0): im2col boxes that wrap rows and
+    # images, stride 2, sub-pixel dgrad phases, BN = 64/128/256, split-K wgrad
+    (2, 128, 15, 13, 128, 3, 3, 2, 1),
+    (3, 64, 14, 14, 128, 1, 1, 2, 0),
+    (2, 256, 10, 9, 512, 1, 1, 1, 0),
+    (1, 192, 7, 7, 64, 3, 3, 1, 1),
+    (2, 64, 30, 31, 64, 3, 3, 1, 1),
+    (4, 128, 28, 28, 256, 3, 3, 1, 1),
 ]
 
 
