@@ -49,6 +49,7 @@ struct ConvArgs {
     int accumulate;  // dgrad: out = result + addend
     const void* addend;  // dgrad accumulate source (may alias out)
     int tma_b;       // dgrad: filter operand loaded by TMA (needs K % 64 == 0)
+    int plain;       // 1x1 / stride 1 / pad 0: the activation operand is a plain 2-D [pixels][channels] tile
 };
 
 // TMA descriptors of the dense GEMM operand (filter for fprop/dgrad, DY for wgrad)
@@ -500,8 +501,12 @@ __global__ void __launch_bounds__(288, (BN <= 128) ? 2 : 1)
 //   dgrad  A = im2col(DY) over the sub-pixel phase grid, taps as non-negative
 //              offsets from a shifted base          K-major   (needs K % 64 == 0)
 //          B = W as [c][(tap,k)]                    MN-major  3-D tile
-//   wgrad  A = DY^T             [64 px][128 k]       MN-major  2-D tile
-//          B = im2col(X)^T      [64 px][BN (r,s,c)]  MN-major  (needs C % 64 == 0)
+//   wgrad  computed transposed, DW^T[(r,s,c)][k] = sum_px im2col(X)[px][(r,s,c)] DY[px][k]:
+//          A = im2col(X)^T      [64 px][128 (r,s,c)] MN-major  (needs C % 64 == 0)
+//          B = DY^T             [64 px][BN k]        MN-major  2-D tile
+//          so only 16 KB of each stage goes through the (slower) im2col path;
+//          the fp32 split-K partials are [split][(r,s,c)][k] and the reduce
+//          transposes them into the KRSC gradient.
 // warp 0: TMA producer (one lane), warp 1: MMA issuer + TMEM owner,
 // warps 2-5: epilogue (TMEM lane quadrant = warp & 3).
 struct alignas(64) TmaPair {
@@ -579,7 +584,13 @@ __global__ void __launch_bounds__(192, (BN <= 128) ? 2 : 1)
     if (warp == 0) {
         if (lane == 0) {
             // ------------------------------------------------ TMA producer
+            // A single thread issues every TMA of the CTA, so its per-k-block
+            // instruction latency must stay well below the MMA time of a
+            // k-block (~512 cycles at BN = 256): all divisions are hoisted to
+            // the tile and the k-block coordinates advance by carries.
             const int HoWo = a.Ho * a.Wo;
+            // wgrad: a k-block is 64 consecutive output pixels; 64 = dn*HoWo + doh*Wo + dow
+            const int dn = kBK / HoWo, drem = kBK - dn * HoWo, doh = drem / a.Wo, dow = drem - doh * a.Wo;
             int it = 0;
             for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
                 int m0, n0, kb0, nk;
@@ -600,6 +611,28 @@ __global__ void __launch_bounds__(192, (BN <= 128) ? 2 : 1)
                     bh = i2 + (a.ph + a.pad - a.r0) / a.stride - (a.nr - 1);
                     bw = j2 + (a.pw + a.pad - a.q0) / a.stride - (a.nq - 1);
                 }
+                // k-block coordinates at k = 0, advanced by carries below
+                //   fprop: (r, q, c) of kg0 = kb*64          dgrad: (ti, tq, kout)
+                //   wgrad: output pixel (n, oh, ow) of kb*64
+                int c0 = 0, t0 = 0, t1 = 0;  // channel, tap row, tap col   (fprop / dgrad)
+                int pn = 0, poh = 0, pow_ = 0;  // wgrad pixel
+                int ar[2] = {0, 0}, aq[2] = {0, 0}, ac[2] = {0, 0};  // wgrad A chunks (tap row/col, channel)
+                if (MODE == WGRAD) {
+                    const int p0 = kb0 * kBK;
+                    pn = p0 / HoWo;
+                    const int rem = p0 - pn * HoWo;
+                    poh = rem / a.Wo;
+                    pow_ = rem - poh * a.Wo;
+#pragma unroll
+                    for (int g = 0; g < 2; ++g) {
+                        int col = m0 + 64 * g;
+                        if (col >= a.M) col = 0;  // beyond the filter: any valid box (rows discarded)
+                        const int tap = col / a.C;
+                        ac[g] = col - tap * a.C;
+                        ar[g] = tap / a.S;
+                        aq[g] = tap - ar[g] * a.S;
+                    }
+                }
                 for (int k = 0; k < nk; ++k, ++it) {
                     const int s = it % ST;
                     if (it >= ST) mbar_wait(&empty[s], ((it / ST) - 1) & 1);
@@ -608,30 +641,54 @@ __global__ void __launch_bounds__(192, (BN <= 128) ? 2 : 1)
                     const int kg0 = (kb0 + k) * kBK;
                     mbar_arrive_expect_tx(&full[s], Cfg::kStage);
                     if (MODE == FPROP) {
-                        const int tap = kg0 / a.C, c = kg0 - tap * a.C;
-                        const int r = tap / a.S, q = tap - r * a.S;
-                        tma_im2col_4d(sa, &tm.a, &full[s], c, bw, bh, bn, q, r);
+                        if (a.plain) tma_load_2d(sa, &tm.a, &full[s], kg0, m0);
+                        else tma_im2col_4d(sa, &tm.a, &full[s], c0, bw, bh, bn, t1, t0);
                         tma_load_2d(sb, &tm.b, &full[s], kg0, n0);
+                        // next (r, q, c): c += 64 with carries into q then r
+                        c0 += kBK;
+                        if (c0 >= a.C) {
+                            c0 = 0;
+                            if (++t1 == a.S) {
+                                t1 = 0;
+                                ++t0;
+                            }
+                        }
                     } else if (MODE == DGRAD) {
-                        const int t2 = kg0 / a.K, kout = kg0 - t2 * a.K;
-                        const int ti = t2 / a.nq, tq = t2 - ti * a.nq;
-                        tma_im2col_4d(sa, &tm.a, &full[s], kout, bw, bh, bn, a.nq - 1 - tq, a.nr - 1 - ti);
-                        const int r2 = a.r0 + a.stride * ti, q2 = a.q0 + a.stride * tq;
+                        // (t0, t1) = (ti, tq), c0 = kout
+                        if (a.plain) tma_load_2d(sa, &tm.a, &full[s], c0, m0);
+                        else tma_im2col_4d(sa, &tm.a, &full[s], c0, bw, bh, bn, a.nq - 1 - t1, a.nr - 1 - t0);
+                        const int r2 = a.r0 + a.stride * t0, q2 = a.q0 + a.stride * t1;
 #pragma unroll
                         for (int g = 0; g < BN / 64; ++g)
-                            tma_load_3d(sb + g * 8192, &tm.b, &full[s], n0 + 64 * g, r2 * a.S + q2, kout);
+                            tma_load_3d(sb + g * 8192, &tm.b, &full[s], n0 + 64 * g, r2 * a.S + q2, c0);
+                        c0 += kBK;
+                        if (c0 >= a.K) {
+                            c0 = 0;
+                            if (++t1 == a.nq) {
+                                t1 = 0;
+                                ++t0;
+                            }
+                        }
                     } else {
-                        tma_load_2d(sa, &tm.a, &full[s], m0, kg0);
-                        tma_load_2d(sa + 8192, &tm.a, &full[s], m0 + 64, kg0);
-                        const int n = kg0 / HoWo, rem = kg0 - n * HoWo, oh = rem / a.Wo, ow = rem - oh * a.Wo;
-                        const int h = oh * a.stride - a.pad, w = ow * a.stride - a.pad;
+                        const int h = poh * a.stride - a.pad, w = pow_ * a.stride - a.pad;
 #pragma unroll
-                        for (int g = 0; g < BN / 64; ++g) {
-                            int col = n0 + 64 * g;
-                            if (col >= a.NG) col = 0;  // beyond the filter: any valid box (columns discarded)
-                            const int tap = col / a.C, c = col - tap * a.C;
-                            const int r = tap / a.S, q = tap - r * a.S;
-                            tma_im2col_4d(sb + g * 8192, &tm.b, &full[s], c, w, h, n, q, r);
+                        for (int g = 0; g < 2; ++g) {
+                            if (a.plain) tma_load_2d(sa + g * 8192, &tm.a, &full[s], ac[g], kg0);
+                            else tma_im2col_4d(sa + g * 8192, &tm.a, &full[s], ac[g], w, h, pn, aq[g], ar[g]);
+                        }
+#pragma unroll
+                        for (int g = 0; g < BN / 64; ++g) tma_load_2d(sb + g * 8192, &tm.b, &full[s], n0 + 64 * g, kg0);
+                        // next pixel block: + (dn, doh, dow) in mixed radix (N, Ho, Wo)
+                        pow_ += dow;
+                        poh += doh;
+                        pn += dn;
+                        if (pow_ >= a.Wo) {
+                            pow_ -= a.Wo;
+                            ++poh;
+                        }
+                        if (poh >= a.Ho) {
+                            poh -= a.Ho;
+                            ++pn;
                         }
                     }
                 }
@@ -820,6 +877,29 @@ __global__ void wgrad_reduce_kernel(const float* __restrict__ ws, int splits, in
     }
 }
 
+// same, from transposed partials ws[s][j][i] (j < n_rows = R*S*C, i < n_cols = K)
+// into dw[i][j]: 32x32 tiles through shared memory, both sides coalesced
+template <class T>
+__global__ void wgrad_reduce_t_kernel(const float* __restrict__ ws, int splits, int n_rows, int n_cols,
+                                      T* __restrict__ dw) {
+    __shared__ float tile[32][33];
+    const int j0 = blockIdx.x * 32, i0 = blockIdx.y * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+    const int64_t per = static_cast<int64_t>(n_rows) * n_cols;
+    for (int jj = ty; jj < 32; jj += 8) {
+        const int j = j0 + jj, i = i0 + tx;
+        float acc = 0.f;
+        if (j < n_rows && i < n_cols)
+            for (int k = 0; k < splits; ++k) acc += ws[k * per + static_cast<int64_t>(j) * n_cols + i];
+        tile[jj][tx] = acc;
+    }
+    __syncthreads();
+    for (int ii = ty; ii < 32; ii += 8) {
+        const int i = i0 + ii, j = j0 + tx;
+        if (i < n_cols && j < n_rows) dw[static_cast<int64_t>(i) * n_rows + j] = from_f<T>(tile[tx][ii]);
+    }
+}
+
 // zero the dgrad output positions of a phase with no taps
 template <class T>
 __global__ void dgrad_zero_phase_kernel(ConvArgs a) {
@@ -906,7 +986,7 @@ static bool tma_ok(const ConvArgs& a, int mode) {
 }
 
 template <int MODE, int BN, int ST>
-static cudaError_t launch_tma(const ConvArgs& a, int splits, cudaStream_t st) {
+static cudaError_t launch_tma(ConvArgs a, int splits, cudaStream_t st) {
     using Cfg = TmaCfg<MODE, BN, ST>;
     static bool configured = false;
     if (!configured) {
@@ -919,9 +999,18 @@ static cudaError_t launch_tma(const ConvArgs& a, int splits, cudaStream_t st) {
     TmaPair tm;
     std::memset(&tm, 0, sizeof(tm));
     bool ok;
+    a.plain = (a.R == 1 && a.S == 1 && a.stride == 1 && a.pad == 0) ? 1 : 0;
+    // plain 2-D view of the activation operand: [pixels][channels]
+    auto plain_map = [&](CUtensorMap* m, const void* p, int64_t pixels, int chans, uint32_t box_pixels) {
+        const uint64_t dims[2] = {static_cast<uint64_t>(chans), static_cast<uint64_t>(pixels)};
+        const uint64_t strides[1] = {static_cast<uint64_t>(chans) * 2};
+        const uint32_t box[2] = {64, box_pixels};
+        return make_tmap(m, p, 2, dims, strides, box);
+    };
     if (MODE == FPROP) {
-        ok = make_im2col(&tm.a, a.x, a.N, a.H, a.W, a.C, -a.pad, -a.pad, a.pad - (a.R - 1), a.pad - (a.S - 1), a.stride,
-                         kBM);
+        ok = a.plain ? plain_map(&tm.a, a.x, static_cast<int64_t>(a.N) * a.H * a.W, a.C, kBM)
+                     : make_im2col(&tm.a, a.x, a.N, a.H, a.W, a.C, -a.pad, -a.pad, a.pad - (a.R - 1),
+                                   a.pad - (a.S - 1), a.stride, kBM);
         const uint64_t dims[2] = {static_cast<uint64_t>(a.KG), static_cast<uint64_t>(a.NG)};
         const uint64_t strides[1] = {static_cast<uint64_t>(a.KG) * 2};
         const uint32_t box[2] = {64, static_cast<uint32_t>(BN)};
@@ -930,18 +1019,21 @@ static cudaError_t launch_tma(const ConvArgs& a, int splits, cudaStream_t st) {
         // DY over the phase grid: Hp x Wp output positions, base shifted by (nr-1, nq-1)
         const int lh = (a.ph + a.pad - a.r0) / a.stride - (a.nr - 1);
         const int lw = (a.pw + a.pad - a.q0) / a.stride - (a.nq - 1);
-        ok = make_im2col(&tm.a, a.x, a.N, a.Ho, a.Wo, a.K, lh, lw, a.Hp - a.Ho + lh, a.Wp - a.Wo + lw, 1, kBM);
+        ok = a.plain ? plain_map(&tm.a, a.x, static_cast<int64_t>(a.N) * a.Ho * a.Wo, a.K, kBM)
+                     : make_im2col(&tm.a, a.x, a.N, a.Ho, a.Wo, a.K, lh, lw, a.Hp - a.Ho + lh, a.Wp - a.Wo + lw, 1, kBM);
         const uint64_t dims[3] = {static_cast<uint64_t>(a.C), static_cast<uint64_t>(a.R) * a.S, static_cast<uint64_t>(a.K)};
         const uint64_t strides[2] = {static_cast<uint64_t>(a.C) * 2, static_cast<uint64_t>(a.R) * a.S * a.C * 2};
         const uint32_t box[3] = {64, 1, 64};
         ok = ok && make_tmap(&tm.b, a.w, 3, dims, strides, box);
     } else {
-        const uint64_t dims[2] = {static_cast<uint64_t>(a.M), static_cast<uint64_t>(a.KG)};
-        const uint64_t strides[1] = {static_cast<uint64_t>(a.M) * 2};
+        // transposed orientation: M = (r,s,c), N = k; DY viewed as [pixels][k]
+        ok = a.plain ? plain_map(&tm.a, a.x, static_cast<int64_t>(a.N) * a.H * a.W, a.C, kBK)
+                     : make_im2col(&tm.a, a.x, a.N, a.H, a.W, a.C, -a.pad, -a.pad, a.pad - (a.R - 1),
+                                   a.pad - (a.S - 1), a.stride, kBK);
+        const uint64_t dims[2] = {static_cast<uint64_t>(a.NG), static_cast<uint64_t>(a.KG)};
+        const uint64_t strides[1] = {static_cast<uint64_t>(a.NG) * 2};
         const uint32_t box[2] = {64, 64};
-        ok = make_tmap(&tm.a, a.w, 2, dims, strides, box);
-        ok = ok && make_im2col(&tm.b, a.x, a.N, a.H, a.W, a.C, -a.pad, -a.pad, a.pad - (a.R - 1), a.pad - (a.S - 1),
-                               a.stride, kBK);
+        ok = ok && make_tmap(&tm.b, a.w, 2, dims, strides, box);
     }
     if (!ok) return cudaErrorInvalidValue;
     conv_tma_kernel<MODE, BN, ST><<<grid, Cfg::kThreads, Cfg::kSmem, st>>>(a, tiles_m, tiles_n, n_tiles, tm);
@@ -1116,8 +1208,10 @@ static int wgrad_splits(const ConvShape& g, int dtype) {
     const int64_t nkb = (KG + bk - 1) / bk;
     int64_t tiles, per_sm;
     if (tc && tma_ok(a, WGRAD)) {
+        // transposed orientation: GEMM M = R*S*C, N = K
+        std::swap(a.M, a.NG);
         const int bn = tma_bn(a);
-        tiles = ((M + 127) / 128) * ((NG + bn - 1) / bn);
+        tiles = ((a.M + 127) / 128) * ((a.NG + bn - 1) / bn);
         per_sm = bn <= 128 ? 2 : 1;
     } else if (tc) {
         const int bn = NG <= 64 ? 64 : 128;  // split-K launches never pick BN=256 unless tiles are plentiful
@@ -1155,7 +1249,21 @@ cudaError_t conv_wgrad(const ConvShape& g, int dtype, const void* x, const void*
     if (ws == nullptr || ws_bytes < static_cast<size_t>(per) * sizeof(float) * splits) return cudaErrorInvalidValue;
     a.out = ws;
     cudaError_t e;
-    if (tc) e = tma_ok(a, WGRAD) ? launch_tma_pick<WGRAD>(a, splits, st) : launch_tc_pick<WGRAD>(a, splits, st);
+    if (tc && tma_ok(a, WGRAD)) {
+        ConvArgs at = a;
+        std::swap(at.M, at.NG);  // partials [split][(r,s,c)][k]
+        e = launch_tma_pick<WGRAD>(at, splits, st);
+        if (e != cudaSuccess) return e;
+        const dim3 grid((at.M + 31) / 32, (at.NG + 31) / 32);
+        if (dtype == kF16)
+            wgrad_reduce_t_kernel<__half><<<grid, 256, 0, st>>>(static_cast<float*>(ws), splits, at.M, at.NG,
+                                                               static_cast<__half*>(dw));
+        else
+            wgrad_reduce_t_kernel<float><<<grid, 256, 0, st>>>(static_cast<float*>(ws), splits, at.M, at.NG,
+                                                              static_cast<float*>(dw));
+        return cudaGetLastError();
+    }
+    if (tc) e = launch_tc_pick<WGRAD>(a, splits, st);
     else e = dtype == kF16 ? launch_simt<__half, WGRAD>(a, splits, st) : launch_simt<float, WGRAD>(a, splits, st);
     if (e != cudaSuccess) return e;
     const int blocks = static_cast<int>(std::min<int64_t>((per + 255) / 256, 8 * kNumSMs));
