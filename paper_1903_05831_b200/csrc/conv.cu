@@ -491,6 +491,129 @@ __global__ void __launch_bounds__(288, (BN <= 128) ? 2 : 1)
     }
 }
 
+// Epilogue v2 (all-TMA kernel): warp w drains TMEM lane quadrant q = w & 3
+// (tile rows 32q..32q+31) over columns [c_lo, c_lo + NCOL), SC columns per
+// step: tcgen05.ld -> XOR-swizzled smem staging (row = lane, SC/4 slots of
+// 16 B) -> coalesced 16-byte stores (SC/8 lanes per row).  The dgrad residual
+// addend of step j+1 is loaded while step j is stored, so its global latency
+// hides behind the TMEM drain instead of being exposed at every step.
+template <int SC>
+SDB_DEV void tmem_ld_cols(uint32_t taddr, uint32_t (&v)[SC]);
+template <>
+SDB_DEV void tmem_ld_cols<16>(uint32_t taddr, uint32_t (&v)[16]) { tmem_ld16(taddr, v); }
+template <>
+SDB_DEV void tmem_ld_cols<32>(uint32_t taddr, uint32_t (&v)[32]) { tmem_ld32(taddr, v); }
+
+template <int MODE, int NCOL, int SC>
+SDB_DEV void epilogue_tile_v2(const ConvArgs& a, int split, int m0, int n0, int nk, uint32_t tacc, int q, int lane,
+                              int c_lo, float* stg, uint64_t* tempty_acc) {
+    constexpr int LPR = SC / 8;        // lanes per row in the store phase
+    constexpr int NK = LPR;            // store rows per lane = 32 / (32 / LPR)
+    constexpr int SLOTS = SC / 4;      // 16-byte slots per staged row
+    int64_t rowp[NK];
+#pragma unroll
+    for (int k = 0; k < NK; ++k) {
+        const int r = (k * 32 + lane) / LPR;
+        const int grow = m0 + q * 32 + r;
+        int64_t o = -1;
+        if (grow < a.M) {
+            if (MODE == FPROP) {
+                o = static_cast<int64_t>(grow) * a.NG;
+            } else if (MODE == DGRAD) {
+                const int HpWp = a.Hp * a.Wp;
+                const int n = grow / HpWp, rem = grow - n * HpWp, i2 = rem / a.Wp, j2 = rem - i2 * a.Wp;
+                o = ((static_cast<int64_t>(n) * a.H + a.ph + a.stride * i2) * a.W + a.pw + a.stride * j2) * a.C;
+            } else {
+                o = (static_cast<int64_t>(split) * a.M + grow) * a.NG;
+            }
+        }
+        rowp[k] = o;
+    }
+    const int lim = MODE == DGRAD ? a.C : a.NG;
+    const bool vec = MODE == WGRAD ? (lim & 3) == 0 : (lim & 7) == 0;
+    const bool add = MODE == DGRAD && a.accumulate;
+    const int c8 = lane % LPR;
+    uint4 addv[NK], addn[NK];
+    auto load_add = [&](uint4 (&dst)[NK], int cb) {
+        const int col = n0 + c_lo + cb + c8 * 8;
+#pragma unroll
+        for (int k = 0; k < NK; ++k) {
+            dst[k] = make_uint4(0, 0, 0, 0);
+            if (rowp[k] >= 0 && col + 8 <= lim && vec)
+                dst[k] = *reinterpret_cast<const uint4*>(static_cast<const __half*>(a.addend) + rowp[k] + col);
+        }
+    };
+    if (add) load_add(addv, 0);
+#pragma unroll 1
+    for (int cb = 0; cb < NCOL; cb += SC) {
+        if (add && cb + SC < NCOL) load_add(addn, cb + SC);
+        uint32_t v[SC];
+        tmem_ld_cols<SC>(tacc + (static_cast<uint32_t>(q * 32) << 16) + c_lo + cb, v);
+        if (cb + SC >= NCOL) {
+            // this warp's part of the accumulator is in registers: release it
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tempty_acc);
+        }
+        if (nk == 0) {
+#pragma unroll
+            for (int j = 0; j < SC; ++j) v[j] = 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < SLOTS; ++j) {
+            const int slot = j ^ (lane & (SLOTS - 1));
+            *reinterpret_cast<float4*>(stg + lane * SC + slot * 4) =
+                make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]), __uint_as_float(v[4 * j + 2]),
+                            __uint_as_float(v[4 * j + 3]));
+        }
+        __syncwarp();
+        const int col = n0 + c_lo + cb + c8 * 8;
+#pragma unroll
+        for (int k = 0; k < NK; ++k) {
+            const int r = (k * 32 + lane) / LPR;
+            const int sw = r & (SLOTS - 1);
+            const float4 f0 = *reinterpret_cast<const float4*>(stg + r * SC + (((2 * c8) ^ sw) * 4));
+            const float4 f1 = *reinterpret_cast<const float4*>(stg + r * SC + (((2 * c8 + 1) ^ sw) * 4));
+            if (rowp[k] < 0 || col >= lim) continue;
+            float f[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
+            if (MODE == WGRAD) {
+                float* o = static_cast<float*>(a.out) + rowp[k] + col;
+                if (col + 8 <= lim && vec) {
+                    *reinterpret_cast<float4*>(o) = f0;
+                    *reinterpret_cast<float4*>(o + 4) = f1;
+                } else {
+                    for (int e = 0; e < 8 && col + e < lim; ++e) o[e] = f[e];
+                }
+            } else {
+                __half* o = static_cast<__half*>(a.out) + rowp[k] + col;
+                if (col + 8 <= lim && vec) {
+                    if (add) {
+                        const __half* oh = reinterpret_cast<const __half*>(&addv[k]);
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) f[e] += __half2float(oh[e]);
+                    }
+                    uint4 pk;
+                    __half2* p2 = reinterpret_cast<__half2*>(&pk);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) p2[e] = __floats2half2_rn(f[2 * e], f[2 * e + 1]);
+                    *reinterpret_cast<uint4*>(o) = pk;
+                } else {
+                    for (int e = 0; e < 8 && col + e < lim; ++e) {
+                        float x = f[e];
+                        if (add) x += __half2float(static_cast<const __half*>(a.addend)[rowp[k] + col + e]);
+                        o[e] = __float2half_rn(x);
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        if (add) {
+#pragma unroll
+            for (int k = 0; k < NK; ++k) addv[k] = addn[k];
+        }
+    }
+}
+
 // ============================================================ all-TMA tcgen05 kernel
 // Both operands arrive by TMA, the activation side through the im2col mode of
 // cp.async.bulk.tensor (the hardware walks the output-pixel traversal of the
@@ -523,19 +646,23 @@ SDB_DEV void tma_im2col_4d(uint32_t dst, const void* map, uint64_t* bar, int c, 
         : "memory");
 }
 
+// BN = 256: 8 epilogue warps (two per TMEM lane quadrant, 128 columns each,
+// 32-column steps); BN <= 128: 4 warps, 16-column steps (two CTAs per SM).
 template <int MODE, int BN, int ST>
 struct TmaCfg {
     static constexpr int kABytes = kBM * kBK * 2;
     static constexpr int kBBytes = BN * kBK * 2;
     static constexpr int kStage = kABytes + kBBytes;
-    static constexpr int kStaging = 4 * 32 * 16 * 4;
+    static constexpr int kEpiWarps = BN == 256 ? 8 : 4;
+    static constexpr int kSC = BN == 256 ? 32 : 16;
+    static constexpr int kStaging = kEpiWarps * 32 * kSC * 4;
     static constexpr int kSmem = ST * kStage + kStaging + 1024 + 256;
-    static constexpr int kThreads = 192;
+    static constexpr int kThreads = 64 + 32 * kEpiWarps;
     static constexpr int kPerSM = BN <= 128 ? 2 : 1;
 };
 
 template <int MODE, int BN, int ST>
-__global__ void __launch_bounds__(192, (BN <= 128) ? 2 : 1)
+__global__ void __launch_bounds__(TmaCfg<MODE, BN, ST>::kThreads, (BN <= 128) ? 2 : 1)
     conv_tma_kernel(ConvArgs a, int tiles_m, int tiles_n, int n_tiles, const __grid_constant__ TmaPair tm) {
     using Cfg = TmaCfg<MODE, BN, ST>;
     extern __shared__ uint8_t smem_raw[];
@@ -560,7 +687,7 @@ __global__ void __launch_bounds__(192, (BN <= 128) ? 2 : 1)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
-            mbar_init(&tempty[i], 4);
+            mbar_init(&tempty[i], Cfg::kEpiWarps);
         }
         mbar_fence_init();
     }
@@ -730,8 +857,11 @@ __global__ void __launch_bounds__(192, (BN <= 128) ? 2 : 1)
         }
         __syncwarp();
     } else {
-        // ------------------------------------------------ epilogue warps 2..5
-        float* stg = staging + (warp - 2) * 32 * 16;
+        // ------------------------------------------------ epilogue warps 2..
+        constexpr int kNCol = BN * 4 / Cfg::kEpiWarps;  // columns per warp
+        const int ew = warp - 2;
+        float* stg = staging + ew * 32 * Cfg::kSC;
+        const int c_lo = (ew / 4) * kNCol;
         int lt = 0;
         for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++lt) {
             int m0, n0, kb0, nk;
@@ -739,8 +869,8 @@ __global__ void __launch_bounds__(192, (BN <= 128) ? 2 : 1)
             const int acc = lt & 1;
             mbar_wait(&tfull[acc], (lt >> 1) & 1);
             tc_fence_after();
-            epilogue_tile<MODE, BN>(a, t / (tiles_m * tiles_n), m0, n0, nk, tmem + acc * BN, warp & 3, lane, stg,
-                                    &tempty[acc]);
+            epilogue_tile_v2<MODE, kNCol, Cfg::kSC>(a, t / (tiles_m * tiles_n), m0, n0, nk, tmem + acc * BN, warp & 3,
+                                                   lane, c_lo, stg, &tempty[acc]);
         }
     }
     tc_fence_before();
