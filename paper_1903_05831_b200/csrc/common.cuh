@@ -157,6 +157,34 @@ __host__ __device__ constexpr uint32_t umma_idesc_f16(int M, int N, int a_mn_maj
            (static_cast<uint32_t>(N >> 3) << 17) | (static_cast<uint32_t>(M >> 4) << 24);
 }
 
+// ---------------------------------------------------------------- PDL
+// Programmatic dependent launch: a kernel launched with launch_pdl() may start
+// (prologue: barrier init, TMEM alloc, descriptor prefetch) while its
+// predecessor in the stream is still running; pdl_wait() blocks until the
+// predecessor has completed and its writes are visible.  Every kernel launched
+// through launch_pdl() must call pdl_wait() before touching global memory
+// written upstream.  pdl_trigger() lets the successor start launching.
+SDB_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+SDB_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+bool pdl_enabled();  // host: SDB_NO_PDL unset
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // ---------------------------------------------------------------- misc
 template <class T>
 SDB_DEV float to_f(T v);

@@ -34,6 +34,11 @@
 
 namespace sdb {
 
+bool pdl_enabled() {
+    static const bool e = std::getenv("SDB_NO_PDL") == nullptr;
+    return e;
+}
+
 enum ConvMode { FPROP = 0, DGRAD = 1, WGRAD = 2 };
 
 struct ConvArgs {
@@ -696,6 +701,9 @@ __global__ void __launch_bounds__(TmaCfg<MODE, BN, ST>::kThreads, (BN <= 128) ? 
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    // everything above overlapped the previous kernel's tail (PDL)
+    pdl_wait();
+    pdl_trigger();
 
     auto tile_coords = [&](int t, int& m0, int& n0, int& kb0, int& nk) {
         const int tm_ = t % tiles_m;
@@ -999,10 +1007,20 @@ __global__ void __launch_bounds__(256) conv_simt_kernel(ConvArgs a) {
 // deterministic split-K reduction: dw[i] = sum_s ws[s][i] (fixed order), cast
 template <class T>
 __global__ void wgrad_reduce_kernel(const float* __restrict__ ws, int splits, int64_t n, T* __restrict__ dw) {
+    pdl_wait();
+    pdl_trigger();
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         float s = 0.f;
-        for (int k = 0; k < splits; ++k) s += ws[k * n + i];
+        int k = 0;
+        for (; k + 4 <= splits; k += 4) {
+            const float a0 = ws[k * n + i], a1 = ws[(k + 1) * n + i], a2 = ws[(k + 2) * n + i], a3 = ws[(k + 3) * n + i];
+            s += a0;
+            s += a1;
+            s += a2;
+            s += a3;
+        }
+        for (; k < splits; ++k) s += ws[k * n + i];
         dw[i] = from_f<T>(s);
     }
 }
@@ -1013,16 +1031,40 @@ template <class T>
 __global__ void wgrad_reduce_t_kernel(const float* __restrict__ ws, int splits, int n_rows, int n_cols,
                                       T* __restrict__ dw) {
     __shared__ float tile[32][33];
+    pdl_wait();
+    pdl_trigger();
     const int j0 = blockIdx.x * 32, i0 = blockIdx.y * 32;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
     const int64_t per = static_cast<int64_t>(n_rows) * n_cols;
-    for (int jj = ty; jj < 32; jj += 8) {
-        const int j = j0 + jj, i = i0 + tx;
-        float acc = 0.f;
-        if (j < n_rows && i < n_cols)
-            for (int k = 0; k < splits; ++k) acc += ws[k * per + static_cast<int64_t>(j) * n_cols + i];
-        tile[jj][tx] = acc;
+    // 4 rows per thread, the split loop unrolled by 4: 16 independent loads in
+    // flight per thread (a dependent load chain per split was latency-bound)
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    const int i = i0 + tx;
+    bool ok[4];
+    int64_t off[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int j = j0 + ty + 8 * u;
+        ok[u] = j < n_rows && i < n_cols;
+        off[u] = ok[u] ? static_cast<int64_t>(j) * n_cols + i : 0;
     }
+    int k = 0;
+    for (; k + 4 <= splits; k += 4) {
+        float v[4][4];
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[kk][u] = ok[u] ? ws[(k + kk) * per + off[u]] : 0.f;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) acc[u] += v[kk][u];
+    }
+    for (; k < splits; ++k)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc[u] += ok[u] ? ws[k * per + off[u]] : 0.f;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) tile[ty + 8 * u][tx] = acc[u];
     __syncthreads();
     for (int ii = ty; ii < 32; ii += 8) {
         const int i = i0 + ii, j = j0 + tx;
@@ -1166,8 +1208,8 @@ static cudaError_t launch_tma(ConvArgs a, int splits, cudaStream_t st) {
         ok = ok && make_tmap(&tm.b, a.w, 2, dims, strides, box);
     }
     if (!ok) return cudaErrorInvalidValue;
-    conv_tma_kernel<MODE, BN, ST><<<grid, Cfg::kThreads, Cfg::kSmem, st>>>(a, tiles_m, tiles_n, n_tiles, tm);
-    return cudaGetLastError();
+    return launch_pdl(conv_tma_kernel<MODE, BN, ST>, dim3(grid), dim3(Cfg::kThreads), Cfg::kSmem, st, a, tiles_m,
+                      tiles_n, n_tiles, tm);
 }
 
 // tile width: 256 when the GEMM N is wide enough (one CTA per SM, 2 x 256 TMEM
@@ -1386,20 +1428,20 @@ cudaError_t conv_wgrad(const ConvShape& g, int dtype, const void* x, const void*
         if (e != cudaSuccess) return e;
         const dim3 grid((at.M + 31) / 32, (at.NG + 31) / 32);
         if (dtype == kF16)
-            wgrad_reduce_t_kernel<__half><<<grid, 256, 0, st>>>(static_cast<float*>(ws), splits, at.M, at.NG,
-                                                               static_cast<__half*>(dw));
-        else
-            wgrad_reduce_t_kernel<float><<<grid, 256, 0, st>>>(static_cast<float*>(ws), splits, at.M, at.NG,
-                                                              static_cast<float*>(dw));
-        return cudaGetLastError();
+            return launch_pdl(wgrad_reduce_t_kernel<__half>, grid, dim3(256), 0, st, static_cast<const float*>(ws),
+                              splits, at.M, at.NG, static_cast<__half*>(dw));
+        return launch_pdl(wgrad_reduce_t_kernel<float>, grid, dim3(256), 0, st, static_cast<const float*>(ws), splits,
+                          at.M, at.NG, static_cast<float*>(dw));
     }
     if (tc) e = launch_tc_pick<WGRAD>(a, splits, st);
     else e = dtype == kF16 ? launch_simt<__half, WGRAD>(a, splits, st) : launch_simt<float, WGRAD>(a, splits, st);
     if (e != cudaSuccess) return e;
     const int blocks = static_cast<int>(std::min<int64_t>((per + 255) / 256, 8 * kNumSMs));
-    if (dtype == kF16) wgrad_reduce_kernel<__half><<<blocks, 256, 0, st>>>(static_cast<float*>(ws), splits, per, static_cast<__half*>(dw));
-    else wgrad_reduce_kernel<float><<<blocks, 256, 0, st>>>(static_cast<float*>(ws), splits, per, static_cast<float*>(dw));
-    return cudaGetLastError();
+    if (dtype == kF16)
+        return launch_pdl(wgrad_reduce_kernel<__half>, dim3(blocks), dim3(256), 0, st, static_cast<const float*>(ws),
+                          splits, per, static_cast<__half*>(dw));
+    return launch_pdl(wgrad_reduce_kernel<float>, dim3(blocks), dim3(256), 0, st, static_cast<const float*>(ws), splits,
+                      per, static_cast<float*>(dw));
 }
 
 }  // namespace sdb

@@ -142,6 +142,8 @@ __global__ void __launch_bounds__(kStatThreads, 2) stats_kernel(StatArgs p) {
         mbar_fence_init();
     }
     __syncthreads();
+    pdl_wait();
+    pdl_trigger();
     const uint32_t sbase = smem_u32(sm);
     const int tpr = C / 8;
     const int rpi = kThreads / tpr;
@@ -260,6 +262,8 @@ __global__ void __launch_bounds__(1024) finalize_kernel(const double* __restrict
                                                         int64_t count, float eps, int mode, float* mean, float* invstd,
                                                         float* dgamma, float* dbeta, float* coef) {
     __shared__ double rs[32][33], rq[32][33];
+    pdl_wait();
+    pdl_trigger();
     const int cx = threadIdx.x & 31, ry = threadIdx.x >> 5;
     const int c = blockIdx.x * 32 + cx;
     double S = 0.0, Q = 0.0;
@@ -362,6 +366,8 @@ __global__ void __launch_bounds__(kStatThreads, 2) apply_kernel(ApplyArgs p, int
         mbar_fence_init();
     }
     __syncthreads();
+    pdl_wait();
+    pdl_trigger();
     if (warp == kThreads / 32) {
         if (lane == 0)
             stream_tiles<T, NIN, ST>(smem_u32(sm), full, empty, p.a, p.dy, p.y, r_begin, r_end, ntiles, TR, C);
@@ -470,8 +476,7 @@ cudaError_t run_stats(const StatArgs& a0, const Plan& pl, cudaStream_t st) {
     }
     StatArgs a = a0;
     a.rows_per_block = pl.rpb;
-    stats_kernel<T, KIND, NIN><<<pl.nblocks, kStatThreads, StatPipe<NIN>::kSmem, st>>>(a);
-    return cudaGetLastError();
+    return launch_pdl(stats_kernel<T, KIND, NIN>, dim3(pl.nblocks), dim3(kStatThreads), StatPipe<NIN>::kSmem, st, a);
 }
 
 template <class T, int KIND, int NIN>
@@ -482,14 +487,14 @@ cudaError_t run_apply(const ApplyArgs& aa, int64_t rows, const Plan& pl, cudaStr
                              StatPipe<NIN>::kSmem);
         configured = true;
     }
-    apply_kernel<T, KIND, NIN><<<pl.nblocks, kStatThreads, StatPipe<NIN>::kSmem, st>>>(aa, rows, pl.rpb);
-    return cudaGetLastError();
+    return launch_pdl(apply_kernel<T, KIND, NIN>, dim3(pl.nblocks), dim3(kStatThreads), StatPipe<NIN>::kSmem, st, aa,
+                      rows, pl.rpb);
 }
 
 void finalize(const double* partial, const Plan& pl, int C, int64_t rows, float eps, int mode, float* mean,
               float* invstd, float* dgamma, float* dbeta, float* coef, cudaStream_t st) {
-    finalize_kernel<<<(C + 31) / 32, 1024, 0, st>>>(partial, pl.nblocks, C, rows, eps, mode, mean, invstd, dgamma,
-                                                      dbeta, coef);
+    launch_pdl(finalize_kernel, dim3((C + 31) / 32), dim3(1024), 0, st, partial, pl.nblocks, C, rows, eps, mode, mean,
+               invstd, dgamma, dbeta, coef);
 }
 
 }  // namespace
