@@ -587,9 +587,9 @@ void run_step(sdb_det* d) {
                      d->a_targets, 1.0 / 9.0, static_cast<double>(cf.rpn_batch) * cf.batch, d->d_rpn_deltas, la,
                      d->ws, st));
     la.slot = 2;
-    CK(softmax_ce(d->dt, d->cls_logits.p, d->R, d->ncls, d->ncls_pad, d->roi_labels, g0, la, nullptr, st));
+    CK(softmax_ce(d->dt, d->cls_logits.p, d->R, d->ncls, d->ncls_pad, d->roi_labels, g0, la, d->ws, st));
     la.slot = 3;
-    CK(rcnn_smooth_l1(d->dt, d->bbox_pred.p, d->R, d->nbox_pad, d->roi_labels, d->roi_targets, 1.0, g1, la, nullptr,
+    CK(rcnn_smooth_l1(d->dt, d->bbox_pred.p, d->R, d->nbox_pad, d->roi_labels, d->roi_targets, 1.0, g1, la, d->ws,
                       st));
     }
 

@@ -134,6 +134,7 @@ constexpr int kTile = 8;        // 8x8 pixel tile
 constexpr int kSlab = 256;      // channels per CTA
 constexpr int kBwdThreads = 256;
 constexpr int kMaxP = 16;
+constexpr int kRB = 8;          // RoIs per barrier
 
 template <class T>
 __global__ void __launch_bounds__(kBwdThreads) roialign_bwd_kernel(const T* __restrict__ dy, int H, int W, int C,
@@ -142,16 +143,19 @@ __global__ void __launch_bounds__(kBwdThreads) roialign_bwd_kernel(const T* __re
                                                                    T* __restrict__ dfeat) {
     // dY holds every `step`-th bin of the P x P grid (Po x Po of them)
     const int Po = (P + step - 1) / step;
-    __shared__ float WY[kMaxP][kTile];
-    __shared__ float WX[kMaxP][kTile];
-    __shared__ int rng[2][4][kTile];  // double-buffered [row lo, row hi, col lo, col hi] of nonzero bins
+    // RoIs are processed in batches of kRB: one barrier per batch.  Weights are
+    // double-buffered and the nonzero-bin ranges triple-buffered so a batch's
+    // setup never races with slower threads still accumulating the previous one.
+    __shared__ float WY[2][kRB][kMaxP][kTile];
+    __shared__ float WX[2][kRB][kMaxP][kTile];
+    __shared__ int rng[3][kRB][4][kTile];  // [row lo, row hi, col lo, col hi] of nonzero bins
     __shared__ int list[1024];
     __shared__ int sh[40];
-    if (threadIdx.x < 64) {
-        const int t = threadIdx.x & 31;
-        rng[threadIdx.x >> 5][t >> 3][t & 7] = ((t >> 3) & 1) ? -1 : Po;
+    for (int t = threadIdx.x; t < 3 * kRB * 4 * kTile; t += kBwdThreads) {
+        const int k4 = (t / kTile) & 3;
+        (&rng[0][0][0][0])[t] = (k4 & 1) ? -1 : Po;
     }
-    int it_count = 0;
+    int batch = 0;
     const int n = blockIdx.z;
     const int tiles_x = (W + kTile - 1) / kTile;
     const int ty = blockIdx.x / tiles_x, tx = blockIdx.x % tiles_x;
@@ -206,19 +210,21 @@ __global__ void __launch_bounds__(kBwdThreads) roialign_bwd_kernel(const T* __re
             if (mine[q]) list[pos++] = base + threadIdx.x * 4 + q;
         __syncthreads();
 
-        for (int li = 0; li < total; ++li, ++it_count) {
-            const int r = list[li];
-            const int buf = it_count & 1;
-            const Geom g = roi_geom(rois + static_cast<int64_t>(r) * 5, P, scale);
-            // reset the other range buffer (last read two RoIs ago, before a barrier)
-            if (threadIdx.x < 32) {
-                const int t = threadIdx.x;
-                rng[buf ^ 1][t >> 3][t & 7] = ((t >> 3) & 1) ? -1 : Po;
+        for (int l0 = 0; l0 < total; l0 += kRB, ++batch) {
+            const int nb = min(kRB, total - l0);
+            const int wb = batch & 1, rb = batch % 3, rnext = (batch + 1) % 3;
+            // reset the range buffer of the next batch (last read three batches ago)
+            for (int t = threadIdx.x; t < kRB * 4 * kTile; t += kBwdThreads) {
+                const int k4 = (t / kTile) & 3;
+                (&rng[rnext][0][0][0])[t] = (k4 & 1) ? -1 : Po;
             }
-            // separable weights for this tile
-            for (int t = threadIdx.x; t < 2 * Po * kTile; t += kBwdThreads) {
-                const bool isx = t >= Po * kTile;
-                const int tt = isx ? t - Po * kTile : t;
+            // separable weights of the batch's RoIs for this tile
+            const int per = 2 * Po * kTile;
+            for (int t = threadIdx.x; t < nb * per; t += kBwdThreads) {
+                const int j = t / per, tt0 = t - j * per;
+                const Geom g = roi_geom(rois + static_cast<int64_t>(list[l0 + j]) * 5, P, scale);
+                const bool isx = tt0 >= Po * kTile;
+                const int tt = isx ? tt0 - Po * kTile : tt0;
                 const int pb = tt / kTile, lo = tt % kTile;
                 const int pix = (isx ? x0 : y0) + lo;
                 const int lim = isx ? W : H;
@@ -234,39 +240,41 @@ __global__ void __launch_bounds__(kBwdThreads) roialign_bwd_kernel(const T* __re
                     if (lo_i == pix) wsum += h;
                     if (hi_i == pix) wsum += l;
                 }
-                if (isx) WX[pb][lo] = wsum;
-                else WY[pb][lo] = wsum;
+                if (isx) WX[wb][j][pb][lo] = wsum;
+                else WY[wb][j][pb][lo] = wsum;
                 if (wsum != 0.f) {
-                    atomicMin(&rng[buf][isx ? 2 : 0][lo], pb);
-                    atomicMax(&rng[buf][isx ? 3 : 1][lo], pb);
+                    atomicMin(&rng[rb][j][isx ? 2 : 0][lo], pb);
+                    atomicMax(&rng[rb][j][isx ? 3 : 1][lo], pb);
                 }
             }
             __syncthreads();
             if (c_ok) {
-                const T* d = dy + static_cast<int64_t>(r) * Po * Po * C + c;
+                for (int j = 0; j < nb; ++j) {
+                    const T* d = dy + static_cast<int64_t>(list[l0 + j]) * Po * Po * C + c;
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    const int p = pix0 + 8 * i;
-                    const int ly = p >> 3, lx = p & 7;
-                    if (y0 + ly >= H || x0 + lx >= W) continue;
-                    const int phe = rng[buf][1][ly], pwb = rng[buf][2][lx], pwe = rng[buf][3][lx];
-                    for (int ph = rng[buf][0][ly]; ph <= phe; ++ph) {
-                        const float wy = WY[ph][ly];
-                        if (wy == 0.f) continue;
-                        for (int pw = pwb; pw <= pwe; ++pw) {
-                            const float wx = WX[pw][lx];
-                            if (wx == 0.f) continue;
-                            const float wgt = wy * wx * inv_count;
-                            float v[8];
-                            ld8<T>(d + (static_cast<int64_t>(ph) * Po + pw) * C, v);
+                    for (int i = 0; i < 8; ++i) {
+                        const int p = pix0 + 8 * i;
+                        const int ly = p >> 3, lx = p & 7;
+                        if (y0 + ly >= H || x0 + lx >= W) continue;
+                        const int phe = rng[rb][j][1][ly], pwb = rng[rb][j][2][lx], pwe = rng[rb][j][3][lx];
+                        for (int ph = rng[rb][j][0][ly]; ph <= phe; ++ph) {
+                            const float wy = WY[wb][j][ph][ly];
+                            if (wy == 0.f) continue;
+                            for (int pw = pwb; pw <= pwe; ++pw) {
+                                const float wx = WX[wb][j][pw][lx];
+                                if (wx == 0.f) continue;
+                                const float wgt = wy * wx * inv_count;
+                                float v[8];
+                                ld8<T>(d + (static_cast<int64_t>(ph) * Po + pw) * C, v);
 #pragma unroll
-                            for (int j = 0; j < 8; ++j) acc[i][j] += wgt * v[j];
+                                for (int jj = 0; jj < 8; ++jj) acc[i][jj] += wgt * v[jj];
+                            }
                         }
                     }
                 }
             }
-            __syncthreads();
         }
+        __syncthreads();  // `list` is rewritten by the next compaction round
     }
     if (!c_ok) return;
 #pragma unroll
@@ -595,6 +603,103 @@ SDB_DEV void sl1(double d, double beta, double& l, double& g) {
     }
 }
 
+// Multi-CTA variants (the single-CTA kernels above took ~100 us each at
+// R = 1024): every CTA recounts the valid rows (R labels, a few KB), handles 8
+// rows (one warp per row for CE) and writes a per-row / per-CTA fp64 loss; a
+// one-warp kernel then sums them in a fixed order (deterministic).
+constexpr int kRowsPerCta = 8;
+
+template <class T>
+__global__ void __launch_bounds__(256) softmax_ce_mc_kernel(const T* __restrict__ logits, int R, int ncls, int ld,
+                                                            const int32_t* __restrict__ labels,
+                                                            T* __restrict__ dlogits, const double* scale,
+                                                            double* __restrict__ rowloss) {
+    __shared__ double sh[32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int cnt = 0;
+    for (int r = threadIdx.x; r < R; r += blockDim.x) cnt += labels[r] >= 0;
+    const double B = block_sum_d(static_cast<double>(cnt), sh);
+    if (blockIdx.x == 0 && threadIdx.x == 0) rowloss[R] = B;
+    const double gs = scale ? *scale : 1.0;
+    const float g = B > 0 ? static_cast<float>(1.0 * gs / B) : 0.f;
+    const int r = blockIdx.x * kRowsPerCta + wid;
+    if (r >= R) return;
+    const int y = labels[r];
+    const T* x = logits + static_cast<int64_t>(r) * ld;
+    T* dx = dlogits + static_cast<int64_t>(r) * ld;
+    if (y < 0) {
+        for (int j = lane; j < ld; j += 32) dx[j] = from_f<T>(0.f);
+        if (lane == 0) rowloss[r] = 0.0;
+        return;
+    }
+    double mx = -INFINITY;
+    for (int j = lane; j < ncls; j += 32) mx = fmax(mx, static_cast<double>(ldv(x, j)));
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    double z = 0.0;
+    for (int j = lane; j < ncls; j += 32) z += exp(static_cast<double>(ldv(x, j)) - mx);
+    z = warp_sum(z);
+    float py = 0.f;
+    for (int j = lane; j < ld; j += 32) {
+        if (j < ncls) {
+            const float pj = static_cast<float>(exp(static_cast<double>(ldv(x, j)) - mx) / z);
+            if (j == y) py = pj;
+            dx[j] = from_f<T>((pj - (j == y ? 1.0f : 0.0f)) * g);
+        } else {
+            dx[j] = from_f<T>(0.f);
+        }
+    }
+    py = __shfl_sync(0xffffffffu, py, y & 31);
+    if (lane == 0) rowloss[r] = -log(fmax(1e-30, static_cast<double>(py)));
+}
+
+template <class T>
+__global__ void __launch_bounds__(256) rcnn_sl1_mc_kernel(const T* __restrict__ pred, int R, int ld,
+                                                          const int32_t* __restrict__ labels,
+                                                          const float* __restrict__ targets, double beta,
+                                                          T* __restrict__ dp, const double* scale,
+                                                          double* __restrict__ partial) {
+    __shared__ double sh[32];
+    int cnt = 0;
+    for (int r = threadIdx.x; r < R; r += blockDim.x) cnt += labels[r] >= 0;
+    const double norm = block_sum_d(static_cast<double>(cnt), sh);
+    if (blockIdx.x == 0 && threadIdx.x == 0) partial[gridDim.x] = norm;
+    const double gs = (scale ? *scale : 1.0) / (norm > 0 ? norm : 1.0);
+    double acc = 0.0;
+    const int r0 = blockIdx.x * kRowsPerCta;
+    const int r1 = min(R, r0 + kRowsPerCta);
+    for (int64_t i = static_cast<int64_t>(r0) * ld + threadIdx.x; i < static_cast<int64_t>(r1) * ld; i += blockDim.x) {
+        const int r = static_cast<int>(i / ld), col = static_cast<int>(i % ld);
+        const int lab = labels[r];
+        float gout = 0.f;
+        if (lab > 0 && col >= 4 * lab && col < 4 * lab + 4) {
+            const double d = static_cast<double>(ldv(pred, i)) - static_cast<double>(targets[r * 4 + (col - 4 * lab)]);
+            double l, gg;
+            sl1(d, beta, l, gg);
+            acc += l;
+            gout = static_cast<float>(gg * gs);
+        }
+        dp[i] = from_f<T>(gout);
+    }
+    const double tot = block_sum_d(acc, sh);
+    if (threadIdx.x == 0) partial[blockIdx.x] = tot;
+}
+
+// loss = sum(v[0..n)) / v[n], fixed order: lane-strided partial sums, then an
+// in-order sum of the 32 lane totals by lane 0
+__global__ void ordered_mean_kernel(const double* __restrict__ v, int n, double* loss_out, int slot) {
+    __shared__ double t[32];
+    double a = 0.0;
+    for (int i = threadIdx.x; i < n; i += 32) a += v[i];
+    t[threadIdx.x] = a;
+    __syncwarp();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int i = 0; i < 32; ++i) s += t[i];
+        const double d = v[n];
+        loss_out[slot] = d > 0 ? s / d : 0.0;
+    }
+}
+
 template <class T>
 __global__ void __launch_bounds__(kLossBlockThreads) rpn_sl1_kernel(const T* __restrict__ deltas, int64_t n_loc, int A,
                                                                     int A_pad, const int8_t* __restrict__ labels,
@@ -818,7 +923,20 @@ cudaError_t add_inplace(int dtype, void* acc, const void* b, int64_t n, cudaStre
 size_t loss_workspace_bytes(int64_t) { return 3 * kLossBlocks * sizeof(double); }
 
 cudaError_t softmax_ce(int dtype, const void* logits, int R, int ncls, int ld, const int32_t* labels, void* dlogits,
-                       const LossArgs& la, void*, cudaStream_t st) {
+                       const LossArgs& la, void* ws, cudaStream_t st) {
+    if (ws && R > 0) {
+        // ws: R + 1 doubles (per-row losses, then the valid-row count)
+        double* rl = static_cast<double*>(ws);
+        const int g = (R + kRowsPerCta - 1) / kRowsPerCta;
+        if (dtype == kF16)
+            softmax_ce_mc_kernel<__half><<<g, 256, 0, st>>>(cp<__half>(logits), R, ncls, ld, labels,
+                                                            static_cast<__half*>(dlogits), la.scale, rl);
+        else
+            softmax_ce_mc_kernel<float><<<g, 256, 0, st>>>(cp<float>(logits), R, ncls, ld, labels,
+                                                           static_cast<float*>(dlogits), la.scale, rl);
+        ordered_mean_kernel<<<1, 32, 0, st>>>(rl, R, la.loss_out, la.slot);
+        return cudaGetLastError();
+    }
     if (dtype == kF16)
         softmax_ce_kernel<__half><<<1, kLossThreads, 0, st>>>(cp<__half>(logits), R, ncls, ld, labels,
                                                              static_cast<__half*>(dlogits), la.scale, la.loss_out,
@@ -861,7 +979,20 @@ cudaError_t rpn_smooth_l1(int dtype, const void* deltas, int64_t n_loc, int A, i
 }
 
 cudaError_t rcnn_smooth_l1(int dtype, const void* pred, int R, int ld, const int32_t* labels, const float* targets,
-                           double beta, void* dp, const LossArgs& la, void*, cudaStream_t st) {
+                           double beta, void* dp, const LossArgs& la, void* ws, cudaStream_t st) {
+    if (ws && R > 0) {
+        // ws: one fp64 partial per CTA, then the valid-row count
+        double* part = static_cast<double*>(ws);
+        const int g = (R + kRowsPerCta - 1) / kRowsPerCta;
+        if (dtype == kF16)
+            rcnn_sl1_mc_kernel<__half><<<g, 256, 0, st>>>(cp<__half>(pred), R, ld, labels, targets, beta,
+                                                          static_cast<__half*>(dp), la.scale, part);
+        else
+            rcnn_sl1_mc_kernel<float><<<g, 256, 0, st>>>(cp<float>(pred), R, ld, labels, targets, beta,
+                                                         static_cast<float*>(dp), la.scale, part);
+        ordered_mean_kernel<<<1, 32, 0, st>>>(part, g, la.loss_out, la.slot);
+        return cudaGetLastError();
+    }
     if (dtype == kF16)
         rcnn_sl1_kernel<__half><<<1, kLossThreads, 0, st>>>(cp<__half>(pred), R, ld, labels, targets, beta,
                                                            static_cast<__half*>(dp), la.scale, la.loss_out, la.slot);
