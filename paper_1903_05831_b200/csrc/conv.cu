@@ -705,11 +705,24 @@ __global__ void __launch_bounds__(TmaCfg<MODE, BN, ST>::kThreads, (BN <= 128) ? 
     pdl_wait();
     pdl_trigger();
 
+    // Rasterisation: fprop/dgrad stream a large activation operand against a
+    // small filter, so the N tiles of one M tile run on neighbouring CTAs at
+    // the same time (each activation block is read from HBM once, the filter
+    // stays in L2); m-fastest order re-read the activation tiles_n times
+    // (727 MB of DRAM reads for a 103 MB input, res5 shortcut).  wgrad streams
+    // both operands along K and keeps m-fastest order within a split.
     auto tile_coords = [&](int t, int& m0, int& n0, int& kb0, int& nk) {
-        const int tm_ = t % tiles_m;
-        const int rest = t / tiles_m;
-        const int tn = rest % tiles_n;
-        const int split = rest / tiles_n;
+        int tm_, tn, split;
+        if (MODE == WGRAD) {
+            tm_ = t % tiles_m;
+            const int rest = t / tiles_m;
+            tn = rest % tiles_n;
+            split = rest / tiles_n;
+        } else {
+            tn = t % tiles_n;
+            tm_ = t / tiles_n;
+            split = 0;
+        }
         m0 = tm_ * kBM;
         n0 = tn * BN;
         kb0 = MODE == WGRAD ? split * a.kb_per_split : 0;
