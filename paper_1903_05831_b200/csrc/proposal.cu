@@ -8,8 +8,9 @@
 // sampled RoIs) is BIT-EXACT against it given identical fp32 inputs.  This TU
 // is compiled with -fmad=false so no float/double FMA contraction occurs.
 //
-//   topk      one CTA per image: 64-bit radix select over the composite key
-//             (~orderable(score) << 32 | index) -> bitonic sort in smem
+//   topk      64 CTAs per image: 8 radix-select passes over the composite
+//             key (~orderable(score) << 32 | index) through global histograms,
+//             compaction, then a rank-by-counting sort (deterministic)
 //   decode    anchors + deltas -> clipped boxes, portable exp (bit-identical to
 //             orc_expf)
 //   nms mask  64x64 IoU tiles -> upper-triangular bitmask (fp64, -fmad=false)
@@ -69,6 +70,23 @@ SDB_DEV double iou_d(double ax1, double ay1, double ax2, double ay2, double bx1,
     const double ab = __dmul_rn(__dsub_rn(bx2, bx1), __dsub_rn(by2, by1));
     const double uni = __dsub_rn(__dadd_rn(aa, ab), inter);
     return uni > 0.0 ? __ddiv_rn(inter, uni) : 0.0;
+}
+// iou_d(...) > thr, decided without the fp64 division unless inter/uni lies
+// within 4e-15 (relative) of thr: outside that band the rounded quotient is
+// on the same side of thr as the exact one, so the result is identical.
+SDB_DEV bool iou_gt(double ax1, double ay1, double ax2, double ay2, double bx1, double by1, double bx2, double by2,
+                    double thr) {
+    const double ix = fmax(0.0, __dsub_rn(fmin(ax2, bx2), fmax(ax1, bx1)));
+    const double iy = fmax(0.0, __dsub_rn(fmin(ay2, by2), fmax(ay1, by1)));
+    const double inter = __dmul_rn(ix, iy);
+    const double aa = __dmul_rn(__dsub_rn(ax2, ax1), __dsub_rn(ay2, ay1));
+    const double ab = __dmul_rn(__dsub_rn(bx2, bx1), __dsub_rn(by2, by1));
+    const double uni = __dsub_rn(__dadd_rn(aa, ab), inter);
+    if (!(uni > 0.0)) return 0.0 > thr;
+    const double a = __dmul_rn(thr, uni);
+    if (inter > __dmul_rn(a, 1.0 + 4e-15)) return true;
+    if (inter < __dmul_rn(a, 1.0 - 4e-15)) return false;
+    return __ddiv_rn(inter, uni) > thr;
 }
 SDB_DEV double iou_f4(const float* a, const float* b) {
     return iou_d(a[0], a[1], a[2], a[3], b[0], b[1], b[2], b[3]);
@@ -232,7 +250,6 @@ __global__ void anchors_kernel(AnchorCfg a, float* __restrict__ out) {
 }
 
 // ---------------------------------------------------------------- top-k + decode
-constexpr int kTopkThreads = 1024;
 
 // logits: [img][loc][A_pad] (fp16 or fp32), valid anchors a < A; anchor index = loc*A + a
 struct TopkArgs {
@@ -253,54 +270,185 @@ SDB_DEV float load_val(const void* p, int dtype, int64_t i) {
     return dtype == kF16 ? __half2float(static_cast<const __half*>(p)[i]) : static_cast<const float*>(p)[i];
 }
 
-__global__ void __launch_bounds__(kTopkThreads) topk_decode_kernel(TopkArgs a) {
-    extern __shared__ uint64_t keys[];  // k_pow2
-    __shared__ int hist[256];
-    __shared__ int sh[64];
-    __shared__ int n_sel;
-    const int img = blockIdx.x;
-    const int n = a.n_loc * a.A;
-    auto keyfn = [&](int i, bool& f) -> uint64_t {
-        f = true;
-        const int loc = i / a.A, an = i - loc * a.A;
-        const float s = load_val(a.logits, a.dtype, (static_cast<int64_t>(img) * a.n_loc + loc) * a.A_pad + an);
-        return (static_cast<uint64_t>(desc_key(s)) << 32) | static_cast<uint32_t>(i);
-    };
-    int n_lt;
-    const uint64_t T = block_radix_select<kTopkThreads>(n, a.k, keyfn, hist, sh, &n_lt);
-    if (threadIdx.x == 0) n_sel = 0;
-    for (int i = threadIdx.x; i < a.k_pow2; i += kTopkThreads) keys[i] = ~0ull;
-    __syncthreads();
-    for (int i = threadIdx.x; i < n; i += kTopkThreads) {
-        bool f;
-        const uint64_t key = keyfn(i, f);
-        if (key <= T) {
-            const int slot = atomicAdd(&n_sel, 1);
-            if (slot < a.k_pow2) keys[slot] = key;
-        }
+// ---------------------------------------------------------------- multi-CTA top-k
+// The single-CTA radix select + bitonic sort above ran ~380 us per step on one
+// SM per image.  Here the same selection runs on kTopkG CTAs per image:
+//   pass p = 0..7 (one launch each): every CTA replays the digit choice of
+//     pass p-1 from the (complete) global histogram of that pass, then bins its
+//     share of the keys matching the selected prefix into a shared histogram
+//     and adds the non-zero bins to the global histogram of pass p;
+//   compact: every CTA recovers the threshold T and appends its keys <= T
+//     (exactly k of them, keys are unique) to a per-image list;
+//   rank + decode: each selected key's position = #(selected keys smaller),
+//     counted by 8 warps over 1/8 of the list each (4 keys per lane) -- a
+//     deterministic sort independent of the append order -- then decoded into
+//     its slot.  Same keys, same T, same order as the single-CTA path.
+constexpr int kTopkG = 64;        // CTAs per image for the histogram passes
+constexpr int kTopkPassT = 256;
+
+struct TopkState {
+    unsigned long long prefix;
+    int kk, below;
+};
+
+struct TopkMC {
+    TopkArgs a;
+    unsigned int* hist;   // [img][8][256]
+    TopkState* state;     // [img][8]
+    unsigned long long* sel;  // [img][k]
+    int* sel_count;       // [img]
+};
+
+SDB_DEV uint64_t topk_key(const TopkArgs& a, int img, int i) {
+    const int loc = i / a.A, an = i - loc * a.A;
+    const float s = load_val(a.logits, a.dtype, (static_cast<int64_t>(img) * a.n_loc + loc) * a.A_pad + an);
+    return (static_cast<uint64_t>(desc_key(s)) << 32) | static_cast<uint32_t>(i);
+}
+
+// digit choice of pass q from its complete histogram (warp 0; result in sh)
+SDB_DEV void topk_replay(const unsigned int* h, TopkState& st, int q, TopkState* out_sh) {
+    const int lane = threadIdx.x & 31;
+    // 8 bins per lane, inclusive scan over lanes
+    unsigned int c[8], tot = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        c[j] = h[lane * 8 + j];
+        tot += c[j];
     }
-    __syncthreads();
-    // bitonic sort ascending (keys are unique)
-    for (int size = 2; size <= a.k_pow2; size <<= 1) {
-        for (int stride = size >> 1; stride > 0; stride >>= 1) {
-            for (int t = threadIdx.x; t < a.k_pow2 / 2; t += kTopkThreads) {
-                const int lo = 2 * t - (t & (stride - 1));
-                const int hi = lo + stride;
-                const bool up = (lo & size) == 0;
-                const uint64_t x = keys[lo], y = keys[hi];
-                if ((x > y) == up) {
-                    keys[lo] = y;
-                    keys[hi] = x;
-                }
+    unsigned int incl = tot;
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const unsigned int excl = incl - tot;
+    // the digit d: first bin where the running count reaches kk
+    const unsigned int kk = static_cast<unsigned int>(st.kk);
+    int d = -1;
+    unsigned int acc = 0;
+    if (excl < kk && incl >= kk) {
+        unsigned int run = excl;
+        for (int j = 0; j < 8; ++j) {
+            if (run + c[j] >= kk) {
+                d = lane * 8 + j;
+                acc = run;
+                break;
             }
-            __syncthreads();
+            run += c[j];
         }
     }
-    // decode the sorted candidates (orc_decode with unit weights)
-    for (int r = threadIdx.x; r < a.k; r += kTopkThreads) {
-        const int i = static_cast<int>(keys[r] & 0xffffffffu);
-        const int loc = i / a.A, an = i - loc * a.A;
-        const float* an4 = a.anchors + static_cast<int64_t>(i) * 4;
+    const unsigned int ball = __ballot_sync(0xffffffffu, d >= 0);
+    const int src = __ffs(ball) - 1;
+    d = __shfl_sync(0xffffffffu, d, src);
+    acc = __shfl_sync(0xffffffffu, acc, src);
+    if (lane == 0) {
+        const int shift = 56 - 8 * q;
+        out_sh->prefix = st.prefix | (static_cast<unsigned long long>(d) << shift);
+        out_sh->kk = st.kk - static_cast<int>(acc);
+        out_sh->below = st.below + static_cast<int>(acc);
+    }
+}
+
+__global__ void __launch_bounds__(kTopkPassT) topk_pass_kernel(TopkMC m, int pass) {
+    __shared__ unsigned int hs[256];
+    __shared__ TopkState cur;
+    const int img = blockIdx.y;
+    const TopkArgs& a = m.a;
+    const int n = a.n_loc * a.A;
+    for (int b = threadIdx.x; b < 256; b += kTopkPassT) hs[b] = 0;
+    if (pass == 0) {
+        if (threadIdx.x == 0) {
+            cur.prefix = 0;
+            cur.kk = a.k;
+            cur.below = 0;
+        }
+    } else if (threadIdx.x < 32) {
+        TopkState st = m.state[img * 8 + pass - 1];
+        topk_replay(m.hist + (static_cast<int64_t>(img) * 8 + pass - 1) * 256, st, pass - 1, &cur);
+    }
+    __syncthreads();
+    if (blockIdx.x == 0 && threadIdx.x == 0) m.state[img * 8 + pass] = cur;
+    const int shift = 56 - 8 * pass;
+    const unsigned long long mask = pass == 0 ? 0ull : (~0ull << (64 - 8 * pass));
+    const unsigned long long prefix = cur.prefix;
+    const int per = (n + gridDim.x - 1) / gridDim.x;
+    const int i0 = blockIdx.x * per, i1 = min(n, i0 + per);
+    for (int i = i0 + threadIdx.x; i < i1; i += kTopkPassT) {
+        const uint64_t key = topk_key(a, img, i);
+        if ((key & mask) == prefix) atomicAdd(&hs[(key >> shift) & 255], 1u);
+    }
+    __syncthreads();
+    unsigned int* gh = m.hist + (static_cast<int64_t>(img) * 8 + pass) * 256;
+    for (int b = threadIdx.x; b < 256; b += kTopkPassT)
+        if (hs[b]) atomicAdd(&gh[b], hs[b]);
+}
+
+__global__ void __launch_bounds__(kTopkPassT) topk_compact_kernel(TopkMC m, int select_all) {
+    __shared__ TopkState fin;
+    const int img = blockIdx.y;
+    const TopkArgs& a = m.a;
+    const int n = a.n_loc * a.A;
+    if (select_all) {
+        if (threadIdx.x == 0) fin.prefix = ~0ull;
+    } else if (threadIdx.x < 32) {
+        TopkState st = m.state[img * 8 + 7];
+        topk_replay(m.hist + (static_cast<int64_t>(img) * 8 + 7) * 256, st, 7, &fin);
+    }
+    __syncthreads();
+    const unsigned long long T = fin.prefix;
+    const int per = (n + gridDim.x - 1) / gridDim.x;
+    const int i0 = blockIdx.x * per, i1 = min(n, i0 + per);
+    for (int i = i0 + threadIdx.x; i < i1; i += kTopkPassT) {
+        const uint64_t key = topk_key(a, img, i);
+        if (key <= T) {
+            const int slot = atomicAdd(&m.sel_count[img], 1);
+            if (slot < a.k) m.sel[static_cast<int64_t>(img) * a.k + slot] = key;
+        }
+    }
+}
+
+constexpr int kRankKeys = 128;   // keys per CTA (4 per lane)
+__global__ void __launch_bounds__(256) topk_rank_decode_kernel(TopkMC m) {
+    __shared__ int part[8][kRankKeys];
+    const int img = blockIdx.y;
+    const TopkArgs& a = m.a;
+    const int k = a.k;
+    const unsigned long long* S = m.sel + static_cast<int64_t>(img) * k;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int base = blockIdx.x * kRankKeys;
+    unsigned long long mine[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int i = base + u * 32 + lane;
+        mine[u] = i < k ? S[i] : ~0ull;
+    }
+    int cnt[4] = {0, 0, 0, 0};
+    const int per = (k + 7) / 8;
+    const int j0 = wid * per, j1 = min(k, j0 + per);
+    for (int jb = j0; jb < j1; jb += 32) {
+        const int j = jb + lane;
+        const unsigned long long kj = j < j1 ? S[j] : ~0ull;
+        const int nj = min(32, j1 - jb);
+        for (int t = 0; t < nj; ++t) {
+            const unsigned long long v = __shfl_sync(0xffffffffu, kj, t);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) cnt[u] += v < mine[u];
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) part[wid][u * 32 + lane] = cnt[u];
+    __syncthreads();
+    if (wid != 0) return;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int i = base + u * 32 + lane;
+        if (i >= k) continue;
+        int r = 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) r += part[w][u * 32 + lane];
+        // decode the candidate into slot r (orc_decode with unit weights)
+        const int ai = static_cast<int>(mine[u] & 0xffffffffu);
+        const int loc = ai / a.A, an = ai - loc * a.A;
+        const float* an4 = a.anchors + static_cast<int64_t>(ai) * 4;
         const int64_t dbase = (static_cast<int64_t>(img) * a.n_loc + loc) * 4 * a.A_pad + 4 * an;
         const float dx = load_val(a.deltas, a.dtype, dbase + 0), dy = load_val(a.deltas, a.dtype, dbase + 1);
         const float dw = fminf(load_val(a.deltas, a.dtype, dbase + 2), a.clip_dw);
@@ -309,13 +457,13 @@ __global__ void __launch_bounds__(kTopkThreads) topk_decode_kernel(TopkArgs a) {
         const float acx = __fadd_rn(an4[0], __fmul_rn(0.5f, aw)), acy = __fadd_rn(an4[1], __fmul_rn(0.5f, ah));
         const float pcx = __fadd_rn(__fmul_rn(dx, aw), acx), pcy = __fadd_rn(__fmul_rn(dy, ah), acy);
         const float pw = __fmul_rn(portable_expf(dw), aw), ph = __fmul_rn(portable_expf(dh), ah);
-        float* o = a.boxes + (static_cast<int64_t>(img) * a.k + r) * 4;
+        float* o = a.boxes + (static_cast<int64_t>(img) * k + r) * 4;
         o[0] = fminf(fmaxf(__fsub_rn(pcx, __fmul_rn(0.5f, pw)), 0.0f), a.img_w);
         o[1] = fminf(fmaxf(__fsub_rn(pcy, __fmul_rn(0.5f, ph)), 0.0f), a.img_h);
         o[2] = fminf(fmaxf(__fadd_rn(pcx, __fmul_rn(0.5f, pw)), 0.0f), a.img_w);
         o[3] = fminf(fmaxf(__fadd_rn(pcy, __fmul_rn(0.5f, ph)), 0.0f), a.img_h);
-        a.order[static_cast<int64_t>(img) * a.k + r] = i;
-        a.scores[static_cast<int64_t>(img) * a.k + r] =
+        a.order[static_cast<int64_t>(img) * k + r] = ai;
+        a.scores[static_cast<int64_t>(img) * k + r] =
             load_val(a.logits, a.dtype, (static_cast<int64_t>(img) * a.n_loc + loc) * a.A_pad + an);
     }
 }
@@ -345,7 +493,7 @@ __global__ void __launch_bounds__(64) nms_mask_kernel(const float* __restrict__ 
         if (j <= i) continue;
         // cheap exact reject: no overlap -> IoU is 0, never > thr (thr >= 0)
         if (cbx[jj][0] >= bi[2] || cbx[jj][2] <= bi[0] || cbx[jj][1] >= bi[3] || cbx[jj][3] <= bi[1]) continue;
-        if (iou_d(x1, y1, x2, y2, cbx[jj][0], cbx[jj][1], cbx[jj][2], cbx[jj][3]) > thr) bits |= 1ull << jj;
+        if (iou_gt(x1, y1, x2, y2, cbx[jj][0], cbx[jj][1], cbx[jj][2], cbx[jj][3], thr)) bits |= 1ull << jj;
     }
     mask[(static_cast<int64_t>(img) * k + i) * nwords + cb] = bits;
 }
@@ -696,7 +844,8 @@ static int next_pow2(int v) {
 size_t proposal_workspace_bytes(int n_img, int n_anchors, int pre_k) {
     const int k = std::min(pre_k, n_anchors);
     const int nwords = (k + 63) / 64;
-    return static_cast<size_t>(n_img) * k * (16 + 4 + 4) + static_cast<size_t>(n_img) * k * nwords * 8 + 1024;
+    return static_cast<size_t>(n_img) * k * (16 + 4 + 4) + static_cast<size_t>(n_img) * k * nwords * 8 + 1024 +
+           static_cast<size_t>(n_img) * (static_cast<size_t>(k) * 8 + 8 * 256 * 4 + 8 * sizeof(TopkState) + 16) + 1024;
 }
 
 cudaError_t rpn_proposals(const ProposalArgs& p, void* ws, cudaStream_t st) {
@@ -721,9 +870,27 @@ cudaError_t rpn_proposals(const ProposalArgs& p, void* ws, cudaStream_t st) {
     t.n_loc = p.n_loc; t.A = p.A; t.A_pad = p.A_pad; t.k = k; t.k_pow2 = kp2;
     t.img_h = p.img_h; t.img_w = p.img_w; t.clip_dw = p.clip_dw;
     t.boxes = boxes; t.order = order; t.scores = scores;
-    const size_t smem = static_cast<size_t>(kp2) * 8;
-    cudaFuncSetAttribute(topk_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384 * 8);
-    topk_decode_kernel<<<p.n_img, kTopkThreads, smem, st>>>(t);
+    // multi-CTA selection state after the NMS mask (all 256-byte aligned)
+    uint8_t* w2 = reinterpret_cast<uint8_t*>(mask) + static_cast<size_t>(p.n_img) * k * nwords * 8;
+    w2 = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(w2) + 255) & ~uintptr_t(255));
+    TopkMC m{};
+    m.a = t;
+    m.sel = reinterpret_cast<unsigned long long*>(w2);
+    w2 += static_cast<size_t>(p.n_img) * k * 8;
+    unsigned int* zero_begin = reinterpret_cast<unsigned int*>(w2);
+    m.hist = reinterpret_cast<unsigned int*>(w2);
+    w2 += static_cast<size_t>(p.n_img) * 8 * 256 * 4;
+    m.sel_count = reinterpret_cast<int*>(w2);
+    w2 += static_cast<size_t>(p.n_img) * 4;
+    const size_t zero_bytes = static_cast<size_t>(w2 - reinterpret_cast<uint8_t*>(zero_begin));
+    w2 = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(w2) + 255) & ~uintptr_t(255));
+    m.state = reinterpret_cast<TopkState*>(w2);
+    cudaMemsetAsync(zero_begin, 0, zero_bytes, st);
+    const bool select_all = k >= nA;
+    if (!select_all)
+        for (int pass = 0; pass < 8; ++pass) topk_pass_kernel<<<dim3(kTopkG, p.n_img), kTopkPassT, 0, st>>>(m, pass);
+    topk_compact_kernel<<<dim3(kTopkG, p.n_img), kTopkPassT, 0, st>>>(m, select_all ? 1 : 0);
+    topk_rank_decode_kernel<<<dim3((k + kRankKeys - 1) / kRankKeys, p.n_img), 256, 0, st>>>(m);
     if (p.topk_order_out) {
         cudaMemcpyAsync(p.topk_order_out, order, static_cast<size_t>(p.n_img) * k * 4, cudaMemcpyDeviceToDevice, st);
     }
