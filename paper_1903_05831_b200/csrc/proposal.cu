@@ -593,6 +593,163 @@ __global__ void __launch_bounds__(kScanThreads) nms_scan_kernel(const float* __r
     if (threadIdx.x == 0) count[img] = nk;
 }
 
+// Pipelined keep scan.  The greedy decision for 64-box chunk c needs only
+// removed[c]; it reads the chunk's diagonal words diag[c] (its rows' word c)
+// and, for the kept rows, their word c+1 (sdiag[c]) -- both preloaded into
+// shared memory for every chunk, so the decision warp never waits on global
+// memory.  The kept rows' words >= c+2 are ORed into removed[] by two worker
+// groups (even / odd chunks) that run one to two chunks behind: the decision
+// for chunk c only needs the bulk OR of chunks <= c-2, so the L2 round trips
+// of the bulk OR overlap the following decisions instead of serialising them.
+// Same greedy order, same keep list as nms_scan_kernel (deterministic:
+// atomicOr is order-independent).
+constexpr int kScan2Warps = 9;   // warp 0: decisions; warps 1-4: even chunks; 5-8: odd chunks
+constexpr int kScan2Threads = 32 * kScan2Warps;
+constexpr int kScan2MaxWords = 192;
+
+__global__ void __launch_bounds__(kScan2Threads) nms_scan2_kernel(const float* __restrict__ boxes,
+                                                                  const uint64_t* __restrict__ mask,
+                                                                  const float* __restrict__ scores, int k, int nwords,
+                                                                  int post_k, float* __restrict__ rois,
+                                                                  float* __restrict__ roi_scores,
+                                                                  int32_t* __restrict__ keep_pos,
+                                                                  int32_t* __restrict__ count) {
+    extern __shared__ uint64_t sm2[];
+    uint64_t* diag = sm2;                              // [nwords][64]
+    uint64_t* sdiag = diag + nwords * 64;              // [nwords][64]
+    uint64_t* removed = sdiag + nwords * 64;           // [nwords]
+    __shared__ int rows[2][64];
+    __shared__ int nrows[2];
+    __shared__ uint64_t rows_ready[2], or_done[2];
+    __shared__ int kept_total;
+    const int img = blockIdx.x;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint64_t* M = mask + static_cast<int64_t>(img) * k * nwords;
+    // preload: diagonal and super-diagonal words of every chunk
+    // (8 independent loads in flight per thread)
+    for (int e0 = tid; e0 < nwords * 64; e0 += 4 * kScan2Threads) {
+        uint64_t dv[4], sv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int e = e0 + u * kScan2Threads;
+            const int c = e >> 6, r = c * 64 + (e & 63);
+            dv[u] = sv[u] = 0;
+            if (e < nwords * 64 && r < k) {
+                dv[u] = __ldg(M + static_cast<int64_t>(r) * nwords + c);
+                if (c + 1 < nwords) sv[u] = __ldg(M + static_cast<int64_t>(r) * nwords + c + 1);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int e = e0 + u * kScan2Threads;
+            if (e < nwords * 64) {
+                diag[e] = dv[u];
+                sdiag[e] = sv[u];
+            }
+        }
+    }
+    for (int w = tid; w < nwords; w += kScan2Threads) removed[w] = 0;
+    if (tid == 0) {
+        for (int g = 0; g < 2; ++g) {
+            mbar_init(&rows_ready[g], 1);
+            mbar_init(&or_done[g], 4);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    if (warp == 0) {
+        // ------------------------------------------------ decisions (lane 0)
+        if (lane == 0) {
+            int kc = 0;
+            int c = 0;
+            for (; c < nwords; ++c) {
+                const int g = c & 1, it = c >> 1;
+                // bulk OR of chunk c-2 (same worker group) must be in removed[]
+                if (c >= 2) mbar_wait(&or_done[g], (it - 1) & 1);
+                const int lim = min(64, k - c * 64);
+                const uint64_t valid = lim >= 64 ? ~0ull : ((1ull << lim) - 1ull);
+                uint64_t w = atomicOr(reinterpret_cast<unsigned long long*>(&removed[c]), 0ull);
+                uint64_t nxt = 0;
+                int nr = 0;
+                uint64_t cand = ~w & valid;
+                while (cand && kc < post_k) {
+                    const int b = __ffsll(static_cast<long long>(cand)) - 1;
+                    keep_pos[static_cast<int64_t>(img) * post_k + kc] = c * 64 + b;
+                    ++kc;
+                    rows[g][nr++] = c * 64 + b;
+                    w |= diag[c * 64 + b];
+                    nxt |= sdiag[c * 64 + b];
+                    cand = ~w & valid & ~((2ull << b) - 1ull);
+                }
+                if (c + 1 < nwords && nxt) atomicOr(reinterpret_cast<unsigned long long*>(&removed[c + 1]), nxt);
+                const bool finished = kc >= post_k || c + 1 >= nwords;
+                nrows[g] = finished ? -1 - nr : nr;  // negative: last chunk (workers stop after it)
+                mbar_arrive(&rows_ready[g]);
+                if (finished) {
+                    // release the other group, waiting for chunk c + 1, once it has
+                    // finished chunk c - 1
+                    const int g2 = g ^ 1, c2 = c + 1;
+                    if (c2 >= 2) mbar_wait(&or_done[g2], ((c2 >> 1) - 1) & 1);
+                    nrows[g2] = -1;
+                    mbar_arrive(&rows_ready[g2]);
+                    break;
+                }
+            }
+            kept_total = kc;
+        }
+    } else {
+        // ------------------------------------------------ bulk OR workers
+        const int g = (warp - 1) >> 2;           // 0: even chunks, 1: odd chunks
+        const int wt = tid - 32 - g * 128;       // 0..127 within the group
+        for (int c = g, it = 0;; c += 2, ++it) {
+            mbar_wait(&rows_ready[g], it & 1);
+            int nr = nrows[g];
+            const bool last = nr < 0;
+            if (last) nr = -1 - nr;
+            const int w0 = c + 2, nrem = nwords - w0;
+            if (nr > 0 && nrem > 0) {
+                const int total = nr * nrem;
+                for (int e0 = wt; e0 < total; e0 += 4 * 128) {
+                    uint64_t v[4];
+                    int wi[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int e = e0 + u * 128;
+                        v[u] = 0;
+                        wi[u] = 0;
+                        if (e < total) {
+                            const int r = e / nrem;
+                            wi[u] = w0 + (e - r * nrem);
+                            v[u] = __ldg(M + static_cast<int64_t>(rows[g][r]) * nwords + wi[u]);
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        if (v[u]) atomicOr(reinterpret_cast<unsigned long long*>(&removed[wi[u]]),
+                                           static_cast<unsigned long long>(v[u]));
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&or_done[g]);
+            if (last) break;
+        }
+    }
+    __syncthreads();
+    const int nk = kept_total;
+    for (int j = tid; j < post_k; j += kScan2Threads) {
+        float* o = rois + (static_cast<int64_t>(img) * post_k + j) * 4;
+        if (j < nk) {
+            const int i = keep_pos[static_cast<int64_t>(img) * post_k + j];
+            const float* b = boxes + (static_cast<int64_t>(img) * k + i) * 4;
+            o[0] = b[0]; o[1] = b[1]; o[2] = b[2]; o[3] = b[3];
+            if (roi_scores) roi_scores[static_cast<int64_t>(img) * post_k + j] = scores[static_cast<int64_t>(img) * k + i];
+        } else {
+            o[0] = o[1] = o[2] = o[3] = 0.0f;
+        }
+    }
+    if (tid == 0) count[img] = nk;
+}
+
 // ---------------------------------------------------------------- anchor targets
 // per anchor: inside flag, max IoU, argmax; per gt: max IoU over inside anchors
 __global__ void anchor_iou_kernel(const float* __restrict__ anchors, int nA, const float* __restrict__ gt, int gt_stride,
@@ -896,8 +1053,15 @@ cudaError_t rpn_proposals(const ProposalArgs& p, void* ws, cudaStream_t st) {
     }
     dim3 mg(nwords, nwords, p.n_img);
     nms_mask_kernel<<<mg, 64, 0, st>>>(boxes, k, nwords, p.iou_thr, mask);
-    nms_scan_kernel<<<p.n_img, kScanThreads, static_cast<size_t>(nwords) * 8, st>>>(
-        boxes, mask, scores, k, nwords, p.post_k, p.rois, p.roi_scores, p.keep_pos, p.count);
+    if (nwords <= kScan2MaxWords) {
+        const size_t smem2 = static_cast<size_t>(nwords) * (2 * 64 + 1) * 8;
+        cudaFuncSetAttribute(nms_scan2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem2));
+        nms_scan2_kernel<<<p.n_img, kScan2Threads, smem2, st>>>(boxes, mask, scores, k, nwords, p.post_k, p.rois,
+                                                                p.roi_scores, p.keep_pos, p.count);
+    } else {
+        nms_scan_kernel<<<p.n_img, kScanThreads, static_cast<size_t>(nwords) * 8, st>>>(
+            boxes, mask, scores, k, nwords, p.post_k, p.rois, p.roi_scores, p.keep_pos, p.count);
+    }
     return cudaGetLastError();
 }
 
