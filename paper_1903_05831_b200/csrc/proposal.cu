@@ -13,7 +13,8 @@
 //             compaction, then a rank-by-counting sort (deterministic)
 //   decode    anchors + deltas -> clipped boxes, portable exp (bit-identical to
 //             orc_expf)
-//   nms mask  64x64 IoU tiles -> upper-triangular bitmask (fp64, -fmad=false)
+//   nms mask  64x64 IoU tiles -> upper-triangular bitmask (fp64, -fmad=false),
+//             persistent CTAs over the triangle
 //   nms scan  one CTA per image: chunked keep scan, diagonal words in smem,
 //             parallel OR of kept rows, early exit at post_k
 //   targets   fp64 IoU vs ground truth, Detectron-style labels, counter-RNG
@@ -469,33 +470,74 @@ __global__ void __launch_bounds__(256) topk_rank_decode_kernel(TopkMC m) {
 }
 
 // ---------------------------------------------------------------- NMS
-__global__ void __launch_bounds__(64) nms_mask_kernel(const float* __restrict__ boxes, int k, int nwords, double thr,
-                                                      uint64_t* __restrict__ mask) {
-    const int img = blockIdx.z, rb = blockIdx.y, cb = blockIdx.x;
-    if (cb < rb) return;
-    __shared__ float cbx[64][4];
-    const float* B = boxes + static_cast<int64_t>(img) * k * 4;
-    const int j0 = cb * 64;
-    const int t = threadIdx.x;
-    if (j0 + t < k) {
-#pragma unroll
-        for (int c = 0; c < 4; ++c) cbx[t][c] = B[(j0 + t) * 4 + c];
+// Persistent upper-triangular mask: 4 tiles (64 rows x 64 columns) in flight
+// per 256-thread CTA, tiles strided over a grid of a few CTAs per SM (the
+// (nwords x nwords x img) grid of 64-thread blocks spent most of its time
+// launching and retiring blocks, half of which exited at once).
+__global__ void __launch_bounds__(256) nms_mask2_kernel(const float* __restrict__ boxes, int k, int nwords, double thr,
+                                                       uint64_t* __restrict__ mask) {
+    __shared__ float4 cbox[4][64];
+    const int img = blockIdx.y;
+    const int T = nwords * (nwords + 1) / 2;
+    const int grp = threadIdx.x >> 6, t = threadIdx.x & 63;
+    const float4* B = reinterpret_cast<const float4*>(boxes + static_cast<int64_t>(img) * k * 4);
+    // fp32 screen: inter_f and uni_f are within ~2e-6 (relative) of the exact
+    // values (every float difference is exactly rounded, products and the
+    // union add at most a few ulps), so outside a 1e-5 band around the
+    // threshold the fp32 comparison decides exactly as the fp64 reference
+    const float thr_hi = static_cast<float>(thr) * (1.0f + 1e-5f), thr_lo = static_cast<float>(thr) * (1.0f - 1e-5f);
+    const int tiles_per_pass = gridDim.x * 4;
+    const int n_pass = (T + tiles_per_pass - 1) / tiles_per_pass;
+    for (int pass = 0; pass < n_pass; ++pass) {
+        const int tile = pass * tiles_per_pass + blockIdx.x * 4 + grp;
+        const bool live = tile < T;
+        int rb = 0, cb = 0;
+        if (live) {
+            // row block rb: first tile index S(rb) = rb*nwords - rb*(rb-1)/2 <= tile
+            int lo = 0, hi = nwords - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                const int smid = mid * nwords - mid * (mid - 1) / 2;
+                if (smid <= tile) lo = mid;
+                else hi = mid - 1;
+            }
+            rb = lo;
+            cb = rb + (tile - (rb * nwords - rb * (rb - 1) / 2));
+            const int jt = cb * 64 + t;
+            if (jt < k) cbox[grp][t] = __ldg(B + jt);
+        }
+        asm volatile("bar.sync %0, 64;" ::"r"(grp + 1) : "memory");
+        const int i = rb * 64 + t;
+        if (live && i < k) {
+            const float4 bi = __ldg(B + i);
+            const float ai = __fmul_rn(__fsub_rn(bi.z, bi.x), __fsub_rn(bi.w, bi.y));
+            uint64_t bits = 0;
+            const int j0 = cb * 64;
+            const int jn = min(64, k - j0);
+            for (int jj = 0; jj < jn; ++jj) {
+                const int j = j0 + jj;
+                if (j <= i) continue;
+                const float4 bj = cbox[grp][jj];
+                // cheap exact reject: no overlap -> IoU is 0, never > thr (thr >= 0)
+                if (bj.x >= bi.z || bj.z <= bi.x || bj.y >= bi.w || bj.w <= bi.y) continue;
+                const float ix = __fsub_rn(fminf(bi.z, bj.z), fmaxf(bi.x, bj.x));
+                const float iy = __fsub_rn(fminf(bi.w, bj.w), fmaxf(bi.y, bj.y));
+                const float inter = __fmul_rn(ix, iy);
+                const float aj = __fmul_rn(__fsub_rn(bj.z, bj.x), __fsub_rn(bj.w, bj.y));
+                const float uni = __fsub_rn(__fadd_rn(ai, aj), inter);
+                if (uni > 0.0f) {
+                    if (inter > __fmul_rn(thr_hi, uni)) {
+                        bits |= 1ull << jj;
+                        continue;
+                    }
+                    if (inter < __fmul_rn(thr_lo, uni)) continue;
+                }
+                if (iou_gt(bi.x, bi.y, bi.z, bi.w, bj.x, bj.y, bj.z, bj.w, thr)) bits |= 1ull << jj;
+            }
+            mask[(static_cast<int64_t>(img) * k + i) * nwords + cb] = bits;
+        }
+        asm volatile("bar.sync %0, 64;" ::"r"(grp + 1) : "memory");
     }
-    __syncthreads();
-    const int i = rb * 64 + t;
-    if (i >= k) return;
-    const float* bi = B + static_cast<int64_t>(i) * 4;
-    const double x1 = bi[0], y1 = bi[1], x2 = bi[2], y2 = bi[3];
-    uint64_t bits = 0;
-    const int jn = min(64, k - j0);
-    for (int jj = 0; jj < jn; ++jj) {
-        const int j = j0 + jj;
-        if (j <= i) continue;
-        // cheap exact reject: no overlap -> IoU is 0, never > thr (thr >= 0)
-        if (cbx[jj][0] >= bi[2] || cbx[jj][2] <= bi[0] || cbx[jj][1] >= bi[3] || cbx[jj][3] <= bi[1]) continue;
-        if (iou_gt(x1, y1, x2, y2, cbx[jj][0], cbx[jj][1], cbx[jj][2], cbx[jj][3], thr)) bits |= 1ull << jj;
-    }
-    mask[(static_cast<int64_t>(img) * k + i) * nwords + cb] = bits;
 }
 
 constexpr int kScanThreads = 256;
@@ -1051,8 +1093,11 @@ cudaError_t rpn_proposals(const ProposalArgs& p, void* ws, cudaStream_t st) {
     if (p.topk_order_out) {
         cudaMemcpyAsync(p.topk_order_out, order, static_cast<size_t>(p.n_img) * k * 4, cudaMemcpyDeviceToDevice, st);
     }
-    dim3 mg(nwords, nwords, p.n_img);
-    nms_mask_kernel<<<mg, 64, 0, st>>>(boxes, k, nwords, p.iou_thr, mask);
+    {
+        const int tiles = nwords * (nwords + 1) / 2;
+        const int g = std::max(1, std::min((tiles + 3) / 4, 4 * kNumSMs / std::max(1, p.n_img)));
+        nms_mask2_kernel<<<dim3(g, p.n_img), 256, 0, st>>>(boxes, k, nwords, p.iou_thr, mask);
+    }
     if (nwords <= kScan2MaxWords) {
         const size_t smem2 = static_cast<size_t>(nwords) * (2 * 64 + 1) * 8;
         cudaFuncSetAttribute(nms_scan2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem2));
