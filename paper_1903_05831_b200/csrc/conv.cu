@@ -573,12 +573,18 @@ SDB_DEV void epilogue_tile_v2(const ConvArgs& a, int split, int m0, int n0, int 
         }
         __syncwarp();
         const int col = n0 + c_lo + cb + c8 * 8;
+        // all staged reads first (independent LDS in flight), then the stores
+        float4 fa[NK], fb[NK];
 #pragma unroll
         for (int k = 0; k < NK; ++k) {
             const int r = (k * 32 + lane) / LPR;
             const int sw = r & (SLOTS - 1);
-            const float4 f0 = *reinterpret_cast<const float4*>(stg + r * SC + (((2 * c8) ^ sw) * 4));
-            const float4 f1 = *reinterpret_cast<const float4*>(stg + r * SC + (((2 * c8 + 1) ^ sw) * 4));
+            fa[k] = *reinterpret_cast<const float4*>(stg + r * SC + (((2 * c8) ^ sw) * 4));
+            fb[k] = *reinterpret_cast<const float4*>(stg + r * SC + (((2 * c8 + 1) ^ sw) * 4));
+        }
+#pragma unroll
+        for (int k = 0; k < NK; ++k) {
+            const float4 f0 = fa[k], f1 = fb[k];
             if (rowp[k] < 0 || col >= lim) continue;
             float f[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
             if (MODE == WGRAD) {
