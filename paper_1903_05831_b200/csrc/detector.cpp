@@ -443,6 +443,27 @@ void block_fwd(sdb_det* d, Block& b) {
     conv_fwd(d, b.c2, b.a1, b.z2);
     norm_fwd(d, b.n2, b.z2, b.a2);
     conv_fwd(d, b.c3, b.a2, b.z3);
+    if (b.n3.act == 2) {
+        // InPlace-ABN bn3: statistics now, the apply fused with the residual
+        // add + leaky that closes the block (one pass: reads z3 + shortcut,
+        // writes y3 in place and the block output)
+        const int64_t rows = static_cast<int64_t>(b.z3.n) * b.z3.h * b.z3.w;
+        {
+            PScope ps(d, P_NORM_F, 0, 1.0 * d->es * b.z3.numel(), 2);
+            CK(bn_forward_stats(d->dt, b.z3.p, b.n3.mean, b.n3.invstd, rows, b.n3.C, d->cfg.eps, b.n3.act, d->ws,
+                                d->ctx->stream));
+        }
+        const Act* sc = &b.in;
+        if (b.has_down) {
+            conv_fwd(d, b.down, b.in, b.zd);
+            norm_fwd(d, b.nd, b.zd, b.d);
+            sc = &b.d;
+        }
+        PScope ps(d, P_NORM_F, 0, 4.0 * d->es * b.out.numel());
+        CK(bn_apply_add_act(d->dt, b.z3.p, d->bnp(b.n3.pg), d->bnp(b.n3.pb), b.n3.mean, b.n3.invstd, b.b3.p, sc->p,
+                            b.out.p, rows, b.n3.C, b.n3.slope, 2, d->cfg.slope, d->ctx->stream));
+        return;
+    }
     norm_fwd(d, b.n3, b.z3, b.b3);
     const Act* sc = &b.in;
     if (b.has_down) {

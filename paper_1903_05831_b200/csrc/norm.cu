@@ -332,6 +332,11 @@ struct ApplyArgs {
     int act;
     int64_t n8;  // number of 8-element groups
     int C;
+    // KIND 4 (IABN fwd fused with the residual add + activation): the shortcut
+    // arrives through the `dy` slot, out2 = act2(round(y) + shortcut)
+    void* out2;
+    int act2;
+    float slope2;
 };
 
 SDB_DEV void ldf8(const float* p, float (&v)[8]) {
@@ -406,13 +411,26 @@ __global__ void __launch_bounds__(kStatThreads, 2) apply_kernel(ApplyArgs p, int
             const int off = rr * C + c0;
             float v[8], o[8];
             load8<T>(ta + off, v);
-            if (KIND == 0 || KIND == 1) {
+            if (KIND == 0 || KIND == 1 || KIND == 4) {
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     // gamma*(x-mean)*invstd + beta, evaluated like the reference (no contraction)
                     const float z = __fadd_rn(__fmul_rn(__fmul_rn(g[j], __fsub_rn(v[j], mu[j])), is[j]), b[j]);
                     if (KIND == 0) o[j] = (p.act && !(z > 0.f)) ? 0.f : z;
                     else o[j] = z > 0.f ? z : __fmul_rn(p.slope, z);
+                }
+                if (KIND == 4) {
+                    // residual node: s = round(round(y) + shortcut) (src/tensor.cpp:125), then
+                    // relu / leaky, exactly as the separate add_act pass
+                    float sc[8], o2[8];
+                    load8<T>(td + off, sc);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const float yr = to_f<T>(from_f<T>(o[j]));
+                        const float sr = to_f<T>(from_f<T>(__fadd_rn(yr, sc[j])));
+                        o2[j] = p.act2 == 0 ? sr : (sr > 0.f ? sr : (p.act2 == 1 ? 0.f : __fmul_rn(p.slope2, sr)));
+                    }
+                    store8<T>(static_cast<T*>(p.out2) + (r0 + rr) * C + c0, o2);
                 }
             } else {
                 float d[8];
@@ -524,6 +542,29 @@ cudaError_t bn_forward(int dtype, const void* x, const float* gamma, const float
     aa.slope = slope; aa.act = act; aa.n8 = rows * C / 8; aa.C = C;
     if (act == 2) return dtype == kF16 ? run_apply<__half, 1, 1>(aa, rows, pl, st) : run_apply<float, 1, 1>(aa, rows, pl, st);
     return dtype == kF16 ? run_apply<__half, 0, 1>(aa, rows, pl, st) : run_apply<float, 0, 1>(aa, rows, pl, st);
+}
+
+cudaError_t bn_forward_stats(int dtype, const void* x, float* mean, float* invstd, int64_t rows, int C, float eps,
+                             int act, void* ws, cudaStream_t st) {
+    const Plan pl = plan_for(rows, C, dtype == kF16 ? 2 : 4);
+    double* partial = static_cast<double*>(ws);
+    StatArgs sa{};
+    sa.a = x; sa.rows = rows; sa.C = C; sa.partial = partial; sa.slope = 1.f;
+    cudaError_t e = dtype == kF16 ? run_stats<__half, 0, 1>(sa, pl, st) : run_stats<float, 0, 1>(sa, pl, st);
+    if (e != cudaSuccess) return e;
+    finalize(partial, pl, C, rows, eps, act == 2 ? 1 : 0, mean, invstd, nullptr, nullptr, nullptr, st);
+    return cudaGetLastError();
+}
+
+cudaError_t bn_apply_add_act(int dtype, const void* x, const float* gamma, const float* beta, const float* mean,
+                             const float* invstd, void* y, const void* shortcut, void* out, int64_t rows, int C,
+                             float slope, int act2, float slope2, cudaStream_t st) {
+    const Plan pl = plan_for(rows, C, dtype == kF16 ? 2 : 4);
+    ApplyArgs aa{};
+    aa.a = x; aa.dy = shortcut; aa.out = y; aa.gamma = gamma; aa.beta = beta; aa.mean = mean; aa.invstd = invstd;
+    aa.slope = slope; aa.act = 2; aa.n8 = rows * C / 8; aa.C = C;
+    aa.out2 = out; aa.act2 = act2; aa.slope2 = slope2;
+    return dtype == kF16 ? run_apply<__half, 4, 2>(aa, rows, pl, st) : run_apply<float, 4, 2>(aa, rows, pl, st);
 }
 
 cudaError_t bn_backward(int dtype, const void* dy, const void* x, const void* y_mask, const float* gamma,

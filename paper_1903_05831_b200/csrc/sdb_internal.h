@@ -39,6 +39,15 @@ size_t norm_workspace_bytes(int64_t rows, int C);
 cudaError_t bn_forward(int dtype, const void* x, const float* gamma, const float* beta, void* y, float* mean,
                        float* invstd, int64_t rows, int C, float eps, int act, float slope, void* ws,
                        cudaStream_t st);
+// the two halves of bn_forward, for an IABN layer whose apply is fused with the
+// residual add + activation that follows it: out = act2(round(y) + shortcut)
+// (act2: 0 none, 1 relu, 2 leaky slope2); y is still written (IABN backward
+// recomputes from it)
+cudaError_t bn_forward_stats(int dtype, const void* x, float* mean, float* invstd, int64_t rows, int C, float eps,
+                             int act, void* ws, cudaStream_t st);
+cudaError_t bn_apply_add_act(int dtype, const void* x, const float* gamma, const float* beta, const float* mean,
+                             const float* invstd, void* y, const void* shortcut, void* out, int64_t rows, int C,
+                             float slope, int act2, float slope2, cudaStream_t st);
 // y_mask: stored BN+ReLU output (relu mask) or null for plain BN
 cudaError_t bn_backward(int dtype, const void* dy, const void* x, const void* y_mask, const float* gamma,
                         const float* mean, const float* invstd, void* dx, float* dgamma, float* dbeta, int64_t rows,
