@@ -315,6 +315,19 @@ def run_ours(args):
     peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1400.0)))
     achieved = conv_flops / (conv_ms / 1e3) / 1e12 if conv_ms > 0 else 0.0
     launches_per_step = det.kernel_launches()
+    # DRAM traffic of the conv family, from the committed ncu capture of one C4
+    # step (profiles/r01_conv_traffic.json: dram__bytes_read.sum +
+    # dram__bytes_write.sum over every conv launch of the step); the bench itself
+    # never runs under a profiler
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_conv_traffic.json")) as f:
+            tj = json.load(f)
+        if args.config == "c4":
+            traffic = {"bytes_per_launch": tj["conv_dram_bytes_per_launch"],
+                       "bytes_per_step": tj["conv_dram_bytes_per_step"], "source": tj["source"]}
+    except Exception:
+        traffic = None
 
     if rank != 0:
         if dist is not None:
@@ -344,7 +357,7 @@ def run_ours(args):
                    "loss_scale": scale_used, "last_losses": losses[:5], "overflow": overflow},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak if peak else None, "traffic": None,
+                     "frac": achieved / peak if peak else None, "traffic": traffic,
                      "kernel": "conv_tc_kernel (tcgen05 implicit GEMM, fprop+dgrad+wgrad, FLOP-weighted)",
                      "peak_source": f"{peak_kind} bf16_tflops_sustained",
                      "flop_per_step": conv_flops, "ms_per_step": conv_ms, "launches_per_step": conv_launches},
