@@ -162,7 +162,10 @@ __global__ void __launch_bounds__(kBwdThreads) roialign_bwd_kernel(const T* __re
     const int y0 = ty * kTile, x0 = tx * kTile;
     const int c_base = blockIdx.y * kSlab;
     const int chunk = threadIdx.x & 31;         // 8-channel chunk within the slab
-    const int pix0 = threadIdx.x >> 5;          // pixels pix0 + 8*i
+    // warp w owns pixels (row i, column (w + i) & 7), i = 0..7: every warp has one
+    // pixel in each row and each column of the tile, so a rectangular RoI gives
+    // every warp (nearly) the same amount of work between barriers
+    const int pix0 = threadIdx.x >> 5;
     const int c = c_base + chunk * 8;
     const bool c_ok = c < C;
     const float inv_count = 1.0f / static_cast<float>(max(sr * sr, 1));
@@ -253,7 +256,7 @@ __global__ void __launch_bounds__(kBwdThreads) roialign_bwd_kernel(const T* __re
                     const T* d = dy + static_cast<int64_t>(list[l0 + j]) * Po * Po * C + c;
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
-                        const int p = pix0 + 8 * i;
+                        const int p = i * 8 + ((pix0 + i) & 7);
                         const int ly = p >> 3, lx = p & 7;
                         if (y0 + ly >= H || x0 + lx >= W) continue;
                         const int phe = rng[rb][j][1][ly], pwb = rng[rb][j][2][lx], pwe = rng[rb][j][3][lx];
@@ -279,7 +282,7 @@ __global__ void __launch_bounds__(kBwdThreads) roialign_bwd_kernel(const T* __re
     if (!c_ok) return;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        const int p = pix0 + 8 * i;
+        const int p = i * 8 + ((pix0 + i) & 7);
         const int yy = y0 + (p >> 3), xx = x0 + (p & 7);
         if (yy >= H || xx >= W) continue;
         st8<T>(dfeat + ((static_cast<int64_t>(n) * H + yy) * W + xx) * C + c, acc[i]);
