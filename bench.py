@@ -210,6 +210,68 @@ def run_reference(args):
     print(json.dumps(line))
 
 
+# ------------------------------------------------------------------ C3 microbenchmark
+def run_c3(args):
+    """BASELINE config C3: RPN proposal layer + RoIAlign 14x14 forward and backward.
+    Batch 8, 1024-channel fp16 C4 feature 50x84 (stride 16 on 800x1333), 15 anchors
+    per location, logits N(0,2), deltas N(0,0.2), 12000 -> 2000 at IoU 0.7, RoIAlign
+    on the first 512 proposals of each image, dY N(0,1).  One step = proposals +
+    RoIAlign fwd + bwd over the batch, inputs resident in HBM."""
+    import ctypes as C
+    import torch
+
+    from paper_1903_05831_b200 import simdet as sd
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    lib = sd.L()
+    B, H, W, Cc, A, Ap, P = 8, 50, 84, 1024, 15, 16, 14
+    g = torch.Generator(device="cuda")
+    g.manual_seed(3 + rank)
+    feat = torch.randn((B, H, W, Cc), generator=g, device="cuda").half()
+    logits = (torch.randn((B, H * W, Ap), generator=g, device="cuda") * 2).half()
+    deltas = (torch.randn((B, H * W, 4 * Ap), generator=g, device="cuda") * 0.2).half()
+    anchors = sd.make_anchors(H, W, 16.0, (32.0, 64.0, 128.0, 256.0, 512.0), (0.5, 1.0, 2.0))
+    R = B * 512
+    rois5 = torch.zeros((R, 5), device="cuda", dtype=torch.float32)
+    rois5[:, 0] = torch.arange(B, device="cuda").repeat_interleave(512).float()
+    out = torch.empty((R, P, P, Cc), device="cuda", dtype=torch.float16)
+    dy = torch.randn((R, P, P, Cc), generator=g, device="cuda").half()
+    dx = torch.empty_like(feat)
+    st = sd.stream()
+
+    def one():
+        rois, _, _, _ = sd.rpn_proposal(logits, deltas, anchors, A, 12000, 0.7, 2000, 800.0, 1333.0)
+        rois5[:, 1:] = rois[:, :512, :].reshape(R, 4)
+        sd.check(lib.sdb_roialign_fwd(sd.ctx(), 1, sd.ptr(feat), B, H, W, Cc, sd.ptr(rois5), R, P, 1.0 / 16, 2,
+                                      sd.ptr(out), st))
+        sd.check(lib.sdb_roialign_bwd(sd.ctx(), 1, sd.ptr(dy), B, H, W, Cc, sd.ptr(rois5), R, P, 1.0 / 16, 2,
+                                      sd.ptr(dx), st))
+
+    for _ in range(max(args.warmup, 3)):
+        one()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        e0.record()
+        for _ in range(args.steps):
+            one()
+        e1.record()
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    # algorithmic bytes of the RoIAlign passes (SURVEY 8(d)): fwd writes R*P*P*C fp16
+    # and reads the feature once; bwd reads dY and writes dX
+    ra_bytes = 2 * (R * P * P * Cc * 2) + 2 * feat.numel() * 2
+    line = {"metric": "C3 proposal + RoIAlign fwd/bwd microbenchmark", "value": B / (ms / 1e3), "unit": "images/s",
+            "n_gpus": 1, "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp16 features, fp32 boxes",
+            "data": "synthetic (BASELINE C3 distributions)",
+            "config": {"workload": "C3: batch 8, 1024x50x84 fp16, 15 anchors/loc, 12000->2000 @0.7, RoIAlign 14x14 "
+                                   "on 512 RoIs/img fwd+bwd"},
+            "roialign_alg_bytes_per_step": ra_bytes, "clocks": clk.summary()}
+    if rank == 0:
+        print(json.dumps(line))
+
+
 # ------------------------------------------------------------------ ours
 def run_ours(args):
     import numpy as np
@@ -379,6 +441,8 @@ def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.config == "c3":
+        run_c3(args)
     else:
         run_ours(args)
 

@@ -263,13 +263,9 @@ int sdb_rpn_proposal(sdb_ctx* ctx, int dtype, const void* logits, const void* de
     if (std::min<int64_t>(pre_k, static_cast<int64_t>(n_loc) * A) > 16384)
         return fail(SDB_UNSUPPORTED, "rpn_proposal: pre_k > 16384");
     const size_t wsb = sdb::proposal_workspace_bytes(n_img, n_loc * A, pre_k);
-    void* ws = ctx->scratch(wsb);
-    if (!ws) return fail(SDB_CUDA, "workspace allocation failed");
-    std::vector<int32_t> dummy;
-    int32_t* keep = static_cast<int32_t*>(ctx->scratch(0)) ;
-    (void)keep;
-    // keep positions live in a second scratch region after the proposal workspace
+    // one scratch region: the proposal workspace, then the keep positions
     void* ws2 = ctx->scratch(wsb + static_cast<size_t>(n_img) * post_k * 4 + 256);
+    if (!ws2) return fail(SDB_CUDA, "workspace allocation failed");
     sdb::ProposalArgs p{};
     p.logits = logits; p.deltas = deltas; p.dtype = dtype; p.anchors = anchors;
     p.n_img = n_img; p.n_loc = n_loc; p.A = A; p.A_pad = A_pad; p.pre_k = pre_k; p.post_k = post_k;
