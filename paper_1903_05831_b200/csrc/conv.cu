@@ -53,6 +53,11 @@ struct ConvArgs {
     int kb_per_split;
     int accumulate;  // dgrad: out = result + addend
     const void* addend;  // dgrad accumulate source (may alias out)
+    // dgrad: gradient through the activation that produced the layer input:
+    // out = round(round(result + addend) * (mask > 0 ? 1 : mask_neg)) -- the
+    // separate act_bwd pass (src/autograd.cpp:340-351) folded into the epilogue
+    const void* mask;
+    float mask_neg;
     int tma_b;       // dgrad: filter operand loaded by TMA (needs K % 64 == 0)
     int plain;       // 1x1 / stride 1 / pad 0: the activation operand is a plain 2-D [pixels][channels] tile
 };
@@ -537,21 +542,24 @@ SDB_DEV void epilogue_tile_v2(const ConvArgs& a, int split, int m0, int n0, int 
     const int lim = MODE == DGRAD ? a.C : a.NG;
     const bool vec = MODE == WGRAD ? (lim & 3) == 0 : (lim & 7) == 0;
     const bool add = MODE == DGRAD && a.accumulate;
+    const bool msk = MODE == DGRAD && a.mask != nullptr;
     const int c8 = lane % LPR;
-    uint4 addv[NK], addn[NK];
-    auto load_add = [&](uint4 (&dst)[NK], int cb) {
+    uint4 addv[NK], addn[NK], mskv[NK], mskn[NK];
+    auto load_vec = [&](const void* src, uint4 (&dst)[NK], int cb) {
         const int col = n0 + c_lo + cb + c8 * 8;
 #pragma unroll
         for (int k = 0; k < NK; ++k) {
             dst[k] = make_uint4(0, 0, 0, 0);
             if (rowp[k] >= 0 && col + 8 <= lim && vec)
-                dst[k] = *reinterpret_cast<const uint4*>(static_cast<const __half*>(a.addend) + rowp[k] + col);
+                dst[k] = *reinterpret_cast<const uint4*>(static_cast<const __half*>(src) + rowp[k] + col);
         }
     };
-    if (add) load_add(addv, 0);
+    if (add) load_vec(a.addend, addv, 0);
+    if (msk) load_vec(a.mask, mskv, 0);
 #pragma unroll 1
     for (int cb = 0; cb < NCOL; cb += SC) {
-        if (add && cb + SC < NCOL) load_add(addn, cb + SC);
+        if (add && cb + SC < NCOL) load_vec(a.addend, addn, cb + SC);
+        if (msk && cb + SC < NCOL) load_vec(a.mask, mskn, cb + SC);
         uint32_t v[SC];
         tmem_ld_cols<SC>(tacc + (static_cast<uint32_t>(q * 32) << 16) + c_lo + cb, v);
         if (cb + SC >= NCOL) {
@@ -607,11 +615,25 @@ SDB_DEV void epilogue_tile_v2(const ConvArgs& a, int split, int m0, int n0, int 
                     __half2* p2 = reinterpret_cast<__half2*>(&pk);
 #pragma unroll
                     for (int e = 0; e < 4; ++e) p2[e] = __floats2half2_rn(f[2 * e], f[2 * e + 1]);
+                    if (msk) {
+                        const __half2* m2 = reinterpret_cast<const __half2*>(&mskv[k]);
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const float2 gv = __half22float2(p2[e]), yv = __half22float2(m2[e]);
+                            p2[e] = __floats2half2_rn(yv.x > 0.f ? gv.x : __fmul_rn(a.mask_neg, gv.x),
+                                                      yv.y > 0.f ? gv.y : __fmul_rn(a.mask_neg, gv.y));
+                        }
+                    }
                     *reinterpret_cast<uint4*>(o) = pk;
                 } else {
                     for (int e = 0; e < 8 && col + e < lim; ++e) {
                         float x = f[e];
                         if (add) x += __half2float(static_cast<const __half*>(a.addend)[rowp[k] + col + e]);
+                        if (MODE == DGRAD && a.mask) {
+                            x = __half2float(__float2half_rn(x));
+                            if (!(__half2float(static_cast<const __half*>(a.mask)[rowp[k] + col + e]) > 0.f))
+                                x = __fmul_rn(a.mask_neg, x);
+                        }
                         o[e] = __float2half_rn(x);
                     }
                 }
@@ -621,6 +643,10 @@ SDB_DEV void epilogue_tile_v2(const ConvArgs& a, int split, int m0, int n0, int 
         if (add) {
 #pragma unroll
             for (int k = 0; k < NK; ++k) addv[k] = addn[k];
+        }
+        if (msk) {
+#pragma unroll
+            for (int k = 0; k < NK; ++k) mskv[k] = mskn[k];
         }
     }
 }
@@ -1017,6 +1043,11 @@ __global__ void __launch_bounds__(256) conv_simt_kernel(ConvArgs a) {
                 T* o = static_cast<T*>(a.out) + row + n;
                 float f = acc[i][j];
                 if (MODE == DGRAD && a.accumulate) f += to_f<T>(static_cast<const T*>(a.addend)[o - static_cast<T*>(a.out)]);
+                if (MODE == DGRAD && a.mask) {
+                    f = to_f<T>(from_f<T>(f));
+                    if (!(to_f<T>(static_cast<const T*>(a.mask)[o - static_cast<T*>(a.out)]) > 0.f))
+                        f = __fmul_rn(a.mask_neg, f);
+                }
                 *o = from_f<T>(f);
             }
         }
@@ -1331,21 +1362,27 @@ cudaError_t conv_fprop(const ConvShape& g, int dtype, const void* x, const void*
 }
 
 cudaError_t conv_dgrad(const ConvShape& g, int dtype, const void* dy, const void* w, void* dx, int accumulate,
-                       cudaStream_t st, const void* addend) {
+                       cudaStream_t st, const void* addend, const void* mask, float mask_neg) {
     ConvArgs base = make_args(g);
     base.x = dy; base.w = w; base.out = dx; base.accumulate = accumulate || addend != nullptr;
+    base.mask = mask;
+    base.mask_neg = mask_neg;
     base.addend = addend ? addend : dx;
     base.NG = g.C;
     const int sd = g.stride;
     // phases whose taps are all empty (e.g. the odd pixels of a 1x1 stride-2
     // conv) receive no gradient: zero the whole output once with a contiguous
     // memset (or leave it untouched when accumulating)
+    if (mask && tc_ok(g, dtype) && (g.K % kBK) != 0) return cudaErrorNotSupported;  // mask: TMA / SIMT epilogues only
     bool empty_phase = false;
     for (int ph = 0; ph < sd; ++ph)
         for (int pw = 0; pw < sd; ++pw) {
             const int r0 = (ph + g.pad) % sd, q0 = (pw + g.pad) % sd;
             if (r0 >= g.R || q0 >= g.S) empty_phase = true;
         }
+    // positions no tap reaches keep the addend (or zero) unmasked: only valid
+    // when they are zero, i.e. without a separate addend
+    if (mask && empty_phase && base.accumulate && base.addend != dx) return cudaErrorNotSupported;
     if (empty_phase && base.accumulate && base.addend != dx) {
         // taps never reach some output phases: those positions take the addend as is
         const cudaError_t e = cudaMemcpyAsync(dx, base.addend,

@@ -476,10 +476,11 @@ void block_fwd(sdb_det* d, Block& b) {
 }
 
 // ------------------------------------------------------------------ backward helpers
-void dgrad(sdb_det* d, const ConvL& c, const void* dy, void* dx, int accumulate, const void* addend = nullptr) {
+void dgrad(sdb_det* d, const ConvL& c, const void* dy, void* dx, int accumulate, const void* addend = nullptr,
+           const void* mask = nullptr, float mask_neg = 0.0f) {
     PScope ps(d, P_DGRAD, conv_flops(c.g), 0, c.g.stride * c.g.stride);
     if (d->prof.on) { ps.label = shape_label("dgrad", c.g); ps.flops_ = conv_flops(c.g); }
-    CK(conv_dgrad(c.g, d->dt, dy, d->wdev_ptr(c.p), dx, accumulate, d->ctx->stream, addend));
+    CK(conv_dgrad(c.g, d->dt, dy, d->wdev_ptr(c.p), dx, accumulate, d->ctx->stream, addend, mask, mask_neg));
 }
 
 struct Bwd {
@@ -513,18 +514,15 @@ void conv_wgrad_to(Bwd& B, const ConvL& c, const Act& x, const void* dy) {
     grads_ready(B, c.p);
 }
 
-// backward of a bottleneck; dout = grad wrt b.out (buffer may be clobbered);
-// writes grad wrt b.in into dx.  Uses scratch buffers s0..s2.
-void block_bwd(Bwd& B, Block& b, void* dout, void* dx, void* s0, void* s1, void* s2) {
+// backward of a bottleneck.  dS = gradient at the residual add node (the
+// block's output activation already back-propagated: the producer of dS applied
+// the activation mask in its dgrad epilogue).  Writes the gradient wrt b.in into
+// dx; when b.in is itself a residual-block output (in_mask != null) the final
+// dgrad epilogue applies that block's activation mask too, so dx is the next
+// block's dS.  Uses scratch buffers s1, s2.
+void block_bwd(Bwd& B, Block& b, const void* dS, void* dx, void* s1, void* s2, const void* in_mask) {
     sdb_det* d = B.d;
-    cudaStream_t st = d->ctx->stream;
     const float neg = d->cfg.mode == 0 ? 0.0f : d->cfg.slope;
-    // add + activation: dS = act'(out) * dout   (rounded at the add node)
-    void* dS = s0;
-    {
-        PScope ps(d, P_ELEM, 0, 3.0 * d->es * b.out.numel());
-        CK(act_bwd(d->dt, dout, b.out.p, dS, b.out.numel(), neg, st));
-    }
     // shortcut first (its params come last in the block's pack order)
     if (b.has_down) {
         norm_bwd(d, b.nd, b.zd, b.d, dS, s1);
@@ -539,9 +537,10 @@ void block_bwd(Bwd& B, Block& b, void* dout, void* dx, void* s0, void* s1, void*
     dgrad(d, b.c2, s1, s2, 0);
     norm_bwd(d, b.n1, b.z1, b.a1, s2, s1);
     conv_wgrad_to(B, b.c1, b.in, s1);
-    // residual fan-in in the dgrad epilogue: dx = conv1^T(dz1) + (down-path dx | identity dS)
-    if (b.has_down) dgrad(d, b.c1, s1, dx, 1);
-    else dgrad(d, b.c1, s1, dx, 1, dS);
+    // residual fan-in in the dgrad epilogue: dx = conv1^T(dz1) + (down-path dx | identity dS),
+    // then the previous block's activation mask
+    if (b.has_down) dgrad(d, b.c1, s1, dx, 1, nullptr, in_mask, neg);
+    else dgrad(d, b.c1, s1, dx, 1, dS, in_mask, neg);
 }
 
 // ------------------------------------------------------------------ the step
@@ -628,8 +627,16 @@ void run_step(sdb_det* d) {
     CK(avgpool_bwd(d->dt, dpool, d->R, d->head_out.h * d->head_out.w, d->feat_c, dhead, st)); }
     void* cur = dhead;
     void* spare = d->gbuf[2];
+    const float neg = cf.mode == 0 ? 0.0f : cf.slope;
+    if (!d->head.empty()) {
+        // the last head block's output activation (its dS); inner block boundaries
+        // are masked in the dgrad epilogues
+        PScope ps(d, P_ELEM, 0, 3.0 * d->es * d->head_out.numel());
+        CK(act_bwd(d->dt, dhead, d->head_out.p, dhead, d->head_out.numel(), neg, st));
+    }
     for (int i = static_cast<int>(d->head.size()) - 1; i >= 0; --i) {
-        block_bwd(B, d->head[i], cur, spare, d->gbuf[0], d->gbuf[1], d->gbuf[4]);
+        const void* in_mask = i > 0 ? d->head[i - 1].out.p : nullptr;  // head[0].in = RoIAlign output (linear)
+        block_bwd(B, d->head[i], cur, spare, d->gbuf[1], d->gbuf[4], in_mask);
         std::swap(cur, spare);
     }
     (void)spare;
@@ -641,18 +648,29 @@ void run_step(sdb_det* d) {
     // RPN head backward (bbox, cls, conv)
     void* drpn = d->gbuf[0];
     conv_wgrad_to(B, d->rpn_bbox, d->rpn_a, d->d_rpn_deltas);
-    dgrad(d, d->rpn_bbox, d->d_rpn_deltas, drpn, 0);
     conv_wgrad_to(B, d->rpn_cls, d->rpn_a, d->d_rpn_logits);
-    dgrad(d, d->rpn_cls, d->d_rpn_logits, drpn, 1);
-    { PScope ps(d, P_ELEM, 0, 3.0 * d->es * d->rpn_a.numel());
-    CK(act_bwd(d->dt, drpn, d->rpn_a.p, drpn, d->rpn_a.numel(), 0.0f, st)); }
+    // the RPN ReLU backward is folded into whichever dgrad writes drpn last (the
+    // one with K % 64 == 0 on the tensor-core path)
+    const bool bbox_last = (d->rpn_bbox.g.K % 64) == 0 || d->dt != kF16;
+    const ConvL& r_first = bbox_last ? d->rpn_cls : d->rpn_bbox;
+    const ConvL& r_last = bbox_last ? d->rpn_bbox : d->rpn_cls;
+    dgrad(d, r_first, bbox_last ? d->d_rpn_logits : d->d_rpn_deltas, drpn, 0);
+    if ((r_last.g.K % 64) == 0 || d->dt != kF16) {
+        dgrad(d, r_last, bbox_last ? d->d_rpn_deltas : d->d_rpn_logits, drpn, 1, nullptr, d->rpn_a.p, 0.0f);
+    } else {
+        dgrad(d, r_last, bbox_last ? d->d_rpn_deltas : d->d_rpn_logits, drpn, 1);
+        PScope ps(d, P_ELEM, 0, 3.0 * d->es * d->rpn_a.numel());
+        CK(act_bwd(d->dt, drpn, d->rpn_a.p, drpn, d->rpn_a.numel(), 0.0f, st));
+    }
     conv_wgrad_to(B, d->rpn_conv, d->c4, drpn);
-    dgrad(d, d->rpn_conv, drpn, dc4, 1);
+    // dc4 (RoIAlign part) + RPN part, then the last backbone block's activation mask
+    dgrad(d, d->rpn_conv, drpn, dc4, 1, nullptr, d->c4.p, neg);
     // backbone
     cur = dc4;
     spare = dc4 == d->gbuf[2] ? d->gbuf[3] : d->gbuf[2];
     for (int i = static_cast<int>(d->backbone.size()) - 1; i >= 0; --i) {
-        block_bwd(B, d->backbone[i], cur, spare, d->gbuf[0], d->gbuf[1], d->gbuf[4]);
+        const void* in_mask = i > 0 ? d->backbone[i - 1].out.p : nullptr;  // backbone[0].in = max-pool output
+        block_bwd(B, d->backbone[i], cur, spare, d->gbuf[1], d->gbuf[4], in_mask);
         std::swap(cur, spare);
     }
     // maxpool, stem norm, stem wgrad (the image gradient is not needed)

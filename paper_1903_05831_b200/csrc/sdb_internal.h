@@ -24,8 +24,11 @@ struct ConvShape {
 // ---- conv.cu
 cudaError_t conv_fprop(const ConvShape& g, int dtype, const void* x, const void* w, void* y, cudaStream_t st);
 // accumulate: dx = conv^T(dy, w) + addend (addend = dx itself when null)
+// mask (optional): dx = round(dx) * (mask > 0 ? 1 : mask_neg), the backward of
+// the ReLU / leaky that produced this layer's input, fused into the epilogue
 cudaError_t conv_dgrad(const ConvShape& g, int dtype, const void* dy, const void* w, void* dx, int accumulate,
-                       cudaStream_t st, const void* addend = nullptr);
+                       cudaStream_t st, const void* addend = nullptr, const void* mask = nullptr,
+                       float mask_neg = 0.0f);
 size_t conv_wgrad_workspace(const ConvShape& g, int dtype);
 cudaError_t conv_wgrad(const ConvShape& g, int dtype, const void* x, const void* dy, void* dw, void* ws,
                        size_t ws_bytes, cudaStream_t st);
