@@ -851,13 +851,25 @@ __global__ void anchor_label_kernel(const float* __restrict__ anchors, int nA, c
 
 constexpr int kSampleThreads = 1024;
 
-// one CTA per image: keep <= cap fg by smallest mix64(key, a), then bg to fill `batch`
+// one CTA per image: keep <= cap fg by smallest mix64(key, a), then bg to fill `batch`.
+// Fast path (the usual case, k << flagged count): the hash priorities are
+// uniform, so every element with priority below B = ~(4k + 64) / n_flagged of
+// the 64-bit range is collected into shared memory in one pass (expected
+// ~4k + 64 candidates); if at least k and at most kCandCap arrive, the k
+// smallest (priority, index) among them are exactly the k smallest overall --
+// found by a bitonic sort of the candidates.  Otherwise the exact radix select
+// below runs (same result, more passes).
+constexpr int kCandCap = 2048;
+
 __global__ void __launch_bounds__(kSampleThreads) anchor_sample_kernel(int nA, const uint64_t* __restrict__ keys,
                                                                        int batch, int fg_cap,
                                                                        int8_t* __restrict__ labels) {
     __shared__ int hist[256];
     __shared__ int sh[64];
     __shared__ int tie_list[64];
+    __shared__ unsigned long long cand_key[kCandCap];
+    __shared__ int cand_idx[kCandCap];
+    __shared__ int n_cand;
     const int img = blockIdx.x;
     int8_t* L = labels + static_cast<int64_t>(img) * nA;
     const uint64_t kfg = keys[img];
@@ -871,6 +883,78 @@ __global__ void __launch_bounds__(kSampleThreads) anchor_sample_kernel(int nA, c
             f = L[i] == want;
             return f ? mix64(key, static_cast<uint64_t>(i)) : 0ull;
         };
+        // ---- flagged count
+        int cnt = 0;
+        for (int i = threadIdx.x; i < nA; i += kSampleThreads) cnt += L[i] == want;
+        const int n_flag = block_sum_int<kSampleThreads>(cnt, sh);
+        if (n_flag <= k || k <= 0) {
+            if (k <= 0)
+                for (int i = threadIdx.x; i < nA; i += kSampleThreads)
+                    if (L[i] == want) L[i] = -1;
+            __syncthreads();
+            if (pass == 0) n_fg_kept = k <= 0 ? 0 : n_flag;
+            continue;
+        }
+        // ---- fast path: candidates below the priority bound
+        const double frac = static_cast<double>(4 * k + 64) / static_cast<double>(n_flag);
+        const uint64_t B = frac >= 1.0 ? ~0ull : static_cast<uint64_t>(frac * 18446744073709551616.0);
+        if (threadIdx.x == 0) n_cand = 0;
+        __syncthreads();
+        for (int i = threadIdx.x; i < nA; i += kSampleThreads) {
+            if (L[i] != want) continue;
+            const uint64_t pk = mix64(key, static_cast<uint64_t>(i));
+            if (pk < B) {
+                const int slot = atomicAdd(&n_cand, 1);
+                if (slot < kCandCap) {
+                    cand_key[slot] = pk;
+                    cand_idx[slot] = i;
+                }
+            }
+        }
+        __syncthreads();
+        const int nc = n_cand;
+        if (nc >= k && nc <= kCandCap) {
+            // bitonic sort of (priority, index) ascending over the padded candidate list
+            int np2 = 1;
+            while (np2 < nc) np2 <<= 1;
+            for (int t = nc + threadIdx.x; t < np2; t += kSampleThreads) {
+                cand_key[t] = ~0ull;
+                cand_idx[t] = 0x7fffffff;
+            }
+            __syncthreads();
+            for (int size = 2; size <= np2; size <<= 1) {
+                for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                    for (int t = threadIdx.x; t < np2 / 2; t += kSampleThreads) {
+                        const int lo = 2 * t - (t & (stride - 1));
+                        const int hi = lo + stride;
+                        const bool up = (lo & size) == 0;
+                        const unsigned long long xk = cand_key[lo], yk = cand_key[hi];
+                        const int xi = cand_idx[lo], yi = cand_idx[hi];
+                        const bool gt = xk > yk || (xk == yk && xi > yi);
+                        if (gt == up) {
+                            cand_key[lo] = yk;
+                            cand_key[hi] = xk;
+                            cand_idx[lo] = yi;
+                            cand_idx[hi] = xi;
+                        }
+                    }
+                    __syncthreads();
+                }
+            }
+            // keep exactly the first k: the k-th (priority, index) is the threshold
+            const unsigned long long Tk = cand_key[k - 1];
+            const int Ti = cand_idx[k - 1];
+            for (int i = threadIdx.x; i < nA; i += kSampleThreads) {
+                if (L[i] != want) continue;
+                const uint64_t pk = mix64(key, static_cast<uint64_t>(i));
+                const bool keep = pk < Tk || (pk == Tk && i <= Ti);
+                if (!keep) L[i] = -1;
+            }
+            __syncthreads();
+            if (pass == 0) n_fg_kept = k;
+            continue;
+        }
+        // ---- exact radix select (fallback)
         int n_lt;
         const uint64_t T = block_radix_select<kSampleThreads>(nA, k, keyfn, hist, sh, &n_lt);
         int kept_here;
