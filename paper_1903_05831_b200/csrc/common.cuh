@@ -37,6 +37,19 @@ SDB_DEV void mbar_wait(uint64_t* bar, uint32_t phase) {
         : "memory");
 }
 
+// busy-poll variant (test_wait, no suspend) for latency-critical handshakes
+// between warps of one CTA
+SDB_DEV void mbar_wait_spin(uint64_t* bar, uint32_t phase) {
+    const uint32_t addr = smem_u32(bar);
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "SPIN_%=:\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra SPIN_%=;\n\t}" ::"r"(addr),
+        "r"(phase)
+        : "memory");
+}
+
 // ---------------------------------------------------------------- cp.async
 // 16-byte async copy; src_bytes = 0 zero-fills the destination (padding/OOB).
 SDB_DEV void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {

@@ -645,7 +645,8 @@ __global__ void __launch_bounds__(kScanThreads) nms_scan_kernel(const float* __r
 // of the bulk OR overlap the following decisions instead of serialising them.
 // Same greedy order, same keep list as nms_scan_kernel (deterministic:
 // atomicOr is order-independent).
-constexpr int kScan2Warps = 9;   // warp 0: decisions; warps 1-4: even chunks; 5-8: odd chunks
+constexpr int kScan2GW = 15;     // warps per worker group
+constexpr int kScan2Warps = 1 + 2 * kScan2GW;  // warp 0: decisions; then the even-chunk and odd-chunk groups
 constexpr int kScan2Threads = 32 * kScan2Warps;
 constexpr int kScan2MaxWords = 192;
 
@@ -694,7 +695,7 @@ __global__ void __launch_bounds__(kScan2Threads) nms_scan2_kernel(const float* _
     if (tid == 0) {
         for (int g = 0; g < 2; ++g) {
             mbar_init(&rows_ready[g], 1);
-            mbar_init(&or_done[g], 4);
+            mbar_init(&or_done[g], kScan2GW);
         }
         mbar_fence_init();
     }
@@ -707,7 +708,7 @@ __global__ void __launch_bounds__(kScan2Threads) nms_scan2_kernel(const float* _
             for (; c < nwords; ++c) {
                 const int g = c & 1, it = c >> 1;
                 // bulk OR of chunk c-2 (same worker group) must be in removed[]
-                if (c >= 2) mbar_wait(&or_done[g], (it - 1) & 1);
+                if (c >= 2) mbar_wait_spin(&or_done[g], (it - 1) & 1);
                 const int lim = min(64, k - c * 64);
                 const uint64_t valid = lim >= 64 ? ~0ull : ((1ull << lim) - 1ull);
                 uint64_t w = atomicOr(reinterpret_cast<unsigned long long*>(&removed[c]), 0ull);
@@ -731,7 +732,7 @@ __global__ void __launch_bounds__(kScan2Threads) nms_scan2_kernel(const float* _
                     // release the other group, waiting for chunk c + 1, once it has
                     // finished chunk c - 1
                     const int g2 = g ^ 1, c2 = c + 1;
-                    if (c2 >= 2) mbar_wait(&or_done[g2], ((c2 >> 1) - 1) & 1);
+                    if (c2 >= 2) mbar_wait_spin(&or_done[g2], ((c2 >> 1) - 1) & 1);
                     nrows[g2] = -1;
                     mbar_arrive(&rows_ready[g2]);
                     break;
@@ -741,22 +742,23 @@ __global__ void __launch_bounds__(kScan2Threads) nms_scan2_kernel(const float* _
         }
     } else {
         // ------------------------------------------------ bulk OR workers
-        const int g = (warp - 1) >> 2;           // 0: even chunks, 1: odd chunks
-        const int wt = tid - 32 - g * 128;       // 0..127 within the group
+        const int g = (warp - 1) / kScan2GW;     // 0: even chunks, 1: odd chunks
+        constexpr int GT = 32 * kScan2GW;        // threads per group
+        const int wt = tid - 32 - g * GT;        // 0..GT-1 within the group
         for (int c = g, it = 0;; c += 2, ++it) {
-            mbar_wait(&rows_ready[g], it & 1);
+            mbar_wait_spin(&rows_ready[g], it & 1);
             int nr = nrows[g];
             const bool last = nr < 0;
             if (last) nr = -1 - nr;
             const int w0 = c + 2, nrem = nwords - w0;
             if (nr > 0 && nrem > 0) {
                 const int total = nr * nrem;
-                for (int e0 = wt; e0 < total; e0 += 4 * 128) {
-                    uint64_t v[4];
-                    int wi[4];
+                for (int e0 = wt; e0 < total; e0 += 8 * GT) {
+                    uint64_t v[8];
+                    int wi[8];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int e = e0 + u * 128;
+                    for (int u = 0; u < 8; ++u) {
+                        const int e = e0 + u * GT;
                         v[u] = 0;
                         wi[u] = 0;
                         if (e < total) {
@@ -766,7 +768,7 @@ __global__ void __launch_bounds__(kScan2Threads) nms_scan2_kernel(const float* _
                         }
                     }
 #pragma unroll
-                    for (int u = 0; u < 4; ++u)
+                    for (int u = 0; u < 8; ++u)
                         if (v[u]) atomicOr(reinterpret_cast<unsigned long long*>(&removed[wi[u]]),
                                            static_cast<unsigned long long>(v[u]));
                 }
