@@ -12,8 +12,9 @@ One JSON line on rank 0:
   value  = images/s of the whole job, device-resident inputs (images already in
            HBM, per-step D2D into the step's input buffer), CUDA events on the
            step stream, max over ranks;
-  e2e    = the same metric through the C-ABI host call sdb_det_train_step_host
-           (pinned host images + GT copied H2D, step, losses D2H) every step;
+  e2e    = the same metric through the C-ABI host call sdb_det_train_step_host_nchw
+           (pinned host images in the reference [B][3][H][W] layout + GT copied
+           H2D, step, losses D2H) every step;
   roofline  = the tensor-core implicit-GEMM conv kernels (fprop+dgrad+wgrad,
            FLOP-weighted) from a CUDA-event-instrumented step;
   cpu_baseline = the reference engine's own conv2d (oracle/_ref, compiled from
@@ -347,19 +348,21 @@ def run_ours(args):
     value = world * B * K / (ms_max / 1e3)
 
     # ---------------- end to end through the host C-ABI call
-    host_imgs = make_images(nbuf).cpu().pin_memory()
+    # host images in the reference layout [B][3][H][W] fp16 (pinned): only the 3
+    # real channels cross PCIe, the NHWC8 padding happens on device
+    host_imgs = make_images(nbuf)[..., :3].permute(0, 1, 4, 2, 3).contiguous().cpu().pin_memory()
     gts = []
     for i in range(K + 1):
         slots = D.batch_slots(step_no + 1 + i, rank, world, B)
         gts.append((slots, det.gt_batch(slots)))
     h2d = host_imgs[0].numel() * 2 + sum(a.nbytes for a in gts[0][1]) + 2 * B * 8
     d2h = 4 * 8
-    det.train_step_host(C.c_void_p(host_imgs[0].data_ptr()), gts[0][0], gts[0][1])  # warm
+    det.train_step_host_nchw(C.c_void_p(host_imgs[0].data_ptr()), gts[0][0], gts[0][1])  # warm
     barrier()
     e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2.record(stream)
     for i in range(K):
-        det.train_step_host(C.c_void_p(host_imgs[i % nbuf].data_ptr()), gts[i + 1][0], gts[i + 1][1])
+        det.train_step_host_nchw(C.c_void_p(host_imgs[i % nbuf].data_ptr()), gts[i + 1][0], gts[i + 1][1])
     e3.record(stream)
     barrier()
     ms_e2e = e2.elapsed_time(e3)

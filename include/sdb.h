@@ -184,6 +184,12 @@ int sdb_det_read_losses(sdb_det* det, double* losses5, double* scale_used, int* 
 /* end-to-end call with HOST buffers: H2D of images+GT, the step, D2H of losses */
 int sdb_det_train_step_host(sdb_det* det, const void* images_host, const float* gt_boxes, const int32_t* gt_cls,
                             const int32_t* gt_count, const int64_t* slots, double* losses5);
+/* the same with images in the reference layout [batch][3][H][W] (Tensor NCHW,
+ * src/tensor.cpp; dtype of the detector): only the 3 real channels cross PCIe,
+ * the 8-channel NHWC padding is done on device */
+int sdb_det_train_step_host_nchw(sdb_det* det, const void* images_nchw_host, const float* gt_boxes,
+                                 const int32_t* gt_cls, const int32_t* gt_count, const int64_t* slots,
+                                 double* losses5);
 /* debug/parity exports of the last step's discrete decisions & intermediates.
  * what: 0 anchor labels (int8 [batch][nA]), 1 anchor targets (f32 [batch][nA][4]),
  * 2 proposals (f32 [batch][post][4]), 3 proposal counts (i32 [batch]),

@@ -95,6 +95,8 @@ cudaError_t roialign_fwd(int dtype, const void* feat, int N, int H, int W, int C
                          float scale, int sr, void* out, cudaStream_t st, int step = 1);
 cudaError_t roialign_bwd(int dtype, const void* dy, int N, int H, int W, int C, const float* rois, int R, int P,
                          float scale, int sr, void* dfeat, cudaStream_t st, int step = 1);
+// [n][3][H][W] (the reference image layout) -> NHWC with Cp channels (zero padded)
+cudaError_t nchw3_to_nhwc(int dtype, const void* in, int n, int H, int W, int Cp, void* out, cudaStream_t st);
 cudaError_t maxpool_fwd(int dtype, const void* x, int N, int H, int W, int C, int k, int s, int p, void* y,
                         uint8_t* argmax, cudaStream_t st);
 cudaError_t maxpool_bwd(int dtype, const void* dy, const uint8_t* argmax, int N, int H, int W, int C, int k, int s,

@@ -160,6 +160,7 @@ struct sdb_det {
     int A = 0, A_pad = 0, n_loc = 0, nA = 0, fh = 0, fw = 0, ncls = 0, ncls_pad = 0, nbox_pad = 0;
     int R = 0, P = 0, head_hw = 0, feat_c = 0;
     int roi_step = 1;  // RoIAlign bin subsampling folded from a 1x1 stride-2 head entry
+    void* img3 = nullptr;  // device staging of [N][3][H][W] host images (train_step_host_nchw)
     float* anchors = nullptr;
     // targets
     float* gt = nullptr;
@@ -1147,6 +1148,24 @@ int sdb_det_train_step_host(sdb_det* d, const void* images_host, const float* gt
     try {
         cudaStream_t st = d->ctx->stream;
         CK(cudaMemcpyAsync(d->img.p, images_host, d->img.numel() * d->es, cudaMemcpyHostToDevice, st));
+        stage_gt(d, gt_boxes, gt_cls, gt_count, slots);
+    } catch (const std::exception& e) {
+        return det_fail(SDB_CUDA, e.what());
+    }
+    if (int rc = sdb_det_step(d)) return rc;
+    return sdb_det_read_losses(d, losses5, nullptr, nullptr);
+}
+
+int sdb_det_train_step_host_nchw(sdb_det* d, const void* images_nchw_host, const float* gt_boxes,
+                                 const int32_t* gt_cls, const int32_t* gt_count, const int64_t* slots,
+                                 double* losses5) {
+    try {
+        cudaStream_t st = d->ctx->stream;
+        const size_t bytes = static_cast<size_t>(d->img.n) * 3 * d->img.h * d->img.w * d->es;
+        if (!d->img3) d->img3 = d->alloc(bytes);
+        // only the 3 real channels cross PCIe; the 8-channel padding happens on device
+        CK(cudaMemcpyAsync(d->img3, images_nchw_host, bytes, cudaMemcpyHostToDevice, st));
+        CK(nchw3_to_nhwc(d->dt, d->img3, d->img.n, d->img.h, d->img.w, d->img.c, d->img.p, st));
         stage_gt(d, gt_boxes, gt_cls, gt_count, slots);
     } catch (const std::exception& e) {
         return det_fail(SDB_CUDA, e.what());

@@ -81,6 +81,7 @@ struct StatArgs {
     int C;
     int64_t rows_per_block;
     double* partial;
+    int keep_l2;  // operands small enough to stay in L2 for the apply pass
 };
 
 // Bulk-copy pipeline: a producer lane streams contiguous row tiles (16 KB per
@@ -106,10 +107,12 @@ SDB_DEV int tile_rows_for(int C) {
 
 // producer lane: stream row tiles [r_begin, r_end) of up to three operands
 // into the stage ring
+// hint: 0 default, 1 evict_last (a second pass follows), 2 evict_first (last read)
 template <class T, int NIN, int ST>
 SDB_DEV void stream_tiles(uint32_t sbase, uint64_t* full, uint64_t* empty, const void* a, const void* b,
-                          const void* c, int64_t r_begin, int64_t r_end, int ntiles, int TR, int C) {
+                          const void* c, int64_t r_begin, int64_t r_end, int ntiles, int TR, int C, int hint = 0) {
     const T* src[3] = {static_cast<const T*>(a), static_cast<const T*>(b), static_cast<const T*>(c)};
+    const uint64_t pol = hint == 1 ? l2_evict_last_policy() : (hint == 2 ? l2_evict_first_policy() : 0ull);
     for (int i = 0; i < ntiles; ++i) {
         const int s = i % ST;
         if (i >= ST) mbar_wait(&empty[s], ((i / ST) - 1) & 1);
@@ -118,7 +121,10 @@ SDB_DEV void stream_tiles(uint32_t sbase, uint64_t* full, uint64_t* empty, const
         const uint32_t bytes = static_cast<uint32_t>(nr) * C * sizeof(T);
         mbar_arrive_expect_tx(&full[s], bytes * NIN);
 #pragma unroll
-        for (int j = 0; j < NIN; ++j) bulk_load(sbase + (s * NIN + j) * kTileBytes, src[j] + r0 * C, bytes, &full[s]);
+        for (int j = 0; j < NIN; ++j) {
+            if (hint) bulk_load_hint(sbase + (s * NIN + j) * kTileBytes, src[j] + r0 * C, bytes, &full[s], pol);
+            else bulk_load(sbase + (s * NIN + j) * kTileBytes, src[j] + r0 * C, bytes, &full[s]);
+        }
     }
 }
 
@@ -155,7 +161,8 @@ __global__ void __launch_bounds__(kStatThreads, 2) stats_kernel(StatArgs p) {
     if (warp == kThreads / 32) {
         // ------------------------------------------------ producer
         if (lane == 0)
-            stream_tiles<T, NIN, ST>(sbase, full, empty, p.a, p.dy, p.y, r_begin, r_end, ntiles, TR, C);
+            stream_tiles<T, NIN, ST>(sbase, full, empty, p.a, p.dy, p.y, r_begin, r_end, ntiles, TR, C,
+                                     p.keep_l2 ? 1 : 0);
     } else {
         // ------------------------------------------------ consumers
         float g[8], b[8], mu[8], is[8];
@@ -375,7 +382,7 @@ __global__ void __launch_bounds__(kStatThreads, 2) apply_kernel(ApplyArgs p, int
     pdl_trigger();
     if (warp == kThreads / 32) {
         if (lane == 0)
-            stream_tiles<T, NIN, ST>(smem_u32(sm), full, empty, p.a, p.dy, p.y, r_begin, r_end, ntiles, TR, C);
+            stream_tiles<T, NIN, ST>(smem_u32(sm), full, empty, p.a, p.dy, p.y, r_begin, r_end, ntiles, TR, C, 2);
         return;
     }
     const int tpr = C / 8;
@@ -494,6 +501,9 @@ cudaError_t run_stats(const StatArgs& a0, const Plan& pl, cudaStream_t st) {
     }
     StatArgs a = a0;
     a.rows_per_block = pl.rpb;
+    // the apply pass re-reads the same operands: keep them in L2 when they fit
+    // in well under half of its 126 MB
+    a.keep_l2 = static_cast<double>(a.rows) * a.C * sizeof(T) * NIN <= 48e6 ? 1 : 0;
     return launch_pdl(stats_kernel<T, KIND, NIN>, dim3(pl.nblocks), dim3(kStatThreads), StatPipe<NIN>::kSmem, st, a);
 }
 

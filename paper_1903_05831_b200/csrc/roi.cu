@@ -770,6 +770,23 @@ SDB_DEV uint64_t mix64d(uint64_t a, uint64_t b) {
     return z ^ (z >> 31);
 }
 
+// reference image layout [N][3][H][W] -> device NHWC with channels padded to Cp
+// (zeros), one pixel per thread, one 16-byte store per pixel for fp16/Cp = 8
+template <class T>
+__global__ void nchw3_to_nhwc_kernel(const T* __restrict__ in, int n, int H, int W, int Cp, T* __restrict__ out) {
+    const int64_t hw = static_cast<int64_t>(H) * W, total = static_cast<int64_t>(n) * hw;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t img = e / hw, px = e - img * hw;
+        const T* src = in + img * 3 * hw + px;
+        T* o = out + e * Cp;
+        o[0] = src[0];
+        o[1] = src[hw];
+        o[2] = src[2 * hw];
+        for (int c = 3; c < Cp; ++c) o[c] = from_f<T>(0.f);
+    }
+}
+
 template <class T>
 __global__ void synth_kernel(T* __restrict__ out, int n, int H, int W, int Cp, uint64_t seed,
                              const int64_t* __restrict__ slots, int64_t slot0) {
@@ -1002,6 +1019,15 @@ cudaError_t rcnn_smooth_l1(int dtype, const void* pred, int R, int ld, const int
     else
         rcnn_sl1_kernel<float><<<1, kLossThreads, 0, st>>>(cp<float>(pred), R, ld, labels, targets, beta,
                                                           static_cast<float*>(dp), la.scale, la.loss_out, la.slot);
+    return cudaGetLastError();
+}
+
+cudaError_t nchw3_to_nhwc(int dtype, const void* in, int n, int H, int W, int Cp, void* out, cudaStream_t st) {
+    const int64_t total = static_cast<int64_t>(n) * H * W;
+    if (dtype == kF16)
+        nchw3_to_nhwc_kernel<__half><<<grid_for(total), 256, 0, st>>>(cp<__half>(in), n, H, W, Cp, static_cast<__half*>(out));
+    else
+        nchw3_to_nhwc_kernel<float><<<grid_for(total), 256, 0, st>>>(cp<float>(in), n, H, W, Cp, static_cast<float*>(out));
     return cudaGetLastError();
 }
 

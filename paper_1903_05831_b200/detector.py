@@ -118,6 +118,7 @@ _SIGS = {
     "sdb_det_step": [_P],
     "sdb_det_read_losses": [_P, _P, C.POINTER(_D), C.POINTER(_I)],
     "sdb_det_train_step_host": [_P, _P, _P, _P, _P, _P, _P],
+    "sdb_det_train_step_host_nchw": [_P, _P, _P, _P, _P, _P, _P],
     "sdb_det_export": [_P, _I, _P, _L, C.POINTER(_L)],
     "sdb_det_dims": [_P, C.POINTER(_I), C.POINTER(_I), C.POINTER(_I), C.POINTER(_I)],
     "sdb_det_kernel_launches": [_P, C.POINTER(_L)],
@@ -265,6 +266,14 @@ class Detector:
         out = (_D * 5)()
         slots = np.ascontiguousarray(slots, np.int64)
         check(L().sdb_det_train_step_host(self.h, images_host_ptr, boxes.ctypes.data_as(_P), cls.ctypes.data_as(_P),
+                                          cnt.ctypes.data_as(_P), slots.ctypes.data_as(_P), out))
+        return list(out)
+
+    def train_step_host_nchw(self, images_host_ptr, slots, gt):
+        boxes, cls, cnt = gt
+        out = (_D * 5)()
+        slots = np.ascontiguousarray(slots, np.int64)
+        check(L().sdb_det_train_step_host_nchw(self.h, images_host_ptr, boxes.ctypes.data_as(_P), cls.ctypes.data_as(_P),
                                           cnt.ctypes.data_as(_P), slots.ctypes.data_as(_P), out))
         return list(out)
 

@@ -213,3 +213,30 @@ def test_res5_head_fp32_one_step(ref, orc):
         assert norm_rel(a, b) <= 1e-2, (name, norm_rel(a, b))
     assert norm_rel(g, g_ref) <= 1e-3
     det.close()
+
+
+def test_host_nchw_entry_matches_nhwc8():
+    """sdb_det_train_step_host_nchw (reference [B][3][H][W] images, padded on
+    device) == sdb_det_train_step_host (device layout NHWC8), bit for bit."""
+    import ctypes as C
+    from paper_1903_05831_b200 import detector as D
+    rng = np.random.default_rng(5)
+    p = D.preset("c2", img_h=128, img_w=128)
+    imgs = [rng.standard_normal((p.batch, 3, p.img_h, p.img_w)).astype(np.float16) for _ in range(2)]
+    out = []
+    for use_nchw in (False, True):
+        det = D.Detector(p)
+        for step in (1, 2):
+            slots = D.batch_slots(step, 0, 1, p.batch)
+            x = imgs[step - 1]
+            if use_nchw:
+                buf = np.ascontiguousarray(x)
+                det.train_step_host_nchw(C.c_void_p(buf.ctypes.data), slots, det.gt_batch(slots))
+            else:
+                buf = np.zeros((p.batch, p.img_h, p.img_w, 8), np.float16)
+                buf[..., :3] = x.transpose(0, 2, 3, 1)
+                det.train_step_host(C.c_void_p(buf.ctypes.data), slots, det.gt_batch(slots))
+        out.append((det.losses()[0], dp.flat_params(det)))
+        det.close()
+    assert out[0][0] == out[1][0]
+    assert np.array_equal(out[0][1].view(np.uint32), out[1][1].view(np.uint32))
