@@ -1122,6 +1122,77 @@ __global__ void wgrad_reduce_t_kernel(const float* __restrict__ ws, int splits, 
     }
 }
 
+// All deferred split-K reductions of a backward pass in one launch: CTA b
+// finds its job in the tile prefix table, then reduces one 32x32 tile exactly
+// like wgrad_reduce_t_kernel (transposed jobs) or wgrad_reduce_kernel (plain
+// [K][RSC] partials) -- same per-element summation order (splits in order).
+__global__ void __launch_bounds__(256) wgrad_reduce_batched_kernel(const WgradJob* __restrict__ jobs,
+                                                                  const int* __restrict__ tile_start, int njobs) {
+    __shared__ float tile[32][33];
+    pdl_wait();
+    pdl_trigger();
+    int lo = 0, hi = njobs - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (tile_start[mid] <= static_cast<int>(blockIdx.x)) lo = mid;
+        else hi = mid - 1;
+    }
+    const WgradJob jb = jobs[lo];
+    const int t = blockIdx.x - tile_start[lo];
+    const int tiles_j = (jb.rows + 31) / 32;
+    const int j0 = (t % tiles_j) * 32, i0 = (t / tiles_j) * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int64_t per = static_cast<int64_t>(jb.rows) * jb.cols;
+    // element (j, i) of partial s at ws[s][j][i]: rows j (R*S*C for transposed jobs, K otherwise)
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    const int i = i0 + tx;
+    bool ok[4];
+    int64_t off[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int j = j0 + ty + 8 * u;
+        ok[u] = j < jb.rows && i < jb.cols;
+        off[u] = ok[u] ? static_cast<int64_t>(j) * jb.cols + i : 0;
+    }
+    int k = 0;
+    for (; k + 4 <= jb.splits; k += 4) {
+        float v[4][4];
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[kk][u] = ok[u] ? jb.ws[(k + kk) * per + off[u]] : 0.f;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) acc[u] += v[kk][u];
+    }
+    for (; k < jb.splits; ++k)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc[u] += ok[u] ? jb.ws[k * per + off[u]] : 0.f;
+    __half* dw = static_cast<__half*>(jb.dw);
+    if (jb.transposed) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) tile[ty + 8 * u][tx] = acc[u];
+        __syncthreads();
+        for (int ii = ty; ii < 32; ii += 8) {
+            const int io = i0 + ii, jo = j0 + tx;
+            if (io < jb.cols && jo < jb.rows) dw[static_cast<int64_t>(io) * jb.rows + jo] = __float2half_rn(tile[tx][ii]);
+        }
+    } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (ok[u]) dw[off[u]] = __float2half_rn(acc[u]);
+    }
+}
+
+cudaError_t wgrad_reduce_batched(const WgradJob* jobs_dev, const int* tile_start_dev, int njobs, int total_tiles,
+                                 cudaStream_t st) {
+    if (njobs == 0) return cudaSuccess;
+    return launch_pdl(wgrad_reduce_batched_kernel, dim3(total_tiles), dim3(256), 0, st, jobs_dev, tile_start_dev, njobs);
+}
+
+int wgrad_job_tiles(const WgradJob& j) { return ((j.rows + 31) / 32) * ((j.cols + 31) / 32); }
+
 // zero the dgrad output positions of a phase with no taps
 template <class T>
 __global__ void dgrad_zero_phase_kernel(ConvArgs a) {
@@ -1462,6 +1533,11 @@ size_t conv_wgrad_workspace(const ConvShape& g, int dtype) {
 
 cudaError_t conv_wgrad(const ConvShape& g, int dtype, const void* x, const void* dy, void* dw, void* ws,
                        size_t ws_bytes, cudaStream_t st) {
+    return conv_wgrad_deferred(g, dtype, x, dy, dw, ws, ws_bytes, st, nullptr);
+}
+
+cudaError_t conv_wgrad_deferred(const ConvShape& g, int dtype, const void* x, const void* dy, void* dw, void* ws,
+                                size_t ws_bytes, cudaStream_t st, WgradJob* job) {
     ConvArgs a = make_args(g);
     a.x = x; a.w = dy;
     a.M = g.K;
@@ -1482,6 +1558,10 @@ cudaError_t conv_wgrad(const ConvShape& g, int dtype, const void* x, const void*
         std::swap(at.M, at.NG);  // partials [split][(r,s,c)][k]
         e = launch_tma_pick<WGRAD>(at, splits, st);
         if (e != cudaSuccess) return e;
+        if (job) {
+            *job = WgradJob{static_cast<const float*>(ws), dw, splits, at.M, at.NG, 1};
+            return cudaSuccess;
+        }
         const dim3 grid((at.M + 31) / 32, (at.NG + 31) / 32);
         if (dtype == kF16)
             return launch_pdl(wgrad_reduce_t_kernel<__half>, grid, dim3(256), 0, st, static_cast<const float*>(ws),
@@ -1492,6 +1572,10 @@ cudaError_t conv_wgrad(const ConvShape& g, int dtype, const void* x, const void*
     if (tc) e = launch_tc_pick<WGRAD>(a, splits, st);
     else e = dtype == kF16 ? launch_simt<__half, WGRAD>(a, splits, st) : launch_simt<float, WGRAD>(a, splits, st);
     if (e != cudaSuccess) return e;
+    if (job) {
+        *job = WgradJob{static_cast<const float*>(ws), dw, splits, a.M, a.NG, 0};
+        return cudaSuccess;
+    }
     const int blocks = static_cast<int>(std::min<int64_t>((per + 255) / 256, 8 * kNumSMs));
     if (dtype == kF16)
         return launch_pdl(wgrad_reduce_kernel<__half>, dim3(blocks), dim3(256), 0, st, static_cast<const float*>(ws),

@@ -23,6 +23,7 @@
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <map>
 #include <vector>
 
 #include "../../include/sdb.h"
@@ -160,6 +161,15 @@ struct sdb_det {
     int A = 0, A_pad = 0, n_loc = 0, nA = 0, fh = 0, fw = 0, ncls = 0, ncls_pad = 0, nbox_pad = 0;
     int R = 0, P = 0, head_hw = 0, feat_c = 0;
     int roi_step = 1;  // RoIAlign bin subsampling folded from a 1x1 stride-2 head entry
+    // deferred split-K wgrad reduction (fp16, one rank): every conv keeps its fp32
+    // partials in its own arena slice; one batched reduce before the optimizer
+    bool defer_wgrad = false;
+    uint8_t* wg_arena = nullptr;
+    std::map<int, size_t> wg_off;  // param index -> arena byte offset
+    std::vector<WgradJob> wg_jobs;
+    WgradJob* wg_jobs_dev = nullptr;
+    int* wg_tiles_dev = nullptr;
+    int wg_njobs_dev = 0, wg_total_tiles = 0;
     void* img3 = nullptr;  // device staging of [N][3][H][W] host images (train_step_host_nchw)
     float* anchors = nullptr;
     // targets
@@ -510,7 +520,16 @@ void conv_wgrad_to(Bwd& B, const ConvL& c, const Act& x, const void* dy) {
     {
     PScope ps(d, P_WGRAD, conv_flops(c.g), 0, 2);
     if (d->prof.on) { ps.label = shape_label("wgrad", c.g); ps.flops_ = conv_flops(c.g); }
-    CK(conv_wgrad(c.g, d->dt, x.p, dy, d->gptr(c.p), d->ws, d->ws_bytes, d->ctx->stream));
+    if (d->defer_wgrad) {
+        auto it = d->wg_off.find(c.p);
+        if (it == d->wg_off.end()) throw std::runtime_error("wgrad arena: unknown conv");
+        WgradJob job{};
+        CK(conv_wgrad_deferred(c.g, d->dt, x.p, dy, d->gptr(c.p), d->wg_arena + it->second,
+                               conv_wgrad_workspace(c.g, d->dt), d->ctx->stream, &job));
+        d->wg_jobs.push_back(job);
+    } else {
+        CK(conv_wgrad(c.g, d->dt, x.p, dy, d->gptr(c.p), d->ws, d->ws_bytes, d->ctx->stream));
+    }
     }
     grads_ready(B, c.p);
 }
@@ -689,6 +708,30 @@ void run_step(sdb_det* d) {
         CK(comm_allreduce_sum(d->ctx, d->losses, 4, 3 /* f64 */, d->comm));
         CK(cudaEventRecord(d->ev_join, d->comm));
         CK(cudaStreamWaitEvent(st, d->ev_join, 0));
+    }
+    if (d->defer_wgrad) {
+        // the job table is the same every step (static shapes and buffers):
+        // uploaded once, from the first (eager) step
+        if (!d->wg_jobs_dev) {
+            std::vector<int> start(d->wg_jobs.size());
+            int tot = 0;
+            for (size_t k = 0; k < d->wg_jobs.size(); ++k) {
+                start[k] = tot;
+                tot += wgrad_job_tiles(d->wg_jobs[k]);
+            }
+            d->wg_jobs_dev = static_cast<WgradJob*>(d->alloc(d->wg_jobs.size() * sizeof(WgradJob)));
+            d->wg_tiles_dev = static_cast<int*>(d->alloc(start.size() * sizeof(int)));
+            CK(cudaMemcpy(d->wg_jobs_dev, d->wg_jobs.data(), d->wg_jobs.size() * sizeof(WgradJob),
+                          cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(d->wg_tiles_dev, start.data(), start.size() * sizeof(int), cudaMemcpyHostToDevice));
+            d->wg_njobs_dev = static_cast<int>(d->wg_jobs.size());
+            d->wg_total_tiles = tot;
+        } else if (static_cast<int>(d->wg_jobs.size()) != d->wg_njobs_dev) {
+            throw std::runtime_error("wgrad job table changed between steps");
+        }
+        d->wg_jobs.clear();
+        PScope ps(d, P_WGRAD, 0, 0, 1);
+        CK(wgrad_reduce_batched(d->wg_jobs_dev, d->wg_tiles_dev, d->wg_njobs_dev, d->wg_total_tiles, st));
     }
     PScope ps_opt(d, P_OPTIM, 0, (d->es + 12.0 + (d->dt == kF16 ? 2.0 : 0.0)) * d->n_w + 16.0 * d->n_bn, 5);
     CK(cudaMemsetAsync(d->flag, 0, sizeof(int), st));
@@ -894,6 +937,23 @@ int sdb_det_create(sdb_ctx* ctx, const sdb_det_config* cfgp, sdb_det** out) {
         d->roi_count = static_cast<int32_t*>(d->alloc(b * 4));
         d->ws_bytes = max_ws(d);
         d->ws = d->alloc(d->ws_bytes);
+        d->defer_wgrad = d->dt == kF16 && ctx->world == 1 && std::getenv("SDB_NO_DEFER_WGRAD") == nullptr;
+        if (d->defer_wgrad) {
+            size_t off = 0;
+            auto add = [&](const ConvL& c) {
+                if (c.p < 0 || d->wg_off.count(c.p)) return;
+                d->wg_off[c.p] = off;
+                off += (conv_wgrad_workspace(c.g, d->dt) + 255) & ~size_t(255);
+            };
+            add(d->stem);
+            for (auto* stg : {&d->backbone, &d->head})
+                for (auto& bl : *stg) {
+                    add(bl.c1); add(bl.c2); add(bl.c3);
+                    if (bl.has_down) add(bl.down);
+                }
+            add(d->rpn_conv); add(d->rpn_cls); add(d->rpn_bbox); add(d->fc_cls); add(d->fc_bbox);
+            d->wg_arena = static_cast<uint8_t*>(d->alloc(off));
+        }
         CK(cudaMallocHost(&d->h_gt, static_cast<size_t>(b) * cf.max_gt * 16));
         CK(cudaMallocHost(&d->h_cls, static_cast<size_t>(b) * cf.max_gt * 4));
         CK(cudaMallocHost(&d->h_cnt, b * 4));

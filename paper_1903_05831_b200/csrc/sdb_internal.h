@@ -32,6 +32,20 @@ cudaError_t conv_dgrad(const ConvShape& g, int dtype, const void* dy, const void
 size_t conv_wgrad_workspace(const ConvShape& g, int dtype);
 cudaError_t conv_wgrad(const ConvShape& g, int dtype, const void* x, const void* dy, void* dw, void* ws,
                        size_t ws_bytes, cudaStream_t st);
+// split-K wgrad whose reduction is deferred: the fp32 partials stay in `ws`
+// (which must then not be reused before the batched reduce runs) and the job
+// is described for wgrad_reduce_batched (fp16 gradients only)
+struct WgradJob {
+    const float* ws;
+    void* dw;
+    int splits, rows, cols;  // partials [splits][rows][cols]
+    int transposed;          // 1: rows = R*S*C, cols = K, dw[K][R*S*C] written transposed
+};
+cudaError_t conv_wgrad_deferred(const ConvShape& g, int dtype, const void* x, const void* dy, void* dw, void* ws,
+                                size_t ws_bytes, cudaStream_t st, WgradJob* job);
+cudaError_t wgrad_reduce_batched(const WgradJob* jobs_dev, const int* tile_start_dev, int njobs, int total_tiles,
+                                 cudaStream_t st);
+int wgrad_job_tiles(const WgradJob& j);
 bool conv_force_simt();
 void conv_set_force_simt(bool v);
 
