@@ -1288,7 +1288,12 @@ static cudaError_t launch_tma(ConvArgs a, int splits, cudaStream_t st) {
     }
     const int tiles_m = (a.M + kBM - 1) / kBM, tiles_n = (a.NG + BN - 1) / BN;
     const int n_tiles = tiles_m * tiles_n * splits;
-    const int grid = std::min(n_tiles, Cfg::kPerSM * kNumSMs);
+    int grid = std::min(n_tiles, Cfg::kPerSM * kNumSMs);
+    if (MODE == WGRAD) {
+        // experiment knob: SMs a wgrad may occupy (leaves room for the concurrent norm chain)
+        static const int cap = [] { const char* e = std::getenv("SDB_WGRAD_SMS"); return e ? std::atoi(e) : 0; }();
+        if (cap > 0) grid = std::min(grid, Cfg::kPerSM * cap);
+    }
     TmaPair tm;
     std::memset(&tm, 0, sizeof(tm));
     bool ok;

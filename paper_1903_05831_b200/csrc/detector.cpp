@@ -170,6 +170,17 @@ struct sdb_det {
     WgradJob* wg_jobs_dev = nullptr;
     int* wg_tiles_dev = nullptr;
     int wg_njobs_dev = 0, wg_total_tiles = 0;
+    // the deferred wgrads run on a side stream, overlapping the dgrad -> norm
+    // backward chain; each takes its dz from a ring whose slots are recycled
+    // only after the wgrad that read them has finished
+    static constexpr int kDzRing = 6;
+    bool side_wgrad = false;
+    cudaStream_t wst = nullptr;
+    cudaEvent_t wev_fork = nullptr, wev_join = nullptr;
+    void* dzr[kDzRing] = {};
+    cudaEvent_t dzr_ev[kDzRing] = {};
+    bool dzr_busy[kDzRing] = {};
+    int dzr_next = 0;
     void* img3 = nullptr;  // device staging of [N][3][H][W] host images (train_step_host_nchw)
     float* anchors = nullptr;
     // targets
@@ -498,7 +509,22 @@ struct Bwd {
     sdb_det* d;
     int64_t issued_lo;  // lowest g offset whose bucket has been issued
     size_t next_bucket = 0;
+    bool side = false;  // wgrads on d->wst (not while profiling: per-category events live on the main stream)
+    int slot = -1;      // dz ring slot handed out by dz_buf and not yet consumed by a wgrad
 };
+
+// where the next norm backward writes the dz that a wgrad will read: a ring slot
+// (waiting for the wgrad that last read it) when wgrads run on the side stream
+void* dz_buf(Bwd& B, void* fallback) {
+    sdb_det* d = B.d;
+    if (!B.side) return fallback;
+    const int k = d->dzr_next;
+    d->dzr_next = (k + 1) % sdb_det::kDzRing;
+    if (d->dzr_busy[k]) CK(cudaStreamWaitEvent(d->ctx->stream, d->dzr_ev[k], 0));
+    d->dzr_busy[k] = false;
+    B.slot = k;
+    return d->dzr[k];
+}
 
 void grads_ready(Bwd& B, int pi) {
     sdb_det* d = B.d;
@@ -523,10 +549,21 @@ void conv_wgrad_to(Bwd& B, const ConvL& c, const Act& x, const void* dy) {
     if (d->defer_wgrad) {
         auto it = d->wg_off.find(c.p);
         if (it == d->wg_off.end()) throw std::runtime_error("wgrad arena: unknown conv");
+        cudaStream_t ws = d->ctx->stream;
+        if (B.side) {
+            CK(cudaEventRecord(d->wev_fork, ws));
+            CK(cudaStreamWaitEvent(d->wst, d->wev_fork, 0));
+            ws = d->wst;
+        }
         WgradJob job{};
         CK(conv_wgrad_deferred(c.g, d->dt, x.p, dy, d->gptr(c.p), d->wg_arena + it->second,
-                               conv_wgrad_workspace(c.g, d->dt), d->ctx->stream, &job));
+                               conv_wgrad_workspace(c.g, d->dt), ws, &job));
         d->wg_jobs.push_back(job);
+        if (B.side && B.slot >= 0 && dy == d->dzr[B.slot]) {
+            CK(cudaEventRecord(d->dzr_ev[B.slot], d->wst));
+            d->dzr_busy[B.slot] = true;
+            B.slot = -1;
+        }
     } else {
         CK(conv_wgrad(c.g, d->dt, x.p, dy, d->gptr(c.p), d->ws, d->ws_bytes, d->ctx->stream));
     }
@@ -544,23 +581,28 @@ void block_bwd(Bwd& B, Block& b, const void* dS, void* dx, void* s1, void* s2, c
     sdb_det* d = B.d;
     const float neg = d->cfg.mode == 0 ? 0.0f : d->cfg.slope;
     // shortcut first (its params come last in the block's pack order)
+    void* z;
     if (b.has_down) {
-        norm_bwd(d, b.nd, b.zd, b.d, dS, s1);
-        conv_wgrad_to(B, b.down, b.in, s1);
-        dgrad(d, b.down, s1, dx, 0);
+        z = dz_buf(B, s1);
+        norm_bwd(d, b.nd, b.zd, b.d, dS, z);
+        conv_wgrad_to(B, b.down, b.in, z);
+        dgrad(d, b.down, z, dx, 0);
     }
-    norm_bwd(d, b.n3, b.z3, b.b3, dS, s1);
-    conv_wgrad_to(B, b.c3, b.a2, s1);
-    dgrad(d, b.c3, s1, s2, 0);
-    norm_bwd(d, b.n2, b.z2, b.a2, s2, s1);
-    conv_wgrad_to(B, b.c2, b.a1, s1);
-    dgrad(d, b.c2, s1, s2, 0);
-    norm_bwd(d, b.n1, b.z1, b.a1, s2, s1);
-    conv_wgrad_to(B, b.c1, b.in, s1);
+    z = dz_buf(B, s1);
+    norm_bwd(d, b.n3, b.z3, b.b3, dS, z);
+    conv_wgrad_to(B, b.c3, b.a2, z);
+    dgrad(d, b.c3, z, s2, 0);
+    z = dz_buf(B, s1);
+    norm_bwd(d, b.n2, b.z2, b.a2, s2, z);
+    conv_wgrad_to(B, b.c2, b.a1, z);
+    dgrad(d, b.c2, z, s2, 0);
+    z = dz_buf(B, s1);
+    norm_bwd(d, b.n1, b.z1, b.a1, s2, z);
+    conv_wgrad_to(B, b.c1, b.in, z);
     // residual fan-in in the dgrad epilogue: dx = conv1^T(dz1) + (down-path dx | identity dS),
     // then the previous block's activation mask
-    if (b.has_down) dgrad(d, b.c1, s1, dx, 1, nullptr, in_mask, neg);
-    else dgrad(d, b.c1, s1, dx, 1, dS, in_mask, neg);
+    if (b.has_down) dgrad(d, b.c1, z, dx, 1, nullptr, in_mask, neg);
+    else dgrad(d, b.c1, z, dx, 1, dS, in_mask, neg);
 }
 
 // ------------------------------------------------------------------ the step
@@ -635,6 +677,8 @@ void run_step(sdb_det* d) {
 
     // ---- backward
     Bwd B{d, 0, 0};
+    B.side = d->side_wgrad && !d->prof.on;
+    for (bool& bz : d->dzr_busy) bz = false;  // the previous step joined the side stream
     // fc layers (bbox then cls: reverse pack order)
     void* dpool = d->gbuf[2];
     conv_wgrad_to(B, d->fc_bbox, d->pooled, g1);
@@ -666,7 +710,7 @@ void run_step(sdb_det* d) {
     CK(roialign_bwd(d->dt, cur, d->c4.n, d->c4.h, d->c4.w, d->c4.c, d->rois, d->R, d->P, sscale, cf.sampling_ratio,
                     dc4, st, d->roi_step)); }
     // RPN head backward (bbox, cls, conv)
-    void* drpn = d->gbuf[0];
+    void* drpn = dz_buf(B, d->gbuf[0]);
     conv_wgrad_to(B, d->rpn_bbox, d->rpn_a, d->d_rpn_deltas);
     conv_wgrad_to(B, d->rpn_cls, d->rpn_a, d->d_rpn_logits);
     // the RPN ReLU backward is folded into whichever dgrad writes drpn last (the
@@ -696,8 +740,13 @@ void run_step(sdb_det* d) {
     // maxpool, stem norm, stem wgrad (the image gradient is not needed)
     { PScope ps(d, P_POOL, 0, d->es * (2.0 * d->stem_a.numel() + d->pool.numel()));
     CK(maxpool_bwd(d->dt, cur, d->pool_arg, d->stem_a.n, d->stem_a.h, d->stem_a.w, d->stem_a.c, 3, 2, 1, spare, st)); }
-    norm_bwd(d, d->stem_n, d->stem_z, d->stem_a, spare, d->gbuf[0]);
-    conv_wgrad_to(B, d->stem, d->img, d->gbuf[0]);
+    void* dstem = dz_buf(B, d->gbuf[0]);
+    norm_bwd(d, d->stem_n, d->stem_z, d->stem_a, spare, dstem);
+    conv_wgrad_to(B, d->stem, d->img, dstem);
+    if (B.side) {
+        CK(cudaEventRecord(d->wev_join, d->wst));
+        CK(cudaStreamWaitEvent(st, d->wev_join, 0));
+    }
 
     // ---- data-parallel reduction, overflow check, update
     if (d->ctx->world > 1) {
@@ -953,6 +1002,19 @@ int sdb_det_create(sdb_ctx* ctx, const sdb_det_config* cfgp, sdb_det** out) {
                 }
             add(d->rpn_conv); add(d->rpn_cls); add(d->rpn_bbox); add(d->fc_cls); add(d->fc_bbox);
             d->wg_arena = static_cast<uint8_t*>(d->alloc(off));
+            d->side_wgrad = std::getenv("SDB_NO_SIDE_WGRAD") == nullptr;
+        }
+        if (d->side_wgrad) {
+            int lo = 0, hi = 0;
+            CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            // lower priority than the main stream's dgrad/norm chain (the critical path)
+            CK(cudaStreamCreateWithPriority(&d->wst, cudaStreamNonBlocking, lo));
+            CK(cudaEventCreateWithFlags(&d->wev_fork, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&d->wev_join, cudaEventDisableTiming));
+            for (int k = 0; k < sdb_det::kDzRing; ++k) {
+                d->dzr[k] = d->alloc(static_cast<size_t>(d->gbuf_elems) * d->es);
+                CK(cudaEventCreateWithFlags(&d->dzr_ev[k], cudaEventDisableTiming));
+            }
         }
         CK(cudaMallocHost(&d->h_gt, static_cast<size_t>(b) * cf.max_gt * 16));
         CK(cudaMallocHost(&d->h_cls, static_cast<size_t>(b) * cf.max_gt * 4));
@@ -1003,6 +1065,12 @@ int sdb_det_destroy(sdb_det* d) {
     cudaFreeHost(d->h_slots);
     cudaFreeHost(d->h_losses);
     for (auto e : d->bucket_ev) cudaEventDestroy(e);
+    if (d->wst) {
+        for (auto e : d->dzr_ev) cudaEventDestroy(e);
+        cudaEventDestroy(d->wev_fork);
+        cudaEventDestroy(d->wev_join);
+        cudaStreamDestroy(d->wst);
+    }
     if (d->comm) {
         cudaEventDestroy(d->ev_fork);
         cudaEventDestroy(d->ev_join);
