@@ -118,7 +118,7 @@ struct Prof {
     size_t used = 0;
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> recs;
     std::vector<std::string> labels;
-    std::vector<double> rec_flops;
+    std::vector<double> rec_flops, rec_bytes;
     double flops[P_NCAT] = {}, bytes[P_NCAT] = {};
     int64_t launches[P_NCAT] = {};
     cudaEvent_t get() {
@@ -304,9 +304,10 @@ struct PScope {
         d->prof.recs.push_back({cat, {e0, e1}});
         d->prof.labels.push_back(label);
         d->prof.rec_flops.push_back(flops_);
+        d->prof.rec_bytes.push_back(bytes_);
     }
     std::string label;
-    double flops_ = 0;
+    double flops_ = 0, bytes_ = 0;
 };
 
 std::string shape_label(const char* what, const ConvShape& g) {
@@ -442,6 +443,10 @@ void conv_fwd(sdb_det* d, const ConvL& c, const Act& x, const Act& y) {
 void norm_fwd(sdb_det* d, const NormL& n, const Act& z, const Act& a) {
     const int64_t rows = static_cast<int64_t>(z.n) * z.h * z.w;
     PScope ps(d, P_NORM_F, 0, 2.0 * d->es * z.numel(), 3);
+    if (d->prof.on && std::getenv("SDB_PROFILE_VERBOSE")) {
+        ps.label = "norm_fwd rows " + std::to_string(rows) + " C " + std::to_string(n.C);
+        ps.bytes_ = 3.0 * d->es * z.numel();
+    }
     CK(bn_forward(d->dt, z.p, d->bnp(n.pg), d->bnp(n.pb), a.p, n.mean, n.invstd, rows, n.C, d->cfg.eps, n.act,
                   n.slope, d->ws, d->ctx->stream));
 }
@@ -450,6 +455,10 @@ void norm_fwd(sdb_det* d, const NormL& n, const Act& z, const Act& a) {
 void norm_bwd(sdb_det* d, const NormL& n, const Act& z, const Act& a, const void* da, void* dz) {
     const int64_t rows = static_cast<int64_t>(z.n) * z.h * z.w;
     PScope ps(d, P_NORM_B, 0, 3.0 * d->es * z.numel(), 3);
+    if (d->prof.on && std::getenv("SDB_PROFILE_VERBOSE")) {
+        ps.label = "norm_bwd rows " + std::to_string(rows) + " C " + std::to_string(n.C);
+        ps.bytes_ = 5.0 * d->es * z.numel();
+    }
     if (d->cfg.mode == 0) {
         CK(bn_backward(d->dt, da, z.p, n.act == 1 ? a.p : nullptr, d->bnp(n.pg), n.mean, n.invstd, dz,
                        d->bngp(n.pg), d->bngp(n.pb), rows, n.C, d->ws, d->ctx->stream));
@@ -472,6 +481,10 @@ void block_fwd(sdb_det* d, Block& b) {
         const int64_t rows = static_cast<int64_t>(b.z3.n) * b.z3.h * b.z3.w;
         {
             PScope ps(d, P_NORM_F, 0, 1.0 * d->es * b.z3.numel(), 2);
+            if (d->prof.on && std::getenv("SDB_PROFILE_VERBOSE")) {
+                ps.label = "norm_stats3 rows " + std::to_string(rows) + " C " + std::to_string(b.n3.C);
+                ps.bytes_ = 1.0 * d->es * b.z3.numel();
+            }
             CK(bn_forward_stats(d->dt, b.z3.p, b.n3.mean, b.n3.invstd, rows, b.n3.C, d->cfg.eps, b.n3.act, d->ws,
                                 d->ctx->stream));
         }
@@ -482,6 +495,10 @@ void block_fwd(sdb_det* d, Block& b) {
             sc = &b.d;
         }
         PScope ps(d, P_NORM_F, 0, 4.0 * d->es * b.out.numel());
+        if (d->prof.on && std::getenv("SDB_PROFILE_VERBOSE")) {
+            ps.label = "norm_apply_add rows " + std::to_string(rows) + " C " + std::to_string(b.n3.C);
+            ps.bytes_ = 4.0 * d->es * b.out.numel();
+        }
         CK(bn_apply_add_act(d->dt, b.z3.p, d->bnp(b.n3.pg), d->bnp(b.n3.pb), b.n3.mean, b.n3.invstd, b.b3.p, sc->p,
                             b.out.p, rows, b.n3.C, b.n3.slope, 2, d->cfg.slope, d->ctx->stream));
         return;
@@ -1353,6 +1370,7 @@ int sdb_det_profile(sdb_det* d, double* ms, double* flops, double* bytes, int64_
         p.recs.clear();
         p.labels.clear();
         p.rec_flops.clear();
+        p.rec_bytes.clear();
         std::fill(p.flops, p.flops + P_NCAT, 0.0);
         std::fill(p.bytes, p.bytes + P_NCAT, 0.0);
         std::fill(p.launches, p.launches + P_NCAT, 0);
@@ -1368,11 +1386,12 @@ int sdb_det_profile(sdb_det* d, double* ms, double* flops, double* bytes, int64_
             CK(cudaEventElapsedTime(&t, r.second.first, r.second.second));
             acc[r.first] += t;
             if (verbose && !p.labels[k].empty())
-                std::fprintf(stderr, "[sdb-prof] %-60s %8.1f us %7.0f TF/s\n", p.labels[k].c_str(), t * 1e3,
-                             p.rec_flops[k] / (t * 1e-3) / 1e12);
+                std::fprintf(stderr, "[sdb-prof] %-60s %8.1f us %7.0f TF/s %7.0f GB/s\n", p.labels[k].c_str(),
+                             t * 1e3, p.rec_flops[k] / (t * 1e-3) / 1e12, p.rec_bytes[k] / (t * 1e-3) / 1e9);
         }
         p.labels.clear();
         p.rec_flops.clear();
+        p.rec_bytes.clear();
         for (int i = 0; i < ncat && i < P_NCAT; ++i) {
             if (ms) ms[i] = acc[i];
             if (flops) flops[i] = p.flops[i];

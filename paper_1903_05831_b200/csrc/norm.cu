@@ -230,14 +230,15 @@ __global__ void __launch_bounds__(kStatThreads, 2) stats_kernel(StatArgs p) {
         }
     }
     // every stage has been consumed (all bulk copies landed): reuse the ring
-    // as the fixed-order block reduction buffer
+    // as the fixed-order block reduction buffer, laid out [value][thread] so a
+    // warp's stores and loads hit consecutive banks
     __syncthreads();
     double* red = reinterpret_cast<double*>(sm);
-    if (tid < kThreads) {
+    if (tid < kThreads && rg != 0) {
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-            red[tid * 16 + j] = S[j];
-            red[tid * 16 + 8 + j] = Q[j];
+            red[j * kThreads + tid] = S[j];
+            red[(8 + j) * kThreads + tid] = Q[j];
         }
     }
     __syncthreads();
@@ -246,8 +247,8 @@ __global__ void __launch_bounds__(kStatThreads, 2) stats_kernel(StatArgs p) {
             const int t = k * tpr + cg;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-                S[j] += red[t * 16 + j];
-                Q[j] += red[t * 16 + 8 + j];
+                S[j] += red[j * kThreads + t];
+                Q[j] += red[(8 + j) * kThreads + t];
             }
         }
         double* out = p.partial + static_cast<int64_t>(blockIdx.x) * 2 * C;
@@ -261,44 +262,69 @@ __global__ void __launch_bounds__(kStatThreads, 2) stats_kernel(StatArgs p) {
 
 // MODE 0: BN fwd (sums rounded to float first), 1: IABN fwd (double)
 // MODE 2: BN bwd, 3: IABN bwd  -> coef[0..C) = s1/m, coef[C..2C) = s2/m
-// Fixed-order parallel reduction of the per-block partials: thread (cx, ry)
-// of a 32x32 block sums partial[b][c] for b = ry, ry+32, ... (coalesced across
-// cx, 4 independent loads in flight); the 32 row sums are then added in order.
-// Deterministic, no atomics.
-__global__ void __launch_bounds__(1024) finalize_kernel(const double* __restrict__ partial, int nblocks, int C,
-                                                        int64_t count, float eps, int mode, float* mean, float* invstd,
-                                                        float* dgamma, float* dbeta, float* coef) {
-    __shared__ double rs[32][33], rq[32][33];
+// Fixed-order parallel reduction of the per-block partials, spread over many
+// SMs (8 channels per CTA): thread (ch, g) of 128 groups loads partial[b][c] for
+// b = g, g+128, g+256 in one L2 round trip and adds them in block order; the
+// 128 group sums are combined by a fixed tree (shuffles inside a warp, then the
+// 32 warp sums through shared memory).  Deterministic, no atomics.
+constexpr int kFinCh = 8;
+constexpr int kFinThreads = 1024;
+constexpr int kFinGroups = kFinThreads / kFinCh;
+__global__ void __launch_bounds__(kFinThreads) finalize_kernel(const double* __restrict__ partial, int nblocks, int C,
+                                                               int64_t count, float eps, int mode, float* mean,
+                                                               float* invstd, float* dgamma, float* dbeta,
+                                                               float* coef) {
+    __shared__ double rs[32][kFinCh], rq[32][kFinCh];
     pdl_wait();
     pdl_trigger();
-    const int cx = threadIdx.x & 31, ry = threadIdx.x >> 5;
-    const int c = blockIdx.x * 32 + cx;
-    double S = 0.0, Q = 0.0;
+    const int ch = threadIdx.x % kFinCh, g = threadIdx.x / kFinCh;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int c = blockIdx.x * kFinCh + ch;
+    // -0.0 is the exact additive identity (keeps the sign of an all -0 sum)
+    double S = -0.0, Q = -0.0;
     if (c < C) {
         const int64_t stride = 2 * static_cast<int64_t>(C);
-        int b = ry;
-        for (; b + 96 < nblocks; b += 128) {
-            const double* p0 = partial + b * stride + c;
-            const double s0 = p0[0], s1 = p0[32 * stride], s2 = p0[64 * stride], s3 = p0[96 * stride];
-            const double q0 = p0[C], q1 = p0[32 * stride + C], q2 = p0[64 * stride + C], q3 = p0[96 * stride + C];
-            S += s0; S += s1; S += s2; S += s3;
-            Q += q0; Q += q1; Q += q2; Q += q3;
+        constexpr int kPer = (kMaxBlocks + kFinGroups - 1) / kFinGroups;
+        double sv[kPer], qv[kPer];
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+            const int b = g + kFinGroups * u;
+            sv[u] = b < nblocks ? partial[b * stride + c] : -0.0;
+            qv[u] = b < nblocks ? partial[b * stride + C + c] : -0.0;
         }
-        for (; b < nblocks; b += 32) {
-            S += partial[b * stride + c];
-            Q += partial[b * stride + C + c];
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+            S += sv[u];
+            Q += qv[u];
         }
     }
-    rs[ry][cx] = S;
-    rq[ry][cx] = Q;
+    // groups 4w..4w+3 of warp w: fixed pairwise tree
+#pragma unroll
+    for (int o = kFinCh; o < 32; o <<= 1) {
+        S += __shfl_xor_sync(0xffffffffu, S, o);
+        Q += __shfl_xor_sync(0xffffffffu, Q, o);
+    }
+    if (lane < kFinCh) {
+        rs[warp][lane] = S;
+        rq[warp][lane] = Q;
+    }
     __syncthreads();
-    if (ry != 0 || c >= C) return;
-    S = 0.0;
-    Q = 0.0;
-    for (int k = 0; k < 32; ++k) {
-        S += rs[k][cx];
-        Q += rq[k][cx];
+    if (warp != 0) return;
+    // lane = (ch, quarter): 4 quarters of 8 warp sums each, then a 2-level tree
+    const int qtr = lane / kFinCh;
+    S = -0.0;
+    Q = -0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        S += rs[qtr * 8 + k][ch];
+        Q += rq[qtr * 8 + k][ch];
     }
+#pragma unroll
+    for (int o = kFinCh; o < 32; o <<= 1) {
+        S += __shfl_xor_sync(0xffffffffu, S, o);
+        Q += __shfl_xor_sync(0xffffffffu, Q, o);
+    }
+    if (lane >= kFinCh || c >= C) return;
     if (mode == 0 || mode == 1) {
         double mu, var;
         if (mode == 0) {
@@ -521,7 +547,7 @@ cudaError_t run_apply(const ApplyArgs& aa, int64_t rows, const Plan& pl, cudaStr
 
 void finalize(const double* partial, const Plan& pl, int C, int64_t rows, float eps, int mode, float* mean,
               float* invstd, float* dgamma, float* dbeta, float* coef, cudaStream_t st) {
-    launch_pdl(finalize_kernel, dim3((C + 31) / 32), dim3(1024), 0, st, partial, pl.nblocks, C, rows, eps, mode, mean,
+    launch_pdl(finalize_kernel, dim3((C + kFinCh - 1) / kFinCh), dim3(kFinThreads), 0, st, partial, pl.nblocks, C, rows, eps, mode, mean,
                invstd, dgamma, dbeta, coef);
 }
 
