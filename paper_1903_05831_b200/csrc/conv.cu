@@ -26,6 +26,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include <cuda.h>
 
@@ -514,9 +515,10 @@ SDB_DEV void tmem_ld_cols<16>(uint32_t taddr, uint32_t (&v)[16]) { tmem_ld16(tad
 template <>
 SDB_DEV void tmem_ld_cols<32>(uint32_t taddr, uint32_t (&v)[32]) { tmem_ld32(taddr, v); }
 
-template <int MODE, int NCOL, int SC>
+template <int MODE, int NCOL, int SC, bool ADD, bool MSK>
 SDB_DEV void epilogue_tile_v2(const ConvArgs& a, int split, int m0, int n0, int nk, uint32_t tacc, int q, int lane,
-                              int c_lo, float* stg, uint64_t* tempty_acc) {
+                              int c_lo, float* stg, uint64_t* tfull_acc, uint32_t tfull_phase, uint64_t* tempty_acc) {
+    constexpr int NSTEP = NCOL / SC;
     constexpr int LPR = SC / 8;        // lanes per row in the store phase
     constexpr int NK = LPR;            // store rows per lane = 32 / (32 / LPR)
     constexpr int SLOTS = SC / 4;      // 16-byte slots per staged row
@@ -530,9 +532,14 @@ SDB_DEV void epilogue_tile_v2(const ConvArgs& a, int split, int m0, int n0, int 
             if (MODE == FPROP) {
                 o = static_cast<int64_t>(grow) * a.NG;
             } else if (MODE == DGRAD) {
-                const int HpWp = a.Hp * a.Wp;
-                const int n = grow / HpWp, rem = grow - n * HpWp, i2 = rem / a.Wp, j2 = rem - i2 * a.Wp;
-                o = ((static_cast<int64_t>(n) * a.H + a.ph + a.stride * i2) * a.W + a.pw + a.stride * j2) * a.C;
+                if (a.stride == 1) {
+                    // one phase covering the whole input grid: GEMM row = input pixel
+                    o = static_cast<int64_t>(grow) * a.C;
+                } else {
+                    const int HpWp = a.Hp * a.Wp;
+                    const int n = grow / HpWp, rem = grow - n * HpWp, i2 = rem / a.Wp, j2 = rem - i2 * a.Wp;
+                    o = ((static_cast<int64_t>(n) * a.H + a.ph + a.stride * i2) * a.W + a.pw + a.stride * j2) * a.C;
+                }
             } else {
                 o = (static_cast<int64_t>(split) * a.M + grow) * a.NG;
             }
@@ -541,10 +548,13 @@ SDB_DEV void epilogue_tile_v2(const ConvArgs& a, int split, int m0, int n0, int 
     }
     const int lim = MODE == DGRAD ? a.C : a.NG;
     const bool vec = MODE == WGRAD ? (lim & 3) == 0 : (lim & 7) == 0;
-    const bool add = MODE == DGRAD && a.accumulate;
-    const bool msk = MODE == DGRAD && a.mask != nullptr;
+    constexpr bool add = MODE == DGRAD && ADD;
+    constexpr bool msk = MODE == DGRAD && MSK;
     const int c8 = lane % LPR;
-    uint4 addv[NK], addn[NK], mskv[NK], mskn[NK];
+    // dgrad residual addend / activation mask: a 3-deep register ring over the
+    // (fully unrolled) column steps, two steps loaded ahead; the first two are
+    // issued before the accumulator is even ready
+    uint4 addb[3][NK], mskb[3][NK];
     auto load_vec = [&](const void* src, uint4 (&dst)[NK], int cb) {
         const int col = n0 + c_lo + cb + c8 * 8;
 #pragma unroll
@@ -554,12 +564,21 @@ SDB_DEV void epilogue_tile_v2(const ConvArgs& a, int split, int m0, int n0, int 
                 dst[k] = *reinterpret_cast<const uint4*>(static_cast<const __half*>(src) + rowp[k] + col);
         }
     };
-    if (add) load_vec(a.addend, addv, 0);
-    if (msk) load_vec(a.mask, mskv, 0);
-#pragma unroll 1
-    for (int cb = 0; cb < NCOL; cb += SC) {
-        if (add && cb + SC < NCOL) load_vec(a.addend, addn, cb + SC);
-        if (msk && cb + SC < NCOL) load_vec(a.mask, mskn, cb + SC);
+    auto prefetch = [&](int js) {
+        if (js >= NSTEP) return;
+        if (add) load_vec(a.addend, addb[js % 3], js * SC);
+        if (msk) load_vec(a.mask, mskb[js % 3], js * SC);
+    };
+    prefetch(0);
+    prefetch(1);
+    mbar_wait(tfull_acc, tfull_phase);
+    tc_fence_after();
+#pragma unroll
+    for (int js = 0; js < NSTEP; ++js) {
+        const int cb = js * SC;
+        prefetch(js + 2);
+        const uint4* addv = addb[js % 3];
+        const uint4* mskv = mskb[js % 3];
         uint32_t v[SC];
         tmem_ld_cols<SC>(tacc + (static_cast<uint32_t>(q * 32) << 16) + c_lo + cb, v);
         if (cb + SC >= NCOL) {
@@ -629,7 +648,7 @@ SDB_DEV void epilogue_tile_v2(const ConvArgs& a, int split, int m0, int n0, int 
                     for (int e = 0; e < 8 && col + e < lim; ++e) {
                         float x = f[e];
                         if (add) x += __half2float(static_cast<const __half*>(a.addend)[rowp[k] + col + e]);
-                        if (MODE == DGRAD && a.mask) {
+                        if (msk) {
                             x = __half2float(__float2half_rn(x));
                             if (!(__half2float(static_cast<const __half*>(a.mask)[rowp[k] + col + e]) > 0.f))
                                 x = __fmul_rn(a.mask_neg, x);
@@ -640,14 +659,6 @@ SDB_DEV void epilogue_tile_v2(const ConvArgs& a, int split, int m0, int n0, int 
             }
         }
         __syncwarp();
-        if (add) {
-#pragma unroll
-            for (int k = 0; k < NK; ++k) addv[k] = addn[k];
-        }
-        if (msk) {
-#pragma unroll
-            for (int k = 0; k < NK; ++k) mskv[k] = mskn[k];
-        }
     }
 }
 
@@ -915,16 +926,25 @@ __global__ void __launch_bounds__(TmaCfg<MODE, BN, ST>::kThreads, (BN <= 128) ? 
         const int ew = warp - 2;
         float* stg = staging + ew * 32 * Cfg::kSC;
         const int c_lo = (ew / 4) * kNCol;
-        int lt = 0;
-        for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++lt) {
-            int m0, n0, kb0, nk;
-            tile_coords(t, m0, n0, kb0, nk);
-            const int acc = lt & 1;
-            mbar_wait(&tfull[acc], (lt >> 1) & 1);
-            tc_fence_after();
-            epilogue_tile_v2<MODE, kNCol, Cfg::kSC>(a, t / (tiles_m * tiles_n), m0, n0, nk, tmem + acc * BN, warp & 3,
-                                                   lane, c_lo, stg, &tempty[acc]);
-        }
+        // the dgrad residual addend / activation mask are compile-time variants
+        // (a lean epilogue is what keeps these warps ahead of the stores)
+        auto run = [&](auto add_c, auto msk_c) {
+            int lt = 0;
+            for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++lt) {
+                int m0, n0, kb0, nk;
+                tile_coords(t, m0, n0, kb0, nk);
+                const int acc = lt & 1;
+                epilogue_tile_v2<MODE, kNCol, Cfg::kSC, decltype(add_c)::value, decltype(msk_c)::value>(
+                    a, t / (tiles_m * tiles_n), m0, n0, nk, tmem + acc * BN, warp & 3, lane, c_lo, stg, &tfull[acc],
+                    (lt >> 1) & 1, &tempty[acc]);
+            }
+        };
+        using T_ = std::true_type;
+        using F_ = std::false_type;
+        if (MODE == DGRAD && a.accumulate && a.mask) run(T_{}, T_{});
+        else if (MODE == DGRAD && a.accumulate) run(T_{}, F_{});
+        else if (MODE == DGRAD && a.mask) run(F_{}, T_{});
+        else run(F_{}, F_{});
     }
     tc_fence_before();
     __syncthreads();
