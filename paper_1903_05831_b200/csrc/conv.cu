@@ -515,6 +515,31 @@ SDB_DEV void tmem_ld_cols<16>(uint32_t taddr, uint32_t (&v)[16]) { tmem_ld16(tad
 template <>
 SDB_DEV void tmem_ld_cols<32>(uint32_t taddr, uint32_t (&v)[32]) { tmem_ld32(taddr, v); }
 
+// f32 + f16 -> f32 with one rounding (sm_100 mixed-precision add)
+SDB_DEV float fadd_f16(uint16_t h, float c) {
+    float r;
+    asm("add.rn.f32.f16 %0, %1, %2;" : "=f"(r) : "h"(h), "f"(c));
+    return r;
+}
+SDB_DEV uint32_t pack_half2(float lo, float hi) {
+    const __half2 h = __floats2half2_rn(lo, hi);
+    return *reinterpret_cast<const uint32_t*>(&h);
+}
+// backward of the leaky / ReLU that produced y, on a pair of rounded fp16
+// gradients p: y > 0 ? p : rn16(f32(p) * neg)  (neg2 = neg in both halves of a
+// f32x2), exactly the scalar float expression, in 5 instructions per pair
+SDB_DEV uint32_t leaky_mask_half2(uint32_t p, uint32_t y, uint64_t neg2) {
+    const __half2 ph = *reinterpret_cast<const __half2*>(&p);
+    const float2 pf = __half22float2(ph);
+    const uint64_t pf2 = static_cast<uint64_t>(__float_as_uint(pf.x)) |
+                         (static_cast<uint64_t>(__float_as_uint(pf.y)) << 32);
+    uint64_t q2;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(q2) : "l"(pf2), "l"(neg2));
+    const uint32_t q = pack_half2(__uint_as_float(static_cast<uint32_t>(q2)), __uint_as_float(static_cast<uint32_t>(q2 >> 32)));
+    const uint32_t m = __hgt2_mask(*reinterpret_cast<const __half2*>(&y), __float2half2_rn(0.f));
+    return (p & m) | (q & ~m);
+}
+
 template <int MODE, int NCOL, int SC, bool ADD, bool MSK>
 SDB_DEV void epilogue_tile_v2(const ConvArgs& a, int split, int m0, int n0, int nk, uint32_t tacc, int q, int lane,
                               int c_lo, float* stg, uint64_t* tfull_acc, uint32_t tfull_phase, uint64_t* tempty_acc) {
@@ -569,6 +594,7 @@ SDB_DEV void epilogue_tile_v2(const ConvArgs& a, int split, int m0, int n0, int 
         if (add) load_vec(a.addend, addb[js % 3], js * SC);
         if (msk) load_vec(a.mask, mskb[js % 3], js * SC);
     };
+    const uint64_t neg2 = static_cast<uint64_t>(__float_as_uint(a.mask_neg)) * 0x100000001ull;
     prefetch(0);
     prefetch(1);
     mbar_wait(tfull_acc, tfull_phase);
@@ -625,25 +651,21 @@ SDB_DEV void epilogue_tile_v2(const ConvArgs& a, int split, int m0, int n0, int 
             } else {
                 __half* o = static_cast<__half*>(a.out) + rowp[k] + col;
                 if (col + 8 <= lim && vec) {
-                    if (add) {
-                        const __half* oh = reinterpret_cast<const __half*>(&addv[k]);
+                    // per pair: s = acc + addend (mixed-precision add, one rounding),
+                    // p = rn16(s); masked: out = y > 0 ? p : rn16(f32(p) * neg)
+                    uint32_t pk[4];
 #pragma unroll
-                        for (int e = 0; e < 8; ++e) f[e] += __half2float(oh[e]);
-                    }
-                    uint4 pk;
-                    __half2* p2 = reinterpret_cast<__half2*>(&pk);
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) p2[e] = __floats2half2_rn(f[2 * e], f[2 * e + 1]);
-                    if (msk) {
-                        const __half2* m2 = reinterpret_cast<const __half2*>(&mskv[k]);
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const float2 gv = __half22float2(p2[e]), yv = __half22float2(m2[e]);
-                            p2[e] = __floats2half2_rn(yv.x > 0.f ? gv.x : __fmul_rn(a.mask_neg, gv.x),
-                                                      yv.y > 0.f ? gv.y : __fmul_rn(a.mask_neg, gv.y));
+                    for (int e = 0; e < 4; ++e) {
+                        float s0 = f[2 * e], s1 = f[2 * e + 1];
+                        if (add) {
+                            const uint32_t h2 = reinterpret_cast<const uint32_t*>(&addv[k])[e];
+                            s0 = fadd_f16(static_cast<uint16_t>(h2 & 0xffffu), s0);
+                            s1 = fadd_f16(static_cast<uint16_t>(h2 >> 16), s1);
                         }
+                        pk[e] = pack_half2(s0, s1);
+                        if (msk) pk[e] = leaky_mask_half2(pk[e], reinterpret_cast<const uint32_t*>(&mskv[k])[e], neg2);
                     }
-                    *reinterpret_cast<uint4*>(o) = pk;
+                    *reinterpret_cast<uint4*>(o) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
                 } else {
                     for (int e = 0; e < 8 && col + e < lim; ++e) {
                         float x = f[e];
