@@ -61,6 +61,7 @@ struct ConvArgs {
     float mask_neg;
     int tma_b;       // dgrad: filter operand loaded by TMA (needs K % 64 == 0)
     int plain;       // 1x1 / stride 1 / pad 0: the activation operand is a plain 2-D [pixels][channels] tile
+    int tma_out;     // fp16 output written by TMA stores from swizzled staging (tm.o)
 };
 
 // TMA descriptors of the dense GEMM operand (filter for fprop/dgrad, DY for wgrad)
@@ -684,6 +685,58 @@ SDB_DEV void epilogue_tile_v2(const ConvArgs& a, int split, int m0, int n0, int 
     }
 }
 
+// Epilogue v3 (fp16 output through TMA stores): the warp's TMEM lane quadrant
+// is read with tcgen05.ld (lane = tile row, SC consecutive columns), packed to
+// fp16 in registers and written row-per-lane into a swizzled staging box
+// (SWIZZLE_64B for 64-byte rows, SWIZZLE_32B for 32-byte rows: conflict-free),
+// which one lane hands to the TMA engine (cp.async.bulk.tensor store).  Two
+// staging boxes per warp alternate, so the store of step j overlaps step j+1;
+// partial tiles are clipped by the tensor map bounds.
+template <int NCOL, int SC>
+SDB_DEV void epilogue_tile_tmastore(const CUtensorMap* omap, int m0, int n0, int nk, uint32_t tacc, int q, int lane,
+                                    int c_lo, uint8_t* stg, uint64_t* tfull_acc, uint32_t tfull_phase,
+                                    uint64_t* tempty_acc, int& sb) {
+    constexpr int NSTEP = NCOL / SC;
+    constexpr int ROWB = SC * 2;
+    constexpr int BUFB = 32 * ROWB;
+    mbar_wait(tfull_acc, tfull_phase);
+    tc_fence_after();
+#pragma unroll
+    for (int js = 0; js < NSTEP; ++js) {
+        uint32_t v[SC];
+        tmem_ld_cols<SC>(tacc + (static_cast<uint32_t>(q * 32) << 16) + c_lo + js * SC, v);
+        if (js == NSTEP - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tempty_acc);
+        }
+        if (nk == 0) {
+#pragma unroll
+            for (int j = 0; j < SC; ++j) v[j] = 0u;
+        }
+        // the box about to be overwritten was handed to the TMA two steps ago
+        if (lane == 0) bulk_wait_read<1>();
+        __syncwarp();
+        uint8_t* buf = stg + sb * BUFB;
+#pragma unroll
+        for (int j = 0; j < SC / 8; ++j) {
+            const uint4 pk = make_uint4(pack_half2(__uint_as_float(v[8 * j]), __uint_as_float(v[8 * j + 1])),
+                                        pack_half2(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3])),
+                                        pack_half2(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5])),
+                                        pack_half2(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7])));
+            const int pj = SC == 32 ? (j ^ ((lane >> 1) & 3)) : (j ^ ((lane >> 2) & 1));
+            *reinterpret_cast<uint4*>(buf + lane * ROWB + pj * 16) = pk;
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+            tma_store_2d(omap, smem_u32(buf), n0 + c_lo + js * SC, m0 + q * 32);
+            bulk_commit();
+        }
+        sb ^= 1;
+    }
+}
+
 // ============================================================ all-TMA tcgen05 kernel
 // Both operands arrive by TMA, the activation side through the im2col mode of
 // cp.async.bulk.tensor (the hardware walks the output-pixel traversal of the
@@ -704,6 +757,7 @@ SDB_DEV void epilogue_tile_v2(const ConvArgs& a, int split, int m0, int n0, int 
 // warps 2-5: epilogue (TMEM lane quadrant = warp & 3).
 struct alignas(64) TmaPair {
     CUtensorMap a, b;
+    CUtensorMap o;  // output [rows][cols] fp16, box {SC cols, 32 rows} (when ConvArgs::tma_out)
 };
 
 SDB_DEV void tma_im2col_4d(uint32_t dst, const void* map, uint64_t* bar, int c, int w, int h, int n, int off_w,
@@ -751,6 +805,7 @@ __global__ void __launch_bounds__(TmaCfg<MODE, BN, ST>::kThreads, (BN <= 128) ? 
     if (tid == 0) {
         prefetch_tmap(&tm.a);
         prefetch_tmap(&tm.b);
+        if (a.tma_out) prefetch_tmap(&tm.o);
         for (int s = 0; s < ST; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
@@ -963,7 +1018,19 @@ __global__ void __launch_bounds__(TmaCfg<MODE, BN, ST>::kThreads, (BN <= 128) ? 
         };
         using T_ = std::true_type;
         using F_ = std::false_type;
-        if (MODE == DGRAD && a.accumulate && a.mask) run(T_{}, T_{});
+        if (MODE != WGRAD && a.tma_out) {
+            int lt = 0, sb = 0;
+            uint8_t* stg8 = reinterpret_cast<uint8_t*>(stg);
+            for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++lt) {
+                int m0, n0, kb0, nk;
+                tile_coords(t, m0, n0, kb0, nk);
+                const int acc = lt & 1;
+                epilogue_tile_tmastore<kNCol, Cfg::kSC>(&tm.o, m0, n0, nk, tmem + acc * BN, warp & 3, lane, c_lo,
+                                                        stg8, &tfull[acc], (lt >> 1) & 1, &tempty[acc], sb);
+            }
+            if (lane == 0) bulk_wait_all();
+            __syncwarp();
+        } else if (MODE == DGRAD && a.accumulate && a.mask) run(T_{}, T_{});
         else if (MODE == DGRAD && a.accumulate) run(T_{}, F_{});
         else if (MODE == DGRAD && a.mask) run(F_{}, T_{});
         else run(F_{}, F_{});
@@ -1257,7 +1324,7 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 static bool make_tmap(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
-                      const uint32_t* box) {
+                      const uint32_t* box, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
     static EncodeTiledFn fn = nullptr;
     if (!fn) {
         cudaDriverEntryPointQueryResult q;
@@ -1275,7 +1342,7 @@ static bool make_tmap(CUtensorMap* m, const void* base, int rank, const uint64_t
         if (i + 1 < rank) st[i] = strides[i];
     }
     return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, rank, const_cast<void*>(base), d, st, b, es,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -1374,6 +1441,29 @@ static cudaError_t launch_tma(ConvArgs a, int splits, cudaStream_t st) {
         const uint64_t strides[1] = {static_cast<uint64_t>(a.NG) * 2};
         const uint32_t box[2] = {64, 64};
         ok = ok && make_tmap(&tm.b, a.w, 2, dims, strides, box);
+    }
+    // fp16 output through TMA stores: fprop, and stride-1 dgrad without the
+    // residual addend / activation mask (SDB_CONV_NO_TMA_STORE disables).  It
+    // pays where the epilogue bounds the tile (short K: <= 4 k-blocks) or the
+    // mainloop is long enough to hide it (3x3); for 1x1 convs with 8+ k-blocks
+    // the stores compete with the operand loads for the TMA unit (measured
+    // 1.1x slower on the res5 expansion convs), so those keep the LSU stores.
+    static const bool no_tma_store = std::getenv("SDB_CONV_NO_TMA_STORE") != nullptr;
+    a.tma_out = 0;
+    const bool epi_pays = a.R * a.S > 1 || (a.KG + kBK - 1) / kBK <= 4;
+    if (ok && !no_tma_store && epi_pays &&
+        (MODE == FPROP || (MODE == DGRAD && a.stride == 1 && !a.accumulate && !a.mask))) {
+        const int cols = MODE == FPROP ? a.NG : a.C;
+        const int64_t rows = MODE == FPROP ? static_cast<int64_t>(a.M) : static_cast<int64_t>(a.N) * a.H * a.W;
+        if ((cols % 8) == 0) {
+            const uint64_t dims[2] = {static_cast<uint64_t>(cols), static_cast<uint64_t>(rows)};
+            const uint64_t strides[1] = {static_cast<uint64_t>(cols) * 2};
+            const uint32_t box[2] = {static_cast<uint32_t>(Cfg::kSC), 32};
+            a.tma_out = make_tmap(&tm.o, a.out, 2, dims, strides, box,
+                                  Cfg::kSC == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B)
+                            ? 1
+                            : 0;
+        }
     }
     if (!ok) return cudaErrorInvalidValue;
     return launch_pdl(conv_tma_kernel<MODE, BN, ST>, dim3(grid), dim3(Cfg::kThreads), Cfg::kSmem, st, a, tiles_m,
