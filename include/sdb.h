@@ -65,6 +65,14 @@ int sdb_conv_fprop(sdb_ctx* ctx, int dtype, const void* x, const void* w, void* 
 int sdb_conv_dgrad(sdb_ctx* ctx, int dtype, const void* dy, const void* w, void* dx, int N, int H, int W, int C, int K,
                    int R, int S, int stride, int pad, int accumulate, void* stream);
 /* dw = sum over pixels dy (x) im2col(x); deterministic split-K (no atomics) */
+/* fused residual fan-in + activation backward of the training step (tests and
+ * tools): dx = act'(y) * rn16(conv^T(dy, w) + addend), act' = 1 where y > 0
+ * else neg (the Tape's add + leaky/relu backward, src/autograd.cpp:340-351,
+ * folded into the dgrad epilogue).  y_bits (optional) = sign bitmap of y, bit
+ * c%8 of byte [pixel][c/8]; results are identical with and without it. */
+int sdb_conv_dgrad_act(sdb_ctx* ctx, int dtype, const void* dy, const void* w, void* dx, int N, int H, int W, int C,
+                       int K, int R, int S, int stride, int pad, const void* addend, const void* y, float neg,
+                       const void* y_bits, void* stream);
 int sdb_conv_wgrad(sdb_ctx* ctx, int dtype, const void* x, const void* dy, void* dw, int N, int H, int W, int C, int K,
                    int R, int S, int stride, int pad, void* stream);
 

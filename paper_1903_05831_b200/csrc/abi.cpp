@@ -140,6 +140,18 @@ int sdb_conv_dgrad(sdb_ctx* ctx, int dtype, const void* dy, const void* w, void*
     return cuda_status(sdb::conv_dgrad(g, dtype, dy, w, dx, accumulate, pick(ctx, stream)), "conv_dgrad");
 }
 
+int sdb_conv_dgrad_act(sdb_ctx* ctx, int dtype, const void* dy, const void* w, void* dx, int N, int H, int W, int C,
+                       int K, int R, int S, int stride, int pad, const void* addend, const void* y, float neg,
+                       const void* y_bits, void* stream) {
+    if (int rc = check_dtype(dtype)) return rc;
+    if (int rc = check_conv(N, H, W, C, K, R, S, stride, pad)) return rc;
+    if (!y) return fail(SDB_PARAM, "conv_dgrad_act: null activation y");
+    const sdb::ConvShape g{N, H, W, C, K, R, S, stride, pad};
+    return cuda_status(sdb::conv_dgrad(g, dtype, dy, w, dx, 1, pick(ctx, stream), addend, y, neg,
+                                       static_cast<const uint8_t*>(y_bits)),
+                       "conv_dgrad_act");
+}
+
 int sdb_conv_wgrad(sdb_ctx* ctx, int dtype, const void* x, const void* dy, void* dw, int N, int H, int W, int C, int K,
                    int R, int S, int stride, int pad, void* stream) {
     if (!ctx) return fail(SDB_PARAM, "conv_wgrad needs a context (workspace)");

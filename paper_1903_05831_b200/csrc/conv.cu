@@ -62,6 +62,7 @@ struct ConvArgs {
     int tma_b;       // dgrad: filter operand loaded by TMA (needs K % 64 == 0)
     int plain;       // 1x1 / stride 1 / pad 0: the activation operand is a plain 2-D [pixels][channels] tile
     int tma_out;     // fp16 output written by TMA stores from swizzled staging (tm.o)
+    const uint8_t* mbits;  // dgrad: sign bitmap of the mask tensor (bit c%8 of byte [row][c/8] = mask > 0)
 };
 
 // TMA descriptors of the dense GEMM operand (filter for fprop/dgrad, DY for wgrad)
@@ -737,6 +738,99 @@ SDB_DEV void epilogue_tile_tmastore(const CUtensorMap* omap, int m0, int n0, int
     }
 }
 
+// Epilogue v4 (stride-1 dgrad with the residual addend and a sign-bitmap
+// mask, BN = 256): lane = tile row as in v3.  The addend box of each column
+// step arrives by TMA into a two-slot ring (issued two steps ahead, the first
+// two before the accumulator is ready), the 32 mask bits of the row are one
+// 4-byte load, and the result leaves by TMA store:
+//   out = m ? p : rn16(f32(p) * neg),  p = rn16(acc + addend)
+template <int NCOL, int SC>
+SDB_DEV void epilogue_tile_resid(const ConvArgs& a, const CUtensorMap* omap, const CUtensorMap* rmap, int m0, int n0,
+                                 int nk, uint32_t tacc, int q, int lane, int c_lo, uint8_t* ostg, uint8_t* rstg,
+                                 uint64_t* rbar, uint64_t* tfull_acc, uint32_t tfull_phase, uint64_t* tempty_acc,
+                                 int& sb) {
+    static_assert(SC == 32, "residual epilogue: 64-byte rows");
+    constexpr int NSTEP = NCOL / SC;
+    constexpr int ROWB = SC * 2;
+    constexpr int BUFB = 32 * ROWB;
+    static_assert(NSTEP % 2 == 0, "two-slot ring: slot = step & 1");
+    const int row = m0 + q * 32 + lane;
+    const int cbase = n0 + c_lo;
+    auto issue = [&](int js) {
+        if (lane == 0 && js < NSTEP) {
+            uint64_t* bar = &rbar[js & 1];
+            mbar_arrive_expect_tx(bar, BUFB);
+            tma_load_2d(smem_u32(rstg + (js & 1) * BUFB), rmap, bar, cbase + js * SC, m0 + q * 32);
+        }
+    };
+    issue(0);
+    issue(1);
+    // the row's mask bits for the whole tile (NCOL / 8 bytes)
+    uint32_t mb[NSTEP];
+    const int cb8 = a.C / 8;
+#pragma unroll
+    for (int js = 0; js < NSTEP; ++js)
+        mb[js] = (row < a.M && cbase + js * SC < a.C)
+                     ? *reinterpret_cast<const uint32_t*>(a.mbits + static_cast<int64_t>(row) * cb8 + (cbase + js * SC) / 8)
+                     : 0u;
+    const uint64_t neg2 = static_cast<uint64_t>(__float_as_uint(a.mask_neg)) * 0x100000001ull;
+    mbar_wait(tfull_acc, tfull_phase);
+    tc_fence_after();
+#pragma unroll
+    for (int js = 0; js < NSTEP; ++js) {
+        uint32_t v[SC];
+        tmem_ld_cols<SC>(tacc + (static_cast<uint32_t>(q * 32) << 16) + c_lo + js * SC, v);
+        if (js == NSTEP - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tempty_acc);
+        }
+        if (nk == 0) {
+#pragma unroll
+            for (int j = 0; j < SC; ++j) v[j] = 0u;
+        }
+        mbar_wait(&rbar[js & 1], (js >> 1) & 1);
+        const uint8_t* rb = rstg + (js & 1) * BUFB + lane * ROWB;
+        if (lane == 0) bulk_wait_read<1>();
+        __syncwarp();
+        uint8_t* buf = ostg + sb * BUFB;
+#pragma unroll
+        for (int j = 0; j < SC / 8; ++j) {
+            const int pj = j ^ ((lane >> 1) & 3);
+            const uint4 r4 = *reinterpret_cast<const uint4*>(rb + pj * 16);
+            const uint32_t rw[4] = {r4.x, r4.y, r4.z, r4.w};
+            uint32_t pk[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const float s0 = fadd_f16(static_cast<uint16_t>(rw[e] & 0xffffu), __uint_as_float(v[8 * j + 2 * e]));
+                const float s1 = fadd_f16(static_cast<uint16_t>(rw[e] >> 16), __uint_as_float(v[8 * j + 2 * e + 1]));
+                const uint32_t p = pack_half2(s0, s1);
+                const uint32_t b2 = mb[js] >> (8 * j + 2 * e);
+                const uint32_t m = ((0u - (b2 & 1u)) & 0xffffu) | ((0u - ((b2 >> 1) & 1u)) & 0xffff0000u);
+                const __half2 ph = *reinterpret_cast<const __half2*>(&p);
+                const float2 pf = __half22float2(ph);
+                const uint64_t pf2 = static_cast<uint64_t>(__float_as_uint(pf.x)) |
+                                     (static_cast<uint64_t>(__float_as_uint(pf.y)) << 32);
+                uint64_t q2;
+                asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(q2) : "l"(pf2), "l"(neg2));
+                const uint32_t qn = pack_half2(__uint_as_float(static_cast<uint32_t>(q2)),
+                                               __uint_as_float(static_cast<uint32_t>(q2 >> 32)));
+                pk[e] = (p & m) | (qn & ~m);
+            }
+            *reinterpret_cast<uint4*>(buf + lane * ROWB + pj * 16) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        }
+        // the addend slot is free again (all lanes read it): reload it two steps ahead
+        fence_proxy_async();
+        __syncwarp();
+        issue(js + 2);
+        if (lane == 0) {
+            tma_store_2d(omap, smem_u32(buf), cbase + js * SC, m0 + q * 32);
+            bulk_commit();
+        }
+        sb ^= 1;
+    }
+}
+
 // ============================================================ all-TMA tcgen05 kernel
 // Both operands arrive by TMA, the activation side through the im2col mode of
 // cp.async.bulk.tensor (the hardware walks the output-pixel traversal of the
@@ -758,6 +852,7 @@ SDB_DEV void epilogue_tile_tmastore(const CUtensorMap* omap, int m0, int n0, int
 struct alignas(64) TmaPair {
     CUtensorMap a, b;
     CUtensorMap o;  // output [rows][cols] fp16, box {SC cols, 32 rows} (when ConvArgs::tma_out)
+    CUtensorMap r;  // dgrad residual addend, same box (EPI 1)
 };
 
 SDB_DEV void tma_im2col_4d(uint32_t dst, const void* map, uint64_t* bar, int c, int w, int h, int n, int off_w,
@@ -772,23 +867,25 @@ SDB_DEV void tma_im2col_4d(uint32_t dst, const void* map, uint64_t* bar, int c, 
 
 // BN = 256: 8 epilogue warps (two per TMEM lane quadrant, 128 columns each,
 // 32-column steps); BN <= 128: 4 warps, 16-column steps (two CTAs per SM).
-template <int MODE, int BN, int ST>
+// EPI 1 (dgrad residual + bitmask epilogue, BN = 256): per epilogue warp two
+// output staging boxes and a two-slot addend ring (4 x 2 KB)
+template <int MODE, int BN, int ST, int EPI = 0>
 struct TmaCfg {
     static constexpr int kABytes = kBM * kBK * 2;
     static constexpr int kBBytes = BN * kBK * 2;
     static constexpr int kStage = kABytes + kBBytes;
     static constexpr int kEpiWarps = BN == 256 ? 8 : 4;
     static constexpr int kSC = BN == 256 ? 32 : 16;
-    static constexpr int kStaging = kEpiWarps * 32 * kSC * 4;
+    static constexpr int kStaging = EPI ? kEpiWarps * 4 * 32 * kSC * 2 : kEpiWarps * 32 * kSC * 4;
     static constexpr int kSmem = ST * kStage + kStaging + 1024 + 256;
     static constexpr int kThreads = 64 + 32 * kEpiWarps;
     static constexpr int kPerSM = BN <= 128 ? 2 : 1;
 };
 
-template <int MODE, int BN, int ST>
-__global__ void __launch_bounds__(TmaCfg<MODE, BN, ST>::kThreads, (BN <= 128) ? 2 : 1)
+template <int MODE, int BN, int ST, int EPI = 0>
+__global__ void __launch_bounds__(TmaCfg<MODE, BN, ST, EPI>::kThreads, (BN <= 128) ? 2 : 1)
     conv_tma_kernel(ConvArgs a, int tiles_m, int tiles_n, int n_tiles, const __grid_constant__ TmaPair tm) {
-    using Cfg = TmaCfg<MODE, BN, ST>;
+    using Cfg = TmaCfg<MODE, BN, ST, EPI>;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
@@ -798,7 +895,8 @@ __global__ void __launch_bounds__(TmaCfg<MODE, BN, ST>::kThreads, (BN <= 128) ? 
     uint64_t* empty = full + ST;
     uint64_t* tfull = empty + ST;   // [2]
     uint64_t* tempty = tfull + 2;   // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* rbar = tempty + 2;    // [kEpiWarps][2] addend ring (EPI 1)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + (EPI ? 2 * Cfg::kEpiWarps : 0));
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int nkb_total = (a.KG + kBK - 1) / kBK;
@@ -806,10 +904,12 @@ __global__ void __launch_bounds__(TmaCfg<MODE, BN, ST>::kThreads, (BN <= 128) ? 
         prefetch_tmap(&tm.a);
         prefetch_tmap(&tm.b);
         if (a.tma_out) prefetch_tmap(&tm.o);
+        if (EPI) prefetch_tmap(&tm.r);
         for (int s = 0; s < ST; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
+        for (int i = 0; i < (EPI ? 2 * Cfg::kEpiWarps : 0); ++i) mbar_init(&rbar[i], 1);
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
             mbar_init(&tempty[i], Cfg::kEpiWarps);
@@ -1018,7 +1118,21 @@ __global__ void __launch_bounds__(TmaCfg<MODE, BN, ST>::kThreads, (BN <= 128) ? 
         };
         using T_ = std::true_type;
         using F_ = std::false_type;
-        if (MODE != WGRAD && a.tma_out) {
+        if constexpr (EPI == 1) {
+            int lt = 0, sb = 0;
+            uint8_t* ostg = reinterpret_cast<uint8_t*>(staging) + ew * 4 * (32 * Cfg::kSC * 2);
+            uint8_t* rstg = ostg + 2 * (32 * Cfg::kSC * 2);
+            for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++lt) {
+                int m0, n0, kb0, nk;
+                tile_coords(t, m0, n0, kb0, nk);
+                const int acc = lt & 1;
+                epilogue_tile_resid<kNCol, Cfg::kSC>(a, &tm.o, &tm.r, m0, n0, nk, tmem + acc * BN, warp & 3, lane,
+                                                     c_lo, ostg, rstg, rbar + 2 * ew, &tfull[acc], (lt >> 1) & 1,
+                                                     &tempty[acc], sb);
+            }
+            if (lane == 0) bulk_wait_all();
+            __syncwarp();
+        } else if (MODE != WGRAD && a.tma_out) {
             int lt = 0, sb = 0;
             uint8_t* stg8 = reinterpret_cast<uint8_t*>(stg);
             for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++lt) {
@@ -1387,12 +1501,13 @@ static bool tma_ok(const ConvArgs& a, int mode) {
     return (a.C % 64) == 0;
 }
 
-template <int MODE, int BN, int ST>
+template <int MODE, int BN, int ST, int EPI = 0>
 static cudaError_t launch_tma(ConvArgs a, int splits, cudaStream_t st) {
-    using Cfg = TmaCfg<MODE, BN, ST>;
+    using Cfg = TmaCfg<MODE, BN, ST, EPI>;
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(conv_tma_kernel<MODE, BN, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
+        cudaFuncSetAttribute(conv_tma_kernel<MODE, BN, ST, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             Cfg::kSmem);
         configured = true;
     }
     const int tiles_m = (a.M + kBM - 1) / kBM, tiles_n = (a.NG + BN - 1) / BN;
@@ -1465,8 +1580,17 @@ static cudaError_t launch_tma(ConvArgs a, int splits, cudaStream_t st) {
                             : 0;
         }
     }
+    if (EPI == 1 && ok) {
+        // output and residual addend views [N*H*W][C], 32 x 32 boxes
+        const uint64_t dims[2] = {static_cast<uint64_t>(a.C), static_cast<uint64_t>(a.N) * a.H * a.W};
+        const uint64_t strides[1] = {static_cast<uint64_t>(a.C) * 2};
+        const uint32_t box[2] = {static_cast<uint32_t>(Cfg::kSC), 32};
+        ok = make_tmap(&tm.o, a.out, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_64B) &&
+             make_tmap(&tm.r, a.addend, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_64B);
+        a.tma_out = 0;
+    }
     if (!ok) return cudaErrorInvalidValue;
-    return launch_pdl(conv_tma_kernel<MODE, BN, ST>, dim3(grid), dim3(Cfg::kThreads), Cfg::kSmem, st, a, tiles_m,
+    return launch_pdl(conv_tma_kernel<MODE, BN, ST, EPI>, dim3(grid), dim3(Cfg::kThreads), Cfg::kSmem, st, a, tiles_m,
                       tiles_n, n_tiles, tm);
 }
 
@@ -1570,10 +1694,12 @@ cudaError_t conv_fprop(const ConvShape& g, int dtype, const void* x, const void*
 }
 
 cudaError_t conv_dgrad(const ConvShape& g, int dtype, const void* dy, const void* w, void* dx, int accumulate,
-                       cudaStream_t st, const void* addend, const void* mask, float mask_neg) {
+                       cudaStream_t st, const void* addend, const void* mask, float mask_neg,
+                       const uint8_t* mask_bits) {
     ConvArgs base = make_args(g);
     base.x = dy; base.w = w; base.out = dx; base.accumulate = accumulate || addend != nullptr;
     base.mask = mask;
+    base.mbits = mask_bits;
     base.mask_neg = mask_neg;
     base.addend = addend ? addend : dx;
     base.NG = g.C;
@@ -1621,7 +1747,12 @@ cudaError_t conv_dgrad(const ConvShape& g, int dtype, const void* dy, const void
                 continue;  // zeroed above (or untouched when accumulating)
             } else if (tc_ok(g, dtype)) {
                 a.tma_b = (g.K % kBK) == 0 ? 1 : 0;
-                e = tma_ok(a, DGRAD) ? launch_tma_pick<DGRAD>(a, 1, st) : launch_tc_pick<DGRAD>(a, 1, st);
+                static const bool no_resid = std::getenv("SDB_CONV_NO_RESID_EPI") != nullptr;
+                if (tma_ok(a, DGRAD) && a.mbits && a.accumulate && sd == 1 && tma_bn(a) == 256 && (g.C % 32) == 0 &&
+                    !no_resid)
+                    e = launch_tma<DGRAD, 256, 3, 1>(a, 1, st);
+                else
+                    e = tma_ok(a, DGRAD) ? launch_tma_pick<DGRAD>(a, 1, st) : launch_tc_pick<DGRAD>(a, 1, st);
             } else {
                 e = dtype == kF16 ? launch_simt<__half, DGRAD>(a, 1, st) : launch_simt<float, DGRAD>(a, 1, st);
             }

@@ -104,6 +104,9 @@ struct Block {
     NormL n1, n2, n3, nd;
     bool has_down = false;
     Act in, z1, a1, z2, a2, z3, b3, zd, d, out;
+    // sign bitmap of `out` ([rows][C/8] bytes, bit = out > 0), written by the
+    // fused bn3 apply (IABN fp16) for the next layer's dgrad-epilogue mask
+    uint8_t* obits = nullptr;
 };
 
 enum ProfCat {
@@ -365,6 +368,8 @@ void alloc_stage(sdb_det* d, std::vector<Block>& st, Act in) {
             bl.d = d->cfg.mode == 0 ? d->act(bl.zd.n, bl.zd.h, bl.zd.w, bl.zd.c) : bl.zd;
         }
         bl.out = d->act(bl.z3.n, bl.z3.h, bl.z3.w, bl.z3.c);
+        if (d->cfg.mode != 0 && d->dt == kF16)
+            bl.obits = static_cast<uint8_t*>(d->alloc(static_cast<size_t>(bl.out.numel() / 8)));
         d->gbuf_elems = std::max({d->gbuf_elems, in.numel(), bl.z1.numel(), bl.z2.numel(), bl.z3.numel()});
         in = bl.out;
     }
@@ -500,7 +505,7 @@ void block_fwd(sdb_det* d, Block& b) {
             ps.bytes_ = 4.0 * d->es * b.out.numel();
         }
         CK(bn_apply_add_act(d->dt, b.z3.p, d->bnp(b.n3.pg), d->bnp(b.n3.pb), b.n3.mean, b.n3.invstd, b.b3.p, sc->p,
-                            b.out.p, rows, b.n3.C, b.n3.slope, 2, d->cfg.slope, d->ctx->stream));
+                            b.out.p, rows, b.n3.C, b.n3.slope, 2, d->cfg.slope, d->ctx->stream, b.obits));
         return;
     }
     norm_fwd(d, b.n3, b.z3, b.b3);
@@ -516,10 +521,11 @@ void block_fwd(sdb_det* d, Block& b) {
 
 // ------------------------------------------------------------------ backward helpers
 void dgrad(sdb_det* d, const ConvL& c, const void* dy, void* dx, int accumulate, const void* addend = nullptr,
-           const void* mask = nullptr, float mask_neg = 0.0f) {
+           const void* mask = nullptr, float mask_neg = 0.0f, const uint8_t* mask_bits = nullptr) {
     PScope ps(d, P_DGRAD, conv_flops(c.g), 0, c.g.stride * c.g.stride);
-    if (d->prof.on) { ps.label = shape_label("dgrad", c.g); ps.flops_ = conv_flops(c.g); }
-    CK(conv_dgrad(c.g, d->dt, dy, d->wdev_ptr(c.p), dx, accumulate, d->ctx->stream, addend, mask, mask_neg));
+    if (d->prof.on) { ps.label = shape_label(mask_bits ? "dgrad+res" : "dgrad", c.g); ps.flops_ = conv_flops(c.g); }
+    CK(conv_dgrad(c.g, d->dt, dy, d->wdev_ptr(c.p), dx, accumulate, d->ctx->stream, addend, mask, mask_neg,
+                  mask_bits));
 }
 
 struct Bwd {
@@ -594,7 +600,8 @@ void conv_wgrad_to(Bwd& B, const ConvL& c, const Act& x, const void* dy) {
 // dx; when b.in is itself a residual-block output (in_mask != null) the final
 // dgrad epilogue applies that block's activation mask too, so dx is the next
 // block's dS.  Uses scratch buffers s1, s2.
-void block_bwd(Bwd& B, Block& b, const void* dS, void* dx, void* s1, void* s2, const void* in_mask) {
+void block_bwd(Bwd& B, Block& b, const void* dS, void* dx, void* s1, void* s2, const void* in_mask,
+               const uint8_t* in_bits) {
     sdb_det* d = B.d;
     const float neg = d->cfg.mode == 0 ? 0.0f : d->cfg.slope;
     // shortcut first (its params come last in the block's pack order)
@@ -618,8 +625,8 @@ void block_bwd(Bwd& B, Block& b, const void* dS, void* dx, void* s1, void* s2, c
     conv_wgrad_to(B, b.c1, b.in, z);
     // residual fan-in in the dgrad epilogue: dx = conv1^T(dz1) + (down-path dx | identity dS),
     // then the previous block's activation mask
-    if (b.has_down) dgrad(d, b.c1, z, dx, 1, nullptr, in_mask, neg);
-    else dgrad(d, b.c1, z, dx, 1, dS, in_mask, neg);
+    if (b.has_down) dgrad(d, b.c1, z, dx, 1, nullptr, in_mask, neg, in_bits);
+    else dgrad(d, b.c1, z, dx, 1, dS, in_mask, neg, in_bits);
 }
 
 // ------------------------------------------------------------------ the step
@@ -717,7 +724,7 @@ void run_step(sdb_det* d) {
     }
     for (int i = static_cast<int>(d->head.size()) - 1; i >= 0; --i) {
         const void* in_mask = i > 0 ? d->head[i - 1].out.p : nullptr;  // head[0].in = RoIAlign output (linear)
-        block_bwd(B, d->head[i], cur, spare, d->gbuf[1], d->gbuf[4], in_mask);
+        block_bwd(B, d->head[i], cur, spare, d->gbuf[1], d->gbuf[4], in_mask, i > 0 ? d->head[i - 1].obits : nullptr);
         std::swap(cur, spare);
     }
     (void)spare;
@@ -745,13 +752,14 @@ void run_step(sdb_det* d) {
     }
     conv_wgrad_to(B, d->rpn_conv, d->c4, drpn);
     // dc4 (RoIAlign part) + RPN part, then the last backbone block's activation mask
-    dgrad(d, d->rpn_conv, drpn, dc4, 1, nullptr, d->c4.p, neg);
+    dgrad(d, d->rpn_conv, drpn, dc4, 1, nullptr, d->c4.p, neg, d->backbone.empty() ? nullptr : d->backbone.back().obits);
     // backbone
     cur = dc4;
     spare = dc4 == d->gbuf[2] ? d->gbuf[3] : d->gbuf[2];
     for (int i = static_cast<int>(d->backbone.size()) - 1; i >= 0; --i) {
         const void* in_mask = i > 0 ? d->backbone[i - 1].out.p : nullptr;  // backbone[0].in = max-pool output
-        block_bwd(B, d->backbone[i], cur, spare, d->gbuf[1], d->gbuf[4], in_mask);
+        block_bwd(B, d->backbone[i], cur, spare, d->gbuf[1], d->gbuf[4], in_mask,
+                  i > 0 ? d->backbone[i - 1].obits : nullptr);
         std::swap(cur, spare);
     }
     // maxpool, stem norm, stem wgrad (the image gradient is not needed)

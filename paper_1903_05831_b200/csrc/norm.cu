@@ -370,6 +370,9 @@ struct ApplyArgs {
     void* out2;
     int act2;
     float slope2;
+    // optional sign bitmap of the stored out2 (bit j of byte [row][c/8] = out2 > 0),
+    // what the dgrad epilogue of the next layer needs of it
+    uint8_t* bits;
 };
 
 SDB_DEV void ldf8(const float* p, float (&v)[8]) {
@@ -464,6 +467,12 @@ __global__ void __launch_bounds__(kStatThreads, 2) apply_kernel(ApplyArgs p, int
                         o2[j] = p.act2 == 0 ? sr : (sr > 0.f ? sr : (p.act2 == 1 ? 0.f : __fmul_rn(p.slope2, sr)));
                     }
                     store8<T>(static_cast<T*>(p.out2) + (r0 + rr) * C + c0, o2);
+                    if (p.bits) {
+                        uint32_t bm = 0;
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) bm |= (to_f<T>(from_f<T>(o2[j])) > 0.f ? 1u : 0u) << j;
+                        p.bits[(r0 + rr) * (C / 8) + cg] = static_cast<uint8_t>(bm);
+                    }
                 }
             } else {
                 float d[8];
@@ -594,9 +603,10 @@ cudaError_t bn_forward_stats(int dtype, const void* x, float* mean, float* invst
 
 cudaError_t bn_apply_add_act(int dtype, const void* x, const float* gamma, const float* beta, const float* mean,
                              const float* invstd, void* y, const void* shortcut, void* out, int64_t rows, int C,
-                             float slope, int act2, float slope2, cudaStream_t st) {
+                             float slope, int act2, float slope2, cudaStream_t st, uint8_t* out_bits) {
     const Plan pl = plan_for(rows, C, dtype == kF16 ? 2 : 4);
     ApplyArgs aa{};
+    aa.bits = out_bits;
     aa.a = x; aa.dy = shortcut; aa.out = y; aa.gamma = gamma; aa.beta = beta; aa.mean = mean; aa.invstd = invstd;
     aa.slope = slope; aa.act = 2; aa.n8 = rows * C / 8; aa.C = C;
     aa.out2 = out; aa.act2 = act2; aa.slope2 = slope2;

@@ -26,9 +26,11 @@ cudaError_t conv_fprop(const ConvShape& g, int dtype, const void* x, const void*
 // accumulate: dx = conv^T(dy, w) + addend (addend = dx itself when null)
 // mask (optional): dx = round(dx) * (mask > 0 ? 1 : mask_neg), the backward of
 // the ReLU / leaky that produced this layer's input, fused into the epilogue
+// mask_bits (optional): sign bitmap of `mask` (bit c%8 of byte [row][c/8] = mask > 0),
+// used by the stride-1 residual epilogue instead of the fp16 mask when present
 cudaError_t conv_dgrad(const ConvShape& g, int dtype, const void* dy, const void* w, void* dx, int accumulate,
                        cudaStream_t st, const void* addend = nullptr, const void* mask = nullptr,
-                       float mask_neg = 0.0f);
+                       float mask_neg = 0.0f, const uint8_t* mask_bits = nullptr);
 size_t conv_wgrad_workspace(const ConvShape& g, int dtype);
 cudaError_t conv_wgrad(const ConvShape& g, int dtype, const void* x, const void* dy, void* dw, void* ws,
                        size_t ws_bytes, cudaStream_t st);
@@ -64,7 +66,7 @@ cudaError_t bn_forward_stats(int dtype, const void* x, float* mean, float* invst
                              int act, void* ws, cudaStream_t st);
 cudaError_t bn_apply_add_act(int dtype, const void* x, const float* gamma, const float* beta, const float* mean,
                              const float* invstd, void* y, const void* shortcut, void* out, int64_t rows, int C,
-                             float slope, int act2, float slope2, cudaStream_t st);
+                             float slope, int act2, float slope2, cudaStream_t st, uint8_t* out_bits = nullptr);
 // y_mask: stored BN+ReLU output (relu mask) or null for plain BN
 cudaError_t bn_backward(int dtype, const void* dy, const void* x, const void* y_mask, const float* gamma,
                         const float* mean, const float* invstd, void* dx, float* dgamma, float* dbeta, int64_t rows,

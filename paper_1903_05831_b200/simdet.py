@@ -31,6 +31,7 @@ _SIGS = {
     "sdb_get_nccl_unique_id": [_P],
     "sdb_conv_fprop": [_P, _I, _P, _P, _P] + [_I] * 9 + [_P],
     "sdb_conv_dgrad": [_P, _I, _P, _P, _P] + [_I] * 10 + [_P],
+    "sdb_conv_dgrad_act": [_P, _I, _P, _P, _P] + [_I] * 9 + [_P, _P, C.c_float, _P, _P],
     "sdb_conv_wgrad": [_P, _I, _P, _P, _P] + [_I] * 9 + [_P],
     "sdb_bn_fwd": [_P, _I, _P, _P, _P, _P, _P, _P, _L, _I, _F, _I, _P],
     "sdb_bn_bwd": [_P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _L, _I, _P],
@@ -127,6 +128,24 @@ def conv_dgrad_nhwc(dy, w, x_shape, stride, pad, out=None, accumulate=False):
     dx = out if out is not None else torch.empty((N, H, W, Cc), device=dy.device, dtype=dy.dtype)
     check(L().sdb_conv_dgrad(ctx(), dt(dy), ptr(dy), ptr(w), ptr(dx), N, H, W, Cc, K, R, S, stride, pad,
                              1 if accumulate else 0, stream()))
+    return dx
+
+
+def sign_bits_nhwc(y):
+    """sign bitmap of an NHWC tensor: bit c%8 of byte [pixel][c/8] = (y > 0)"""
+    b = (y.reshape(-1, y.shape[-1] // 8, 8) > 0).to(torch.int32)
+    w8 = torch.tensor([1 << j for j in range(8)], dtype=torch.int32, device=y.device)
+    return (b * w8).sum(-1).to(torch.uint8).contiguous()
+
+
+def conv_dgrad_act_nhwc(dy, w, addend, y, neg, stride, pad, y_bits=None):
+    """dx = act'(y) * rn16(conv^T(dy, w) + addend): the step's fused residual + activation backward"""
+    N, H, W, Cc = y.shape
+    K, R, S, _ = w.shape
+    dx = torch.empty((N, H, W, Cc), device=dy.device, dtype=dy.dtype)
+    check(L().sdb_conv_dgrad_act(ctx(), dt(dy), ptr(dy), ptr(w), ptr(dx), N, H, W, Cc, K, R, S, stride, pad,
+                                 ptr(addend), ptr(y), float(neg), ptr(y_bits) if y_bits is not None else None,
+                                 stream()))
     return dx
 
 

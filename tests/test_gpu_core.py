@@ -93,6 +93,40 @@ def test_conv_large_tile_path(ref):
     assert_close(y, y_ref, 2e-3, "y")
 
 
+# (N, H, W, C, K, R, S, stride, pad): the first four take the TMA residual
+# epilogue (stride 1, BN = 256, sign bitmap), the last two fall back to the
+# fp16-mask epilogue (BN = 128 / stride 2) and must ignore the bitmap
+DGRAD_ACT_CASES = [(2, 20, 30, 256, 64, 1, 1, 1, 0), (16, 7, 7, 2048, 512, 1, 1, 1, 0), (1, 25, 42, 1024, 256, 3, 3, 1, 1),
+                   (2, 13, 17, 512, 128, 1, 1, 1, 0), (2, 9, 9, 128, 64, 1, 1, 1, 0), (2, 14, 14, 256, 128, 3, 3, 2, 1)]
+
+
+@pytest.mark.parametrize("case", DGRAD_ACT_CASES)
+def test_dgrad_act_bitmap_matches_fp16_mask(case):
+    """the step's fused residual + leaky backward: the sign-bitmap epilogue is
+    bit-identical to the fp16-mask one, and both match an fp32 torch reference"""
+    from paper_1903_05831_b200 import simdet as sd
+    N, H, W, C, K, R, S, st, pd = case
+    g = torch.Generator(device="cuda").manual_seed(hash(case) % 2**31)
+    Ho, Wo = (H + 2 * pd - R) // st + 1, (W + 2 * pd - S) // st + 1
+    dy = torch.randn((N, Ho, Wo, K), device="cuda", generator=g).half()
+    w = (torch.randn((K, R, S, C), device="cuda", generator=g) / np.sqrt(K * R * S)).half()
+    add = torch.randn((N, H, W, C), device="cuda", generator=g).half()
+    y = torch.randn((N, H, W, C), device="cuda", generator=g).half()
+    y[..., ::7] = 0  # y == 0 takes the negative branch
+    neg = 0.01
+    bits = sd.sign_bits_nhwc(y)
+    dx_m = sd.conv_dgrad_act_nhwc(dy, w, add, y, neg, st, pd)
+    dx_b = sd.conv_dgrad_act_nhwc(dy, w, add, y, neg, st, pd, y_bits=bits)
+    torch.cuda.synchronize()
+    assert torch.equal(dx_m.view(torch.int16), dx_b.view(torch.int16))
+    # fp32 reference of the same op
+    acc = torch.nn.grad.conv2d_input((N, C, H, W), w.float().permute(0, 3, 1, 2), dy.float().permute(0, 3, 1, 2),
+                                     stride=st, padding=pd).permute(0, 2, 3, 1)
+    p = (acc + add.float()).half().float()
+    ref = torch.where(y.float() > 0, p, (p * neg).half().float())
+    assert_close(dx_m.float(), ref, 2e-3, "dx")
+
+
 # the last two are large enough that every CTA of the bulk-copy statistics
 # pipeline streams more tiles than it has stages (ring wrap-around)
 BN_SHAPES = [(2, 64, 7, 9), (4, 256, 5, 5), (2, 2048, 3, 3), (1, 8, 4, 4), (2, 512, 16, 12), (6, 128, 150, 160),

@@ -56,7 +56,8 @@ int main(int argc, char** argv) {
     const char* which = argc > 11 ? argv[11] : "fdmw";
     const size_t nx = size_t(g.N) * g.H * g.W * g.C, ny = size_t(g.N) * g.Ho() * g.Wo() * g.K,
                  nw = size_t(g.K) * g.R * g.S * g.C;
-    void *x, *y, *w, *dx, *mask, *add, *dw, *ws;
+    void *x, *y, *w, *dx, *mask, *add, *dw, *ws, *mbits;
+    CK(cudaMalloc(&mbits, nx / 8 + 16)); CK(cudaMemset(mbits, 0xa5, nx / 8 + 16));
     CK(cudaMalloc(&x, nx * 2)); CK(cudaMalloc(&dx, nx * 2)); CK(cudaMalloc(&mask, nx * 2)); CK(cudaMalloc(&add, nx * 2));
     CK(cudaMalloc(&y, ny * 2)); CK(cudaMalloc(&w, nw * 2)); CK(cudaMalloc(&dw, nw * 2));
     const size_t wsb = sdb::conv_wgrad_workspace(g, 1) + 256;
@@ -77,6 +78,11 @@ int main(int argc, char** argv) {
         if (*p == 'm')
             rep("dgrad+a+m", graph_us(st, reps, [&] { CK(sdb::conv_dgrad(g, 1, y, w, dx, 1, st, add, mask, 0.01f)); }),
                 2.0 * (3 * nx + ny + nw));
+        if (*p == 'b')
+            rep("dgrad+a+bits", graph_us(st, reps, [&] {
+                    CK(sdb::conv_dgrad(g, 1, y, w, dx, 1, st, add, mask, 0.01f, static_cast<const uint8_t*>(mbits)));
+                }),
+                2.0 * (2 * nx + ny + nw) + nx / 8.0);
         if (*p == 'w')
             rep("wgrad", graph_us(st, reps, [&] { CK(sdb::conv_wgrad(g, 1, x, y, dw, ws, wsb, st)); }),
                 2.0 * (nx + ny + nw));
