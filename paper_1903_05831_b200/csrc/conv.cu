@@ -1596,11 +1596,24 @@ static cudaError_t launch_tma(ConvArgs a, int splits, cudaStream_t st) {
 
 // tile width: 256 when the GEMM N is wide enough (one CTA per SM, 2 x 256 TMEM
 // columns), else 128 / 64 (two CTAs per SM)
-static int tma_bn(const ConvArgs& a) { return a.NG >= 256 ? 256 : (a.NG > 64 ? 128 : 64); }
+// fprop/dgrad: when 128x256 tiles would leave more than half of the 148 SMs
+// idle (small-M res4 layers with N = 256: 66 tiles), 128x128 tiles put one CTA
+// on twice as many SMs (measured 1.08-1.1x: the narrow tile needs 1.33x the
+// operand bytes per FLOP, so L2 bandwidth caps the gain; with 132 tiles it is a
+// loss).  wgrad fills the machine with split-K instead.
+static int tma_bn(const ConvArgs& a, int mode = WGRAD) {
+    if (a.NG >= 256) {
+        const int64_t tiles256 = static_cast<int64_t>((a.M + kBM - 1) / kBM) * ((a.NG + 255) / 256);
+        static const bool no_narrow = std::getenv("SDB_CONV_NO_NARROW") != nullptr;
+        if (mode != WGRAD && 2 * tiles256 <= kNumSMs && !no_narrow) return 128;
+        return 256;
+    }
+    return a.NG > 64 ? 128 : 64;
+}
 
 template <int MODE>
 static cudaError_t launch_tma_pick(const ConvArgs& a, int splits, cudaStream_t st) {
-    switch (tma_bn(a)) {
+    switch (tma_bn(a, MODE)) {
         case 256: return launch_tma<MODE, 256, 4>(a, splits, st);
         case 128: return launch_tma<MODE, 128, 3>(a, splits, st);
         default: return launch_tma<MODE, 64, 4>(a, splits, st);
@@ -1748,7 +1761,7 @@ cudaError_t conv_dgrad(const ConvShape& g, int dtype, const void* dy, const void
             } else if (tc_ok(g, dtype)) {
                 a.tma_b = (g.K % kBK) == 0 ? 1 : 0;
                 static const bool no_resid = std::getenv("SDB_CONV_NO_RESID_EPI") != nullptr;
-                if (tma_ok(a, DGRAD) && a.mbits && a.accumulate && sd == 1 && tma_bn(a) == 256 && (g.C % 32) == 0 &&
+                if (tma_ok(a, DGRAD) && a.mbits && a.accumulate && sd == 1 && tma_bn(a, DGRAD) == 256 && (g.C % 32) == 0 &&
                     !no_resid)
                     e = launch_tma<DGRAD, 256, 3, 1>(a, 1, st);
                 else
