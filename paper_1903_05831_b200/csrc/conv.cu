@@ -1803,7 +1803,17 @@ static int wgrad_splits(const ConvShape& g, int dtype) {
     }
     const int64_t target = per_sm * kNumSMs;
     int64_t splits = target / std::max<int64_t>(tiles, 1);
-    splits = std::max<int64_t>(1, std::min<int64_t>(splits, nkb / 8));
+    // every split writes a full fp32 partial tile (which the reduce reads back):
+    // keep each split at least kMinKb k-blocks long so that partial traffic
+    // stays well below the operand traffic.  Measured on the C4 step (CUDA
+    // graph, wgrads on the side stream): 8 -> 13.06 ms, 24 -> 11.73,
+    // 32 -> 11.62, 48 -> 11.99 (785 MB -> ~300 MB of partials per step, and
+    // wgrad grids that leave SMs to the concurrent dgrad/norm chain)
+    static const int64_t kMinKb = [] {
+        const char* e = std::getenv("SDB_WGRAD_MINKB");
+        return e ? std::max(1, std::atoi(e)) : 32;
+    }();
+    splits = std::max<int64_t>(1, std::min<int64_t>(splits, nkb / kMinKb));
     return static_cast<int>(std::min<int64_t>(splits, 64));
 }
 
