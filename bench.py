@@ -424,7 +424,7 @@ def run_ours(args):
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak if peak else None, "traffic": traffic,
-                     "kernel": "conv_tc_kernel (tcgen05 implicit GEMM, fprop+dgrad+wgrad, FLOP-weighted)",
+                     "kernel": "conv_tma_kernel (tcgen05 implicit GEMM, TMA/im2col-TMA operands; fprop+dgrad+wgrad, FLOP-weighted)",
                      "peak_source": f"{peak_kind} bf16_tflops_sustained",
                      "flop_per_step": conv_flops, "ms_per_step": conv_ms, "launches_per_step": conv_launches},
         "breakdown_ms": {k: round(v[0], 3) for k, v in prof.items()},
