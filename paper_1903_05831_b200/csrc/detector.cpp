@@ -181,6 +181,10 @@ struct sdb_det {
     cudaStream_t wst = nullptr;
     cudaEvent_t wev_fork = nullptr, wev_join = nullptr;
     void* dzr[kDzRing] = {};
+    // anchor targets depend only on the fed GT: they run on the side stream
+    // at the start of the step, behind the backbone forward
+    void* ws_at = nullptr;
+    cudaEvent_t ev_at_fork = nullptr, ev_at_join = nullptr;
     cudaEvent_t dzr_ev[kDzRing] = {};
     bool dzr_busy[kDzRing] = {};
     int dzr_next = 0;
@@ -633,6 +637,18 @@ void block_bwd(Bwd& B, Block& b, const void* dS, void* dx, void* s1, void* s2, c
 void run_step(sdb_det* d) {
     cudaStream_t st = d->ctx->stream;
     const auto& cf = d->cfg;
+    const bool side = d->side_wgrad && !d->prof.on;
+    AnchorTargetArgs at{};
+    at.anchors = d->anchors; at.nA = d->nA; at.n_img = cf.batch; at.gt = d->gt; at.gt_stride = cf.max_gt;
+    at.gt_count = d->gt_count; at.img_h = static_cast<float>(cf.img_h); at.img_w = static_cast<float>(cf.img_w);
+    at.keys = d->keys; at.fg_thr = cf.rpn_fg_thr; at.bg_thr = cf.rpn_bg_thr; at.batch = cf.rpn_batch;
+    at.fg_cap = static_cast<int>(cf.rpn_fg_frac * cf.rpn_batch); at.labels = d->a_labels; at.targets = d->a_targets;
+    if (side) {
+        CK(cudaEventRecord(d->ev_at_fork, st));
+        CK(cudaStreamWaitEvent(d->wst, d->ev_at_fork, 0));
+        CK(anchor_targets(at, d->ws_at, d->wst));
+        CK(cudaEventRecord(d->ev_at_join, d->wst));
+    }
     // ---- forward: backbone
     conv_fwd(d, d->stem, d->img, d->stem_z);
     norm_fwd(d, d->stem_n, d->stem_z, d->stem_a);
@@ -647,12 +663,7 @@ void run_step(sdb_det* d) {
     conv_fwd(d, d->rpn_cls, d->rpn_a, d->rpn_logits);
     conv_fwd(d, d->rpn_bbox, d->rpn_a, d->rpn_deltas);
     // ---- targets and proposals (no gradient)
-    AnchorTargetArgs at{};
-    at.anchors = d->anchors; at.nA = d->nA; at.n_img = cf.batch; at.gt = d->gt; at.gt_stride = cf.max_gt;
-    at.gt_count = d->gt_count; at.img_h = static_cast<float>(cf.img_h); at.img_w = static_cast<float>(cf.img_w);
-    at.keys = d->keys; at.fg_thr = cf.rpn_fg_thr; at.bg_thr = cf.rpn_bg_thr; at.batch = cf.rpn_batch;
-    at.fg_cap = static_cast<int>(cf.rpn_fg_frac * cf.rpn_batch); at.labels = d->a_labels; at.targets = d->a_targets;
-    { PScope ps(d, P_TARGETS, 0, 0, 5); CK(anchor_targets(at, d->ws, st)); }
+    if (!side) { PScope ps(d, P_TARGETS, 0, 0, 5); CK(anchor_targets(at, d->ws, st)); }
     ProposalArgs pa{};
     pa.logits = d->rpn_logits.p; pa.deltas = d->rpn_deltas.p; pa.dtype = d->dt; pa.anchors = d->anchors;
     pa.n_img = cf.batch; pa.n_loc = d->n_loc; pa.A = d->A; pa.A_pad = d->A_pad; pa.pre_k = cf.pre_nms;
@@ -680,6 +691,7 @@ void run_step(sdb_det* d) {
     conv_fwd(d, d->fc_cls, d->pooled, d->cls_logits);
     conv_fwd(d, d->fc_bbox, d->pooled, d->bbox_pred);
     // ---- losses (scale folded into backward)
+    if (side) CK(cudaStreamWaitEvent(st, d->ev_at_join, 0));
     CK(cudaMemcpyAsync(d->scale_used, d->scale, 8, cudaMemcpyDeviceToDevice, st));
     void* g0 = d->d_cls;
     void* g1 = d->d_bbox;
@@ -1036,6 +1048,9 @@ int sdb_det_create(sdb_ctx* ctx, const sdb_det_config* cfgp, sdb_det** out) {
             CK(cudaStreamCreateWithPriority(&d->wst, cudaStreamNonBlocking, lo));
             CK(cudaEventCreateWithFlags(&d->wev_fork, cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&d->wev_join, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&d->ev_at_fork, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&d->ev_at_join, cudaEventDisableTiming));
+            d->ws_at = d->alloc(anchor_target_workspace_bytes(cf.batch, d->nA, cf.max_gt));
             for (int k = 0; k < sdb_det::kDzRing; ++k) {
                 d->dzr[k] = d->alloc(static_cast<size_t>(d->gbuf_elems) * d->es);
                 CK(cudaEventCreateWithFlags(&d->dzr_ev[k], cudaEventDisableTiming));
@@ -1094,6 +1109,8 @@ int sdb_det_destroy(sdb_det* d) {
         for (auto e : d->dzr_ev) cudaEventDestroy(e);
         cudaEventDestroy(d->wev_fork);
         cudaEventDestroy(d->wev_join);
+        cudaEventDestroy(d->ev_at_fork);
+        cudaEventDestroy(d->ev_at_join);
         cudaStreamDestroy(d->wst);
     }
     if (d->comm) {
