@@ -93,6 +93,34 @@ def test_conv_large_tile_path(ref):
     assert_close(y, y_ref, 2e-3, "y")
 
 
+# small-M layers whose 128x256 tiles fill less than half the SMs (the
+# narrow-tile choice); odd k-block counts and partial M tiles included
+SMALL_M_CASES = [(2, 256, 50, 84, 256, 3, 3, 1, 1), (2, 1024, 50, 84, 256, 1, 1, 1, 0), (2, 256, 50, 84, 1024, 1, 1, 1, 0),
+                (1, 192, 13, 17, 256, 3, 3, 1, 1)]
+
+
+@pytest.mark.parametrize("case", SMALL_M_CASES)
+def test_conv_small_m_layers(case):
+    """fprop and dgrad of the res4-sized layers vs an fp32 torch reference"""
+    from paper_1903_05831_b200 import simdet as sd
+    N, C, H, W, K, R, S, st, pd = case
+    g = torch.Generator(device="cuda").manual_seed(hash(case) % 2**31)
+    x = torch.randn((N, H, W, C), device="cuda", generator=g).half()
+    w = (torch.randn((K, R, S, C), device="cuda", generator=g) / np.sqrt(C * R * S)).half()
+    y = sd.conv_fprop_nhwc(x, w, st, pd)
+    ref = torch.nn.functional.conv2d(x.float().permute(0, 3, 1, 2), w.float().permute(0, 3, 1, 2), stride=st,
+                                     padding=pd).permute(0, 2, 3, 1)
+    dy = torch.randn(ref.shape, device="cuda", generator=g).half()
+    dx = sd.conv_dgrad_nhwc(dy, w, (N, H, W, C), st, pd)
+    dref = torch.nn.grad.conv2d_input((N, C, H, W), w.float().permute(0, 3, 1, 2), dy.float().permute(0, 3, 1, 2),
+                                      stride=st, padding=pd).permute(0, 2, 3, 1)
+    y2 = sd.conv_fprop_nhwc(x, w, st, pd)
+    torch.cuda.synchronize()
+    assert_close(y.float(), ref, 2e-3, "y")
+    assert_close(dx.float(), dref, 2e-3, "dx")
+    assert torch.equal(y, y2), "conv must be deterministic"
+
+
 # (N, H, W, C, K, R, S, stride, pad): the first four take the TMA residual
 # epilogue (stride 1, BN = 256, sign bitmap), the last two fall back to the
 # fp16-mask epilogue (BN = 128 / stride 2) and must ignore the bitmap
