@@ -21,6 +21,8 @@ template <class F>
 double graph_us(cudaStream_t st, int reps, F&& body) {
     cudaGraph_t g;
     cudaGraphExec_t ge;
+    body();  // eager first call (lazy per-device scratch is allocated outside the capture)
+    CK(cudaStreamSynchronize(st));
     CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
     for (int i = 0; i < reps; ++i) body();
     CK(cudaStreamEndCapture(st, &g));
