@@ -723,16 +723,15 @@ void run_step(sdb_det* d) {
     dgrad(d, d->fc_cls, g0, dpool, 1);
     // avgpool, then the res5 head
     void* dhead = d->gbuf[3];
-    { PScope ps(d, P_POOL, 0, static_cast<double>(d->es) * d->head_out.numel());
-    CK(avgpool_bwd(d->dt, dpool, d->R, d->head_out.h * d->head_out.w, d->feat_c, dhead, st)); }
     void* cur = dhead;
     void* spare = d->gbuf[2];
     const float neg = cf.mode == 0 ? 0.0f : cf.slope;
-    if (!d->head.empty()) {
-        // the last head block's output activation (its dS); inner block boundaries
-        // are masked in the dgrad epilogues
-        PScope ps(d, P_ELEM, 0, 3.0 * d->es * d->head_out.numel());
-        CK(act_bwd(d->dt, dhead, d->head_out.p, dhead, d->head_out.numel(), neg, st));
+    {
+        // avgpool backward with the last head block's output activation (its dS)
+        // fused in; inner block boundaries are masked in the dgrad epilogues
+        PScope ps(d, P_POOL, 0, static_cast<double>(d->es) * 2.0 * d->head_out.numel());
+        CK(avgpool_bwd(d->dt, dpool, d->R, d->head_out.h * d->head_out.w, d->feat_c, dhead, st,
+                       d->head.empty() ? nullptr : d->head_out.p, neg));
     }
     for (int i = static_cast<int>(d->head.size()) - 1; i >= 0; --i) {
         const void* in_mask = i > 0 ? d->head[i - 1].out.p : nullptr;  // head[0].in = RoIAlign output (linear)

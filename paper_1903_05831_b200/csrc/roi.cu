@@ -290,17 +290,19 @@ __global__ void __launch_bounds__(kBwdThreads) roialign_bwd_kernel(const T* __re
 }
 
 // ---------------------------------------------------------------- pooling
-template <class T>
+// I = int32_t whenever the element count allows: the per-element index
+// decomposition is then 32-bit (64-bit div/mod chains dominated these kernels)
+template <class T, class I>
 __global__ void maxpool_fwd_kernel(const T* __restrict__ x, int N, int H, int W, int C, int k, int s, int p,
                                    int Ho, int Wo, T* __restrict__ y, uint8_t* __restrict__ am) {
     const int C8 = C / 8;
-    const int64_t total = static_cast<int64_t>(N) * Ho * Wo * C8;
-    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
-         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const I total = static_cast<I>(N) * Ho * Wo * C8;
+    for (I e = blockIdx.x * static_cast<I>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<I>(gridDim.x) * blockDim.x) {
         const int c8 = static_cast<int>(e % C8);
-        const int64_t pix = e / C8;
+        const I pix = e / C8;
         const int ow = static_cast<int>(pix % Wo), oh = static_cast<int>((pix / Wo) % Ho);
-        const int n = static_cast<int>(pix / (static_cast<int64_t>(Wo) * Ho));
+        const int n = static_cast<int>(pix / (static_cast<I>(Wo) * Ho));
         float m[8];
         int at[8];
 #pragma unroll
@@ -315,7 +317,7 @@ __global__ void maxpool_fwd_kernel(const T* __restrict__ x, int N, int H, int W,
                 for (int j = 0; j < 8; ++j)
                     if (at[j] < 0 || v[j] > m[j]) { m[j] = v[j]; at[j] = r * k + q; }
             }
-        st8<T>(y + e * 8, m);
+        st8<T>(y + static_cast<int64_t>(e) * 8, m);
         uint64_t pk = 0;
 #pragma unroll
         for (int j = 0; j < 8; ++j) pk |= static_cast<uint64_t>(at[j] & 0xff) << (8 * j);
@@ -323,17 +325,17 @@ __global__ void maxpool_fwd_kernel(const T* __restrict__ x, int N, int H, int W,
     }
 }
 
-template <class T>
+template <class T, class I>
 __global__ void maxpool_bwd_kernel(const T* __restrict__ dy, const uint8_t* __restrict__ am, int N, int H, int W, int C,
                                    int k, int s, int p, int Ho, int Wo, T* __restrict__ dx) {
     const int C8 = C / 8;
-    const int64_t total = static_cast<int64_t>(N) * H * W * C8;
-    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
-         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const I total = static_cast<I>(N) * H * W * C8;
+    for (I e = blockIdx.x * static_cast<I>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<I>(gridDim.x) * blockDim.x) {
         const int c8 = static_cast<int>(e % C8);
-        const int64_t pix = e / C8;
+        const I pix = e / C8;
         const int iw = static_cast<int>(pix % W), ih = static_cast<int>((pix / W) % H);
-        const int n = static_cast<int>(pix / (static_cast<int64_t>(W) * H));
+        const int n = static_cast<int>(pix / (static_cast<I>(W) * H));
         float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         const int oh_lo = max(0, (ih + p - k + s) / s), oh_hi = min(Ho - 1, (ih + p) / s);
         const int ow_lo = max(0, (iw + p - k + s) / s), ow_hi = min(Wo - 1, (iw + p) / s);
@@ -349,7 +351,7 @@ __global__ void maxpool_bwd_kernel(const T* __restrict__ dy, const uint8_t* __re
                 for (int j = 0; j < 8; ++j)
                     if (static_cast<int>((pk >> (8 * j)) & 0xff) == r * k + q) acc[j] += g[j];
             }
-        st8<T>(dx + e * 8, acc);
+        st8<T>(dx + static_cast<int64_t>(e) * 8, acc);
     }
 }
 
@@ -374,19 +376,31 @@ __global__ void avgpool_fwd_kernel(const T* __restrict__ x, int N, int HW, int C
     }
 }
 
-template <class T>
-__global__ void avgpool_bwd_kernel(const T* __restrict__ dy, int N, int HW, int C, float inv, T* __restrict__ dx) {
+// y (optional): the activation backward of the pooled tensor's producer fused
+// in, exactly as the separate act_bwd pass on the rounded pooling gradient
+template <class T, class I>
+__global__ void avgpool_bwd_kernel(const T* __restrict__ dy, int N, int HW, int C, float inv, T* __restrict__ dx,
+                                   const T* __restrict__ y, float neg) {
     const int C8 = C / 8;
-    const int64_t total = static_cast<int64_t>(N) * HW * C8;
-    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
-         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const I total = static_cast<I>(N) * HW * C8;
+    for (I e = blockIdx.x * static_cast<I>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<I>(gridDim.x) * blockDim.x) {
         const int c8 = static_cast<int>(e % C8);
-        const int64_t n = e / (static_cast<int64_t>(HW) * C8);
+        const I n = e / (static_cast<I>(HW) * C8);
         float g[8];
-        ld8<T>(dy + (n * C8 + c8) * 8, g);
+        ld8<T>(dy + (static_cast<int64_t>(n) * C8 + c8) * 8, g);
 #pragma unroll
         for (int j = 0; j < 8; ++j) g[j] = g[j] * inv;
-        st8<T>(dx + e * 8, g);
+        if (y) {
+            float v[8];
+            ld8<T>(y + static_cast<int64_t>(e) * 8, v);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const float r = to_f<T>(from_f<T>(g[j]));
+                g[j] = v[j] > 0.f ? r : neg * r;  // src/autograd.cpp:340-351
+            }
+        }
+        st8<T>(dx + static_cast<int64_t>(e) * 8, g);
     }
 }
 
@@ -855,16 +869,27 @@ cudaError_t roialign_bwd(int dtype, const void* dy, int N, int H, int W, int C, 
     return cudaGetLastError();
 }
 
+// 32-bit element indexing when the grid-stride range fits (with room for the stride step)
+template <class F>
+void launch_idx(int64_t total, F&& f) {
+    if (total + static_cast<int64_t>(grid_for(total)) * 256 < (int64_t{1} << 31)) f(int32_t{0});
+    else f(int64_t{0});
+}
+
 cudaError_t maxpool_fwd(int dtype, const void* x, int N, int H, int W, int C, int k, int s, int p, void* y,
                         uint8_t* argmax, cudaStream_t st) {
     const int Ho = (H + 2 * p - k) / s + 1, Wo = (W + 2 * p - k) / s + 1;
     const int64_t total = static_cast<int64_t>(N) * Ho * Wo * (C / 8);
     if (dtype == kF16)
-        maxpool_fwd_kernel<__half><<<grid_for(total), 256, 0, st>>>(cp<__half>(x), N, H, W, C, k, s, p, Ho, Wo,
-                                                                    static_cast<__half*>(y), argmax);
+        launch_idx(total, [&](auto idx) {
+            maxpool_fwd_kernel<__half, decltype(idx)><<<grid_for(total), 256, 0, st>>>(
+                cp<__half>(x), N, H, W, C, k, s, p, Ho, Wo, static_cast<__half*>(y), argmax);
+        });
     else
-        maxpool_fwd_kernel<float><<<grid_for(total), 256, 0, st>>>(cp<float>(x), N, H, W, C, k, s, p, Ho, Wo,
-                                                                   static_cast<float*>(y), argmax);
+        launch_idx(total, [&](auto idx) {
+            maxpool_fwd_kernel<float, decltype(idx)><<<grid_for(total), 256, 0, st>>>(
+                cp<float>(x), N, H, W, C, k, s, p, Ho, Wo, static_cast<float*>(y), argmax);
+        });
     return cudaGetLastError();
 }
 
@@ -873,11 +898,15 @@ cudaError_t maxpool_bwd(int dtype, const void* dy, const uint8_t* argmax, int N,
     const int Ho = (H + 2 * p - k) / s + 1, Wo = (W + 2 * p - k) / s + 1;
     const int64_t total = static_cast<int64_t>(N) * H * W * (C / 8);
     if (dtype == kF16)
-        maxpool_bwd_kernel<__half><<<grid_for(total), 256, 0, st>>>(cp<__half>(dy), argmax, N, H, W, C, k, s, p, Ho, Wo,
-                                                                    static_cast<__half*>(dx));
+        launch_idx(total, [&](auto idx) {
+            maxpool_bwd_kernel<__half, decltype(idx)><<<grid_for(total), 256, 0, st>>>(
+                cp<__half>(dy), argmax, N, H, W, C, k, s, p, Ho, Wo, static_cast<__half*>(dx));
+        });
     else
-        maxpool_bwd_kernel<float><<<grid_for(total), 256, 0, st>>>(cp<float>(dy), argmax, N, H, W, C, k, s, p, Ho, Wo,
-                                                                   static_cast<float*>(dx));
+        launch_idx(total, [&](auto idx) {
+            maxpool_bwd_kernel<float, decltype(idx)><<<grid_for(total), 256, 0, st>>>(
+                cp<float>(dy), argmax, N, H, W, C, k, s, p, Ho, Wo, static_cast<float*>(dx));
+        });
     return cudaGetLastError();
 }
 
@@ -890,14 +919,20 @@ cudaError_t avgpool_fwd(int dtype, const void* x, int N, int HW, int C, void* y,
     return cudaGetLastError();
 }
 
-cudaError_t avgpool_bwd(int dtype, const void* dy, int N, int HW, int C, void* dx, cudaStream_t st) {
+cudaError_t avgpool_bwd(int dtype, const void* dy, int N, int HW, int C, void* dx, cudaStream_t st, const void* act_y,
+                        float neg) {
     const int64_t total = static_cast<int64_t>(N) * HW * (C / 8);
     const float inv = static_cast<float>(1.0 / static_cast<double>(HW));  // src/autograd.cpp:381-384
     if (dtype == kF16)
-        avgpool_bwd_kernel<__half><<<grid_for(total), 256, 0, st>>>(cp<__half>(dy), N, HW, C, inv,
-                                                                    static_cast<__half*>(dx));
+        launch_idx(total, [&](auto idx) {
+            avgpool_bwd_kernel<__half, decltype(idx)><<<grid_for(total), 256, 0, st>>>(
+                cp<__half>(dy), N, HW, C, inv, static_cast<__half*>(dx), cp<__half>(act_y), neg);
+        });
     else
-        avgpool_bwd_kernel<float><<<grid_for(total), 256, 0, st>>>(cp<float>(dy), N, HW, C, inv, static_cast<float*>(dx));
+        launch_idx(total, [&](auto idx) {
+            avgpool_bwd_kernel<float, decltype(idx)><<<grid_for(total), 256, 0, st>>>(
+                cp<float>(dy), N, HW, C, inv, static_cast<float*>(dx), cp<float>(act_y), neg);
+        });
     return cudaGetLastError();
 }
 
