@@ -97,6 +97,12 @@ cudaError_t roialign_bwd(int dtype, const void* dy, int N, int H, int W, int C, 
                          float scale, int sr, void* dfeat, cudaStream_t st, int step = 1);
 // [n][3][H][W] (the reference image layout) -> NHWC with Cp channels (zero padded)
 cudaError_t nchw3_to_nhwc(int dtype, const void* in, int n, int H, int W, int Cp, void* out, cudaStream_t st);
+// the 7x7 stem as a 1x1 GEMM over its im2col matrix X' [pixels][192] (fp16):
+// stem_im2col builds X'; stem_weights packs W [K][7][7][Cs] -> W' [K][192]
+// (fold = 1: dW' -> dW, zeros for the padded channels)
+cudaError_t stem_im2col(const void* x, int N, int H, int W, int Cs, int Ho, int Wo, int stride, int pad, void* out,
+                        cudaStream_t st);
+cudaError_t stem_weights(const void* w, int K, int Cs, void* w2, int fold, cudaStream_t st);
 cudaError_t maxpool_fwd(int dtype, const void* x, int N, int H, int W, int C, int k, int s, int p, void* y,
                         uint8_t* argmax, cudaStream_t st);
 cudaError_t maxpool_bwd(int dtype, const void* dy, const uint8_t* argmax, int N, int H, int W, int C, int k, int s,

@@ -157,6 +157,10 @@ struct sdb_det {
     ConvL stem;
     NormL stem_n;
     Act img, stem_z, stem_a, pool;
+    // fp16: the stem as a 1x1 GEMM over its im2col matrix (stem2.g = [1][1][pixels][192] -> 64)
+    bool stem_gemm = false;
+    ConvL stem2;
+    void *stem_x2 = nullptr, *stem_w2 = nullptr, *stem_dw2 = nullptr;
     uint8_t* pool_arg = nullptr;
     std::vector<Block> backbone, head;
     ConvL rpn_conv, rpn_cls, rpn_bbox, fc_cls, fc_bbox;
@@ -427,6 +431,7 @@ size_t max_ws(sdb_det* d) {
     auto conv_ws = [&](const ConvL& c) { m = std::max(m, conv_wgrad_workspace(c.g, d->dt)); };
     auto norm_ws = [&](const NormL& n, int64_t rows) { m = std::max(m, norm_workspace_bytes(rows, n.C)); };
     conv_ws(d->stem);
+    if (d->stem_gemm) conv_ws(d->stem2);
     norm_ws(d->stem_n, static_cast<int64_t>(d->stem_z.n) * d->stem_z.h * d->stem_z.w);
     for (auto* st : {&d->backbone, &d->head})
         for (auto& b : *st) {
@@ -568,8 +573,10 @@ void grads_ready(Bwd& B, int pi) {
     }
 }
 
-void conv_wgrad_to(Bwd& B, const ConvL& c, const Act& x, const void* dy) {
+void conv_wgrad_to(Bwd& B, const ConvL& c, const Act& x, const void* dy, void* dw_override = nullptr,
+                   bool ready = true) {
     sdb_det* d = B.d;
+    void* dwp = dw_override ? dw_override : d->gptr(c.p);
     {
     PScope ps(d, P_WGRAD, conv_flops(c.g), 0, 2);
     if (d->prof.on) { ps.label = shape_label("wgrad", c.g); ps.flops_ = conv_flops(c.g); }
@@ -583,7 +590,7 @@ void conv_wgrad_to(Bwd& B, const ConvL& c, const Act& x, const void* dy) {
             ws = d->wst;
         }
         WgradJob job{};
-        CK(conv_wgrad_deferred(c.g, d->dt, x.p, dy, d->gptr(c.p), d->wg_arena + it->second,
+        CK(conv_wgrad_deferred(c.g, d->dt, x.p, dy, dwp, d->wg_arena + it->second,
                                conv_wgrad_workspace(c.g, d->dt), ws, &job));
         d->wg_jobs.push_back(job);
         if (B.side && B.slot >= 0 && dy == d->dzr[B.slot]) {
@@ -592,10 +599,23 @@ void conv_wgrad_to(Bwd& B, const ConvL& c, const Act& x, const void* dy) {
             B.slot = -1;
         }
     } else {
-        CK(conv_wgrad(c.g, d->dt, x.p, dy, d->gptr(c.p), d->ws, d->ws_bytes, d->ctx->stream));
+        CK(conv_wgrad(c.g, d->dt, x.p, dy, dwp, d->ws, d->ws_bytes, d->ctx->stream));
     }
     }
-    grads_ready(B, c.p);
+    if (ready) grads_ready(B, c.p);
+}
+
+// the stem's GEMM-form wgrad into dW' (stem_dw2); without the deferred reduce
+// it is folded into the gradient right away, else after the batched reduce
+void stem_wgrad_to(Bwd& B, const ConvL& c2, void* x2, const void* dy) {
+    sdb_det* d = B.d;
+    Act xa{};
+    xa.p = x2;
+    conv_wgrad_to(B, c2, xa, dy, d->stem_dw2, false);
+    if (!d->defer_wgrad) {
+        CK(stem_weights(d->stem_dw2, 64, 8, d->gptr(d->stem.p), 1, d->ctx->stream));
+        grads_ready(B, d->stem.p);
+    }
 }
 
 // backward of a bottleneck.  dS = gradient at the residual add node (the
@@ -650,7 +670,20 @@ void run_step(sdb_det* d) {
         CK(cudaEventRecord(d->ev_at_join, d->wst));
     }
     // ---- forward: backbone
-    conv_fwd(d, d->stem, d->img, d->stem_z);
+    if (d->stem_gemm) {
+        {
+            PScope ps(d, P_ELEM, 0, 2.0 * (d->img.numel() + static_cast<double>(d->stem2.g.W) * 192), 3);
+            if (d->prof.on) ps.label = "stem im2col + weight pack";
+            CK(stem_weights(d->wdev_ptr(d->stem.p), 64, 8, d->stem_w2, 0, st));
+            CK(stem_im2col(d->img.p, d->img.n, d->img.h, d->img.w, 8, d->stem_z.h, d->stem_z.w, 2, 3, d->stem_x2,
+                           st));
+        }
+        PScope ps(d, P_FPROP, conv_flops(d->stem2.g));
+        if (d->prof.on) { ps.label = shape_label("fprop(stem gemm)", d->stem2.g); ps.flops_ = conv_flops(d->stem2.g); }
+        CK(conv_fprop(d->stem2.g, d->dt, d->stem_x2, d->stem_w2, d->stem_z.p, st));
+    } else {
+        conv_fwd(d, d->stem, d->img, d->stem_z);
+    }
     norm_fwd(d, d->stem_n, d->stem_z, d->stem_a);
     { PScope ps(d, P_POOL, 0, d->es * (d->stem_a.numel() + d->pool.numel()));
     CK(maxpool_fwd(d->dt, d->stem_a.p, d->stem_a.n, d->stem_a.h, d->stem_a.w, d->stem_a.c, 3, 2, 1, d->pool.p,
@@ -778,7 +811,14 @@ void run_step(sdb_det* d) {
     CK(maxpool_bwd(d->dt, cur, d->pool_arg, d->stem_a.n, d->stem_a.h, d->stem_a.w, d->stem_a.c, 3, 2, 1, spare, st)); }
     void* dstem = dz_buf(B, d->gbuf[0]);
     norm_bwd(d, d->stem_n, d->stem_z, d->stem_a, spare, dstem);
-    conv_wgrad_to(B, d->stem, d->img, dstem);
+    if (d->stem_gemm) {
+        // dW' = X'^T dZ as a 1x1 wgrad; folded back to [64][7][7][8] once reduced
+        ConvL c2 = d->stem2;
+        c2.p = d->stem.p;  // its arena slice / job
+        stem_wgrad_to(B, c2, d->stem_x2, dstem);
+    } else {
+        conv_wgrad_to(B, d->stem, d->img, dstem);
+    }
     if (B.side) {
         CK(cudaEventRecord(d->wev_join, d->wst));
         CK(cudaStreamWaitEvent(st, d->wev_join, 0));
@@ -817,6 +857,7 @@ void run_step(sdb_det* d) {
         d->wg_jobs.clear();
         PScope ps(d, P_WGRAD, 0, 0, 1);
         CK(wgrad_reduce_batched(d->wg_jobs_dev, d->wg_tiles_dev, d->wg_njobs_dev, d->wg_total_tiles, st));
+        if (d->stem_gemm) CK(stem_weights(d->stem_dw2, 64, 8, d->gptr(d->stem.p), 1, st));
     }
     PScope ps_opt(d, P_OPTIM, 0, (d->es + 12.0 + (d->dt == kF16 ? 2.0 : 0.0)) * d->n_w + 16.0 * d->n_bn, 5);
     CK(cudaMemsetAsync(d->flag, 0, sizeof(int), st));
@@ -916,6 +957,15 @@ int sdb_det_create(sdb_ctx* ctx, const sdb_det_config* cfgp, sdb_det** out) {
         d->img = d->act(b, cf.img_h, cf.img_w, 8);
         d->stem.g.N = b; d->stem.g.H = cf.img_h; d->stem.g.W = cf.img_w;
         d->stem_z = d->act(b, d->stem.g.Ho(), d->stem.g.Wo(), 64);
+        d->stem_gemm = d->dt == kF16 && std::getenv("SDB_NO_STEM_GEMM") == nullptr;
+        if (d->stem_gemm) {
+            const int64_t px = d->stem_z.numel() / 64;
+            d->stem2.p = d->stem.p;
+            d->stem2.g = ConvShape{1, 1, static_cast<int>(px), 192, 64, 1, 1, 1, 0};
+            d->stem_x2 = d->alloc(static_cast<size_t>(px) * 192 * 2);
+            d->stem_w2 = d->alloc(64 * 192 * 2);
+            d->stem_dw2 = d->alloc(64 * 192 * 2);
+        }
         d->stem_a = cf.mode == 0 ? d->act(b, d->stem_z.h, d->stem_z.w, 64) : d->stem_z;
         const int ph = (d->stem_a.h + 2 - 3) / 2 + 1, pw = (d->stem_a.w + 2 - 3) / 2 + 1;
         d->pool = d->act(b, ph, pw, 64);
@@ -1030,7 +1080,7 @@ int sdb_det_create(sdb_ctx* ctx, const sdb_det_config* cfgp, sdb_det** out) {
                 d->wg_off[c.p] = off;
                 off += (conv_wgrad_workspace(c.g, d->dt) + 255) & ~size_t(255);
             };
-            add(d->stem);
+            add(d->stem_gemm ? d->stem2 : d->stem);
             for (auto* stg : {&d->backbone, &d->head})
                 for (auto& bl : *stg) {
                     add(bl.c1); add(bl.c2); add(bl.c3);

@@ -1057,6 +1057,102 @@ cudaError_t rcnn_smooth_l1(int dtype, const void* pred, int R, int ld, const int
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- stem as a GEMM
+// The 7x7 stride-2 stem sees 3 real input channels (of 8 stored): its im2col
+// matrix X' [pixels][192] (column j = r*24 + s*3 + c for c < 3, zeros
+// elsewhere) turns fprop and wgrad into 1x1 tensor-core GEMMs with 64-wide
+// K blocks (src/tensor.cpp:178-194 semantics; accumulation order differs).
+constexpr int kStemK = 7, kStemCols = 192;
+
+// One CTA per (image row of output, 64 output columns): the 7 input rows x
+// 133 input columns it needs (3 real channels, read as 8-byte pixel heads) are
+// staged in shared memory once, the segment's 64 x 192 output block (one
+// contiguous 24 KB run of X') is assembled in shared memory and leaves with a
+// single bulk copy.
+constexpr int kStemSeg = 64;
+__global__ void __launch_bounds__(256) stem_im2col_kernel(const __half* __restrict__ x, int N, int H, int W, int Cs,
+                                                          int Ho, int Wo, int stride, int pad,
+                                                          __half* __restrict__ out) {
+    constexpr int kCols = (kStemSeg - 1) * 2 + kStemK;  // input columns of a segment (stride 2)
+    __shared__ uint2 patch[kStemK][kCols];
+    __shared__ __align__(128) uint4 ob[kStemSeg * kStemCols / 8];
+    const int oh = blockIdx.y % Ho, n = blockIdx.y / Ho;
+    const int ow0 = blockIdx.x * kStemSeg;
+    const int ih0 = oh * stride - pad, iw0 = ow0 * stride - pad;
+    for (int i = threadIdx.x; i < kStemK * kCols; i += blockDim.x) {
+        const int rr = i / kCols, cc = i - rr * kCols;
+        const int ih = ih0 + rr, iw = iw0 + cc;
+        uint2 v = make_uint2(0u, 0u);
+        if (ih >= 0 && ih < H && iw >= 0 && iw < W)
+            v = *reinterpret_cast<const uint2*>(x + ((static_cast<int64_t>(n) * H + ih) * W + iw) * Cs);
+        patch[rr][cc] = v;
+    }
+    __syncthreads();
+    const int npx = min(kStemSeg, Wo - ow0);
+    for (int i = threadIdx.x; i < kStemSeg * 8; i += blockDim.x) {
+        const int j = i >> 3, r = i & 7;  // output column in the segment, tap row (7 = zero pad chunk)
+        __half v[24];
+#pragma unroll
+        for (int k = 0; k < 24; ++k) v[k] = __float2half_rn(0.f);
+        if (r < kStemK) {
+#pragma unroll
+            for (int q = 0; q < kStemK; ++q) {
+                const uint2 u = patch[r][j * stride + q];
+                const __half* h = reinterpret_cast<const __half*>(&u);
+                v[q * 3] = h[0];
+                v[q * 3 + 1] = h[1];
+                v[q * 3 + 2] = h[2];
+            }
+        }
+        const uint4* src = reinterpret_cast<const uint4*>(v);
+        uint4* o = ob + (j * kStemCols + r * 24) / 8;
+        o[0] = src[0];
+        o[1] = src[1];
+        o[2] = src[2];
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (threadIdx.x == 0 && npx > 0) {
+        const int64_t px0 = (static_cast<int64_t>(n) * Ho + oh) * Wo + ow0;
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out + px0 * kStemCols),
+                     "r"(smem_u32(ob)), "r"(npx * kStemCols * 2)
+                     : "memory");
+        bulk_commit();
+        bulk_wait_all();
+    }
+}
+
+// W [K][7][7][Cs] -> W' [K][192] (and the transposed fold of dW' back)
+__global__ void stem_wrepack_kernel(const __half* __restrict__ w, int K, int Cs, __half* __restrict__ w2, int fold) {
+    const int total = K * kStemK * kStemK * Cs;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+        const int c = e % Cs, rs = (e / Cs) % (kStemK * kStemK), k = e / (Cs * kStemK * kStemK);
+        const int r = rs / kStemK, q = rs % kStemK;
+        const int j = k * kStemCols + r * 24 + q * 3 + c;
+        if (fold) w2[e] = c < 3 ? w[j] : __float2half_rn(0.f);  // here w = dW', w2 = dW (KRSC)
+        else if (c < 3) w2[j] = w[e];
+    }
+}
+
+cudaError_t stem_im2col(const void* x, int N, int H, int W, int Cs, int Ho, int Wo, int stride, int pad, void* out,
+                        cudaStream_t st) {
+    if (stride != 2) return cudaErrorNotSupported;  // the segment staging assumes the stem's stride
+    const dim3 grid((Wo + kStemSeg - 1) / kStemSeg, N * Ho);
+    stem_im2col_kernel<<<grid, 256, 0, st>>>(cp<__half>(x), N, H, W, Cs, Ho, Wo, stride, pad,
+                                             static_cast<__half*>(out));
+    return cudaGetLastError();
+}
+
+cudaError_t stem_weights(const void* w, int K, int Cs, void* w2, int fold, cudaStream_t st) {
+    if (!fold) {
+        const cudaError_t e = cudaMemsetAsync(w2, 0, static_cast<size_t>(K) * kStemCols * 2, st);
+        if (e != cudaSuccess) return e;
+    }
+    const int total = K * kStemK * kStemK * Cs;
+    stem_wrepack_kernel<<<(total + 255) / 256, 256, 0, st>>>(cp<__half>(w), K, Cs, static_cast<__half*>(w2), fold);
+    return cudaGetLastError();
+}
+
 cudaError_t nchw3_to_nhwc(int dtype, const void* in, int n, int H, int W, int Cp, void* out, cudaStream_t st) {
     const int64_t total = static_cast<int64_t>(n) * H * W;
     if (dtype == kF16)
