@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -86,7 +87,12 @@ int sdb_ctx_create(int device, int rank, int world, const void* nccl_id, sdb_ctx
     c->device = device;
     c->rank = rank;
     c->world = world;
-    if (int rc = cuda_status(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream")) {
+    // the step's critical chain runs on this stream: above the side stream that
+    // carries the overlapped wgrads (least priority), below the comm stream
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    const int prio = std::getenv("SDB_FLAT_PRIORITY") ? 0 : (hi < lo ? hi + 1 : hi);
+    if (int rc = cuda_status(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio), "stream")) {
         delete c;
         return rc;
     }

@@ -1115,7 +1115,9 @@ int sdb_det_create(sdb_ctx* ctx, const sdb_det_config* cfgp, sdb_det** out) {
 
         // ---- comm: fp16 buckets from the end of the flat gradient (backward order)
         if (ctx->world > 1) {
-            CK(cudaStreamCreateWithPriority(&d->comm, cudaStreamNonBlocking, -1));
+            int plo = 0, phi = 0;
+            CK(cudaDeviceGetStreamPriorityRange(&plo, &phi));
+            CK(cudaStreamCreateWithPriority(&d->comm, cudaStreamNonBlocking, phi));
             CK(cudaEventCreateWithFlags(&d->ev_fork, cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&d->ev_join, cudaEventDisableTiming));
             const int64_t cap = static_cast<int64_t>(cf.bucket_mb * 1024 * 1024 / d->es);
