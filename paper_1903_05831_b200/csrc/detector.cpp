@@ -189,6 +189,11 @@ struct sdb_det {
     // at the start of the step, behind the backbone forward
     void* ws_at = nullptr;
     cudaEvent_t ev_at_fork = nullptr, ev_at_join = nullptr;
+    // the RPN losses and RPN head backward (all but the rpn_conv dgrad, which
+    // accumulates onto the RoIAlign gradient) also run there, while the main
+    // stream is in the latency-bound proposal layer and the RoI head
+    cudaEvent_t ev_rpn_fork = nullptr, ev_rpn_join = nullptr;
+    void* drpn_side = nullptr;
     cudaEvent_t dzr_ev[kDzRing] = {};
     bool dzr_busy[kDzRing] = {};
     int dzr_next = 0;
@@ -653,6 +658,43 @@ void block_bwd(Bwd& B, Block& b, const void* dS, void* dx, void* s1, void* s2, c
     else dgrad(d, b.c1, z, dx, 1, dS, in_mask, neg, in_bits);
 }
 
+// RPN losses + RPN head backward on the side stream (see sdb_det::ev_rpn_fork);
+// leaves the RPN-conv input gradient in d->drpn_side
+void rpn_branch_side(sdb_det* d) {
+    const auto& cf = d->cfg;
+    cudaStream_t s2 = d->wst;
+    LossArgs la{d->scale, d->losses, 0};
+    CK(sigmoid_bce(d->dt, d->rpn_logits.p, static_cast<int64_t>(d->n_loc) * cf.batch, d->A, d->A_pad, d->a_labels,
+                   d->d_rpn_logits, la, d->ws_at, s2));
+    la.slot = 1;
+    CK(rpn_smooth_l1(d->dt, d->rpn_deltas.p, static_cast<int64_t>(d->n_loc) * cf.batch, d->A, d->A_pad, d->a_labels,
+                     d->a_targets, 1.0 / 9.0, static_cast<double>(cf.rpn_batch) * cf.batch, d->d_rpn_deltas, la,
+                     d->ws_at, s2));
+    auto wgrad = [&](const ConvL& c, const void* x, const void* dy) {
+        WgradJob job{};
+        CK(conv_wgrad_deferred(c.g, d->dt, x, dy, d->gptr(c.p), d->wg_arena + d->wg_off.at(c.p),
+                               conv_wgrad_workspace(c.g, d->dt), s2, &job));
+        d->wg_jobs.push_back(job);
+    };
+    wgrad(d->rpn_bbox, d->rpn_a.p, d->d_rpn_deltas);
+    wgrad(d->rpn_cls, d->rpn_a.p, d->d_rpn_logits);
+    // the RPN ReLU backward folded into the dgrad that writes drpn last (K % 64 == 0)
+    const bool bbox_last = (d->rpn_bbox.g.K % 64) == 0;
+    const ConvL& r_first = bbox_last ? d->rpn_cls : d->rpn_bbox;
+    const ConvL& r_last = bbox_last ? d->rpn_bbox : d->rpn_cls;
+    CK(conv_dgrad(r_first.g, d->dt, bbox_last ? d->d_rpn_logits : d->d_rpn_deltas, d->wdev_ptr(r_first.p),
+                  d->drpn_side, 0, s2));
+    if ((r_last.g.K % 64) == 0) {
+        CK(conv_dgrad(r_last.g, d->dt, bbox_last ? d->d_rpn_deltas : d->d_rpn_logits, d->wdev_ptr(r_last.p),
+                      d->drpn_side, 1, s2, nullptr, d->rpn_a.p, 0.0f));
+    } else {
+        CK(conv_dgrad(r_last.g, d->dt, bbox_last ? d->d_rpn_deltas : d->d_rpn_logits, d->wdev_ptr(r_last.p),
+                      d->drpn_side, 1, s2));
+        CK(act_bwd(d->dt, d->drpn_side, d->rpn_a.p, d->drpn_side, d->rpn_a.numel(), 0.0f, s2));
+    }
+    wgrad(d->rpn_conv, d->c4.p, d->drpn_side);
+}
+
 // ------------------------------------------------------------------ the step
 void run_step(sdb_det* d) {
     cudaStream_t st = d->ctx->stream;
@@ -695,6 +737,13 @@ void run_step(sdb_det* d) {
     CK(relu_fwd(d->dt, d->rpn_z.p, d->rpn_a.p, d->rpn_a.numel(), st)); }
     conv_fwd(d, d->rpn_cls, d->rpn_a, d->rpn_logits);
     conv_fwd(d, d->rpn_bbox, d->rpn_a, d->rpn_deltas);
+    if (side) {
+        // wst already holds the anchor targets; add the RPN losses and head backward
+        CK(cudaEventRecord(d->ev_rpn_fork, st));
+        CK(cudaStreamWaitEvent(d->wst, d->ev_rpn_fork, 0));
+        rpn_branch_side(d);
+        CK(cudaEventRecord(d->ev_rpn_join, d->wst));
+    }
     // ---- targets and proposals (no gradient)
     if (!side) { PScope ps(d, P_TARGETS, 0, 0, 5); CK(anchor_targets(at, d->ws, st)); }
     ProposalArgs pa{};
@@ -724,19 +773,20 @@ void run_step(sdb_det* d) {
     conv_fwd(d, d->fc_cls, d->pooled, d->cls_logits);
     conv_fwd(d, d->fc_bbox, d->pooled, d->bbox_pred);
     // ---- losses (scale folded into backward)
-    if (side) CK(cudaStreamWaitEvent(st, d->ev_at_join, 0));
     CK(cudaMemcpyAsync(d->scale_used, d->scale, 8, cudaMemcpyDeviceToDevice, st));
     void* g0 = d->d_cls;
     void* g1 = d->d_bbox;
     {
     PScope ps_loss(d, P_LOSS, 0, 0, 4);
     LossArgs la{d->scale, d->losses, 0};
-    CK(sigmoid_bce(d->dt, d->rpn_logits.p, static_cast<int64_t>(d->n_loc) * cf.batch, d->A, d->A_pad, d->a_labels,
-                   d->d_rpn_logits, la, d->ws, st));
-    la.slot = 1;
-    CK(rpn_smooth_l1(d->dt, d->rpn_deltas.p, static_cast<int64_t>(d->n_loc) * cf.batch, d->A, d->A_pad, d->a_labels,
-                     d->a_targets, 1.0 / 9.0, static_cast<double>(cf.rpn_batch) * cf.batch, d->d_rpn_deltas, la,
-                     d->ws, st));
+    if (!side) {
+        CK(sigmoid_bce(d->dt, d->rpn_logits.p, static_cast<int64_t>(d->n_loc) * cf.batch, d->A, d->A_pad,
+                       d->a_labels, d->d_rpn_logits, la, d->ws, st));
+        la.slot = 1;
+        CK(rpn_smooth_l1(d->dt, d->rpn_deltas.p, static_cast<int64_t>(d->n_loc) * cf.batch, d->A, d->A_pad,
+                         d->a_labels, d->a_targets, 1.0 / 9.0, static_cast<double>(cf.rpn_batch) * cf.batch,
+                         d->d_rpn_deltas, la, d->ws, st));
+    }
     la.slot = 2;
     CK(softmax_ce(d->dt, d->cls_logits.p, d->R, d->ncls, d->ncls_pad, d->roi_labels, g0, la, d->ws, st));
     la.slot = 3;
@@ -778,6 +828,13 @@ void run_step(sdb_det* d) {
     CK(roialign_bwd(d->dt, cur, d->c4.n, d->c4.h, d->c4.w, d->c4.c, d->rois, d->R, d->P, sscale, cf.sampling_ratio,
                     dc4, st, d->roi_step)); }
     // RPN head backward (bbox, cls, conv)
+    if (side) {
+        // done on the side stream behind the proposal layer: only the rpn_conv
+        // dgrad (onto the RoIAlign gradient, then the c4 activation mask) is left
+        CK(cudaStreamWaitEvent(st, d->ev_rpn_join, 0));
+        dgrad(d, d->rpn_conv, d->drpn_side, dc4, 1, nullptr, d->c4.p, neg,
+              d->backbone.empty() ? nullptr : d->backbone.back().obits);
+    } else {
     void* drpn = dz_buf(B, d->gbuf[0]);
     conv_wgrad_to(B, d->rpn_bbox, d->rpn_a, d->d_rpn_deltas);
     conv_wgrad_to(B, d->rpn_cls, d->rpn_a, d->d_rpn_logits);
@@ -797,6 +854,7 @@ void run_step(sdb_det* d) {
     conv_wgrad_to(B, d->rpn_conv, d->c4, drpn);
     // dc4 (RoIAlign part) + RPN part, then the last backbone block's activation mask
     dgrad(d, d->rpn_conv, drpn, dc4, 1, nullptr, d->c4.p, neg, d->backbone.empty() ? nullptr : d->backbone.back().obits);
+    }
     // backbone
     cur = dc4;
     spare = dc4 == d->gbuf[2] ? d->gbuf[3] : d->gbuf[2];
@@ -1099,6 +1157,9 @@ int sdb_det_create(sdb_ctx* ctx, const sdb_det_config* cfgp, sdb_det** out) {
             CK(cudaEventCreateWithFlags(&d->wev_join, cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&d->ev_at_fork, cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&d->ev_at_join, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&d->ev_rpn_fork, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&d->ev_rpn_join, cudaEventDisableTiming));
+            d->drpn_side = d->alloc(static_cast<size_t>(d->rpn_a.numel()) * d->es);
             d->ws_at = d->alloc(anchor_target_workspace_bytes(cf.batch, d->nA, cf.max_gt));
             for (int k = 0; k < sdb_det::kDzRing; ++k) {
                 d->dzr[k] = d->alloc(static_cast<size_t>(d->gbuf_elems) * d->es);
@@ -1162,6 +1223,8 @@ int sdb_det_destroy(sdb_det* d) {
         cudaEventDestroy(d->wev_join);
         cudaEventDestroy(d->ev_at_fork);
         cudaEventDestroy(d->ev_at_join);
+        cudaEventDestroy(d->ev_rpn_fork);
+        cudaEventDestroy(d->ev_rpn_join);
         cudaStreamDestroy(d->wst);
     }
     if (d->comm) {
