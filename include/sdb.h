@@ -86,6 +86,19 @@ int sdb_bn_bwd(sdb_ctx* ctx, int dtype, const void* dy, const void* x, const voi
                const float* mean, const float* invstd, void* dx, float* dgamma, float* dbeta, int64_t rows, int C,
                void* stream);
 
+/* ---- SyncBN across the context's ranks: syncbn_forward/backward with a group
+ * (src/syncbn.cpp:21-117).  Forward: per-rank FP64 sums rounded to float into
+ * agg[2C+1] = [sum, sumsq, count] (device, caller-owned; keep it for the
+ * backward), one fp32 SUM allreduce over the ranks (NCCL on `stream`; identity
+ * at world 1), mean/invstd from the global sums.  Backward: red[2C] = [sum dy,
+ * sum dy*xhat] allreduced the same way; dgamma/dbeta are the GLOBAL sums, as in
+ * the reference -- a caller must not allreduce them again (the reference
+ * trainer does). rows = this rank's N*H*W. */
+int sdb_syncbn_fwd(sdb_ctx* ctx, int dtype, const void* x, const float* gamma, const float* beta, void* y,
+                   float* mean, float* invstd, float* agg, int64_t rows, int C, float eps, int relu, void* stream);
+int sdb_syncbn_bwd(sdb_ctx* ctx, int dtype, const void* dy, const void* x, const void* y_relu, const float* gamma,
+                   const float* mean, const float* invstd, const float* agg_fwd, float* red, void* dx, float* dgamma,
+                   float* dbeta, int64_t rows, int C, void* stream);
 /* ---- InPlace-ABN: iabn_forward / iabn_backward (src/memopt.cpp:226-327).
  * Backward recomputes from the OUTPUT y only. */
 int sdb_iabn_fwd(sdb_ctx* ctx, int dtype, const void* x, const float* gamma, const float* beta, void* y, float* mean,

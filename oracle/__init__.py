@@ -50,6 +50,9 @@ _ORC_SIGS = {
     "orc_maxpool_bwd": (None, [_P, _P, _I, _I, _I, _I, _I, _I, _I, _P]),
     "orc_avgpool_fwd": (None, [_P, _I, _I, _I, _I, _P]),
     "orc_avgpool_bwd": (None, [_P, _I, _I, _I, _I, _P]),
+    "orc_ring_allreduce_sum": (None, [_P, _I, _L]),
+    "orc_syncbn_forward_k": (None, [_I, _P, _I, _I, _I, _I, _P, _P, _F, _I, _P, _P, _P, _P]),
+    "orc_syncbn_backward_k": (None, [_I, _P, _P, _I, _I, _I, _I, _P, _P, _P, _L, _P, _P, _P]),
 }
 
 _REF_SIGS = {
@@ -61,6 +64,8 @@ _REF_SIGS = {
     "ref_matmul": (_I, [_P, _I, _I, _P, _I, _I, _P, _P, _P, _P]),
     "ref_bn_forward": (_I, [_P, _I, _I, _I, _I, _P, _P, _F, _I, _P, _P, _P]),
     "ref_bn_backward": (_I, [_P, _P, _I, _I, _I, _I, _P, _P, _P, _I, _P, _P, _P]),
+    "ref_syncbn_forward_k": (_I, [_I, _P, _I, _I, _I, _I, _P, _P, _F, _I, _P, _P, _P, _P]),
+    "ref_syncbn_backward_k": (_I, [_I, _P, _P, _I, _I, _I, _I, _P, _P, _P, _L, _I, _P, _P, _P]),
     "ref_iabn_forward": (_I, [_P, _I, _I, _I, _I, _P, _P, _F, _F, _I, _P, _P, _P]),
     "ref_iabn_backward": (_I, [_P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _F, _F, _I, _P, _P, _P]),
     "ref_iou": (_D, [_P, _P]),

@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "simdet/autograd.hpp"
+#include "simdet/comm.hpp"
 #include "simdet/errors.hpp"
 #include "simdet/half.hpp"
 #include "simdet/memopt.hpp"
@@ -135,6 +136,53 @@ int ref_bn_backward(const float* dy, const float* x, int N, int C, int H, int W,
         put(g.dx, dx);
         std::memcpy(dgamma, g.dgamma.data(), C * sizeof(float));
         std::memcpy(dbeta, g.dbeta.data(), C * sizeof(float));
+    });
+}
+
+// syncbn_forward / syncbn_backward with a K-rank in-process group: the
+// reference's own run_workers + CommGroup ring allreduce (src/comm.cpp:242-315).
+// x_all/dy_all/y_all/dx_all = [K][N][C][H][W]; mean/invstd/sum/sumsq/count and
+// dgamma/dbeta are rank 0's (all ranks agree bitwise).
+int ref_syncbn_forward_k(int K, const float* x_all, int N, int C, int H, int W, const float* gamma,
+                         const float* beta, float eps, int fp16, float* y_all, float* mean, float* invstd,
+                         float* agg) {
+    return guarded([&] {
+        const int64_t per = static_cast<int64_t>(N) * C * H * W;
+        run_workers(K, make_inproc_transport(K), [&](CommGroup& g) {
+            const int r = g.rank();
+            auto [out, st] = syncbn_forward(mk({N, C, H, W}, fp16, x_all + r * per), std::span<const float>(gamma, C),
+                                            std::span<const float>(beta, C), eps, &g);
+            put(out, y_all + r * per);
+            if (r == 0) {
+                std::memcpy(mean, st.mean.data(), C * sizeof(float));
+                std::memcpy(invstd, st.invstd.data(), C * sizeof(float));
+                std::memcpy(agg, st.sum.data(), C * sizeof(float));
+                std::memcpy(agg + C, st.sumsq.data(), C * sizeof(float));
+                agg[2 * C] = static_cast<float>(st.count);
+            }
+        });
+    });
+}
+
+int ref_syncbn_backward_k(int K, const float* dy_all, const float* x_all, int N, int C, int H, int W,
+                          const float* gamma, const float* mean, const float* invstd, int64_t count, int fp16,
+                          float* dx_all, float* dgamma, float* dbeta) {
+    return guarded([&] {
+        const int64_t per = static_cast<int64_t>(N) * C * H * W;
+        run_workers(K, make_inproc_transport(K), [&](CommGroup& g) {
+            const int r = g.rank();
+            BNStats st;
+            st.count = count;
+            st.mean.assign(mean, mean + C);
+            st.invstd.assign(invstd, invstd + C);
+            BnGrads gr = syncbn_backward(mk({N, C, H, W}, 0, dy_all + r * per), mk({N, C, H, W}, fp16, x_all + r * per),
+                                         st, std::span<const float>(gamma, C), &g);
+            put(gr.dx, dx_all + r * per);
+            if (r == 0) {
+                std::memcpy(dgamma, gr.dgamma.data(), C * sizeof(float));
+                std::memcpy(dbeta, gr.dbeta.data(), C * sizeof(float));
+            }
+        });
     });
 }
 

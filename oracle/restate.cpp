@@ -562,4 +562,114 @@ void orc_avgpool_bwd(const float* dy, int N, int C, int H, int W, float* dx) {
         for (int64_t i = 0; i < static_cast<int64_t>(H) * W; ++i) dx[nc * H * W + i] = dy[nc] / static_cast<float>(H * W);
 }
 
+// ---- SyncBN over K ranks (TEST-ONLY restatement).
+// CommGroup::allreduce_sum (src/comm.cpp:230-240, 288-315): ring reduce-scatter
+// over ring_chunks(n, K); the element of chunk c is left-folded in rank order
+// c, c+1, ..., c+K-1 (mod K), then all-gathered, so every rank holds the same
+// bits.  bufs = [K][n], reduced in place.
+void orc_ring_allreduce_sum(float* bufs, int K, int64_t n) {
+    if (K <= 1) return;
+    const int64_t base = n / K, rem = n % K;
+    int64_t at = 0;
+    for (int c = 0; c < K; ++c) {
+        const int64_t len = base + (c < rem ? 1 : 0);
+        for (int64_t i = at; i < at + len; ++i) {
+            float acc = bufs[static_cast<int64_t>(c) * n + i];
+            for (int j = 1; j < K; ++j) acc = acc + bufs[static_cast<int64_t>((c + j) % K) * n + i];
+            for (int r = 0; r < K; ++r) bufs[static_cast<int64_t>(r) * n + i] = acc;
+        }
+        at += len;
+    }
+}
+
+// syncbn_forward with a K-rank group (src/syncbn.cpp:21-70): x_all = [K][N][C][H][W]
+// (each rank's shard, NCHW); y_all likewise; mean/invstd/agg are the (identical)
+// per-rank results; agg = [sum, sumsq, count] after the allreduce.  fp16: the
+// output is rounded to binary16 (Tensor::quantize).
+void orc_syncbn_forward_k(int K, const float* x_all, int N, int C, int H, int W, const float* gamma,
+                          const float* beta, float eps, int fp16, float* y_all, float* mean, float* invstd,
+                          float* agg) {
+    const int64_t hw = static_cast<int64_t>(H) * W, per = static_cast<int64_t>(N) * C * hw, n = 2 * C + 1;
+    std::vector<float> bufs(static_cast<size_t>(K) * n, 0.0f);
+    for (int r = 0; r < K; ++r) {
+        const float* xd = x_all + r * per;
+        float* a = bufs.data() + static_cast<int64_t>(r) * n;
+        for (int c = 0; c < C; ++c) {
+            double s = 0.0, sq = 0.0;
+            for (int b = 0; b < N; ++b)
+                for (int64_t i = 0; i < hw; ++i) {
+                    const double v = xd[(static_cast<int64_t>(b) * C + c) * hw + i];
+                    s += v;
+                    sq += v * v;
+                }
+            a[c] = static_cast<float>(s);
+            a[C + c] = static_cast<float>(sq);
+        }
+        a[2 * C] = static_cast<float>(static_cast<int64_t>(N) * hw);
+    }
+    orc_ring_allreduce_sum(bufs.data(), K, n);
+    const float* g = bufs.data();
+    std::memcpy(agg, g, static_cast<size_t>(n) * sizeof(float));
+    const int64_t count = static_cast<int64_t>(g[2 * C]);
+    for (int c = 0; c < C; ++c) {
+        const double mu = static_cast<double>(g[c]) / count;
+        double var = static_cast<double>(g[C + c]) / count - mu * mu;
+        if (var < 0.0) var = 0.0;
+        mean[c] = static_cast<float>(mu);
+        invstd[c] = static_cast<float>(1.0 / std::sqrt(var + eps));
+    }
+    for (int r = 0; r < K; ++r)
+        for (int b = 0; b < N; ++b)
+            for (int c = 0; c < C; ++c)
+                for (int64_t i = 0; i < hw; ++i) {
+                    const int64_t at = r * per + (static_cast<int64_t>(b) * C + c) * hw + i;
+                    const float v = gamma[c] * (x_all[at] - mean[c]) * invstd[c] + beta[c];
+                    y_all[at] = fp16 ? orc_half_round(v) : v;
+                }
+}
+
+// syncbn_backward with a K-rank group (src/syncbn.cpp:72-117); count = the
+// forward's GLOBAL count; dgamma/dbeta = the all-reduced sums
+void orc_syncbn_backward_k(int K, const float* dy_all, const float* x_all, int N, int C, int H, int W,
+                           const float* gamma, const float* mean, const float* invstd, int64_t count, float* dx_all,
+                           float* dgamma, float* dbeta) {
+    const int64_t hw = static_cast<int64_t>(H) * W, per = static_cast<int64_t>(N) * C * hw, n = 2 * C;
+    std::vector<float> bufs(static_cast<size_t>(K) * n, 0.0f);
+    for (int r = 0; r < K; ++r) {
+        const float* xd = x_all + r * per;
+        const float* gd = dy_all + r * per;
+        float* red = bufs.data() + static_cast<int64_t>(r) * n;
+        for (int c = 0; c < C; ++c) {
+            double s1 = 0.0, s2 = 0.0;
+            for (int b = 0; b < N; ++b)
+                for (int64_t i = 0; i < hw; ++i) {
+                    const int64_t at = (static_cast<int64_t>(b) * C + c) * hw + i;
+                    const double xh = (xd[at] - mean[c]) * invstd[c];
+                    s1 += gd[at];
+                    s2 += gd[at] * xh;
+                }
+            red[c] = static_cast<float>(s1);
+            red[C + c] = static_cast<float>(s2);
+        }
+    }
+    orc_ring_allreduce_sum(bufs.data(), K, n);
+    const float* red = bufs.data();
+    const float m = static_cast<float>(count);
+    for (int c = 0; c < C; ++c) {
+        dgamma[c] = red[C + c];
+        dbeta[c] = red[c];
+    }
+    for (int r = 0; r < K; ++r)
+        for (int b = 0; b < N; ++b)
+            for (int c = 0; c < C; ++c) {
+                const float gis = gamma[c] * invstd[c];
+                const float s1 = red[c] / m, s2 = red[C + c] / m;
+                for (int64_t i = 0; i < hw; ++i) {
+                    const int64_t at = r * per + (static_cast<int64_t>(b) * C + c) * hw + i;
+                    const float xh = (x_all[at] - mean[c]) * invstd[c];
+                    dx_all[at] = gis * (dy_all[at] - s1 - xh * s2);
+                }
+            }
+}
+
 }  // extern "C"

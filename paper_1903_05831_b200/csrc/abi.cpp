@@ -17,6 +17,10 @@
 #include "detect.h"
 #include "sdb_internal.h"
 
+namespace sdb {
+cudaError_t comm_allreduce_sum(Ctx* c, void* buf, int64_t n, int dtype, cudaStream_t st);
+}
+
 namespace {
 
 thread_local std::string g_err;
@@ -196,6 +200,49 @@ int sdb_bn_bwd(sdb_ctx* ctx, int dtype, const void* dy, const void* x, const voi
     return cuda_status(sdb::bn_backward(dtype, dy, x, y_relu, gamma, mean, invstd, dx, dgamma, dbeta, rows, C, ws,
                                         pick(ctx, stream)),
                        "bn_bwd");
+}
+
+// SyncBN over the context's ranks: local fp64 sums -> float buffer -> one fp32
+// SUM allreduce (NCCL, on the op's stream) -> statistics from the global sums
+int sdb_syncbn_fwd(sdb_ctx* ctx, int dtype, const void* x, const float* gamma, const float* beta, void* y,
+                   float* mean, float* invstd, float* agg, int64_t rows, int C, float eps, int relu, void* stream) {
+    if (!ctx) return fail(SDB_PARAM, "null ctx");
+    if (!agg) return fail(SDB_PARAM, "syncbn_fwd: null reduction buffer");
+    if (int rc = check_dtype(dtype)) return rc;
+    // src/syncbn.cpp:47: the GLOBAL count must be >= 2 (ranks hold equal shards)
+    if (rows * ctx->world < 2) return fail(SDB_DEGENERATE, "syncbn: global batch count < 2 per channel");
+    if (rows < 1 || !sdb::norm_channels_ok(C))
+        return fail(SDB_UNSUPPORTED, "norm kernels need C % 8 == 0, C <= 2048, C | 2048 and rows >= 1");
+    cudaStream_t st = pick(ctx, stream);
+    void* ws = ctx->scratch(sdb::norm_workspace_bytes(rows, C));
+    if (int rc = cuda_status(sdb::syncbn_local_sums(dtype, x, rows, C, agg, ws, st), "syncbn_fwd")) return rc;
+    if (int rc = cuda_status(sdb::comm_allreduce_sum(ctx, agg, 2 * static_cast<int64_t>(C) + 1, sdb::kF32, st),
+                             "syncbn_fwd allreduce"))
+        return rc;
+    return cuda_status(
+        sdb::syncbn_forward_finish(dtype, x, gamma, beta, y, mean, invstd, agg, rows, C, eps, relu ? 1 : 0, st),
+        "syncbn_fwd");
+}
+
+int sdb_syncbn_bwd(sdb_ctx* ctx, int dtype, const void* dy, const void* x, const void* y_relu, const float* gamma,
+                   const float* mean, const float* invstd, const float* agg_fwd, float* red, void* dx, float* dgamma,
+                   float* dbeta, int64_t rows, int C, void* stream) {
+    if (!ctx) return fail(SDB_PARAM, "null ctx");
+    if (!agg_fwd || !red) return fail(SDB_PARAM, "syncbn_bwd: null forward statistics / reduction buffer");
+    if (int rc = check_dtype(dtype)) return rc;
+    if (rows < 1 || !sdb::norm_channels_ok(C))
+        return fail(SDB_UNSUPPORTED, "norm kernels need C % 8 == 0, C <= 2048, C | 2048 and rows >= 1");
+    cudaStream_t st = pick(ctx, stream);
+    void* ws = ctx->scratch(sdb::norm_workspace_bytes(rows, C));
+    if (int rc = cuda_status(
+            sdb::syncbn_backward_local_sums(dtype, dy, x, y_relu, mean, invstd, red, rows, C, ws, st), "syncbn_bwd"))
+        return rc;
+    if (int rc = cuda_status(sdb::comm_allreduce_sum(ctx, red, 2 * static_cast<int64_t>(C), sdb::kF32, st),
+                             "syncbn_bwd allreduce"))
+        return rc;
+    return cuda_status(sdb::syncbn_backward_finish(dtype, dy, x, y_relu, gamma, mean, invstd, red, agg_fwd, dx,
+                                                   dgamma, dbeta, rows, C, ws, st),
+                       "syncbn_bwd");
 }
 
 // iabn_forward's contract checks, src/memopt.cpp:229-235

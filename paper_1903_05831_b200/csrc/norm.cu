@@ -262,6 +262,7 @@ __global__ void __launch_bounds__(kStatThreads, 2) stats_kernel(StatArgs p) {
 
 // MODE 0: BN fwd (sums rounded to float first), 1: IABN fwd (double)
 // MODE 2: BN bwd, 3: IABN bwd  -> coef[0..C) = s1/m, coef[C..2C) = s2/m
+// MODE 4/5: SyncBN fwd/bwd local sums as floats into coef (+ count for 4)
 // Fixed-order parallel reduction of the per-block partials, spread over many
 // SMs (8 channels per CTA): thread (ch, g) of 128 groups loads partial[b][c] for
 // b = g, g+128, g+256 in one L2 round trip and adds them in block order; the
@@ -325,6 +326,14 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const double* __r
         Q += __shfl_xor_sync(0xffffffffu, Q, o);
     }
     if (lane >= kFinCh || c >= C) return;
+    if (mode == 4 || mode == 5) {
+        // SyncBN: this rank's sums rounded to float into the reduction buffer
+        // [S_0..S_{C-1}, Q_0..Q_{C-1}(, count)] (src/syncbn.cpp:27-40 / 83-95)
+        coef[c] = static_cast<float>(S);
+        coef[C + c] = static_cast<float>(Q);
+        if (mode == 4 && c == 0) coef[2 * C] = static_cast<float>(count);
+        return;
+    }
     if (mode == 0 || mode == 1) {
         double mu, var;
         if (mode == 0) {
@@ -508,6 +517,37 @@ __global__ void __launch_bounds__(kStatThreads, 2) apply_kernel(ApplyArgs p, int
     }
 }
 
+// SyncBN statistics from the (all-reduced) float buffer agg = [sum, sumsq,
+// count] -- src/syncbn.cpp:43-57 -- and backward coefficients from red =
+// [sum dy, sum dy*xhat] with the forward's global count (src/syncbn.cpp:98-111)
+__global__ void syncbn_stats_kernel(const float* __restrict__ agg, int C, float eps, float* __restrict__ mean,
+                                    float* __restrict__ invstd) {
+    pdl_wait();
+    pdl_trigger();
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= C) return;
+    const int64_t count = static_cast<int64_t>(agg[2 * C]);
+    const double mu = static_cast<double>(agg[c]) / static_cast<double>(count);
+    double var = static_cast<double>(agg[C + c]) / static_cast<double>(count) - mu * mu;
+    if (var < 0.0) var = 0.0;
+    mean[c] = static_cast<float>(mu);
+    invstd[c] = static_cast<float>(1.0 / sqrt(var + static_cast<double>(eps)));
+}
+
+__global__ void syncbn_coef_kernel(const float* __restrict__ red, const float* __restrict__ agg_fwd, int C,
+                                   float* __restrict__ dgamma, float* __restrict__ dbeta, float* __restrict__ coef) {
+    pdl_wait();
+    pdl_trigger();
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= C) return;
+    const float m = static_cast<float>(static_cast<int64_t>(agg_fwd[2 * C]));
+    const float s1 = red[c], s2 = red[C + c];
+    dgamma[c] = s2;
+    dbeta[c] = s1;
+    coef[c] = s1 / m;
+    coef[C + c] = s2 / m;
+}
+
 struct Plan {
     int nblocks;
     int64_t rpb;
@@ -652,6 +692,63 @@ cudaError_t iabn_backward(int dtype, const void* dy, const void* y, const float*
     aa.a = y; aa.dy = dy; aa.out = dx; aa.gamma = gamma; aa.beta = beta; aa.invstd = invstd; aa.coef = coef;
     aa.slope = slope; aa.n8 = rows * C / 8; aa.C = C;
     return dtype == kF16 ? run_apply<__half, 3, 2>(aa, rows, pl, st) : run_apply<float, 3, 2>(aa, rows, pl, st);
+}
+
+// ---------------------------------------------------------------- SyncBN
+cudaError_t syncbn_local_sums(int dtype, const void* x, int64_t rows, int C, float* agg, void* ws, cudaStream_t st) {
+    const Plan pl = plan_for(rows, C, dtype == kF16 ? 2 : 4);
+    double* partial = static_cast<double*>(ws);
+    StatArgs sa{};
+    sa.a = x; sa.rows = rows; sa.C = C; sa.partial = partial; sa.slope = 1.f;
+    cudaError_t e = dtype == kF16 ? run_stats<__half, 0, 1>(sa, pl, st) : run_stats<float, 0, 1>(sa, pl, st);
+    if (e != cudaSuccess) return e;
+    finalize(partial, pl, C, rows, 0.f, 4, nullptr, nullptr, nullptr, nullptr, agg, st);
+    return cudaGetLastError();
+}
+
+cudaError_t syncbn_forward_finish(int dtype, const void* x, const float* gamma, const float* beta, void* y,
+                                  float* mean, float* invstd, const float* agg, int64_t rows, int C, float eps,
+                                  int act, cudaStream_t st) {
+    cudaError_t e = launch_pdl(syncbn_stats_kernel, dim3((C + 255) / 256), dim3(256), 0, st, agg, C, eps, mean, invstd);
+    if (e != cudaSuccess) return e;
+    const Plan pl = plan_for(rows, C, dtype == kF16 ? 2 : 4);
+    ApplyArgs aa{};
+    aa.a = x; aa.out = y; aa.gamma = gamma; aa.beta = beta; aa.mean = mean; aa.invstd = invstd;
+    aa.slope = 1.f; aa.act = act; aa.n8 = rows * C / 8; aa.C = C;
+    return dtype == kF16 ? run_apply<__half, 0, 1>(aa, rows, pl, st) : run_apply<float, 0, 1>(aa, rows, pl, st);
+}
+
+cudaError_t syncbn_backward_local_sums(int dtype, const void* dy, const void* x, const void* y_mask,
+                                       const float* mean, const float* invstd, float* red, int64_t rows, int C,
+                                       void* ws, cudaStream_t st) {
+    const Plan pl = plan_for(rows, C, dtype == kF16 ? 2 : 4);
+    double* partial = static_cast<double*>(ws);
+    StatArgs sa{};
+    sa.a = x; sa.dy = dy; sa.y = y_mask; sa.mean = mean; sa.invstd = invstd;
+    sa.rows = rows; sa.C = C; sa.partial = partial; sa.slope = 1.f;
+    cudaError_t e;
+    if (y_mask) e = dtype == kF16 ? run_stats<__half, 1, 3>(sa, pl, st) : run_stats<float, 1, 3>(sa, pl, st);
+    else e = dtype == kF16 ? run_stats<__half, 1, 2>(sa, pl, st) : run_stats<float, 1, 2>(sa, pl, st);
+    if (e != cudaSuccess) return e;
+    finalize(partial, pl, C, rows, 0.f, 5, nullptr, nullptr, nullptr, nullptr, red, st);
+    return cudaGetLastError();
+}
+
+cudaError_t syncbn_backward_finish(int dtype, const void* dy, const void* x, const void* y_mask, const float* gamma,
+                                   const float* mean, const float* invstd, const float* red, const float* agg_fwd,
+                                   void* dx, float* dgamma, float* dbeta, int64_t rows, int C, void* ws,
+                                   cudaStream_t st) {
+    float* coef = static_cast<float*>(ws);
+    cudaError_t e = launch_pdl(syncbn_coef_kernel, dim3((C + 255) / 256), dim3(256), 0, st, red, agg_fwd, C, dgamma,
+                               dbeta, coef);
+    if (e != cudaSuccess) return e;
+    const Plan pl = plan_for(rows, C, dtype == kF16 ? 2 : 4);
+    ApplyArgs aa{};
+    aa.a = x; aa.dy = dy; aa.y = y_mask; aa.out = dx; aa.gamma = gamma; aa.mean = mean; aa.invstd = invstd;
+    aa.coef = coef; aa.n8 = rows * C / 8; aa.C = C;
+    if (y_mask)
+        return dtype == kF16 ? run_apply<__half, 2, 3>(aa, rows, pl, st) : run_apply<float, 2, 3>(aa, rows, pl, st);
+    return dtype == kF16 ? run_apply<__half, 2, 2>(aa, rows, pl, st) : run_apply<float, 2, 2>(aa, rows, pl, st);
 }
 
 }  // namespace sdb

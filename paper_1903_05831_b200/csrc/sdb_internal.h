@@ -72,6 +72,20 @@ cudaError_t bn_backward(int dtype, const void* dy, const void* x, const void* y_
                         const float* mean, const float* invstd, void* dx, float* dgamma, float* dbeta, int64_t rows,
                         int C, void* ws, cudaStream_t st);
 bool norm_channels_ok(int C);
+// SyncBN (src/syncbn.cpp:21-117 with a group): the per-rank float sums go to
+// agg [2C+1] (forward: sum, sumsq, count) / red [2C] (backward: sum dy, sum
+// dy*xhat); the caller all-reduces them between the two halves
+cudaError_t syncbn_local_sums(int dtype, const void* x, int64_t rows, int C, float* agg, void* ws, cudaStream_t st);
+cudaError_t syncbn_forward_finish(int dtype, const void* x, const float* gamma, const float* beta, void* y,
+                                  float* mean, float* invstd, const float* agg, int64_t rows, int C, float eps,
+                                  int act, cudaStream_t st);
+cudaError_t syncbn_backward_local_sums(int dtype, const void* dy, const void* x, const void* y_mask,
+                                       const float* mean, const float* invstd, float* red, int64_t rows, int C,
+                                       void* ws, cudaStream_t st);
+cudaError_t syncbn_backward_finish(int dtype, const void* dy, const void* x, const void* y_mask, const float* gamma,
+                                   const float* mean, const float* invstd, const float* red, const float* agg_fwd,
+                                   void* dx, float* dgamma, float* dbeta, int64_t rows, int C, void* ws,
+                                   cudaStream_t st);
 cudaError_t iabn_backward(int dtype, const void* dy, const void* y, const float* gamma, const float* beta,
                           const float* mean, const float* invstd, void* dx, float* dgamma, float* dbeta,
                           int64_t rows, int C, float slope, void* ws, cudaStream_t st);

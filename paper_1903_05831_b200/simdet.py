@@ -32,6 +32,8 @@ _SIGS = {
     "sdb_conv_fprop": [_P, _I, _P, _P, _P] + [_I] * 9 + [_P],
     "sdb_conv_dgrad": [_P, _I, _P, _P, _P] + [_I] * 10 + [_P],
     "sdb_conv_dgrad_act": [_P, _I, _P, _P, _P] + [_I] * 9 + [_P, _P, C.c_float, _P, _P],
+    "sdb_syncbn_fwd": [_P, _I] + [_P] * 7 + [_L, _I, _F, _I, _P],
+    "sdb_syncbn_bwd": [_P, _I] + [_P] * 11 + [_L, _I, _P],
     "sdb_conv_wgrad": [_P, _I, _P, _P, _P] + [_I] * 9 + [_P],
     "sdb_bn_fwd": [_P, _I, _P, _P, _P, _P, _P, _P, _L, _I, _F, _I, _P],
     "sdb_bn_bwd": [_P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _L, _I, _P],
@@ -207,6 +209,33 @@ def syncbn_backward(dy, x, mean, invstd, gamma, y_relu=None):
     dbeta = torch.empty_like(dgamma)
     check(L().sdb_bn_bwd(ctx(), dt(x), ptr(dyn), ptr(xn), ptr(yr), ptr(gamma), ptr(mean), ptr(invstd), ptr(dx),
                          ptr(dgamma), ptr(dbeta), rows, Cc, stream()))
+    return nhwc_to_nchw(dx), dgamma, dbeta
+
+
+def syncbn_forward_group(x, gamma, beta, eps: float, relu: bool = False):
+    """syncbn_forward with the context's ranks as the group (src/syncbn.cpp:21-70):
+    returns (y, mean, invstd, agg) -- agg = [sum, sumsq, count] after the allreduce."""
+    xn, rows, Cc = _bn_io(x)
+    y = torch.empty_like(xn)
+    mean = torch.empty(Cc, device=x.device, dtype=torch.float32)
+    invstd = torch.empty_like(mean)
+    agg = torch.empty(2 * Cc + 1, device=x.device, dtype=torch.float32)
+    check(L().sdb_syncbn_fwd(ctx(), dt(x), ptr(xn), ptr(gamma), ptr(beta), ptr(y), ptr(mean), ptr(invstd), ptr(agg),
+                             rows, Cc, eps, 1 if relu else 0, stream()))
+    return nhwc_to_nchw(y), mean, invstd, agg
+
+
+def syncbn_backward_group(dy, x, mean, invstd, gamma, agg, y_relu=None):
+    """syncbn_backward with the context's ranks as the group (src/syncbn.cpp:72-117)."""
+    xn, rows, Cc = _bn_io(x)
+    dyn = nchw_to_nhwc(dy.to(x.dtype))
+    yr = nchw_to_nhwc(y_relu) if y_relu is not None else None
+    dx = torch.empty_like(xn)
+    dgamma = torch.empty(Cc, device=x.device, dtype=torch.float32)
+    dbeta = torch.empty_like(dgamma)
+    red = torch.empty(2 * Cc, device=x.device, dtype=torch.float32)
+    check(L().sdb_syncbn_bwd(ctx(), dt(x), ptr(dyn), ptr(xn), ptr(yr), ptr(gamma), ptr(mean), ptr(invstd), ptr(agg),
+                             ptr(red), ptr(dx), ptr(dgamma), ptr(dbeta), rows, Cc, stream()))
     return nhwc_to_nchw(dx), dgamma, dbeta
 
 

@@ -198,6 +198,43 @@ def test_bn_fwd_bwd(ref, shape, fp16):
 
 
 @pytest.mark.parametrize("fp16", [False, True])
+@pytest.mark.parametrize("relu", [False, True])
+@pytest.mark.parametrize("shape", [(2, 64, 7, 9), (6, 128, 150, 160)])
+def test_syncbn_group_world1(ref, shape, fp16, relu):
+    """SyncBN through the context's group (sdb_syncbn_fwd/bwd: local sums, NCCL
+    allreduce -- the identity at one rank --, global statistics) is bit-identical
+    to plain BN at world 1; its reduction buffer holds the reference's
+    [sum, sumsq, count] (K = 1 run_workers group)"""
+    from paper_1903_05831_b200 import simdet as sd
+    N, C, H, W = shape
+    rng = np.random.default_rng(C + H + 7)
+    x = _rand(rng, shape, fp16, 2.0) + 0.5
+    x = x.astype(np.float16).astype(np.float32) if fp16 else x
+    g = (1.0 + 0.2 * rng.standard_normal(C)).astype(np.float32)
+    b = (0.1 * rng.standard_normal(C)).astype(np.float32)
+    dy = _rand(rng, shape, fp16)
+    tdt = torch.float16 if fp16 else torch.float32
+    xt, dyt = torch.from_numpy(x).to("cuda", tdt), torch.from_numpy(dy).to("cuda", tdt)
+    gt, bt = torch.from_numpy(g).cuda(), torch.from_numpy(b).cuda()
+    y0, m0, i0 = sd.syncbn_forward(xt, gt, bt, 1e-5, relu=relu)
+    y1, m1, i1, agg = sd.syncbn_forward_group(xt, gt, bt, 1e-5, relu=relu)
+    dx0, dg0, db0 = sd.syncbn_backward(dyt, xt, m0, i0, gt, y_relu=y0 if relu else None)
+    dx1, dg1, db1 = sd.syncbn_backward_group(dyt, xt, m1, i1, gt, agg, y_relu=y1 if relu else None)
+    torch.cuda.synchronize()
+    for a0, a1 in ((y0, y1), (m0, m1), (i0, i1), (dx0, dx1), (dg0, dg1), (db0, db1)):
+        assert torch.equal(a0, a1)
+    y_r = np.zeros((1,) + shape, np.float32)
+    m_r, i_r = np.zeros(C, np.float32), np.zeros(C, np.float32)
+    agg_r = np.zeros(2 * C + 1, np.float32)
+    assert ref.ref_syncbn_forward_k(1, oracle.p(x), N, C, H, W, oracle.p(g), oracle.p(b), 1e-5, int(fp16),
+                                    oracle.p(y_r), oracle.p(m_r), oracle.p(i_r), oracle.p(agg_r)) == 0
+    a = agg.cpu().numpy()
+    assert a[2 * C] == agg_r[2 * C] == N * H * W
+    assert_close(a[:2 * C], agg_r[:2 * C], 1e-6, "local sums")
+    assert_close(m1, m_r, 1e-5, "mean")
+
+
+@pytest.mark.parametrize("fp16", [False, True])
 @pytest.mark.parametrize("slope", [0.1, 1.0])
 @pytest.mark.parametrize("shape", BN_SHAPES)
 def test_iabn_fwd_bwd(ref, shape, fp16, slope):

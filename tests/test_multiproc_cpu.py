@@ -90,3 +90,51 @@ def test_bucket_plan_r50():
     assert set(b[:, 0]).issubset(set(offs.tolist()))        # boundaries at parameter starts
     assert all((hi - lo) >= cap for lo, hi in b[:-1])       # every bucket but the last reaches the cap
     assert nb == -(-total // cap) or nb == total // cap + 1 or nb <= total // cap + 1
+
+
+def _syncbn_worker(rank, world, port, q):
+    """one rank of the SyncBN aggregation protocol the GPU path runs (local FP64
+    sums rounded to float into [sum, sumsq, count], one fp32 SUM allreduce,
+    statistics from the global sums -- src/syncbn.cpp:21-57), over gloo"""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from tests.test_oracle_pins import _shards
+    x, _, _, _ = _shards(world, 2, 24, 5, 7, 0, 10 * world)
+    xr = x[rank].astype(np.float64)
+    agg = np.concatenate([xr.sum(axis=(0, 2, 3)), (xr * xr).sum(axis=(0, 2, 3)), [xr.shape[0] * 35]])
+    t = torch.from_numpy(agg.astype(np.float32))
+    dist.all_reduce(t)
+    a = t.numpy().astype(np.float64)
+    Cc = 24
+    mu = a[:Cc] / a[2 * Cc]
+    var = np.maximum(a[Cc:2 * Cc] / a[2 * Cc] - mu * mu, 0.0)
+    q.put((rank, t.numpy().tolist(), mu.astype(np.float32).tolist(), (1.0 / np.sqrt(var + 1e-5)).astype(np.float32).tolist()))
+    dist.destroy_process_group()
+
+
+def test_syncbn_protocol_gloo_world2(orc):
+    """two gloo ranks agree bitwise on the all-reduced statistics buffer, and
+    their global statistics equal the K = 2 restatement's (a 2-term float sum is
+    order-free, so NCCL's reduction order cannot change it either)"""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_syncbn_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = sorted(q.get(timeout=120) for _ in range(2))
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    assert res[0][1] == res[1][1]
+    from oracle import p
+    from tests.test_oracle_pins import _shards
+    x, _, g, b = _shards(2, 2, 24, 5, 7, 0, 20)
+    y = np.zeros_like(x)
+    mean, inv = np.zeros(24, np.float32), np.zeros(24, np.float32)
+    agg = np.zeros(49, np.float32)
+    orc.orc_syncbn_forward_k(2, p(x), 2, 24, 5, 7, p(g), p(b), 1e-5, 0, p(y), p(mean), p(inv), p(agg))
+    assert np.allclose(np.array(res[0][1], np.float32), agg, rtol=1e-6, atol=1e-5)
+    assert np.allclose(np.array(res[0][2], np.float32), mean, rtol=1e-5, atol=1e-6)
+    assert np.allclose(np.array(res[0][3], np.float32), inv, rtol=1e-5)

@@ -148,3 +148,63 @@ def test_mix64_matches_reference_dataset_rng(orc):
     # mix64 (src/dataset.cpp:11-17); splitmix64 first output for seed 0 is a
     # well-known constant: next() of state 0 -> 0xe220a8397b1dcdaf
     assert orc.orc_mix64(0, 0) == 0xE220A8397B1DCDAF
+
+
+# ---------------------------------------------------------------- SyncBN over K ranks
+def _shards(K, N, Cc, H, W, fp16, seed):
+    rng = np.random.default_rng(seed)
+    x = (rng.standard_normal((K, N, Cc, H, W)) * 1.7 + 0.3).astype(np.float32)
+    dy = rng.standard_normal((K, N, Cc, H, W)).astype(np.float32)
+    if fp16:
+        x = x.astype(np.float16).astype(np.float32)
+        dy = dy.astype(np.float16).astype(np.float32)
+    g = (rng.random(Cc) + 0.5).astype(np.float32)
+    b = (rng.standard_normal(Cc) * 0.1).astype(np.float32)
+    return x, dy, g, b
+
+
+@pytest.mark.parametrize("K", [1, 2, 3, 4])
+@pytest.mark.parametrize("fp16", [0, 1])
+def test_syncbn_k_ranks_restatement_matches_reference(orc, ref, K, fp16):
+    """syncbn_forward/backward with a K-rank group (src/syncbn.cpp:21-117 over
+    the ring allreduce of src/comm.cpp:288-315), reference run_workers vs the
+    restatement: bit-identical outputs, statistics and gamma/beta gradients"""
+    N, Cc, H, W = 2, 24, 5, 7
+    x, dy, g, b = _shards(K, N, Cc, H, W, fp16, 10 * K + fp16)
+    outs = {}
+    for name, lib in (("orc", orc), ("ref", ref)):
+        y = np.zeros_like(x)
+        mean, inv = np.zeros(Cc, np.float32), np.zeros(Cc, np.float32)
+        agg = np.zeros(2 * Cc + 1, np.float32)
+        fn = lib.orc_syncbn_forward_k if name == "orc" else lib.ref_syncbn_forward_k
+        rc = fn(K, p(x), N, Cc, H, W, p(g), p(b), 1e-5, fp16, p(y), p(mean), p(inv), p(agg))
+        assert not rc
+        count = int(agg[2 * Cc])
+        dx = np.zeros_like(x)
+        dg, db = np.zeros(Cc, np.float32), np.zeros(Cc, np.float32)
+        if name == "orc":
+            lib.orc_syncbn_backward_k(K, p(dy), p(x), N, Cc, H, W, p(g), p(mean), p(inv), count, p(dx), p(dg), p(db))
+        else:
+            assert not lib.ref_syncbn_backward_k(K, p(dy), p(x), N, Cc, H, W, p(g), p(mean), p(inv), count, fp16,
+                                                 p(dx), p(dg), p(db))
+        outs[name] = (y, mean, inv, agg, dx, dg, db)
+    for a, r in zip(outs["orc"], outs["ref"]):
+        assert np.array_equal(a.view(np.uint32), r.view(np.uint32))
+    assert int(outs["ref"][3][2 * Cc]) == K * N * H * W  # the global count
+
+
+def test_ring_allreduce_fold_order(orc):
+    """src/comm.cpp:288-315: chunk c of the buffer is left-folded in rank order
+    c, c+1, ... -- visible with values whose float sum depends on the order"""
+    K, n = 3, 7
+    bufs = np.zeros((K, n), np.float32)
+    bufs[:, :] = np.array([1e8, 1.0, -1e8], np.float32)[:, None]
+    orc.orc_ring_allreduce_sum(p(bufs), K, n)
+    chunks = [(0, 3), (3, 2), (5, 2)]  # ring_chunks(7, 3)
+    for c, (at, ln) in enumerate(chunks):
+        vals = [np.float32([1e8, 1.0, -1e8][(c + j) % K]) for j in range(K)]
+        acc = vals[0]
+        for v in vals[1:]:
+            acc = np.float32(acc + v)
+        assert np.all(bufs[:, at:at + ln] == acc)
+    assert not np.all(bufs[:, 0] == bufs[:, 5])  # the order is observable (0 vs 1)
