@@ -38,7 +38,8 @@ typedef enum {
     SDB_PARAM = 5,          /* simdet::ParamError            errors.hpp:35  */
     SDB_COLLECTIVE = 6,     /* simdet::CollectiveError       errors.hpp:31  */
     SDB_CUDA = 7,           /* CUDA runtime / launch failure                */
-    SDB_UNSUPPORTED = 8     /* shape outside the kernels' envelope          */
+    SDB_UNSUPPORTED = 8,    /* shape outside the kernels' envelope          */
+    SDB_FORMAT = 9          /* simdet::FormatError           errors.hpp:40  */
 } sdb_status;
 
 typedef enum { SDB_F32 = 0, SDB_F16 = 1 } sdb_dtype;
@@ -189,6 +190,14 @@ int sdb_det_get_param(sdb_det* det, int idx, float* host);  /* fp32 master, refe
 int sdb_det_set_param(sdb_det* det, int idx, const float* host);
 int sdb_det_get_grad(sdb_det* det, int idx, float* host);   /* last step's summed gradient (scaled) */
 int sdb_det_get_velocity(sdb_det* det, int idx, float* host);       /* SGD momentum buffer */
+/* Training state in the reference's SDCK v1 format (src/checkpoint.cpp:47-128):
+ * fp32 masters in pack order and reference layouts, the flat velocity, the
+ * loss-scale state; no running-stat blocks (IABN keeps none).  A run resumed
+ * from it continues bit-identically (tests/test_trainer.cpp:203-290).  Load
+ * checks magic/version/truncation (SDB_FORMAT) and that names and shapes match
+ * this detector (SDB_CONTRACT); step and config digest are returned. */
+int sdb_det_save_checkpoint(sdb_det* det, const char* path, uint64_t config_digest, int64_t step);
+int sdb_det_load_checkpoint(sdb_det* det, const char* path, uint64_t* config_digest, int64_t* step);
 int sdb_det_set_velocity(sdb_det* det, int idx, const float* host);
 /* feed one batch: images NHWC with C padded to 8 (dtype of the mode), on host
  * (pinned, copied H2D on the step stream) or device; GT arrays on host

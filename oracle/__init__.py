@@ -66,6 +66,7 @@ _REF_SIGS = {
     "ref_bn_backward": (_I, [_P, _P, _I, _I, _I, _I, _P, _P, _P, _I, _P, _P, _P]),
     "ref_syncbn_forward_k": (_I, [_I, _P, _I, _I, _I, _I, _P, _P, _F, _I, _P, _P, _P, _P]),
     "ref_syncbn_backward_k": (_I, [_I, _P, _P, _I, _I, _I, _I, _P, _P, _P, _L, _I, _P, _P, _P]),
+    "ref_checkpoint_read": (_I, [C.c_char_p, _P, _P, _P, _P, _P, _P, _P, _I, C.c_char_p, _I, _P, _L, _P, _L]),
     "ref_iabn_forward": (_I, [_P, _I, _I, _I, _I, _P, _P, _F, _F, _I, _P, _P, _P]),
     "ref_iabn_backward": (_I, [_P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _F, _F, _I, _P, _P, _P]),
     "ref_iou": (_D, [_P, _P]),

@@ -8,12 +8,15 @@
 //
 // Status codes mirror the reference's exception taxonomy (errors.hpp:9-40) the
 // same way include/sdb.h does, so error-behaviour parity can be asserted.
+#include <algorithm>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <string>
 #include <vector>
 
 #include "simdet/autograd.hpp"
+#include "simdet/checkpoint.hpp"
 #include "simdet/comm.hpp"
 #include "simdet/errors.hpp"
 #include "simdet/half.hpp"
@@ -183,6 +186,31 @@ int ref_syncbn_backward_k(int K, const float* dy_all, const float* x_all, int N,
                 std::memcpy(dbeta, gr.dbeta.data(), C * sizeof(float));
             }
         });
+    });
+}
+
+// load_checkpoint (src/checkpoint.cpp:86-128) of a file written by the GPU
+// detector: header fields, the idx-th parameter (name, data) and the velocity
+int ref_checkpoint_read(const char* path, int64_t* step, uint64_t* digest, int* nparams, int64_t* nvel,
+                        double* scale, int64_t* good, int* mode, int idx, char* name, int name_cap, float* param,
+                        int64_t pcap, float* vel, int64_t vcap) {
+    return guarded([&] {
+        CheckpointState st = load_checkpoint(path);
+        *step = st.step;
+        *digest = st.config_digest;
+        *nparams = static_cast<int>(st.params.size());
+        *nvel = static_cast<int64_t>(st.velocity.size());
+        *scale = st.scale.scale;
+        *good = st.scale.good_steps;
+        *mode = st.scale.mode == ScaleMode::Dynamic ? 1 : 0;
+        if (idx >= 0 && idx < *nparams) {
+            const auto& [nm, t] = st.params[static_cast<size_t>(idx)];
+            std::snprintf(name, static_cast<size_t>(name_cap), "%s", nm.c_str());
+            const int64_t n = std::min<int64_t>(pcap, t.numel());
+            std::memcpy(param, t.data().data(), static_cast<size_t>(n) * sizeof(float));
+        }
+        const int64_t nv = std::min<int64_t>(vcap, *nvel);
+        std::memcpy(vel, st.velocity.data(), static_cast<size_t>(nv) * sizeof(float));
     });
 }
 

@@ -59,8 +59,12 @@ class UnsupportedError(SdbError):
     pass
 
 
+class FormatError(SdbError):
+    pass
+
+
 _STATUS = {1: ShapeError, 2: ContractError, 3: DegenerateBatchError, 4: NonInvertibleError, 5: ParamError,
-           6: CollectiveError, 7: CudaError, 8: UnsupportedError}
+           6: CollectiveError, 7: CudaError, 8: UnsupportedError, 9: FormatError}
 
 
 def header_functions() -> list[str]:

@@ -21,6 +21,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <fstream>
 #include <stdexcept>
 #include <string>
 #include <map>
@@ -423,10 +424,13 @@ void init_params(sdb_det* d) {
                 for (int64_t o = 0; o < outc; ++o) dst[o * p.C + ii] = ref[ii * outc + o];
         }
     }
-    CK(cudaMemcpy(d->w32, wh.data(), wh.size() * 4, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(d->bn32, bh.data(), bh.size() * 4, cudaMemcpyHostToDevice));
-    CK(cudaMemset(d->v32, 0, wh.size() * 4));
-    CK(cudaMemset(d->bnv, 0, bh.size() * 4));
+    // stream-ordered copies: a pageable cudaMemcpy may return before its DMA
+    // lands, and the cast below runs on the (non-blocking) context stream
+    cudaStream_t st0 = d->ctx->stream;
+    CK(cudaMemcpyAsync(d->w32, wh.data(), wh.size() * 4, cudaMemcpyHostToDevice, st0));
+    CK(cudaMemcpyAsync(d->bn32, bh.data(), bh.size() * 4, cudaMemcpyHostToDevice, st0));
+    CK(cudaMemsetAsync(d->v32, 0, wh.size() * 4, st0));
+    CK(cudaMemsetAsync(d->bnv, 0, bh.size() * 4, st0));
     if (d->dt == kF16) CK(cast_f32_f16(d->w32, static_cast<__half*>(d->wdev), d->n_w, d->ctx->stream));
     CK(cudaStreamSynchronize(d->ctx->stream));
 }
@@ -904,9 +908,11 @@ void run_step(sdb_det* d) {
             }
             d->wg_jobs_dev = static_cast<WgradJob*>(d->alloc(d->wg_jobs.size() * sizeof(WgradJob)));
             d->wg_tiles_dev = static_cast<int*>(d->alloc(start.size() * sizeof(int)));
-            CK(cudaMemcpy(d->wg_jobs_dev, d->wg_jobs.data(), d->wg_jobs.size() * sizeof(WgradJob),
-                          cudaMemcpyHostToDevice));
-            CK(cudaMemcpy(d->wg_tiles_dev, start.data(), start.size() * sizeof(int), cudaMemcpyHostToDevice));
+            // ordered on the step's stream (pageable copies: staged before return)
+            CK(cudaMemcpyAsync(d->wg_jobs_dev, d->wg_jobs.data(), d->wg_jobs.size() * sizeof(WgradJob),
+                               cudaMemcpyHostToDevice, st));
+            CK(cudaMemcpyAsync(d->wg_tiles_dev, start.data(), start.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+            CK(cudaStreamSynchronize(st));
             d->wg_njobs_dev = static_cast<int>(d->wg_jobs.size());
             d->wg_total_tiles = tot;
         } else if (static_cast<int>(d->wg_jobs.size()) != d->wg_njobs_dev) {
@@ -1101,9 +1107,10 @@ int sdb_det_create(sdb_ctx* ctx, const sdb_det_config* cfgp, sdb_det** out) {
         d->scale_used = static_cast<double*>(d->alloc(8));
         const double s0 = cf.mode == 1 ? cf.scale_init : 1.0;
         const int64_t zero = 0;
-        CK(cudaMemcpy(d->scale, &s0, 8, cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(d->good, &zero, 8, cudaMemcpyHostToDevice));
-        CK(cudaMemset(d->losses, 0, 64));
+        CK(cudaMemcpyAsync(d->scale, &s0, 8, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(d->good, &zero, 8, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemsetAsync(d->losses, 0, 64, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
 
         // ---- targets / proposals buffers
         d->anchors = static_cast<float*>(d->alloc(static_cast<size_t>(d->nA) * 16));
@@ -1263,25 +1270,31 @@ static int param_xfer(sdb_det* d, int idx, float* host, int which) {
     const Param& p = d->params[idx];
     cudaStream_t st = d->ctx->stream;
     try {
+        // every copy is ordered on the context stream: a pageable cudaMemcpy may
+        // return before its DMA lands, and the stream is non-blocking
         CK(cudaStreamSynchronize(st));
         if (p.kind >= 2) {
             float* src = (which == 2 ? d->bng : (which >= 3 ? d->bnv : d->bn32)) + p.off;
-            if (which == 1 || which == 4) CK(cudaMemcpy(src, host, p.numel * 4, cudaMemcpyHostToDevice));
-            else CK(cudaMemcpy(host, src, p.numel * 4, cudaMemcpyDeviceToHost));
+            if (which == 1 || which == 4) CK(cudaMemcpyAsync(src, host, p.numel * 4, cudaMemcpyHostToDevice, st));
+            else CK(cudaMemcpyAsync(host, src, p.numel * 4, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
             return SDB_OK;
         }
         std::vector<float> dev(static_cast<size_t>(p.numel));
         if (which == 2) {
             if (d->dt == kF16) {
                 std::vector<__half> h(static_cast<size_t>(p.numel));
-                CK(cudaMemcpy(h.data(), d->gptr(idx), p.numel * 2, cudaMemcpyDeviceToHost));
+                CK(cudaMemcpyAsync(h.data(), d->gptr(idx), p.numel * 2, cudaMemcpyDeviceToHost, st));
+                CK(cudaStreamSynchronize(st));
                 for (size_t i = 0; i < h.size(); ++i) dev[i] = __half2float(h[i]);
             } else {
-                CK(cudaMemcpy(dev.data(), d->gptr(idx), p.numel * 4, cudaMemcpyDeviceToHost));
+                CK(cudaMemcpyAsync(dev.data(), d->gptr(idx), p.numel * 4, cudaMemcpyDeviceToHost, st));
+                CK(cudaStreamSynchronize(st));
             }
         } else {
             const float* src = which >= 3 ? d->v32 + p.off : d->wptr(idx);
-            CK(cudaMemcpy(dev.data(), src, p.numel * 4, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpyAsync(dev.data(), src, p.numel * 4, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
         }
         int64_t n = 1;
         for (int64_t s : p.ref_shape) n *= s;
@@ -1302,7 +1315,8 @@ static int param_xfer(sdb_det* d, int idx, float* host, int which) {
         };
         if (which == 1 || which == 4) {
             map([&](int64_t ri, int64_t di) { dev[di] = host[ri]; });
-            CK(cudaMemcpy(which == 4 ? d->v32 + p.off : d->wptr(idx), dev.data(), p.numel * 4, cudaMemcpyHostToDevice));
+            CK(cudaMemcpyAsync(which == 4 ? d->v32 + p.off : d->wptr(idx), dev.data(), p.numel * 4,
+                               cudaMemcpyHostToDevice, st));
             if (which == 1 && d->dt == kF16) CK(cast_f32_f16(d->wptr(idx), static_cast<__half*>(d->wdev_ptr(idx)), p.numel, st));
             CK(cudaStreamSynchronize(st));
         } else {
@@ -1320,6 +1334,144 @@ int sdb_det_get_grad(sdb_det* d, int idx, float* host) { return param_xfer(d, id
 int sdb_det_get_velocity(sdb_det* d, int idx, float* host) { return param_xfer(d, idx, host, 3); }
 int sdb_det_set_velocity(sdb_det* d, int idx, const float* host) {
     return param_xfer(d, idx, const_cast<float*>(host), 4);
+}
+
+// ---- SDCK v1 checkpoints (src/checkpoint.cpp:47-128, little endian)
+int sdb_det_save_checkpoint(sdb_det* d, const char* path, uint64_t config_digest, int64_t step) {
+    std::ofstream f(path ? path : "", std::ios::binary);
+    if (!f) return det_fail(SDB_FORMAT, "cannot open checkpoint for writing");
+    auto bytes = [&](const void* p, size_t n) { f.write(static_cast<const char*>(p), static_cast<std::streamsize>(n)); };
+    auto pod = [&](auto v) { bytes(&v, sizeof v); };
+    bytes("SDCK", 4);
+    pod(static_cast<uint32_t>(1));
+    pod(config_digest);
+    pod(step);
+    pod(static_cast<uint32_t>(d->params.size()));
+    std::vector<float> vel;
+    for (int i = 0; i < static_cast<int>(d->params.size()); ++i) {
+        const Param& p = d->params[i];
+        int64_t n = 1;
+        for (int64_t s2 : p.ref_shape) n *= s2;
+        std::vector<float> w(static_cast<size_t>(n)), v(static_cast<size_t>(n));
+        if (int rc = param_xfer(d, i, w.data(), 0)) return rc;
+        if (int rc = param_xfer(d, i, v.data(), 3)) return rc;
+        pod(static_cast<uint16_t>(p.name.size()));
+        bytes(p.name.data(), p.name.size());
+        pod(static_cast<uint8_t>(0));  // DType::F32 masters
+        pod(static_cast<uint8_t>(p.ref_shape.size()));
+        for (int64_t dim : p.ref_shape) pod(dim);
+        bytes(w.data(), w.size() * sizeof(float));
+        vel.insert(vel.end(), v.begin(), v.end());
+    }
+    pod(static_cast<uint64_t>(vel.size()));
+    bytes(vel.data(), vel.size() * sizeof(float));
+    double scale = 0.0;
+    int64_t good = 0;
+    try {
+        CK(cudaMemcpyAsync(&scale, d->scale, 8, cudaMemcpyDeviceToHost, d->ctx->stream));
+        CK(cudaMemcpyAsync(&good, d->good, 8, cudaMemcpyDeviceToHost, d->ctx->stream));
+        CK(cudaStreamSynchronize(d->ctx->stream));
+    } catch (const std::exception& e) {
+        return det_fail(SDB_CUDA, e.what());
+    }
+    const auto& cf = d->cfg;
+    pod(scale);
+    pod(good);
+    pod(static_cast<uint8_t>(cf.dynamic_scale ? 1 : 0));  // ScaleMode {Static, Dynamic}
+    pod(static_cast<int64_t>(cf.growth_interval));
+    pod(cf.growth);
+    pod(cf.backoff);
+    pod(cf.min_scale);
+    pod(cf.max_scale);
+    pod(static_cast<uint32_t>(0));  // running-stat blocks
+    if (!f) return det_fail(SDB_FORMAT, "checkpoint write failed");
+    return SDB_OK;
+}
+
+int sdb_det_load_checkpoint(sdb_det* d, const char* path, uint64_t* config_digest, int64_t* step) {
+    std::ifstream f(path ? path : "", std::ios::binary);
+    if (!f) return det_fail(SDB_FORMAT, "cannot open checkpoint");
+    bool ok = true;
+    auto bytes = [&](void* p, size_t n) {
+        f.read(static_cast<char*>(p), static_cast<std::streamsize>(n));
+        if (static_cast<size_t>(f.gcount()) != n) ok = false;
+    };
+    auto pod = [&](auto& v) { bytes(&v, sizeof v); };
+    char magic[4];
+    bytes(magic, 4);
+    if (!ok || std::memcmp(magic, "SDCK", 4) != 0) return det_fail(SDB_FORMAT, "not a checkpoint file (bad magic)");
+    uint32_t version = 0;
+    pod(version);
+    if (!ok || version != 1) return det_fail(SDB_FORMAT, "unsupported checkpoint version");
+    uint64_t digest = 0;
+    int64_t st = 0;
+    uint32_t np = 0;
+    pod(digest);
+    pod(st);
+    pod(np);
+    if (!ok) return det_fail(SDB_FORMAT, "truncated checkpoint file");
+    if (np != d->params.size()) return det_fail(SDB_CONTRACT, "checkpoint parameter count differs from this detector");
+    std::vector<std::vector<float>> ws(np);
+    for (uint32_t i = 0; i < np; ++i) {
+        const Param& p = d->params[i];
+        uint16_t len = 0;
+        pod(len);
+        std::string name(len, '\0');
+        bytes(name.data(), len);
+        uint8_t dtype = 0, rank = 0;
+        pod(dtype);
+        pod(rank);
+        if (!ok) return det_fail(SDB_FORMAT, "truncated checkpoint file");
+        if (rank < 1 || rank > 4) return det_fail(SDB_FORMAT, "checkpoint parameter rank out of range");
+        std::vector<int64_t> shape(rank);
+        for (auto& dim : shape) pod(dim);
+        if (!ok) return det_fail(SDB_FORMAT, "truncated checkpoint file");
+        if (name != p.name || shape != p.ref_shape || dtype != 0)
+            return det_fail(SDB_CONTRACT, ("checkpoint parameter mismatch at " + p.name).c_str());
+        int64_t n = 1;
+        for (int64_t dim : shape) n *= dim;
+        ws[i].resize(static_cast<size_t>(n));
+        bytes(ws[i].data(), ws[i].size() * sizeof(float));
+        if (!ok) return det_fail(SDB_FORMAT, "truncated checkpoint file");
+    }
+    uint64_t nvel = 0;
+    pod(nvel);
+    std::vector<float> vel(static_cast<size_t>(ok ? nvel : 0));
+    bytes(vel.data(), vel.size() * sizeof(float));
+    double scale = 0.0, growth = 0.0, backoff = 0.0, mn = 0.0, mx = 0.0;
+    int64_t good = 0, gi = 0;
+    uint8_t mode = 0;
+    uint32_t nrun = 0;
+    pod(scale); pod(good); pod(mode); pod(gi); pod(growth); pod(backoff); pod(mn); pod(mx); pod(nrun);
+    if (!ok) return det_fail(SDB_FORMAT, "truncated checkpoint file");
+    size_t total = 0;
+    for (const auto& w : ws) total += w.size();
+    if (vel.size() != total) return det_fail(SDB_FORMAT, "checkpoint velocity length differs from the parameters");
+    // running-stat blocks are skipped (IABN keeps none; a BN checkpoint's stats are not step state here)
+    for (uint32_t i = 0; i < nrun; ++i) {
+        float mom = 0.f;
+        uint64_t c = 0;
+        pod(mom);
+        pod(c);
+        if (!ok || c > (uint64_t{1} << 32)) return det_fail(SDB_FORMAT, "truncated checkpoint file");
+        f.seekg(static_cast<std::streamoff>(2 * c * sizeof(float)), std::ios::cur);
+    }
+    size_t off = 0;
+    for (uint32_t i = 0; i < np; ++i) {
+        if (int rc = param_xfer(d, static_cast<int>(i), ws[i].data(), 1)) return rc;
+        if (int rc = param_xfer(d, static_cast<int>(i), vel.data() + off, 4)) return rc;
+        off += ws[i].size();
+    }
+    try {
+        CK(cudaMemcpyAsync(d->scale, &scale, 8, cudaMemcpyHostToDevice, d->ctx->stream));
+        CK(cudaMemcpyAsync(d->good, &good, 8, cudaMemcpyHostToDevice, d->ctx->stream));
+        CK(cudaStreamSynchronize(d->ctx->stream));
+    } catch (const std::exception& e) {
+        return det_fail(SDB_CUDA, e.what());
+    }
+    if (config_digest) *config_digest = digest;
+    if (step) *step = st;
+    return SDB_OK;
 }
 
 static void stage_gt(sdb_det* d, const float* gt_boxes, const int32_t* gt_cls, const int32_t* gt_count,
@@ -1476,6 +1628,11 @@ int sdb_det_export(sdb_det* d, int what, void* host, int64_t cap, int64_t* bytes
         case 9: src = d->anchors; n = static_cast<int64_t>(d->nA) * 16; break;
         case 10: src = d->c4.p; n = d->c4.numel() * d->es; break;
         case 11: src = d->img.p; n = d->img.numel() * d->es; break;
+        case 13: src = d->stem_z.p; n = d->stem_z.numel() * d->es; break;
+        case 14: src = d->pool.p; n = d->pool.numel() * d->es; break;
+        case 15: src = d->stem_x2; n = d->stem_x2 ? static_cast<int64_t>(d->stem2.g.W) * 192 * 2 : 0; break;
+        case 16: src = d->wdev; n = d->n_w * d->es; break;
+        case 17: src = d->w32; n = d->n_w * 4; break;
         case 12: {
             cudaStreamSynchronize(d->ctx->stream);
             cudaMemcpy(&tmp_state[0], d->scale, 8, cudaMemcpyDeviceToHost);

@@ -112,6 +112,8 @@ _SIGS = {
     "sdb_det_set_param": [_P, _I, _P],
     "sdb_det_get_grad": [_P, _I, _P],
     "sdb_det_get_velocity": [_P, _I, _P],
+    "sdb_det_save_checkpoint": [_P, C.c_char_p, C.c_uint64, _L],
+    "sdb_det_load_checkpoint": [_P, C.c_char_p, _P, _P],
     "sdb_det_set_velocity": [_P, _I, _P],
     "sdb_det_set_batch": [_P, _P, _I, _P, _P, _P, _P],
     "sdb_det_synth_images": [_P, _P],
@@ -294,6 +296,16 @@ class Detector:
         la = (_L * n)()
         check(L().sdb_det_profile(self.h, ms, fl, by, la, n))
         return {c: (ms[i], fl[i], by[i], la[i]) for i, c in enumerate(self.PROFILE_CATS)}
+
+    def save_checkpoint(self, path: str, step: int, config_digest: int = 0):
+        """SDCK v1 file (src/checkpoint.cpp:47-84): masters, velocity, loss-scale state"""
+        check(L().sdb_det_save_checkpoint(self.h, path.encode(), config_digest, step))
+
+    def load_checkpoint(self, path: str):
+        """restores the training state; returns (step, config_digest)"""
+        dg, st = C.c_uint64(), _L()
+        check(L().sdb_det_load_checkpoint(self.h, path.encode(), C.byref(dg), C.byref(st)))
+        return st.value, dg.value
 
     def kernel_launches(self) -> int:
         n = _L()

@@ -240,3 +240,60 @@ def test_host_nchw_entry_matches_nhwc8():
         det.close()
     assert out[0][0] == out[1][0]
     assert np.array_equal(out[0][1].view(np.uint32), out[1][1].view(np.uint32))
+
+
+def test_checkpoint_resume_is_bitwise_and_reference_readable(ref, tmp_path):
+    """SDCK v1 round trip (src/checkpoint.cpp:47-128): a run resumed from a
+    step-3 checkpoint continues bit-identically (tests/test_trainer.cpp:203-290
+    analogue, dynamic loss scale), and the reference's own load_checkpoint reads
+    the file: same parameter count, names, masters, velocity and scale state"""
+    from paper_1903_05831_b200 import detector as D
+    import paper_1903_05831_b200 as pkg
+    cfg = dict(img_h=128, img_w=128, dynamic_scale=1, scale_init=1024.0, growth_interval=2)
+    path = str(tmp_path / "det.sdck")
+    a = D.Detector(D.preset("c2", **cfg))
+    for step in range(1, 4):
+        a.feed(D.batch_slots(step, 0, 1, 2))
+        a.step()
+    a.losses()
+    a.save_checkpoint(path, step=3, config_digest=0xC0FFEE)
+    w3, v3 = dp.flat_params(a), dp.flat_velocity(a)
+    for step in range(4, 6):
+        a.feed(D.batch_slots(step, 0, 1, 2))
+        a.step()
+    la = a.losses()
+    wa = dp.flat_params(a)
+    b = D.Detector(D.preset("c2", **cfg))
+    assert b.load_checkpoint(path) == (3, 0xC0FFEE)
+    assert np.array_equal(dp.flat_params(b).view(np.uint32), w3.view(np.uint32))
+    for step in range(4, 6):
+        b.feed(D.batch_slots(step, 0, 1, 2))
+        b.step()
+    lb = b.losses()
+    assert np.array_equal(dp.flat_params(b).view(np.uint32), wa.view(np.uint32))
+    assert np.array_equal(np.asarray(la[0]), np.asarray(lb[0])) and la[1] == lb[1]
+    # the reference reader
+    step, dig, npar, nvel = C.c_int64(), C.c_uint64(), C.c_int(), C.c_int64()
+    scale, good, mode = C.c_double(), C.c_int64(), C.c_int()
+    name = C.create_string_buffer(128)
+    p0 = a.get_param(0).ravel()
+    buf = np.zeros(p0.size, np.float32)
+    vel = np.zeros(v3.size, np.float32)
+    assert ref.ref_checkpoint_read(path.encode(), C.byref(step), C.byref(dig), C.byref(npar), C.byref(nvel),
+                                   C.byref(scale), C.byref(good), C.byref(mode), 0, name, 128, ptr(buf), buf.size,
+                                   ptr(vel), vel.size) == 0
+    assert (step.value, dig.value, npar.value, nvel.value, mode.value) == (3, 0xC0FFEE, a.n_tensors, v3.size, 1)
+    assert name.value.decode() == a.params[0][0]
+    assert np.array_equal(buf.view(np.uint32), w3[: p0.size].view(np.uint32))
+    assert np.array_equal(vel.view(np.uint32), v3.view(np.uint32))
+    # format errors map to FormatError, foreign layouts to ContractError
+    bad = tmp_path / "bad.sdck"
+    bad.write_bytes(b"NOPE" + open(path, "rb").read()[4:])
+    with pytest.raises(pkg.FormatError):
+        b.load_checkpoint(str(bad))
+    trunc = tmp_path / "trunc.sdck"
+    trunc.write_bytes(open(path, "rb").read()[:200])
+    with pytest.raises(pkg.FormatError):
+        b.load_checkpoint(str(trunc))
+    a.close()
+    b.close()
