@@ -297,3 +297,27 @@ def test_checkpoint_resume_is_bitwise_and_reference_readable(ref, tmp_path):
         b.load_checkpoint(str(trunc))
     a.close()
     b.close()
+
+
+def test_training_driver_metrics_and_resume(tmp_path):
+    """run_training (src/trainer.cpp:186-283 analogue): metrics.csv rows are
+    well-formed with strictly increasing steps (tests/test_trainer.cpp:175-200),
+    and a run resumed from its step-2 checkpoint reproduces steps 3-4 exactly
+    (loss, scale used, skipped) -- tests/test_trainer.cpp:203-290"""
+    import re
+    from paper_1903_05831_b200 import detector as D
+    from paper_1903_05831_b200 import trainer as T
+    p = D.preset("c2", img_h=128, img_w=128, dynamic_scale=1, scale_init=1024.0, growth_interval=2)
+    full = T.run_training(p, 4, metrics_path=str(tmp_path / "metrics.csv"))
+    lines = open(tmp_path / "metrics.csv").read().splitlines()
+    assert lines[0] == "step,loss,scale,skipped,step_time_model,peak_bytes"
+    rows = [ln.split(",") for ln in lines[1:]]
+    assert [int(r[0]) for r in rows] == [1, 2, 3, 4]
+    for r in rows:
+        assert re.fullmatch(r"-?\d+", r[0]) and int(r[3]) in (0, 1) and float(r[4]) > 0 and int(r[5]) > 0
+    ck = str(tmp_path / "ck.sdck")
+    T.run_training(p, 2, checkpoint_path=ck, checkpoint_every=2)
+    resumed = T.run_training(p, 4, resume=ck)
+    rl = resumed.metrics_csv.splitlines()
+    assert [ln.split(",")[:4] for ln in rl[1:]] == [ln.split(",")[:4] for ln in lines[3:]]
+    assert resumed.losses == full.losses[2:]
