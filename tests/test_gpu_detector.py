@@ -321,3 +321,33 @@ def test_training_driver_metrics_and_resume(tmp_path):
     rl = resumed.metrics_csv.splitlines()
     assert [ln.split(",")[:4] for ln in rl[1:]] == [ln.split(",")[:4] for ln in lines[3:]]
     assert resumed.losses == full.losses[2:]
+
+
+@pytest.mark.parametrize("counts", [(0, 1), (0, 0)])
+def test_images_without_ground_truth(counts):
+    """edge cases of the targets: an image with no GT box (every anchor and RoI
+    background) and one with a single box -- all discrete decisions stay
+    bit-exact against the restatement and the losses stay finite"""
+    from paper_1903_05831_b200 import detector as D
+    det = D.Detector(D.preset("c2", img_h=128, img_w=128))
+    orig = det.gt_batch
+
+    def gt_batch(slots):
+        boxes, cls, cnt = orig(slots)
+        cnt = cnt.copy()
+        for j, c in enumerate(counts):
+            cnt[j] = min(int(cnt[j]), c)
+        return boxes, cls, cnt
+
+    det.gt_batch = gt_batch
+    for step in (1, 2):
+        slots = D.batch_slots(step, 0, 1, 2)
+        det.feed(slots)
+        det.step()
+        losses, _, ov = det.losses()
+        assert ov == 0 and all(np.isfinite(losses))
+        rep = dp.check_discrete(det, dp.gpu_state(det), slots)
+        for j, c in enumerate(counts):
+            if c == 0:
+                assert rep[j]["fg_anchors"] == 0 and rep[j]["fg_rois"] == 0
+    det.close()
