@@ -1367,6 +1367,53 @@ __global__ void __launch_bounds__(256) wgrad_reduce_batched_kernel(const WgradJo
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const int64_t per = static_cast<int64_t>(jb.rows) * jb.cols;
     // element (j, i) of partial s at ws[s][j][i]: rows j (R*S*C for transposed jobs, K otherwise)
+    if ((jb.cols & 3) == 0) {
+        // vector path: thread = (row j, 4 consecutive columns), one 16-byte load
+        // per split; same fixed split order, so bit-identical to the scalar path
+        const int q = threadIdx.x & 7, jr = threadIdx.x >> 3;
+        const int j = j0 + jr, iq = i0 + 4 * q;
+        const bool okv = j < jb.rows && iq < jb.cols;
+        const float4* src = reinterpret_cast<const float4*>(jb.ws + (okv ? static_cast<int64_t>(j) * jb.cols + iq : 0));
+        const int64_t per4 = per / 4;
+        float4 a4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        int k = 0;
+        for (; k + 4 <= jb.splits; k += 4) {
+            float4 v[4];
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) v[kk] = okv ? src[(k + kk) * per4] : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+                a4.x += v[kk].x;
+                a4.y += v[kk].y;
+                a4.z += v[kk].z;
+                a4.w += v[kk].w;
+            }
+        }
+        for (; k < jb.splits; ++k) {
+            const float4 v = okv ? src[k * per4] : make_float4(0.f, 0.f, 0.f, 0.f);
+            a4.x += v.x;
+            a4.y += v.y;
+            a4.z += v.z;
+            a4.w += v.w;
+        }
+        __half* dw = static_cast<__half*>(jb.dw);
+        if (jb.transposed) {
+            tile[jr][4 * q] = a4.x;
+            tile[jr][4 * q + 1] = a4.y;
+            tile[jr][4 * q + 2] = a4.z;
+            tile[jr][4 * q + 3] = a4.w;
+            __syncthreads();
+            for (int ii = ty; ii < 32; ii += 8) {
+                const int io = i0 + ii, jo = j0 + tx;
+                if (io < jb.cols && jo < jb.rows) dw[static_cast<int64_t>(io) * jb.rows + jo] = __float2half_rn(tile[tx][ii]);
+            }
+        } else if (okv) {
+            __half2* o = reinterpret_cast<__half2*>(dw + static_cast<int64_t>(j) * jb.cols + iq);
+            o[0] = __floats2half2_rn(a4.x, a4.y);
+            o[1] = __floats2half2_rn(a4.z, a4.w);
+        }
+        return;
+    }
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
     const int i = i0 + tx;
     bool ok[4];
