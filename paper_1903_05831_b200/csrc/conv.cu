@@ -63,6 +63,10 @@ struct ConvArgs {
     int plain;       // 1x1 / stride 1 / pad 0: the activation operand is a plain 2-D [pixels][channels] tile
     int tma_out;     // fp16 output written by TMA stores from swizzled staging (tm.o)
     const uint8_t* mbits;  // dgrad: sign bitmap of the mask tensor (bit c%8 of byte [row][c/8] = mask > 0)
+    // fprop with the TMA-store epilogue: per-channel FP64 [sum, sumsq] of the
+    // rounded fp16 output, accumulated by each CTA over its tiles (one n-tile
+    // per CTA) and written as stats[cta][quadrant][2][BN] (norm statistics fused)
+    double* stats;
 };
 
 // TMA descriptors of the dense GEMM operand (filter for fprop/dgrad, DY for wgrad)
@@ -693,10 +697,40 @@ SDB_DEV void epilogue_tile_v2(const ConvArgs& a, int split, int m0, int n0, int 
 // which one lane hands to the TMA engine (cp.async.bulk.tensor store).  Two
 // staging boxes per warp alternate, so the store of step j overlaps step j+1;
 // partial tiles are clipped by the tensor map bounds.
+// Column statistics of a staged fp16 box (rows = lanes of the quadrant): lane
+// L sums column L (SC = 32) or half a column (SC = 16: lanes 16-31 take rows
+// 16-31, folded in by one shuffle) -- every value widened to FP64 and its
+// square formed exactly, like the statistics kernel (src/syncbn.cpp:29-39).
+template <int SC>
+SDB_DEV void box_column_stats(const uint8_t* buf, int lane, double& S, double& Q) {
+    constexpr int ROWB = SC * 2;
+    const int col = SC == 32 ? lane : (lane & 15);
+    const int r0 = SC == 32 ? 0 : (lane >> 4) * 16;
+    constexpr int NR = SC == 32 ? 32 : 16;
+    double s = 0.0, qq = 0.0;
+#pragma unroll 8
+    for (int rr = 0; rr < NR; ++rr) {
+        const int r = r0 + rr;
+        const int j = col >> 3;
+        const int pj = SC == 32 ? (j ^ ((r >> 1) & 3)) : (j ^ ((r >> 2) & 1));
+        const __half h = *reinterpret_cast<const __half*>(buf + r * ROWB + pj * 16 + (col & 7) * 2);
+        const double x = static_cast<double>(__half2float(h));
+        s = __dadd_rn(s, x);
+        qq = __fma_rn(x, x, qq);
+    }
+    if (SC == 16) {
+        const double so = __shfl_down_sync(0xffffffffu, s, 16), qo = __shfl_down_sync(0xffffffffu, qq, 16);
+        s = __dadd_rn(s, so);
+        qq = __dadd_rn(qq, qo);
+    }
+    S = __dadd_rn(S, s);
+    Q = __dadd_rn(Q, qq);
+}
+
 template <int NCOL, int SC>
 SDB_DEV void epilogue_tile_tmastore(const CUtensorMap* omap, int m0, int n0, int nk, uint32_t tacc, int q, int lane,
                                     int c_lo, uint8_t* stg, uint64_t* tfull_acc, uint32_t tfull_phase,
-                                    uint64_t* tempty_acc, int& sb) {
+                                    uint64_t* tempty_acc, int& sb, double* cs = nullptr) {
     constexpr int NSTEP = NCOL / SC;
     constexpr int ROWB = SC * 2;
     constexpr int BUFB = 32 * ROWB;
@@ -734,6 +768,8 @@ SDB_DEV void epilogue_tile_tmastore(const CUtensorMap* omap, int m0, int n0, int
             tma_store_2d(omap, smem_u32(buf), n0 + c_lo + js * SC, m0 + q * 32);
             bulk_commit();
         }
+        // rows beyond M hold zeros (TMA zero-fills the A operand), adding +0.0
+        if (cs) box_column_stats<SC>(buf, lane, cs[2 * js], cs[2 * js + 1]);
         sb ^= 1;
     }
 }
@@ -1135,12 +1171,30 @@ __global__ void __launch_bounds__(TmaCfg<MODE, BN, ST, EPI>::kThreads, (BN <= 12
         } else if (MODE != WGRAD && a.tma_out) {
             int lt = 0, sb = 0;
             uint8_t* stg8 = reinterpret_cast<uint8_t*>(stg);
+            constexpr int kStep = kNCol / Cfg::kSC;
+            double cs[2 * kStep];
+#pragma unroll
+            for (int j = 0; j < 2 * kStep; ++j) cs[j] = 0.0;
             for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++lt) {
                 int m0, n0, kb0, nk;
                 tile_coords(t, m0, n0, kb0, nk);
                 const int acc = lt & 1;
                 epilogue_tile_tmastore<kNCol, Cfg::kSC>(&tm.o, m0, n0, nk, tmem + acc * BN, warp & 3, lane, c_lo,
-                                                        stg8, &tfull[acc], (lt >> 1) & 1, &tempty[acc], sb);
+                                                        stg8, &tfull[acc], (lt >> 1) & 1, &tempty[acc], sb,
+                                                        (MODE == FPROP && a.stats) ? cs : nullptr);
+            }
+            if (MODE == FPROP && a.stats) {
+                // this CTA's column block: stats[cta][quadrant][sum | sumsq][BN] (the host
+                // guarantees that every tile of a CTA has the same n0)
+                const int lanes = Cfg::kSC == 32 ? 32 : 16;
+                if (lane < lanes) {
+                    double* o = a.stats + (static_cast<int64_t>(blockIdx.x) * 4 + (warp & 3)) * 2 * BN;
+#pragma unroll
+                    for (int js = 0; js < kStep; ++js) {
+                        o[c_lo + js * Cfg::kSC + lane] = cs[2 * js];
+                        o[BN + c_lo + js * Cfg::kSC + lane] = cs[2 * js + 1];
+                    }
+                }
             }
             if (lane == 0) bulk_wait_all();
             __syncwarp();
@@ -1549,7 +1603,7 @@ static bool tma_ok(const ConvArgs& a, int mode) {
 }
 
 template <int MODE, int BN, int ST, int EPI = 0>
-static cudaError_t launch_tma(ConvArgs a, int splits, cudaStream_t st) {
+static cudaError_t launch_tma(ConvArgs a, int splits, cudaStream_t st, ConvStats* cst = nullptr) {
     using Cfg = TmaCfg<MODE, BN, ST, EPI>;
     static bool configured = false;
     if (!configured) {
@@ -1637,6 +1691,20 @@ static cudaError_t launch_tma(ConvArgs a, int splits, cudaStream_t st) {
         a.tma_out = 0;
     }
     if (!ok) return cudaErrorInvalidValue;
+    a.stats = nullptr;
+    if (cst) {
+        cst->produced = 0;
+        static const bool no_fused_stats = std::getenv("SDB_NO_FUSED_STATS") != nullptr;
+        const size_t need = static_cast<size_t>(grid) * 4 * 2 * BN * sizeof(double);
+        if (MODE == FPROP && EPI == 0 && a.tma_out && splits == 1 && grid % tiles_n == 0 && need <= cst->cap_bytes &&
+            !no_fused_stats) {
+            a.stats = cst->buf;
+            cst->produced = 1;
+            cst->ctas = grid;
+            cst->tiles_n = tiles_n;
+            cst->bn = BN;
+        }
+    }
     return launch_pdl(conv_tma_kernel<MODE, BN, ST, EPI>, dim3(grid), dim3(Cfg::kThreads), Cfg::kSmem, st, a, tiles_m,
                       tiles_n, n_tiles, tm);
 }
@@ -1659,11 +1727,11 @@ static int tma_bn(const ConvArgs& a, int mode = WGRAD) {
 }
 
 template <int MODE>
-static cudaError_t launch_tma_pick(const ConvArgs& a, int splits, cudaStream_t st) {
+static cudaError_t launch_tma_pick(const ConvArgs& a, int splits, cudaStream_t st, ConvStats* cst = nullptr) {
     switch (tma_bn(a, MODE)) {
-        case 256: return launch_tma<MODE, 256, 4>(a, splits, st);
-        case 128: return launch_tma<MODE, 128, 3>(a, splits, st);
-        default: return launch_tma<MODE, 64, 4>(a, splits, st);
+        case 256: return launch_tma<MODE, 256, 4>(a, splits, st, cst);
+        case 128: return launch_tma<MODE, 128, 3>(a, splits, st, cst);
+        default: return launch_tma<MODE, 64, 4>(a, splits, st, cst);
     }
 }
 
@@ -1743,13 +1811,16 @@ static bool& force_simt_flag() {
 bool conv_force_simt() { return force_simt_flag(); }
 void conv_set_force_simt(bool v) { force_simt_flag() = v; }
 
-cudaError_t conv_fprop(const ConvShape& g, int dtype, const void* x, const void* w, void* y, cudaStream_t st) {
+cudaError_t conv_fprop(const ConvShape& g, int dtype, const void* x, const void* w, void* y, cudaStream_t st,
+                       ConvStats* cst) {
     ConvArgs a = make_args(g);
     a.x = x; a.w = w; a.out = y;
     a.M = g.N * a.Ho * a.Wo;
     a.NG = g.K;
     a.KG = g.R * g.S * g.C;
-    if (tc_ok(g, dtype)) return tma_ok(a, FPROP) ? launch_tma_pick<FPROP>(a, 1, st) : launch_tc_pick<FPROP>(a, 1, st);
+    if (cst) cst->produced = 0;
+    if (tc_ok(g, dtype))
+        return tma_ok(a, FPROP) ? launch_tma_pick<FPROP>(a, 1, st, cst) : launch_tc_pick<FPROP>(a, 1, st);
     return dtype == kF16 ? launch_simt<__half, FPROP>(a, 1, st) : launch_simt<float, FPROP>(a, 1, st);
 }
 

@@ -219,6 +219,8 @@ struct sdb_det {
     int64_t gbuf_elems = 0;
     void* ws = nullptr;
     size_t ws_bytes = 0;
+    // fused output statistics of the fprop that precedes each norm layer
+    ConvStats cst{};
     // host staging
     float* h_gt = nullptr;
     int32_t *h_cls = nullptr, *h_cnt = nullptr;
@@ -457,14 +459,28 @@ size_t max_ws(sdb_det* d) {
 }
 
 // ------------------------------------------------------------------ forward helpers
-void conv_fwd(sdb_det* d, const ConvL& c, const Act& x, const Act& y) {
+void conv_fwd(sdb_det* d, const ConvL& c, const Act& x, const Act& y, bool want_stats = false) {
     PScope ps(d, P_FPROP, conv_flops(c.g));
     if (d->prof.on) { ps.label = shape_label("fprop", c.g); ps.flops_ = conv_flops(c.g); }
-    CK(conv_fprop(c.g, d->dt, x.p, d->wdev_ptr(c.p), y.p, d->ctx->stream));
+    CK(conv_fprop(c.g, d->dt, x.p, d->wdev_ptr(c.p), y.p, d->ctx->stream,
+                  want_stats && d->cst.buf ? &d->cst : nullptr));
+    if (!(want_stats && d->cst.buf)) d->cst.produced = 0;
 }
 
 void norm_fwd(sdb_det* d, const NormL& n, const Act& z, const Act& a) {
     const int64_t rows = static_cast<int64_t>(z.n) * z.h * z.w;
+    if (d->cst.produced) {
+        // statistics came out of the producing fprop's epilogue: finalize + apply
+        PScope ps(d, P_NORM_F, 0, 2.0 * d->es * z.numel(), 2);
+        if (d->prof.on && std::getenv("SDB_PROFILE_VERBOSE")) {
+            ps.label = "norm_fwd(fused stats) rows " + std::to_string(rows) + " C " + std::to_string(n.C);
+            ps.bytes_ = 2.0 * d->es * z.numel();
+        }
+        CK(bn_forward_conv_stats(d->dt, z.p, d->bnp(n.pg), d->bnp(n.pb), a.p, n.mean, n.invstd, rows, n.C, d->cfg.eps,
+                                 n.act, n.slope, d->cst, d->ctx->stream));
+        d->cst.produced = 0;
+        return;
+    }
     PScope ps(d, P_NORM_F, 0, 2.0 * d->es * z.numel(), 3);
     if (d->prof.on && std::getenv("SDB_PROFILE_VERBOSE")) {
         ps.label = "norm_fwd rows " + std::to_string(rows) + " C " + std::to_string(n.C);
@@ -492,11 +508,11 @@ void norm_bwd(sdb_det* d, const NormL& n, const Act& z, const Act& a, const void
 }
 
 void block_fwd(sdb_det* d, Block& b) {
-    conv_fwd(d, b.c1, b.in, b.z1);
+    conv_fwd(d, b.c1, b.in, b.z1, true);
     norm_fwd(d, b.n1, b.z1, b.a1);
-    conv_fwd(d, b.c2, b.a1, b.z2);
+    conv_fwd(d, b.c2, b.a1, b.z2, true);
     norm_fwd(d, b.n2, b.z2, b.a2);
-    conv_fwd(d, b.c3, b.a2, b.z3);
+    conv_fwd(d, b.c3, b.a2, b.z3, true);
     if (b.n3.act == 2) {
         // InPlace-ABN bn3: statistics now, the apply fused with the residual
         // add + leaky that closes the block (one pass: reads z3 + shortcut,
@@ -505,15 +521,22 @@ void block_fwd(sdb_det* d, Block& b) {
         {
             PScope ps(d, P_NORM_F, 0, 1.0 * d->es * b.z3.numel(), 2);
             if (d->prof.on && std::getenv("SDB_PROFILE_VERBOSE")) {
-                ps.label = "norm_stats3 rows " + std::to_string(rows) + " C " + std::to_string(b.n3.C);
+                ps.label = std::string(d->cst.produced ? "norm_stats3(fused) rows " : "norm_stats3 rows ") +
+                           std::to_string(rows) + " C " + std::to_string(b.n3.C);
                 ps.bytes_ = 1.0 * d->es * b.z3.numel();
             }
-            CK(bn_forward_stats(d->dt, b.z3.p, b.n3.mean, b.n3.invstd, rows, b.n3.C, d->cfg.eps, b.n3.act, d->ws,
-                                d->ctx->stream));
+            if (d->cst.produced) {
+                CK(bn_forward_conv_stats(d->dt, b.z3.p, nullptr, nullptr, nullptr, b.n3.mean, b.n3.invstd, rows,
+                                         b.n3.C, d->cfg.eps, b.n3.act, 1.0f, d->cst, d->ctx->stream));
+                d->cst.produced = 0;
+            } else {
+                CK(bn_forward_stats(d->dt, b.z3.p, b.n3.mean, b.n3.invstd, rows, b.n3.C, d->cfg.eps, b.n3.act, d->ws,
+                                    d->ctx->stream));
+            }
         }
         const Act* sc = &b.in;
         if (b.has_down) {
-            conv_fwd(d, b.down, b.in, b.zd);
+            conv_fwd(d, b.down, b.in, b.zd, true);
             norm_fwd(d, b.nd, b.zd, b.d);
             sc = &b.d;
         }
@@ -529,7 +552,7 @@ void block_fwd(sdb_det* d, Block& b) {
     norm_fwd(d, b.n3, b.z3, b.b3);
     const Act* sc = &b.in;
     if (b.has_down) {
-        conv_fwd(d, b.down, b.in, b.zd);
+        conv_fwd(d, b.down, b.in, b.zd, true);
         norm_fwd(d, b.nd, b.zd, b.d);
         sc = &b.d;
     }
@@ -726,9 +749,9 @@ void run_step(sdb_det* d) {
         }
         PScope ps(d, P_FPROP, conv_flops(d->stem2.g));
         if (d->prof.on) { ps.label = shape_label("fprop(stem gemm)", d->stem2.g); ps.flops_ = conv_flops(d->stem2.g); }
-        CK(conv_fprop(d->stem2.g, d->dt, d->stem_x2, d->stem_w2, d->stem_z.p, st));
+        CK(conv_fprop(d->stem2.g, d->dt, d->stem_x2, d->stem_w2, d->stem_z.p, st, d->cst.buf ? &d->cst : nullptr));
     } else {
-        conv_fwd(d, d->stem, d->img, d->stem_z);
+        conv_fwd(d, d->stem, d->img, d->stem_z, true);
     }
     norm_fwd(d, d->stem_n, d->stem_z, d->stem_a);
     { PScope ps(d, P_POOL, 0, d->es * (d->stem_a.numel() + d->pool.numel()));
@@ -1137,6 +1160,10 @@ int sdb_det_create(sdb_ctx* ctx, const sdb_det_config* cfgp, sdb_det** out) {
         d->roi_count = static_cast<int32_t*>(d->alloc(b * 4));
         d->ws_bytes = max_ws(d);
         d->ws = d->alloc(d->ws_bytes);
+        if (d->dt == kF16) {
+            d->cst.cap_bytes = static_cast<size_t>(2 * 148) * 4 * 2 * 256 * sizeof(double);  // 2 CTAs x 148 SMs
+            d->cst.buf = static_cast<double*>(d->alloc(d->cst.cap_bytes));
+        }
         d->defer_wgrad = d->dt == kF16 && ctx->world == 1 && std::getenv("SDB_NO_DEFER_WGRAD") == nullptr;
         if (d->defer_wgrad) {
             size_t off = 0;

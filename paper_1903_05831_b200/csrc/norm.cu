@@ -548,6 +548,84 @@ __global__ void syncbn_coef_kernel(const float* __restrict__ red, const float* _
     coef[C + c] = s2 / m;
 }
 
+// Finalize from an fprop's fused statistics (ConvStats): channel c lives in
+// n-tile nt = c / bn at column j = c % bn of the CTAs b = nt, nt + tiles_n, ...
+// (T = 4 * ctas / tiles_n quadrant terms).  Same thread layout and fixed
+// reduction tree as finalize_kernel (8 channels per CTA, 128 term groups).
+constexpr int kConvTermsMax = 2 * kNumSMs * 4;
+__global__ void __launch_bounds__(kFinThreads) finalize_conv_kernel(const double* __restrict__ cs, int ctas, int tiles_n,
+                                                                    int bn, int C, int64_t count, float eps, int mode,
+                                                                    float* mean, float* invstd) {
+    __shared__ double rs[32][kFinCh], rq[32][kFinCh];
+    pdl_wait();
+    pdl_trigger();
+    const int ch = threadIdx.x % kFinCh, g = threadIdx.x / kFinCh;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int c = blockIdx.x * kFinCh + ch;
+    double S = -0.0, Q = -0.0;
+    if (c < C) {
+        const int nt = c / bn, j = c - nt * bn;
+        const int T = 4 * (ctas / tiles_n);
+        constexpr int kPer = (kConvTermsMax + kFinGroups - 1) / kFinGroups;
+        double sv[kPer], qv[kPer];
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+            const int t = g + kFinGroups * u;
+            if (t < T) {
+                const int b = nt + (t >> 2) * tiles_n, q = t & 3;
+                const double* p = cs + (static_cast<int64_t>(b) * 4 + q) * 2 * bn + j;
+                sv[u] = p[0];
+                qv[u] = p[bn];
+            } else {
+                sv[u] = -0.0;
+                qv[u] = -0.0;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+            S += sv[u];
+            Q += qv[u];
+        }
+    }
+#pragma unroll
+    for (int o = kFinCh; o < 32; o <<= 1) {
+        S += __shfl_xor_sync(0xffffffffu, S, o);
+        Q += __shfl_xor_sync(0xffffffffu, Q, o);
+    }
+    if (lane < kFinCh) {
+        rs[warp][lane] = S;
+        rq[warp][lane] = Q;
+    }
+    __syncthreads();
+    if (warp != 0) return;
+    const int qtr = lane / kFinCh;
+    S = -0.0;
+    Q = -0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        S += rs[qtr * 8 + k][ch];
+        Q += rq[qtr * 8 + k][ch];
+    }
+#pragma unroll
+    for (int o = kFinCh; o < 32; o <<= 1) {
+        S += __shfl_xor_sync(0xffffffffu, S, o);
+        Q += __shfl_xor_sync(0xffffffffu, Q, o);
+    }
+    if (lane >= kFinCh || c >= C) return;
+    double mu, var;
+    if (mode == 0) {
+        const float sf = static_cast<float>(S), qf = static_cast<float>(Q);
+        mu = static_cast<double>(sf) / static_cast<double>(count);
+        var = static_cast<double>(qf) / static_cast<double>(count) - mu * mu;
+    } else {
+        mu = S / static_cast<double>(count);
+        var = Q / static_cast<double>(count) - mu * mu;
+    }
+    if (var < 0.0) var = 0.0;
+    mean[c] = static_cast<float>(mu);
+    invstd[c] = static_cast<float>(1.0 / sqrt(var + static_cast<double>(eps)));
+}
+
 struct Plan {
     int nblocks;
     int64_t rpb;
@@ -692,6 +770,24 @@ cudaError_t iabn_backward(int dtype, const void* dy, const void* y, const float*
     aa.a = y; aa.dy = dy; aa.out = dx; aa.gamma = gamma; aa.beta = beta; aa.invstd = invstd; aa.coef = coef;
     aa.slope = slope; aa.n8 = rows * C / 8; aa.C = C;
     return dtype == kF16 ? run_apply<__half, 3, 2>(aa, rows, pl, st) : run_apply<float, 3, 2>(aa, rows, pl, st);
+}
+
+// ---------------------------------------------------------------- fused statistics
+// mean/invstd from an fprop's fused output statistics (act == 2: IABN double
+// statistics, else BN float-rounded sums), then (y != nullptr) the apply pass
+cudaError_t bn_forward_conv_stats(int dtype, const void* x, const float* gamma, const float* beta, void* y,
+                                  float* mean, float* invstd, int64_t rows, int C, float eps, int act, float slope,
+                                  const ConvStats& cs, cudaStream_t st) {
+    if (!cs.produced || 4 * (cs.ctas / cs.tiles_n) > kConvTermsMax) return cudaErrorInvalidValue;
+    cudaError_t e = launch_pdl(finalize_conv_kernel, dim3((C + kFinCh - 1) / kFinCh), dim3(kFinThreads), 0, st, cs.buf,
+                               cs.ctas, cs.tiles_n, cs.bn, C, rows, eps, act == 2 ? 1 : 0, mean, invstd);
+    if (e != cudaSuccess || !y) return e;
+    const Plan pl = plan_for(rows, C, dtype == kF16 ? 2 : 4);
+    ApplyArgs aa{};
+    aa.a = x; aa.out = y; aa.gamma = gamma; aa.beta = beta; aa.mean = mean; aa.invstd = invstd;
+    aa.slope = slope; aa.act = act; aa.n8 = rows * C / 8; aa.C = C;
+    if (act == 2) return dtype == kF16 ? run_apply<__half, 1, 1>(aa, rows, pl, st) : run_apply<float, 1, 1>(aa, rows, pl, st);
+    return dtype == kF16 ? run_apply<__half, 0, 1>(aa, rows, pl, st) : run_apply<float, 0, 1>(aa, rows, pl, st);
 }
 
 // ---------------------------------------------------------------- SyncBN

@@ -22,7 +22,15 @@ struct ConvShape {
 };
 
 // ---- conv.cu
-cudaError_t conv_fprop(const ConvShape& g, int dtype, const void* x, const void* w, void* y, cudaStream_t st);
+// optional fused output statistics of an fprop (see ConvArgs::stats): when
+// `produced`, buf holds [ctas][4][sum | sumsq][bn] fp64 for finalize_conv_stats
+struct ConvStats {
+    double* buf;
+    size_t cap_bytes;
+    int produced, ctas, tiles_n, bn;
+};
+cudaError_t conv_fprop(const ConvShape& g, int dtype, const void* x, const void* w, void* y, cudaStream_t st,
+                       ConvStats* stats = nullptr);
 // accumulate: dx = conv^T(dy, w) + addend (addend = dx itself when null)
 // mask (optional): dx = round(dx) * (mask > 0 ? 1 : mask_neg), the backward of
 // the ReLU / leaky that produced this layer's input, fused into the epilogue
@@ -72,6 +80,11 @@ cudaError_t bn_backward(int dtype, const void* dy, const void* x, const void* y_
                         const float* mean, const float* invstd, void* dx, float* dgamma, float* dbeta, int64_t rows,
                         int C, void* ws, cudaStream_t st);
 bool norm_channels_ok(int C);
+// BN/IABN forward whose statistics came fused out of the producing fprop
+// (ConvStats.produced); y == nullptr: statistics only (the fused bn3 apply)
+cudaError_t bn_forward_conv_stats(int dtype, const void* x, const float* gamma, const float* beta, void* y,
+                                  float* mean, float* invstd, int64_t rows, int C, float eps, int act, float slope,
+                                  const ConvStats& cs, cudaStream_t st);
 // SyncBN (src/syncbn.cpp:21-117 with a group): the per-rank float sums go to
 // agg [2C+1] (forward: sum, sumsq, count) / red [2C] (backward: sum dy, sum
 // dy*xhat); the caller all-reduces them between the two halves
