@@ -1667,7 +1667,11 @@ static cudaError_t launch_tma(ConvArgs a, int splits, cudaStream_t st, ConvStats
     static const bool no_tma_store = std::getenv("SDB_CONV_NO_TMA_STORE") != nullptr;
     a.tma_out = 0;
     const bool epi_pays = a.R * a.S > 1 || (a.KG + kBK - 1) / kBK <= 4;
-    if (ok && !no_tma_store && epi_pays &&
+    // an fprop whose output statistics are wanted always takes the TMA-store
+    // epilogue: the fused statistics save a full read pass of the output,
+    // more than the slower stores cost on 8+ k-block 1x1 shapes
+    static const bool stats_force = std::getenv("SDB_STATS_NO_FORCE_TMA") == nullptr;
+    if (ok && !no_tma_store && (epi_pays || (MODE == FPROP && cst && stats_force)) &&
         (MODE == FPROP || (MODE == DGRAD && a.stride == 1 && !a.accumulate && !a.mask))) {
         const int cols = MODE == FPROP ? a.NG : a.C;
         const int64_t rows = MODE == FPROP ? static_cast<int64_t>(a.M) : static_cast<int64_t>(a.N) * a.H * a.W;
