@@ -42,7 +42,7 @@ typedef enum {
     SDB_FORMAT = 9          /* simdet::FormatError           errors.hpp:40  */
 } sdb_status;
 
-typedef enum { SDB_F32 = 0, SDB_F16 = 1 } sdb_dtype;
+typedef enum { SDB_F32 = 0, SDB_F16 = 1, SDB_F64 = 2 /* collectives only */ } sdb_dtype;
 
 typedef struct sdb_ctx sdb_ctx;
 
@@ -50,12 +50,25 @@ const char* sdb_last_error(void);
 int sdb_version(void);
 
 /* ---- context: replaces run_workers + CommGroup (src/comm.cpp:242-245,451-471).
- * nccl_id: 128-byte ncclUniqueId shared by all ranks (NULL when world == 1). */
+ * nccl_id: 128-byte ncclUniqueId shared by all ranks (required when world > 1).
+ * world == 1 with an id builds a 1-rank NCCL communicator: every collective of
+ * the data-parallel step is then issued (and captured) as at world > 1.
+ * Ops that take context workspace (conv wgrad, norms, proposal/targets,
+ * losses) must be issued on one stream per context. */
 int sdb_ctx_create(int device, int rank, int world, const void* nccl_id, sdb_ctx** out);
 int sdb_ctx_destroy(sdb_ctx* ctx);
 void* sdb_ctx_stream(sdb_ctx* ctx);
 int sdb_get_nccl_unique_id(void* out128);
 int sdb_synchronize(sdb_ctx* ctx);
+/* in-place SUM over the context's ranks: CommGroup::allreduce_sum
+ * (src/comm.cpp:288-315), NCCL on `stream`; dtype SDB_F32 / SDB_F16 / SDB_F64;
+ * identity without a communicator.  Issue order must agree on every rank (the
+ * reference's sequence check, src/comm.cpp:268-278). */
+int sdb_allreduce_sum(sdb_ctx* ctx, int dtype, void* buf, int64_t n, void* stream);
+/* watchdog: SDB_COLLECTIVE when the communicator reported an asynchronous
+ * error (ncclCommGetAsyncError) -- the CollectiveError path of
+ * src/comm.cpp:270-282 for failures that surface after the call returned */
+int sdb_comm_check(sdb_ctx* ctx);
 
 /* ---- convolution: simdet::conv2d (src/tensor.cpp:169-196) and
  * Tape::conv2d backward (src/autograd.cpp:290-320).
@@ -149,6 +162,42 @@ int sdb_roialign_bwd(sdb_ctx* ctx, int dtype, const void* dy, int N, int H, int 
  * logits/dlogits [R][ld] (first ncls columns valid); loss written to *loss. */
 int sdb_softmax_ce(sdb_ctx* ctx, int dtype, const void* logits, int R, int ncls, int ld, const int32_t* labels,
                    const double* grad_scale, double* loss, void* dlogits, void* stream);
+
+/* losses of the detection step (scale folded into the backward like the CE op,
+ * src/model.cpp:139; loss values are unscaled, written as double to *loss).
+ * RPN objectness: sigmoid BCE, mean over anchors labelled 0/1 (label -1 =
+ * ignored); logits [n_loc][A_pad], labels [n_loc*A] int8. */
+int sdb_rpn_bce(sdb_ctx* ctx, int dtype, const void* logits, int64_t n_loc, int A, int A_pad, const int8_t* labels,
+                const double* grad_scale, double* loss, void* dlogits, void* stream);
+/* RPN box regression: smooth-L1 (beta) over anchors labelled 1, summed and
+ * divided by norm; deltas [n_loc][4*A_pad], targets [n_loc*A][4] fp32 */
+int sdb_rpn_smoothl1(sdb_ctx* ctx, int dtype, const void* deltas, int64_t n_loc, int A, int A_pad,
+                     const int8_t* labels, const float* targets, double beta, double norm, const double* grad_scale,
+                     double* loss, void* ddeltas, void* stream);
+/* RCNN class-specific box regression: smooth-L1 (beta) of pred[r][4*label ..
+ * 4*label+3] against targets[r] for foreground RoIs (label > 0), summed and
+ * divided by the number of RoIs with label >= 0; pred [R][ld] */
+int sdb_smoothl1(sdb_ctx* ctx, int dtype, const void* pred, int R, int ld, const int32_t* labels,
+                 const float* targets, double beta, const double* grad_scale, double* loss, void* dpred,
+                 void* stream);
+/* RPN anchor targets per image: IoU of every anchor with the GT (FP64,
+ * src/postproc.cpp:20-26 convention), fg = best IoU >= fg_thr or the best
+ * anchor of a GT box, bg = best IoU < bg_thr, anchors crossing the image
+ * ignored, then keyed random subsampling to batch anchors with at most
+ * fg_frac*batch foreground (keys [n_img], splitmix64 of the slot);
+ * labels [n_img][nA] (1 fg, 0 bg, -1 ignored), targets [n_img][nA][4]. */
+int sdb_anchor_targets(sdb_ctx* ctx, const float* anchors, int nA, int n_img, const float* gt, int gt_stride,
+                       const int32_t* gt_count, float img_h, float img_w, const uint64_t* keys, double fg_thr,
+                       double bg_thr, int batch, double fg_frac, int8_t* labels, float* targets, void* stream);
+/* RCNN proposal targets per image: candidates = proposals + GT boxes, fg =
+ * IoU >= fg_thr, bg = IoU in [bg_lo, bg_hi), keyed sampling of batch RoIs with
+ * at most round(fg_frac*batch) fg; out_rois [n_img*batch][5] (image, box),
+ * labels (class, 0 bg, -1 padding), targets [..][4], count [n_img] */
+int sdb_proposal_targets(sdb_ctx* ctx, const float* proposals, int prop_stride, const int32_t* prop_count,
+                         const float* gt, const int32_t* gt_cls, int gt_stride, const int32_t* gt_count, int n_img,
+                         const uint64_t* keys, double fg_thr, double bg_hi, double bg_lo, int batch, double fg_frac,
+                         float* out_rois, int32_t* out_labels, float* out_targets, int32_t* out_count,
+                         void* stream);
 
 /* ---- the data-parallel Faster R-CNN C4 training step (src/trainer.cpp:217-271) ---- */
 typedef struct {

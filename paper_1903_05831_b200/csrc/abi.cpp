@@ -17,10 +17,6 @@
 #include "detect.h"
 #include "sdb_internal.h"
 
-namespace sdb {
-cudaError_t comm_allreduce_sum(Ctx* c, void* buf, int64_t n, int dtype, cudaStream_t st);
-}
-
 namespace {
 
 thread_local std::string g_err;
@@ -56,10 +52,14 @@ namespace sdb {
 int set_error(int code, const char* msg) { return fail(code, msg); }
 }  // namespace sdb
 
+// Grow-only scratch shared by the ABI ops of one context.  Ops that take
+// workspace must be issued on ONE stream per context (or be serialised by the
+// caller): two streams would race on its contents.  Growing waits for the
+// whole device, so a caller stream still reading the old buffer is covered.
 void* sdb_ctx::scratch(size_t bytes) {
     if (bytes <= ws_bytes) return ws;
     if (ws) {
-        cudaStreamSynchronize(stream);
+        cudaDeviceSynchronize();
         cudaFree(ws);
     }
     ws_bytes = std::max(bytes, ws_bytes * 2);
@@ -100,12 +100,17 @@ int sdb_ctx_create(int device, int rank, int world, const void* nccl_id, sdb_ctx
         delete c;
         return rc;
     }
-    if (world > 1) {
-        if (!nccl_id) {
-            delete c;
-            return fail(SDB_PARAM, "world > 1 requires an nccl unique id");
-        }
+    // world > 1 needs the shared id; world == 1 with an id builds a 1-rank
+    // communicator, so the data-parallel code path (bucket allreduces inside
+    // the captured step, the loss/BN-gradient allreduces) runs on one GPU
+    if (world > 1 && !nccl_id) {
+        cudaStreamDestroy(c->stream);
+        delete c;
+        return fail(SDB_PARAM, "world > 1 requires an nccl unique id");
+    }
+    if (nccl_id) {
         if (int rc = sdb::comm_init(c, nccl_id)) {
+            cudaStreamDestroy(c->stream);
             delete c;
             return rc;
         }
@@ -366,6 +371,114 @@ int sdb_softmax_ce(sdb_ctx* ctx, int dtype, const void* logits, int R, int ncls,
     sdb::LossArgs la{grad_scale, loss, 0};
     return cuda_status(sdb::softmax_ce(dtype, logits, R, ncls, ld, labels, dlogits, la, nullptr, pick(ctx, stream)),
                        "softmax_ce");
+}
+
+// ---- losses and targets of the detection step (no reference implementation;
+// semantics of the restated oracle, oracle/restate.cpp orc_* -- the same
+// kernels the training step runs)
+
+static size_t loss_scratch(int64_t rows) {
+    return std::max(sdb::loss_workspace_bytes(rows), static_cast<size_t>(rows + 2) * sizeof(double)) + 256;
+}
+
+int sdb_rpn_bce(sdb_ctx* ctx, int dtype, const void* logits, int64_t n_loc, int A, int A_pad, const int8_t* labels,
+                const double* grad_scale, double* loss, void* dlogits, void* stream) {
+    if (!ctx) return fail(SDB_PARAM, "null ctx");
+    if (int rc = check_dtype(dtype)) return rc;
+    if (n_loc < 1 || A < 1 || A_pad < A) return fail(SDB_SHAPE, "rpn_bce: bad sizes");
+    void* ws = ctx->scratch(loss_scratch(n_loc * A));
+    if (!ws) return fail(SDB_CUDA, "workspace allocation failed");
+    sdb::LossArgs la{grad_scale, loss, 0};
+    return cuda_status(sdb::sigmoid_bce(dtype, logits, n_loc, A, A_pad, labels, dlogits, la, ws, pick(ctx, stream)),
+                       "rpn_bce");
+}
+
+int sdb_rpn_smoothl1(sdb_ctx* ctx, int dtype, const void* deltas, int64_t n_loc, int A, int A_pad,
+                     const int8_t* labels, const float* targets, double beta, double norm, const double* grad_scale,
+                     double* loss, void* ddeltas, void* stream) {
+    if (!ctx) return fail(SDB_PARAM, "null ctx");
+    if (int rc = check_dtype(dtype)) return rc;
+    if (n_loc < 1 || A < 1 || A_pad < A) return fail(SDB_SHAPE, "rpn_smoothl1: bad sizes");
+    if (!(beta > 0.0) || !(norm > 0.0)) return fail(SDB_PARAM, "rpn_smoothl1: beta and norm must be > 0");
+    void* ws = ctx->scratch(loss_scratch(n_loc * A));
+    if (!ws) return fail(SDB_CUDA, "workspace allocation failed");
+    sdb::LossArgs la{grad_scale, loss, 0};
+    return cuda_status(sdb::rpn_smooth_l1(dtype, deltas, n_loc, A, A_pad, labels, targets, beta, norm, ddeltas, la,
+                                          ws, pick(ctx, stream)),
+                       "rpn_smoothl1");
+}
+
+int sdb_smoothl1(sdb_ctx* ctx, int dtype, const void* pred, int R, int ld, const int32_t* labels,
+                 const float* targets, double beta, const double* grad_scale, double* loss, void* dpred,
+                 void* stream) {
+    if (!ctx) return fail(SDB_PARAM, "null ctx");
+    if (int rc = check_dtype(dtype)) return rc;
+    if (R < 1 || ld < 8) return fail(SDB_SHAPE, "smoothl1: bad sizes");
+    if (!(beta > 0.0)) return fail(SDB_PARAM, "smoothl1: beta must be > 0");
+    void* ws = ctx->scratch(loss_scratch(R));
+    if (!ws) return fail(SDB_CUDA, "workspace allocation failed");
+    sdb::LossArgs la{grad_scale, loss, 0};
+    return cuda_status(sdb::rcnn_smooth_l1(dtype, pred, R, ld, labels, targets, beta, dpred, la, ws,
+                                           pick(ctx, stream)),
+                       "smoothl1");
+}
+
+int sdb_anchor_targets(sdb_ctx* ctx, const float* anchors, int nA, int n_img, const float* gt, int gt_stride,
+                       const int32_t* gt_count, float img_h, float img_w, const uint64_t* keys, double fg_thr,
+                       double bg_thr, int batch, double fg_frac, int8_t* labels, float* targets, void* stream) {
+    if (!ctx) return fail(SDB_PARAM, "null ctx");
+    if (nA < 1 || n_img < 1 || gt_stride < 1 || batch < 1) return fail(SDB_SHAPE, "anchor_targets: bad sizes");
+    if (!(fg_frac >= 0.0 && fg_frac <= 1.0) || bg_thr > fg_thr)
+        return fail(SDB_PARAM, "anchor_targets: fg fraction in [0,1], bg threshold <= fg threshold");
+    void* ws = ctx->scratch(sdb::anchor_target_workspace_bytes(n_img, nA, gt_stride));
+    if (!ws) return fail(SDB_CUDA, "workspace allocation failed");
+    sdb::AnchorTargetArgs a{};
+    a.anchors = anchors; a.nA = nA; a.n_img = n_img; a.gt = gt; a.gt_stride = gt_stride; a.gt_count = gt_count;
+    a.img_h = img_h; a.img_w = img_w; a.keys = keys; a.fg_thr = fg_thr; a.bg_thr = bg_thr; a.batch = batch;
+    a.fg_cap = static_cast<int>(fg_frac * batch); a.labels = labels; a.targets = targets;
+    return cuda_status(sdb::anchor_targets(a, ws, pick(ctx, stream)), "anchor_targets");
+}
+
+int sdb_proposal_targets(sdb_ctx* ctx, const float* proposals, int prop_stride, const int32_t* prop_count,
+                         const float* gt, const int32_t* gt_cls, int gt_stride, const int32_t* gt_count, int n_img,
+                         const uint64_t* keys, double fg_thr, double bg_hi, double bg_lo, int batch, double fg_frac,
+                         float* out_rois, int32_t* out_labels, float* out_targets, int32_t* out_count,
+                         void* stream) {
+    if (!ctx) return fail(SDB_PARAM, "null ctx");
+    if (prop_stride < 1 || gt_stride < 1 || n_img < 1 || batch < 1)
+        return fail(SDB_SHAPE, "proposal_targets: bad sizes");
+    if (!(fg_frac >= 0.0 && fg_frac <= 1.0) || bg_lo > bg_hi)
+        return fail(SDB_PARAM, "proposal_targets: fg fraction in [0,1], bg_lo <= bg_hi");
+    const int stride = prop_stride + gt_stride;
+    const size_t flag_bytes = (static_cast<size_t>(n_img) * stride + 255) & ~size_t(255);
+    void* ws = ctx->scratch(flag_bytes + static_cast<size_t>(n_img) * stride * 4);
+    if (!ws) return fail(SDB_CUDA, "workspace allocation failed");
+    sdb::ProposalTargetArgs a{};
+    a.proposals = proposals; a.prop_stride = prop_stride; a.prop_count = prop_count; a.gt = gt; a.gt_cls = gt_cls;
+    a.gt_stride = gt_stride; a.gt_count = gt_count; a.keys = keys; a.fg_thr = fg_thr; a.bg_hi = bg_hi;
+    a.bg_lo = bg_lo; a.batch = batch; a.fg_cap = static_cast<int>(std::llround(fg_frac * batch)); a.n_img = n_img;
+    a.work_flag = static_cast<int8_t*>(ws);
+    a.work_arg = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(ws) + flag_bytes);
+    a.work_stride = stride;
+    a.out_rois = out_rois; a.out_labels = out_labels; a.out_targets = out_targets; a.out_src = nullptr;
+    a.out_count = out_count;
+    return cuda_status(sdb::proposal_targets(a, pick(ctx, stream)), "proposal_targets");
+}
+
+// ---- collectives: CommGroup::allreduce_sum (src/comm.cpp:288-315)
+int sdb_allreduce_sum(sdb_ctx* ctx, int dtype, void* buf, int64_t n, void* stream) {
+    if (!ctx) return fail(SDB_PARAM, "null ctx");
+    if (dtype != SDB_F32 && dtype != SDB_F16 && dtype != SDB_F64) return fail(SDB_PARAM, "allreduce: dtype");
+    if (n < 0) return fail(SDB_SHAPE, "allreduce: negative length");
+    const int d = dtype == SDB_F64 ? 3 : dtype;
+    if (sdb::comm_allreduce(ctx, buf, n, d, 0, pick(ctx, stream)) != cudaSuccess) return SDB_COLLECTIVE;
+    return SDB_OK;
+}
+
+int sdb_comm_check(sdb_ctx* ctx) {
+    if (!ctx) return fail(SDB_PARAM, "null ctx");
+    if (sdb::comm_async_error(ctx)) return fail(SDB_COLLECTIVE, "communicator reported an asynchronous error");
+    return SDB_OK;
 }
 
 int sdb_cast(sdb_ctx* ctx, int src_dtype, const void* src, int dst_dtype, void* dst, int64_t n, void* stream) {

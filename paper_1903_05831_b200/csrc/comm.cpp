@@ -11,11 +11,15 @@
 #include "ctx.h"
 #include "sdb_internal.h"
 
+namespace {
+constexpr int SDB_COLLECTIVE_CODE = 6;  // SDB_COLLECTIVE (include/sdb.h)
+}
+
 namespace sdb {
 
 int comm_unique_id(void* out128) {
     ncclUniqueId id;
-    if (ncclGetUniqueId(&id) != ncclSuccess) return 6;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return SDB_COLLECTIVE_CODE;
     std::memcpy(out128, &id, sizeof(id));
     return 0;
 }
@@ -24,7 +28,11 @@ int comm_init(Ctx* c, const void* id128) {
     ncclUniqueId id;
     std::memcpy(&id, id128, sizeof(id));
     ncclComm_t comm;
-    if (ncclCommInitRank(&comm, c->world, id, c->rank) != ncclSuccess) return 6;
+    const ncclResult_t r = ncclCommInitRank(&comm, c->world, id, c->rank);
+    if (r != ncclSuccess) {
+        set_error(SDB_COLLECTIVE_CODE, (std::string("ncclCommInitRank: ") + ncclGetErrorString(r)).c_str());
+        return SDB_COLLECTIVE_CODE;
+    }
     c->nccl = comm;
     return 0;
 }
@@ -36,16 +44,40 @@ void comm_destroy(Ctx* c) {
     }
 }
 
-// in-place SUM allreduce (the reference's allreduce_sum contract)
-cudaError_t comm_allreduce_sum(Ctx* c, void* buf, int64_t n, int dtype, cudaStream_t st) {
-    if (c->world == 1 || n == 0) return cudaSuccess;
+// in-place allreduce on `st` (the reference's allreduce_sum contract,
+// src/comm.cpp:288-315).  avg = 1: ncclAvg, which NCCL implements for floating
+// types as a pre-multiply of every rank's values by 1/K followed by the sum --
+// used for the fp16 gradient buckets so the reduced value cannot overflow when
+// no rank's value does.  A no-op without a communicator; with a forced 1-rank
+// communicator the call is issued (and captured) like at K > 1.
+cudaError_t comm_allreduce(Ctx* c, void* buf, int64_t n, int dtype, int avg, cudaStream_t st) {
+    if (!c->nccl || n == 0) return cudaSuccess;
     // dtype: kF32, kF16, 2 = int32, 3 = float64
     const ncclDataType_t t = dtype == kF16 ? ncclFloat16
                              : dtype == kF32 ? ncclFloat32
                              : dtype == 3 ? ncclFloat64 : ncclInt32;
-    const ncclResult_t r =
-        ncclAllReduce(buf, buf, static_cast<size_t>(n), t, ncclSum, static_cast<ncclComm_t>(c->nccl), st);
-    return r == ncclSuccess ? cudaSuccess : cudaErrorUnknown;
+    const ncclResult_t r = ncclAllReduce(buf, buf, static_cast<size_t>(n), t, avg ? ncclAvg : ncclSum,
+                                         static_cast<ncclComm_t>(c->nccl), st);
+    if (r != ncclSuccess) {
+        set_error(SDB_COLLECTIVE_CODE, (std::string("ncclAllReduce: ") + ncclGetErrorString(r) + " / " +
+                                        ncclGetLastError(static_cast<ncclComm_t>(c->nccl))).c_str());
+        c->last_nccl_error = static_cast<int>(r);
+        return cudaErrorUnknown;
+    }
+    return cudaSuccess;
+}
+
+cudaError_t comm_allreduce_sum(Ctx* c, void* buf, int64_t n, int dtype, cudaStream_t st) {
+    return comm_allreduce(c, buf, n, dtype, 0, st);
+}
+
+// asynchronous communicator errors (a peer died, a network failure): the
+// watchdog half of the reference's CollectiveError path (src/comm.cpp:270-282)
+int comm_async_error(Ctx* c) {
+    if (!c->nccl) return 0;
+    ncclResult_t a = ncclSuccess;
+    if (ncclCommGetAsyncError(static_cast<ncclComm_t>(c->nccl), &a) != ncclSuccess) return 1;
+    return a == ncclSuccess || a == ncclInProgress ? 0 : 1;
 }
 
 }  // namespace sdb

@@ -32,15 +32,20 @@
 #include "detect.h"
 #include "sdb_internal.h"
 
-namespace sdb {
-cudaError_t comm_allreduce_sum(Ctx* c, void* buf, int64_t n, int dtype, cudaStream_t st);
-}
-
 using namespace sdb;
 
 namespace {
 
 int det_fail(int code, const std::string& m) { return sdb::set_error(code, m.c_str()); }
+
+// a failed NCCL call (its message is in sdb_last_error): maps to SDB_COLLECTIVE
+struct CollectiveFailure : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+#define CKC(expr)                                                                         \
+    do {                                                                                  \
+        if ((expr) != cudaSuccess) throw CollectiveFailure(std::string(#expr) + ": " + sdb_last_error()); \
+    } while (0)
 
 #define CK(expr)                                                                          \
     do {                                                                                  \
@@ -169,15 +174,24 @@ struct sdb_det {
     int A = 0, A_pad = 0, n_loc = 0, nA = 0, fh = 0, fw = 0, ncls = 0, ncls_pad = 0, nbox_pad = 0;
     int R = 0, P = 0, head_hw = 0, feat_c = 0;
     int roi_step = 1;  // RoIAlign bin subsampling folded from a 1x1 stride-2 head entry
-    // deferred split-K wgrad reduction (fp16, one rank): every conv keeps its fp32
-    // partials in its own arena slice; one batched reduce before the optimizer
+    // deferred split-K wgrad reduction (fp16): every conv keeps its fp32
+    // partials in its own arena slice; each gradient bucket is reduced by one
+    // batched launch as soon as the last wgrad of the bucket has been issued
+    // (then, with a communicator, allreduced) -- the same schedule at every
+    // world size
     bool defer_wgrad = false;
     uint8_t* wg_arena = nullptr;
     std::map<int, size_t> wg_off;  // param index -> arena byte offset
-    std::vector<WgradJob> wg_jobs;
-    WgradJob* wg_jobs_dev = nullptr;
-    int* wg_tiles_dev = nullptr;
-    int wg_njobs_dev = 0, wg_total_tiles = 0;
+    struct BucketTab {
+        WgradJob* jobs = nullptr;  // device job table (uploaded at the first step)
+        int* tiles = nullptr;      // tile prefix of the jobs
+        int njobs = 0, total = 0;
+    };
+    std::vector<int> bucket_of;                // param index -> bucket (conv/fc), -1 otherwise
+    std::vector<int> bucket_nparams;           // conv/fc params per bucket
+    std::vector<int> bucket_left;              // this step: params whose wgrad is not issued yet
+    std::vector<std::vector<WgradJob>> bjobs;  // this step: issued jobs per bucket
+    std::vector<BucketTab> btab;
     // the deferred wgrads run on a side stream, overlapping the dgrad -> norm
     // backward chain; each takes its dz from a ring whose slots are recycled
     // only after the wgrad that read them has finished
@@ -221,14 +235,21 @@ struct sdb_det {
     size_t ws_bytes = 0;
     // fused output statistics of the fprop that precedes each norm layer
     ConvStats cst{};
-    // host staging
-    float* h_gt = nullptr;
-    int32_t *h_cls = nullptr, *h_cnt = nullptr;
-    uint64_t* h_keys = nullptr;
-    int64_t* h_slots = nullptr;
+    // host staging, double-buffered: a call waits only for the copies that
+    // read its slot two calls ago (never for the previous step's compute)
+    static constexpr int kStage = 2;
+    float* h_gt[kStage] = {};
+    int32_t *h_cls[kStage] = {}, *h_cnt[kStage] = {};
+    uint64_t* h_keys[kStage] = {};
+    int64_t* h_slots[kStage] = {};
+    cudaEvent_t stage_ev[kStage] = {};
+    bool stage_busy[kStage] = {};
+    int stage_next = 0;
     int64_t* slots_dev = nullptr;
     double* h_losses = nullptr;
-    // comm
+    // comm: an NCCL communicator exists (world > 1, or a forced 1-rank one that
+    // runs the data-parallel code path on one GPU)
+    bool comm_on = false;
     cudaStream_t comm = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     std::vector<cudaEvent_t> bucket_ev;
@@ -590,19 +611,77 @@ void* dz_buf(Bwd& B, void* fallback) {
     return d->dzr[k];
 }
 
+// allreduce of gradient bucket b on the comm stream once `st` reaches this
+// point.  fp16 buckets are AVERAGED (ncclAvg: NCCL pre-multiplies each rank's
+// values by 1/K, then sums), so the reduced value stays in range whenever
+// every rank's is -- overflow detection does not depend on K -- and the
+// optimizer divides by the loss scale only; fp32 buckets are summed and the
+// optimizer divides by scale*K (src/trainer.cpp:86-94).
+void issue_bucket_allreduce(sdb_det* d, size_t b, cudaStream_t st) {
+    const auto [lo, hi] = d->buckets[b];
+    cudaEvent_t ev = d->bucket_ev[b];
+    CK(cudaEventRecord(ev, st));
+    CK(cudaStreamWaitEvent(d->comm, ev, 0));
+    CKC(comm_allreduce(d->ctx, static_cast<uint8_t*>(d->g) + lo * d->es, hi - lo, d->dt, d->dt == kF16, d->comm));
+}
+
+// non-deferred wgrads (fp32 modes): buckets are issued in plan order as the
+// backward pass walks past their lower edge
 void grads_ready(Bwd& B, int pi) {
     sdb_det* d = B.d;
-    if (d->ctx->world == 1) return;
+    if (!d->comm_on) return;
     const int64_t off = d->params[pi].off;
     while (B.next_bucket < d->buckets.size() && off <= d->buckets[B.next_bucket].first) {
-        const auto [lo, hi] = d->buckets[B.next_bucket];
-        cudaEvent_t ev = d->bucket_ev[B.next_bucket];
-        PScope ps(d, P_COMM, 0, static_cast<double>(hi - lo) * d->es);
-        CK(cudaEventRecord(ev, d->ctx->stream));
-        CK(cudaStreamWaitEvent(d->comm, ev, 0));
-        CK(comm_allreduce_sum(d->ctx, static_cast<uint8_t*>(d->g) + lo * d->es, hi - lo, d->dt, d->comm));
+        PScope ps(d, P_COMM, 0, static_cast<double>(d->buckets[B.next_bucket].second - d->buckets[B.next_bucket].first) * d->es);
+        issue_bucket_allreduce(d, B.next_bucket, d->ctx->stream);
         ++B.next_bucket;
     }
+}
+
+// deferred wgrads: bucket b is complete once the wgrad of each of its
+// parameters has been issued; its split-K partials are then reduced by one
+// batched launch on the stream that ran those wgrads (stream order covers
+// them), the stem's GEMM-form gradient is folded back, and the bucket goes to
+// the comm stream.  The job tables are static (fixed shapes and buffers):
+// uploaded once, from the first (eager) step.
+void flush_bucket(sdb_det* d, int b, cudaStream_t st) {
+    auto& T = d->btab[b];
+    auto& J = d->bjobs[b];
+    if (!T.jobs) {
+        std::vector<int> start(J.size());
+        int tot = 0;
+        for (size_t k = 0; k < J.size(); ++k) {
+            start[k] = tot;
+            tot += wgrad_job_tiles(J[k]);
+        }
+        T.jobs = static_cast<WgradJob*>(d->alloc(J.size() * sizeof(WgradJob)));
+        T.tiles = static_cast<int*>(d->alloc(start.size() * sizeof(int)));
+        CK(cudaMemcpyAsync(T.jobs, J.data(), J.size() * sizeof(WgradJob), cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(T.tiles, start.data(), start.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+        CK(cudaStreamSynchronize(st));
+        T.njobs = static_cast<int>(J.size());
+        T.total = tot;
+    } else if (static_cast<int>(J.size()) != T.njobs) {
+        throw std::runtime_error("wgrad job table changed between steps");
+    }
+    J.clear();
+    {
+        PScope ps(d, P_WGRAD, 0, 0, 1);
+        CK(wgrad_reduce_batched(T.jobs, T.tiles, T.njobs, T.total, st));
+        if (d->stem_gemm && d->bucket_of[d->stem.p] == b)
+            CK(stem_weights(d->stem_dw2, 64, 8, d->gptr(d->stem.p), 1, st));
+    }
+    if (d->comm_on) {
+        PScope ps(d, P_COMM, 0, static_cast<double>(d->buckets[b].second - d->buckets[b].first) * d->es);
+        issue_bucket_allreduce(d, static_cast<size_t>(b), st);
+    }
+}
+
+void job_issued(sdb_det* d, int pi, const WgradJob& job, cudaStream_t st) {
+    const int b = d->bucket_of.at(pi);
+    if (b < 0) throw std::runtime_error("wgrad of a parameter outside the bucket plan");
+    d->bjobs[b].push_back(job);
+    if (--d->bucket_left[b] == 0) flush_bucket(d, b, st);
 }
 
 void conv_wgrad_to(Bwd& B, const ConvL& c, const Act& x, const void* dy, void* dw_override = nullptr,
@@ -624,21 +703,21 @@ void conv_wgrad_to(Bwd& B, const ConvL& c, const Act& x, const void* dy, void* d
         WgradJob job{};
         CK(conv_wgrad_deferred(c.g, d->dt, x.p, dy, dwp, d->wg_arena + it->second,
                                conv_wgrad_workspace(c.g, d->dt), ws, &job));
-        d->wg_jobs.push_back(job);
         if (B.side && B.slot >= 0 && dy == d->dzr[B.slot]) {
             CK(cudaEventRecord(d->dzr_ev[B.slot], d->wst));
             d->dzr_busy[B.slot] = true;
             B.slot = -1;
         }
-    } else {
-        CK(conv_wgrad(c.g, d->dt, x.p, dy, dwp, d->ws, d->ws_bytes, d->ctx->stream));
+        job_issued(d, c.p, job, ws);
+        return;
     }
+    CK(conv_wgrad(c.g, d->dt, x.p, dy, dwp, d->ws, d->ws_bytes, d->ctx->stream));
     }
     if (ready) grads_ready(B, c.p);
 }
 
 // the stem's GEMM-form wgrad into dW' (stem_dw2); without the deferred reduce
-// it is folded into the gradient right away, else after the batched reduce
+// it is folded into the gradient right away, else by its bucket's flush
 void stem_wgrad_to(Bwd& B, const ConvL& c2, void* x2, const void* dy) {
     sdb_det* d = B.d;
     Act xa{};
@@ -701,7 +780,7 @@ void rpn_branch_side(sdb_det* d) {
         WgradJob job{};
         CK(conv_wgrad_deferred(c.g, d->dt, x, dy, d->gptr(c.p), d->wg_arena + d->wg_off.at(c.p),
                                conv_wgrad_workspace(c.g, d->dt), s2, &job));
-        d->wg_jobs.push_back(job);
+        job_issued(d, c.p, job, s2);
     };
     wgrad(d->rpn_bbox, d->rpn_a.p, d->d_rpn_deltas);
     wgrad(d->rpn_cls, d->rpn_a.p, d->d_rpn_logits);
@@ -727,6 +806,8 @@ void run_step(sdb_det* d) {
     cudaStream_t st = d->ctx->stream;
     const auto& cf = d->cfg;
     const bool side = d->side_wgrad && !d->prof.on;
+    d->bucket_left = d->bucket_nparams;
+    for (auto& j : d->bjobs) j.clear();
     AnchorTargetArgs at{};
     at.anchors = d->anchors; at.nA = d->nA; at.n_img = cf.batch; at.gt = d->gt; at.gt_stride = cf.max_gt;
     at.gt_count = d->gt_count; at.img_h = static_cast<float>(cf.img_h); at.img_w = static_cast<float>(cf.img_w);
@@ -909,50 +990,30 @@ void run_step(sdb_det* d) {
         CK(cudaStreamWaitEvent(st, d->wev_join, 0));
     }
 
+    if (d->defer_wgrad)
+        for (int left : d->bucket_left)
+            if (left != 0) throw std::runtime_error("gradient bucket left incomplete by the backward schedule");
+
     // ---- data-parallel reduction, overflow check, update
-    if (d->ctx->world > 1) {
-        grads_ready(B, 0);  // flush any remaining bucket
+    if (d->comm_on) {
+        if (!d->defer_wgrad) grads_ready(B, 0);  // flush any remaining bucket
+        PScope ps(d, P_COMM, 0, 4.0 * d->n_bn + 32.0);
         CK(cudaEventRecord(d->ev_fork, st));
         CK(cudaStreamWaitEvent(d->comm, d->ev_fork, 0));
-        CK(comm_allreduce_sum(d->ctx, d->bng, d->n_bn, kF32, d->comm));
-        CK(comm_allreduce_sum(d->ctx, d->losses, 4, 3 /* f64 */, d->comm));
+        CKC(comm_allreduce(d->ctx, d->bng, d->n_bn, kF32, 0, d->comm));
+        CKC(comm_allreduce(d->ctx, d->losses, 4, 3 /* f64 */, 0, d->comm));
         CK(cudaEventRecord(d->ev_join, d->comm));
         CK(cudaStreamWaitEvent(st, d->ev_join, 0));
-    }
-    if (d->defer_wgrad) {
-        // the job table is the same every step (static shapes and buffers):
-        // uploaded once, from the first (eager) step
-        if (!d->wg_jobs_dev) {
-            std::vector<int> start(d->wg_jobs.size());
-            int tot = 0;
-            for (size_t k = 0; k < d->wg_jobs.size(); ++k) {
-                start[k] = tot;
-                tot += wgrad_job_tiles(d->wg_jobs[k]);
-            }
-            d->wg_jobs_dev = static_cast<WgradJob*>(d->alloc(d->wg_jobs.size() * sizeof(WgradJob)));
-            d->wg_tiles_dev = static_cast<int*>(d->alloc(start.size() * sizeof(int)));
-            // ordered on the step's stream (pageable copies: staged before return)
-            CK(cudaMemcpyAsync(d->wg_jobs_dev, d->wg_jobs.data(), d->wg_jobs.size() * sizeof(WgradJob),
-                               cudaMemcpyHostToDevice, st));
-            CK(cudaMemcpyAsync(d->wg_tiles_dev, start.data(), start.size() * sizeof(int), cudaMemcpyHostToDevice, st));
-            CK(cudaStreamSynchronize(st));
-            d->wg_njobs_dev = static_cast<int>(d->wg_jobs.size());
-            d->wg_total_tiles = tot;
-        } else if (static_cast<int>(d->wg_jobs.size()) != d->wg_njobs_dev) {
-            throw std::runtime_error("wgrad job table changed between steps");
-        }
-        d->wg_jobs.clear();
-        PScope ps(d, P_WGRAD, 0, 0, 1);
-        CK(wgrad_reduce_batched(d->wg_jobs_dev, d->wg_tiles_dev, d->wg_njobs_dev, d->wg_total_tiles, st));
-        if (d->stem_gemm) CK(stem_weights(d->stem_dw2, 64, 8, d->gptr(d->stem.p), 1, st));
     }
     PScope ps_opt(d, P_OPTIM, 0, (d->es + 12.0 + (d->dt == kF16 ? 2.0 : 0.0)) * d->n_w + 16.0 * d->n_bn, 5);
     CK(cudaMemsetAsync(d->flag, 0, sizeof(int), st));
     CK(nonfinite_check(d->dt, d->g, d->n_w, d->flag, st));
     CK(nonfinite_check(kF32, d->bng, d->n_bn, d->flag, st));
     const double K = static_cast<double>(d->ctx->world);
+    // fp16 buckets arrive averaged over the ranks (issue_bucket_allreduce)
+    const double Kw = d->dt == kF16 ? 1.0 : K;
     CK(fused_sgd(d->dt, d->g, d->w32, d->v32, d->dt == kF16 ? static_cast<__half*>(d->wdev) : nullptr, d->n_w, cf.lr,
-                 cf.momentum, d->scale, K, d->flag, st));
+                 cf.momentum, d->scale, Kw, d->flag, st));
     CK(fused_sgd(kF32, d->bng, d->bn32, d->bnv, nullptr, d->n_bn, cf.lr, cf.momentum, d->scale, K, d->flag, st));
     CK(update_scale_device(d->scale, d->good, d->flag, cf.dynamic_scale, cf.growth_interval, cf.growth, cf.backoff,
                            cf.min_scale, cf.max_scale, st));
@@ -1164,7 +1225,8 @@ int sdb_det_create(sdb_ctx* ctx, const sdb_det_config* cfgp, sdb_det** out) {
             d->cst.cap_bytes = static_cast<size_t>(2 * 148) * 4 * 2 * 256 * sizeof(double);  // 2 CTAs x 148 SMs
             d->cst.buf = static_cast<double*>(d->alloc(d->cst.cap_bytes));
         }
-        d->defer_wgrad = d->dt == kF16 && ctx->world == 1 && std::getenv("SDB_NO_DEFER_WGRAD") == nullptr;
+        d->comm_on = ctx->nccl != nullptr;
+        d->defer_wgrad = d->dt == kF16 && std::getenv("SDB_NO_DEFER_WGRAD") == nullptr;
         if (d->defer_wgrad) {
             size_t off = 0;
             auto add = [&](const ConvL& c) {
@@ -1200,21 +1262,21 @@ int sdb_det_create(sdb_ctx* ctx, const sdb_det_config* cfgp, sdb_det** out) {
                 CK(cudaEventCreateWithFlags(&d->dzr_ev[k], cudaEventDisableTiming));
             }
         }
-        CK(cudaMallocHost(&d->h_gt, static_cast<size_t>(b) * cf.max_gt * 16));
-        CK(cudaMallocHost(&d->h_cls, static_cast<size_t>(b) * cf.max_gt * 4));
-        CK(cudaMallocHost(&d->h_cnt, b * 4));
-        CK(cudaMallocHost(&d->h_keys, 2 * b * 8));
-        CK(cudaMallocHost(&d->h_slots, b * 8));
+        for (int k = 0; k < sdb_det::kStage; ++k) {
+            CK(cudaMallocHost(&d->h_gt[k], static_cast<size_t>(b) * cf.max_gt * 16));
+            CK(cudaMallocHost(&d->h_cls[k], static_cast<size_t>(b) * cf.max_gt * 4));
+            CK(cudaMallocHost(&d->h_cnt[k], b * 4));
+            CK(cudaMallocHost(&d->h_keys[k], 2 * b * 8));
+            CK(cudaMallocHost(&d->h_slots[k], b * 8));
+            CK(cudaEventCreateWithFlags(&d->stage_ev[k], cudaEventDisableTiming));
+        }
         d->slots_dev = static_cast<int64_t*>(d->alloc(b * 8));
         CK(cudaMallocHost(&d->h_losses, 16 * 8));
 
-        // ---- comm: fp16 buckets from the end of the flat gradient (backward order)
-        if (ctx->world > 1) {
-            int plo = 0, phi = 0;
-            CK(cudaDeviceGetStreamPriorityRange(&plo, &phi));
-            CK(cudaStreamCreateWithPriority(&d->comm, cudaStreamNonBlocking, phi));
-            CK(cudaEventCreateWithFlags(&d->ev_fork, cudaEventDisableTiming));
-            CK(cudaEventCreateWithFlags(&d->ev_join, cudaEventDisableTiming));
+        // ---- gradient buckets over the flat fp16/fp32 gradient, formed from the
+        // END (backward produces the last layers first); planned at every world
+        // size, so one schedule serves N = 1 and N > 1
+        if (d->comm_on || d->defer_wgrad) {
             const int64_t cap = static_cast<int64_t>(cf.bucket_mb * 1024 * 1024 / d->es);
             std::vector<int64_t> offs;
             for (const Param& p : d->params)
@@ -1223,11 +1285,30 @@ int sdb_det_create(sdb_ctx* ctx, const sdb_det_config* cfgp, sdb_det** out) {
             const int nb = sdb_plan_buckets(offs.data(), static_cast<int>(offs.size()), d->n_w, cap, lohi.data(),
                                             static_cast<int>(offs.size()) + 1);
             for (int i = 0; i < nb; ++i) d->buckets.push_back({lohi[2 * i], lohi[2 * i + 1]});
+            d->bucket_of.assign(d->params.size(), -1);
+            d->bucket_nparams.assign(d->buckets.size(), 0);
+            for (size_t pi = 0; pi < d->params.size(); ++pi) {
+                if (d->params[pi].kind > 1) continue;
+                for (size_t bi = 0; bi < d->buckets.size(); ++bi)
+                    if (d->params[pi].off >= d->buckets[bi].first && d->params[pi].off < d->buckets[bi].second) {
+                        d->bucket_of[pi] = static_cast<int>(bi);
+                        ++d->bucket_nparams[bi];
+                    }
+            }
+            d->bjobs.resize(d->buckets.size());
+            d->btab.resize(d->buckets.size());
             for (size_t i = 0; i < d->buckets.size(); ++i) {
                 cudaEvent_t e;
                 CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
                 d->bucket_ev.push_back(e);
             }
+        }
+        if (d->comm_on) {
+            int plo = 0, phi = 0;
+            CK(cudaDeviceGetStreamPriorityRange(&plo, &phi));
+            CK(cudaStreamCreateWithPriority(&d->comm, cudaStreamNonBlocking, phi));
+            CK(cudaEventCreateWithFlags(&d->ev_fork, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&d->ev_join, cudaEventDisableTiming));
         }
         init_params(d);
     } catch (const std::exception& e) {
@@ -1244,11 +1325,14 @@ int sdb_det_destroy(sdb_det* d) {
     cudaStreamSynchronize(d->ctx->stream);
     if (d->gexec) cudaGraphExecDestroy(d->gexec);
     for (void* p : d->allocs) cudaFree(p);
-    cudaFreeHost(d->h_gt);
-    cudaFreeHost(d->h_cls);
-    cudaFreeHost(d->h_cnt);
-    cudaFreeHost(d->h_keys);
-    cudaFreeHost(d->h_slots);
+    for (int k = 0; k < sdb_det::kStage; ++k) {
+        cudaFreeHost(d->h_gt[k]);
+        cudaFreeHost(d->h_cls[k]);
+        cudaFreeHost(d->h_cnt[k]);
+        cudaFreeHost(d->h_keys[k]);
+        cudaFreeHost(d->h_slots[k]);
+        if (d->stage_ev[k]) cudaEventDestroy(d->stage_ev[k]);
+    }
     cudaFreeHost(d->h_losses);
     for (auto e : d->bucket_ev) cudaEventDestroy(e);
     if (d->wst) {
@@ -1501,34 +1585,52 @@ int sdb_det_load_checkpoint(sdb_det* d, const char* path, uint64_t* config_diges
     return SDB_OK;
 }
 
+// next pinned staging slot: waits (host) only for the H2D copies that read it
+// two calls ago -- those sit at the start of an earlier step, so the host runs
+// ahead of the device instead of draining the stream every step
+static int stage_slot(sdb_det* d) {
+    const int k = d->stage_next;
+    d->stage_next = (k + 1) % sdb_det::kStage;
+    if (d->stage_busy[k]) CK(cudaEventSynchronize(d->stage_ev[k]));
+    d->stage_busy[k] = false;
+    return k;
+}
+
+static void stage_done(sdb_det* d, int k) {
+    CK(cudaEventRecord(d->stage_ev[k], d->ctx->stream));
+    d->stage_busy[k] = true;
+}
+
 static void stage_gt(sdb_det* d, const float* gt_boxes, const int32_t* gt_cls, const int32_t* gt_count,
                      const int64_t* slots) {
     const auto& cf = d->cfg;
     const int b = cf.batch;
-    std::memcpy(d->h_gt, gt_boxes, static_cast<size_t>(b) * cf.max_gt * 16);
-    std::memcpy(d->h_cls, gt_cls, static_cast<size_t>(b) * cf.max_gt * 4);
-    for (int j = 0; j < b; ++j) d->h_cnt[j] = std::min(std::max(gt_count[j], 0), cf.max_gt);
+    const int k = stage_slot(d);
+    std::memcpy(d->h_gt[k], gt_boxes, static_cast<size_t>(b) * cf.max_gt * 16);
+    std::memcpy(d->h_cls[k], gt_cls, static_cast<size_t>(b) * cf.max_gt * 4);
+    for (int j = 0; j < b; ++j) d->h_cnt[k][j] = std::min(std::max(gt_count[j], 0), cf.max_gt);
     for (int j = 0; j < b; ++j) {
-        d->h_keys[j] = mix64(cf.seed ^ 0xA11C0000ull, static_cast<uint64_t>(slots[j]));
-        d->h_keys[b + j] = mix64(cf.seed ^ 0x5A3B0000ull, static_cast<uint64_t>(slots[j]));
+        d->h_keys[k][j] = mix64(cf.seed ^ 0xA11C0000ull, static_cast<uint64_t>(slots[j]));
+        d->h_keys[k][b + j] = mix64(cf.seed ^ 0x5A3B0000ull, static_cast<uint64_t>(slots[j]));
     }
     cudaStream_t st = d->ctx->stream;
-    CK(cudaMemcpyAsync(d->gt, d->h_gt, static_cast<size_t>(b) * cf.max_gt * 16, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(d->gt_cls, d->h_cls, static_cast<size_t>(b) * cf.max_gt * 4, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(d->gt_count, d->h_cnt, b * 4, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(d->keys, d->h_keys, 2 * b * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d->gt, d->h_gt[k], static_cast<size_t>(b) * cf.max_gt * 16, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d->gt_cls, d->h_cls[k], static_cast<size_t>(b) * cf.max_gt * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d->gt_count, d->h_cnt[k], b * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d->keys, d->h_keys[k], 2 * b * 8, cudaMemcpyHostToDevice, st));
+    stage_done(d, k);
 }
 
 int sdb_det_set_batch(sdb_det* d, const void* images, int on_host, const float* gt_boxes, const int32_t* gt_cls,
                       const int32_t* gt_count, const int64_t* slots) {
     try {
         cudaStream_t st = d->ctx->stream;
+        // stream-ordered behind the previous step; `images` must stay valid
+        // until this batch's step has consumed it (as for any async copy)
         if (images)
             CK(cudaMemcpyAsync(d->img.p, images, d->img.numel() * d->es,
                                on_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st));
         stage_gt(d, gt_boxes, gt_cls, gt_count, slots);
-        // the pinned staging buffers are reused next call: wait for the copies
-        CK(cudaStreamSynchronize(st));
     } catch (const std::exception& e) {
         return det_fail(SDB_CUDA, e.what());
     }
@@ -1540,9 +1642,10 @@ int sdb_det_synth_images(sdb_det* d, const int64_t* slots) {
         // stream-ordered after the previous step (never touch the step workspace:
         // the previous step may still be running on the context stream)
         cudaStream_t st = d->ctx->stream;
-        CK(cudaStreamSynchronize(st));
-        std::memcpy(d->h_slots, slots, d->cfg.batch * 8);
-        CK(cudaMemcpyAsync(d->slots_dev, d->h_slots, d->cfg.batch * 8, cudaMemcpyHostToDevice, st));
+        const int k = stage_slot(d);
+        std::memcpy(d->h_slots[k], slots, d->cfg.batch * 8);
+        CK(cudaMemcpyAsync(d->slots_dev, d->h_slots[k], d->cfg.batch * 8, cudaMemcpyHostToDevice, st));
+        stage_done(d, k);
         CK(synth_images(d->dt, d->img.p, d->cfg.batch, d->cfg.img_h, d->cfg.img_w, 8, d->cfg.seed, d->slots_dev, 0, st));
     } catch (const std::exception& e) {
         return det_fail(SDB_CUDA, e.what());
@@ -1578,6 +1681,8 @@ int sdb_det_step(sdb_det* d) {
             CK(cudaGraphLaunch(d->gexec, st));
         }
         ++d->steps_done;
+    } catch (const CollectiveFailure& e) {
+        return det_fail(SDB_COLLECTIVE, e.what());
     } catch (const std::exception& e) {
         return det_fail(SDB_CUDA, e.what());
     }

@@ -167,9 +167,19 @@ def batch_slots(step: int, rank: int, world: int, b: int):
 
 
 class Detector:
-    def __init__(self, p: Preset, device: int = 0, rank: int = 0, world: int = 1, nccl_id: bytes | None = None):
+    def __init__(self, p: Preset, device: int = 0, rank: int = 0, world: int = 1, nccl_id: bytes | None = None,
+                 force_comm: bool = False):
+        """force_comm (world 1 only): build a 1-rank NCCL communicator so the
+        data-parallel code path -- bucket allreduces inside the captured step,
+        the loss and BN-gradient allreduces -- runs on one GPU."""
         self.p = p
         lb = L()
+        if force_comm and nccl_id is None:
+            if world != 1:
+                raise ValueError("force_comm is for world == 1; pass the shared nccl_id at world > 1")
+            buf = C.create_string_buffer(128)
+            check(lb.sdb_get_nccl_unique_id(buf))
+            nccl_id = bytes(buf.raw)
         self.ctx = _P()
         idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
         check(lb.sdb_ctx_create(device, rank, world, idbuf, C.byref(self.ctx)))

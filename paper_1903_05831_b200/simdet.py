@@ -13,6 +13,10 @@ Reference entry points mirrored (file:line under /root/reference/proj):
   iabn_forward / _backward    src/memopt.cpp:226-327
   apply_sgd / has_nonfinite   src/trainer.cpp:78-94
   update_scale                src/precision.cpp:45-56
+  allreduce_sum               src/comm.cpp:288-315      (CommGroup, NCCL)
+and the detection operators the reference lacks (restated semantics,
+oracle/restate.cpp): anchors, proposal layer, anchor / proposal targets,
+RoIAlign, softmax-CE, sigmoid BCE, smooth-L1.
 """
 from __future__ import annotations
 
@@ -49,6 +53,13 @@ _SIGS = {
     "sdb_roialign_bwd": [_P, _I, _P, _I, _I, _I, _I, _P, _I, _I, _F, _I, _P, _P],
     "sdb_softmax_ce": [_P, _I, _P, _I, _I, _I, _P, _P, _P, _P, _P],
     "sdb_debug_set": [_I, _I],
+    "sdb_rpn_bce": [_P, _I, _P, _L, _I, _I, _P, _P, _P, _P, _P],
+    "sdb_rpn_smoothl1": [_P, _I, _P, _L, _I, _I, _P, _P, _D, _D, _P, _P, _P, _P],
+    "sdb_smoothl1": [_P, _I, _P, _I, _I, _P, _P, _D, _P, _P, _P, _P],
+    "sdb_anchor_targets": [_P, _P, _I, _I, _P, _I, _P, _F, _F, _P, _D, _D, _I, _D, _P, _P, _P],
+    "sdb_proposal_targets": [_P, _P, _I, _P, _P, _P, _I, _P, _I, _P, _D, _D, _D, _I, _D, _P, _P, _P, _P, _P],
+    "sdb_allreduce_sum": [_P, _I, _P, _L, _P],
+    "sdb_comm_check": [_P],
 }
 
 _configured = False
@@ -339,3 +350,73 @@ def update_scale(scale_dev, good_dev, flag_dev, dynamic: bool, growth_interval=2
     """update_scale (src/precision.cpp:45-56) on device-resident state."""
     check(L().sdb_update_scale(ctx(), ptr(scale_dev), ptr(good_dev), ptr(flag_dev), 1 if dynamic else 0,
                                growth_interval, growth, backoff, min_scale, max_scale, stream()))
+
+
+def rpn_bce(logits, labels, A, grad_scale=None):
+    """RPN objectness loss: sigmoid BCE averaged over anchors labelled 0/1.
+    logits [n_loc, A_pad] (NHWC-flat), labels int8 [n_loc*A]; returns (loss, dlogits)"""
+    n_loc, A_pad = logits.shape
+    loss = torch.zeros(1, device=logits.device, dtype=torch.float64)
+    dx = torch.zeros_like(logits)
+    check(L().sdb_rpn_bce(ctx(), dt(logits), ptr(logits), n_loc, A, A_pad, ptr(labels), ptr(grad_scale), ptr(loss),
+                          ptr(dx), stream()))
+    return loss, dx
+
+
+def rpn_smoothl1(deltas, labels, targets, A, beta, norm, grad_scale=None):
+    """RPN box loss: smooth-L1 over anchors labelled 1, / norm.
+    deltas [n_loc, 4*A_pad], targets fp32 [n_loc*A, 4]; returns (loss, ddeltas)"""
+    n_loc, A4 = deltas.shape
+    loss = torch.zeros(1, device=deltas.device, dtype=torch.float64)
+    dd = torch.zeros_like(deltas)
+    check(L().sdb_rpn_smoothl1(ctx(), dt(deltas), ptr(deltas), n_loc, A, A4 // 4, ptr(labels), ptr(targets), beta,
+                               norm, ptr(grad_scale), ptr(loss), ptr(dd), stream()))
+    return loss, dd
+
+
+def smoothl1(pred, labels, targets, beta, grad_scale=None):
+    """RCNN class-specific box loss: pred [R, ld] (slot 4*label), targets [R, 4];
+    summed over foreground RoIs, / #RoIs with label >= 0; returns (loss, dpred)"""
+    R, ld = pred.shape
+    loss = torch.zeros(1, device=pred.device, dtype=torch.float64)
+    dp = torch.zeros_like(pred)
+    check(L().sdb_smoothl1(ctx(), dt(pred), ptr(pred), R, ld, ptr(labels), ptr(targets), beta, ptr(grad_scale),
+                           ptr(loss), ptr(dp), stream()))
+    return loss, dp
+
+
+def anchor_targets(anchors, gt, gt_count, keys, img_h, img_w, fg_thr=0.7, bg_thr=0.3, batch=256, fg_frac=0.5):
+    """RPN anchor targets: anchors [nA,4], gt [n_img, G, 4], gt_count int32 [n_img],
+    keys uint64 [n_img] (as int64 tensor); returns (labels int8 [n_img, nA], targets [n_img, nA, 4])"""
+    nA = anchors.shape[0]
+    n_img, G, _ = gt.shape
+    labels = torch.empty((n_img, nA), device=anchors.device, dtype=torch.int8)
+    targets = torch.empty((n_img, nA, 4), device=anchors.device, dtype=torch.float32)
+    check(L().sdb_anchor_targets(ctx(), ptr(anchors), nA, n_img, ptr(gt), G, ptr(gt_count), img_h, img_w, ptr(keys),
+                                 fg_thr, bg_thr, batch, fg_frac, ptr(labels), ptr(targets), stream()))
+    return labels, targets
+
+
+def proposal_targets(proposals, prop_count, gt, gt_cls, gt_count, keys, batch=512, fg_frac=0.25, fg_thr=0.5,
+                     bg_hi=0.5, bg_lo=0.0):
+    """RCNN proposal targets: proposals [n_img, P, 4], counts int32 [n_img];
+    returns (rois [n_img*batch, 5], labels int32, targets [.., 4], count int32 [n_img])"""
+    n_img, Pst, _ = proposals.shape
+    G = gt.shape[1]
+    dev = proposals.device
+    rois = torch.empty((n_img * batch, 5), device=dev, dtype=torch.float32)
+    labels = torch.empty(n_img * batch, device=dev, dtype=torch.int32)
+    targets = torch.empty((n_img * batch, 4), device=dev, dtype=torch.float32)
+    count = torch.empty(n_img, device=dev, dtype=torch.int32)
+    check(L().sdb_proposal_targets(ctx(), ptr(proposals), Pst, ptr(prop_count), ptr(gt), ptr(gt_cls), G,
+                                   ptr(gt_count), n_img, ptr(keys), fg_thr, bg_hi, bg_lo, batch, fg_frac, ptr(rois),
+                                   ptr(labels), ptr(targets), ptr(count), stream()))
+    return rois, labels, targets, count
+
+
+def allreduce_sum(buf, context=None):
+    """CommGroup::allreduce_sum (src/comm.cpp:288-315): in-place SUM over the
+    context's ranks (NCCL); identity on a context without a communicator"""
+    code = {torch.float32: F32, torch.float16: F16, torch.float64: 2}[buf.dtype]
+    check(L().sdb_allreduce_sum(context if context is not None else ctx(), code, ptr(buf), buf.numel(), stream()))
+    return buf
