@@ -16,8 +16,9 @@ Bars (BASELINE.json north star):
     on the same weights, inputs and targets, with the global (all-parameter)
     step delta held to the same rule.  DESIGN.md ("fp16 noise floor") has the
     numbers.
-Sizes are reduced where the single-threaded CPU oracle would take minutes
-(C2 runs 10 steps at 128x128; C1 one step at its full 256x256)."""
+C1 runs one step and C2 ten steps at the stated 256x256 (C2 also at 128x128,
+where the oracle's determinism is re-checked); the R50-C4 headline config is
+in tests/test_gpu_c4_parity.py."""
 import ctypes as C
 
 import numpy as np
@@ -107,7 +108,8 @@ def _ref16_vs_ref32(det, cfg16, w, s, scale):
     return g16, g32
 
 
-def test_c2_fp16_ten_steps(ref, orc):
+@pytest.mark.parametrize("size", [128, 256])
+def test_c2_fp16_ten_steps(ref, orc, size):
     """Per tensor, the GPU's fp16 gradient error against ref16 is held to the
     reference's own fp16 noise level for that tensor, measured as err(ref16,
     ref32) on the same inputs.  That noise level is itself a noisy estimate
@@ -119,7 +121,7 @@ def test_c2_fp16_ten_steps(ref, orc):
     the global parameter delta are still checked against the same step's
     floor."""
     from paper_1903_05831_b200 import detector as D
-    det = D.Detector(D.preset("c2", img_h=128, img_w=128))
+    det = D.Detector(D.preset("c2", img_h=size, img_w=size))  # 256: BASELINE config C2 as stated
     cfg = dp.ref_cfg(det)
     dp.check_param_order(det, cfg)
     errs, floors = [], []
@@ -132,8 +134,13 @@ def test_c2_fp16_ten_steps(ref, orc):
         lr, g16, lg_ref, dl_ref = dp.oracle_step(det, cfg, w_ref, s, scale)
         _losses_close(lg, lr, 1e-2)
         assert norm_rel(s["logits"][..., :det.A].astype(np.float32).transpose(0, 3, 1, 2), lg_ref) <= 1e-2
-        g16b, g32 = _ref16_vs_ref32(det, cfg, w_ref, s, scale)
-        assert np.array_equal(g16, g16b)  # the oracle is deterministic
+        if size == 128:
+            g16b, g32 = _ref16_vs_ref32(det, cfg, w_ref, s, scale)
+            assert np.array_equal(g16, g16b)  # the oracle is deterministic
+        else:
+            cfg32 = dp.ref_cfg(det)
+            cfg32.mode = 2
+            _, g32, _, _ = dp.oracle_step(det, cfg32, w_ref, s, scale)
         g = dp.flat_grads(det)
         errs.append([norm_rel(a, b) for a, b in zip(dp.split(det, g), dp.split(det, g16))])
         floors.append([norm_rel(b, c) for b, c in zip(dp.split(det, g16), dp.split(det, g32))])
