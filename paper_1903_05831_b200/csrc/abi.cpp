@@ -359,8 +359,12 @@ int sdb_roialign_bwd(sdb_ctx* ctx, int dtype, const void* dy, int N, int H, int 
     if (int rc = check_dtype(dtype)) return rc;
     if (C % 8 || P < 1 || P > 16 || sampling_ratio < 1 || R < 0)
         return fail(SDB_UNSUPPORTED, "roialign: C % 8, P <= 16, ratio");
-    return cuda_status(sdb::roialign_bwd(dtype, dy, N, H, W, C, rois, R, P, spatial_scale, sampling_ratio, dfeat,
-                                         pick(ctx, stream)),
+    if (!ctx) return fail(SDB_PARAM, "roialign_bwd needs a context (workspace)");
+    const size_t wsb = sdb::roialign_bwd_workspace(R, H, W, P);
+    void* ws = ctx->scratch(wsb);
+    if (!ws) return fail(SDB_CUDA, "workspace allocation failed");
+    return cuda_status(sdb::roialign_bwd(dtype, dy, N, H, W, C, rois, R, P, spatial_scale, sampling_ratio, dfeat, ws,
+                                         wsb, pick(ctx, stream)),
                        "roialign_bwd");
 }
 

@@ -93,8 +93,10 @@ cudaError_t proposal_targets(const ProposalTargetArgs& a, cudaStream_t st);
 // convolution reads, so the stride folds into the pooling.
 cudaError_t roialign_fwd(int dtype, const void* feat, int N, int H, int W, int C, const float* rois, int R, int P,
                          float scale, int sr, void* out, cudaStream_t st, int step = 1);
+// backward workspace: per-RoI separable weight tables + boxes (roialign_bwd_workspace bytes)
+size_t roialign_bwd_workspace(int R, int H, int W, int P, int step = 1);
 cudaError_t roialign_bwd(int dtype, const void* dy, int N, int H, int W, int C, const float* rois, int R, int P,
-                         float scale, int sr, void* dfeat, cudaStream_t st, int step = 1);
+                         float scale, int sr, void* dfeat, void* ws, size_t ws_bytes, cudaStream_t st, int step = 1);
 // [n][3][H][W] (the reference image layout) -> NHWC with Cp channels (zero padded)
 cudaError_t nchw3_to_nhwc(int dtype, const void* in, int n, int H, int W, int Cp, void* out, cudaStream_t st);
 // the 7x7 stem as a 1x1 GEMM over its im2col matrix X' [pixels][192] (fp16):

@@ -476,6 +476,7 @@ size_t max_ws(sdb_det* d) {
     conv_ws(d->rpn_conv); conv_ws(d->rpn_cls); conv_ws(d->rpn_bbox); conv_ws(d->fc_cls); conv_ws(d->fc_bbox);
     m = std::max(m, proposal_workspace_bytes(d->cfg.batch, d->nA, d->cfg.pre_nms));
     m = std::max(m, anchor_target_workspace_bytes(d->cfg.batch, d->nA, d->cfg.max_gt));
+    m = std::max(m, roialign_bwd_workspace(d->R, d->fh, d->fw, d->P, d->roi_step));
     return m;
 }
 
@@ -934,7 +935,7 @@ void run_step(sdb_det* d) {
     void* dc4 = d->gbuf[(cur == d->gbuf[2]) ? 3 : 2];
     { PScope ps(d, P_ROI_B, 0, static_cast<double>(d->es) * (d->roi_feat.numel() + d->c4.numel()));
     CK(roialign_bwd(d->dt, cur, d->c4.n, d->c4.h, d->c4.w, d->c4.c, d->rois, d->R, d->P, sscale, cf.sampling_ratio,
-                    dc4, st, d->roi_step)); }
+                    dc4, d->ws, d->ws_bytes, st, d->roi_step)); }
     // RPN head backward (bbox, cls, conv)
     if (side) {
         // done on the side stream behind the proposal layer: only the rpn_conv

@@ -129,164 +129,200 @@ __global__ void roialign_fwd_kernel(const T* __restrict__ feat, int H, int W, in
     }
 }
 
-// ---------------------------------------------------------------- RoIAlign bwd (gather)
-constexpr int kTile = 8;        // 8x8 pixel tile
-constexpr int kSlab = 256;      // channels per CTA
-constexpr int kBwdThreads = 256;
-constexpr int kMaxP = 16;
-constexpr int kRB = 8;          // RoIs per barrier
-
+// ---------------------------------------------------------------- RoIAlign fwd (smem-staged)
+// One CTA per (image, 8-channel slab): the slab of the image's whole feature
+// map (H*W pixels x 16 B fp16 / 32 B fp32) is staged in shared memory once, so
+// the 16 bilinear corner reads of every output bin hit smem instead of L2 (the
+// RoIs of an image overlap heavily: at C4 every feature pixel is read by ~100
+// RoI samples; through L2 that read amplification capped the direct kernel at
+// ~1.6 GB of L2 traffic per step).  Threads take the image's (RoI, bin) items
+// with consecutive lanes on consecutive bins of one RoI (neighbouring pixels:
+// few smem bank conflicts).  Same per-output arithmetic as roialign_fwd_kernel.
 template <class T>
-__global__ void __launch_bounds__(kBwdThreads) roialign_bwd_kernel(const T* __restrict__ dy, int H, int W, int C,
-                                                                   const float* __restrict__ rois, int R, int P,
-                                                                   float scale, int sr, int step,
-                                                                   T* __restrict__ dfeat) {
-    // dY holds every `step`-th bin of the P x P grid (Po x Po of them)
-    const int Po = (P + step - 1) / step;
-    // RoIs are processed in batches of kRB: one barrier per batch.  Weights are
-    // double-buffered and the nonzero-bin ranges triple-buffered so a batch's
-    // setup never races with slower threads still accumulating the previous one.
-    __shared__ float WY[2][kRB][kMaxP][kTile];
-    __shared__ float WX[2][kRB][kMaxP][kTile];
-    __shared__ int rng[3][kRB][4][kTile];  // [row lo, row hi, col lo, col hi] of nonzero bins
-    __shared__ int list[1024];
-    __shared__ int sh[40];
-    for (int t = threadIdx.x; t < 3 * kRB * 4 * kTile; t += kBwdThreads) {
-        const int k4 = (t / kTile) & 3;
-        (&rng[0][0][0][0])[t] = (k4 & 1) ? -1 : Po;
+__global__ void __launch_bounds__(256) roialign_fwd_smem_kernel(const T* __restrict__ feat, int H, int W, int C,
+                                                                const float* __restrict__ rois, int R, int P,
+                                                                float scale, int sr, int step, T* __restrict__ out) {
+    extern __shared__ __align__(16) unsigned char ra_smem[];
+    constexpr int kChunk = 8 * sizeof(T);  // bytes of one pixel's 8 channels
+    const int n = blockIdx.y, c8 = blockIdx.x;
+    const int HW = H * W;
+    int* list = reinterpret_cast<int*>(ra_smem + static_cast<size_t>(HW) * kChunk);
+    __shared__ int cnt;
+    if (threadIdx.x == 0) cnt = 0;
+    const T* src = feat + static_cast<int64_t>(n) * HW * C + c8 * 8;
+    for (int p = threadIdx.x; p < HW; p += blockDim.x) {
+        const uint4* s = reinterpret_cast<const uint4*>(src + static_cast<int64_t>(p) * C);
+        uint4* d = reinterpret_cast<uint4*>(ra_smem + static_cast<size_t>(p) * kChunk);
+        d[0] = __ldg(s);
+        if (kChunk == 32) d[1] = __ldg(s + 1);
     }
-    int batch = 0;
+    __syncthreads();
+    // this image's RoIs (order irrelevant: every output bin is written by one thread)
+    for (int r = threadIdx.x; r < R; r += blockDim.x)
+        if (static_cast<int>(rois[static_cast<int64_t>(r) * 5]) == n) list[atomicAdd(&cnt, 1)] = r;
+    __syncthreads();
+    const int Po = (P + step - 1) / step, PP = Po * Po;
+    const int items = cnt * PP;
+    const float count = static_cast<float>(max(sr * sr, 1));
+    const T* f = reinterpret_cast<const T*>(ra_smem);
+    for (int e = threadIdx.x; e < items; e += blockDim.x) {
+        const int r = list[e / PP], bin = e % PP;
+        const int ph = (bin / Po) * step, pw = (bin % Po) * step;
+        const Geom g = roi_geom(rois + static_cast<int64_t>(r) * 5, P, scale);
+        float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int iy = 0; iy < sr; ++iy) {
+            float y = sample_coord(g.sh, ph, g.bh, iy, sr);
+            for (int ix = 0; ix < sr; ++ix) {
+                float x = sample_coord(g.sw, pw, g.bw, ix, sr);
+                if (y < -1.0f || y > static_cast<float>(H) || x < -1.0f || x > static_cast<float>(W)) continue;
+                float yy = y <= 0.f ? 0.f : y, xx = x <= 0.f ? 0.f : x;
+                int yl = static_cast<int>(yy), xl = static_cast<int>(xx), yh, xh;
+                if (yl >= H - 1) { yh = yl = H - 1; yy = static_cast<float>(yl); } else yh = yl + 1;
+                if (xl >= W - 1) { xh = xl = W - 1; xx = static_cast<float>(xl); } else xh = xl + 1;
+                const float ly = yy - static_cast<float>(yl), lx = xx - static_cast<float>(xl);
+                const float hy = 1.f - ly, hx = 1.f - lx;
+                const float w1 = hy * hx, w2 = hy * lx, w3 = ly * hx, w4 = ly * lx;
+                float v1[8], v2[8], v3[8], v4[8];
+                ld8<T>(f + (yl * W + xl) * 8, v1);
+                ld8<T>(f + (yl * W + xh) * 8, v2);
+                ld8<T>(f + (yh * W + xl) * 8, v3);
+                ld8<T>(f + (yh * W + xh) * 8, v4);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[j] += w1 * v1[j] + w2 * v2[j] + w3 * v3[j] + w4 * v4[j];
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = acc[j] / count;
+        st8<T>(out + (static_cast<int64_t>(r) * PP + bin) * C + c8 * 8, acc);
+    }
+}
+
+// ---------------------------------------------------------------- RoIAlign bwd
+// dX[n, y, x, c] = sum over RoIs r of image n (index order), bins (ph, pw)
+// (row-major) of WY_r[y][ph] * WX_r[x][pw] / sr^2 * dY[r, ph, pw, c], with
+// WY_r[y][ph] = the bilinear weights of pixel row y summed over the samples of
+// bin row ph (separable).  A deterministic GATHER, no atomics:
+//   1. roialign_bwd_weights_kernel: one warp per RoI tabulates WY_r / WX_r for
+//      every pixel row / column and the bounding box of the nonzero ones
+//      (shared by all pixels and channel slabs: computed once per step);
+//   2. roialign_bwd_gather_kernel: one warp per (pixel, 256*V-channel slab),
+//      lane = V 8-channel chunks; it walks the RoIs whose box holds its pixel
+//      (ballot over the box table, index order), fetches the RoI's 2 x pw
+//      weights of its row and column in one load per lane, and accumulates
+//      the nonzero bin pairs in registers.  No shared memory and no barriers;
+//      a CTA is a 4x4 pixel block, so the dY rows its pixels share hit L1.
+// The summation order per output element is the same as a per-pixel loop
+// over (RoI, ph, pw) -- bitwise reproducible run to run.
+constexpr int kRaBlk = 4;  // CTA = kRaBlk x kRaBlk pixels (one warp each)
+
+SDB_DEV float bin_axis_weight(float start, float bin, int pb_full, int sr, int pix, int lim) {
+    float wsum = 0.f;
+    for (int is = 0; is < sr; ++is) {
+        float v = sample_coord(start, pb_full, bin, is, sr);
+        if (v < -1.0f || v > static_cast<float>(lim)) continue;
+        if (v <= 0.f) v = 0.f;
+        int lo_i = static_cast<int>(v), hi_i;
+        if (lo_i >= lim - 1) { hi_i = lo_i = lim - 1; v = static_cast<float>(lo_i); } else hi_i = lo_i + 1;
+        const float l = v - static_cast<float>(lo_i), h = 1.f - l;
+        if (lo_i == pix) wsum += h;
+        if (hi_i == pix) wsum += l;
+    }
+    return wsum;
+}
+
+__global__ void __launch_bounds__(256) roialign_bwd_weights_kernel(const float* __restrict__ rois, int R, int H, int W,
+                                                                   int P, float scale, int sr, int step, int pw,
+                                                                   float* __restrict__ tab, int4* __restrict__ box) {
+    const int r = static_cast<int>((blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
+    if (r >= R) return;
+    const Geom g = roi_geom(rois + static_cast<int64_t>(r) * 5, P, scale);
+    const int Po = (P + step - 1) / step;
+    float* ty = tab + static_cast<int64_t>(r) * (H + W) * pw;
+    int ylo = 0x7fff, yhi = -1, xlo = 0x7fff, xhi = -1;
+    for (int t = lane; t < H + W; t += 32) {
+        const bool isx = t >= H;
+        const int pix = isx ? t - H : t;
+        bool any = false;
+        for (int pb = 0; pb < pw; ++pb) {
+            const float w = pb < Po ? (isx ? bin_axis_weight(g.sw, g.bw, pb * step, sr, pix, W)
+                                           : bin_axis_weight(g.sh, g.bh, pb * step, sr, pix, H))
+                                    : 0.f;
+            ty[static_cast<int64_t>(t) * pw + pb] = w;
+            any |= w != 0.f;
+        }
+        if (any) {
+            if (isx) { xlo = min(xlo, pix); xhi = max(xhi, pix); }
+            else { ylo = min(ylo, pix); yhi = max(yhi, pix); }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        ylo = min(ylo, __shfl_xor_sync(0xffffffffu, ylo, o));
+        yhi = max(yhi, __shfl_xor_sync(0xffffffffu, yhi, o));
+        xlo = min(xlo, __shfl_xor_sync(0xffffffffu, xlo, o));
+        xhi = max(xhi, __shfl_xor_sync(0xffffffffu, xhi, o));
+    }
+    if (lane == 0) {
+        const bool empty = yhi < 0 || xhi < 0 || g.b < 0;
+        box[r] = make_int4(empty ? -1 : g.b, ylo | (max(yhi, 0) << 16), xlo | (max(xhi, 0) << 16), 0);
+    }
+}
+
+template <class T, int V>
+__global__ void __launch_bounds__(kRaBlk * kRaBlk * 32) roialign_bwd_gather_kernel(
+    const T* __restrict__ dy, int H, int W, int C, const int4* __restrict__ box, const float* __restrict__ tab, int R,
+    int Po, int pw, float inv_count, T* __restrict__ dfeat) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int bxn = (W + kRaBlk - 1) / kRaBlk;
+    const int y = (blockIdx.x / bxn) * kRaBlk + warp / kRaBlk;
+    const int x = (blockIdx.x % bxn) * kRaBlk + warp % kRaBlk;
     const int n = blockIdx.z;
-    const int tiles_x = (W + kTile - 1) / kTile;
-    const int ty = blockIdx.x / tiles_x, tx = blockIdx.x % tiles_x;
-    const int y0 = ty * kTile, x0 = tx * kTile;
-    const int c_base = blockIdx.y * kSlab;
-    const int chunk = threadIdx.x & 31;         // 8-channel chunk within the slab
-    // warp w owns pixels (row i, column (w + i) & 7), i = 0..7: every warp has one
-    // pixel in each row and each column of the tile, so a rectangular RoI gives
-    // every warp (nearly) the same amount of work between barriers
-    const int pix0 = threadIdx.x >> 5;
-    const int c = c_base + chunk * 8;
-    const bool c_ok = c < C;
-    const float inv_count = 1.0f / static_cast<float>(max(sr * sr, 1));
-    float acc[8][8];
+    const int c0 = blockIdx.y * 256 * V + lane * 8;
+    if (y >= H || x >= W) return;  // whole warp: no barriers below
+    float acc[V][8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+    for (int v = 0; v < V; ++v)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
-
-    for (int base = 0; base < R; base += 1024) {
-        // compact (in index order) the RoIs of image n that reach this tile
-        int cnt_local = 0;
-        int mine[4];
-        for (int q = 0; q < 4; ++q) {
-            const int r = base + threadIdx.x * 4 + q;
-            mine[q] = 0;
-            if (r >= R) continue;
-            const float* rr = rois + static_cast<int64_t>(r) * 5;
-            if (static_cast<int>(rr[0]) != n) continue;
-            const Geom g = roi_geom(rr, P, scale);
-            const float ylo = g.sh - 1.0f, yhi = g.sh + g.bh * P + 1.0f;
-            const float xlo = g.sw - 1.0f, xhi = g.sw + g.bw * P + 1.0f;
-            if (yhi < static_cast<float>(y0) || ylo > static_cast<float>(y0 + kTile) || xhi < static_cast<float>(x0) ||
-                xlo > static_cast<float>(x0 + kTile))
-                continue;
-            mine[q] = 1;
-            ++cnt_local;
+        for (int k = 0; k < 8; ++k) acc[v][k] = 0.f;
+    const int64_t row_stride = static_cast<int64_t>(Po) * C;
+    for (int r0 = 0; r0 < R; r0 += 32) {
+        bool hit = false;
+        if (r0 + lane < R) {
+            const int4 b = __ldg(box + r0 + lane);
+            hit = b.x == n && y >= (b.y & 0xffff) && y <= (b.y >> 16) && x >= (b.z & 0xffff) && x <= (b.z >> 16);
         }
-        // exclusive scan of cnt_local
-        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-        int xs = cnt_local;
-        for (int o = 1; o < 32; o <<= 1) {
-            const int yv = __shfl_up_sync(0xffffffffu, xs, o);
-            if (lane >= o) xs += yv;
-        }
-        if (lane == 31) sh[wid] = xs;
-        __syncthreads();
-        int wbase = 0, total = 0;
-        for (int w2 = 0; w2 < kBwdThreads / 32; ++w2) {
-            if (w2 < wid) wbase += sh[w2];
-            total += sh[w2];
-        }
-        int pos = wbase + xs - cnt_local;
-        for (int q = 0; q < 4; ++q)
-            if (mine[q]) list[pos++] = base + threadIdx.x * 4 + q;
-        __syncthreads();
-
-        for (int l0 = 0; l0 < total; l0 += kRB, ++batch) {
-            const int nb = min(kRB, total - l0);
-            const int wb = batch & 1, rb = batch % 3, rnext = (batch + 1) % 3;
-            // reset the range buffer of the next batch (last read three batches ago)
-            for (int t = threadIdx.x; t < kRB * 4 * kTile; t += kBwdThreads) {
-                const int k4 = (t / kTile) & 3;
-                (&rng[rnext][0][0][0])[t] = (k4 & 1) ? -1 : Po;
-            }
-            // separable weights of the batch's RoIs for this tile
-            const int per = 2 * Po * kTile;
-            for (int t = threadIdx.x; t < nb * per; t += kBwdThreads) {
-                const int j = t / per, tt0 = t - j * per;
-                const Geom g = roi_geom(rois + static_cast<int64_t>(list[l0 + j]) * 5, P, scale);
-                const bool isx = tt0 >= Po * kTile;
-                const int tt = isx ? tt0 - Po * kTile : tt0;
-                const int pb = tt / kTile, lo = tt % kTile;
-                const int pix = (isx ? x0 : y0) + lo;
-                const int lim = isx ? W : H;
-                float wsum = 0.f;
-                for (int is = 0; is < sr; ++is) {
-                    float v = isx ? sample_coord(g.sw, pb * step, g.bw, is, sr)
-                                  : sample_coord(g.sh, pb * step, g.bh, is, sr);
-                    if (v < -1.0f || v > static_cast<float>(lim)) continue;
-                    if (v <= 0.f) v = 0.f;
-                    int lo_i = static_cast<int>(v), hi_i;
-                    if (lo_i >= lim - 1) { hi_i = lo_i = lim - 1; v = static_cast<float>(lo_i); } else hi_i = lo_i + 1;
-                    const float l = v - static_cast<float>(lo_i), h = 1.f - l;
-                    if (lo_i == pix) wsum += h;
-                    if (hi_i == pix) wsum += l;
-                }
-                if (isx) WX[wb][j][pb][lo] = wsum;
-                else WY[wb][j][pb][lo] = wsum;
-                if (wsum != 0.f) {
-                    atomicMin(&rng[rb][j][isx ? 2 : 0][lo], pb);
-                    atomicMax(&rng[rb][j][isx ? 3 : 1][lo], pb);
-                }
-            }
-            __syncthreads();
-            if (c_ok) {
-                for (int j = 0; j < nb; ++j) {
-                    const T* d = dy + static_cast<int64_t>(list[l0 + j]) * Po * Po * C + c;
+        for (unsigned m = __ballot_sync(0xffffffffu, hit); m; m &= m - 1) {
+            const int r = r0 + __ffs(m) - 1;
+            const float* trow = tab + static_cast<int64_t>(r) * (H + W) * pw;
+            float w = 0.f;
+            if (lane < pw) w = __ldg(trow + y * pw + lane);
+            else if (lane >= 16 && lane < 16 + pw) w = __ldg(trow + (H + x) * pw + (lane - 16));
+            const unsigned nz = __ballot_sync(0xffffffffu, w != 0.f);
+            const T* d = dy + static_cast<int64_t>(r) * Po * row_stride + c0;
+            for (unsigned a = nz & 0xffffu; a; a &= a - 1) {
+                const int ph = __ffs(a) - 1;
+                const float wy = __shfl_sync(0xffffffffu, w, ph);
+                for (unsigned b2 = nz >> 16; b2; b2 &= b2 - 1) {
+                    const int pwi = __ffs(b2) - 1;
+                    const float wx = __shfl_sync(0xffffffffu, w, 16 + pwi);
+                    const float wgt = wy * wx * inv_count;
+                    const T* dd = d + ph * row_stride + static_cast<int64_t>(pwi) * C;
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        const int p = i * 8 + ((pix0 + i) & 7);
-                        const int ly = p >> 3, lx = p & 7;
-                        if (y0 + ly >= H || x0 + lx >= W) continue;
-                        const int phe = rng[rb][j][1][ly], pwb = rng[rb][j][2][lx], pwe = rng[rb][j][3][lx];
-                        for (int ph = rng[rb][j][0][ly]; ph <= phe; ++ph) {
-                            const float wy = WY[wb][j][ph][ly];
-                            if (wy == 0.f) continue;
-                            for (int pw = pwb; pw <= pwe; ++pw) {
-                                const float wx = WX[wb][j][pw][lx];
-                                if (wx == 0.f) continue;
-                                const float wgt = wy * wx * inv_count;
-                                float v[8];
-                                ld8<T>(d + (static_cast<int64_t>(ph) * Po + pw) * C, v);
+                    for (int v = 0; v < V; ++v) {
+                        if (c0 + v * 256 >= C) break;
+                        float val[8];
+                        ld8<T>(dd + v * 256, val);
 #pragma unroll
-                                for (int jj = 0; jj < 8; ++jj) acc[i][jj] += wgt * v[jj];
-                            }
-                        }
+                        for (int k = 0; k < 8; ++k) acc[v][k] += wgt * val[k];
                     }
                 }
             }
         }
-        __syncthreads();  // `list` is rewritten by the next compaction round
     }
-    if (!c_ok) return;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const int p = i * 8 + ((pix0 + i) & 7);
-        const int yy = y0 + (p >> 3), xx = x0 + (p & 7);
-        if (yy >= H || xx >= W) continue;
-        st8<T>(dfeat + ((static_cast<int64_t>(n) * H + yy) * W + xx) * C + c, acc[i]);
-    }
+    for (int v = 0; v < V; ++v)
+        if (c0 + v * 256 < C) st8<T>(dfeat + ((static_cast<int64_t>(n) * H + y) * W + x) * C + c0 + v * 256, acc[v]);
 }
 
 // ---------------------------------------------------------------- pooling
@@ -841,11 +877,32 @@ int grid_for(int64_t n) {
 template <class T>
 static inline const T* cp(const void* p) { return static_cast<const T*>(p); }
 
+// shared memory of the staged forward: the image's feature slab + its RoI list
+static size_t ra_fwd_smem(int H, int W, int R, int dtype) {
+    return static_cast<size_t>(H) * W * 8 * (dtype == kF16 ? 2 : 4) + static_cast<size_t>(R) * 4;
+}
+
 cudaError_t roialign_fwd(int dtype, const void* feat, int N, int H, int W, int C, const float* rois, int R, int P,
                          float scale, int sr, void* out, cudaStream_t st, int step) {
-    (void)N;
     if (step < 1) return cudaErrorInvalidValue;
+    if (R == 0) return cudaSuccess;
     const int Po = (P + step - 1) / step;
+    const size_t smem = ra_fwd_smem(H, W, R, dtype);
+    if (smem <= 200 * 1024) {
+        const dim3 grid(C / 8, N);
+        if (dtype == kF16) {
+            auto k = roialign_fwd_smem_kernel<__half>;
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            k<<<grid, 256, smem, st>>>(cp<__half>(feat), H, W, C, rois, R, P, scale, sr, step,
+                                      static_cast<__half*>(out));
+        } else {
+            auto k = roialign_fwd_smem_kernel<float>;
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            k<<<grid, 256, smem, st>>>(cp<float>(feat), H, W, C, rois, R, P, scale, sr, step, static_cast<float*>(out));
+        }
+        return cudaGetLastError();
+    }
+    // feature maps too large to stage: one thread per (RoI, bin, 8 channels) through L2
     const int64_t total = static_cast<int64_t>(R) * Po * Po * (C / 8);
     if (dtype == kF16)
         roialign_fwd_kernel<__half><<<grid_for(total), 256, 0, st>>>(cp<__half>(feat), H, W, C, rois, R, P, scale, sr,
@@ -856,16 +913,42 @@ cudaError_t roialign_fwd(int dtype, const void* feat, int N, int H, int W, int C
     return cudaGetLastError();
 }
 
+static int ra_table_width(int P, int step) { return (P + step - 1) / step <= 8 ? 8 : 16; }
+
+size_t roialign_bwd_workspace(int R, int H, int W, int P, int step) {
+    if (step < 1) return 0;
+    return (static_cast<size_t>(R) * (H + W) * ra_table_width(P, step) * 4 + 255) / 256 * 256 +
+           static_cast<size_t>(R) * 16 + 256;
+}
+
+template <class T, int V>
+static void ra_gather(dim3 grid, const void* dy, int H, int W, int C, const int4* box, const float* tab, int R, int Po,
+                      int pw, float inv, void* dfeat, cudaStream_t st) {
+    roialign_bwd_gather_kernel<T, V><<<grid, kRaBlk * kRaBlk * 32, 0, st>>>(cp<T>(dy), H, W, C, box, tab, R, Po, pw,
+                                                                           inv, static_cast<T*>(dfeat));
+}
+
 cudaError_t roialign_bwd(int dtype, const void* dy, int N, int H, int W, int C, const float* rois, int R, int P,
-                         float scale, int sr, void* dfeat, cudaStream_t st, int step) {
-    if (step < 1 || (P + step - 1) / step > kMaxP) return cudaErrorInvalidValue;
-    dim3 grid(((H + kTile - 1) / kTile) * ((W + kTile - 1) / kTile), (C + kSlab - 1) / kSlab, N);
-    if (dtype == kF16)
-        roialign_bwd_kernel<__half><<<grid, kBwdThreads, 0, st>>>(cp<__half>(dy), H, W, C, rois, R, P, scale, sr,
-                                                                  step, static_cast<__half*>(dfeat));
-    else
-        roialign_bwd_kernel<float><<<grid, kBwdThreads, 0, st>>>(cp<float>(dy), H, W, C, rois, R, P, scale, sr,
-                                                                 step, static_cast<float*>(dfeat));
+                         float scale, int sr, void* dfeat, void* ws, size_t ws_bytes, cudaStream_t st, int step) {
+    if (step < 1 || (P + step - 1) / step > 16) return cudaErrorInvalidValue;
+    if (ws_bytes < roialign_bwd_workspace(R, H, W, P, step)) return cudaErrorInvalidValue;
+    const int Po = (P + step - 1) / step, pw = ra_table_width(P, step);
+    float* tab = static_cast<float*>(ws);
+    int4* box = reinterpret_cast<int4*>(static_cast<uint8_t*>(ws) +
+                                        (static_cast<size_t>(R) * (H + W) * pw * 4 + 255) / 256 * 256);
+    if (R > 0)
+        roialign_bwd_weights_kernel<<<(R + 7) / 8, 256, 0, st>>>(rois, R, H, W, P, scale, sr, step, pw, tab, box);
+    // channel slab per warp: 256*V channels (V 8-channel chunks per lane)
+    const int V = C >= 2048 ? 4 : (C >= 512 ? 2 : 1);
+    const dim3 grid(((H + kRaBlk - 1) / kRaBlk) * ((W + kRaBlk - 1) / kRaBlk), (C + 256 * V - 1) / (256 * V), N);
+    const float inv = 1.0f / static_cast<float>(max(sr * sr, 1));
+    const bool h = dtype == kF16;
+    if (V == 4) h ? ra_gather<__half, 4>(grid, dy, H, W, C, box, tab, R, Po, pw, inv, dfeat, st)
+                  : ra_gather<float, 4>(grid, dy, H, W, C, box, tab, R, Po, pw, inv, dfeat, st);
+    else if (V == 2) h ? ra_gather<__half, 2>(grid, dy, H, W, C, box, tab, R, Po, pw, inv, dfeat, st)
+                       : ra_gather<float, 2>(grid, dy, H, W, C, box, tab, R, Po, pw, inv, dfeat, st);
+    else h ? ra_gather<__half, 1>(grid, dy, H, W, C, box, tab, R, Po, pw, inv, dfeat, st)
+           : ra_gather<float, 1>(grid, dy, H, W, C, box, tab, R, Po, pw, inv, dfeat, st);
     return cudaGetLastError();
 }
 

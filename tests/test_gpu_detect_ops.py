@@ -241,3 +241,36 @@ def test_detection_losses_abi(orc, fp16):
         if rl[i] > 0:
             mask[i, 4 * rl[i]: 4 * rl[i] + 4] = False
     assert np.all(dg[mask] == 0)
+
+
+@pytest.mark.parametrize("fp16", [True, False])
+def test_roialign_c3_shape(orc, fp16):
+    """BASELINE config C3 shape: 8 x 1024-channel 50x84 features, 8 x 512 RoIs,
+    RoIAlign 14x14 (sampling ratio 2) forward and backward.  RoIAlign is
+    channel-separable, so the CPU restatement runs on a 64-channel subset (both
+    ends of the channel range: first and last slab of every kernel tiling)."""
+    from paper_1903_05831_b200 import simdet as sd
+    rng = np.random.default_rng(41 + fp16)
+    N, Cc, H, W, P = 8, 1024, 50, 84, 14
+    R = N * 512
+    tdt = torch.float16 if fp16 else torch.float32
+    feat = torch.randn((N, Cc, H, W), device="cuda").to(tdt)
+    rois = _rois(rng, R, N, H, W)
+    rois[:, 0] = np.repeat(np.arange(N), 512)
+    rt = torch.from_numpy(rois).cuda()
+    dy = torch.randn((R, Cc, P, P), device="cuda").to(tdt)
+    out = sd.roialign_forward(feat, rt, P, 1 / 16, 2)
+    dx = sd.roialign_backward(dy, (N, Cc, H, W), rt, P, 1 / 16, 2)
+    dx2 = sd.roialign_backward(dy, (N, Cc, H, W), rt, P, 1 / 16, 2)
+    torch.cuda.synchronize()
+    assert torch.equal(dx, dx2), "backward must be bitwise deterministic"
+    ch = np.r_[0:32, Cc - 32:Cc]
+    f_sub = np.ascontiguousarray(feat[:, ch].float().cpu().numpy())
+    dy_sub = np.ascontiguousarray(dy[:, ch].float().cpu().numpy())
+    out_ref = np.zeros((R, len(ch), P, P), np.float32)
+    orc.orc_roialign_fwd(p(f_sub), N, len(ch), H, W, p(rois), R, P, 1 / 16, 2, 1, p(out_ref))
+    dx_ref = np.zeros_like(f_sub)
+    orc.orc_roialign_bwd(p(dy_sub), N, len(ch), H, W, p(rois), R, P, 1 / 16, 2, 1, p(dx_ref))
+    tol = 1e-2 if fp16 else 1e-5
+    assert_close(out[:, ch], out_ref, tol, "roialign fwd C3")
+    assert_close(dx[:, ch], dx_ref, tol, "roialign bwd C3")
