@@ -9,6 +9,7 @@
 // Status codes mirror the reference's exception taxonomy (errors.hpp:9-40) the
 // same way include/sdb.h does, so error-behaviour parity can be asserted.
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -280,6 +281,25 @@ int ref_update_scale(double* scale, int64_t* good, int dynamic, int64_t interval
         update_scale(s, overflow != 0);
         *scale = s.scale;
         *good = s.good_steps;
+    });
+}
+
+// CommGroup::allreduce_sum (src/comm.cpp:288-315) over K in-process ranks
+// (run_workers, src/comm.cpp:451-471): seconds per call on rank 0, averaged
+// over `iters` calls on n floats per rank (the CPU baseline's allreduce term)
+int ref_allreduce_seconds(int K, int64_t n, int iters, double* seconds) {
+    return guarded([&] {
+        auto tr = make_inproc_transport(K);
+        double sec = 0.0;
+        run_workers(K, tr, [&](CommGroup& g) {
+            std::vector<float> buf(static_cast<size_t>(n), 1.0f + static_cast<float>(g.rank()));
+            g.allreduce_sum(buf);  // warm-up
+            const auto t0 = std::chrono::steady_clock::now();
+            for (int i = 0; i < iters; ++i) g.allreduce_sum(buf);
+            const auto t1 = std::chrono::steady_clock::now();
+            if (g.rank() == 0) sec = std::chrono::duration<double>(t1 - t0).count() / std::max(iters, 1);
+        });
+        *seconds = sec;
     });
 }
 

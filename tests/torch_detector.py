@@ -54,13 +54,16 @@ class TorchDetector:
     BN [C]) -- the fp32 masters as sdb_det_get_param returns them."""
 
     def __init__(self, params: dict, mode: int, blocks, A: int, pool: int, device="cpu", eps=1e-5, slope=0.1,
-                 sampling_ratio=2, rpn_batch=256):
+                 sampling_ratio=2, rpn_batch=256, dtype=torch.float32):
+        """dtype=torch.float64 (modes 0/2) runs the same graph in double: the
+        fp32 arithmetic noise floor of each gradient tensor (its conditioning)"""
         self.mode, self.blocks, self.A, self.pool = mode, tuple(blocks), A, pool
         self.eps, self.slope, self.sr, self.rpn_batch = eps, slope, sampling_ratio, rpn_batch
         self.dev = torch.device(device)
+        self.dt = dtype if mode != 1 else torch.float32
         self.p = {}
         for k, v in params.items():
-            t = torch.from_numpy(np.ascontiguousarray(v, np.float32)).to(self.dev)
+            t = torch.from_numpy(np.ascontiguousarray(v, np.float32)).to(self.dev, self.dt)
             if mode == 1 and not (k.endswith(".gamma") or k.endswith(".beta")):
                 t = t.half().float()  # fp16 shadow of the master
             self.p[k] = t.requires_grad_(True)
@@ -77,8 +80,8 @@ class TorchDetector:
         xd = x.double()
         mean = xd.mean(dim=(0, 2, 3))
         var = torch.clamp((xd * xd).mean(dim=(0, 2, 3)) - mean * mean, min=0.0)
-        invstd = (1.0 / torch.sqrt(var + self.eps)).float()
-        y = g.view(1, -1, 1, 1) * (x - mean.float().view(1, -1, 1, 1)) * invstd.view(1, -1, 1, 1) + b.view(1, -1, 1, 1)
+        invstd = (1.0 / torch.sqrt(var + self.eps)).to(self.dt)
+        y = g.view(1, -1, 1, 1) * (x - mean.to(self.dt).view(1, -1, 1, 1)) * invstd.view(1, -1, 1, 1) + b.view(1, -1, 1, 1)
         if self.mode == 0:
             y = self.q(y)
             return self.q(F.relu(y)) if act else y
@@ -116,7 +119,7 @@ class TorchDetector:
         grad_scale and finalised in the leaf dtype, rpn logits NCHW)."""
         from torchvision.ops import roi_align
         dev = self.dev
-        T = lambda a, dt=torch.float32: torch.as_tensor(np.ascontiguousarray(a)).to(dev, dt)
+        T = lambda a: torch.as_tensor(np.ascontiguousarray(a)).to(dev, self.dt)
         x = T(images)
         if self.mode == 1:
             x = x.half().float()
@@ -135,7 +138,7 @@ class TorchDetector:
         lg = logits.permute(0, 2, 3, 1).reshape(-1)
         valid = lab >= 0
         cnt = max(int(valid.sum()), 1)
-        l1 = F.binary_cross_entropy_with_logits(lg[valid], lab[valid].float(), reduction="sum") / cnt
+        l1 = F.binary_cross_entropy_with_logits(lg[valid], lab[valid].to(self.dt), reduction="sum") / cnt
         dl = deltas.permute(0, 2, 3, 1).reshape(-1, 4)
         fg = lab == 1
         beta = 1.0 / 9.0
@@ -167,9 +170,9 @@ class TorchDetector:
             g = v.grad if v.grad is not None else torch.zeros_like(v)
             if self.mode == 1 and not (k.endswith(".gamma") or k.endswith(".beta")):
                 g = g.half().float()  # leaf dtype F16 (src/autograd.cpp:481)
-            grads[k] = g.detach().cpu().numpy()
+            grads[k] = g.detach().float().cpu().numpy()
         losses = np.array([float(v.detach()) for v in (l1, l2, l3, l4)], np.float64)
-        return losses, grads, logits.detach().cpu().numpy()
+        return losses, grads, logits.detach().float().cpu().numpy()
 
 
 def gpu_params(det) -> dict:
@@ -177,12 +180,12 @@ def gpu_params(det) -> dict:
     return {det.params[i][0]: det.get_param(i) for i in range(det.n_tensors)}
 
 
-def run_checker(det, params, s, mode, grad_scale, device):
+def run_checker(det, params, s, mode, grad_scale, device, dtype=torch.float32):
     """teacher-forced TorchDetector step on the GPU step's decisions `s`
     (tests.det_parity.gpu_state); returns (losses, flat grads in pack order, logits)"""
     pr = det.p
     img = np.ascontiguousarray(s["images"][..., :3].astype(np.float32).transpose(0, 3, 1, 2))
-    td = TorchDetector(params, mode, pr.blocks, det.A, pr.pool, device=device)
+    td = TorchDetector(params, mode, pr.blocks, det.A, pr.pool, device=device, dtype=dtype)
     losses, grads, lg = td.step(img, s["a_labels"], s["a_targets"], s["rois"], s["roi_labels"], s["roi_targets"],
                                 grad_scale)
     flat = np.concatenate([grads[det.params[i][0]].ravel() for i in range(det.n_tensors)]).astype(np.float32)
