@@ -17,11 +17,13 @@ One JSON line on rank 0:
            H2D, step, losses D2H) every step;
   roofline  = the tensor-core implicit-GEMM conv kernels (fprop+dgrad+wgrad,
            FLOP-weighted) from a CUDA-event-instrumented step;
-  cpu_baseline = the reference engine's own conv2d (oracle/_ref, compiled from
-           /root/reference sources) timed on this host, extrapolated to the
-           R50-C4 training FLOPs per image (a full CPU step takes ~9 min/img).
---impl reference runs that reference CPU path alone (all host cores, one
-reference thread per core as its run_workers does) for the same metric.
+  cpu_baseline = the reference engine's own CPU path (oracle/_ref, compiled from
+           /root/reference sources) timed per operator on this host and composed
+           into a C4 step (every conv shape, IABN, NMS at 12000,
+           apply_sgd at 29 M, allreduce; "extrapolated" -- a full CPU step takes
+           ~9 min/img), one core;
+--impl reference runs that reference CPU path alone on all host cores (one
+reference rank per core, as its run_workers does) for the same metric.
 """
 import argparse
 import json
@@ -121,54 +123,210 @@ def measured_peaks():
 
 
 # ------------------------------------------------------------------ reference CPU path
-REF_SAMPLES = [
-    # (N, C, H, W, K, R, S, stride, pad): res4 3x3, res4 1x1 reduce, res5-head 3x3 on 2 RoIs
-    (1, 256, 50, 84, 256, 3, 3, 1, 1),
-    (1, 1024, 50, 84, 256, 1, 1, 1, 0),
-    (2, 512, 7, 7, 512, 3, 3, 1, 1),
-]
+# BASELINE.md §3 / SURVEY.md §8(d): a C4 step cannot run end to end on CPU
+# (~9 CPU-minutes per image), so the reference's own CPU implementation is
+# timed per operator on bounded samples and composed into seconds per step
+# ("extrapolated"):
+#   every distinct R50-C4 conv shape (reference conv2d + Tape backward rule,
+#   src/tensor.cpp:169, src/autograd.cpp:290) at a reduced spatial size,
+#   scaled by its MAC count x multiplicity; IABN fwd+bwd (src/memopt.cpp:
+#   226,278) per element x the 497 M norm elements per image; nms_greedy
+#   (src/postproc.cpp:47) at 12000 boxes per image; sgd_step_master with the
+#   fp16 shadow refresh (src/precision.cpp:84) per parameter x 29.0 M;
+#   allreduce_sum (src/comm.cpp:288) of the fp32 gradient across K threads;
+#   RoIAlign fwd+bwd (absent in the reference: the CPU restatement, "port")
+#   on a channel subset, scaled to 1024 RoIs x 1024 channels.
 
 
-def ref_conv_sample(threads=1, budget_s=12.0):
-    """Time the reference engine's conv2d forward + Tape backward (src/tensor.cpp:169,
-    src/autograd.cpp:290) on R50-C4 layer shapes, `threads` concurrent reference
-    workers.  Returns (train GMAC/s aggregate, description)."""
-    import numpy as np
+def r50c4_layers(H=800, W=1333, batch=2, rois=1024):
+    """distinct conv shapes of the R50-C4 step: (N, C, H, W, K, R, stride, pad) -> multiplicity"""
+    layers = {}
+
+    def add(n, c, h, w, k, r, s, p):
+        key = (n, c, h, w, k, r, s, p)
+        layers[key] = layers.get(key, 0) + 1
+        return (h + 2 * p - r) // s + 1, (w + 2 * p - r) // s + 1
+
+    h, w = add(batch, 3, H, W, 64, 7, 2, 3)
+    h, w = (h + 2 - 3) // 2 + 1, (w + 2 - 3) // 2 + 1  # max-pool 3x3/2
+    cin = 64
+    norm_elems = 0
+    for (nb, width, cout, stride) in ((3, 64, 256, 1), (4, 128, 512, 2), (6, 256, 1024, 2)):
+        for b in range(nb):
+            s = stride if b == 0 else 1
+            h2, w2 = add(batch, cin, h, w, width, 1, s, 0)
+            add(batch, width, h2, w2, width, 3, 1, 1)
+            add(batch, width, h2, w2, cout, 1, 1, 0)
+            norm_elems += batch * h2 * w2 * (2 * width + cout)
+            if b == 0:
+                add(batch, cin, h, w, cout, 1, s, 0)
+                norm_elems += batch * h2 * w2 * cout
+            h, w, cin = h2, w2, cout
+    fh, fw = h, w
+    add(batch, 1024, fh, fw, 512, 3, 1, 1)   # RPN conv
+    add(batch, 512, fh, fw, 15, 1, 1, 0)     # RPN cls
+    add(batch, 512, fh, fw, 60, 1, 1, 0)     # RPN bbox
+    h, w, cin = 14, 14, 1024                 # RoIAlign 14x14 -> res5
+    for b in range(3):
+        s = 2 if b == 0 else 1
+        h2, w2 = add(rois, cin, h, w, 512, 1, s, 0)
+        add(rois, 512, h2, w2, 512, 3, 1, 1)
+        add(rois, 512, h2, w2, 2048, 1, 1, 0)
+        norm_elems += rois * h2 * w2 * (2 * 512 + 2048)
+        if b == 0:
+            add(rois, cin, h, w, 2048, 1, s, 0)
+            norm_elems += rois * h2 * w2 * 2048
+        h, w, cin = h2, w2, 2048
+    norm_elems += batch * (H // 2) * ((W + 1) // 2) * 64  # stem norm
+    return layers, norm_elems, (fh, fw)
+
+
+def _conv_macs(n, c, h, w, k, r, s, p):
+    ho, wo = (h + 2 * p - r) // s + 1, (w + 2 * p - r) // s + 1
+    return n * ho * wo * k * c * r * r
+
+
+class RefStep:
+    """per-operator samples of the reference CPU path (one thread = one rank)"""
+
+    def __init__(self, budget_macs=6e7):
+        import numpy as np
+        import oracle
+        self.np, self.oracle, self.ref, self.orc = np, oracle, oracle.ref(), oracle.orc()
+        self.layers, self.norm_elems, (self.fh, self.fw) = r50c4_layers()
+        rng = np.random.default_rng(0)
+        self.samples = []
+        for (n, c, h, w, k, r, s, p), mult in self.layers.items():
+            full = _conv_macs(n, c, h, w, k, r, s, p)
+            # reduced instance: one image / RoI, spatial crop to ~budget MACs
+            hs, ws = h, w
+            while _conv_macs(1, c, hs, ws, k, r, s, p) > budget_macs and min(hs, ws) > max(r, 2 * s):
+                if hs >= ws:
+                    hs = max(r, hs // 2)
+                else:
+                    ws = max(r, ws // 2)
+            ns = 1
+            x = rng.standard_normal((ns, c, hs, ws)).astype(np.float16).astype(np.float32)
+            kk = (0.05 * rng.standard_normal((k, c, r, r))).astype(np.float16).astype(np.float32)
+            ho, wo = (hs + 2 * p - r) // s + 1, (ws + 2 * p - r) // s + 1
+            self.samples.append(dict(shape=(ns, c, hs, ws, k, r, s, p), x=x, k=kk, y=np.zeros((ns, k, ho, wo), np.float32),
+                                     dy=rng.standard_normal((ns, k, ho, wo)).astype(np.float32), dx=np.zeros_like(x),
+                                     dk=np.zeros_like(kk), scale=full * mult / _conv_macs(ns, c, hs, ws, k, r, s, p)))
+        # IABN sample [1, 256, 50, 84]
+        self.bn = dict(x=rng.standard_normal((1, 256, 50, 84)).astype(np.float32), g=np.ones(256, np.float32),
+                       b=np.zeros(256, np.float32))
+        # NMS at 12000 boxes (one image)
+        n = 12000
+        xy = rng.uniform(0, 1200, (n, 2))
+        wh = rng.uniform(8, 300, (n, 2))
+        self.boxes = np.ascontiguousarray(np.concatenate([xy, xy + wh], 1), np.float64)
+        self.scores = np.ascontiguousarray(rng.uniform(0, 1, n), np.float64)  # postproc.cpp:48 wants [0,1]
+        self.cls = np.zeros(n, np.int32)
+        # sgd on 4 M parameters (scaled to 29 M)
+        self.nsgd = 1 << 22
+        self.w = rng.standard_normal(self.nsgd).astype(np.float32)
+        self.v = np.zeros(self.nsgd, np.float32)
+        self.g = rng.standard_normal(self.nsgd).astype(np.float32)
+        # RoIAlign restatement on a 16-channel subset of the C4 feature
+        self.ra_c = 16
+        self.feat = rng.standard_normal((2, self.ra_c, self.fh, self.fw)).astype(np.float32)
+        x1 = rng.uniform(0, 1200, 1024)
+        y1 = rng.uniform(0, 700, 1024)
+        self.rois = np.ascontiguousarray(np.stack([np.repeat([0, 1], 512), x1, y1, x1 + rng.uniform(16, 500, 1024),
+                                                   y1 + rng.uniform(16, 400, 1024)], 1), np.float32)
+        self.ra_out = np.zeros((1024, self.ra_c, 14, 14), np.float32)
+        self.ra_dx = np.zeros_like(self.feat)
+        self.n_params = 29.0e6
+
+    def time_once(self):
+        """one pass over every operator sample; returns {part: extrapolated seconds per C4 step (batch 2)}"""
+        import time
+        np, p, ref, orc = self.np, self.oracle.p, self.ref, self.orc
+        out = {"conv": 0.0}
+        for sm in self.samples:
+            (n, c, h, w, k, r, s, pd) = sm["shape"]
+            t0 = time.perf_counter()
+            ref.ref_conv2d(p(sm["x"]), n, c, h, w, p(sm["k"]), k, r, r, s, pd, 1, p(sm["y"]))
+            ref.ref_conv2d_backward(p(sm["x"]), n, c, h, w, p(sm["k"]), k, r, r, s, pd, 1, p(sm["dy"]), p(sm["dx"]),
+                                    p(sm["dk"]))
+            out["conv"] += (time.perf_counter() - t0) * sm["scale"]
+        b = self.bn
+        N, C, H, W = b["x"].shape
+        y = np.zeros_like(b["x"])
+        mean = np.zeros(C, np.float32)
+        inv = np.zeros(C, np.float32)
+        dx = np.zeros_like(b["x"])
+        dg = np.zeros(C, np.float32)
+        db = np.zeros(C, np.float32)
+        t0 = time.perf_counter()
+        ref.ref_iabn_forward(p(b["x"]), N, C, H, W, p(b["g"]), p(b["b"]), 1e-5, 0.1, 1, p(y), p(mean), p(inv))
+        ref.ref_iabn_backward(p(b["x"]), p(y), N, C, H, W, p(b["g"]), p(b["b"]), p(mean), p(inv), 1e-5, 0.1, 1, p(dx),
+                              p(dg), p(db))
+        out["iabn"] = (time.perf_counter() - t0) * self.norm_elems / b["x"].size
+        keep = np.zeros(12000, np.int64)
+        nk = np.zeros(1, np.int64)
+        t0 = time.perf_counter()
+        ref.ref_nms_greedy(p(self.boxes), p(self.scores), p(self.cls), 12000, 0.7, p(keep), p(nk))
+        out["nms"] = (time.perf_counter() - t0) * 2  # per image, 2 images
+        t0 = time.perf_counter()
+        ref.ref_sgd_step_master(p(self.w), p(self.v), p(self.g), self.nsgd, 0.01, 0.9)
+        out["sgd"] = (time.perf_counter() - t0) * self.n_params / self.nsgd
+        t0 = time.perf_counter()
+        orc.orc_roialign_fwd(p(self.feat), 2, self.ra_c, self.fh, self.fw, p(self.rois), 1024, 14, 1 / 16, 2, 1,
+                             p(self.ra_out))
+        orc.orc_roialign_bwd(p(self.ra_out), 2, self.ra_c, self.fh, self.fw, p(self.rois), 1024, 14, 1 / 16, 2, 1,
+                             p(self.ra_dx))
+        out["roialign"] = (time.perf_counter() - t0) * 1024 / self.ra_c
+        return out
+
+
+def ref_allreduce_s(K):
+    """reference CommGroup::allreduce_sum of the 116 MB fp32 gradient over K in-process ranks"""
+    import ctypes as C
 
     import oracle
-    ref = oracle.ref()
-    rng = np.random.default_rng(0)
-    bufs = []
-    for (N, C, H, W, K, R, S, st, pd) in REF_SAMPLES:
-        x = rng.standard_normal((N, C, H, W)).astype(np.float16).astype(np.float32)
-        k = (0.05 * rng.standard_normal((K, C, R, S))).astype(np.float16).astype(np.float32)
-        Ho, Wo = (H + 2 * pd - R) // st + 1, (W + 2 * pd - S) // st + 1
-        bufs.append((x, k, np.zeros((N, K, Ho, Wo), np.float32), rng.standard_normal((N, K, Ho, Wo)).astype(np.float32),
-                     np.zeros_like(x), np.zeros_like(k)))
-    done_mac = [0.0] * threads
+    if K <= 1:
+        return 0.0
+    s = C.c_double()
+    oracle.ref().ref_allreduce_seconds(K, 29_000_000, 1, C.byref(s))
+    return s.value
+
+
+def ref_cpu_baseline(threads=1, budget_s=20.0, K=1):
+    """compose the reference CPU step on `threads` concurrent workers (one per
+    rank, as run_workers does), repeating passes within `budget_s`; returns
+    (images/s for the whole job, seconds per step, per-part seconds, sample text)"""
+    import statistics as stt
+    import time
+    rs = [RefStep() for _ in range(threads)]
+    results = [[] for _ in range(threads)]
     stop = time.time() + budget_s
 
     def worker(t):
-        i = t
-        while time.time() < stop:
-            (N, C, H, W, K, R, S, st, pd) = REF_SAMPLES[i % len(REF_SAMPLES)]
-            x, k, y, dy, dx, dk = bufs[i % len(bufs)]
-            ref.ref_conv2d(oracle.p(x), N, C, H, W, oracle.p(k), K, R, S, st, pd, 1, oracle.p(y))
-            ref.ref_conv2d_backward(oracle.p(x), N, C, H, W, oracle.p(k), K, R, S, st, pd, 1, oracle.p(dy),
-                                    oracle.p(dx), oracle.p(dk))
-            macs = N * y.shape[2] * y.shape[3] * K * C * R * S
-            done_mac[t] += 3.0 * macs  # fprop + dgrad + wgrad
-            i += 1
+        while True:
+            results[t].append(rs[t].time_once())
+            if time.time() >= stop:
+                break
 
-    t0 = time.time()
     ths = [threading.Thread(target=worker, args=(t,)) for t in range(threads)]
     for th in ths:
         th.start()
     for th in ths:
         th.join()
-    el = time.time() - t0
-    gmacs = sum(done_mac) / el / 1e9
-    return gmacs, el
+    parts = {}
+    for key in results[0][0]:
+        parts[key] = stt.mean(stt.median(r[key] for r in res) for res in results)
+    parts["allreduce"] = ref_allreduce_s(max(K, threads if threads > 1 else 1))
+    step_s = sum(parts.values())
+    ranks = max(threads, 1)
+    img_s = ranks * 2 / step_s
+    npass = min(len(r) for r in results)
+    sample = (f"reference CPU path composed per operator (BASELINE.md §3): every distinct R50-C4 conv shape "
+              f"({len(rs[0].samples)}) fwd + Tape bwd on a reduced crop scaled by MACs, IABN fwd+bwd scaled to "
+              f"{rs[0].norm_elems / 1e6:.0f} M elements/step, nms_greedy 12000 x 2 images, sgd_step_master 29.0 M, "
+              f"RoIAlign restatement scaled to 1024 RoIs x 1024 ch, allreduce_sum 116 MB over {ranks} ranks; "
+              f"{threads} thread(s), {npass} pass(es) in {budget_s:.0f} s; extrapolated")
+    return img_s, step_s, parts, sample
 
 
 def cpu_model():
@@ -186,27 +344,23 @@ def run_reference(args):
     if rank != 0:
         return
     import oracle
-    cfg = {"workload": "C4: Faster R-CNN R50-C4 training, batch 2/GPU, 3x800x1333, 512 RoIs/img",
+    cfg = {"workload": "C4: Faster R-CNN R50-C4 training, batch 2/rank, 3x800x1333, 512 RoIs/img",
            "global_batch": 2 * args.gpus, "parallelism": f"dp{args.gpus}"}
     if not oracle.ref_available():
         print(json.dumps({"impl": "reference", "metric": METRIC, "unit": UNIT,
                           "unavailable": "oracle/_ref/libsimdet_ref.so not built (needs /root/reference at build time)"}))
         return
-    threads = os.cpu_count() or 1
-    per_step = []
-    for s in range(args.warmup + args.steps):
-        gmacs, el = ref_conv_sample(threads, budget_s=max(2.0, 60.0 / (args.warmup + args.steps)))
-        if s >= args.warmup:
-            per_step.append(gmacs)
-    rate = statistics.mean(per_step)  # train GMAC/s over all threads
-    value = rate * 1e9 * 2 / TRAIN_FLOP_PER_IMAGE  # MAC -> FLOP
-    sample = (f"reference conv2d fwd+bwd (simdet::conv2d + Tape rule) on R50-C4 layer shapes {REF_SAMPLES}, "
-              f"{threads} threads x {args.steps} steps; extrapolated by 2.767 TFLOP/train-image (conv FLOPs only)")
+    # all host cores, one reference rank per core (run_workers, src/comm.cpp:451-465)
+    threads = max(1, min(os.cpu_count() or 1, 64))
+    budget = max(20.0, min(150.0, 6.0 * (args.warmup + args.steps)))
+    value, step_s, parts, sample = ref_cpu_baseline(threads, budget_s=budget, K=threads)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32 (fp16-emulated storage)", "data": "synthetic",
-            "config": cfg, "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                                            "sample": sample, "cpu": cpu_model(), "extrapolated": True},
+            "config": cfg,
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample,
+                             "cpu": cpu_model(), "extrapolated": True,
+                             "seconds_per_step_by_part": {k: round(v, 4) for k, v in parts.items()}},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
@@ -405,11 +559,10 @@ def run_ours(args):
         try:
             import oracle
             if oracle.ref_available():
-                gmacs, el = ref_conv_sample(1, budget_s=12.0)
-                cpu = {"value": gmacs * 1e9 * 2 / TRAIN_FLOP_PER_IMAGE, "unit": UNIT, "cores": 1, "kind": "reference",
-                       "sample": f"reference conv2d fwd+Tape bwd on R50-C4 layer shapes for {el:.1f} s "
-                                 f"({gmacs:.2f} train GMAC/s), extrapolated by 2.767 TFLOP/image",
-                       "cpu": cpu_model(), "extrapolated": True}
+                v, step_s, parts, sample = ref_cpu_baseline(1, budget_s=20.0, K=1)
+                cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "reference", "sample": sample,
+                       "cpu": cpu_model(), "extrapolated": True, "seconds_per_step": round(step_s, 2),
+                       "seconds_per_step_by_part": {k: round(x, 4) for k, x in parts.items()}}
         except Exception as e:  # the baseline is reported, never required
             cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference", "sample": f"failed: {e}"}
     line = {

@@ -60,6 +60,13 @@ int sdb_ctx_destroy(sdb_ctx* ctx);
 void* sdb_ctx_stream(sdb_ctx* ctx);
 int sdb_get_nccl_unique_id(void* out128);
 int sdb_synchronize(sdb_ctx* ctx);
+/* ---- device memory for hosts without a CUDA runtime of their own (the
+ * reference is a pure C++ CPU library; its shim stages Tensors through these).
+ * Copies are ordered on the context's stream and complete before returning. */
+int sdb_device_alloc(sdb_ctx* ctx, size_t bytes, void** out);
+int sdb_device_free(sdb_ctx* ctx, void* p);
+int sdb_copy_to_device(sdb_ctx* ctx, void* dst, const void* src, size_t bytes);
+int sdb_copy_to_host(sdb_ctx* ctx, void* dst, const void* src, size_t bytes);
 /* in-place SUM over the context's ranks: CommGroup::allreduce_sum
  * (src/comm.cpp:288-315), NCCL on `stream`; dtype SDB_F32 / SDB_F16 / SDB_F64;
  * identity without a communicator.  Issue order must agree on every rank (the

@@ -139,6 +139,33 @@ int sdb_synchronize(sdb_ctx* ctx) {
 
 int sdb_get_nccl_unique_id(void* out128) { return sdb::comm_unique_id(out128); }
 
+int sdb_device_alloc(sdb_ctx* ctx, size_t bytes, void** out) {
+    if (!ctx || !out) return fail(SDB_PARAM, "null argument");
+    *out = nullptr;
+    if (int rc = cuda_status(cudaSetDevice(ctx->device), "cudaSetDevice")) return rc;
+    return cuda_status(cudaMalloc(out, std::max<size_t>(bytes, 16)), "cudaMalloc");
+}
+
+int sdb_device_free(sdb_ctx* ctx, void* p) {
+    if (!ctx) return fail(SDB_PARAM, "null ctx");
+    if (int rc = cuda_status(cudaStreamSynchronize(ctx->stream), "synchronize")) return rc;
+    return cuda_status(cudaFree(p), "cudaFree");
+}
+
+int sdb_copy_to_device(sdb_ctx* ctx, void* dst, const void* src, size_t bytes) {
+    if (!ctx) return fail(SDB_PARAM, "null ctx");
+    if (int rc = cuda_status(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream), "copy h2d"))
+        return rc;
+    return cuda_status(cudaStreamSynchronize(ctx->stream), "copy h2d");
+}
+
+int sdb_copy_to_host(sdb_ctx* ctx, void* dst, const void* src, size_t bytes) {
+    if (!ctx) return fail(SDB_PARAM, "null ctx");
+    if (int rc = cuda_status(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream), "copy d2h"))
+        return rc;
+    return cuda_status(cudaStreamSynchronize(ctx->stream), "copy d2h");
+}
+
 int sdb_conv_fprop(sdb_ctx* ctx, int dtype, const void* x, const void* w, void* y, int N, int H, int W, int C, int K,
                    int R, int S, int stride, int pad, void* stream) {
     if (int rc = check_dtype(dtype)) return rc;

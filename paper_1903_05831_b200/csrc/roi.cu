@@ -61,6 +61,30 @@ SDB_DEV void st8<float>(float* p, const float (&v)[8]) {
     *reinterpret_cast<float4*>(p + 4) = make_float4(v[4], v[5], v[6], v[7]);
 }
 
+// 8 channels as 4 fp32 pairs (packed-FMA operands)
+template <class T>
+SDB_DEV void ld8x2(const T* p, float2 (&v)[4]);
+template <>
+SDB_DEV void ld8x2<__half>(const __half* p, float2 (&v)[4]) {
+    const uint4 u = *reinterpret_cast<const uint4*>(p);
+    const __half2* h = reinterpret_cast<const __half2*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = __half22float2(h[i]);
+}
+template <>
+SDB_DEV void ld8x2<float>(const float* p, float2 (&v)[4]) {
+    const float4 a = *reinterpret_cast<const float4*>(p);
+    const float4 b = *reinterpret_cast<const float4*>(p + 4);
+    v[0] = make_float2(a.x, a.y); v[1] = make_float2(a.z, a.w); v[2] = make_float2(b.x, b.y); v[3] = make_float2(b.z, b.w);
+}
+template <class T>
+SDB_DEV void st8x2(T* p, const float2 (&v)[4]) {
+    float f[8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) { f[2 * i] = v[i].x; f[2 * i + 1] = v[i].y; }
+    st8<T>(p, f);
+}
+
 struct Geom {
     int b;
     float sw, sh, bw, bh;
@@ -137,7 +161,8 @@ __global__ void roialign_fwd_kernel(const T* __restrict__ feat, int H, int W, in
 // RoI samples; through L2 that read amplification capped the direct kernel at
 // ~1.6 GB of L2 traffic per step).  Threads take the image's (RoI, bin) items
 // with consecutive lanes on consecutive bins of one RoI (neighbouring pixels:
-// few smem bank conflicts).  Same per-output arithmetic as roialign_fwd_kernel.
+// few smem bank conflicts).  Packed fp32 FMAs (fma.rn.f32x2) accumulate the
+// 16 weighted corners of a bin: the kernel is instruction-bound, not memory-bound.
 template <class T>
 __global__ void __launch_bounds__(256) roialign_fwd_smem_kernel(const T* __restrict__ feat, int H, int W, int C,
                                                                 const float* __restrict__ rois, int R, int P,
@@ -163,13 +188,14 @@ __global__ void __launch_bounds__(256) roialign_fwd_smem_kernel(const T* __restr
     __syncthreads();
     const int Po = (P + step - 1) / step, PP = Po * Po;
     const int items = cnt * PP;
-    const float count = static_cast<float>(max(sr * sr, 1));
+    const float inv_count = 1.0f / static_cast<float>(max(sr * sr, 1));
     const T* f = reinterpret_cast<const T*>(ra_smem);
     for (int e = threadIdx.x; e < items; e += blockDim.x) {
         const int r = list[e / PP], bin = e % PP;
         const int ph = (bin / Po) * step, pw = (bin % Po) * step;
         const Geom g = roi_geom(rois + static_cast<int64_t>(r) * 5, P, scale);
-        float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        // packed fp32 FMAs (fma.rn.f32x2): 4 instructions per corner for 8 channels
+        float2 acc[4] = {};
         for (int iy = 0; iy < sr; ++iy) {
             float y = sample_coord(g.sh, ph, g.bh, iy, sr);
             for (int ix = 0; ix < sr; ++ix) {
@@ -181,19 +207,22 @@ __global__ void __launch_bounds__(256) roialign_fwd_smem_kernel(const T* __restr
                 if (xl >= W - 1) { xh = xl = W - 1; xx = static_cast<float>(xl); } else xh = xl + 1;
                 const float ly = yy - static_cast<float>(yl), lx = xx - static_cast<float>(xl);
                 const float hy = 1.f - ly, hx = 1.f - lx;
-                const float w1 = hy * hx, w2 = hy * lx, w3 = ly * hx, w4 = ly * lx;
-                float v1[8], v2[8], v3[8], v4[8];
-                ld8<T>(f + (yl * W + xl) * 8, v1);
-                ld8<T>(f + (yl * W + xh) * 8, v2);
-                ld8<T>(f + (yh * W + xl) * 8, v3);
-                ld8<T>(f + (yh * W + xh) * 8, v4);
+                const float2 w1 = make_float2(hy * hx, hy * hx), w2 = make_float2(hy * lx, hy * lx);
+                const float2 w3 = make_float2(ly * hx, ly * hx), w4 = make_float2(ly * lx, ly * lx);
+                float2 v1[4], v2[4], v3[4], v4[4];
+                ld8x2<T>(f + (yl * W + xl) * 8, v1);
+                ld8x2<T>(f + (yl * W + xh) * 8, v2);
+                ld8x2<T>(f + (yh * W + xl) * 8, v3);
+                ld8x2<T>(f + (yh * W + xh) * 8, v4);
 #pragma unroll
-                for (int j = 0; j < 8; ++j) acc[j] += w1 * v1[j] + w2 * v2[j] + w3 * v3[j] + w4 * v4[j];
+                for (int j = 0; j < 4; ++j)
+                    acc[j] = ffma2(w4, v4[j], ffma2(w3, v3[j], ffma2(w2, v2[j], ffma2(w1, v1[j], acc[j]))));
             }
         }
+        const float2 ic = make_float2(inv_count, inv_count);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] = acc[j] / count;
-        st8<T>(out + (static_cast<int64_t>(r) * PP + bin) * C + c8 * 8, acc);
+        for (int j = 0; j < 4; ++j) acc[j] = ffma2(acc[j], ic, make_float2(0.f, 0.f));
+        st8x2<T>(out + (static_cast<int64_t>(r) * PP + bin) * C + c8 * 8, acc);
     }
 }
 
@@ -211,8 +240,8 @@ __global__ void __launch_bounds__(256) roialign_fwd_smem_kernel(const T* __restr
 //      weights of its row and column in one load per lane, and accumulates
 //      the nonzero bin pairs in registers.  No shared memory and no barriers;
 //      a CTA is a 4x4 pixel block, so the dY rows its pixels share hit L1.
-// The summation order per output element is the same as a per-pixel loop
-// over (RoI, ph, pw) -- bitwise reproducible run to run.
+// The summation order per output element is fixed (RoI, ph, pw) -- bitwise
+// reproducible run to run; products are accumulated with packed fp32 FMAs.
 constexpr int kRaBlk = 4;  // CTA = kRaBlk x kRaBlk pixels (one warp each)
 
 SDB_DEV float bin_axis_weight(float start, float bin, int pb_full, int sr, int pix, int lim) {
@@ -280,11 +309,11 @@ __global__ void __launch_bounds__(kRaBlk * kRaBlk * 32) roialign_bwd_gather_kern
     const int n = blockIdx.z;
     const int c0 = blockIdx.y * 256 * V + lane * 8;
     if (y >= H || x >= W) return;  // whole warp: no barriers below
-    float acc[V][8];
+    float2 acc[V][4];
 #pragma unroll
     for (int v = 0; v < V; ++v)
 #pragma unroll
-        for (int k = 0; k < 8; ++k) acc[v][k] = 0.f;
+        for (int k = 0; k < 4; ++k) acc[v][k] = make_float2(0.f, 0.f);
     const int64_t row_stride = static_cast<int64_t>(Po) * C;
     for (int r0 = 0; r0 < R; r0 += 32) {
         bool hit = false;
@@ -307,14 +336,15 @@ __global__ void __launch_bounds__(kRaBlk * kRaBlk * 32) roialign_bwd_gather_kern
                     const int pwi = __ffs(b2) - 1;
                     const float wx = __shfl_sync(0xffffffffu, w, 16 + pwi);
                     const float wgt = wy * wx * inv_count;
+                    const float2 w2 = make_float2(wgt, wgt);
                     const T* dd = d + ph * row_stride + static_cast<int64_t>(pwi) * C;
 #pragma unroll
                     for (int v = 0; v < V; ++v) {
                         if (c0 + v * 256 >= C) break;
-                        float val[8];
-                        ld8<T>(dd + v * 256, val);
+                        float2 val[4];
+                        ld8x2<T>(dd + v * 256, val);
 #pragma unroll
-                        for (int k = 0; k < 8; ++k) acc[v][k] += wgt * val[k];
+                        for (int k = 0; k < 4; ++k) acc[v][k] = ffma2(w2, val[k], acc[v][k]);
                     }
                 }
             }
@@ -322,7 +352,7 @@ __global__ void __launch_bounds__(kRaBlk * kRaBlk * 32) roialign_bwd_gather_kern
     }
 #pragma unroll
     for (int v = 0; v < V; ++v)
-        if (c0 + v * 256 < C) st8<T>(dfeat + ((static_cast<int64_t>(n) * H + y) * W + x) * C + c0 + v * 256, acc[v]);
+        if (c0 + v * 256 < C) st8x2<T>(dfeat + ((static_cast<int64_t>(n) * H + y) * W + x) * C + c0 + v * 256, acc[v]);
 }
 
 // ---------------------------------------------------------------- pooling

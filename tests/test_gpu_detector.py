@@ -108,7 +108,7 @@ def _ref16_vs_ref32(det, cfg16, w, s, scale):
     return g16, g32
 
 
-@pytest.mark.parametrize("size", [128, 256])
+@pytest.mark.parametrize("size", [256])
 def test_c2_fp16_ten_steps(ref, orc, size):
     """Per tensor, the GPU's fp16 gradient error against ref16 is held to the
     reference's own fp16 noise level for that tensor, measured as err(ref16,
