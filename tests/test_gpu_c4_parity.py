@@ -16,8 +16,8 @@ and the fp16-contract emulation), teacher-forced on the step's own decisions.  E
       RPN logits <= 1e-3; every parameter gradient and per-step delta <= 1e-2
       or, where the fp32 arithmetic itself is noisier (the checker's own fp32
       vs fp64 error), <= 1.5x that floor;
-  mode 1 (fp16, the benchmarked graph): losses and RPN logits within 1e-2 of
-      the fp32 truth; per tensor, the gradient and the parameter delta no
+  mode 1 (fp16, the benchmarked graph): losses within 1e-2 of the fp32
+      truth, RPN logits within max(1e-2, 1.5 x err(torch16, torch32)); per tensor, the gradient and the parameter delta no
       further from the fp16-contract emulation (torch16) than torch16 is from
       the fp32 truth (x2 per tensor, x1.5 globally, floor 1e-2) -- the same
       noise-floor rule as the C2 test against the reference's own fp16 run.
@@ -111,11 +111,15 @@ def test_c4_fp16_benchmarked_graph(orc, steps):
         params = gpu_params(det)
         _, w0, v0, lg, scale, s = _step_and_check(det, step)
         assert scale == 128.0
-        l16, g16, _ = run_checker(det, params, s, 1, scale, "cuda")
+        l16, g16, lg16 = run_checker(det, params, s, 1, scale, "cuda")
         l32, g32, lg32 = run_checker(det, params, s, 2, scale, "cuda")
         for i in range(4):
             assert abs(lg[i] - l32[i]) <= 1e-2 * abs(l32[i]), (step, i, lg[i], l32[i])
-        assert norm_rel(s["logits"][..., :det.A].astype(np.float32).transpose(0, 3, 1, 2), lg32) <= 1e-2
+        # RPN logits after 16 fp16 bottlenecks at 800x1333: the fp16 contract
+        # itself moves them by ~1.5% (torch16 vs torch32); same floor rule
+        lg_gpu = s["logits"][..., :det.A].astype(np.float32).transpose(0, 3, 1, 2)
+        assert norm_rel(lg_gpu, lg32) <= max(1e-2, 1.5 * norm_rel(lg16, lg32)), (norm_rel(lg_gpu, lg32),
+                                                                                 norm_rel(lg16, lg32))
         g = dp.flat_grads(det)
         e_gpu = _split_err(det, g, g16)
         floor = _split_err(det, g16, g32)
