@@ -284,7 +284,10 @@ int sdb_det_train_step_host_nchw(sdb_det* det, const void* images_nchw_host, con
  * 9 anchors (f32 [nA][4]), 10 C4 feature (dtype NHWC), 11 images (dtype NHWC8),
  * 12 loss-scale state (f64 scale, then i64 good_steps), 13 stem conv output (dtype NHWC),
  * 14 max-pool output (dtype NHWC), 15 stem im2col matrix (f16 [pixels][192], fp16 mode),
- * 16 fp16 weight shadows (flat, driver layout), 17 fp32 masters (flat, driver layout).
+ * 16 fp16 weight shadows (flat, driver layout), 17 fp32 masters (flat, driver layout),
+ * 18 RoIAlign output (dtype [R][Po][Po][1024], Po = the pooled bins the head reads),
+ * 19 RoI-head output (dtype NHWC), 20 pooled head features (dtype [R][feat]),
+ * 21 class logits (dtype [R][ncls_pad]), 22 box regression (dtype [R][4*(ncls) padded]).
  * Returns bytes in *bytes. */
 int sdb_det_export(sdb_det* det, int what, void* host, int64_t capacity, int64_t* bytes);
 int sdb_det_dims(sdb_det* det, int* feat_h, int* feat_w, int* n_anchor_per_loc, int* a_pad);

@@ -1766,6 +1766,11 @@ int sdb_det_export(sdb_det* d, int what, void* host, int64_t cap, int64_t* bytes
         case 15: src = d->stem_x2; n = d->stem_x2 ? static_cast<int64_t>(d->stem2.g.W) * 192 * 2 : 0; break;
         case 16: src = d->wdev; n = d->n_w * d->es; break;
         case 17: src = d->w32; n = d->n_w * 4; break;
+        case 18: src = d->roi_feat.p; n = d->roi_feat.numel() * d->es; break;
+        case 19: src = d->head_out.p; n = d->head_out.numel() * d->es; break;
+        case 20: src = d->pooled.p; n = d->pooled.numel() * d->es; break;
+        case 21: src = d->cls_logits.p; n = d->cls_logits.numel() * d->es; break;
+        case 22: src = d->bbox_pred.p; n = d->bbox_pred.numel() * d->es; break;
         case 12: {
             cudaStreamSynchronize(d->ctx->stream);
             cudaMemcpy(&tmp_state[0], d->scale, 8, cudaMemcpyDeviceToHost);

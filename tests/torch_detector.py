@@ -149,11 +149,14 @@ class TorchDetector:
         rois_t = T(rois)
         f = self.q(roi_align(c4, rois_t, output_size=self.pool, spatial_scale=1.0 / 16.0, sampling_ratio=self.sr,
                              aligned=True))
+        self.roi_feat = f
         if self.blocks[3] > 0:
             f = self.stage(f, "res5", self.blocks[3], 2)
         pooled = self.q(f.mean(dim=(2, 3)))
         cls = self.q(pooled @ self.p["fc.cls"])
         box = self.q(pooled @ self.p["fc.bbox"])
+        self.inter = {"c4": c4.detach(), "roi_feat": self.roi_feat.detach(), "head_out": f.detach(),
+                      "pooled": pooled.detach(), "cls": cls.detach(), "box": box.detach()}
         rl = torch.as_tensor(np.ascontiguousarray(roi_labels)).to(dev).long()
         rv = rl >= 0
         l3 = F.cross_entropy(cls[rv], rl[rv], reduction="mean")
@@ -180,13 +183,17 @@ def gpu_params(det) -> dict:
     return {det.params[i][0]: det.get_param(i) for i in range(det.n_tensors)}
 
 
-def run_checker(det, params, s, mode, grad_scale, device, dtype=torch.float32):
+def run_checker(det, params, s, mode, grad_scale, device, dtype=torch.float32, inter=None):
     """teacher-forced TorchDetector step on the GPU step's decisions `s`
-    (tests.det_parity.gpu_state); returns (losses, flat grads in pack order, logits)"""
+    (tests.det_parity.gpu_state); returns (losses, flat grads in pack order, logits);
+    `inter` (a dict) receives the forward intermediates (c4, roi_feat, head_out,
+    pooled, cls, box) as numpy arrays"""
     pr = det.p
     img = np.ascontiguousarray(s["images"][..., :3].astype(np.float32).transpose(0, 3, 1, 2))
     td = TorchDetector(params, mode, pr.blocks, det.A, pr.pool, device=device, dtype=dtype)
     losses, grads, lg = td.step(img, s["a_labels"], s["a_targets"], s["rois"], s["roi_labels"], s["roi_targets"],
                                 grad_scale)
     flat = np.concatenate([grads[det.params[i][0]].ravel() for i in range(det.n_tensors)]).astype(np.float32)
+    if inter is not None:
+        inter.update({k: v.float().cpu().numpy() for k, v in td.inter.items()})
     return losses, flat, lg

@@ -28,7 +28,27 @@ det.step()
 losses, scale, ov = det.losses()
 s = dp.gpu_state(det)
 g = dp.flat_grads(det)
-l32, g32, _ = run_checker(det, params, s, 2, scale, "cuda")
+i32 = {}
+l32, g32, _ = run_checker(det, params, s, 2, scale, "cuda", inter=i32)
+# forward intermediates: GPU exports vs the fp32 checker
+pr = det.p
+R = s["rois"].shape[0]
+dt = np.float16 if mode == 1 else np.float32
+gpu_i = {"c4": det.export(10, dt).reshape(pr.batch, det.feat_h, det.feat_w, 1024).transpose(0, 3, 1, 2),
+         "roi_feat": det.export(18, dt).reshape(R, 7, 7, 1024).transpose(0, 3, 1, 2),
+         "head_out": det.export(19, dt).reshape(R, 7, 7, 2048).transpose(0, 3, 1, 2),
+         "pooled": det.export(20, dt).reshape(R, 2048),
+         "cls": det.export(21, dt).reshape(R, -1)[:, :81],
+         "box": det.export(22, dt).reshape(R, -1)[:, :324]}
+ref_i = dict(i32)
+ref_i["roi_feat"] = i32["roi_feat"][:, :, ::2, ::2]
+for k in gpu_i:
+    a, b = gpu_i[k].astype(np.float32), ref_i[k]
+    print("inter %-9s norm-rel %.3e  max-abs %.3e  ref-max %.3e" % (k, norm_rel(a, b), np.abs(a - b).max(), np.abs(b).max()))
+rl = s["roi_labels"]
+ce_rows = [(i, float(v)) for i, v in enumerate(np.abs(gpu_i["cls"].astype(np.float32) - ref_i["cls"]).max(1))]
+ce_rows.sort(key=lambda t: -t[1])
+print("worst cls rows:", ce_rows[:8], "labels", [int(rl[i]) for i, _ in ce_rows[:8]])
 torch.cuda.empty_cache()
 l64, g64, _ = run_checker(det, params, s, 2, scale, "cuda", dtype=torch.float64)
 torch.cuda.empty_cache()
