@@ -160,6 +160,13 @@ class TorchDetector:
         rl = torch.as_tensor(np.ascontiguousarray(roi_labels)).to(dev).long()
         rv = rl >= 0
         l3 = F.cross_entropy(cls[rv], rl[rv], reduction="mean")
+        # the reported value follows the reference CE op (src/model.cpp:117-134):
+        # probabilities stashed as float, loss = mean(-log(max(1e-30, p_y))) --
+        # a row whose p_y underflows float contributes 69.08, not its true
+        # -log p_y (logits reach ~100 at C4); the backward is (p - onehot) as here
+        with torch.no_grad():
+            p_y = torch.softmax(cls[rv].double(), 1).float().gather(1, rl[rv][:, None]).squeeze(1).double()
+            l3_value = (-torch.log(torch.clamp(p_y, min=1e-30))).mean()
         R = int(rv.sum())
         rfg = (rl > 0).nonzero().squeeze(1)
         sel = box[rfg.unsqueeze(1), (4 * rl[rfg]).unsqueeze(1) + torch.arange(4, device=dev)]
@@ -174,7 +181,7 @@ class TorchDetector:
             if self.mode == 1 and not (k.endswith(".gamma") or k.endswith(".beta")):
                 g = g.half().float()  # leaf dtype F16 (src/autograd.cpp:481)
             grads[k] = g.detach().float().cpu().numpy()
-        losses = np.array([float(v.detach()) for v in (l1, l2, l3, l4)], np.float64)
+        losses = np.array([float(v.detach()) for v in (l1, l2, l3_value, l4)], np.float64)
         return losses, grads, logits.detach().float().cpu().numpy()
 
 

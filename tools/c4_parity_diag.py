@@ -48,6 +48,14 @@ for k in gpu_i:
 rl = s["roi_labels"]
 ce_rows = [(i, float(v)) for i, v in enumerate(np.abs(gpu_i["cls"].astype(np.float32) - ref_i["cls"]).max(1))]
 ce_rows.sort(key=lambda t: -t[1])
+def _ce(lg, lab):
+    lg = lg.astype(np.float64)
+    m = lg.max(1)
+    lse = m + np.log(np.exp(lg - m[:, None]).sum(1))
+    return lse - lg[np.arange(lg.shape[0]), lab]
+ce_g, ce_r = _ce(gpu_i["cls"], rl), _ce(ref_i["cls"], rl)
+print("CE on exported GPU logits %.6f, on checker logits %.6f; largest per-row diffs" % (ce_g.mean(), ce_r.mean()),
+      sorted(zip(np.abs(ce_g - ce_r), range(len(rl))))[-5:])
 print("worst cls rows:", ce_rows[:8], "labels", [int(rl[i]) for i, _ in ce_rows[:8]])
 torch.cuda.empty_cache()
 l64, g64, _ = run_checker(det, params, s, 2, scale, "cuda", dtype=torch.float64)
