@@ -164,6 +164,16 @@ int sdb_roialign_fwd(sdb_ctx* ctx, int dtype, const void* feat, int N, int H, in
                      int P, float spatial_scale, int sampling_ratio, void* out, void* stream);
 int sdb_roialign_bwd(sdb_ctx* ctx, int dtype, const void* dy, int N, int H, int W, int C, const float* rois, int R,
                      int P, float spatial_scale, int sampling_ratio, void* dfeat, void* stream);
+/* the same with the bin subsampling of the training step folded in: only every
+ * bin_step-th bin of the P x P grid is pooled (out/dy [R][Po][Po][C], Po =
+ * ceil(P / bin_step)) -- exactly the values a following 1x1 stride-bin_step
+ * convolution reads (the res5 entry block of the C4 head) */
+int sdb_roialign_fwd_folded(sdb_ctx* ctx, int dtype, const void* feat, int N, int H, int W, int C, const float* rois,
+                            int R, int P, float spatial_scale, int sampling_ratio, int bin_step, void* out,
+                            void* stream);
+int sdb_roialign_bwd_folded(sdb_ctx* ctx, int dtype, const void* dy, int N, int H, int W, int C, const float* rois,
+                            int R, int P, float spatial_scale, int sampling_ratio, int bin_step, void* dfeat,
+                            void* stream);
 /* softmax cross-entropy, the reference CE op (src/model.cpp:101-151): mean over
  * rows with label >= 0, backward scaled by *grad_scale (device double or NULL).
  * logits/dlogits [R][ld] (first ncls columns valid); loss written to *loss. */

@@ -395,6 +395,32 @@ int sdb_roialign_bwd(sdb_ctx* ctx, int dtype, const void* dy, int N, int H, int 
                        "roialign_bwd");
 }
 
+int sdb_roialign_fwd_folded(sdb_ctx* ctx, int dtype, const void* feat, int N, int H, int W, int C, const float* rois,
+                            int R, int P, float spatial_scale, int sampling_ratio, int bin_step, void* out,
+                            void* stream) {
+    if (int rc = check_dtype(dtype)) return rc;
+    if (C % 8 || P < 1 || sampling_ratio < 1 || R < 0 || bin_step < 1)
+        return fail(SDB_UNSUPPORTED, "roialign: C % 8, P, ratio, bin_step");
+    return cuda_status(sdb::roialign_fwd(dtype, feat, N, H, W, C, rois, R, P, spatial_scale, sampling_ratio, out,
+                                         pick(ctx, stream), bin_step),
+                       "roialign_fwd");
+}
+
+int sdb_roialign_bwd_folded(sdb_ctx* ctx, int dtype, const void* dy, int N, int H, int W, int C, const float* rois,
+                            int R, int P, float spatial_scale, int sampling_ratio, int bin_step, void* dfeat,
+                            void* stream) {
+    if (int rc = check_dtype(dtype)) return rc;
+    if (!ctx) return fail(SDB_PARAM, "roialign_bwd needs a context (workspace)");
+    if (C % 8 || P < 1 || bin_step < 1 || (P + bin_step - 1) / bin_step > 16 || sampling_ratio < 1 || R < 0)
+        return fail(SDB_UNSUPPORTED, "roialign: C % 8, pooled bins <= 16, ratio, bin_step");
+    const size_t wsb = sdb::roialign_bwd_workspace(R, H, W, P, bin_step);
+    void* ws = ctx->scratch(wsb);
+    if (!ws) return fail(SDB_CUDA, "workspace allocation failed");
+    return cuda_status(sdb::roialign_bwd(dtype, dy, N, H, W, C, rois, R, P, spatial_scale, sampling_ratio, dfeat, ws,
+                                         wsb, pick(ctx, stream), bin_step),
+                       "roialign_bwd");
+}
+
 int sdb_softmax_ce(sdb_ctx* ctx, int dtype, const void* logits, int R, int ncls, int ld, const int32_t* labels,
                    const double* grad_scale, double* loss, void* dlogits, void* stream) {
     if (int rc = check_dtype(dtype)) return rc;

@@ -60,6 +60,8 @@ _SIGS = {
     "sdb_proposal_targets": [_P, _P, _I, _P, _P, _P, _I, _P, _I, _P, _D, _D, _D, _I, _D, _P, _P, _P, _P, _P],
     "sdb_allreduce_sum": [_P, _I, _P, _L, _P],
     "sdb_comm_check": [_P],
+    "sdb_roialign_fwd_folded": [_P, _I, _P, _I, _I, _I, _I, _P, _I, _I, _F, _I, _I, _P, _P],
+    "sdb_roialign_bwd_folded": [_P, _I, _P, _I, _I, _I, _I, _P, _I, _I, _F, _I, _I, _P, _P],
 }
 
 _configured = False
