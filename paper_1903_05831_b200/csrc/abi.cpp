@@ -387,7 +387,7 @@ int sdb_roialign_bwd(sdb_ctx* ctx, int dtype, const void* dy, int N, int H, int 
     if (C % 8 || P < 1 || P > 16 || sampling_ratio < 1 || R < 0)
         return fail(SDB_UNSUPPORTED, "roialign: C % 8, P <= 16, ratio");
     if (!ctx) return fail(SDB_PARAM, "roialign_bwd needs a context (workspace)");
-    const size_t wsb = sdb::roialign_bwd_workspace(R, H, W, P);
+    const size_t wsb = sdb::roialign_bwd_workspace(R, H, W, P, 1, N);
     void* ws = ctx->scratch(wsb);
     if (!ws) return fail(SDB_CUDA, "workspace allocation failed");
     return cuda_status(sdb::roialign_bwd(dtype, dy, N, H, W, C, rois, R, P, spatial_scale, sampling_ratio, dfeat, ws,
@@ -413,7 +413,7 @@ int sdb_roialign_bwd_folded(sdb_ctx* ctx, int dtype, const void* dy, int N, int 
     if (!ctx) return fail(SDB_PARAM, "roialign_bwd needs a context (workspace)");
     if (C % 8 || P < 1 || bin_step < 1 || (P + bin_step - 1) / bin_step > 16 || sampling_ratio < 1 || R < 0)
         return fail(SDB_UNSUPPORTED, "roialign: C % 8, pooled bins <= 16, ratio, bin_step");
-    const size_t wsb = sdb::roialign_bwd_workspace(R, H, W, P, bin_step);
+    const size_t wsb = sdb::roialign_bwd_workspace(R, H, W, P, bin_step, N);
     void* ws = ctx->scratch(wsb);
     if (!ws) return fail(SDB_CUDA, "workspace allocation failed");
     return cuda_status(sdb::roialign_bwd(dtype, dy, N, H, W, C, rois, R, P, spatial_scale, sampling_ratio, dfeat, ws,

@@ -93,8 +93,8 @@ cudaError_t proposal_targets(const ProposalTargetArgs& a, cudaStream_t st);
 // convolution reads, so the stride folds into the pooling.
 cudaError_t roialign_fwd(int dtype, const void* feat, int N, int H, int W, int C, const float* rois, int R, int P,
                          float scale, int sr, void* out, cudaStream_t st, int step = 1);
-// backward workspace: per-RoI separable weight tables + boxes (roialign_bwd_workspace bytes)
-size_t roialign_bwd_workspace(int R, int H, int W, int P, int step = 1);
+// backward workspace: per-RoI separable weight tables, boxes and per-pixel-block RoI lists
+size_t roialign_bwd_workspace(int R, int H, int W, int P, int step = 1, int N = 1);
 cudaError_t roialign_bwd(int dtype, const void* dy, int N, int H, int W, int C, const float* rois, int R, int P,
                          float scale, int sr, void* dfeat, void* ws, size_t ws_bytes, cudaStream_t st, int step = 1);
 // [n][3][H][W] (the reference image layout) -> NHWC with Cp channels (zero padded)

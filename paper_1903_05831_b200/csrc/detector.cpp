@@ -476,7 +476,7 @@ size_t max_ws(sdb_det* d) {
     conv_ws(d->rpn_conv); conv_ws(d->rpn_cls); conv_ws(d->rpn_bbox); conv_ws(d->fc_cls); conv_ws(d->fc_bbox);
     m = std::max(m, proposal_workspace_bytes(d->cfg.batch, d->nA, d->cfg.pre_nms));
     m = std::max(m, anchor_target_workspace_bytes(d->cfg.batch, d->nA, d->cfg.max_gt));
-    m = std::max(m, roialign_bwd_workspace(d->R, d->fh, d->fw, d->P, d->roi_step));
+    m = std::max(m, roialign_bwd_workspace(d->R, d->fh, d->fw, d->P, d->roi_step, d->cfg.batch));
     return m;
 }
 

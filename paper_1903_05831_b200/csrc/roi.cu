@@ -17,6 +17,7 @@
 // Compiled with -fmad=false (no contraction) so float expressions evaluate
 // as written in the oracle.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "detect.h"
@@ -155,58 +156,88 @@ __global__ void roialign_fwd_kernel(const T* __restrict__ feat, int H, int W, in
 
 // ---------------------------------------------------------------- RoIAlign fwd (smem-staged)
 // One CTA per (image, 8-channel slab): the slab of the image's whole feature
-// map (H*W pixels x 16 B fp16 / 32 B fp32) is staged in shared memory once, so
-// the 16 bilinear corner reads of every output bin hit smem instead of L2 (the
-// RoIs of an image overlap heavily: at C4 every feature pixel is read by ~100
-// RoI samples; through L2 that read amplification capped the direct kernel at
-// ~1.6 GB of L2 traffic per step).  The image's RoIs are taken in chunks of
-// kRaChunk: the separable sample table of a chunk -- per (RoI, axis, bin,
-// sample): low/high pixel and their bilinear weights, zero weights for
-// samples outside [-1, H] -- is built once in smem, then every (RoI, bin)
-// item of the chunk reads it and blends its 16 corners with packed fp32 FMAs
-// (fma.rn.f32x2).  Same sample positions, clamps and corner weights as the
-// direct kernel above.
+// map is staged in shared memory once (16 B per pixel in fp16), so the 16
+// bilinear corner reads of every output bin
+// hit smem instead of L2 (the RoIs of an image overlap heavily: at C4 every
+// feature pixel is read by ~100 RoI samples; through L2 that read
+// amplification capped the direct kernel at ~1.6 GB of L2 traffic per step).
+// The image's RoIs are taken in chunks of kRaChunk: the separable sample
+// table of a chunk -- per (RoI, axis, bin, sample): element offsets of the
+// low/high pixel row (y) or column (x) and their bilinear weights, zero
+// weights for samples outside [-1, H] -- is built once in smem, then every
+// (RoI, bin) item of the chunk reads it and blends its 16 corners with packed
+// fp32 FMAs (fma.rn.f32x2).  Same sample positions, clamps and corner weights
+// as the direct kernel above.
 constexpr int kRaChunk = 32;
 constexpr int kRaFwdThreads = 512;
 
 struct RaTab {
-    int lo, hi;
+    int lo, hi;  // element offsets into the staged slab (row * W * 8 for y, col * 8 for x)
     float wl, wh;
 };
 
-SDB_DEV RaTab ra_axis(float v, int lim) {
+SDB_DEV RaTab ra_axis(float v, int lim, int mult) {
     RaTab t{0, 0, 0.f, 0.f};
     if (v < -1.0f || v > static_cast<float>(lim)) return t;
     if (v <= 0.f) v = 0.f;
     int lo = static_cast<int>(v), hi;
     if (lo >= lim - 1) { hi = lo = lim - 1; v = static_cast<float>(lo); } else hi = lo + 1;
-    t.lo = lo;
-    t.hi = hi;
+    t.lo = lo * mult;
+    t.hi = hi * mult;
     t.wh = v - static_cast<float>(lo);
     t.wl = 1.f - t.wh;
     return t;
 }
 
-template <class T>
+// one bin: the SR x SR samples' 16 corners blended with packed fp32 FMAs
+// (compile-time SR: all corner loads of the bin are issued back to back)
+template <class T, int SR>
+SDB_DEV void ra_bin(const T* f, const RaTab* ty, const RaTab* tx, int sr, float2 (&acc)[4]) {
+    const int n = SR > 0 ? SR : sr;
+#pragma unroll
+    for (int iy = 0; iy < (SR > 0 ? SR : 1); ++iy) {
+        for (int iy2 = iy; iy2 < (SR > 0 ? iy + 1 : n); ++iy2) {
+            const RaTab Y = ty[iy2];
+#pragma unroll
+            for (int ix = 0; ix < (SR > 0 ? SR : 1); ++ix) {
+                for (int ix2 = ix; ix2 < (SR > 0 ? ix + 1 : n); ++ix2) {
+                    const RaTab X = tx[ix2];
+                    const float2 w1 = make_float2(Y.wl * X.wl, Y.wl * X.wl), w2 = make_float2(Y.wl * X.wh, Y.wl * X.wh);
+                    const float2 w3 = make_float2(Y.wh * X.wl, Y.wh * X.wl), w4 = make_float2(Y.wh * X.wh, Y.wh * X.wh);
+                    float2 v1[4], v2[4], v3[4], v4[4];
+                    ld8x2<T>(f + Y.lo + X.lo, v1);
+                    ld8x2<T>(f + Y.lo + X.hi, v2);
+                    ld8x2<T>(f + Y.hi + X.lo, v3);
+                    ld8x2<T>(f + Y.hi + X.hi, v4);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        acc[k] = ffma2(w4, v4[k], ffma2(w3, v3[k], ffma2(w2, v2[k], ffma2(w1, v1[k], acc[k]))));
+                }
+            }
+        }
+    }
+}
+
+template <class T, int SR>
 __global__ void __launch_bounds__(kRaFwdThreads) roialign_fwd_smem_kernel(const T* __restrict__ feat, int H, int W,
                                                                           int C, const float* __restrict__ rois, int R,
                                                                           int P, float scale, int sr, int step,
                                                                           T* __restrict__ out) {
     extern __shared__ __align__(16) unsigned char ra_smem[];
-    constexpr int kChunk = 8 * sizeof(T);  // bytes of one pixel's 8 channels
     const int n = blockIdx.y, c8 = blockIdx.x;
     const int HW = H * W;
     const int Po = (P + step - 1) / step, PP = Po * Po;
-    int* list = reinterpret_cast<int*>(ra_smem + static_cast<size_t>(HW) * kChunk);
+    T* fs = reinterpret_cast<T*>(ra_smem);  // [HW][8]
+    int* list = reinterpret_cast<int*>(ra_smem + static_cast<size_t>(HW) * 8 * sizeof(T));
     RaTab* tab = reinterpret_cast<RaTab*>(list + ((R + 3) & ~3));  // [kRaChunk][2][Po][sr]
     __shared__ int cnt;
     if (threadIdx.x == 0) cnt = 0;
     const T* src = feat + static_cast<int64_t>(n) * HW * C + c8 * 8;
     for (int p = threadIdx.x; p < HW; p += blockDim.x) {
         const uint4* s = reinterpret_cast<const uint4*>(src + static_cast<int64_t>(p) * C);
-        uint4* d = reinterpret_cast<uint4*>(ra_smem + static_cast<size_t>(p) * kChunk);
+        uint4* d = reinterpret_cast<uint4*>(fs + static_cast<size_t>(p) * 8);
         d[0] = __ldg(s);
-        if (kChunk == 32) d[1] = __ldg(s + 1);
+        if (sizeof(T) == 4) d[1] = __ldg(s + 1);
     }
     __syncthreads();
     // this image's RoIs (order irrelevant: every output bin is written by one thread)
@@ -216,7 +247,6 @@ __global__ void __launch_bounds__(kRaFwdThreads) roialign_fwd_smem_kernel(const 
     const int total = cnt;
     const float inv_count = 1.0f / static_cast<float>(max(sr * sr, 1));
     const float2 ic = make_float2(inv_count, inv_count);
-    const T* f = reinterpret_cast<const T*>(ra_smem);
     const int per_roi = 2 * Po * sr;
     for (int r0 = 0; r0 < total; r0 += kRaChunk) {
         const int nr = min(kRaChunk, total - r0);
@@ -225,32 +255,15 @@ __global__ void __launch_bounds__(kRaFwdThreads) roialign_fwd_smem_kernel(const 
             const int axis = q / (Po * sr), q2 = q - axis * Po * sr;
             const int pb = q2 / sr, is = q2 - pb * sr;
             const Geom g = roi_geom(rois + static_cast<int64_t>(list[r0 + j]) * 5, P, scale);
-            tab[t] = axis ? ra_axis(sample_coord(g.sw, pb * step, g.bw, is, sr), W)
-                          : ra_axis(sample_coord(g.sh, pb * step, g.bh, is, sr), H);
+            tab[t] = axis ? ra_axis(sample_coord(g.sw, pb * step, g.bw, is, sr), W, 8)
+                          : ra_axis(sample_coord(g.sh, pb * step, g.bh, is, sr), H, W * 8);
         }
         __syncthreads();
         for (int e = threadIdx.x; e < nr * PP; e += blockDim.x) {
             const int j = e / PP, bin = e - j * PP;
             const int ph = bin / Po, pw = bin - ph * Po;
-            const RaTab* ty = tab + j * per_roi + ph * sr;
-            const RaTab* tx = tab + j * per_roi + Po * sr + pw * sr;
             float2 acc[4] = {};
-            for (int iy = 0; iy < sr; ++iy) {
-                const RaTab Y = ty[iy];
-                for (int ix = 0; ix < sr; ++ix) {
-                    const RaTab X = tx[ix];
-                    const float2 w1 = make_float2(Y.wl * X.wl, Y.wl * X.wl), w2 = make_float2(Y.wl * X.wh, Y.wl * X.wh);
-                    const float2 w3 = make_float2(Y.wh * X.wl, Y.wh * X.wl), w4 = make_float2(Y.wh * X.wh, Y.wh * X.wh);
-                    float2 v1[4], v2[4], v3[4], v4[4];
-                    ld8x2<T>(f + (Y.lo * W + X.lo) * 8, v1);
-                    ld8x2<T>(f + (Y.lo * W + X.hi) * 8, v2);
-                    ld8x2<T>(f + (Y.hi * W + X.lo) * 8, v3);
-                    ld8x2<T>(f + (Y.hi * W + X.hi) * 8, v4);
-#pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        acc[k] = ffma2(w4, v4[k], ffma2(w3, v3[k], ffma2(w2, v2[k], ffma2(w1, v1[k], acc[k]))));
-                }
-            }
+            ra_bin<T, SR>(fs, tab + j * per_roi + ph * sr, tab + j * per_roi + Po * sr + pw * sr, sr, acc);
 #pragma unroll
             for (int k = 0; k < 4; ++k) acc[k] = ffma2(acc[k], ic, make_float2(0.f, 0.f));
             st8x2<T>(out + (static_cast<int64_t>(list[r0 + j]) * PP + bin) * C + c8 * 8, acc);
@@ -270,11 +283,9 @@ __global__ void __launch_bounds__(kRaFwdThreads) roialign_fwd_smem_kernel(const 
 //   2. roialign_bwd_gather_kernel: one warp per (pixel, 256*V-channel slab),
 //      lane = V 8-channel chunks; it walks the RoIs whose box holds its pixel
 //      (ballot over the box table, index order), fetches the RoI's 2 x pw
-//      weights of its row and column in one load per lane, appends the
-//      nonzero bin pairs to a per-warp smem list and consumes the list
-//      kRaBatch dY rows at a time (all loads in flight, then the FMAs in list
-//      order).  No block-level barriers; a CTA is a 4x4 pixel block, so the
-//      dY rows its pixels share hit L1.
+//      weights of its row and column in one load per lane, and accumulates
+//      the nonzero bin pairs in registers.  No shared memory and no barriers;
+//      a CTA is a 4x4 pixel block, so the dY rows its pixels share hit L1.
 // The summation order per output element is fixed (RoI, ph, pw) -- bitwise
 // reproducible run to run; products are accumulated with packed fp32 FMAs.
 constexpr int kRaBlk = 4;  // CTA = kRaBlk x kRaBlk pixels (one warp each)
@@ -333,65 +344,23 @@ __global__ void __launch_bounds__(256) roialign_bwd_weights_kernel(const float* 
     }
 }
 
-constexpr int kRaList = 256;  // per-warp pair list (>= Po*Po for Po <= 16)
-constexpr int kRaBatch = 4;   // dY rows in flight per lane
-
 template <class T, int V>
 __global__ void __launch_bounds__(kRaBlk * kRaBlk * 32) roialign_bwd_gather_kernel(
     const T* __restrict__ dy, int H, int W, int C, const int4* __restrict__ box, const float* __restrict__ tab, int R,
     int Po, int pw, float inv_count, T* __restrict__ dfeat) {
-    // per warp: the (dY row, weight) pairs of its pixel, appended in (RoI, ph,
-    // pw) order, then consumed kRaBatch rows at a time (loads first, FMAs in
-    // list order): the dependent load -> FMA chain of a pair-at-a-time loop
-    // left the kernel stalled on long scoreboard
-    __shared__ int2 lst[kRaBlk * kRaBlk][kRaList];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int bxn = (W + kRaBlk - 1) / kRaBlk;
     const int y = (blockIdx.x / bxn) * kRaBlk + warp / kRaBlk;
     const int x = (blockIdx.x % bxn) * kRaBlk + warp % kRaBlk;
     const int n = blockIdx.z;
     const int c0 = blockIdx.y * 256 * V + lane * 8;
-    if (y >= H || x >= W) return;  // whole warp: no block-level barriers below
-    int2* L = lst[warp];
+    if (y >= H || x >= W) return;  // whole warp: no barriers below
     float2 acc[V][4];
 #pragma unroll
     for (int v = 0; v < V; ++v)
 #pragma unroll
         for (int k = 0; k < 4; ++k) acc[v][k] = make_float2(0.f, 0.f);
-    int cnt = 0;
-    auto consume = [&]() {
-        __syncwarp();
-        for (int k = 0; k < cnt; k += kRaBatch) {
-            float2 val[kRaBatch][V][4];
-            float wq[kRaBatch];
-#pragma unroll
-            for (int q = 0; q < kRaBatch; ++q) {
-                const bool ok = k + q < cnt;
-                const int2 e = ok ? L[k + q] : make_int2(0, 0);
-                wq[q] = ok ? __int_as_float(e.y) : 0.f;
-                const T* d = dy + static_cast<int64_t>(e.x) * C + c0;
-#pragma unroll
-                for (int v = 0; v < V; ++v) {
-                    if (ok && c0 + v * 256 < C) ld8x2<T>(d + v * 256, val[q][v]);
-                    else
-#pragma unroll
-                        for (int kk = 0; kk < 4; ++kk) val[q][v][kk] = make_float2(0.f, 0.f);
-                }
-            }
-#pragma unroll
-            for (int q = 0; q < kRaBatch; ++q) {
-                if (k + q >= cnt) break;
-                const float2 w2 = make_float2(wq[q], wq[q]);
-#pragma unroll
-                for (int v = 0; v < V; ++v)
-#pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) acc[v][kk] = ffma2(w2, val[q][v][kk], acc[v][kk]);
-            }
-        }
-        __syncwarp();
-        cnt = 0;
-    };
-    const int PP = Po * Po;
+    const int64_t row_stride = static_cast<int64_t>(Po) * C;
     for (int r0 = 0; r0 < R; r0 += 32) {
         bool hit = false;
         if (r0 + lane < R) {
@@ -405,24 +374,28 @@ __global__ void __launch_bounds__(kRaBlk * kRaBlk * 32) roialign_bwd_gather_kern
             if (lane < pw) w = __ldg(trow + y * pw + lane);
             else if (lane >= 16 && lane < 16 + pw) w = __ldg(trow + (H + x) * pw + (lane - 16));
             const unsigned nz = __ballot_sync(0xffffffffu, w != 0.f);
-            const unsigned my = nz & 0xffffu, mx = nz >> 16;
-            const int ny = __popc(my), nx = __popc(mx), np = ny * nx;
-            if (np == 0) continue;
-            if (cnt + np > kRaList) consume();
-            for (int base = 0; base < np; base += 32) {
-                const int i = base + lane;
-                const bool ok = i < np;
-                const int a = ok ? i / nx : 0, bb = ok ? i - a * nx : 0;
-                const int ph = ok ? static_cast<int>(__fns(my, 0, a + 1)) : 0;
-                const int pwi = ok ? static_cast<int>(__fns(mx, 0, bb + 1)) : 0;
+            const T* d = dy + static_cast<int64_t>(r) * Po * row_stride + c0;
+            for (unsigned a = nz & 0xffffu; a; a &= a - 1) {
+                const int ph = __ffs(a) - 1;
                 const float wy = __shfl_sync(0xffffffffu, w, ph);
-                const float wx = __shfl_sync(0xffffffffu, w, 16 + pwi);
-                if (ok) L[cnt + i] = make_int2(r * PP + ph * Po + pwi, __float_as_int(wy * wx * inv_count));
+                for (unsigned b2 = nz >> 16; b2; b2 &= b2 - 1) {
+                    const int pwi = __ffs(b2) - 1;
+                    const float wx = __shfl_sync(0xffffffffu, w, 16 + pwi);
+                    const float wgt = wy * wx * inv_count;
+                    const float2 w2 = make_float2(wgt, wgt);
+                    const T* dd = d + ph * row_stride + static_cast<int64_t>(pwi) * C;
+#pragma unroll
+                    for (int v = 0; v < V; ++v) {
+                        if (c0 + v * 256 >= C) break;
+                        float2 val[4];
+                        ld8x2<T>(dd + v * 256, val);
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) acc[v][k] = ffma2(w2, val[k], acc[v][k]);
+                    }
+                }
             }
-            cnt += np;
         }
     }
-    consume();
 #pragma unroll
     for (int v = 0; v < V; ++v)
         if (c0 + v * 256 < C) st8x2<T>(dfeat + ((static_cast<int64_t>(n) * H + y) * W + x) * C + c0 + v * 256, acc[v]);
@@ -987,6 +960,14 @@ static size_t ra_fwd_smem(int H, int W, int R, int Po, int sr, int dtype) {
            static_cast<size_t>(kRaChunk) * 2 * Po * sr * sizeof(RaTab);
 }
 
+template <class T, int SR>
+static void ra_fwd_launch(dim3 grid, size_t smem, const void* feat, int H, int W, int C, const float* rois, int R,
+                          int P, float scale, int sr, int step, void* out, cudaStream_t st) {
+    auto k = roialign_fwd_smem_kernel<T, SR>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    k<<<grid, kRaFwdThreads, smem, st>>>(cp<T>(feat), H, W, C, rois, R, P, scale, sr, step, static_cast<T*>(out));
+}
+
 cudaError_t roialign_fwd(int dtype, const void* feat, int N, int H, int W, int C, const float* rois, int R, int P,
                          float scale, int sr, void* out, cudaStream_t st, int step) {
     if (step < 1) return cudaErrorInvalidValue;
@@ -995,17 +976,13 @@ cudaError_t roialign_fwd(int dtype, const void* feat, int N, int H, int W, int C
     const size_t smem = ra_fwd_smem(H, W, R, Po, sr, dtype);
     if (smem <= 200 * 1024 && sr <= 8) {
         const dim3 grid(C / 8, N);
-        if (dtype == kF16) {
-            auto k = roialign_fwd_smem_kernel<__half>;
-            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-            k<<<grid, kRaFwdThreads, smem, st>>>(cp<__half>(feat), H, W, C, rois, R, P, scale, sr, step,
-                                                static_cast<__half*>(out));
-        } else {
-            auto k = roialign_fwd_smem_kernel<float>;
-            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-            k<<<grid, kRaFwdThreads, smem, st>>>(cp<float>(feat), H, W, C, rois, R, P, scale, sr, step,
-                                                static_cast<float*>(out));
-        }
+        const bool h = dtype == kF16;
+        if (sr == 2)
+            h ? ra_fwd_launch<__half, 2>(grid, smem, feat, H, W, C, rois, R, P, scale, sr, step, out, st)
+              : ra_fwd_launch<float, 2>(grid, smem, feat, H, W, C, rois, R, P, scale, sr, step, out, st);
+        else
+            h ? ra_fwd_launch<__half, 0>(grid, smem, feat, H, W, C, rois, R, P, scale, sr, step, out, st)
+              : ra_fwd_launch<float, 0>(grid, smem, feat, H, W, C, rois, R, P, scale, sr, step, out, st);
         return cudaGetLastError();
     }
     // feature maps too large to stage: one thread per (RoI, bin, 8 channels) through L2
@@ -1021,7 +998,7 @@ cudaError_t roialign_fwd(int dtype, const void* feat, int N, int H, int W, int C
 
 static int ra_table_width(int P, int step) { return (P + step - 1) / step <= 8 ? 8 : 16; }
 
-size_t roialign_bwd_workspace(int R, int H, int W, int P, int step) {
+size_t roialign_bwd_workspace(int R, int H, int W, int P, int step, int) {
     if (step < 1) return 0;
     return (static_cast<size_t>(R) * (H + W) * ra_table_width(P, step) * 4 + 255) / 256 * 256 +
            static_cast<size_t>(R) * 16 + 256;
@@ -1045,11 +1022,13 @@ cudaError_t roialign_bwd(int dtype, const void* dy, int N, int H, int W, int C, 
     if (R > 0)
         roialign_bwd_weights_kernel<<<(R + 7) / 8, 256, 0, st>>>(rois, R, H, W, P, scale, sr, step, pw, tab, box);
     // channel slab per warp: 256*V channels (V 8-channel chunks per lane)
-    const int V = C >= 2048 ? 2 : 1;
+    const int V = C >= 2048 ? 4 : (C >= 512 ? 2 : 1);
     const dim3 grid(((H + kRaBlk - 1) / kRaBlk) * ((W + kRaBlk - 1) / kRaBlk), (C + 256 * V - 1) / (256 * V), N);
     const float inv = 1.0f / static_cast<float>(max(sr * sr, 1));
     const bool h = dtype == kF16;
-    if (V == 2) h ? ra_gather<__half, 2>(grid, dy, H, W, C, box, tab, R, Po, pw, inv, dfeat, st)
+    if (V == 4) h ? ra_gather<__half, 4>(grid, dy, H, W, C, box, tab, R, Po, pw, inv, dfeat, st)
+                  : ra_gather<float, 4>(grid, dy, H, W, C, box, tab, R, Po, pw, inv, dfeat, st);
+    else if (V == 2) h ? ra_gather<__half, 2>(grid, dy, H, W, C, box, tab, R, Po, pw, inv, dfeat, st)
                        : ra_gather<float, 2>(grid, dy, H, W, C, box, tab, R, Po, pw, inv, dfeat, st);
     else h ? ra_gather<__half, 1>(grid, dy, H, W, C, box, tab, R, Po, pw, inv, dfeat, st)
            : ra_gather<float, 1>(grid, dy, H, W, C, box, tab, R, Po, pw, inv, dfeat, st);
