@@ -96,6 +96,16 @@ int sdb_conv_dgrad_act(sdb_ctx* ctx, int dtype, const void* dy, const void* w, v
                        const void* y_bits, void* stream);
 int sdb_conv_wgrad(sdb_ctx* ctx, int dtype, const void* x, const void* dy, void* dw, int N, int H, int W, int C, int K,
                    int R, int S, int stride, int pad, void* stream);
+/* conv2d followed by the BN / IABN forward statistics of its output (what the
+ * training step runs before every norm layer): on the tcgen05 TMA-store path
+ * the per-channel fp64 sums are reduced inside the fprop epilogue (no extra
+ * read of y); elsewhere a separate statistics pass runs.  mean/invstd [K] as
+ * syncbn_forward / iabn_forward compute them (src/syncbn.cpp:27-56,
+ * src/memopt.cpp:247-259); iabn selects the IABN variant; *fused (optional)
+ * reports which path ran. */
+int sdb_conv_fprop_stats(sdb_ctx* ctx, int dtype, const void* x, const void* w, void* y, int N, int H, int W, int C,
+                         int K, int R, int S, int stride, int pad, float eps, int iabn, float* mean, float* invstd,
+                         int* fused, void* stream);
 
 /* ---- BatchNorm: syncbn_forward/backward with group == nullptr
  * (src/syncbn.cpp:21-117).  rows = N*H*W; relu=1 fuses the ReLU that follows

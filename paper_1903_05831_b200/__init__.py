@@ -63,6 +63,10 @@ class FormatError(SdbError):
     pass
 
 
+class ConfigError(SdbError):
+    """simdet::ConfigError (errors.hpp:37): raised by the training driver, not the ABI"""
+
+
 _STATUS = {1: ShapeError, 2: ContractError, 3: DegenerateBatchError, 4: NonInvertibleError, 5: ParamError,
            6: CollectiveError, 7: CudaError, 8: UnsupportedError, 9: FormatError}
 

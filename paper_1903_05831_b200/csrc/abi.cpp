@@ -194,6 +194,33 @@ int sdb_conv_dgrad_act(sdb_ctx* ctx, int dtype, const void* dy, const void* w, v
                        "conv_dgrad_act");
 }
 
+int sdb_conv_fprop_stats(sdb_ctx* ctx, int dtype, const void* x, const void* w, void* y, int N, int H, int W, int C,
+                         int K, int R, int S, int stride, int pad, float eps, int iabn, float* mean, float* invstd,
+                         int* fused, void* stream) {
+    if (!ctx) return fail(SDB_PARAM, "conv_fprop_stats needs a context (workspace)");
+    if (int rc = check_dtype(dtype)) return rc;
+    if (int rc = check_conv(N, H, W, C, K, R, S, stride, pad)) return rc;
+    const sdb::ConvShape g{N, H, W, C, K, R, S, stride, pad};
+    const int64_t rows = static_cast<int64_t>(N) * g.Ho() * g.Wo();
+    if (rows < 2) return fail(SDB_DEGENERATE, "batch norm needs at least 2 values per channel");
+    if (!sdb::norm_channels_ok(K)) return fail(SDB_UNSUPPORTED, "norm kernels need C % 8 == 0, C <= 2048, C | 2048");
+    const size_t cap = static_cast<size_t>(2 * 148) * 4 * 2 * 256 * sizeof(double);
+    const size_t nws = sdb::norm_workspace_bytes(rows, K);
+    uint8_t* ws = static_cast<uint8_t*>(ctx->scratch(cap + nws + 256));
+    if (!ws) return fail(SDB_CUDA, "workspace allocation failed");
+    cudaStream_t st = pick(ctx, stream);
+    sdb::ConvStats cs{reinterpret_cast<double*>(ws), cap, 0, 0, 0, 0};
+    if (int rc = cuda_status(sdb::conv_fprop(g, dtype, x, w, y, st, &cs), "conv_fprop")) return rc;
+    if (fused) *fused = cs.produced;
+    const int act = iabn ? 2 : 0;
+    if (cs.produced)
+        return cuda_status(sdb::bn_forward_conv_stats(dtype, y, nullptr, nullptr, nullptr, mean, invstd, rows, K, eps, act,
+                                                      1.0f, cs, st),
+                           "conv stats finalize");
+    return cuda_status(sdb::bn_forward_stats(dtype, y, mean, invstd, rows, K, eps, act, ws + cap + 256, st),
+                       "norm stats");
+}
+
 int sdb_conv_wgrad(sdb_ctx* ctx, int dtype, const void* x, const void* dy, void* dw, int N, int H, int W, int C, int K,
                    int R, int S, int stride, int pad, void* stream) {
     if (!ctx) return fail(SDB_PARAM, "conv_wgrad needs a context (workspace)");

@@ -1449,7 +1449,7 @@ int sdb_det_set_velocity(sdb_det* d, int idx, const float* host) {
 }
 
 // ---- SDCK v1 checkpoints (src/checkpoint.cpp:47-128, little endian)
-int sdb_det_save_checkpoint(sdb_det* d, const char* path, uint64_t config_digest, int64_t step) {
+static int save_checkpoint_impl(sdb_det* d, const char* path, uint64_t config_digest, int64_t step) {
     std::ofstream f(path ? path : "", std::ios::binary);
     if (!f) return det_fail(SDB_FORMAT, "cannot open checkpoint for writing");
     auto bytes = [&](const void* p, size_t n) { f.write(static_cast<const char*>(p), static_cast<std::streamsize>(n)); };
@@ -1500,7 +1500,15 @@ int sdb_det_save_checkpoint(sdb_det* d, const char* path, uint64_t config_digest
     return SDB_OK;
 }
 
-int sdb_det_load_checkpoint(sdb_det* d, const char* path, uint64_t* config_digest, int64_t* step) {
+int sdb_det_save_checkpoint(sdb_det* d, const char* path, uint64_t config_digest, int64_t step) {
+    try {
+        return save_checkpoint_impl(d, path, config_digest, step);
+    } catch (const std::exception& e) {
+        return det_fail(SDB_FORMAT, std::string("checkpoint: ") + e.what());
+    }
+}
+
+static int load_checkpoint_impl(sdb_det* d, const char* path, uint64_t* config_digest, int64_t* step) {
     std::ifstream f(path ? path : "", std::ios::binary);
     if (!f) return det_fail(SDB_FORMAT, "cannot open checkpoint");
     bool ok = true;
@@ -1548,7 +1556,13 @@ int sdb_det_load_checkpoint(sdb_det* d, const char* path, uint64_t* config_diges
     }
     uint64_t nvel = 0;
     pod(nvel);
-    std::vector<float> vel(static_cast<size_t>(ok ? nvel : 0));
+    size_t total = 0;
+    for (const auto& w : ws) total += w.size();
+    // validate before allocating: a corrupt or hostile length must not throw
+    // out of the C ABI (bad_alloc / length_error)
+    if (!ok) return det_fail(SDB_FORMAT, "truncated checkpoint file");
+    if (nvel != total) return det_fail(SDB_FORMAT, "checkpoint velocity length differs from the parameters");
+    std::vector<float> vel(static_cast<size_t>(nvel));
     bytes(vel.data(), vel.size() * sizeof(float));
     double scale = 0.0, growth = 0.0, backoff = 0.0, mn = 0.0, mx = 0.0;
     int64_t good = 0, gi = 0;
@@ -1556,9 +1570,6 @@ int sdb_det_load_checkpoint(sdb_det* d, const char* path, uint64_t* config_diges
     uint32_t nrun = 0;
     pod(scale); pod(good); pod(mode); pod(gi); pod(growth); pod(backoff); pod(mn); pod(mx); pod(nrun);
     if (!ok) return det_fail(SDB_FORMAT, "truncated checkpoint file");
-    size_t total = 0;
-    for (const auto& w : ws) total += w.size();
-    if (vel.size() != total) return det_fail(SDB_FORMAT, "checkpoint velocity length differs from the parameters");
     // running-stat blocks are skipped (IABN keeps none; a BN checkpoint's stats are not step state here)
     for (uint32_t i = 0; i < nrun; ++i) {
         float mom = 0.f;
@@ -1584,6 +1595,16 @@ int sdb_det_load_checkpoint(sdb_det* d, const char* path, uint64_t* config_diges
     if (config_digest) *config_digest = digest;
     if (step) *step = st;
     return SDB_OK;
+}
+
+int sdb_det_load_checkpoint(sdb_det* d, const char* path, uint64_t* config_digest, int64_t* step) {
+    try {
+        return load_checkpoint_impl(d, path, config_digest, step);
+    } catch (const std::bad_alloc&) {
+        return det_fail(SDB_FORMAT, "checkpoint sizes exceed host memory");
+    } catch (const std::exception& e) {
+        return det_fail(SDB_FORMAT, std::string("checkpoint: ") + e.what());
+    }
 }
 
 // next pinned staging slot: waits (host) only for the H2D copies that read it

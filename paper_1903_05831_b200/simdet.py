@@ -60,6 +60,7 @@ _SIGS = {
     "sdb_proposal_targets": [_P, _P, _I, _P, _P, _P, _I, _P, _I, _P, _D, _D, _D, _I, _D, _P, _P, _P, _P, _P],
     "sdb_allreduce_sum": [_P, _I, _P, _L, _P],
     "sdb_comm_check": [_P],
+    "sdb_conv_fprop_stats": [_P, _I, _P, _P, _P] + [_I] * 9 + [_F, _I, _P, _P, _P, _P],
     "sdb_roialign_fwd_folded": [_P, _I, _P, _I, _I, _I, _I, _P, _I, _I, _F, _I, _I, _P, _P],
     "sdb_roialign_bwd_folded": [_P, _I, _P, _I, _I, _I, _I, _P, _I, _I, _F, _I, _I, _P, _P],
 }
@@ -135,6 +136,22 @@ def conv_fprop_nhwc(x, w, stride, pad):
     y = torch.empty((N, max(Ho, 1), max(Wo, 1), K), device=x.device, dtype=x.dtype)
     check(L().sdb_conv_fprop(ctx(), dt(x), ptr(x), ptr(w), ptr(y), N, H, W, Cc, K, R, S, stride, pad, stream()))
     return y
+
+
+def conv_fprop_stats_nhwc(x, w, stride, pad, eps=1e-5, iabn=False):
+    """fprop + the following norm layer's statistics (fused into the epilogue on
+    the TMA-store path); returns (y, mean, invstd, fused)"""
+    _require_cuda(x, w)
+    N, H, W, Cc = x.shape
+    K, R, S, _ = w.shape
+    Ho, Wo = (H + 2 * pad - R) // stride + 1, (W + 2 * pad - S) // stride + 1
+    y = torch.empty((N, Ho, Wo, K), device=x.device, dtype=x.dtype)
+    mean = torch.empty(K, device=x.device, dtype=torch.float32)
+    invstd = torch.empty_like(mean)
+    fused = C.c_int(0)
+    check(L().sdb_conv_fprop_stats(ctx(), dt(x), ptr(x), ptr(w), ptr(y), N, H, W, Cc, K, R, S, stride, pad, eps,
+                                   1 if iabn else 0, ptr(mean), ptr(invstd), C.byref(fused), stream()))
+    return y, mean, invstd, bool(fused.value)
 
 
 def conv_dgrad_nhwc(dy, w, x_shape, stride, pad, out=None, accumulate=False):

@@ -11,12 +11,30 @@ here it is measured), and the device bytes in use.
 """
 from __future__ import annotations
 
+import dataclasses
+import json
 import time
 from dataclasses import dataclass, field
 
+from . import ConfigError
 from . import detector as D
 
 METRICS_HEADER = "step,loss,scale,skipped,step_time_model,peak_bytes"
+
+
+def config_digest(p: D.Preset) -> int:
+    """64-bit FNV-1a over the canonical JSON of the run's configuration, the
+    scheme of the reference's config_digest (src/config.cpp:247-258): the step
+    horizon is not part of it (resume may extend it).  The detector preset is
+    this driver's config, so the value identifies the same experiment the way
+    the reference's does for its own Config."""
+    tree = dataclasses.asdict(p)
+    s = json.dumps(tree, sort_keys=True, separators=(",", ":"))
+    h = 0xCBF29CE484222325
+    for ch in s.encode():
+        h ^= ch
+        h = (h * 0x100000001B3) & 0xFFFFFFFFFFFFFFFF
+    return h
 
 
 def metrics_row(step: int, loss: float, scale: float, skipped: int, step_ms: float, peak: int) -> str:
@@ -33,7 +51,7 @@ class TrainResult:
 
 def run_training(p: D.Preset, steps: int, rank: int = 0, world: int = 1, nccl_id: bytes | None = None,
                  metrics_path: str | None = None, checkpoint_path: str | None = None, checkpoint_every: int = 0,
-                 resume: str | None = None, config_digest: int = 0) -> TrainResult:
+                 resume: str | None = None, force_resume: bool = False) -> TrainResult:
     """train steps (resume.step, steps] with synthetic images and GT keyed by the
     global batch slots (src/dataset.cpp:82-103), so a resumed run sees exactly
     the batches the uninterrupted one would"""
@@ -44,8 +62,15 @@ def run_training(p: D.Preset, steps: int, rank: int = 0, world: int = 1, nccl_id
     res = TrainResult()
     rows = [METRICS_HEADER]
     start = 0
+    digest = config_digest(p)
     if resume:
-        start, _ = det.load_checkpoint(resume)
+        start, saved = det.load_checkpoint(resume)
+        # the reference refuses a checkpoint of another configuration unless
+        # forced (src/trainer.cpp:138-141)
+        if saved != digest and not force_resume:
+            det.close()
+            raise ConfigError(f"checkpoint config digest {saved:#018x} differs from this run's {digest:#018x} "
+                                "(pass force_resume=True to override)")
     try:
         for step in range(start + 1, steps + 1):
             t0 = time.perf_counter()
@@ -59,7 +84,7 @@ def run_training(p: D.Preset, steps: int, rank: int = 0, world: int = 1, nccl_id
             if rank == 0:
                 rows.append(metrics_row(step, losses[4], scale_used, int(overflow), ms, total - free))
             if checkpoint_path and checkpoint_every and step % checkpoint_every == 0 and rank == 0:
-                det.save_checkpoint(checkpoint_path, step, config_digest)
+                det.save_checkpoint(checkpoint_path, step, digest)
             res.last_step = step
     finally:
         det.close()

@@ -346,3 +346,46 @@ def test_update_scale_matches_reference(ref):
         sd.update_scale(sc, good, flag, True, growth_interval=7)
         torch.cuda.synchronize()
         assert sc.item() == s_ref.value and good.item() == g_ref.value
+
+
+@pytest.mark.parametrize("case", [
+    # (N, H, W, C, K, R, stride): tile widths 256 / 128 / 64 on the TMA-store path, M % 128 != 0
+    (2, 60, 61, 64, 512, 1, 1),    # BN = 256 (res5-like expansion width), M = 7320
+    (2, 47, 33, 128, 128, 3, 1),   # BN = 128, 3x3, M = 3102
+    (1, 29, 43, 64, 64, 1, 1),     # BN = 64, M = 1247
+    (2, 30, 31, 256, 1024, 1, 2),  # stride-2 1x1 into 1024 channels (res4 down), M = 480
+])
+@pytest.mark.parametrize("iabn", [False, True])
+def test_fused_norm_statistics_in_fprop_epilogue(case, iabn):
+    """the fp64 column sums reduced in the fprop's TMA-store epilogue
+    (ConvStats -> finalize) give the same mean/invstd as the separate statistics
+    pass over the same fp16 output, for every tile width and ragged M"""
+    from paper_1903_05831_b200 import simdet as sd
+    N, H, W, C, K, R, s = case
+    pad = R // 2
+    g = torch.Generator(device="cuda").manual_seed(sum(case))
+    x = (torch.randn((N, H, W, C), generator=g, device="cuda") * 2 + 0.5).half()
+    w = (torch.randn((K, R, R, C), generator=g, device="cuda") * (1.0 / (C * R * R) ** 0.5)).half()
+    y, mean, invstd, fused = sd.conv_fprop_stats_nhwc(x, w, s, pad, iabn=iabn)
+    assert fused, "the fused-statistics epilogue did not run for this shape"
+    rows = y.shape[0] * y.shape[1] * y.shape[2]
+    gm = torch.ones(K, device="cuda")
+    bt = torch.zeros(K, device="cuda")
+    m2, i2 = torch.empty_like(mean), torch.empty_like(invstd)
+    out = torch.empty_like(y)
+    if iabn:
+        sd.check(sd.L().sdb_iabn_fwd(sd.ctx(), 1, sd.ptr(y), sd.ptr(gm), sd.ptr(bt), sd.ptr(out), sd.ptr(m2), sd.ptr(i2),
+                                     rows, K, 1e-5, 1.0, sd.stream()))
+    else:
+        sd.check(sd.L().sdb_bn_fwd(sd.ctx(), 1, sd.ptr(y), sd.ptr(gm), sd.ptr(bt), sd.ptr(out), sd.ptr(m2), sd.ptr(i2),
+                                   rows, K, 1e-5, 0, sd.stream()))
+    torch.cuda.synchronize()
+    # both reduce the same fp16 values in fp64; only the summation order differs
+    assert torch.allclose(mean, m2, rtol=1e-6, atol=1e-7), (mean - m2).abs().max()
+    assert torch.allclose(invstd, i2, rtol=1e-6), (invstd - i2).abs().max()
+    # and against a float64 recomputation from y
+    yd = y.double().reshape(-1, K)
+    mu = yd.mean(0)
+    var = (yd * yd).mean(0) - mu * mu
+    assert torch.allclose(mean.double(), mu, rtol=1e-5, atol=1e-6)
+    assert torch.allclose(invstd.double(), 1.0 / torch.sqrt(var.clamp_min(0) + 1e-5), rtol=1e-4)

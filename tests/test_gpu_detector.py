@@ -325,6 +325,12 @@ def test_training_driver_metrics_and_resume(tmp_path):
     ck = str(tmp_path / "ck.sdck")
     T.run_training(p, 2, checkpoint_path=ck, checkpoint_every=2)
     resumed = T.run_training(p, 4, resume=ck)
+    # a checkpoint of another configuration is refused unless forced (src/trainer.cpp:138-141)
+    import paper_1903_05831_b200 as pkg
+    other = D.preset("c2", img_h=128, img_w=128, dynamic_scale=1, scale_init=1024.0, growth_interval=2, lr=0.02)
+    with pytest.raises(pkg.ConfigError):
+        T.run_training(other, 3, resume=ck)
+    assert T.run_training(other, 3, resume=ck, force_resume=True).last_step == 3
     rl = resumed.metrics_csv.splitlines()
     assert [ln.split(",")[:4] for ln in rl[1:]] == [ln.split(",")[:4] for ln in lines[3:]]
     assert resumed.losses == full.losses[2:]
