@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--config", default="c4")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--force-comm", action="store_true",
+                    help="N=1: run the data-parallel path through a 1-rank NCCL communicator")
     return ap.parse_args()
 
 
@@ -451,7 +453,8 @@ def run_ours(args):
 
         nccl_id = dp.share_nccl_id(dist, rank, make_id)
     p = D.preset(args.config)
-    det = D.Detector(p, device=local, rank=rank, world=world, nccl_id=nccl_id)
+    det = D.Detector(p, device=local, rank=rank, world=world, nccl_id=nccl_id,
+                     force_comm=args.force_comm and world == 1)
     import ctypes as C
     lb = D.L()
     lb.sdb_ctx_stream.restype = C.c_void_p
@@ -572,6 +575,10 @@ def run_ours(args):
         "config": {"workload": f"{args.config.upper()}: Faster R-CNN R50-C4 fp16 training, batch {B}/GPU, "
                                f"3x{p.img_h}x{p.img_w}, {p.roi_batch} RoIs/img, {p.pre_nms}->{p.post_nms} proposals",
                    "global_batch": world * B, "per_gpu_batch": B, "parallelism": f"dp{world}",
+                   "comm": ("NCCL fp16 buckets (ncclAvg) + fp32 BN-grad / f64 loss allreduce, in the captured step"
+                            if world > 1 or args.force_comm else "none (one rank)"),
+                   "bucket_mb": 25.0, "loss_scaling": "dynamic from 2^15, x2 / 1000 steps" if p.dynamic_scale
+                   else f"static {p.scale_init:g}",
                    "l2": "per-step working set (activations, weights) >> 126 MB L2; no flush needed",
                    "loss_scale": scale_used, "last_losses": losses[:5], "overflow": overflow},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
