@@ -45,7 +45,7 @@ void comm_destroy(Ctx* c) {
 }
 
 // in-place allreduce on `st` (the reference's allreduce_sum contract,
-// src/comm.cpp:288-315).  avg = 1: ncclAvg, which NCCL implements for floating
+// src/comm.cpp:288-315).  avg = 2: ncclMax (flags); avg = 1: ncclAvg, which NCCL implements for floating
 // types as a pre-multiply of every rank's values by 1/K followed by the sum --
 // used for the fp16 gradient buckets so the reduced value cannot overflow when
 // no rank's value does.  A no-op without a communicator; with a forced 1-rank
@@ -56,8 +56,8 @@ cudaError_t comm_allreduce(Ctx* c, void* buf, int64_t n, int dtype, int avg, cud
     const ncclDataType_t t = dtype == kF16 ? ncclFloat16
                              : dtype == kF32 ? ncclFloat32
                              : dtype == 3 ? ncclFloat64 : ncclInt32;
-    const ncclResult_t r = ncclAllReduce(buf, buf, static_cast<size_t>(n), t, avg ? ncclAvg : ncclSum,
-                                         static_cast<ncclComm_t>(c->nccl), st);
+    const ncclRedOp_t op = avg == 2 ? ncclMax : (avg ? ncclAvg : ncclSum);
+    const ncclResult_t r = ncclAllReduce(buf, buf, static_cast<size_t>(n), t, op, static_cast<ncclComm_t>(c->nccl), st);
     if (r != ncclSuccess) {
         set_error(SDB_COLLECTIVE_CODE, (std::string("ncclAllReduce: ") + ncclGetErrorString(r) + " / " +
                                         ncclGetLastError(static_cast<ncclComm_t>(c->nccl))).c_str());

@@ -1403,11 +1403,18 @@ __global__ void wgrad_reduce_t_kernel(const float* __restrict__ ws, int splits, 
 // finds its job in the tile prefix table, then reduces one 32x32 tile exactly
 // like wgrad_reduce_t_kernel (transposed jobs) or wgrad_reduce_kernel (plain
 // [K][RSC] partials) -- same per-element summation order (splits in order).
+// binary16 bits with an all-ones exponent: inf or NaN
+SDB_DEV bool h_nonfinite(__half h) { return (__half_as_ushort(h) & 0x7c00u) == 0x7c00u; }
+
 __global__ void __launch_bounds__(256) wgrad_reduce_batched_kernel(const WgradJob* __restrict__ jobs,
-                                                                  const int* __restrict__ tile_start, int njobs) {
+                                                                  const int* __restrict__ tile_start, int njobs,
+                                                                  int* __restrict__ nonfinite) {
+    // has_nonfinite (src/trainer.cpp:78-82) of the fp16 gradients this launch
+    // writes, OR-ed into *nonfinite: the optimizer needs no separate pass
     __shared__ float tile[32][33];
     pdl_wait();
     pdl_trigger();
+    bool bad = false;
     int lo = 0, hi = njobs - 1;
     while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
@@ -1459,13 +1466,21 @@ __global__ void __launch_bounds__(256) wgrad_reduce_batched_kernel(const WgradJo
             __syncthreads();
             for (int ii = ty; ii < 32; ii += 8) {
                 const int io = i0 + ii, jo = j0 + tx;
-                if (io < jb.cols && jo < jb.rows) dw[static_cast<int64_t>(io) * jb.rows + jo] = __float2half_rn(tile[tx][ii]);
+                if (io < jb.cols && jo < jb.rows) {
+                    const __half hv = __float2half_rn(tile[tx][ii]);
+                    bad |= h_nonfinite(hv);
+                    dw[static_cast<int64_t>(io) * jb.rows + jo] = hv;
+                }
             }
         } else if (okv) {
             __half2* o = reinterpret_cast<__half2*>(dw + static_cast<int64_t>(j) * jb.cols + iq);
-            o[0] = __floats2half2_rn(a4.x, a4.y);
-            o[1] = __floats2half2_rn(a4.z, a4.w);
+            const __half2 h0 = __floats2half2_rn(a4.x, a4.y), h1 = __floats2half2_rn(a4.z, a4.w);
+            bad |= h_nonfinite(__low2half(h0)) | h_nonfinite(__high2half(h0)) | h_nonfinite(__low2half(h1)) |
+                   h_nonfinite(__high2half(h1));
+            o[0] = h0;
+            o[1] = h1;
         }
+        if (nonfinite && __syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite, 1);
         return;
     }
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
@@ -1500,19 +1515,29 @@ __global__ void __launch_bounds__(256) wgrad_reduce_batched_kernel(const WgradJo
         __syncthreads();
         for (int ii = ty; ii < 32; ii += 8) {
             const int io = i0 + ii, jo = j0 + tx;
-            if (io < jb.cols && jo < jb.rows) dw[static_cast<int64_t>(io) * jb.rows + jo] = __float2half_rn(tile[tx][ii]);
+            if (io < jb.cols && jo < jb.rows) {
+                const __half hv = __float2half_rn(tile[tx][ii]);
+                bad |= h_nonfinite(hv);
+                dw[static_cast<int64_t>(io) * jb.rows + jo] = hv;
+            }
         }
     } else {
 #pragma unroll
         for (int u = 0; u < 4; ++u)
-            if (ok[u]) dw[off[u]] = __float2half_rn(acc[u]);
+            if (ok[u]) {
+                const __half hv = __float2half_rn(acc[u]);
+                bad |= h_nonfinite(hv);
+                dw[off[u]] = hv;
+            }
     }
+    if (nonfinite && __syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite, 1);
 }
 
 cudaError_t wgrad_reduce_batched(const WgradJob* jobs_dev, const int* tile_start_dev, int njobs, int total_tiles,
-                                 cudaStream_t st) {
+                                 cudaStream_t st, int* nonfinite) {
     if (njobs == 0) return cudaSuccess;
-    return launch_pdl(wgrad_reduce_batched_kernel, dim3(total_tiles), dim3(256), 0, st, jobs_dev, tile_start_dev, njobs);
+    return launch_pdl(wgrad_reduce_batched_kernel, dim3(total_tiles), dim3(256), 0, st, jobs_dev, tile_start_dev, njobs,
+                      nonfinite);
 }
 
 int wgrad_job_tiles(const WgradJob& j) { return ((j.rows + 31) / 32) * ((j.cols + 31) / 32); }
@@ -1614,6 +1639,10 @@ static cudaError_t launch_tma(ConvArgs a, int splits, cudaStream_t st, ConvStats
     const int tiles_m = (a.M + kBM - 1) / kBM, tiles_n = (a.NG + BN - 1) / BN;
     const int n_tiles = tiles_m * tiles_n * splits;
     int grid = std::min(n_tiles, Cfg::kPerSM * kNumSMs);
+    // fused output statistics need every CTA on one column block (grid a
+    // multiple of tiles_n): e.g. the res5 expansion convs (tiles_n = 8) give up
+    // 4 of 148 CTAs (< 3% of a ~80 us GEMM) to save a 50 us statistics pass
+    if (MODE == FPROP && EPI == 0 && cst && grid % tiles_n != 0 && grid >= tiles_n) grid -= grid % tiles_n;
     if (MODE == WGRAD) {
         // experiment knob: SMs a wgrad may occupy (leaves room for the concurrent norm chain)
         static const int cap = [] { const char* e = std::getenv("SDB_WGRAD_SMS"); return e ? std::atoi(e) : 0; }();

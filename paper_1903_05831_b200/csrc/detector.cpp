@@ -668,7 +668,7 @@ void flush_bucket(sdb_det* d, int b, cudaStream_t st) {
     J.clear();
     {
         PScope ps(d, P_WGRAD, 0, 0, 1);
-        CK(wgrad_reduce_batched(T.jobs, T.tiles, T.njobs, T.total, st));
+        CK(wgrad_reduce_batched(T.jobs, T.tiles, T.njobs, T.total, st, d->flag));
         if (d->stem_gemm && d->bucket_of[d->stem.p] == b)
             CK(stem_weights(d->stem_dw2, 64, 8, d->gptr(d->stem.p), 1, st));
     }
@@ -809,6 +809,9 @@ void run_step(sdb_det* d) {
     const bool side = d->side_wgrad && !d->prof.on;
     d->bucket_left = d->bucket_nparams;
     for (auto& j : d->bjobs) j.clear();
+    // the overflow flag is OR-ed by the bucket reduces (deferred fp16 wgrads)
+    // and the BN-gradient check; zeroed before any of them can run
+    CK(cudaMemsetAsync(d->flag, 0, sizeof(int), st));
     AnchorTargetArgs at{};
     at.anchors = d->anchors; at.nA = d->nA; at.n_img = cf.batch; at.gt = d->gt; at.gt_stride = cf.max_gt;
     at.gt_count = d->gt_count; at.img_h = static_cast<float>(cf.img_h); at.img_w = static_cast<float>(cf.img_w);
@@ -1003,12 +1006,16 @@ void run_step(sdb_det* d) {
         CK(cudaStreamWaitEvent(d->comm, d->ev_fork, 0));
         CKC(comm_allreduce(d->ctx, d->bng, d->n_bn, kF32, 0, d->comm));
         CKC(comm_allreduce(d->ctx, d->losses, 4, 3 /* f64 */, 0, d->comm));
+        // the reduces flagged this rank's fp16 gradients before the averaging
+        // allreduce; an average of finite values is finite and a non-finite
+        // input stays non-finite, so the summed gradient overflows iff some
+        // rank flagged (MAX over ranks)
+        if (d->defer_wgrad) CKC(comm_allreduce(d->ctx, d->flag, 1, 2 /* int32 */, 2 /* max */, d->comm));
         CK(cudaEventRecord(d->ev_join, d->comm));
         CK(cudaStreamWaitEvent(st, d->ev_join, 0));
     }
     PScope ps_opt(d, P_OPTIM, 0, (d->es + 12.0 + (d->dt == kF16 ? 2.0 : 0.0)) * d->n_w + 16.0 * d->n_bn, 5);
-    CK(cudaMemsetAsync(d->flag, 0, sizeof(int), st));
-    CK(nonfinite_check(d->dt, d->g, d->n_w, d->flag, st));
+    if (!d->defer_wgrad) CK(nonfinite_check(d->dt, d->g, d->n_w, d->flag, st));  // else: in the reduces
     CK(nonfinite_check(kF32, d->bng, d->n_bn, d->flag, st));
     const double K = static_cast<double>(d->ctx->world);
     // fp16 buckets arrive averaged over the ranks (issue_bucket_allreduce)

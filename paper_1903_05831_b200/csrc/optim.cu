@@ -72,6 +72,49 @@ __global__ void fused_sgd_kernel(const T* __restrict__ gsum, float* __restrict__
     }
 }
 
+// fp16 gradients, 8 parameters per thread per iteration: 16-byte loads of g
+// and of the fp16 shadow, 32-byte loads/stores of w and v (n % 8 == 0, all
+// pointers 16-byte aligned); per element the same _rn expression as above
+__global__ void __launch_bounds__(256) fused_sgd_h8_kernel(const uint4* __restrict__ gsum, float4* __restrict__ w,
+                                                           float4* __restrict__ v, uint4* __restrict__ w16, int64_t n8,
+                                                           float lr, float mu, const double* __restrict__ scale,
+                                                           double denom_mult, const int* __restrict__ flag) {
+    if (flag && *flag) return;  // overflow: weights and velocity untouched (trainer.cpp:253)
+    const double denom = __dmul_rn(scale ? *scale : 1.0, denom_mult);
+    const float inv = __double2float_rn(__ddiv_rn(1.0, denom));
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n8;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const uint4 gu = gsum[i];
+        const __half2* g2 = reinterpret_cast<const __half2*>(&gu);
+        float4 wa = w[2 * i], wb = w[2 * i + 1], va = v[2 * i], vb = v[2 * i + 1];
+        float* wf[8] = {&wa.x, &wa.y, &wa.z, &wa.w, &wb.x, &wb.y, &wb.z, &wb.w};
+        float* vf[8] = {&va.x, &va.y, &va.z, &va.w, &vb.x, &vb.y, &vb.z, &vb.w};
+        uint4 hu;
+        __half2* h2 = reinterpret_cast<__half2*>(&hu);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const float2 gf = __half22float2(g2[k]);
+            float o[2];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int e = 2 * k + q;
+                const float g = __fmul_rn(q ? gf.y : gf.x, inv);
+                const float vi = __fadd_rn(__fmul_rn(mu, *vf[e]), g);
+                const float wi = __fsub_rn(*wf[e], __fmul_rn(lr, vi));
+                *vf[e] = vi;
+                *wf[e] = wi;
+                o[q] = wi;
+            }
+            h2[k] = __floats2half2_rn(o[0], o[1]);
+        }
+        w[2 * i] = wa;
+        w[2 * i + 1] = wb;
+        v[2 * i] = va;
+        v[2 * i + 1] = vb;
+        if (w16) w16[i] = hu;
+    }
+}
+
 __global__ void update_scale_kernel(double* scale, int64_t* good, const int* flag, int dynamic, int64_t interval,
                                     double growth, double backoff, double min_scale, double max_scale) {
     if (!dynamic) return;
@@ -114,7 +157,12 @@ cudaError_t nonfinite_check(int gdtype, const void* g, int64_t n, int* flag, cud
 cudaError_t fused_sgd(int gdtype, const void* gsum, float* w, float* v, __half* w16, int64_t n, float lr, float mu,
                       const double* scale, double denom_mult, const int* flag, cudaStream_t st) {
     if (n <= 0) return cudaSuccess;
-    if (gdtype == kF16)
+    const auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+    if (gdtype == kF16 && (n & 7) == 0 && al16(gsum) && al16(w) && al16(v) && (!w16 || al16(w16))) {
+        fused_sgd_h8_kernel<<<grid_for(n / 8, 2), kThreads, 0, st>>>(
+            static_cast<const uint4*>(gsum), reinterpret_cast<float4*>(w), reinterpret_cast<float4*>(v),
+            reinterpret_cast<uint4*>(w16), n / 8, lr, mu, scale, denom_mult, flag);
+    } else if (gdtype == kF16)
         fused_sgd_kernel<__half><<<grid_for(n, 4), kThreads, 0, st>>>(static_cast<const __half*>(gsum), w, v, w16, n, lr,
                                                                      mu, scale, denom_mult, flag);
     else

@@ -53,8 +53,9 @@ struct WgradJob {
 };
 cudaError_t conv_wgrad_deferred(const ConvShape& g, int dtype, const void* x, const void* dy, void* dw, void* ws,
                                 size_t ws_bytes, cudaStream_t st, WgradJob* job);
+// nonfinite (optional): OR-ed with 1 when any fp16 gradient written is inf/NaN
 cudaError_t wgrad_reduce_batched(const WgradJob* jobs_dev, const int* tile_start_dev, int njobs, int total_tiles,
-                                 cudaStream_t st);
+                                 cudaStream_t st, int* nonfinite = nullptr);
 int wgrad_job_tiles(const WgradJob& j);
 bool conv_force_simt();
 void conv_set_force_simt(bool v);
