@@ -288,11 +288,11 @@ def test_iabn_errors():
 
 
 @pytest.mark.parametrize("gfp16", [False, True])
-def test_fused_sgd_bitwise(orc, gfp16):
+@pytest.mark.parametrize("n", [1 << 20 | 77, 1 << 20])  # scalar tail path / 8-wide vector path
+def test_fused_sgd_bitwise(orc, gfp16, n):
     """apply_sgd (src/trainer.cpp:86-94) is FP32 elementwise: compare bit for bit."""
     from paper_1903_05831_b200 import simdet as sd
     rng = np.random.default_rng(11)
-    n = 1 << 20 | 77
     w = rng.standard_normal(n).astype(np.float32)
     v = (0.01 * rng.standard_normal(n)).astype(np.float32)
     g = (300 * rng.standard_normal(n)).astype(np.float32)
