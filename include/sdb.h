@@ -252,6 +252,9 @@ typedef struct {
     uint64_t seed;
     int max_gt;
     double bucket_mb;    /* fp16 gradient bucket size for the NCCL allreduce */
+    int shard_optimizer; /* fp16 with a communicator: reduce-scatter each bucket, update this
+                            rank's 1/K shard of the fp32 masters, all-gather the fp16 shadows
+                            (instead of allreduce + a replicated update) */
 } sdb_det_config;
 
 typedef struct sdb_det sdb_det;

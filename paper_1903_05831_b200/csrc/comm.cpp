@@ -67,6 +67,41 @@ cudaError_t comm_allreduce(Ctx* c, void* buf, int64_t n, int dtype, int avg, cud
     return cudaSuccess;
 }
 
+static ncclDataType_t nccl_type(int dtype) {
+    return dtype == kF16 ? ncclFloat16 : dtype == kF32 ? ncclFloat32 : dtype == 3 ? ncclFloat64 : ncclInt32;
+}
+
+static cudaError_t nccl_status(Ctx* c, ncclResult_t r, const char* what) {
+    if (r == ncclSuccess) return cudaSuccess;
+    set_error(SDB_COLLECTIVE_CODE, (std::string(what) + ": " + ncclGetErrorString(r) + " / " +
+                                    ncclGetLastError(static_cast<ncclComm_t>(c->nccl))).c_str());
+    c->last_nccl_error = static_cast<int>(r);
+    return cudaErrorUnknown;
+}
+
+// in-place reduce-scatter of buf[0, K*cnt): this rank's averaged (avg = 1) or
+// summed chunk lands at buf + rank*cnt -- the first half of the reference's
+// ring allreduce (src/comm.cpp:294-304)
+cudaError_t comm_reduce_scatter(Ctx* c, void* buf, int64_t cnt, int dtype, int avg, cudaStream_t st) {
+    if (!c->nccl || cnt == 0) return cudaSuccess;
+    const size_t es = dtype == kF16 ? 2 : (dtype == 3 ? 8 : 4);
+    void* mine = static_cast<uint8_t*>(buf) + static_cast<size_t>(c->rank) * cnt * es;
+    return nccl_status(c, ncclReduceScatter(buf, mine, static_cast<size_t>(cnt), nccl_type(dtype), avg ? ncclAvg : ncclSum,
+                                            static_cast<ncclComm_t>(c->nccl), st),
+                       "ncclReduceScatter");
+}
+
+// in-place all-gather: every rank's chunk buf + r*cnt to all ranks (the second
+// half of the ring allreduce, src/comm.cpp:305-314)
+cudaError_t comm_all_gather(Ctx* c, void* buf, int64_t cnt, int dtype, cudaStream_t st) {
+    if (!c->nccl || cnt == 0) return cudaSuccess;
+    const size_t es = dtype == kF16 ? 2 : (dtype == 3 ? 8 : 4);
+    const void* mine = static_cast<const uint8_t*>(buf) + static_cast<size_t>(c->rank) * cnt * es;
+    return nccl_status(c, ncclAllGather(mine, buf, static_cast<size_t>(cnt), nccl_type(dtype),
+                                        static_cast<ncclComm_t>(c->nccl), st),
+                       "ncclAllGather");
+}
+
 cudaError_t comm_allreduce_sum(Ctx* c, void* buf, int64_t n, int dtype, cudaStream_t st) {
     return comm_allreduce(c, buf, n, dtype, 0, st);
 }

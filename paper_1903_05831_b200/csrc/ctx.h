@@ -22,4 +22,6 @@ void comm_destroy(Ctx* c);
 cudaError_t comm_allreduce(Ctx* c, void* buf, int64_t n, int dtype, int avg, cudaStream_t st);
 cudaError_t comm_allreduce_sum(Ctx* c, void* buf, int64_t n, int dtype, cudaStream_t st);
 int comm_async_error(Ctx* c);
+cudaError_t comm_reduce_scatter(Ctx* c, void* buf, int64_t cnt, int dtype, int avg, cudaStream_t st);
+cudaError_t comm_all_gather(Ctx* c, void* buf, int64_t cnt, int dtype, cudaStream_t st);
 }  // namespace sdb

@@ -250,6 +250,12 @@ struct sdb_det {
     // comm: an NCCL communicator exists (world > 1, or a forced 1-rank one that
     // runs the data-parallel code path on one GPU)
     bool comm_on = false;
+    // sharded optimizer: buckets are reduce-scattered, each rank
+    // updates its 1/K shard of the fp32 masters and all-gathers the fp16 shadows
+    bool shard = false;
+    bool masters_synced = true;  // the full fp32 masters are current on this rank
+    std::vector<cudaEvent_t> gather_ev;
+    cudaEvent_t ev_gather_join = nullptr;
     cudaStream_t comm = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     std::vector<cudaEvent_t> bucket_ev;
@@ -623,7 +629,11 @@ void issue_bucket_allreduce(sdb_det* d, size_t b, cudaStream_t st) {
     cudaEvent_t ev = d->bucket_ev[b];
     CK(cudaEventRecord(ev, st));
     CK(cudaStreamWaitEvent(d->comm, ev, 0));
-    CKC(comm_allreduce(d->ctx, static_cast<uint8_t*>(d->g) + lo * d->es, hi - lo, d->dt, d->dt == kF16, d->comm));
+    if (d->shard)
+        CKC(comm_reduce_scatter(d->ctx, static_cast<uint8_t*>(d->g) + lo * d->es, (hi - lo) / d->ctx->world, d->dt, 1,
+                                d->comm));
+    else
+        CKC(comm_allreduce(d->ctx, static_cast<uint8_t*>(d->g) + lo * d->es, hi - lo, d->dt, d->dt == kF16, d->comm));
 }
 
 // non-deferred wgrads (fp32 modes): buckets are issued in plan order as the
@@ -1020,8 +1030,26 @@ void run_step(sdb_det* d) {
     const double K = static_cast<double>(d->ctx->world);
     // fp16 buckets arrive averaged over the ranks (issue_bucket_allreduce)
     const double Kw = d->dt == kF16 ? 1.0 : K;
-    CK(fused_sgd(d->dt, d->g, d->w32, d->v32, d->dt == kF16 ? static_cast<__half*>(d->wdev) : nullptr, d->n_w, cf.lr,
-                 cf.momentum, d->scale, Kw, d->flag, st));
+    if (d->shard) {
+        // this rank's shard of every bucket, then the fp16 shadows all-gathered
+        // on the comm stream (each bucket as soon as its shard is updated)
+        const int64_t r = d->ctx->rank, Kr = d->ctx->world;
+        for (size_t b = 0; b < d->buckets.size(); ++b) {
+            const auto [lo, hi] = d->buckets[b];
+            const int64_t cnt = (hi - lo) / Kr, s = lo + r * cnt;
+            CK(fused_sgd(kF16, static_cast<__half*>(d->g) + s, d->w32 + s, d->v32 + s,
+                         static_cast<__half*>(d->wdev) + s, cnt, cf.lr, cf.momentum, d->scale, Kw, d->flag, st));
+            CK(cudaEventRecord(d->gather_ev[b], st));
+            CK(cudaStreamWaitEvent(d->comm, d->gather_ev[b], 0));
+            CKC(comm_all_gather(d->ctx, static_cast<__half*>(d->wdev) + lo, cnt, kF16, d->comm));
+        }
+        CK(cudaEventRecord(d->ev_gather_join, d->comm));
+        CK(cudaStreamWaitEvent(st, d->ev_gather_join, 0));
+        d->masters_synced = Kr == 1;
+    } else {
+        CK(fused_sgd(d->dt, d->g, d->w32, d->v32, d->dt == kF16 ? static_cast<__half*>(d->wdev) : nullptr, d->n_w,
+                     cf.lr, cf.momentum, d->scale, Kw, d->flag, st));
+    }
     CK(fused_sgd(kF32, d->bng, d->bn32, d->bnv, nullptr, d->n_bn, cf.lr, cf.momentum, d->scale, K, d->flag, st));
     CK(update_scale_device(d->scale, d->good, d->flag, cf.dynamic_scale, cf.growth_interval, cf.growth, cf.backoff,
                            cf.min_scale, cf.max_scale, st));
@@ -1317,6 +1345,18 @@ int sdb_det_create(sdb_ctx* ctx, const sdb_det_config* cfgp, sdb_det** out) {
             CK(cudaStreamCreateWithPriority(&d->comm, cudaStreamNonBlocking, phi));
             CK(cudaEventCreateWithFlags(&d->ev_fork, cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&d->ev_join, cudaEventDisableTiming));
+            // the sharded update needs every bucket to split evenly over the ranks
+            bool even = true;
+            for (const auto& bk : d->buckets) even = even && (bk.second - bk.first) % ctx->world == 0;
+            d->shard = d->defer_wgrad && cf.shard_optimizer && even;
+            if (d->shard) {
+                for (size_t i = 0; i < d->buckets.size(); ++i) {
+                    cudaEvent_t e;
+                    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                    d->gather_ev.push_back(e);
+                }
+                CK(cudaEventCreateWithFlags(&d->ev_gather_join, cudaEventDisableTiming));
+            }
         }
         init_params(d);
     } catch (const std::exception& e) {
@@ -1356,6 +1396,8 @@ int sdb_det_destroy(sdb_det* d) {
     if (d->comm) {
         cudaEventDestroy(d->ev_fork);
         cudaEventDestroy(d->ev_join);
+        for (auto e : d->gather_ev) cudaEventDestroy(e);
+        if (d->ev_gather_join) cudaEventDestroy(d->ev_gather_join);
         cudaStreamDestroy(d->comm);
     }
     delete d;
@@ -1383,12 +1425,28 @@ int sdb_det_param_info(sdb_det* d, int idx, char* name, int name_len, int64_t* s
     return SDB_OK;
 }
 
+// with the sharded optimizer each rank updated only its shard of the fp32
+// masters and velocity: gather the full arrays once before host reads
+static void sync_masters(sdb_det* d) {
+    if (d->masters_synced) return;
+    cudaStream_t st = d->ctx->stream;
+    const int64_t Kr = d->ctx->world;
+    for (const auto& bk : d->buckets) {
+        const int64_t cnt = (bk.second - bk.first) / Kr;
+        CKC(comm_all_gather(d->ctx, d->w32 + bk.first, cnt, kF32, st));
+        CKC(comm_all_gather(d->ctx, d->v32 + bk.first, cnt, kF32, st));
+    }
+    CK(cudaStreamSynchronize(st));
+    d->masters_synced = true;
+}
+
 // which: 0 get w, 1 set w, 2 get grad, 3 get velocity, 4 set velocity
 static int param_xfer(sdb_det* d, int idx, float* host, int which) {
     if (idx < 0 || idx >= static_cast<int>(d->params.size())) return det_fail(SDB_PARAM, "param index");
     const Param& p = d->params[idx];
     cudaStream_t st = d->ctx->stream;
     try {
+        if (which != 2 && p.kind <= 1) sync_masters(d);
         // every copy is ordered on the context stream: a pageable cudaMemcpy may
         // return before its DMA lands, and the stream is non-blocking
         CK(cudaStreamSynchronize(st));
@@ -1441,6 +1499,8 @@ static int param_xfer(sdb_det* d, int idx, float* host, int which) {
         } else {
             map([&](int64_t ri, int64_t di) { host[ri] = dev[di]; });
         }
+    } catch (const CollectiveFailure& e) {
+        return det_fail(SDB_COLLECTIVE, e.what());
     } catch (const std::exception& e) {
         return det_fail(SDB_CUDA, e.what());
     }

@@ -30,7 +30,7 @@ class DetConfig(C.Structure):
         ("lr", C.c_float), ("momentum", C.c_float), ("eps", C.c_float), ("slope", C.c_float),
         ("dynamic_scale", C.c_int), ("scale_init", C.c_double), ("growth_interval", C.c_int64),
         ("growth", C.c_double), ("backoff", C.c_double), ("min_scale", C.c_double), ("max_scale", C.c_double),
-        ("seed", C.c_uint64), ("max_gt", C.c_int), ("bucket_mb", C.c_double),
+        ("seed", C.c_uint64), ("max_gt", C.c_int), ("bucket_mb", C.c_double), ("shard_optimizer", C.c_int),
     ]
 
 
@@ -80,6 +80,7 @@ class Preset:
         c.dynamic_scale, c.scale_init, c.growth_interval = self.dynamic_scale, self.scale_init, self.growth_interval
         c.growth, c.backoff, c.min_scale, c.max_scale = 2.0, 0.5, 1.0, 16777216.0
         c.seed, c.max_gt, c.bucket_mb = self.seed, self.max_gt, 25.0
+        c.shard_optimizer = 1
         for k, v in self.extra.items():
             setattr(c, k, v)
         return c

@@ -138,3 +138,92 @@ def test_syncbn_protocol_gloo_world2(orc):
     assert np.allclose(np.array(res[0][1], np.float32), agg, rtol=1e-6, atol=1e-5)
     assert np.allclose(np.array(res[0][2], np.float32), mean, rtol=1e-5, atol=1e-6)
     assert np.allclose(np.array(res[0][3], np.float32), inv, rtol=1e-5)
+
+
+def _shard_worker(rank, world, port, q):
+    """the sharded optimizer's collectives (csrc/detector.cpp)
+    restated over gloo on the R50-C4 bucket plan: per bucket, reduce-scatter of
+    the fp16 gradient (pre-multiplied by 1/K, the ncclAvg contract), apply_sgd
+    (the reference rule, oracle restatement) on this rank's shard only, then an
+    all-gather of the updated shard"""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    import torch.distributed as dist
+    import oracle
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    buckets, total = _c4_buckets()
+    rng = np.random.default_rng(7)
+    w = rng.standard_normal(total).astype(np.float32)
+    v = (0.1 * rng.standard_normal(total)).astype(np.float32)
+    g_all = [(rng.standard_normal(total) * 64).astype(np.float16) for _ in range(world)]
+    g = torch.from_numpy(g_all[rank].astype(np.float32) / world)  # premultiplied by 1/K
+    orc = oracle.orc()
+    for lo, hi in buckets:
+        cnt = (hi - lo) // world
+        out = torch.empty(cnt)
+        dist.reduce_scatter(out, list(g[lo:hi].chunk(world)))
+        s = lo + rank * cnt
+        gs = np.ascontiguousarray(out.numpy())
+        ws, vs = np.ascontiguousarray(w[s:s + cnt]), np.ascontiguousarray(v[s:s + cnt])
+        orc.orc_apply_sgd(oracle.p(ws), oracle.p(vs), oracle.p(gs), cnt, 0.01, 0.9, 128.0)
+        parts = [torch.empty(cnt) for _ in range(world)]
+        dist.all_gather(parts, torch.from_numpy(ws))
+        w[lo:hi] = torch.cat(parts).numpy()
+    q.put((rank, w.tobytes()))
+    dist.destroy_process_group()
+
+
+def _c4_buckets():
+    """the 25 MB fp16 bucket plan of the R50-C4 detector, from the C ABI's planner"""
+    from paper_1903_05831_b200 import detector as D
+    lb = D.L()
+    lb.sdb_plan_buckets.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_int64, C.c_void_p, C.c_int]
+    # conv/fc parameter sizes of R50-C4 in pack order (device layouts: stem input
+    # channels padded to 8, RPN/fc outputs padded to 8), 16-byte aligned slices
+    sizes = [64 * 7 * 7 * 8]
+    for (nb, width, cout) in ((3, 64, 256), (4, 128, 512), (6, 256, 1024)):
+        cin = {64: 64, 128: 256, 256: 512}[width]
+        for b in range(nb):
+            ci = cin if b == 0 else cout
+            sizes += [width * ci, width * width * 9, cout * width] + ([cout * ci] if b == 0 else [])
+    sizes += [512 * 1024 * 9, 16 * 512, 64 * 512]
+    for b in range(3):
+        ci = 1024 if b == 0 else 2048
+        sizes += [512 * ci, 512 * 512 * 9, 2048 * 512] + ([2048 * ci] if b == 0 else [])
+    sizes += [88 * 2048, 328 * 2048]
+    offs, o = [], 0
+    for s in sizes:
+        offs.append(o)
+        o += (s + 7) // 8 * 8
+    offs = np.array(offs, np.int64)
+    out = np.zeros(2 * len(offs) + 2, np.int64)
+    nb = lb.sdb_plan_buckets(offs.ctypes.data, len(offs), o, 25 * 1024 * 1024 // 2, out.ctypes.data, len(offs) + 1)
+    return [(int(out[2 * i]), int(out[2 * i + 1])) for i in range(nb)], o
+
+
+def test_gloo_world2_sharded_optimizer_equals_allreduce_update():
+    """world 2: reduce-scatter -> shard update -> all-gather gives, bit for bit,
+    the replicated allreduce + full apply_sgd of the reference step tail
+    (src/trainer.cpp:251-254) -- the buckets split evenly over the ranks"""
+    import oracle
+    buckets, total = _c4_buckets()
+    assert buckets[-1][0] == 0 and sum(hi - lo for lo, hi in buckets) == total
+    assert all((hi - lo) % 2 == 0 for lo, hi in buckets)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_shard_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = sorted(q.get(timeout=300) for _ in range(2))
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    assert res[0][1] == res[1][1]  # replicas agree bitwise
+    rng = np.random.default_rng(7)
+    w = rng.standard_normal(total).astype(np.float32)
+    v = (0.1 * rng.standard_normal(total)).astype(np.float32)
+    g_all = [(rng.standard_normal(total) * 64).astype(np.float16) for _ in range(2)]
+    gsum = (g_all[0].astype(np.float32) / 2 + g_all[1].astype(np.float32) / 2).astype(np.float32)
+    orc = oracle.orc()
+    orc.orc_apply_sgd(oracle.p(w), oracle.p(v), oracle.p(gsum), total, 0.01, 0.9, 128.0)
+    assert np.frombuffer(res[0][1], np.float32).tobytes() == w.tobytes()
