@@ -40,13 +40,16 @@ def _run(p, steps, force_comm, poison_at=None):
     return traj, w, v
 
 
+@pytest.mark.parametrize("shard", [1, 0])
 @pytest.mark.parametrize("bucket_mb", [25.0, 0.05])
-def test_forced_comm_step_is_bit_identical(bucket_mb):
+def test_forced_comm_step_is_bit_identical(bucket_mb, shard):
     """4 steps (1 eager + 3 graph replays) with the comm path on == the plain
     step, bit for bit; bucket_mb 0.05 splits the tiny detector into dozens of
-    buckets, so bucket completion order and per-bucket reduces are exercised"""
+    buckets, so bucket completion order and per-bucket reduces are exercised.
+    shard = 1: reduce-scatter + per-shard update + all-gather of the fp16
+    shadows; shard = 0: bucket allreduce + replicated update"""
     from paper_1903_05831_b200 import detector as D
-    p = D.preset("c2", img_h=128, img_w=128, extra={"bucket_mb": bucket_mb})
+    p = D.preset("c2", img_h=128, img_w=128, extra={"bucket_mb": bucket_mb, "shard_optimizer": shard})
     t0, w0, v0 = _run(p, 4, False)
     t1, w1, v1 = _run(p, 4, True)
     assert [t[0] for t in t0] == [t[0] for t in t1]
