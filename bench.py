@@ -461,7 +461,11 @@ def run_ours(args):
     sptr = lb.sdb_ctx_stream(det.ctx)
     stream = torch.cuda.ExternalStream(sptr)
     B = p.batch
-    K, W = args.steps, max(args.warmup, 3)
+    # W >= 3 warm-up steps, and at least 12: the first ~10 steps after a cold
+    # start carry a power-management transient (measured: steps 5-10 run 20-40 %
+    # slower while sw_power_cap settles, tools/step_times.py), which would
+    # otherwise land in the timed region
+    K, W = args.steps, max(args.warmup, 12)
     img_shape = (B, p.img_h, p.img_w, 8)
 
     def make_images(n):
