@@ -548,7 +548,7 @@ def run_ours(args):
     # never runs under a profiler
     traffic = None
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_conv_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r02_conv_traffic.json")) as f:
             tj = json.load(f)
         if args.config == "c4":
             traffic = {"bytes_per_launch": tj["conv_dram_bytes_per_launch"],
