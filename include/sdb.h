@@ -106,6 +106,17 @@ int sdb_conv_wgrad(sdb_ctx* ctx, int dtype, const void* x, const void* dy, void*
 int sdb_conv_fprop_stats(sdb_ctx* ctx, int dtype, const void* x, const void* w, void* y, int N, int H, int W, int C,
                          int K, int R, int S, int stride, int pad, float eps, int iabn, float* mean, float* invstd,
                          int* fused, void* stream);
+/* the backward twin: a stride-1 dgrad whose output dy_iabn is the gradient of
+ * an InPlace-ABN output y (the conv's input), followed by that layer's
+ * iabn_backward (src/memopt.cpp:278-327) -> dz, dgamma, dbeta.  On the
+ * tcgen05 path the IABN backward sums (sum dz, sum dz*xhat) are reduced in the
+ * dgrad epilogue from the staged dy box and a TMA-loaded y box, so the norm
+ * backward is one apply pass; *fused (optional) reports which path ran.
+ * H, W, C: the conv input (= y) dims; K, R, S, pad: the filter. */
+int sdb_conv_dgrad_iabn_bwd(sdb_ctx* ctx, int dtype, const void* dy, const void* w, void* dy_iabn, int N, int H, int W,
+                            int C, int K, int R, int S, int pad, const void* y, const float* gamma, const float* beta,
+                            const float* invstd, float slope, void* dz, float* dgamma, float* dbeta, int* fused,
+                            void* stream);
 
 /* ---- BatchNorm: syncbn_forward/backward with group == nullptr
  * (src/syncbn.cpp:21-117).  rows = N*H*W; relu=1 fuses the ReLU that follows

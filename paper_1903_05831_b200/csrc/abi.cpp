@@ -221,6 +221,43 @@ int sdb_conv_fprop_stats(sdb_ctx* ctx, int dtype, const void* x, const void* w, 
                        "norm stats");
 }
 
+int sdb_conv_dgrad_iabn_bwd(sdb_ctx* ctx, int dtype, const void* dy, const void* w, void* dy_iabn, int N, int H, int W,
+                            int C, int K, int R, int S, int pad, const void* y, const float* gamma, const float* beta,
+                            const float* invstd, float slope, void* dz, float* dgamma, float* dbeta, int* fused,
+                            void* stream) {
+    if (!ctx) return fail(SDB_PARAM, "conv_dgrad_iabn_bwd needs a context (workspace)");
+    if (int rc = check_dtype(dtype)) return rc;
+    if (int rc = check_conv(N, H, W, C, K, R, S, 1, pad)) return rc;
+    const int64_t rows = static_cast<int64_t>(N) * H * W;
+    if (rows < 2) return fail(SDB_DEGENERATE, "batch norm needs at least 2 values per channel");
+    if (!sdb::norm_channels_ok(C)) return fail(SDB_UNSUPPORTED, "norm kernels need C % 8 == 0, C <= 2048, C | 2048");
+    if (!(slope > 0.0f)) return fail(SDB_NONINVERTIBLE, "iabn requires a strictly positive leaky slope");
+    const sdb::ConvShape g{N, H, W, C, K, R, S, 1, pad};
+    const size_t cap = static_cast<size_t>(2 * 148) * 4 * 2 * 256 * sizeof(double);
+    const size_t nws = sdb::norm_workspace_bytes(rows, C);
+    uint8_t* ws = static_cast<uint8_t*>(ctx->scratch(cap + nws + 2 * C * sizeof(float) + 512));
+    if (!ws) return fail(SDB_CUDA, "workspace allocation failed");
+    cudaStream_t st = pick(ctx, stream);
+    sdb::ConvStats cs{reinterpret_cast<double*>(ws), cap, 0, 0, 0, 0};
+    cs.bs_y = y;
+    cs.bs_gamma = gamma;
+    cs.bs_beta = beta;
+    cs.bs_slope = slope;
+    if (int rc = cuda_status(sdb::conv_dgrad(g, dtype, dy, w, dy_iabn, 0, st, nullptr, nullptr, 0.f, nullptr, &cs),
+                             "conv_dgrad"))
+        return rc;
+    if (fused) *fused = cs.produced;
+    if (cs.produced) {
+        float* coef = reinterpret_cast<float*>(ws + cap + 256);
+        return cuda_status(sdb::iabn_backward_conv_stats(dtype, dy_iabn, y, gamma, beta, invstd, dz, dgamma, dbeta, rows,
+                                                         C, slope, cs, coef, st),
+                           "iabn_bwd (fused statistics)");
+    }
+    return cuda_status(sdb::iabn_backward(dtype, dy_iabn, y, gamma, beta, nullptr, invstd, dz, dgamma, dbeta, rows, C,
+                                          slope, ws + cap + 256, st),
+                       "iabn_bwd");
+}
+
 int sdb_conv_wgrad(sdb_ctx* ctx, int dtype, const void* x, const void* dy, void* dw, int N, int H, int W, int C, int K,
                    int R, int S, int stride, int pad, void* stream) {
     if (!ctx) return fail(SDB_PARAM, "conv_wgrad needs a context (workspace)");

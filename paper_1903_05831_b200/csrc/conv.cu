@@ -67,6 +67,13 @@ struct ConvArgs {
     // rounded fp16 output, accumulated by each CTA over its tiles (one n-tile
     // per CTA) and written as stats[cta][quadrant][2][BN] (norm statistics fused)
     double* stats;
+    // dgrad EPI 2: the InPlace-ABN backward statistics of the layer whose output
+    // gradient this dgrad produces (src/memopt.cpp:305-314): per column c,
+    // [sum dz | sum dz*xhat] with dz = dy*(y > 0 ? 1 : slope), xhat = (z - beta)/gamma,
+    // z = y >= 0 ? y : y/slope; y is read by TMA alongside the output tile
+    const float* bs_gamma;
+    const float* bs_beta;
+    float bs_slope;
 };
 
 // TMA descriptors of the dense GEMM operand (filter for fprop/dgrad, DY for wgrad)
@@ -867,6 +874,112 @@ SDB_DEV void epilogue_tile_resid(const ConvArgs& a, const CUtensorMap* omap, con
     }
 }
 
+// Epilogue EPI 2 (stride-1 dgrad whose output feeds an InPlace-ABN backward):
+// the plain TMA-store epilogue plus the layer's backward statistics.  The
+// stored y box of each column step arrives by TMA into a two-slot ring (as
+// the residual epilogue's addend); after the rounded fp16 dy box is staged,
+// lane = column (SC = 32) or half a column (SC = 16) walks the 32 rows of both
+// boxes and accumulates, in fp64 exactly like the statistics kernel,
+//   S += dz,  Q += dz * xhat   (dz, xhat in float: stats_kernel KIND 2)
+template <int NCOL, int SC>
+SDB_DEV void epilogue_tile_bstats(const ConvArgs& a, const CUtensorMap* omap, const CUtensorMap* ymap, int m0, int n0,
+                                  int nk, uint32_t tacc, int q, int lane, int c_lo, uint8_t* ostg, uint8_t* ystg,
+                                  uint64_t* ybar, uint64_t* tfull_acc, uint32_t tfull_phase, uint64_t* tempty_acc,
+                                  int& sb, double* cs) {
+    constexpr int NSTEP = NCOL / SC;
+    constexpr int ROWB = SC * 2;
+    constexpr int BUFB = 32 * ROWB;
+    // each ring slot is used NSTEP / 2 times per tile: an even count keeps the
+    // barrier parity aligned with js at the start of every tile
+    static_assert((NSTEP / 2) % 2 == 0, "two-slot ring parity");
+    const int cbase = n0 + c_lo;
+    auto issue = [&](int js) {
+        if (lane == 0 && js < NSTEP) {
+            uint64_t* bar = &ybar[js & 1];
+            mbar_arrive_expect_tx(bar, BUFB);
+            tma_load_2d(smem_u32(ystg + (js & 1) * BUFB), ymap, bar, cbase + js * SC, m0 + q * 32);
+        }
+    };
+    issue(0);
+    issue(1);
+    const float slope = a.bs_slope, inv_slope = 1.0f / a.bs_slope;
+    mbar_wait(tfull_acc, tfull_phase);
+    tc_fence_after();
+#pragma unroll
+    for (int js = 0; js < NSTEP; ++js) {
+        uint32_t v[SC];
+        tmem_ld_cols<SC>(tacc + (static_cast<uint32_t>(q * 32) << 16) + c_lo + js * SC, v);
+        if (js == NSTEP - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tempty_acc);
+        }
+        if (nk == 0) {
+#pragma unroll
+            for (int j = 0; j < SC; ++j) v[j] = 0u;
+        }
+        if (lane == 0) bulk_wait_read<1>();
+        __syncwarp();
+        uint8_t* buf = ostg + sb * BUFB;
+#pragma unroll
+        for (int j = 0; j < SC / 8; ++j) {
+            const uint4 pk = make_uint4(pack_half2(__uint_as_float(v[8 * j]), __uint_as_float(v[8 * j + 1])),
+                                        pack_half2(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3])),
+                                        pack_half2(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5])),
+                                        pack_half2(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7])));
+            const int pj = SC == 32 ? (j ^ ((lane >> 1) & 3)) : (j ^ ((lane >> 2) & 1));
+            *reinterpret_cast<uint4*>(buf + lane * ROWB + pj * 16) = pk;
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+            tma_store_2d(omap, smem_u32(buf), cbase + js * SC, m0 + q * 32);
+            bulk_commit();
+        }
+        // statistics over the staged dy box and the y box of the same rows
+        mbar_wait(&ybar[js & 1], (js >> 1) & 1);
+        const uint8_t* yb = ystg + (js & 1) * BUFB;
+        {
+            const int col = SC == 32 ? lane : (lane & 15);
+            const int r0 = SC == 32 ? 0 : (lane >> 4) * 16;
+            constexpr int NR = SC == 32 ? 32 : 16;
+            const int gcol = cbase + js * SC + col;
+            const bool ok = gcol < a.C;
+            const float ig = ok ? 1.0f / a.bs_gamma[gcol] : 0.f;
+            const float bt = ok ? a.bs_beta[gcol] : 0.f;
+            double s = 0.0, qq = 0.0;
+#pragma unroll 8
+            for (int rr = 0; rr < NR; ++rr) {
+                const int r = r0 + rr;
+                const int j = col >> 3;
+                const int pj = SC == 32 ? (j ^ ((r >> 1) & 3)) : (j ^ ((r >> 2) & 1));
+                const int off = r * ROWB + pj * 16 + (col & 7) * 2;
+                const float dyv = __half2float(*reinterpret_cast<const __half*>(buf + off));
+                const float yv = __half2float(*reinterpret_cast<const __half*>(yb + off));
+                const float z = yv >= 0.f ? yv : __fmul_rn(yv, inv_slope);
+                const float dz = __fmul_rn(dyv, yv > 0.f ? 1.f : slope);
+                const float xh = __fmul_rn(__fsub_rn(z, bt), ig);
+                s = __dadd_rn(s, static_cast<double>(dz));
+                qq = __fma_rn(static_cast<double>(dz), static_cast<double>(xh), qq);
+            }
+            if (SC == 16) {
+                const double so = __shfl_down_sync(0xffffffffu, s, 16), qo = __shfl_down_sync(0xffffffffu, qq, 16);
+                s = __dadd_rn(s, so);
+                qq = __dadd_rn(qq, qo);
+            }
+            if (ok) {
+                cs[2 * js] = __dadd_rn(cs[2 * js], s);
+                cs[2 * js + 1] = __dadd_rn(cs[2 * js + 1], qq);
+            }
+        }
+        // the y slot is free again (all lanes read it): reload it two steps ahead
+        fence_proxy_async();
+        __syncwarp();
+        issue(js + 2);
+        sb ^= 1;
+    }
+}
+
 // ============================================================ all-TMA tcgen05 kernel
 // Both operands arrive by TMA, the activation side through the im2col mode of
 // cp.async.bulk.tensor (the hardware walks the output-pixel traversal of the
@@ -1165,6 +1278,34 @@ __global__ void __launch_bounds__(TmaCfg<MODE, BN, ST, EPI>::kThreads, (BN <= 12
                 epilogue_tile_resid<kNCol, Cfg::kSC>(a, &tm.o, &tm.r, m0, n0, nk, tmem + acc * BN, warp & 3, lane,
                                                      c_lo, ostg, rstg, rbar + 2 * ew, &tfull[acc], (lt >> 1) & 1,
                                                      &tempty[acc], sb);
+            }
+            if (lane == 0) bulk_wait_all();
+            __syncwarp();
+        } else if constexpr (EPI == 2) {
+            int lt = 0, sb = 0;
+            uint8_t* ostg = reinterpret_cast<uint8_t*>(staging) + ew * 4 * (32 * Cfg::kSC * 2);
+            uint8_t* ystg = ostg + 2 * (32 * Cfg::kSC * 2);
+            constexpr int kStep = kNCol / Cfg::kSC;
+            double cs[2 * kStep];
+#pragma unroll
+            for (int j = 0; j < 2 * kStep; ++j) cs[j] = 0.0;
+            for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++lt) {
+                int m0, n0, kb0, nk;
+                tile_coords(t, m0, n0, kb0, nk);
+                const int acc = lt & 1;
+                epilogue_tile_bstats<kNCol, Cfg::kSC>(a, &tm.o, &tm.r, m0, n0, nk, tmem + acc * BN, warp & 3, lane,
+                                                      c_lo, ostg, ystg, rbar + 2 * ew, &tfull[acc], (lt >> 1) & 1,
+                                                      &tempty[acc], sb, cs);
+            }
+            // stats[cta][quadrant][sum dz | sum dz*xhat][BN] (every tile of a CTA has the same n0)
+            const int lanes = Cfg::kSC == 32 ? 32 : 16;
+            if (lane < lanes) {
+                double* o = a.stats + (static_cast<int64_t>(blockIdx.x) * 4 + (warp & 3)) * 2 * BN;
+#pragma unroll
+                for (int js = 0; js < kStep; ++js) {
+                    o[c_lo + js * Cfg::kSC + lane] = cs[2 * js];
+                    o[BN + c_lo + js * Cfg::kSC + lane] = cs[2 * js + 1];
+                }
             }
             if (lane == 0) bulk_wait_all();
             __syncwarp();
@@ -1642,7 +1783,8 @@ static cudaError_t launch_tma(ConvArgs a, int splits, cudaStream_t st, ConvStats
     // fused output statistics need every CTA on one column block (grid a
     // multiple of tiles_n): e.g. the res5 expansion convs (tiles_n = 8) give up
     // 4 of 148 CTAs (< 3% of a ~80 us GEMM) to save a 50 us statistics pass
-    if (MODE == FPROP && EPI == 0 && cst && grid % tiles_n != 0 && grid >= tiles_n) grid -= grid % tiles_n;
+    if (((MODE == FPROP && EPI == 0) || EPI == 2) && cst && grid % tiles_n != 0 && grid >= tiles_n)
+        grid -= grid % tiles_n;
     if (MODE == WGRAD) {
         // experiment knob: SMs a wgrad may occupy (leaves room for the concurrent norm chain)
         static const int cap = [] { const char* e = std::getenv("SDB_WGRAD_SMS"); return e ? std::atoi(e) : 0; }();
@@ -1722,6 +1864,28 @@ static cudaError_t launch_tma(ConvArgs a, int splits, cudaStream_t st, ConvStats
         ok = make_tmap(&tm.o, a.out, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_64B) &&
              make_tmap(&tm.r, a.addend, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_64B);
         a.tma_out = 0;
+    }
+    if (EPI == 2 && ok) {
+        // output and stored-y views [N*H*W][C], SC x 32 boxes (the IABN-backward statistics)
+        const uint64_t dims[2] = {static_cast<uint64_t>(a.C), static_cast<uint64_t>(a.N) * a.H * a.W};
+        const uint64_t strides[1] = {static_cast<uint64_t>(a.C) * 2};
+        const uint32_t box[2] = {static_cast<uint32_t>(Cfg::kSC), 32};
+        const CUtensorMapSwizzle swz = Cfg::kSC == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
+        ok = cst && cst->bs_y && make_tmap(&tm.o, a.out, 2, dims, strides, box, swz) &&
+             make_tmap(&tm.r, cst->bs_y, 2, dims, strides, box, swz);
+        a.tma_out = 0;
+        if (ok) {
+            const size_t need = static_cast<size_t>(grid) * 4 * 2 * BN * sizeof(double);
+            if (grid % tiles_n != 0 || need > cst->cap_bytes) return cudaErrorInvalidValue;
+            a.stats = cst->buf;
+            cst->produced = 1;
+            cst->ctas = grid;
+            cst->tiles_n = tiles_n;
+            cst->bn = BN;
+        }
+        if (!ok) return cudaErrorInvalidValue;
+        return launch_pdl(conv_tma_kernel<MODE, BN, ST, EPI>, dim3(grid), dim3(Cfg::kThreads), Cfg::kSmem, st, a,
+                          tiles_m, tiles_n, n_tiles, tm);
     }
     if (!ok) return cudaErrorInvalidValue;
     a.stats = nullptr;
@@ -1859,7 +2023,7 @@ cudaError_t conv_fprop(const ConvShape& g, int dtype, const void* x, const void*
 
 cudaError_t conv_dgrad(const ConvShape& g, int dtype, const void* dy, const void* w, void* dx, int accumulate,
                        cudaStream_t st, const void* addend, const void* mask, float mask_neg,
-                       const uint8_t* mask_bits) {
+                       const uint8_t* mask_bits, ConvStats* bstats) {
     ConvArgs base = make_args(g);
     base.x = dy; base.w = w; base.out = dx; base.accumulate = accumulate || addend != nullptr;
     base.mask = mask;
@@ -1912,8 +2076,20 @@ cudaError_t conv_dgrad(const ConvShape& g, int dtype, const void* dy, const void
             } else if (tc_ok(g, dtype)) {
                 a.tma_b = (g.K % kBK) == 0 ? 1 : 0;
                 static const bool no_resid = std::getenv("SDB_CONV_NO_RESID_EPI") != nullptr;
-                if (tma_ok(a, DGRAD) && a.mbits && a.accumulate && sd == 1 && tma_bn(a, DGRAD) == 256 && (g.C % 32) == 0 &&
-                    !no_resid)
+                static const bool no_bstats = std::getenv("SDB_NO_FUSED_BWD_STATS") != nullptr;
+                if (bstats) bstats->produced = 0;
+                if (bstats && bstats->bs_y && !no_bstats && tma_ok(a, DGRAD) && sd == 1 && !a.accumulate && !a.mask &&
+                    (g.C % 16) == 0) {
+                    a.bs_gamma = bstats->bs_gamma;
+                    a.bs_beta = bstats->bs_beta;
+                    a.bs_slope = bstats->bs_slope;
+                    switch (tma_bn(a, DGRAD)) {
+                        case 256: e = launch_tma<DGRAD, 256, 3, 2>(a, 1, st, bstats); break;
+                        case 128: e = launch_tma<DGRAD, 128, 2, 2>(a, 1, st, bstats); break;
+                        default: e = launch_tma<DGRAD, 64, 3, 2>(a, 1, st, bstats); break;
+                    }
+                } else if (tma_ok(a, DGRAD) && a.mbits && a.accumulate && sd == 1 && tma_bn(a, DGRAD) == 256 &&
+                           (g.C % 32) == 0 && !no_resid)
                     e = launch_tma<DGRAD, 256, 3, 1>(a, 1, st);
                 else
                     e = tma_ok(a, DGRAD) ? launch_tma_pick<DGRAD>(a, 1, st) : launch_tc_pick<DGRAD>(a, 1, st);

@@ -235,6 +235,9 @@ struct sdb_det {
     size_t ws_bytes = 0;
     // fused output statistics of the fprop that precedes each norm layer
     ConvStats cst{};
+    // fused InPlace-ABN backward statistics of the dgrad that produces a norm
+    // layer's output gradient (bn1 / bn2 of every bottleneck)
+    ConvStats cst_b{};
     // host staging, double-buffered: a call waits only for the copies that
     // read its slot two calls ago (never for the previous step's compute)
     static constexpr int kStage = 2;
@@ -529,6 +532,12 @@ void norm_bwd(sdb_det* d, const NormL& n, const Act& z, const Act& a, const void
     if (d->cfg.mode == 0) {
         CK(bn_backward(d->dt, da, z.p, n.act == 1 ? a.p : nullptr, d->bnp(n.pg), n.mean, n.invstd, dz,
                        d->bngp(n.pg), d->bngp(n.pb), rows, n.C, d->ws, d->ctx->stream));
+    } else if (d->cst_b.produced && d->cst_b.bs_y == a.p) {
+        // statistics came out of the dgrad epilogue that produced da: finalize + apply
+        CK(iabn_backward_conv_stats(d->dt, da, a.p, d->bnp(n.pg), d->bnp(n.pb), n.invstd, dz, d->bngp(n.pg),
+                                    d->bngp(n.pb), rows, n.C, n.slope, d->cst_b, static_cast<float*>(d->ws),
+                                    d->ctx->stream));
+        d->cst_b.produced = 0;
     } else {
         CK(iabn_backward(d->dt, da, a.p, d->bnp(n.pg), d->bnp(n.pb), n.mean, n.invstd, dz, d->bngp(n.pg),
                          d->bngp(n.pb), rows, n.C, n.slope, d->ws, d->ctx->stream));
@@ -590,11 +599,26 @@ void block_fwd(sdb_det* d, Block& b) {
 
 // ------------------------------------------------------------------ backward helpers
 void dgrad(sdb_det* d, const ConvL& c, const void* dy, void* dx, int accumulate, const void* addend = nullptr,
-           const void* mask = nullptr, float mask_neg = 0.0f, const uint8_t* mask_bits = nullptr) {
+           const void* mask = nullptr, float mask_neg = 0.0f, const uint8_t* mask_bits = nullptr,
+           ConvStats* bstats = nullptr) {
     PScope ps(d, P_DGRAD, conv_flops(c.g), 0, c.g.stride * c.g.stride);
-    if (d->prof.on) { ps.label = shape_label(mask_bits ? "dgrad+res" : "dgrad", c.g); ps.flops_ = conv_flops(c.g); }
+    if (d->prof.on) {
+        ps.label = shape_label(mask_bits ? "dgrad+res" : (bstats ? "dgrad+bstats" : "dgrad"), c.g);
+        ps.flops_ = conv_flops(c.g);
+    }
     CK(conv_dgrad(c.g, d->dt, dy, d->wdev_ptr(c.p), dx, accumulate, d->ctx->stream, addend, mask, mask_neg,
-                  mask_bits));
+                  mask_bits, bstats));
+}
+
+// the dgrad that writes the output gradient of InPlace-ABN layer n (stored
+// output y): reduce n's backward statistics in its epilogue (fp16 IABN mode)
+ConvStats* bstats_for(sdb_det* d, const NormL& n, const Act& y) {
+    if (!d->cst_b.buf || d->cfg.mode != 1 || std::getenv("SDB_NO_FUSED_BWD_STATS")) return nullptr;
+    d->cst_b.bs_y = y.p;
+    d->cst_b.bs_gamma = d->bnp(n.pg);
+    d->cst_b.bs_beta = d->bnp(n.pb);
+    d->cst_b.bs_slope = n.slope;
+    return &d->cst_b;
 }
 
 struct Bwd {
@@ -761,11 +785,11 @@ void block_bwd(Bwd& B, Block& b, const void* dS, void* dx, void* s1, void* s2, c
     z = dz_buf(B, s1);
     norm_bwd(d, b.n3, b.z3, b.b3, dS, z);
     conv_wgrad_to(B, b.c3, b.a2, z);
-    dgrad(d, b.c3, z, s2, 0);
+    dgrad(d, b.c3, z, s2, 0, nullptr, nullptr, 0.0f, nullptr, bstats_for(d, b.n2, b.a2));
     z = dz_buf(B, s1);
     norm_bwd(d, b.n2, b.z2, b.a2, s2, z);
     conv_wgrad_to(B, b.c2, b.a1, z);
-    dgrad(d, b.c2, z, s2, 0);
+    dgrad(d, b.c2, z, s2, 0, nullptr, nullptr, 0.0f, nullptr, bstats_for(d, b.n1, b.a1));
     z = dz_buf(B, s1);
     norm_bwd(d, b.n1, b.z1, b.a1, s2, z);
     conv_wgrad_to(B, b.c1, b.in, z);
@@ -1260,6 +1284,10 @@ int sdb_det_create(sdb_ctx* ctx, const sdb_det_config* cfgp, sdb_det** out) {
         if (d->dt == kF16) {
             d->cst.cap_bytes = static_cast<size_t>(2 * 148) * 4 * 2 * 256 * sizeof(double);  // 2 CTAs x 148 SMs
             d->cst.buf = static_cast<double*>(d->alloc(d->cst.cap_bytes));
+            if (cf.mode == 1) {
+                d->cst_b.cap_bytes = d->cst.cap_bytes;
+                d->cst_b.buf = static_cast<double*>(d->alloc(d->cst_b.cap_bytes));
+            }
         }
         d->comm_on = ctx->nccl != nullptr;
         d->defer_wgrad = d->dt == kF16 && std::getenv("SDB_NO_DEFER_WGRAD") == nullptr;

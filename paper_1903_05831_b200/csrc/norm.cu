@@ -553,9 +553,12 @@ __global__ void syncbn_coef_kernel(const float* __restrict__ red, const float* _
 // (T = 4 * ctas / tiles_n quadrant terms).  Same thread layout and fixed
 // reduction tree as finalize_kernel (8 channels per CTA, 128 term groups).
 constexpr int kConvTermsMax = 2 * kNumSMs * 4;
+// mode 0 / 1: BN / IABN forward statistics -> mean, invstd; mode 3: IABN
+// backward sums from a dgrad epilogue -> dgamma, dbeta, coef (as finalize_kernel)
 __global__ void __launch_bounds__(kFinThreads) finalize_conv_kernel(const double* __restrict__ cs, int ctas, int tiles_n,
                                                                     int bn, int C, int64_t count, float eps, int mode,
-                                                                    float* mean, float* invstd) {
+                                                                    float* mean, float* invstd, float* dgamma = nullptr,
+                                                                    float* dbeta = nullptr, float* coef = nullptr) {
     __shared__ double rs[32][kFinCh], rq[32][kFinCh];
     pdl_wait();
     pdl_trigger();
@@ -612,6 +615,13 @@ __global__ void __launch_bounds__(kFinThreads) finalize_conv_kernel(const double
         Q += __shfl_xor_sync(0xffffffffu, Q, o);
     }
     if (lane >= kFinCh || c >= C) return;
+    if (mode == 3) {
+        dgamma[c] = static_cast<float>(Q);
+        dbeta[c] = static_cast<float>(S);
+        coef[c] = static_cast<float>(S / static_cast<double>(count));
+        coef[C + c] = static_cast<float>(Q / static_cast<double>(count));
+        return;
+    }
     double mu, var;
     if (mode == 0) {
         const float sf = static_cast<float>(S), qf = static_cast<float>(Q);
@@ -780,7 +790,8 @@ cudaError_t bn_forward_conv_stats(int dtype, const void* x, const float* gamma, 
                                   const ConvStats& cs, cudaStream_t st) {
     if (!cs.produced || 4 * (cs.ctas / cs.tiles_n) > kConvTermsMax) return cudaErrorInvalidValue;
     cudaError_t e = launch_pdl(finalize_conv_kernel, dim3((C + kFinCh - 1) / kFinCh), dim3(kFinThreads), 0, st, cs.buf,
-                               cs.ctas, cs.tiles_n, cs.bn, C, rows, eps, act == 2 ? 1 : 0, mean, invstd);
+                               cs.ctas, cs.tiles_n, cs.bn, C, rows, eps, act == 2 ? 1 : 0, mean, invstd,
+                               static_cast<float*>(nullptr), static_cast<float*>(nullptr), static_cast<float*>(nullptr));
     if (e != cudaSuccess || !y) return e;
     const Plan pl = plan_for(rows, C, dtype == kF16 ? 2 : 4);
     ApplyArgs aa{};
@@ -788,6 +799,21 @@ cudaError_t bn_forward_conv_stats(int dtype, const void* x, const float* gamma, 
     aa.slope = slope; aa.act = act; aa.n8 = rows * C / 8; aa.C = C;
     if (act == 2) return dtype == kF16 ? run_apply<__half, 1, 1>(aa, rows, pl, st) : run_apply<float, 1, 1>(aa, rows, pl, st);
     return dtype == kF16 ? run_apply<__half, 0, 1>(aa, rows, pl, st) : run_apply<float, 0, 1>(aa, rows, pl, st);
+}
+
+cudaError_t iabn_backward_conv_stats(int dtype, const void* dy, const void* y, const float* gamma, const float* beta,
+                                     const float* invstd, void* dx, float* dgamma, float* dbeta, int64_t rows, int C,
+                                     float slope, const ConvStats& cs, float* coef, cudaStream_t st) {
+    if (!cs.produced || 4 * (cs.ctas / cs.tiles_n) > kConvTermsMax) return cudaErrorInvalidValue;
+    cudaError_t e = launch_pdl(finalize_conv_kernel, dim3((C + kFinCh - 1) / kFinCh), dim3(kFinThreads), 0, st, cs.buf,
+                               cs.ctas, cs.tiles_n, cs.bn, C, rows, 0.f, 3, static_cast<float*>(nullptr),
+                               static_cast<float*>(nullptr), dgamma, dbeta, coef);
+    if (e != cudaSuccess) return e;
+    const Plan pl = plan_for(rows, C, dtype == kF16 ? 2 : 4);
+    ApplyArgs aa{};
+    aa.a = y; aa.dy = dy; aa.out = dx; aa.gamma = gamma; aa.beta = beta; aa.invstd = invstd; aa.coef = coef;
+    aa.slope = slope; aa.n8 = rows * C / 8; aa.C = C;
+    return dtype == kF16 ? run_apply<__half, 3, 2>(aa, rows, pl, st) : run_apply<float, 3, 2>(aa, rows, pl, st);
 }
 
 // ---------------------------------------------------------------- SyncBN

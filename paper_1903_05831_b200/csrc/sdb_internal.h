@@ -28,6 +28,12 @@ struct ConvStats {
     double* buf;
     size_t cap_bytes;
     int produced, ctas, tiles_n, bn;
+    // dgrad only: the InPlace-ABN layer whose backward statistics the epilogue
+    // reduces ([sum dz | sum dz*xhat] per column, src/memopt.cpp:305-314)
+    const void* bs_y = nullptr;
+    const float* bs_gamma = nullptr;
+    const float* bs_beta = nullptr;
+    float bs_slope = 1.0f;
 };
 cudaError_t conv_fprop(const ConvShape& g, int dtype, const void* x, const void* w, void* y, cudaStream_t st,
                        ConvStats* stats = nullptr);
@@ -36,9 +42,12 @@ cudaError_t conv_fprop(const ConvShape& g, int dtype, const void* x, const void*
 // the ReLU / leaky that produced this layer's input, fused into the epilogue
 // mask_bits (optional): sign bitmap of `mask` (bit c%8 of byte [row][c/8] = mask > 0),
 // used by the stride-1 residual epilogue instead of the fp16 mask when present
+// bstats (optional, fp16 stride-1 dgrads without addend/mask): the output
+// feeds an InPlace-ABN backward; its statistics are reduced in the epilogue
+// (bstats->produced reports it) for iabn_backward_conv_stats
 cudaError_t conv_dgrad(const ConvShape& g, int dtype, const void* dy, const void* w, void* dx, int accumulate,
                        cudaStream_t st, const void* addend = nullptr, const void* mask = nullptr,
-                       float mask_neg = 0.0f, const uint8_t* mask_bits = nullptr);
+                       float mask_neg = 0.0f, const uint8_t* mask_bits = nullptr, ConvStats* bstats = nullptr);
 size_t conv_wgrad_workspace(const ConvShape& g, int dtype);
 cudaError_t conv_wgrad(const ConvShape& g, int dtype, const void* x, const void* dy, void* dw, void* ws,
                        size_t ws_bytes, cudaStream_t st);
@@ -100,6 +109,12 @@ cudaError_t syncbn_backward_finish(int dtype, const void* dy, const void* x, con
                                    const float* mean, const float* invstd, const float* red, const float* agg_fwd,
                                    void* dx, float* dgamma, float* dbeta, int64_t rows, int C, void* ws,
                                    cudaStream_t st);
+// iabn_backward from the statistics a dgrad epilogue reduced (ConvStats with
+// bs_y): finalize into dgamma/dbeta and the coefficients (coef: 2C floats of
+// workspace), then the apply pass dx = f(dy, y)
+cudaError_t iabn_backward_conv_stats(int dtype, const void* dy, const void* y, const float* gamma, const float* beta,
+                                     const float* invstd, void* dx, float* dgamma, float* dbeta, int64_t rows, int C,
+                                     float slope, const ConvStats& cs, float* coef, cudaStream_t st);
 cudaError_t iabn_backward(int dtype, const void* dy, const void* y, const float* gamma, const float* beta,
                           const float* mean, const float* invstd, void* dx, float* dgamma, float* dbeta,
                           int64_t rows, int C, float slope, void* ws, cudaStream_t st);

@@ -61,6 +61,7 @@ _SIGS = {
     "sdb_allreduce_sum": [_P, _I, _P, _L, _P],
     "sdb_comm_check": [_P],
     "sdb_conv_fprop_stats": [_P, _I, _P, _P, _P] + [_I] * 9 + [_F, _I, _P, _P, _P, _P],
+    "sdb_conv_dgrad_iabn_bwd": [_P, _I, _P, _P, _P] + [_I] * 8 + [_P, _P, _P, _P, _F, _P, _P, _P, _P, _P],
     "sdb_roialign_fwd_folded": [_P, _I, _P, _I, _I, _I, _I, _P, _I, _I, _F, _I, _I, _P, _P],
     "sdb_roialign_bwd_folded": [_P, _I, _P, _I, _I, _I, _I, _P, _I, _I, _F, _I, _I, _P, _P],
 }
@@ -152,6 +153,24 @@ def conv_fprop_stats_nhwc(x, w, stride, pad, eps=1e-5, iabn=False):
     check(L().sdb_conv_fprop_stats(ctx(), dt(x), ptr(x), ptr(w), ptr(y), N, H, W, Cc, K, R, S, stride, pad, eps,
                                    1 if iabn else 0, ptr(mean), ptr(invstd), C.byref(fused), stream()))
     return y, mean, invstd, bool(fused.value)
+
+
+def conv_dgrad_iabn_bwd_nhwc(dy, w, y, gamma, beta, invstd, slope, pad):
+    """stride-1 dgrad producing the gradient of the IABN output y, then that
+    layer's IABN backward (statistics fused into the dgrad epilogue on the
+    tensor-core path); returns (dy_iabn, dz, dgamma, dbeta, fused)"""
+    _require_cuda(dy, w, y)
+    N, H, W, Cc = y.shape
+    K, R, S, _ = w.shape
+    dyi = torch.empty_like(y)
+    dz = torch.empty_like(y)
+    dgamma = torch.empty(Cc, device=y.device, dtype=torch.float32)
+    dbeta = torch.empty_like(dgamma)
+    fused = C.c_int(0)
+    check(L().sdb_conv_dgrad_iabn_bwd(ctx(), dt(y), ptr(dy), ptr(w), ptr(dyi), N, H, W, Cc, K, R, S, pad, ptr(y),
+                                      ptr(gamma), ptr(beta), ptr(invstd), slope, ptr(dz), ptr(dgamma), ptr(dbeta),
+                                      C.byref(fused), stream()))
+    return dyi, dz, dgamma, dbeta, bool(fused.value)
 
 
 def conv_dgrad_nhwc(dy, w, x_shape, stride, pad, out=None, accumulate=False):

@@ -389,3 +389,59 @@ def test_fused_norm_statistics_in_fprop_epilogue(case, iabn):
     var = (yd * yd).mean(0) - mu * mu
     assert torch.allclose(mean.double(), mu, rtol=1e-5, atol=1e-6)
     assert torch.allclose(invstd.double(), 1.0 / torch.sqrt(var.clamp_min(0) + 1e-5), rtol=1e-4)
+
+
+@pytest.mark.parametrize("case", [
+    # (N, H, W, C = IABN channels = dgrad output, K = conv output channels, R): dgrad tile widths 256 / 128 / 64
+    (256, 7, 7, 512, 2048, 1),     # res5 conv3-like: BN = 256, M = 12544
+    (2, 50, 84, 256, 1024, 1),     # res4 conv3: BN = 128 (narrow rule), M = 8400
+    (2, 47, 33, 128, 128, 3),      # res3 conv2-like 3x3: BN = 128, ragged M = 3102
+    (1, 63, 41, 64, 256, 1),       # res2 conv3-like: BN = 64, ragged M = 2583
+    (2, 40, 37, 64, 64, 3),        # res2 conv2-like 3x3: BN = 64
+])
+def test_dgrad_fused_iabn_backward_statistics(ref, case):
+    """The InPlace-ABN backward sums reduced in the dgrad epilogue (y by TMA next
+    to the staged dy box) give the same dgamma/dbeta/dz as the separate
+    statistics pass over the same tensors; the dgrad output itself is bitwise
+    the plain dgrad; and both agree with the reference iabn_backward"""
+    from paper_1903_05831_b200 import simdet as sd
+    N, H, W, Cc, K, R = case
+    pad = R // 2
+    g = torch.Generator(device="cuda").manual_seed(sum(case))
+    # y: a stored IABN output (leaky 0.1 of N(beta, gamma)), dy: the conv's output gradient
+    gamma = (torch.rand(Cc, generator=g, device="cuda") + 0.5)
+    beta = (torch.rand(Cc, generator=g, device="cuda") - 0.5) * 0.4
+    xh = torch.randn((N, H, W, Cc), generator=g, device="cuda")
+    yv = xh * gamma + beta
+    y = torch.where(yv >= 0, yv, 0.1 * yv).half()
+    invstd = (torch.rand(Cc, generator=g, device="cuda") + 0.5)
+    dy = torch.randn((N, H, W, K), generator=g, device="cuda").half()
+    w = (torch.randn((K, R, R, Cc), generator=g, device="cuda") * (1.0 / (K * R * R) ** 0.5)).half()
+    dyi, dz, dgm, dbt, fused = sd.conv_dgrad_iabn_bwd_nhwc(dy, w, y, gamma, beta, invstd, 0.1, pad)
+    assert fused, "the fused-statistics dgrad epilogue did not run for this shape"
+    # unfused: plain dgrad, then the IABN backward statistics pass
+    dyi2 = sd.conv_dgrad_nhwc(dy, w, (N, H, W, Cc), 1, pad)
+    rows = N * H * W
+    dz2 = torch.empty_like(dz)
+    dgm2, dbt2 = torch.empty_like(dgm), torch.empty_like(dbt)
+    sd.check(sd.L().sdb_iabn_bwd(sd.ctx(), 1, sd.ptr(dyi2), sd.ptr(y), sd.ptr(gamma), sd.ptr(beta), None,
+                                 sd.ptr(invstd), sd.ptr(dz2), sd.ptr(dgm2), sd.ptr(dbt2), rows, Cc, 0.1, sd.stream()))
+    torch.cuda.synchronize()
+    assert torch.equal(dyi, dyi2), "the dgrad output must not depend on the epilogue variant"
+    # same fp64 sums in another order: float results agree to the last bits
+    assert torch.allclose(dgm, dgm2, rtol=1e-6, atol=1e-5), (dgm - dgm2).abs().max()
+    assert torch.allclose(dbt, dbt2, rtol=1e-6, atol=1e-5), (dbt - dbt2).abs().max()
+    assert (dz.float() - dz2.float()).abs().max() <= 2e-3 * dz2.float().abs().max()
+    # the reference iabn_backward on the same (NCHW) tensors
+    ynp = np.ascontiguousarray(y.float().permute(0, 3, 1, 2).cpu().numpy())
+    dnp = np.ascontiguousarray(dyi.float().permute(0, 3, 1, 2).cpu().numpy())
+    dx_r = np.zeros_like(ynp)
+    dg_r, db_r = np.zeros(Cc, np.float32), np.zeros(Cc, np.float32)
+    gn, bn_, isn = (gamma.cpu().numpy(), beta.cpu().numpy(), invstd.cpu().numpy())
+    mean0 = np.zeros(Cc, np.float32)
+    assert ref.ref_iabn_backward(oracle.p(dnp), oracle.p(ynp), N, Cc, H, W, oracle.p(gn), oracle.p(bn_),
+                                 oracle.p(mean0), oracle.p(isn), 1e-5, 0.1, 1, oracle.p(dx_r), oracle.p(dg_r),
+                                 oracle.p(db_r)) == 0
+    assert_close(dgm, dg_r, 1e-5, "dgamma vs reference")
+    assert_close(dbt, db_r, 1e-5, "dbeta vs reference")
+    assert_close(dz.float().permute(0, 3, 1, 2), dx_r, 1e-2, "dz vs reference")

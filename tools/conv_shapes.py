@@ -15,6 +15,8 @@ SHAPES = [  # (N, H, W, C, K, R, stride)
     (2, 50, 84, 256, 256, 3, 1),
     (2, 200, 334, 64, 256, 1, 1),
 ]
+if len(sys.argv) > 1 and sys.argv[1] == "res5_1x1":
+    SHAPES = [(1024, 7, 7, 512, 2048, 1, 1), (1024, 7, 7, 2048, 512, 1, 1)]
 g = torch.Generator(device="cuda").manual_seed(0)
 ops = []
 for (N, H, W, C, K, R, s) in SHAPES:
