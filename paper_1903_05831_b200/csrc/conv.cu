@@ -918,9 +918,11 @@ SDB_DEV void epilogue_tile_bstats(const ConvArgs& a, const CUtensorMap* omap, co
 #pragma unroll
             for (int j = 0; j < SC; ++j) v[j] = 0u;
         }
-        if (lane == 0) bulk_wait_read<1>();
+        // one output box (the smem budget keeps the mainloop's stages): the
+        // previous step's store has had the statistics pass to drain it
+        if (lane == 0) bulk_wait_read<0>();
         __syncwarp();
-        uint8_t* buf = ostg + sb * BUFB;
+        uint8_t* buf = ostg;
 #pragma unroll
         for (int j = 0; j < SC / 8; ++j) {
             const uint4 pk = make_uint4(pack_half2(__uint_as_float(v[8 * j]), __uint_as_float(v[8 * j + 1])),
@@ -976,8 +978,8 @@ SDB_DEV void epilogue_tile_bstats(const ConvArgs& a, const CUtensorMap* omap, co
         fence_proxy_async();
         __syncwarp();
         issue(js + 2);
-        sb ^= 1;
     }
+    (void)sb;
 }
 
 // ============================================================ all-TMA tcgen05 kernel
@@ -1025,7 +1027,9 @@ struct TmaCfg {
     static constexpr int kStage = kABytes + kBBytes;
     static constexpr int kEpiWarps = BN == 256 ? 8 : 4;
     static constexpr int kSC = BN == 256 ? 32 : 16;
-    static constexpr int kStaging = EPI ? kEpiWarps * 4 * 32 * kSC * 2 : kEpiWarps * 32 * kSC * 4;
+    // EPI 1: 2 output boxes + 2 addend slots per warp; EPI 2: 1 output box + 2 y slots
+    static constexpr int kStaging = EPI == 1 ? kEpiWarps * 4 * 32 * kSC * 2
+                                  : EPI == 2 ? kEpiWarps * 3 * 32 * kSC * 2 : kEpiWarps * 32 * kSC * 4;
     static constexpr int kSmem = ST * kStage + kStaging + 1024 + 256;
     static constexpr int kThreads = 64 + 32 * kEpiWarps;
     static constexpr int kPerSM = BN <= 128 ? 2 : 1;
@@ -1283,8 +1287,8 @@ __global__ void __launch_bounds__(TmaCfg<MODE, BN, ST, EPI>::kThreads, (BN <= 12
             __syncwarp();
         } else if constexpr (EPI == 2) {
             int lt = 0, sb = 0;
-            uint8_t* ostg = reinterpret_cast<uint8_t*>(staging) + ew * 4 * (32 * Cfg::kSC * 2);
-            uint8_t* ystg = ostg + 2 * (32 * Cfg::kSC * 2);
+            uint8_t* ostg = reinterpret_cast<uint8_t*>(staging) + ew * 3 * (32 * Cfg::kSC * 2);
+            uint8_t* ystg = ostg + (32 * Cfg::kSC * 2);
             constexpr int kStep = kNCol / Cfg::kSC;
             double cs[2 * kStep];
 #pragma unroll
@@ -2079,15 +2083,15 @@ cudaError_t conv_dgrad(const ConvShape& g, int dtype, const void* dy, const void
                 static const bool no_bstats = std::getenv("SDB_NO_FUSED_BWD_STATS") != nullptr;
                 if (bstats) bstats->produced = 0;
                 if (bstats && bstats->bs_y && !no_bstats && tma_ok(a, DGRAD) && sd == 1 && !a.accumulate && !a.mask &&
-                    (g.C % 16) == 0) {
+                    (g.C % 16) == 0 && tma_bn(a, DGRAD) <= 128) {
                     a.bs_gamma = bstats->bs_gamma;
                     a.bs_beta = bstats->bs_beta;
                     a.bs_slope = bstats->bs_slope;
-                    switch (tma_bn(a, DGRAD)) {
-                        case 256: e = launch_tma<DGRAD, 256, 3, 2>(a, 1, st, bstats); break;
-                        case 128: e = launch_tma<DGRAD, 128, 2, 2>(a, 1, st, bstats); break;
-                        default: e = launch_tma<DGRAD, 64, 3, 2>(a, 1, st, bstats); break;
-                    }
+                    // BN <= 128 only: the 256-wide tile cannot keep its 4 mainloop stages
+                    // next to the y ring, and 3 stages cost the res5 dgrads more than
+                    // the statistics pass they save (measured)
+                    if (tma_bn(a, DGRAD) == 128) e = launch_tma<DGRAD, 128, 3, 2>(a, 1, st, bstats);
+                    else e = launch_tma<DGRAD, 64, 4, 2>(a, 1, st, bstats);
                 } else if (tma_ok(a, DGRAD) && a.mbits && a.accumulate && sd == 1 && tma_bn(a, DGRAD) == 256 &&
                            (g.C % 32) == 0 && !no_resid)
                     e = launch_tma<DGRAD, 256, 3, 1>(a, 1, st);

@@ -391,15 +391,15 @@ def test_fused_norm_statistics_in_fprop_epilogue(case, iabn):
     assert torch.allclose(invstd.double(), 1.0 / torch.sqrt(var.clamp_min(0) + 1e-5), rtol=1e-4)
 
 
-@pytest.mark.parametrize("case", [
+@pytest.mark.parametrize("case,expect_fused", [
     # (N, H, W, C = IABN channels = dgrad output, K = conv output channels, R): dgrad tile widths 256 / 128 / 64
-    (256, 7, 7, 512, 2048, 1),     # res5 conv3-like: BN = 256, M = 12544
-    (2, 50, 84, 256, 1024, 1),     # res4 conv3: BN = 128 (narrow rule), M = 8400
-    (2, 47, 33, 128, 128, 3),      # res3 conv2-like 3x3: BN = 128, ragged M = 3102
-    (1, 63, 41, 64, 256, 1),       # res2 conv3-like: BN = 64, ragged M = 2583
-    (2, 40, 37, 64, 64, 3),        # res2 conv2-like 3x3: BN = 64
+    ((256, 7, 7, 512, 2048, 1), False),  # res5 conv3-like, BN = 256: unfused by design (stats pass)
+    ((2, 50, 84, 256, 1024, 1), True),   # res4 conv3: BN = 128 (narrow rule), M = 8400
+    ((2, 47, 33, 128, 128, 3), True),    # res3 conv2-like 3x3: BN = 128, ragged M = 3102
+    ((1, 63, 41, 64, 256, 1), True),     # res2 conv3-like: BN = 64, ragged M = 2583
+    ((2, 40, 37, 64, 64, 3), True),      # res2 conv2-like 3x3: BN = 64
 ])
-def test_dgrad_fused_iabn_backward_statistics(ref, case):
+def test_dgrad_fused_iabn_backward_statistics(ref, case, expect_fused):
     """The InPlace-ABN backward sums reduced in the dgrad epilogue (y by TMA next
     to the staged dy box) give the same dgamma/dbeta/dz as the separate
     statistics pass over the same tensors; the dgrad output itself is bitwise
@@ -418,7 +418,7 @@ def test_dgrad_fused_iabn_backward_statistics(ref, case):
     dy = torch.randn((N, H, W, K), generator=g, device="cuda").half()
     w = (torch.randn((K, R, R, Cc), generator=g, device="cuda") * (1.0 / (K * R * R) ** 0.5)).half()
     dyi, dz, dgm, dbt, fused = sd.conv_dgrad_iabn_bwd_nhwc(dy, w, y, gamma, beta, invstd, 0.1, pad)
-    assert fused, "the fused-statistics dgrad epilogue did not run for this shape"
+    assert fused == expect_fused, "which statistics path ran"
     # unfused: plain dgrad, then the IABN backward statistics pass
     dyi2 = sd.conv_dgrad_nhwc(dy, w, (N, H, W, Cc), 1, pad)
     rows = N * H * W
