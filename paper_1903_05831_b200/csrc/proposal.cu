@@ -20,6 +20,7 @@
 //   targets   fp64 IoU vs ground truth, Detectron-style labels, counter-RNG
 //             (mix64, src/dataset.cpp:11-17) priority sampling via radix select
 #include <algorithm>
+#include <cstdlib>
 #include <cfloat>
 
 #include "common.cuh"
@@ -474,11 +475,18 @@ __global__ void __launch_bounds__(256) topk_rank_decode_kernel(TopkMC m) {
 // per 256-thread CTA, tiles strided over a grid of a few CTAs per SM (the
 // (nwords x nwords x img) grid of 64-thread blocks spent most of its time
 // launching and retiring blocks, half of which exited at once).
+// Column band [w_lo, w_hi) of the triangle (tiles rb <= cb, w_lo <= cb < w_hi,
+// column-block major): the first launch covers the leading block of the sorted
+// candidates; the rest is computed only if the scan of that block did not fill
+// post_k (done[img] == 0 -- skipped otherwise).
 __global__ void __launch_bounds__(256) nms_mask2_kernel(const float* __restrict__ boxes, int k, int nwords, double thr,
-                                                       uint64_t* __restrict__ mask) {
+                                                       uint64_t* __restrict__ mask, int w_lo, int w_hi,
+                                                       const int* __restrict__ done) {
     __shared__ float4 cbox[4][64];
     const int img = blockIdx.y;
-    const int T = nwords * (nwords + 1) / 2;
+    if (done && done[img]) return;
+    auto tri = [](int n) { return n * (n + 1) / 2; };
+    const int T = tri(w_hi) - tri(w_lo);
     const int grp = threadIdx.x >> 6, t = threadIdx.x & 63;
     const float4* B = reinterpret_cast<const float4*>(boxes + static_cast<int64_t>(img) * k * 4);
     // fp32 screen: inter_f and uni_f are within ~2e-6 (relative) of the exact
@@ -493,16 +501,15 @@ __global__ void __launch_bounds__(256) nms_mask2_kernel(const float* __restrict_
         const bool live = tile < T;
         int rb = 0, cb = 0;
         if (live) {
-            // row block rb: first tile index S(rb) = rb*nwords - rb*(rb-1)/2 <= tile
-            int lo = 0, hi = nwords - 1;
+            // column block cb: tiles of columns [w_lo, cb) come first, tri(cb) - tri(w_lo) <= tile
+            int lo = w_lo, hi = w_hi - 1;
             while (lo < hi) {
                 const int mid = (lo + hi + 1) >> 1;
-                const int smid = mid * nwords - mid * (mid - 1) / 2;
-                if (smid <= tile) lo = mid;
+                if (tri(mid) - tri(w_lo) <= tile) lo = mid;
                 else hi = mid - 1;
             }
-            rb = lo;
-            cb = rb + (tile - (rb * nwords - rb * (rb - 1) / 2));
+            cb = lo;
+            rb = tile - (tri(cb) - tri(w_lo));
             const int jt = cb * 64 + t;
             if (jt < k) cbox[grp][t] = __ldg(B + jt);
         }
@@ -650,48 +657,57 @@ constexpr int kScan2Warps = 1 + 2 * kScan2GW;  // warp 0: decisions; then the ev
 constexpr int kScan2Threads = 32 * kScan2Warps;
 constexpr int kScan2MaxWords = 192;
 
+// nchunks < nwords: the scan of the leading block only (mask words < nchunks
+// computed): it sets done_out[img] = 1 and writes the outputs when post_k
+// boxes are kept inside the block, else done_out[img] = 0 and nothing is
+// written; a second launch with nchunks = nwords (after the rest of the mask)
+// scans again from the start unless done_in[img].  The keep decisions never depend on
+// words beyond the last chunk scanned, so the result equals the full scan.
 __global__ void __launch_bounds__(kScan2Threads) nms_scan2_kernel(const float* __restrict__ boxes,
                                                                   const uint64_t* __restrict__ mask,
                                                                   const float* __restrict__ scores, int k, int nwords,
                                                                   int post_k, float* __restrict__ rois,
                                                                   float* __restrict__ roi_scores,
                                                                   int32_t* __restrict__ keep_pos,
-                                                                  int32_t* __restrict__ count) {
+                                                                  int32_t* __restrict__ count, int nchunks,
+                                                                  int* __restrict__ done_out,
+                                                                  const int* __restrict__ done_in) {
     extern __shared__ uint64_t sm2[];
-    uint64_t* diag = sm2;                              // [nwords][64]
-    uint64_t* sdiag = diag + nwords * 64;              // [nwords][64]
-    uint64_t* removed = sdiag + nwords * 64;           // [nwords]
+    const int img = blockIdx.x;
+    if (done_in && done_in[img]) return;  // the leading-block scan already finished this image
+    uint64_t* diag = sm2;                              // [nchunks][64]
+    uint64_t* sdiag = diag + nchunks * 64;             // [nchunks][64]
+    uint64_t* removed = sdiag + nchunks * 64;          // [nchunks]
     __shared__ int rows[2][64];
     __shared__ int nrows[2];
     __shared__ uint64_t rows_ready[2], or_done[2];
-    __shared__ int kept_total;
-    const int img = blockIdx.x;
+    __shared__ int kept_total, complete;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint64_t* M = mask + static_cast<int64_t>(img) * k * nwords;
     // preload: diagonal and super-diagonal words of every chunk
     // (8 independent loads in flight per thread)
-    for (int e0 = tid; e0 < nwords * 64; e0 += 4 * kScan2Threads) {
+    for (int e0 = tid; e0 < nchunks * 64; e0 += 4 * kScan2Threads) {
         uint64_t dv[4], sv[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const int e = e0 + u * kScan2Threads;
             const int c = e >> 6, r = c * 64 + (e & 63);
             dv[u] = sv[u] = 0;
-            if (e < nwords * 64 && r < k) {
+            if (e < nchunks * 64 && r < k) {
                 dv[u] = __ldg(M + static_cast<int64_t>(r) * nwords + c);
-                if (c + 1 < nwords) sv[u] = __ldg(M + static_cast<int64_t>(r) * nwords + c + 1);
+                if (c + 1 < nchunks) sv[u] = __ldg(M + static_cast<int64_t>(r) * nwords + c + 1);
             }
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const int e = e0 + u * kScan2Threads;
-            if (e < nwords * 64) {
+            if (e < nchunks * 64) {
                 diag[e] = dv[u];
                 sdiag[e] = sv[u];
             }
         }
     }
-    for (int w = tid; w < nwords; w += kScan2Threads) removed[w] = 0;
+    for (int w = tid; w < nchunks; w += kScan2Threads) removed[w] = 0;
     if (tid == 0) {
         for (int g = 0; g < 2; ++g) {
             mbar_init(&rows_ready[g], 1);
@@ -705,7 +721,7 @@ __global__ void __launch_bounds__(kScan2Threads) nms_scan2_kernel(const float* _
         if (lane == 0) {
             int kc = 0;
             int c = 0;
-            for (; c < nwords; ++c) {
+            for (; c < nchunks; ++c) {
                 const int g = c & 1, it = c >> 1;
                 // bulk OR of chunk c-2 (same worker group) must be in removed[]
                 if (c >= 2) mbar_wait_spin(&or_done[g], (it - 1) & 1);
@@ -724,8 +740,8 @@ __global__ void __launch_bounds__(kScan2Threads) nms_scan2_kernel(const float* _
                     nxt |= sdiag[c * 64 + b];
                     cand = ~w & valid & ~((2ull << b) - 1ull);
                 }
-                if (c + 1 < nwords && nxt) atomicOr(reinterpret_cast<unsigned long long*>(&removed[c + 1]), nxt);
-                const bool finished = kc >= post_k || c + 1 >= nwords;
+                if (c + 1 < nchunks && nxt) atomicOr(reinterpret_cast<unsigned long long*>(&removed[c + 1]), nxt);
+                const bool finished = kc >= post_k || c + 1 >= nchunks;
                 nrows[g] = finished ? -1 - nr : nr;  // negative: last chunk (workers stop after it)
                 mbar_arrive(&rows_ready[g]);
                 if (finished) {
@@ -739,6 +755,10 @@ __global__ void __launch_bounds__(kScan2Threads) nms_scan2_kernel(const float* _
                 }
             }
             kept_total = kc;
+            // a leading-block scan is conclusive when it kept post_k boxes or
+            // when the block holds every candidate
+            complete = kc >= post_k || nchunks == nwords;
+            if (done_out) done_out[img] = complete;
         }
     } else {
         // ------------------------------------------------ bulk OR workers
@@ -750,7 +770,7 @@ __global__ void __launch_bounds__(kScan2Threads) nms_scan2_kernel(const float* _
             int nr = nrows[g];
             const bool last = nr < 0;
             if (last) nr = -1 - nr;
-            const int w0 = c + 2, nrem = nwords - w0;
+            const int w0 = c + 2, nrem = nchunks - w0;
             if (nr > 0 && nrem > 0) {
                 const int total = nr * nrem;
                 for (int e0 = wt; e0 < total; e0 += 8 * GT) {
@@ -779,6 +799,7 @@ __global__ void __launch_bounds__(kScan2Threads) nms_scan2_kernel(const float* _
         }
     }
     __syncthreads();
+    if (!complete) return;  // the full-mask launch redoes this image
     const int nk = kept_total;
     for (int j = tid; j < post_k; j += kScan2Threads) {
         float* o = rois + (static_cast<int64_t>(img) * post_k + j) * 4;
@@ -1130,8 +1151,15 @@ size_t proposal_workspace_bytes(int n_img, int n_anchors, int pre_k) {
     const int k = std::min(pre_k, n_anchors);
     const int nwords = (k + 63) / 64;
     return static_cast<size_t>(n_img) * k * (16 + 4 + 4) + static_cast<size_t>(n_img) * k * nwords * 8 + 1024 +
-           static_cast<size_t>(n_img) * (static_cast<size_t>(k) * 8 + 8 * 256 * 4 + 8 * sizeof(TopkState) + 16) + 1024;
+           static_cast<size_t>(n_img) * (static_cast<size_t>(k) * 8 + 8 * 256 * 4 + 8 * sizeof(TopkState) + 16) + 1024 +
+           static_cast<size_t>(n_img) * 4 + 256;
 }
+
+// leading block of the sorted candidates whose NMS mask is computed first:
+// with random RPN scores (C3, and the untrained C4 RPN) 2000 boxes are kept
+// within the first ~2400 of 12000 (oracle restatement), so the 12000^2 / 2
+// pair mask is ~25x more than the greedy scan reads
+constexpr int kNmsLeadWords = 64;  // 4096 candidates
 
 cudaError_t rpn_proposals(const ProposalArgs& p, void* ws, cudaStream_t st) {
     const int nA = p.n_loc * p.A;
@@ -1170,6 +1198,9 @@ cudaError_t rpn_proposals(const ProposalArgs& p, void* ws, cudaStream_t st) {
     const size_t zero_bytes = static_cast<size_t>(w2 - reinterpret_cast<uint8_t*>(zero_begin));
     w2 = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(w2) + 255) & ~uintptr_t(255));
     m.state = reinterpret_cast<TopkState*>(w2);
+    w2 += static_cast<size_t>(p.n_img) * 8 * sizeof(TopkState);
+    w2 = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(w2) + 255) & ~uintptr_t(255));
+    int* done = reinterpret_cast<int*>(w2);
     cudaMemsetAsync(zero_begin, 0, zero_bytes, st);
     const bool select_all = k >= nA;
     if (!select_all)
@@ -1179,17 +1210,29 @@ cudaError_t rpn_proposals(const ProposalArgs& p, void* ws, cudaStream_t st) {
     if (p.topk_order_out) {
         cudaMemcpyAsync(p.topk_order_out, order, static_cast<size_t>(p.n_img) * k * 4, cudaMemcpyDeviceToDevice, st);
     }
-    {
-        const int tiles = nwords * (nwords + 1) / 2;
+    auto mask_band = [&](int w_lo, int w_hi, const int* dn) {
+        const int tiles = w_hi * (w_hi + 1) / 2 - w_lo * (w_lo + 1) / 2;
         const int g = std::max(1, std::min((tiles + 3) / 4, 4 * kNumSMs / std::max(1, p.n_img)));
-        nms_mask2_kernel<<<dim3(g, p.n_img), 256, 0, st>>>(boxes, k, nwords, p.iou_thr, mask);
-    }
+        nms_mask2_kernel<<<dim3(g, p.n_img), 256, 0, st>>>(boxes, k, nwords, p.iou_thr, mask, w_lo, w_hi, dn);
+    };
+    static const bool no_lead = std::getenv("SDB_NMS_FULL_MASK") != nullptr;
     if (nwords <= kScan2MaxWords) {
-        const size_t smem2 = static_cast<size_t>(nwords) * (2 * 64 + 1) * 8;
-        cudaFuncSetAttribute(nms_scan2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem2));
-        nms_scan2_kernel<<<p.n_img, kScan2Threads, smem2, st>>>(boxes, mask, scores, k, nwords, p.post_k, p.rois,
-                                                                p.roi_scores, p.keep_pos, p.count);
+        // leading block first; the rest of the mask and a second scan run only
+        // for images whose leading block did not fill post_k (device flag)
+        const int lead = no_lead ? nwords : std::min(nwords, kNmsLeadWords);
+        cudaFuncSetAttribute(nms_scan2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(static_cast<size_t>(nwords) * (2 * 64 + 1) * 8));
+        mask_band(0, lead, nullptr);
+        nms_scan2_kernel<<<p.n_img, kScan2Threads, static_cast<size_t>(lead) * (2 * 64 + 1) * 8, st>>>(
+            boxes, mask, scores, k, nwords, p.post_k, p.rois, p.roi_scores, p.keep_pos, p.count, lead, done, nullptr);
+        if (lead < nwords) {
+            mask_band(lead, nwords, done);
+            nms_scan2_kernel<<<p.n_img, kScan2Threads, static_cast<size_t>(nwords) * (2 * 64 + 1) * 8, st>>>(
+                boxes, mask, scores, k, nwords, p.post_k, p.rois, p.roi_scores, p.keep_pos, p.count, nwords, nullptr,
+                done);
+        }
     } else {
+        mask_band(0, nwords, nullptr);
         nms_scan_kernel<<<p.n_img, kScanThreads, static_cast<size_t>(nwords) * 8, st>>>(
             boxes, mask, scores, k, nwords, p.post_k, p.rois, p.roi_scores, p.keep_pos, p.count);
     }
