@@ -476,9 +476,9 @@ __global__ void __launch_bounds__(256) topk_rank_decode_kernel(TopkMC m) {
 // (nwords x nwords x img) grid of 64-thread blocks spent most of its time
 // launching and retiring blocks, half of which exited at once).
 // Column band [w_lo, w_hi) of the triangle (tiles rb <= cb, w_lo <= cb < w_hi,
-// column-block major): the first launch covers the leading block of the sorted
-// candidates; the rest is computed only if the scan of that block did not fill
-// post_k (done[img] == 0 -- skipped otherwise).
+// column-block major): the first launch covers the leading band of the sorted
+// candidates; each later band is computed only if the scans so far did not
+// fill post_k (done[img] == 0 -- skipped otherwise).
 __global__ void __launch_bounds__(256) nms_mask2_kernel(const float* __restrict__ boxes, int k, int nwords, double thr,
                                                        uint64_t* __restrict__ mask, int w_lo, int w_hi,
                                                        const int* __restrict__ done) {
@@ -657,20 +657,24 @@ constexpr int kScan2Warps = 1 + 2 * kScan2GW;  // warp 0: decisions; then the ev
 constexpr int kScan2Threads = 32 * kScan2Warps;
 constexpr int kScan2MaxWords = 192;
 
-// nchunks < nwords: the scan of the leading block only (mask words < nchunks
-// computed): it sets done_out[img] = 1 and writes the outputs when post_k
-// boxes are kept inside the block, else done_out[img] = 0 and nothing is
-// written; a second launch with nchunks = nwords (after the rest of the mask)
-// scans again from the start unless done_in[img].  The keep decisions never depend on
-// words beyond the last chunk scanned, so the result equals the full scan.
+// Two-phase use (nchunks < nwords): the first launch scans the leading block
+// only (mask words < nchunks computed, c0 = 0); it sets done_out[img] = 1 and
+// writes the outputs when post_k boxes are kept inside the block, else
+// done_out[img] = 0 and kept_io[img] = the boxes kept so far (their positions
+// are in keep_pos).  The second launch (after the rest of the mask, nchunks =
+// nwords, c0 = the leading block's chunk count) resumes unless done_in[img]:
+// it rebuilds removed[] for words >= c0 from the kept rows and continues the
+// greedy scan at chunk c0.  The keep decisions of the leading block never
+// depend on words beyond it, so the result equals the full scan.
 __global__ void __launch_bounds__(kScan2Threads) nms_scan2_kernel(const float* __restrict__ boxes,
                                                                   const uint64_t* __restrict__ mask,
                                                                   const float* __restrict__ scores, int k, int nwords,
                                                                   int post_k, float* __restrict__ rois,
                                                                   float* __restrict__ roi_scores,
                                                                   int32_t* __restrict__ keep_pos,
-                                                                  int32_t* __restrict__ count, int nchunks,
+                                                                  int32_t* __restrict__ count, int nchunks, int c0,
                                                                   int* __restrict__ done_out,
+                                                                  int* __restrict__ kept_io,
                                                                   const int* __restrict__ done_in) {
     extern __shared__ uint64_t sm2[];
     const int img = blockIdx.x;
@@ -684,9 +688,9 @@ __global__ void __launch_bounds__(kScan2Threads) nms_scan2_kernel(const float* _
     __shared__ int kept_total, complete;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint64_t* M = mask + static_cast<int64_t>(img) * k * nwords;
-    // preload: diagonal and super-diagonal words of every chunk
+    // preload: diagonal and super-diagonal words of every chunk >= c0
     // (8 independent loads in flight per thread)
-    for (int e0 = tid; e0 < nchunks * 64; e0 += 4 * kScan2Threads) {
+    for (int e0 = c0 * 64 + tid; e0 < nchunks * 64; e0 += 4 * kScan2Threads) {
         uint64_t dv[4], sv[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -708,6 +712,32 @@ __global__ void __launch_bounds__(kScan2Threads) nms_scan2_kernel(const float* _
         }
     }
     for (int w = tid; w < nchunks; w += kScan2Threads) removed[w] = 0;
+    const int kc0 = c0 > 0 ? kept_io[img] : 0;
+    if (kc0 > 0) {
+        // resume: every word >= c0 of the rows kept in chunks < c0
+        __syncthreads();
+        const int nrem = nchunks - c0, total = kc0 * nrem;
+        const int32_t* kp = keep_pos + static_cast<int64_t>(img) * post_k;
+        for (int e0 = tid; e0 < total; e0 += 8 * kScan2Threads) {
+            uint64_t v[8];
+            int wi[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int e = e0 + u * kScan2Threads;
+                v[u] = 0;
+                wi[u] = 0;
+                if (e < total) {
+                    const int r = e / nrem;
+                    wi[u] = c0 + (e - r * nrem);
+                    v[u] = __ldg(M + static_cast<int64_t>(kp[r]) * nwords + wi[u]);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (v[u]) atomicOr(reinterpret_cast<unsigned long long*>(&removed[wi[u]]),
+                                   static_cast<unsigned long long>(v[u]));
+        }
+    }
     if (tid == 0) {
         for (int g = 0; g < 2; ++g) {
             mbar_init(&rows_ready[g], 1);
@@ -719,12 +749,11 @@ __global__ void __launch_bounds__(kScan2Threads) nms_scan2_kernel(const float* _
     if (warp == 0) {
         // ------------------------------------------------ decisions (lane 0)
         if (lane == 0) {
-            int kc = 0;
-            int c = 0;
-            for (; c < nchunks; ++c) {
-                const int g = c & 1, it = c >> 1;
+            int kc = kc0;
+            for (int c = c0; c < nchunks; ++c) {
+                const int rel = c - c0, g = rel & 1, it = rel >> 1;
                 // bulk OR of chunk c-2 (same worker group) must be in removed[]
-                if (c >= 2) mbar_wait_spin(&or_done[g], (it - 1) & 1);
+                if (rel >= 2) mbar_wait_spin(&or_done[g], (it - 1) & 1);
                 const int lim = min(64, k - c * 64);
                 const uint64_t valid = lim >= 64 ? ~0ull : ((1ull << lim) - 1ull);
                 uint64_t w = atomicOr(reinterpret_cast<unsigned long long*>(&removed[c]), 0ull);
@@ -747,8 +776,8 @@ __global__ void __launch_bounds__(kScan2Threads) nms_scan2_kernel(const float* _
                 if (finished) {
                     // release the other group, waiting for chunk c + 1, once it has
                     // finished chunk c - 1
-                    const int g2 = g ^ 1, c2 = c + 1;
-                    if (c2 >= 2) mbar_wait_spin(&or_done[g2], ((c2 >> 1) - 1) & 1);
+                    const int g2 = g ^ 1, r2 = rel + 1;
+                    if (r2 >= 2) mbar_wait_spin(&or_done[g2], ((r2 >> 1) - 1) & 1);
                     nrows[g2] = -1;
                     mbar_arrive(&rows_ready[g2]);
                     break;
@@ -758,14 +787,17 @@ __global__ void __launch_bounds__(kScan2Threads) nms_scan2_kernel(const float* _
             // a leading-block scan is conclusive when it kept post_k boxes or
             // when the block holds every candidate
             complete = kc >= post_k || nchunks == nwords;
-            if (done_out) done_out[img] = complete;
+            if (done_out) {
+                done_out[img] = complete;
+                kept_io[img] = kc;
+            }
         }
     } else {
         // ------------------------------------------------ bulk OR workers
         const int g = (warp - 1) / kScan2GW;     // 0: even chunks, 1: odd chunks
         constexpr int GT = 32 * kScan2GW;        // threads per group
         const int wt = tid - 32 - g * GT;        // 0..GT-1 within the group
-        for (int c = g, it = 0;; c += 2, ++it) {
+        for (int c = c0 + g, it = 0;; c += 2, ++it) {
             mbar_wait_spin(&rows_ready[g], it & 1);
             int nr = nrows[g];
             const bool last = nr < 0;
@@ -799,7 +831,7 @@ __global__ void __launch_bounds__(kScan2Threads) nms_scan2_kernel(const float* _
         }
     }
     __syncthreads();
-    if (!complete) return;  // the full-mask launch redoes this image
+    if (!complete) return;  // the resume launch finishes this image
     const int nk = kept_total;
     for (int j = tid; j < post_k; j += kScan2Threads) {
         float* o = rois + (static_cast<int64_t>(img) * post_k + j) * 4;
@@ -1152,14 +1184,15 @@ size_t proposal_workspace_bytes(int n_img, int n_anchors, int pre_k) {
     const int nwords = (k + 63) / 64;
     return static_cast<size_t>(n_img) * k * (16 + 4 + 4) + static_cast<size_t>(n_img) * k * nwords * 8 + 1024 +
            static_cast<size_t>(n_img) * (static_cast<size_t>(k) * 8 + 8 * 256 * 4 + 8 * sizeof(TopkState) + 16) + 1024 +
-           static_cast<size_t>(n_img) * 4 + 256;
+           static_cast<size_t>(n_img) * 8 + 256;
 }
 
-// leading block of the sorted candidates whose NMS mask is computed first:
-// with random RPN scores (C3, and the untrained C4 RPN) 2000 boxes are kept
-// within the first ~2400 of 12000 (oracle restatement), so the 12000^2 / 2
-// pair mask is ~25x more than the greedy scan reads
-constexpr int kNmsLeadWords = 64;  // 4096 candidates
+// NMS mask bands: with random RPN scores (C3, and the untrained C4 RPN) 2000
+// boxes are kept within the first ~2400 of 12000 (oracle restatement), so the
+// 12000^2 / 2 pair mask is ~25x more than the greedy scan reads; while the C4
+// RPN trains, the depth of the 2000th kept box wanders between ~2000 and all
+// 12000 (tools/nms_depth.py), hence bands that resume rather than one lead
+constexpr int kNmsLeadWords = 64;  // band width: 4096 candidates
 
 cudaError_t rpn_proposals(const ProposalArgs& p, void* ws, cudaStream_t st) {
     const int nA = p.n_loc * p.A;
@@ -1201,6 +1234,7 @@ cudaError_t rpn_proposals(const ProposalArgs& p, void* ws, cudaStream_t st) {
     w2 += static_cast<size_t>(p.n_img) * 8 * sizeof(TopkState);
     w2 = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(w2) + 255) & ~uintptr_t(255));
     int* done = reinterpret_cast<int*>(w2);
+    int* kept = done + p.n_img;
     cudaMemsetAsync(zero_begin, 0, zero_bytes, st);
     const bool select_all = k >= nA;
     if (!select_all)
@@ -1219,17 +1253,18 @@ cudaError_t rpn_proposals(const ProposalArgs& p, void* ws, cudaStream_t st) {
     if (nwords <= kScan2MaxWords) {
         // leading block first; the rest of the mask and a second scan run only
         // for images whose leading block did not fill post_k (device flag)
-        const int lead = no_lead ? nwords : std::min(nwords, kNmsLeadWords);
         cudaFuncSetAttribute(nms_scan2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(static_cast<size_t>(nwords) * (2 * 64 + 1) * 8));
-        mask_band(0, lead, nullptr);
-        nms_scan2_kernel<<<p.n_img, kScan2Threads, static_cast<size_t>(lead) * (2 * 64 + 1) * 8, st>>>(
-            boxes, mask, scores, k, nwords, p.post_k, p.rois, p.roi_scores, p.keep_pos, p.count, lead, done, nullptr);
-        if (lead < nwords) {
-            mask_band(lead, nwords, done);
-            nms_scan2_kernel<<<p.n_img, kScan2Threads, static_cast<size_t>(nwords) * (2 * 64 + 1) * 8, st>>>(
-                boxes, mask, scores, k, nwords, p.post_k, p.rois, p.roi_scores, p.keep_pos, p.count, nwords, nullptr,
-                done);
+        // bands [0, 64), [64, 128), [128, nwords) words: each band's mask is
+        // computed, and its scan resumed, only for images not yet complete
+        int lo = 0;
+        for (int band = 0; lo < nwords; ++band) {
+            const int hi = no_lead ? nwords : std::min(nwords, (band + 1) * kNmsLeadWords);
+            mask_band(lo, hi, band ? done : nullptr);
+            nms_scan2_kernel<<<p.n_img, kScan2Threads, static_cast<size_t>(hi) * (2 * 64 + 1) * 8, st>>>(
+                boxes, mask, scores, k, nwords, p.post_k, p.rois, p.roi_scores, p.keep_pos, p.count, hi, lo,
+                hi < nwords ? done : nullptr, kept, band ? done : nullptr);
+            lo = hi;
         }
     } else {
         mask_band(0, nwords, nullptr);

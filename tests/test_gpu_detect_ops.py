@@ -27,12 +27,14 @@ def test_anchors_bit_exact(orc):
 
 
 @pytest.mark.parametrize("n_img,pre_k,post_k", [(2, 12000, 2000), (1, 2000, 300), (1, 50, 7), (1, 300, 2000), (2, 130, 129),
-                                                (2, 12000, 5000), (1, 4100, 4100)])
+                                                (2, 12000, 5000), (1, 4100, 4100), (1, 12000, 9000),
+                                                (1, 8200, 8200)])
 def test_rpn_proposal_bit_exact(orc, n_img, pre_k, post_k):
     """BASELINE config C3: logits N(0,2), deltas N(0,0.2), 50x84x15 anchors, 12000 -> 2000 at IoU 0.7.
-    The NMS mask is computed for the leading 4096 candidates first; (12000, 5000)
-    and (4100, 4100) cannot fill post_k there, so the rest of the mask and the
-    full rescan run (the fallback path)."""
+    The NMS mask is computed in bands of 4096 candidates, the scan resuming band
+    by band until post_k boxes are kept: (12000, 5000) and (4100, 4100) need a
+    second band, (12000, 9000) and (8200, 8200) all three (the last one a
+    single word wide)."""
     from paper_1903_05831_b200 import simdet as sd
     H, W, A, Ap = 50, 84, 15, 16
     rng = np.random.default_rng(pre_k + n_img)
