@@ -266,6 +266,11 @@ typedef struct {
     int shard_optimizer; /* fp16 with a communicator: reduce-scatter each bucket, update this
                             rank's 1/K shard of the fp32 masters, all-gather the fp16 shadows
                             (instead of allreduce + a replicated update) */
+    int sync_bn;         /* mode 0 only: cross-GPU SyncBN (bn.mode "sync", src/model.cpp:204):
+                            every BN layer's float [sum, sumsq, count] and backward [sum dy,
+                            sum dy*xhat] are summed over the ranks (src/syncbn.cpp:21-117);
+                            dgamma/dbeta are then global and, as in the reference trainer
+                            (src/trainer.cpp:251), summed again with the other gradients */
 } sdb_det_config;
 
 typedef struct sdb_det sdb_det;

@@ -101,6 +101,7 @@ struct NormL {
     int C = 0;
     float* mean = nullptr;
     float* invstd = nullptr;
+    float* agg = nullptr;  // sync_bn: [sum, sumsq, count] of the forward, summed over ranks
     int act = 0;  // mode 0: 0 none / 1 relu; mode 1: 2 (iabn)
     float slope = 1.0f;
 };
@@ -253,6 +254,7 @@ struct sdb_det {
     // comm: an NCCL communicator exists (world > 1, or a forced 1-rank one that
     // runs the data-parallel code path on one GPU)
     bool comm_on = false;
+    float* sbn_red = nullptr;  // sync_bn backward sums [2 * max C]
     // sharded optimizer: buckets are reduce-scattered, each rank
     // updates its 1/K shard of the fp32 masters and all-gathers the fp16 shadows
     bool shard = false;
@@ -322,6 +324,7 @@ struct sdb_det {
         nl.pb = add_param(name + ".beta", {C}, 3);
         nl.mean = static_cast<float*>(alloc(C * 4));
         nl.invstd = static_cast<float*>(alloc(C * 4));
+        if (cfg.sync_bn) nl.agg = static_cast<float*>(alloc((2 * C + 1) * 4));
         if (cfg.mode == 0) {
             nl.act = relu_or_leaky ? 1 : 0;
         } else {
@@ -517,6 +520,15 @@ void norm_fwd(sdb_det* d, const NormL& n, const Act& z, const Act& a) {
         ps.label = "norm_fwd rows " + std::to_string(rows) + " C " + std::to_string(n.C);
         ps.bytes_ = 3.0 * d->es * z.numel();
     }
+    if (n.agg) {
+        // SyncBN (src/syncbn.cpp:21-70): this rank's float sums, summed over the
+        // ranks on the step stream, then statistics + apply from the global sums
+        CK(syncbn_local_sums(d->dt, z.p, rows, n.C, n.agg, d->ws, d->ctx->stream));
+        if (d->comm_on) CKC(comm_allreduce(d->ctx, n.agg, 2 * n.C + 1, kF32, 0, d->ctx->stream));
+        CK(syncbn_forward_finish(d->dt, z.p, d->bnp(n.pg), d->bnp(n.pb), a.p, n.mean, n.invstd, n.agg, rows, n.C,
+                                 d->cfg.eps, n.act, d->ctx->stream));
+        return;
+    }
     CK(bn_forward(d->dt, z.p, d->bnp(n.pg), d->bnp(n.pb), a.p, n.mean, n.invstd, rows, n.C, d->cfg.eps, n.act,
                   n.slope, d->ws, d->ctx->stream));
 }
@@ -529,7 +541,16 @@ void norm_bwd(sdb_det* d, const NormL& n, const Act& z, const Act& a, const void
         ps.label = "norm_bwd rows " + std::to_string(rows) + " C " + std::to_string(n.C);
         ps.bytes_ = 5.0 * d->es * z.numel();
     }
-    if (d->cfg.mode == 0) {
+    if (n.agg) {
+        // SyncBN backward (src/syncbn.cpp:72-117): [sum dy, sum dy*xhat] summed over
+        // the ranks, coefficients with the forward's global count
+        const void* mask = n.act == 1 ? a.p : nullptr;
+        CK(syncbn_backward_local_sums(d->dt, da, z.p, mask, n.mean, n.invstd, d->sbn_red, rows, n.C, d->ws,
+                                      d->ctx->stream));
+        if (d->comm_on) CKC(comm_allreduce(d->ctx, d->sbn_red, 2 * n.C, kF32, 0, d->ctx->stream));
+        CK(syncbn_backward_finish(d->dt, da, z.p, mask, d->bnp(n.pg), n.mean, n.invstd, d->sbn_red, n.agg, dz,
+                                  d->bngp(n.pg), d->bngp(n.pb), rows, n.C, d->ws, d->ctx->stream));
+    } else if (d->cfg.mode == 0) {
         CK(bn_backward(d->dt, da, z.p, n.act == 1 ? a.p : nullptr, d->bnp(n.pg), n.mean, n.invstd, dz,
                        d->bngp(n.pg), d->bngp(n.pb), rows, n.C, d->ws, d->ctx->stream));
     } else if (d->cst_b.produced && d->cst_b.bs_y == a.p) {
@@ -1119,6 +1140,7 @@ int sdb_det_create(sdb_ctx* ctx, const sdb_det_config* cfgp, sdb_det** out) {
     if (cf.n_scales < 1 || cf.n_scales > 8 || cf.n_ratios < 1 || cf.n_ratios > 8) return det_fail(SDB_PARAM, "anchors");
     if (cf.nms_iou < 0.0 || cf.nms_iou > 1.0) return det_fail(SDB_PARAM, "iou threshold outside [0,1]");
     if (cf.mode >= 1 && !(cf.slope > 0.0f)) return det_fail(SDB_NONINVERTIBLE, "iabn requires slope > 0");
+    if (cf.sync_bn && cf.mode != 0) return det_fail(SDB_PARAM, "sync_bn is a BN mode (mode 0); IABN statistics stay per GPU");
     auto* d = new sdb_det();
     try {
         d->ctx = ctx;
@@ -1281,6 +1303,7 @@ int sdb_det_create(sdb_ctx* ctx, const sdb_det_config* cfgp, sdb_det** out) {
         d->roi_count = static_cast<int32_t*>(d->alloc(b * 4));
         d->ws_bytes = max_ws(d);
         d->ws = d->alloc(d->ws_bytes);
+        if (cf.sync_bn) d->sbn_red = static_cast<float*>(d->alloc(2 * 2048 * sizeof(float)));
         if (d->dt == kF16) {
             d->cst.cap_bytes = static_cast<size_t>(2 * 148) * 4 * 2 * 256 * sizeof(double);  // 2 CTAs x 148 SMs
             d->cst.buf = static_cast<double*>(d->alloc(d->cst.cap_bytes));

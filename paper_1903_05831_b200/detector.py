@@ -31,6 +31,7 @@ class DetConfig(C.Structure):
         ("dynamic_scale", C.c_int), ("scale_init", C.c_double), ("growth_interval", C.c_int64),
         ("growth", C.c_double), ("backoff", C.c_double), ("min_scale", C.c_double), ("max_scale", C.c_double),
         ("seed", C.c_uint64), ("max_gt", C.c_int), ("bucket_mb", C.c_double), ("shard_optimizer", C.c_int),
+        ("sync_bn", C.c_int),
     ]
 
 

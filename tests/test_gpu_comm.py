@@ -108,3 +108,29 @@ def test_allreduce_abi_on_one_rank():
         assert sd.L().sdb_comm_check(h) == 0
     finally:
         sd.L().sdb_ctx_destroy(h)
+
+
+@pytest.mark.parametrize("force_comm", [False, True])
+def test_sync_bn_mode_on_one_rank_is_plain_bn(force_comm):
+    """bn.mode "sync" (src/model.cpp:204): every BN layer's float [sum, sumsq,
+    count] and backward [sum dy, sum dy*xhat] go through an fp32 SUM allreduce
+    on the step stream (src/syncbn.cpp:21-117).  On one rank the reference skips
+    the allreduce (group->size() > 1) and so the step equals plain BN
+    bit for bit; with the forced 1-rank communicator the NCCL calls run inside
+    the captured step and must not change a bit either.  The K > 1 sums are
+    pinned on CPU (tests/test_oracle_pins.py: the restatement vs the reference's
+    own run_workers groups)."""
+    from paper_1903_05831_b200 import detector as D
+    base = D.preset("c1", img_h=128, img_w=128)
+    t0, w0, v0 = _run(base, 3, False)
+    t1, w1, v1 = _run(D.preset("c1", img_h=128, img_w=128, extra={"sync_bn": 1}), 3, force_comm)
+    assert [t[0] for t in t0] == [t[0] for t in t1]
+    assert np.array_equal(w0.view(np.uint32), w1.view(np.uint32))
+    assert np.array_equal(v0.view(np.uint32), v1.view(np.uint32))
+
+
+def test_sync_bn_needs_bn_mode():
+    from paper_1903_05831_b200 import ParamError
+    from paper_1903_05831_b200 import detector as D
+    with pytest.raises(ParamError):
+        D.Detector(D.preset("c2", img_h=128, img_w=128, extra={"sync_bn": 1}))
