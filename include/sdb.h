@@ -271,6 +271,11 @@ typedef struct {
                             sum dy*xhat] are summed over the ranks (src/syncbn.cpp:21-117);
                             dgamma/dbeta are then global and, as in the reference trainer
                             (src/trainer.cpp:251), summed again with the other gradients */
+    int checkpoint;      /* memory.checkpoint (src/trainer.cpp:233): sqrt(L) activation
+                            checkpointing of the backbone's L bottleneck blocks with the
+                            reference's segment plan (src/memopt.cpp:76-89); only segment
+                            boundary outputs persist, each segment is recomputed from its
+                            boundary in backward (src/memopt.cpp:150-210); bit-identical */
 } sdb_det_config;
 
 typedef struct sdb_det sdb_det;
@@ -332,6 +337,15 @@ int sdb_det_export(sdb_det* det, int what, void* host, int64_t capacity, int64_t
 int sdb_det_dims(sdb_det* det, int* feat_h, int* feat_w, int* n_anchor_per_loc, int* a_pad);
 /* launches of libsdb kernels per step (counted at the first step) */
 int sdb_det_kernel_launches(sdb_det* det, int64_t* n);
+/* the checkpoint segment plan for L layers (host logic, no GPU): starts[0..S]
+ * = segment starts then L; returns S (= ceil(sqrt(L)) segments, the reference's
+ * plan_checkpoints, src/memopt.cpp:76-89), or < 0 (SDB_PARAM for L < 1) */
+int sdb_plan_checkpoints(int L, int* starts, int cap);
+/* device memory: bytes of backbone activations (persistent tensors + the
+ * checkpoint arena), all device bytes the detector allocated, and the
+ * checkpoint segment count (0: checkpointing off) -- the MemoryTrace "act"
+ * peak of tests/test_memopt.cpp:139-150 for this static schedule */
+int sdb_det_memory(sdb_det* det, int64_t* backbone_act_bytes, int64_t* device_bytes, int* segments);
 /* the gradient-bucket plan of the data-parallel allreduce (host logic, no GPU):
  * offsets = start of every conv/fc gradient slice in the flat buffer (pack
  * order), total = buffer length; buckets are emitted in issue order (from the

@@ -74,6 +74,7 @@ _REF_SIGS = {
     "ref_update_scale": (_I, [_P, _P, _I, _L, _D, _D, _D, _D, _I]),
     "ref_sgd_step_master": (_I, [_P, _P, _P, _L, _F, _F]),
     "ref_allreduce_seconds": (_I, [_I, _L, _I, _P]),
+    "ref_plan_checkpoints": (_I, [_L, _P, _I]),
 }
 
 class RefDetCfg(C.Structure):

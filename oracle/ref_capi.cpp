@@ -318,4 +318,17 @@ int ref_sgd_step_master(float* w, float* v, const float* g, int64_t n, float lr,
     });
 }
 
+// plan_checkpoints (src/memopt.cpp:76-89): segment boundaries for L layers;
+// returns their count (or -1 on PlanError / overflow of cap)
+int ref_plan_checkpoints(int64_t L, int64_t* boundaries, int cap) {
+    int n = -1;
+    const int rc = guarded([&] {
+        const CheckpointPlan plan = plan_checkpoints(L);
+        if (static_cast<int>(plan.boundaries.size()) > cap) throw std::runtime_error("cap");
+        for (size_t i = 0; i < plan.boundaries.size(); ++i) boundaries[i] = plan.boundaries[i];
+        n = static_cast<int>(plan.boundaries.size());
+    });
+    return rc == 0 ? n : -1;
+}
+
 }  // extern "C"

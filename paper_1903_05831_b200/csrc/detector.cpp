@@ -170,6 +170,16 @@ struct sdb_det {
     void *stem_x2 = nullptr, *stem_w2 = nullptr, *stem_dw2 = nullptr;
     uint8_t* pool_arg = nullptr;
     std::vector<Block> backbone, head;
+    // sqrt(L) activation checkpointing of the backbone blocks (memory.checkpoint,
+    // src/memopt.cpp:76-89 plan, :150-210 runner): ck_start = segment starts + L;
+    // every tensor of a segment except its last block's output lives in one
+    // arena shared by all segments, refilled by a forward recompute in backward
+    std::vector<int> ck_start;
+    uint8_t* ck_arena = nullptr;
+    size_t ck_off = 0, ck_bytes = 0;
+    bool measuring = false;        // sizing pass: no device allocation
+    cudaEvent_t ck_ev = nullptr;   // side-stream wgrads done with an arena segment
+    int64_t bytes_total = 0, bytes_backbone = 0;
     ConvL rpn_conv, rpn_cls, rpn_bbox, fc_cls, fc_bbox;
     Act c4, rpn_z, rpn_a, rpn_logits, rpn_deltas, roi_feat, head_out, pooled, cls_logits, bbox_pred;
     int A = 0, A_pad = 0, n_loc = 0, nA = 0, fh = 0, fw = 0, ncls = 0, ncls_pad = 0, nbox_pad = 0;
@@ -274,10 +284,19 @@ struct sdb_det {
     Prof prof;
 
     void* alloc(size_t bytes) {
+        if (measuring) return nullptr;
         void* p = nullptr;
         CK(cudaMalloc(&p, std::max<size_t>(bytes, 256)));
         allocs.push_back(p);
+        bytes_total += static_cast<int64_t>(std::max<size_t>(bytes, 256));
         return p;
+    }
+    // a slice of the checkpoint arena (256-byte aligned)
+    void* seg_alloc(size_t bytes) {
+        const size_t off = ck_off;
+        ck_off += (bytes + 255) & ~size_t(255);
+        ck_bytes = std::max(ck_bytes, ck_off);
+        return measuring ? nullptr : ck_arena + off;
     }
     Act act(int n, int h, int w, int c) {
         Act a;
@@ -396,29 +415,69 @@ void build_stage(sdb_det* d, std::vector<Block>& out, const std::string& pref, i
     }
 }
 
-void alloc_stage(sdb_det* d, std::vector<Block>& st, Act in) {
-    for (auto& bl : st) {
+// the reference's plan_checkpoints(L) (src/memopt.cpp:76-89): ceil(sqrt(L))
+// segments, the first L % segs of them one layer longer; returns the segment
+// starts followed by L
+std::vector<int> plan_segments(int L) {
+    std::vector<int> starts{0};
+    const int segs = static_cast<int>(std::ceil(std::sqrt(static_cast<double>(L))));
+    const int base = L / segs, rem = L % segs;
+    int at = 0;
+    for (int j = 0; j + 1 < segs; ++j) {
+        at += base + (j < rem ? 1 : 0);
+        starts.push_back(at);
+    }
+    starts.push_back(L);
+    return starts;
+}
+
+// ck: segment starts (checkpointing) or empty; with segments, every tensor of
+// a block goes to the shared arena except the output of a segment's last block
+// (the next segment's boundary input, or C4)
+void alloc_stage(sdb_det* d, std::vector<Block>& st, Act in, const std::vector<int>& ck = {}) {
+    for (size_t i = 0; i < st.size(); ++i) {
+        Block& bl = st[i];
+        const bool seg = !ck.empty();
+        const bool seg_last = seg && std::find(ck.begin(), ck.end(), static_cast<int>(i) + 1) != ck.end();
+        if (seg && std::find(ck.begin(), ck.end(), static_cast<int>(i)) != ck.end()) d->ck_off = 0;
+        auto mk = [&](int n, int h, int w, int c, bool keep) {
+            if (!seg || keep) {
+                if (&st == &d->backbone) d->bytes_backbone += static_cast<int64_t>(n) * h * w * c * d->es;
+                return d->act(n, h, w, c);
+            }
+            Act a;
+            a.n = n; a.h = h; a.w = w; a.c = c;
+            a.p = d->seg_alloc(static_cast<size_t>(a.numel()) * d->es);
+            return a;
+        };
         bl.in = in;
         auto set = [&](ConvL& c, const Act& x) {
             c.g.N = x.n; c.g.H = x.h; c.g.W = x.w;
         };
         set(bl.c1, in);
-        bl.z1 = d->act(in.n, bl.c1.g.Ho(), bl.c1.g.Wo(), bl.c1.g.K);
-        bl.a1 = d->cfg.mode == 0 ? d->act(bl.z1.n, bl.z1.h, bl.z1.w, bl.z1.c) : bl.z1;
+        bl.z1 = mk(in.n, bl.c1.g.Ho(), bl.c1.g.Wo(), bl.c1.g.K, false);
+        bl.a1 = d->cfg.mode == 0 ? mk(bl.z1.n, bl.z1.h, bl.z1.w, bl.z1.c, false) : bl.z1;
         set(bl.c2, bl.a1);
-        bl.z2 = d->act(in.n, bl.c2.g.Ho(), bl.c2.g.Wo(), bl.c2.g.K);
-        bl.a2 = d->cfg.mode == 0 ? d->act(bl.z2.n, bl.z2.h, bl.z2.w, bl.z2.c) : bl.z2;
+        bl.z2 = mk(in.n, bl.c2.g.Ho(), bl.c2.g.Wo(), bl.c2.g.K, false);
+        bl.a2 = d->cfg.mode == 0 ? mk(bl.z2.n, bl.z2.h, bl.z2.w, bl.z2.c, false) : bl.z2;
         set(bl.c3, bl.a2);
-        bl.z3 = d->act(in.n, bl.c3.g.Ho(), bl.c3.g.Wo(), bl.c3.g.K);
-        bl.b3 = d->cfg.mode == 0 ? d->act(bl.z3.n, bl.z3.h, bl.z3.w, bl.z3.c) : bl.z3;
+        bl.z3 = mk(in.n, bl.c3.g.Ho(), bl.c3.g.Wo(), bl.c3.g.K, false);
+        bl.b3 = d->cfg.mode == 0 ? mk(bl.z3.n, bl.z3.h, bl.z3.w, bl.z3.c, false) : bl.z3;
         if (bl.has_down) {
             set(bl.down, in);
-            bl.zd = d->act(in.n, bl.down.g.Ho(), bl.down.g.Wo(), bl.down.g.K);
-            bl.d = d->cfg.mode == 0 ? d->act(bl.zd.n, bl.zd.h, bl.zd.w, bl.zd.c) : bl.zd;
+            bl.zd = mk(in.n, bl.down.g.Ho(), bl.down.g.Wo(), bl.down.g.K, false);
+            bl.d = d->cfg.mode == 0 ? mk(bl.zd.n, bl.zd.h, bl.zd.w, bl.zd.c, false) : bl.zd;
         }
-        bl.out = d->act(bl.z3.n, bl.z3.h, bl.z3.w, bl.z3.c);
-        if (d->cfg.mode != 0 && d->dt == kF16)
-            bl.obits = static_cast<uint8_t*>(d->alloc(static_cast<size_t>(bl.out.numel() / 8)));
+        bl.out = mk(bl.z3.n, bl.z3.h, bl.z3.w, bl.z3.c, seg_last);
+        if (d->cfg.mode != 0 && d->dt == kF16) {
+            const size_t nb = static_cast<size_t>(bl.out.numel() / 8);
+            if (!seg || seg_last) {
+                if (&st == &d->backbone) d->bytes_backbone += static_cast<int64_t>(nb);
+                bl.obits = static_cast<uint8_t*>(d->alloc(nb));
+            } else {
+                bl.obits = static_cast<uint8_t*>(d->seg_alloc(nb));
+            }
+        }
         d->gbuf_elems = std::max({d->gbuf_elems, in.numel(), bl.z1.numel(), bl.z2.numel(), bl.z3.numel()});
         in = bl.out;
     }
@@ -1025,7 +1084,21 @@ void run_step(sdb_det* d) {
     // backbone
     cur = dc4;
     spare = dc4 == d->gbuf[2] ? d->gbuf[3] : d->gbuf[2];
-    for (int i = static_cast<int>(d->backbone.size()) - 1; i >= 0; --i) {
+    const int L = static_cast<int>(d->backbone.size());
+    for (int i = L - 1; i >= 0; --i) {
+        if (!d->ck_start.empty() && i + 1 < L) {
+            const auto it = std::find(d->ck_start.begin(), d->ck_start.end(), i + 1);
+            if (it != d->ck_start.end()) {
+                // block i closes a segment that is not the last: refill the arena
+                // from the segment's boundary input (src/memopt.cpp:183-189), once
+                // the deferred wgrads of the segment above stopped reading it
+                if (B.side) {
+                    CK(cudaEventRecord(d->ck_ev, d->wst));
+                    CK(cudaStreamWaitEvent(st, d->ck_ev, 0));
+                }
+                for (int j = *(it - 1); j <= i; ++j) block_fwd(d, d->backbone[j]);
+            }
+        }
         const void* in_mask = i > 0 ? d->backbone[i - 1].out.p : nullptr;  // backbone[0].in = max-pool output
         block_bwd(B, d->backbone[i], cur, spare, d->gbuf[1], d->gbuf[4], in_mask,
                   i > 0 ? d->backbone[i - 1].obits : nullptr);
@@ -1201,7 +1274,20 @@ int sdb_det_create(sdb_ctx* ctx, const sdb_det_config* cfgp, sdb_det** out) {
         d->pool = d->act(b, ph, pw, 64);
         d->pool_arg = static_cast<uint8_t*>(d->alloc(static_cast<size_t>(d->pool.numel())));
         d->gbuf_elems = std::max(d->stem_z.numel(), d->pool.numel());
-        alloc_stage(d, d->backbone, d->pool);
+        if (cf.checkpoint) {
+            // sizing pass (no allocation), then the arena, then the real pass
+            d->ck_start = plan_segments(static_cast<int>(d->backbone.size()));
+            d->measuring = true;
+            alloc_stage(d, d->backbone, d->pool, d->ck_start);
+            d->measuring = false;
+            d->bytes_backbone = 0;
+            d->ck_arena = static_cast<uint8_t*>(d->alloc(d->ck_bytes));
+            alloc_stage(d, d->backbone, d->pool, d->ck_start);
+            d->bytes_backbone += static_cast<int64_t>(d->ck_bytes);
+            CK(cudaEventCreateWithFlags(&d->ck_ev, cudaEventDisableTiming));
+        } else {
+            alloc_stage(d, d->backbone, d->pool);
+        }
         d->c4 = d->backbone.back().out;
         d->fh = d->c4.h;
         d->fw = d->c4.w;
@@ -1433,6 +1519,7 @@ int sdb_det_destroy(sdb_det* d) {
         if (d->stage_ev[k]) cudaEventDestroy(d->stage_ev[k]);
     }
     cudaFreeHost(d->h_losses);
+    if (d->ck_ev) cudaEventDestroy(d->ck_ev);
     for (auto e : d->bucket_ev) cudaEventDestroy(e);
     if (d->wst) {
         for (auto e : d->dzr_ev) cudaEventDestroy(e);
@@ -1981,6 +2068,22 @@ int sdb_det_profile(sdb_det* d, double* ms, double* flops, double* bytes, int64_
 
 int sdb_det_kernel_launches(sdb_det* d, int64_t* n) {
     *n = d->launches;
+    return SDB_OK;
+}
+
+int sdb_plan_checkpoints(int L, int* starts, int cap) {
+    if (L < 1) return det_fail(SDB_PARAM, "layer count must be >= 1");
+    const std::vector<int> st = plan_segments(L);
+    if (static_cast<int>(st.size()) > cap) return det_fail(SDB_PARAM, "starts capacity too small");
+    std::copy(st.begin(), st.end(), starts);
+    return static_cast<int>(st.size()) - 1;
+}
+
+int sdb_det_memory(sdb_det* d, int64_t* backbone_act_bytes, int64_t* device_bytes, int* segments) {
+    if (!d) return det_fail(SDB_CONTRACT, "null detector");
+    if (backbone_act_bytes) *backbone_act_bytes = d->bytes_backbone;
+    if (device_bytes) *device_bytes = d->bytes_total;
+    if (segments) *segments = d->ck_start.empty() ? 0 : static_cast<int>(d->ck_start.size()) - 1;
     return SDB_OK;
 }
 

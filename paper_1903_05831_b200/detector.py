@@ -31,7 +31,7 @@ class DetConfig(C.Structure):
         ("dynamic_scale", C.c_int), ("scale_init", C.c_double), ("growth_interval", C.c_int64),
         ("growth", C.c_double), ("backoff", C.c_double), ("min_scale", C.c_double), ("max_scale", C.c_double),
         ("seed", C.c_uint64), ("max_gt", C.c_int), ("bucket_mb", C.c_double), ("shard_optimizer", C.c_int),
-        ("sync_bn", C.c_int),
+        ("sync_bn", C.c_int), ("checkpoint", C.c_int),
     ]
 
 
@@ -126,6 +126,7 @@ _SIGS = {
     "sdb_det_export": [_P, _I, _P, _L, C.POINTER(_L)],
     "sdb_det_dims": [_P, C.POINTER(_I), C.POINTER(_I), C.POINTER(_I), C.POINTER(_I)],
     "sdb_det_kernel_launches": [_P, C.POINTER(_L)],
+    "sdb_det_memory": [_P, C.POINTER(_L), C.POINTER(_L), C.POINTER(_I)],
     "sdb_det_profile": [_P, _P, _P, _P, _P, _I],
     "sdb_ctx_create": [_I, _I, _I, _P, C.POINTER(_P)],
     "sdb_ctx_destroy": [_P],
@@ -318,6 +319,12 @@ class Detector:
         dg, st = C.c_uint64(), _L()
         check(L().sdb_det_load_checkpoint(self.h, path.encode(), C.byref(dg), C.byref(st)))
         return st.value, dg.value
+
+    def memory(self):
+        """(backbone activation bytes, device bytes, checkpoint segments)"""
+        a, t, sg = _L(), _L(), _I()
+        check(L().sdb_det_memory(self.h, C.byref(a), C.byref(t), C.byref(sg)))
+        return a.value, t.value, sg.value
 
     def kernel_launches(self) -> int:
         n = _L()

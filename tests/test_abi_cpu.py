@@ -57,3 +57,26 @@ def test_error_mapping_matches_reference_taxonomy():
     with pytest.raises(pkg.ShapeError):
         pkg.check(1)
     assert ctypes.sizeof(ctypes.c_void_p) == 8
+
+
+def test_checkpoint_plan_matches_reference(ref):
+    """sdb_plan_checkpoints == the reference's plan_checkpoints(L)
+    (src/memopt.cpp:76-89) for L = 1..200, and PlanError's domain (L < 1)
+    is rejected; tests/test_memopt.cpp:88-110 properties hold"""
+    import math
+    import numpy as np
+    lb = pkg.lib()
+    lb.sdb_plan_checkpoints.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int]
+    for L in range(1, 201):
+        starts = np.zeros(64, np.int32)
+        S = lb.sdb_plan_checkpoints(L, starts.ctypes.data, 64)
+        want = np.zeros(64, np.int64)
+        nb = ref.ref_plan_checkpoints(L, want.ctypes.data, 64)
+        assert nb >= 0
+        assert S == nb + 1 == math.ceil(math.sqrt(L))
+        assert starts[0] == 0 and starts[S] == L
+        assert list(starts[1:S]) == list(want[:nb])
+        seg = np.diff(starts[: S + 1])
+        assert seg.min() >= 1 and seg.max() <= (L + S - 1) // S + 1
+    assert lb.sdb_plan_checkpoints(0, None, 0) == 5  # SDB_PARAM
+    assert ref.ref_plan_checkpoints(0, None, 0) == -1
