@@ -28,6 +28,7 @@ reference rank per core, as its run_workers does) for the same metric.
 import argparse
 import json
 import os
+import re
 import statistics
 import subprocess
 import sys
@@ -538,6 +539,19 @@ def run_ours(args):
     conv_flops = sum(prof[c][1] for c in ("conv_fprop", "conv_dgrad", "conv_wgrad"))
     conv_launches = sum(prof[c][3] for c in ("conv_fprop", "conv_dgrad", "conv_wgrad"))
     step_ms_prof = sum(v[0] for v in prof.values())
+    # backbone (stem, res2-res4, RPN) vs RoI head (res5 + fc): the north star's
+    # ">= 50 % tensor pipe on backbone convs", FLOP-weighted over the conv records
+    conv_parts = {"backbone": [0.0, 0.0], "head": [0.0, 0.0]}
+    for cat, label, ms_r, fl_r, _ in det.profile_records():
+        if cat not in ("conv_fprop", "conv_dgrad", "conv_wgrad"):
+            continue
+        m = re.search(r"N(\d+) H(\d+) W(\d+)", label)
+        if not m:
+            continue
+        n_, h_, w_ = (int(x) for x in m.groups())
+        part = "head" if n_ >= 64 and h_ * w_ <= 196 else "backbone"
+        conv_parts[part][0] += ms_r
+        conv_parts[part][1] += fl_r
     peaks, peak_kind = measured_peaks()
     peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1400.0)))
     achieved = conv_flops / (conv_ms / 1e3) / 1e12 if conv_ms > 0 else 0.0
@@ -590,7 +604,13 @@ def run_ours(args):
                      "frac": achieved / peak if peak else None, "traffic": traffic,
                      "kernel": "conv_tma_kernel (tcgen05 implicit GEMM, TMA/im2col-TMA operands; fprop+dgrad+wgrad, FLOP-weighted)",
                      "peak_source": f"{peak_kind} bf16_tflops_sustained",
-                     "flop_per_step": conv_flops, "ms_per_step": conv_ms, "launches_per_step": conv_launches},
+                     "flop_per_step": conv_flops, "ms_per_step": conv_ms, "launches_per_step": conv_launches,
+                     "backbone_frac": (conv_parts["backbone"][1] / (conv_parts["backbone"][0] / 1e3) / 1e12 / peak
+                                       if conv_parts["backbone"][0] > 0 and peak else None),
+                     "head_frac": (conv_parts["head"][1] / (conv_parts["head"][0] / 1e3) / 1e12 / peak
+                                   if conv_parts["head"][0] > 0 and peak else None),
+                     "by_part_ms": {k: round(v[0], 3) for k, v in conv_parts.items()},
+                     "by_part_tflop": {k: round(v[1] / 1e12, 4) for k, v in conv_parts.items()}},
         "breakdown_ms": {k: round(v[0], 3) for k, v in prof.items()},
         "breakdown_share": {k: round(v[0] / step_ms_prof, 4) for k, v in prof.items()} if step_ms_prof else {},
         "hbm_GBps": {k: round(v[2] / (v[0] / 1e3) / 1e9, 1) for k, v in prof.items() if v[2] > 0 and v[0] > 0},

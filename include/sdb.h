@@ -356,6 +356,11 @@ int sdb_plan_buckets(const int64_t* offsets, int n, int64_t total, int64_t cap_e
  * 6 pooling, 7 targets, 8 proposal, 9 roialign fwd, 10 roialign bwd, 11 losses,
  * 12 optimizer, 13 comm) device ms, algorithmic FLOPs, algorithmic bytes, launches */
 int sdb_det_profile(sdb_det* det, double* ms, double* flops, double* bytes, int64_t* launches, int ncat);
+/* the last profiled step's labelled records (every conv: "fprop|dgrad|wgrad N H W
+ * C K R S st"; norms with SDB_PROFILE_VERBOSE): k < 0 returns the count, else
+ * record k's category, label, device ms, algorithmic FLOPs and bytes */
+int sdb_det_profile_record(sdb_det* det, int k, int* cat, char* label, int cap, double* ms, double* flops,
+                           double* bytes);
 
 #ifdef __cplusplus
 }

@@ -131,6 +131,12 @@ struct Prof {
     std::vector<double> rec_flops, rec_bytes;
     double flops[P_NCAT] = {}, bytes[P_NCAT] = {};
     int64_t launches[P_NCAT] = {};
+    struct Rec {
+        int cat;
+        std::string label;
+        double ms, flops, bytes;
+    };
+    std::vector<Rec> last;  // the last profiled step, per labelled record
     cudaEvent_t get() {
         if (used == pool.size()) {
             cudaEvent_t e;
@@ -978,7 +984,15 @@ void run_step(sdb_det* d) {
     pa.post_k = cf.post_nms; pa.iou_thr = cf.nms_iou; pa.img_h = static_cast<float>(cf.img_h);
     pa.img_w = static_cast<float>(cf.img_w); pa.clip_dw = static_cast<float>(std::log(1000.0 / 16.0));
     pa.rois = d->props; pa.roi_scores = nullptr; pa.keep_pos = d->keep_pos; pa.count = d->prop_count;
-    { PScope ps(d, P_PROPOSAL, 0, 0, 3); CK(rpn_proposals(pa, d->ws, st)); }
+    {
+        // algorithmic bytes: objectness + deltas read, anchors read, the pre-NMS
+        // candidate boxes written and read once, the kept boxes written
+        const double kk = std::min<double>(cf.pre_nms, static_cast<double>(d->nA));
+        const double by = static_cast<double>(cf.batch) * d->n_loc * d->A_pad * 5.0 * d->es + 16.0 * d->nA +
+                          cf.batch * (32.0 * kk + 16.0 * cf.post_nms);
+        PScope ps(d, P_PROPOSAL, 0, by, 3);
+        CK(rpn_proposals(pa, d->ws, st));
+    }
     ProposalTargetArgs pt{};
     pt.proposals = d->props; pt.prop_stride = cf.post_nms; pt.prop_count = d->prop_count; pt.gt = d->gt;
     pt.gt_cls = d->gt_cls; pt.gt_stride = cf.max_gt; pt.gt_count = d->gt_count; pt.keys = d->keys + cf.batch;
@@ -2040,11 +2054,13 @@ int sdb_det_profile(sdb_det* d, double* ms, double* flops, double* bytes, int64_
         CK(cudaStreamSynchronize(d->ctx->stream));
         std::vector<double> acc(P_NCAT, 0.0);
         const bool verbose = std::getenv("SDB_PROFILE_VERBOSE") != nullptr;
+        p.last.clear();
         for (size_t k = 0; k < p.recs.size(); ++k) {
             auto& r = p.recs[k];
             float t = 0;
             CK(cudaEventElapsedTime(&t, r.second.first, r.second.second));
             acc[r.first] += t;
+            if (!p.labels[k].empty()) p.last.push_back({r.first, p.labels[k], t, p.rec_flops[k], p.rec_bytes[k]});
             if (verbose && !p.labels[k].empty())
                 std::fprintf(stderr, "[sdb-prof] %-60s %8.1f us %7.0f TF/s %7.0f GB/s\n", p.labels[k].c_str(),
                              t * 1e3, p.rec_flops[k] / (t * 1e-3) / 1e12, p.rec_bytes[k] / (t * 1e-3) / 1e9);
@@ -2063,6 +2079,24 @@ int sdb_det_profile(sdb_det* d, double* ms, double* flops, double* bytes, int64_
         d->prof.on = false;
         return det_fail(SDB_CUDA, e.what());
     }
+    return SDB_OK;
+}
+
+int sdb_det_profile_record(sdb_det* d, int k, int* cat, char* label, int cap, double* ms, double* flops,
+                           double* bytes) {
+    if (!d) return det_fail(SDB_CONTRACT, "null detector");
+    const auto& L = d->prof.last;
+    if (k < 0) return static_cast<int>(L.size());
+    if (k >= static_cast<int>(L.size())) return det_fail(SDB_PARAM, "profile record index out of range");
+    const auto& r = L[static_cast<size_t>(k)];
+    if (cat) *cat = r.cat;
+    if (label && cap > 0) {
+        std::strncpy(label, r.label.c_str(), static_cast<size_t>(cap) - 1);
+        label[cap - 1] = 0;
+    }
+    if (ms) *ms = r.ms;
+    if (flops) *flops = r.flops;
+    if (bytes) *bytes = r.bytes;
     return SDB_OK;
 }
 

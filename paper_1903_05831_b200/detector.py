@@ -128,6 +128,7 @@ _SIGS = {
     "sdb_det_kernel_launches": [_P, C.POINTER(_L)],
     "sdb_det_memory": [_P, C.POINTER(_L), C.POINTER(_L), C.POINTER(_I)],
     "sdb_det_profile": [_P, _P, _P, _P, _P, _I],
+    "sdb_det_profile_record": [_P, _I, C.POINTER(_I), C.c_char_p, _I, C.POINTER(_D), C.POINTER(_D), C.POINTER(_D)],
     "sdb_ctx_create": [_I, _I, _I, _P, C.POINTER(_P)],
     "sdb_ctx_destroy": [_P],
     "sdb_get_nccl_unique_id": [_P],
@@ -309,6 +310,18 @@ class Detector:
         la = (_L * n)()
         check(L().sdb_det_profile(self.h, ms, fl, by, la, n))
         return {c: (ms[i], fl[i], by[i], la[i]) for i, c in enumerate(self.PROFILE_CATS)}
+
+    def profile_records(self):
+        """labelled records of the last profile() step: [(category, label, ms, flops, bytes)]"""
+        lb = L()
+        n = lb.sdb_det_profile_record(self.h, -1, None, None, 0, None, None, None)
+        out = []
+        for k in range(n):
+            cat, ms, fl, by = _I(), _D(), _D(), _D()
+            lab = C.create_string_buffer(160)
+            check(lb.sdb_det_profile_record(self.h, k, C.byref(cat), lab, 160, C.byref(ms), C.byref(fl), C.byref(by)))
+            out.append((self.PROFILE_CATS[cat.value], lab.value.decode(), ms.value, fl.value, by.value))
+        return out
 
     def save_checkpoint(self, path: str, step: int, config_digest: int = 0):
         """SDCK v1 file (src/checkpoint.cpp:47-84): masters, velocity, loss-scale state"""
