@@ -2178,7 +2178,9 @@ cudaError_t conv_wgrad_deferred(const ConvShape& g, int dtype, const void* x, co
     if (tc && tma_ok(a, WGRAD)) {
         ConvArgs at = a;
         std::swap(at.M, at.NG);  // partials [split][(r,s,c)][k]
-        e = launch_tma_pick<WGRAD>(at, splits, st);
+        // diagnostic only (wrong gradients): time the step without the wgrad GEMMs
+        static const bool skip = std::getenv("SDB_DIAG_SKIP_WGRAD") != nullptr;
+        e = skip && job ? cudaSuccess : launch_tma_pick<WGRAD>(at, splits, st);
         if (e != cudaSuccess) return e;
         if (job) {
             *job = WgradJob{static_cast<const float*>(ws), dw, splits, at.M, at.NG, 1};

@@ -1156,7 +1156,9 @@ void run_step(sdb_det* d) {
         CK(cudaEventRecord(d->ev_join, d->comm));
         CK(cudaStreamWaitEvent(st, d->ev_join, 0));
     }
-    PScope ps_opt(d, P_OPTIM, 0, (d->es + 12.0 + (d->dt == kF16 ? 2.0 : 0.0)) * d->n_w + 16.0 * d->n_bn, 5);
+    // algorithmic bytes: gradient read, fp32 master + velocity read and written,
+    // fp16 shadow written (20 B/param in fp16 mode); BN params 20 B (fp32 grads)
+    PScope ps_opt(d, P_OPTIM, 0, (d->es + 16.0 + (d->dt == kF16 ? 2.0 : 0.0)) * d->n_w + 20.0 * d->n_bn, 5);
     if (!d->defer_wgrad) CK(nonfinite_check(d->dt, d->g, d->n_w, d->flag, st));  // else: in the reduces
     CK(nonfinite_check(kF32, d->bng, d->n_bn, d->flag, st));
     const double K = static_cast<double>(d->ctx->world);
