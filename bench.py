@@ -416,6 +416,24 @@ def run_c3(args):
         e1.record()
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
+    # per-part device times (same inputs, each part timed alone after the run)
+    parts_ms = {}
+    rois, _, _, _ = sd.rpn_proposal(logits, deltas, anchors, A, 12000, 0.7, 2000, 800.0, 1333.0)
+    rois5[:, 1:] = rois[:, :512, :].reshape(R, 4)
+    for name, fn in (
+            ("proposal", lambda: sd.rpn_proposal(logits, deltas, anchors, A, 12000, 0.7, 2000, 800.0, 1333.0)),
+            ("roialign_fwd", lambda: sd.check(lib.sdb_roialign_fwd(sd.ctx(), 1, sd.ptr(feat), B, H, W, Cc,
+                                                                   sd.ptr(rois5), R, P, 1.0 / 16, 2, sd.ptr(out), st))),
+            ("roialign_bwd", lambda: sd.check(lib.sdb_roialign_bwd(sd.ctx(), 1, sd.ptr(dy), B, H, W, Cc,
+                                                                   sd.ptr(rois5), R, P, 1.0 / 16, 2, sd.ptr(dx), st)))):
+        fn()
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(10):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        parts_ms[name] = round(e0.elapsed_time(e1) / 10, 4)
     # algorithmic bytes of the RoIAlign passes: fwd writes R*P*P*C fp16
     # and reads the feature once; bwd reads dY and writes dX
     ra_bytes = 2 * (R * P * P * Cc * 2) + 2 * feat.numel() * 2
@@ -425,7 +443,10 @@ def run_c3(args):
             "data": "synthetic (BASELINE C3 distributions)",
             "config": {"workload": "C3: batch 8, 1024x50x84 fp16, 15 anchors/loc, 12000->2000 @0.7, RoIAlign 14x14 "
                                    "on 512 RoIs/img fwd+bwd"},
-            "roialign_alg_bytes_per_step": ra_bytes, "clocks": clk.summary()}
+            "roialign_alg_bytes_per_step": ra_bytes, "breakdown_ms": parts_ms,
+            "hbm_GBps": {k: round(ra_bytes / 2 / (parts_ms[k] / 1e3) / 1e9, 1)
+                         for k in ("roialign_fwd", "roialign_bwd") if parts_ms.get(k)},
+            "clocks": clk.summary()}
     if rank == 0:
         print(json.dumps(line))
 

@@ -3,13 +3,14 @@
 //
 // RoIAlign: aligned (half-pixel) corners, fixed sampling ratio, average of the
 // bilinear samples; the restated oracle is orc_roialign_fwd/bwd (numerically
-// identical to torchvision.ops.roi_align(aligned=True)).  Forward: one thread
-// per (RoI, bin, 8 channels), 128-bit loads of the 4 corners of each sample.
-// Backward is a deterministic GATHER (no atomics): one CTA owns an 8x8 pixel
-// tile x 256-channel slab of dX in registers, walks the RoIs of its image
-// that reach the tile in index order and, using the separable bilinear
-// weights WY[ph][h] x WX[pw][w] staged in smem, accumulates every dY
-// contribution in a fixed order -- bitwise reproducible run to run.
+// identical to torchvision.ops.roi_align(aligned=True)).  Forward: one warp
+// per (RoI, bin row, 256 channels), lane = 8 channels, coalesced 512-byte
+// corner-row reads through L1 (below).
+// Backward is a deterministic GATHER (no atomics): one warp per (pixel,
+// channel slab) walks the RoIs whose nonzero-weight box holds its pixel in
+// index order and accumulates, from the separable per-RoI weight tables
+// WY[h][ph] x WX[w][pw], every dY contribution in a fixed order -- bitwise
+// reproducible run to run.
 //
 // Losses fold the loss scale into backward exactly like the reference CE op
 // (src/model.cpp:132-150): forward returns the unscaled loss, backward
@@ -399,6 +400,79 @@ __global__ void __launch_bounds__(kRaBlk * kRaBlk * 32) roialign_bwd_gather_kern
 #pragma unroll
     for (int v = 0; v < V; ++v)
         if (c0 + v * 256 < C) st8x2<T>(dfeat + ((static_cast<int64_t>(n) * H + y) * W + x) * C + c0 + v * 256, acc[v]);
+}
+
+// ---------------------------------------------------------------- RoIAlign fwd (warp per bin row)
+// Lane = 8 channels of a 256-channel chunk, so every corner read is one
+// coalesced 512-byte row piece through L1 (the image's feature map, 8.6 MB at
+// C4, stays L2-resident; corners shared by neighbouring samples and bins hit
+// L1).  A warp owns one (RoI, bin row, chunk): the bin row's sample rows are
+// tabulated once, each bin's sample columns per bin, and the 4 corners of each
+// sample are blended in the same order and with the same packed FMAs as the
+// smem-staged kernel above (bit-identical outputs); every bin leaves as one
+// coalesced 512-byte store.  (The smem-staged slab kernel is bound by shared-
+// memory bank conflicts of its random per-thread corner reads -- 62 % of its
+// wavefronts were conflicts in ncu -- and stays for sampling ratios != 2.)
+constexpr int kRaWarps = 8;
+
+template <class T, int SR>
+__global__ void __launch_bounds__(32 * kRaWarps) roialign_fwd_warp_kernel(const T* __restrict__ feat, int H, int W,
+                                                                           int C, const float* __restrict__ rois,
+                                                                           int R, int P, float scale, int step,
+                                                                           T* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int Po = (P + step - 1) / step;
+    const int nch = (C + 255) / 256;
+    const int gw = blockIdx.x * kRaWarps + (threadIdx.x >> 5);
+    const int chunk = gw % nch, rest = gw / nch;
+    const int phi = rest % Po, r = rest / Po;
+    if (r >= R) return;
+    const int c = chunk * 256 + lane * 8;
+    if (c >= C) return;
+    T* o = out + (static_cast<int64_t>(r) * Po + phi) * Po * C + c;
+    const Geom g = roi_geom(rois + static_cast<int64_t>(r) * 5, P, scale);
+    const float2 ic = make_float2(1.0f / (SR * SR), 1.0f / (SR * SR));
+    if (g.b < 0) {
+        const float2 z[4] = {};
+        for (int pwi = 0; pwi < Po; ++pwi) st8x2<T>(o + static_cast<int64_t>(pwi) * C, z);
+        return;
+    }
+    // element offsets (pixel row * W * C, pixel column * C) and weights
+    RaTab ty[SR];
+#pragma unroll
+    for (int is = 0; is < SR; ++is) ty[is] = ra_axis(sample_coord(g.sh, phi * step, g.bh, is, SR), H, W * C);
+    const T* f = feat + static_cast<int64_t>(g.b) * H * W * C + c;
+    for (int pwi = 0; pwi < Po; ++pwi) {
+        RaTab tx[SR];
+#pragma unroll
+        for (int is = 0; is < SR; ++is) tx[is] = ra_axis(sample_coord(g.sw, pwi * step, g.bw, is, SR), W, C);
+        float2 acc[4] = {};
+#pragma unroll
+        for (int iy = 0; iy < SR; ++iy) {
+            const RaTab Y = ty[iy];
+            float2 v[SR][4][4];
+#pragma unroll
+            for (int ix = 0; ix < SR; ++ix) {
+                const RaTab X = tx[ix];
+                ld8x2<T>(f + Y.lo + X.lo, v[ix][0]);
+                ld8x2<T>(f + Y.lo + X.hi, v[ix][1]);
+                ld8x2<T>(f + Y.hi + X.lo, v[ix][2]);
+                ld8x2<T>(f + Y.hi + X.hi, v[ix][3]);
+            }
+#pragma unroll
+            for (int ix = 0; ix < SR; ++ix) {
+                const RaTab X = tx[ix];
+                const float2 w1 = make_float2(Y.wl * X.wl, Y.wl * X.wl), w2 = make_float2(Y.wl * X.wh, Y.wl * X.wh);
+                const float2 w3 = make_float2(Y.wh * X.wl, Y.wh * X.wl), w4 = make_float2(Y.wh * X.wh, Y.wh * X.wh);
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    acc[k] = ffma2(w4, v[ix][3][k], ffma2(w3, v[ix][2][k], ffma2(w2, v[ix][1][k], ffma2(w1, v[ix][0][k], acc[k]))));
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) acc[k] = ffma2(acc[k], ic, make_float2(0.f, 0.f));
+        st8x2<T>(o + static_cast<int64_t>(pwi) * C, acc);
+    }
 }
 
 // ---------------------------------------------------------------- pooling
@@ -973,6 +1047,18 @@ cudaError_t roialign_fwd(int dtype, const void* feat, int N, int H, int W, int C
     if (step < 1) return cudaErrorInvalidValue;
     if (R == 0) return cudaSuccess;
     const int Po = (P + step - 1) / step;
+    if (sr == 2 && C % 8 == 0) {
+        const int64_t warps = static_cast<int64_t>(R) * Po * ((C + 255) / 256);
+        const unsigned blocks = static_cast<unsigned>((warps + kRaWarps - 1) / kRaWarps);
+        if (dtype == kF16)
+            roialign_fwd_warp_kernel<__half, 2><<<blocks, 32 * kRaWarps, 0, st>>>(
+                cp<__half>(feat), H, W, C, rois, R, P, scale, step, static_cast<__half*>(out));
+        else
+            roialign_fwd_warp_kernel<float, 2><<<blocks, 32 * kRaWarps, 0, st>>>(
+                cp<float>(feat), H, W, C, rois, R, P, scale, step, static_cast<float*>(out));
+        return cudaGetLastError();
+    }
+    // other sampling ratios: the smem-staged slab kernel
     const size_t smem = ra_fwd_smem(H, W, R, Po, sr, dtype);
     if (smem <= 200 * 1024 && sr <= 8) {
         const dim3 grid(C / 8, N);
