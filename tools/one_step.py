@@ -1,6 +1,6 @@
 """Run the C4 training step a few times (eager first step, then the CUDA graph)
 and bracket exactly ONE graph step with cudaProfilerStart/Stop, for
-    ncu --profile-from-start off ... python tools/one_step.py
+    ncu --profile-from-start off ... python tools/one_step.py [c4] [warm steps]
 (the launch list of one step: profiles/r01_launches_*.csv)."""
 import os
 import sys
@@ -20,11 +20,14 @@ def main():
     g = torch.Generator(device="cuda")
     g.manual_seed(1234)
     imgs[..., :3] = torch.randn((B, p.img_h, p.img_w, 3), generator=g, device="cuda", dtype=torch.float16)
-    for i in range(4):
+    # the profiled step: after `warm` steps (the RoI distribution -- and with
+    # it the RoIAlign backward's cost -- settles after the first ~15 steps)
+    warm = int(sys.argv[2]) if len(sys.argv) > 2 else 20
+    for i in range(warm):
         det.feed(D.batch_slots(i + 1, 0, 1, B), images=imgs, images_on_host=False)
         det.step()
     torch.cuda.synchronize()
-    det.feed(D.batch_slots(5, 0, 1, B), images=imgs, images_on_host=False)
+    det.feed(D.batch_slots(warm + 1, 0, 1, B), images=imgs, images_on_host=False)
     torch.cuda.synchronize()
     torch.cuda.cudart().cudaProfilerStart()
     det.step()
