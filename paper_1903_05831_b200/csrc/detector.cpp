@@ -225,6 +225,11 @@ struct sdb_det {
     // accumulates onto the RoIAlign gradient) also run there, while the main
     // stream is in the latency-bound proposal layer and the RoI head
     cudaEvent_t ev_rpn_fork = nullptr, ev_rpn_join = nullptr;
+    // the downsampling shortcut (down conv + its norm) of a stage's first block
+    // runs on bst, concurrently with the block's conv1-conv3 chain (forward)
+    cudaStream_t bst = nullptr;
+    cudaEvent_t ev_b_fork = nullptr, ev_b_join = nullptr;
+    ConvStats cst2{};
     void* drpn_side = nullptr;
     cudaEvent_t dzr_ev[kDzRing] = {};
     bool dzr_busy[kDzRing] = {};
@@ -271,6 +276,7 @@ struct sdb_det {
     // runs the data-parallel code path on one GPU)
     bool comm_on = false;
     float* sbn_red = nullptr;  // sync_bn backward sums [2 * max C]
+    void* ws2 = nullptr;       // workspace of the concurrent shortcut branch
     // sharded optimizer: buckets are reduce-scattered, each rank
     // updates its 1/K shard of the fp32 masters and all-gathers the fp16 shadows
     bool shard = false;
@@ -630,7 +636,27 @@ void norm_bwd(sdb_det* d, const NormL& n, const Act& z, const Act& a, const void
     }
 }
 
+// the shortcut branch of a downsampling block on d->bst: fused-statistics fprop
+// + InPlace-ABN (in place), its own ConvStats; joined before the residual add
+void shortcut_fwd_branch(sdb_det* d, Block& b) {
+    CK(cudaEventRecord(d->ev_b_fork, d->ctx->stream));
+    CK(cudaStreamWaitEvent(d->bst, d->ev_b_fork, 0));
+    CK(conv_fprop(b.down.g, d->dt, b.in.p, d->wdev_ptr(b.down.p), b.zd.p, d->bst, &d->cst2));
+    const int64_t rows = static_cast<int64_t>(b.zd.n) * b.zd.h * b.zd.w;
+    if (d->cst2.produced)
+        CK(bn_forward_conv_stats(d->dt, b.zd.p, d->bnp(b.nd.pg), d->bnp(b.nd.pb), b.d.p, b.nd.mean, b.nd.invstd, rows,
+                                 b.nd.C, d->cfg.eps, b.nd.act, b.nd.slope, d->cst2, d->bst));
+    else
+        CK(bn_forward(d->dt, b.zd.p, d->bnp(b.nd.pg), d->bnp(b.nd.pb), b.d.p, b.nd.mean, b.nd.invstd, rows, b.nd.C,
+                      d->cfg.eps, b.nd.act, b.nd.slope, d->ws2, d->bst));
+    d->cst2.produced = 0;
+    CK(cudaEventRecord(d->ev_b_join, d->bst));
+}
+
 void block_fwd(sdb_det* d, Block& b) {
+    // concurrent shortcut branch: fp16 InPlace-ABN graph steps (not the eager profile)
+    const bool branch = b.has_down && d->bst && !d->prof.on && b.n3.act == 2;
+    if (branch) shortcut_fwd_branch(d, b);
     conv_fwd(d, b.c1, b.in, b.z1, true);
     norm_fwd(d, b.n1, b.z1, b.a1);
     conv_fwd(d, b.c2, b.a1, b.z2, true);
@@ -659,8 +685,12 @@ void block_fwd(sdb_det* d, Block& b) {
         }
         const Act* sc = &b.in;
         if (b.has_down) {
-            conv_fwd(d, b.down, b.in, b.zd, true);
-            norm_fwd(d, b.nd, b.zd, b.d);
+            if (branch) {
+                CK(cudaStreamWaitEvent(d->ctx->stream, d->ev_b_join, 0));
+            } else {
+                conv_fwd(d, b.down, b.in, b.zd, true);
+                norm_fwd(d, b.nd, b.zd, b.d);
+            }
             sc = &b.d;
         }
         PScope ps(d, P_NORM_F, 0, 4.0 * d->es * b.out.numel());
@@ -1433,6 +1463,21 @@ int sdb_det_create(sdb_ctx* ctx, const sdb_det_config* cfgp, sdb_det** out) {
             d->wg_arena = static_cast<uint8_t*>(d->alloc(off));
             d->side_wgrad = std::getenv("SDB_NO_SIDE_WGRAD") == nullptr;
         }
+        if (d->dt == kF16 && cf.mode == 1 && std::getenv("SDB_NO_BRANCH") == nullptr) {
+            int lo = 0, hi = 0;
+            CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            CK(cudaStreamCreateWithPriority(&d->bst, cudaStreamNonBlocking, hi));
+            CK(cudaEventCreateWithFlags(&d->ev_b_fork, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&d->ev_b_join, cudaEventDisableTiming));
+            d->cst2.cap_bytes = d->cst.cap_bytes;
+            d->cst2.buf = static_cast<double*>(d->alloc(d->cst2.cap_bytes));
+            size_t m2 = 0;
+            for (auto& bl : d->backbone)
+                if (bl.has_down) m2 = std::max(m2, norm_workspace_bytes(static_cast<int64_t>(bl.zd.n) * bl.zd.h * bl.zd.w, bl.zd.c));
+            for (auto& bl : d->head)
+                if (bl.has_down) m2 = std::max(m2, norm_workspace_bytes(static_cast<int64_t>(bl.zd.n) * bl.zd.h * bl.zd.w, bl.zd.c));
+            d->ws2 = d->alloc(std::max<size_t>(m2, 256));
+        }
         if (d->side_wgrad) {
             int lo = 0, hi = 0;
             CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -1536,6 +1581,11 @@ int sdb_det_destroy(sdb_det* d) {
     }
     cudaFreeHost(d->h_losses);
     if (d->ck_ev) cudaEventDestroy(d->ck_ev);
+    if (d->bst) {
+        cudaEventDestroy(d->ev_b_fork);
+        cudaEventDestroy(d->ev_b_join);
+        cudaStreamDestroy(d->bst);
+    }
     for (auto e : d->bucket_ev) cudaEventDestroy(e);
     if (d->wst) {
         for (auto e : d->dzr_ev) cudaEventDestroy(e);
