@@ -281,14 +281,18 @@ __global__ void __launch_bounds__(kRaFwdThreads) roialign_fwd_smem_kernel(const 
 //   1. roialign_bwd_weights_kernel: one warp per RoI tabulates WY_r / WX_r for
 //      every pixel row / column and the bounding box of the nonzero ones
 //      (shared by all pixels and channel slabs: computed once per step);
-//   2. roialign_bwd_gather_kernel: one warp per (pixel, 256*V-channel slab),
-//      lane = V 8-channel chunks; it walks the RoIs whose box holds its pixel
-//      (ballot over the box table, index order), fetches the RoI's 2 x pw
-//      weights of its row and column in one load per lane, and accumulates
-//      the nonzero bin pairs in registers.  No shared memory and no barriers;
-//      a CTA is a 4x4 pixel block, so the dY rows its pixels share hit L1.
-// The summation order per output element is fixed (RoI, ph, pw) -- bitwise
-// reproducible run to run; products are accumulated with packed fp32 FMAs.
+//   2. roialign_tile_list_kernel / roialign_seg_plan_kernel: per 4x4 pixel
+//      block, the RoIs that reach it (index order) and their exact pair
+//      count, cut into work-balanced segments (below);
+//   3. roialign_bwd_gather_kernel: one CTA per (block, segment), one warp per
+//      (pixel, 256*V-channel slab), lane = V 8-channel chunks; it walks the
+//      segment's RoIs whose box holds its pixel (ballot, list order), fetches
+//      the RoI's 2 x pw weights of its row and column in one load per lane,
+//      and accumulates the nonzero bin pairs in registers; the dY rows the
+//      block's pixels share hit L1.
+// The summation order per output element is fixed (segment, RoI, ph, pw) --
+// bitwise reproducible run to run; products are accumulated with packed fp32
+// FMAs.
 constexpr int kRaBlk = 4;  // CTA = kRaBlk x kRaBlk pixels (one warp each)
 
 SDB_DEV float bin_axis_weight(float start, float bin, int pb_full, int sr, int pix, int lim) {
@@ -308,7 +312,8 @@ SDB_DEV float bin_axis_weight(float start, float bin, int pb_full, int sr, int p
 
 __global__ void __launch_bounds__(256) roialign_bwd_weights_kernel(const float* __restrict__ rois, int R, int H, int W,
                                                                    int P, float scale, int sr, int step, int pw,
-                                                                   float* __restrict__ tab, int4* __restrict__ box) {
+                                                                   float* __restrict__ tab, int4* __restrict__ box,
+                                                                   uint8_t* __restrict__ nzc) {
     const int r = static_cast<int>((blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5);
     const int lane = threadIdx.x & 31;
     if (r >= R) return;
@@ -320,13 +325,16 @@ __global__ void __launch_bounds__(256) roialign_bwd_weights_kernel(const float* 
         const bool isx = t >= H;
         const int pix = isx ? t - H : t;
         bool any = false;
+        int nz = 0;
         for (int pb = 0; pb < pw; ++pb) {
             const float w = pb < Po ? (isx ? bin_axis_weight(g.sw, g.bw, pb * step, sr, pix, W)
                                            : bin_axis_weight(g.sh, g.bh, pb * step, sr, pix, H))
                                     : 0.f;
             ty[static_cast<int64_t>(t) * pw + pb] = w;
             any |= w != 0.f;
+            nz += w != 0.f;
         }
+        nzc[static_cast<int64_t>(r) * (H + W) + t] = static_cast<uint8_t>(nz);
         if (any) {
             if (isx) { xlo = min(xlo, pix); xhi = max(xhi, pix); }
             else { ylo = min(ylo, pix); yhi = max(yhi, pix); }
@@ -345,61 +353,305 @@ __global__ void __launch_bounds__(256) roialign_bwd_weights_kernel(const float* 
     }
 }
 
+// Work balance.  The gather above walks, per pixel warp, every RoI that
+// reaches its pixel: where the trained RPN stacks hundreds of small RoIs on a
+// few pixels (thousands of (RoI, bin) contributions on one pixel), that one
+// warp's serial walk was the whole kernel's duration (0.68-2.9 ms instead of
+// 0.14-0.2).  So the pixel blocks' RoI lists are built once
+// (roialign_tile_list_kernel, index order), each block's work -- its exact
+// (pixel, RoI, bin) pair count, from per-row / per-column nonzero-bin counts
+// of the weight table -- is cut into up to kRaSegMax consecutive segments of
+// about kRaSegWork pairs, and one CTA takes each segment: a single-segment
+// block writes dX directly; a split block's segments write fp32 partials and
+// the last to finish (ticket) sums them in segment order.  Per element the
+// order is fixed (segment, RoI, ph, pw): bitwise reproducible, no atomics on
+// data.
+constexpr int kRaSegMax = 32;
+constexpr int kRaSegWork = 1024;  // (pixel, RoI, bin) pairs per segment at 7 x 7 bins, about
+constexpr int kRaSlots = 512;     // partial-sum slots (segments of split blocks) per channel chunk
+
+__global__ void __launch_bounds__(256) roialign_tile_list_kernel(const int4* __restrict__ box,
+                                                                 const uint8_t* __restrict__ nzc, int R, int H, int W,
+                                                                 long long seg_work, int* __restrict__ tl_cnt,
+                                                                 int* __restrict__ tl_nseg,
+                                                                 int* __restrict__ seg_start, int* __restrict__ tl) {
+    extern __shared__ int wk[];  // [R] work of each listed RoI
+    __shared__ int wsum[8];
+    __shared__ long long wtot[8];
+    __shared__ int cnt;
+    __shared__ long long run;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int bxn = (W + kRaBlk - 1) / kRaBlk, byn = (H + kRaBlk - 1) / kRaBlk;
+    const int tile = blockIdx.x, n = blockIdx.y;
+    const int tx0 = (tile % bxn) * kRaBlk, ty0 = (tile / bxn) * kRaBlk;
+    const int t = n * bxn * byn + tile;
+    int* out = tl + static_cast<int64_t>(t) * R;
+    if (tid == 0) cnt = 0;
+    __syncthreads();
+    for (int base = 0; base < R; base += 256) {
+        bool hit = false;
+        int w = 0;
+        if (base + tid < R) {
+            const int r = base + tid;
+            const int4 b = __ldg(box + r);
+            hit = b.x == n && (b.y & 0xffff) <= ty0 + kRaBlk - 1 && (b.y >> 16) >= ty0 &&
+                  (b.z & 0xffff) <= tx0 + kRaBlk - 1 && (b.z >> 16) >= tx0;
+            if (hit) {
+                // pairs over the block's pixels: (sum of the rows' nonzero bins) x (columns')
+                const uint8_t* c = nzc + static_cast<int64_t>(r) * (H + W);
+                int a = 0, bb = 0;
+                for (int k = 0; k < kRaBlk; ++k) {
+                    if (ty0 + k < H) a += c[ty0 + k];
+                    if (tx0 + k < W) bb += c[H + tx0 + k];
+                }
+                w = a * bb;
+            }
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, hit);
+        if (lane == 0) wsum[warp] = __popc(m);
+        __syncthreads();
+        int off = cnt;
+        for (int w2 = 0; w2 < warp; ++w2) off += wsum[w2];
+        if (hit) {
+            const int i = off + __popc(m & ((1u << lane) - 1u));
+            out[i] = base + tid;
+            wk[i] = w;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            int s2 = 0;
+            for (int w2 = 0; w2 < 8; ++w2) s2 += wsum[w2];
+            cnt += s2;
+        }
+        __syncthreads();
+    }
+    const int nl = cnt;
+    // total work -> segment count; cut where the running work passes s * total / ns
+    long long my = 0;
+    for (int i = tid; i < nl; i += 256) my += wk[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) my += __shfl_xor_sync(0xffffffffu, my, o);
+    if (lane == 0) wtot[warp] = my;
+    __syncthreads();
+    long long total = 0;
+    for (int w2 = 0; w2 < 8; ++w2) total += wtot[w2];
+    const long long nsl = (total + seg_work - 1) / seg_work;
+    const int ns = nsl < 1 ? 1 : (nsl > kRaSegMax ? kRaSegMax : static_cast<int>(nsl));
+    int* ss = seg_start + static_cast<int64_t>(t) * (kRaSegMax + 1);
+    if (tid == 0) {
+        tl_cnt[t] = nl;
+        tl_nseg[t] = ns;
+        ss[0] = 0;
+        for (int s2 = 1; s2 <= ns; ++s2) ss[s2] = nl;  // segments left empty by heavy entries end at nl
+        run = 0;
+    }
+    __syncthreads();
+    if (ns > 1) {
+        // entry i belongs to segment min(ns - 1, before_i * ns / total), before_i = the
+        // work of the entries ahead of it (non-decreasing in i); a segment starts at its
+        // first entry, one that no entry maps to is left empty
+        for (int base = 0; base < nl; base += 256) {
+            const int i = base + tid;
+            const long long w = i < nl ? wk[i] : 0;
+            long long v = w;  // inclusive warp scan
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const long long u = __shfl_up_sync(0xffffffffu, v, o);
+                if (lane >= o) v += u;
+            }
+            if (lane == 31) wtot[warp] = v;
+            __syncthreads();
+            long long pre = run;
+            for (int w2 = 0; w2 < warp; ++w2) pre += wtot[w2];
+            const long long before = pre + v - w;
+            if (i < nl) {
+                const long long sq = (before * ns) / total;
+                const int si = sq > ns - 1 ? ns - 1 : static_cast<int>(sq);
+                if (si >= 1) atomicMin(&ss[si], i);
+            }
+            __syncthreads();
+            if (tid == 0)
+                for (int w2 = 0; w2 < 8; ++w2) run += wtot[w2];
+            __syncthreads();
+        }
+        if (tid == 0)
+            for (int s2 = ns - 1; s2 >= 1; --s2) ss[s2] = min(ss[s2], ss[s2 + 1]);
+    }
+}
+
+// one CTA (block scans): the compact table of (block, segment) items and the
+// partial slots of split blocks; a split whose slots would pass the capacity
+// (counted over all requested splits ahead of it) keeps its block whole --
+// slower, same sums
+__global__ void __launch_bounds__(1024) roialign_seg_plan_kernel(const int* __restrict__ tl_nseg, int nt,
+                                                                 int* __restrict__ seg, int* __restrict__ nseg_total,
+                                                                 int* __restrict__ slot, unsigned* __restrict__ ticket,
+                                                                 int nticket) {
+    __shared__ int wa[32], wb[32];
+    __shared__ int run_req, run_seg;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    for (int i = tid; i < nticket; i += blockDim.x) ticket[i] = 0u;
+    if (tid == 0) run_req = run_seg = 0;
+    __syncthreads();
+    for (int base = 0; base < nt; base += 1024) {
+        const int t = base + tid;
+        const int req = t < nt ? tl_nseg[t] : 1;
+        const int want = req > 1 ? req : 0;
+        // exclusive prefix of the requested slots
+        int a = want;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, a, o);
+            if (lane >= o) a += u;
+        }
+        if (lane == 31) wa[warp] = a;
+        __syncthreads();
+        int pre = run_req;
+        for (int w2 = 0; w2 < warp; ++w2) pre += wa[w2];
+        const int before = pre + a - want;
+        const bool split = want > 0 && before + want <= kRaSlots;
+        const int ns = t < nt ? (split ? req : 1) : 0;
+        // exclusive prefix of the segment items
+        int b = ns;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, b, o);
+            if (lane >= o) b += u;
+        }
+        if (lane == 31) wb[warp] = b;
+        __syncthreads();
+        int pre2 = run_seg;
+        for (int w2 = 0; w2 < warp; ++w2) pre2 += wb[w2];
+        const int k0 = pre2 + b - ns;
+        if (t < nt) {
+            slot[t] = split ? before : -1;
+            for (int s2 = 0; s2 < ns; ++s2) seg[k0 + s2] = (t << 5) | s2;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            for (int w2 = 0; w2 < 32; ++w2) {
+                run_req += wa[w2];
+                run_seg += wb[w2];
+            }
+        }
+        __syncthreads();
+    }
+    if (tid == 0) *nseg_total = run_seg;
+}
+
+// the per-pixel gather over one (block, segment) item at a time (persistent CTAs)
 template <class T, int V>
 __global__ void __launch_bounds__(kRaBlk * kRaBlk * 32) roialign_bwd_gather_kernel(
     const T* __restrict__ dy, int H, int W, int C, const int4* __restrict__ box, const float* __restrict__ tab, int R,
-    int Po, int pw, float inv_count, T* __restrict__ dfeat) {
+    int Po, int pw, float inv_count, T* __restrict__ dfeat, const int* __restrict__ tl_cnt,
+    const int* __restrict__ tl_nseg, const int* __restrict__ seg_start, const int* __restrict__ tl,
+    const int* __restrict__ seg, const int* __restrict__ nseg_total, const int* __restrict__ slot,
+    unsigned* __restrict__ ticket, float* __restrict__ part) {
+    __shared__ int s_last;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int bxn = (W + kRaBlk - 1) / kRaBlk;
-    const int y = (blockIdx.x / bxn) * kRaBlk + warp / kRaBlk;
-    const int x = (blockIdx.x % bxn) * kRaBlk + warp % kRaBlk;
-    const int n = blockIdx.z;
-    const int c0 = blockIdx.y * 256 * V + lane * 8;
-    if (y >= H || x >= W) return;  // whole warp: no barriers below
-    float2 acc[V][4];
-#pragma unroll
-    for (int v = 0; v < V; ++v)
-#pragma unroll
-        for (int k = 0; k < 4; ++k) acc[v][k] = make_float2(0.f, 0.f);
+    const int bxn = (W + kRaBlk - 1) / kRaBlk, byn = (H + kRaBlk - 1) / kRaBlk, ntiles = bxn * byn;
+    const int chunk = blockIdx.y, nch = gridDim.y;
+    const int c0 = chunk * 256 * V + lane * 8;
     const int64_t row_stride = static_cast<int64_t>(Po) * C;
-    for (int r0 = 0; r0 < R; r0 += 32) {
-        bool hit = false;
-        if (r0 + lane < R) {
-            const int4 b = __ldg(box + r0 + lane);
-            hit = b.x == n && y >= (b.y & 0xffff) && y <= (b.y >> 16) && x >= (b.z & 0xffff) && x <= (b.z >> 16);
-        }
-        for (unsigned m = __ballot_sync(0xffffffffu, hit); m; m &= m - 1) {
-            const int r = r0 + __ffs(m) - 1;
-            const float* trow = tab + static_cast<int64_t>(r) * (H + W) * pw;
-            float w = 0.f;
-            if (lane < pw) w = __ldg(trow + y * pw + lane);
-            else if (lane >= 16 && lane < 16 + pw) w = __ldg(trow + (H + x) * pw + (lane - 16));
-            const unsigned nz = __ballot_sync(0xffffffffu, w != 0.f);
-            const T* d = dy + static_cast<int64_t>(r) * Po * row_stride + c0;
-            for (unsigned a = nz & 0xffffu; a; a &= a - 1) {
-                const int ph = __ffs(a) - 1;
-                const float wy = __shfl_sync(0xffffffffu, w, ph);
-                for (unsigned b2 = nz >> 16; b2; b2 &= b2 - 1) {
-                    const int pwi = __ffs(b2) - 1;
-                    const float wx = __shfl_sync(0xffffffffu, w, 16 + pwi);
-                    const float wgt = wy * wx * inv_count;
-                    const float2 w2 = make_float2(wgt, wgt);
-                    const T* dd = d + ph * row_stride + static_cast<int64_t>(pwi) * C;
+    const int total = *nseg_total;
+    for (int e = blockIdx.x; e < total; e += gridDim.x) {
+        const int sv = seg[e], t = sv >> 5, sg = sv & 31;
+        const int n = t / ntiles, tile = t - n * ntiles;
+        const int y = (tile / bxn) * kRaBlk + warp / kRaBlk;
+        const int x = (tile % bxn) * kRaBlk + warp % kRaBlk;
+        const int sl = slot[t];
+        const int ns = sl < 0 ? 1 : tl_nseg[t];
+        const int* ss = seg_start + static_cast<int64_t>(t) * (kRaSegMax + 1);
+        const int lo = sl < 0 ? 0 : ss[sg], hi = sl < 0 ? tl_cnt[t] : ss[sg + 1];
+        const int* list = tl + static_cast<int64_t>(t) * R;
+        const bool pix = y < H && x < W;
+        float2 acc[V][4];
 #pragma unroll
-                    for (int v = 0; v < V; ++v) {
-                        if (c0 + v * 256 >= C) break;
-                        float2 val[4];
-                        ld8x2<T>(dd + v * 256, val);
+        for (int v = 0; v < V; ++v)
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) acc[v][k] = ffma2(w2, val[k], acc[v][k]);
+            for (int k = 0; k < 4; ++k) acc[v][k] = make_float2(0.f, 0.f);
+        if (pix) {
+            for (int r0 = lo; r0 < hi; r0 += 32) {
+                bool hit = false;
+                int rl = 0;
+                if (r0 + lane < hi) {
+                    rl = __ldg(list + r0 + lane);
+                    const int4 b = __ldg(box + rl);
+                    hit = y >= (b.y & 0xffff) && y <= (b.y >> 16) && x >= (b.z & 0xffff) && x <= (b.z >> 16);
+                }
+                for (unsigned m = __ballot_sync(0xffffffffu, hit); m; m &= m - 1) {
+                    const int r = __shfl_sync(0xffffffffu, rl, __ffs(m) - 1);
+                    const float* trow = tab + static_cast<int64_t>(r) * (H + W) * pw;
+                    float w = 0.f;
+                    if (lane < pw) w = __ldg(trow + y * pw + lane);
+                    else if (lane >= 16 && lane < 16 + pw) w = __ldg(trow + (H + x) * pw + (lane - 16));
+                    const unsigned nz = __ballot_sync(0xffffffffu, w != 0.f);
+                    const T* d = dy + static_cast<int64_t>(r) * Po * row_stride + c0;
+                    for (unsigned a = nz & 0xffffu; a; a &= a - 1) {
+                        const int ph = __ffs(a) - 1;
+                        const float wy = __shfl_sync(0xffffffffu, w, ph);
+                        for (unsigned b2 = nz >> 16; b2; b2 &= b2 - 1) {
+                            const int pwi = __ffs(b2) - 1;
+                            const float wx = __shfl_sync(0xffffffffu, w, 16 + pwi);
+                            const float wgt = wy * wx * inv_count;
+                            const float2 w2 = make_float2(wgt, wgt);
+                            const T* dd = d + ph * row_stride + static_cast<int64_t>(pwi) * C;
+#pragma unroll
+                            for (int v = 0; v < V; ++v) {
+                                if (c0 + v * 256 >= C) break;
+                                float2 val[4];
+                                ld8x2<T>(dd + v * 256, val);
+#pragma unroll
+                                for (int k = 0; k < 4; ++k) acc[v][k] = ffma2(w2, val[k], acc[v][k]);
+                            }
+                        }
                     }
                 }
             }
         }
-    }
+        if (ns == 1) {
+            if (pix) {
 #pragma unroll
-    for (int v = 0; v < V; ++v)
-        if (c0 + v * 256 < C) st8x2<T>(dfeat + ((static_cast<int64_t>(n) * H + y) * W + x) * C + c0 + v * 256, acc[v]);
+                for (int v = 0; v < V; ++v)
+                    if (c0 + v * 256 < C)
+                        st8x2<T>(dfeat + ((static_cast<int64_t>(n) * H + y) * W + x) * C + c0 + v * 256, acc[v]);
+            }
+            continue;
+        }
+        // split block: this segment's partial; the last segment sums them in order
+        const int64_t pstride = static_cast<int64_t>(kRaBlk * kRaBlk) * 256 * V;
+        float* pp = part + (static_cast<int64_t>(sl + sg) * nch + chunk) * pstride + warp * 256 * V;
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            float4* o = reinterpret_cast<float4*>(pp + v * 256 + lane * 8);
+            o[0] = make_float4(acc[v][0].x, acc[v][0].y, acc[v][1].x, acc[v][1].y);
+            o[1] = make_float4(acc[v][2].x, acc[v][2].y, acc[v][3].x, acc[v][3].y);
+        }
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) s_last = atomicAdd(&ticket[t * nch + chunk], 1u) == static_cast<unsigned>(ns - 1);
+        __syncthreads();
+        if (!s_last) continue;
+        __threadfence();
+        if (threadIdx.x == 0) ticket[t * nch + chunk] = 0u;
+        if (pix) {
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                if (c0 + v * 256 >= C) continue;
+                float2 sum[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) sum[k] = make_float2(0.f, 0.f);
+                for (int s2 = 0; s2 < ns; ++s2) {
+                    const float4* q = reinterpret_cast<const float4*>(
+                        part + (static_cast<int64_t>(sl + s2) * nch + chunk) * pstride + warp * 256 * V + v * 256 + lane * 8);
+                    const float4 a0 = __ldcg(q), a1 = __ldcg(q + 1);
+                    sum[0].x += a0.x; sum[0].y += a0.y; sum[1].x += a0.z; sum[1].y += a0.w;
+                    sum[2].x += a1.x; sum[2].y += a1.y; sum[3].x += a1.z; sum[3].y += a1.w;
+                }
+                st8x2<T>(dfeat + ((static_cast<int64_t>(n) * H + y) * W + x) * C + c0 + v * 256, sum);
+            }
+        }
+    }
 }
 
 // ---------------------------------------------------------------- RoIAlign fwd (warp per bin row)
@@ -1084,40 +1336,92 @@ cudaError_t roialign_fwd(int dtype, const void* feat, int N, int H, int W, int C
 
 static int ra_table_width(int P, int step) { return (P + step - 1) / step <= 8 ? 8 : 16; }
 
-size_t roialign_bwd_workspace(int R, int H, int W, int P, int step, int) {
-    if (step < 1) return 0;
-    return (static_cast<size_t>(R) * (H + W) * ra_table_width(P, step) * 4 + 255) / 256 * 256 +
-           static_cast<size_t>(R) * 16 + 256;
+// backward workspace: weight table, boxes, nonzero-bin counts, then the block
+// plan (lists, segment starts, segment table, partial slots, tickets, partials)
+struct RaBwdWs {
+    float* tab;
+    int4* box;
+    uint8_t* nzc;
+    int *tl_cnt, *tl_nseg, *seg_start, *tl, *seg, *nseg_total, *slot;
+    unsigned* ticket;
+    float* part;
+    size_t bytes;
+};
+
+static RaBwdWs ra_bwd_ws(void* base, int R, int H, int W, int P, int step, int N, int C) {
+    auto al = [](size_t v) { return (v + 255) & ~size_t(255); };
+    const int pw = ra_table_width(P, step);
+    const size_t nt = static_cast<size_t>((H + kRaBlk - 1) / kRaBlk) * ((W + kRaBlk - 1) / kRaBlk) * std::max(N, 1);
+    const int V = C >= 2048 ? 4 : (C >= 512 ? 2 : 1);
+    const size_t nch = static_cast<size_t>((std::max(C, 1) + 256 * V - 1) / (256 * V));
+    RaBwdWs w{};
+    uint8_t* p = static_cast<uint8_t*>(base);
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        uint8_t* q = p ? p + off : nullptr;
+        off += al(bytes);
+        return q;
+    };
+    w.tab = reinterpret_cast<float*>(take(static_cast<size_t>(R) * (H + W) * pw * 4));
+    w.box = reinterpret_cast<int4*>(take(static_cast<size_t>(R) * 16));
+    w.nzc = take(static_cast<size_t>(R) * (H + W));
+    w.tl_cnt = reinterpret_cast<int*>(take(nt * 4));
+    w.tl_nseg = reinterpret_cast<int*>(take(nt * 4));
+    w.seg_start = reinterpret_cast<int*>(take(nt * (kRaSegMax + 1) * 4));
+    w.seg = reinterpret_cast<int*>(take(nt * kRaSegMax * 4));
+    w.nseg_total = reinterpret_cast<int*>(take(4));
+    w.slot = reinterpret_cast<int*>(take(nt * 4));
+    w.ticket = reinterpret_cast<unsigned*>(take(nt * nch * 4));
+    w.part = reinterpret_cast<float*>(take(static_cast<size_t>(kRaSlots) * nch * kRaBlk * kRaBlk * 256 * V * 4));
+    w.tl = reinterpret_cast<int*>(take(nt * static_cast<size_t>(std::max(R, 1)) * 4));
+    w.bytes = off + 256;
+    return w;
 }
 
-template <class T, int V>
-static void ra_gather(dim3 grid, const void* dy, int H, int W, int C, const int4* box, const float* tab, int R, int Po,
-                      int pw, float inv, void* dfeat, cudaStream_t st) {
-    roialign_bwd_gather_kernel<T, V><<<grid, kRaBlk * kRaBlk * 32, 0, st>>>(cp<T>(dy), H, W, C, box, tab, R, Po, pw,
-                                                                           inv, static_cast<T*>(dfeat));
+// C is not a parameter of the reference-shaped query: size for C <= 2048 (V = 4)
+size_t roialign_bwd_workspace(int R, int H, int W, int P, int step, int N) {
+    if (step < 1) return 0;
+    return ra_bwd_ws(nullptr, R, H, W, P, step, N, 2048).bytes;
 }
 
 cudaError_t roialign_bwd(int dtype, const void* dy, int N, int H, int W, int C, const float* rois, int R, int P,
                          float scale, int sr, void* dfeat, void* ws, size_t ws_bytes, cudaStream_t st, int step) {
     if (step < 1 || (P + step - 1) / step > 16) return cudaErrorInvalidValue;
-    if (ws_bytes < roialign_bwd_workspace(R, H, W, P, step)) return cudaErrorInvalidValue;
+    if (ws_bytes < roialign_bwd_workspace(R, H, W, P, step, N)) return cudaErrorInvalidValue;
     const int Po = (P + step - 1) / step, pw = ra_table_width(P, step);
-    float* tab = static_cast<float*>(ws);
-    int4* box = reinterpret_cast<int4*>(static_cast<uint8_t*>(ws) +
-                                        (static_cast<size_t>(R) * (H + W) * pw * 4 + 255) / 256 * 256);
+    const RaBwdWs w = ra_bwd_ws(ws, R, H, W, P, step, N, C);
     if (R > 0)
-        roialign_bwd_weights_kernel<<<(R + 7) / 8, 256, 0, st>>>(rois, R, H, W, P, scale, sr, step, pw, tab, box);
+        roialign_bwd_weights_kernel<<<(R + 7) / 8, 256, 0, st>>>(rois, R, H, W, P, scale, sr, step, pw, w.tab, w.box,
+                                                                 w.nzc);
+    const int ntiles = ((H + kRaBlk - 1) / kRaBlk) * ((W + kRaBlk - 1) / kRaBlk), nt = N * ntiles;
+    const size_t lsm = static_cast<size_t>(std::max(R, 1)) * 4;
+    static int lsm_set = 0;
+    if (lsm > 48 * 1024 && lsm > static_cast<size_t>(lsm_set)) {
+        cudaFuncSetAttribute(roialign_tile_list_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(lsm));
+        lsm_set = static_cast<int>(lsm);
+    }
+    // segment work target: kRaSegWork pairs at 7 x 7 pooled bins, scaled with the bin count
+    const long long seg_work = std::max<long long>(kRaSegWork, static_cast<long long>(kRaSegWork) * Po * Po / 49);
+    roialign_tile_list_kernel<<<dim3(ntiles, N), 256, lsm, st>>>(w.box, w.nzc, R, H, W, seg_work, w.tl_cnt,
+                                                                  w.tl_nseg, w.seg_start, w.tl);
     // channel slab per warp: 256*V channels (V 8-channel chunks per lane)
     const int V = C >= 2048 ? 4 : (C >= 512 ? 2 : 1);
-    const dim3 grid(((H + kRaBlk - 1) / kRaBlk) * ((W + kRaBlk - 1) / kRaBlk), (C + 256 * V - 1) / (256 * V), N);
+    const int nch = (C + 256 * V - 1) / (256 * V);
+    roialign_seg_plan_kernel<<<1, 1024, 0, st>>>(w.tl_nseg, nt, w.seg, w.nseg_total, w.slot, w.ticket, nt * nch);
+    const dim3 grid(static_cast<unsigned>(std::min(nt * 2, 4 * kNumSMs)), nch);
     const float inv = 1.0f / static_cast<float>(max(sr * sr, 1));
     const bool h = dtype == kF16;
-    if (V == 4) h ? ra_gather<__half, 4>(grid, dy, H, W, C, box, tab, R, Po, pw, inv, dfeat, st)
-                  : ra_gather<float, 4>(grid, dy, H, W, C, box, tab, R, Po, pw, inv, dfeat, st);
-    else if (V == 2) h ? ra_gather<__half, 2>(grid, dy, H, W, C, box, tab, R, Po, pw, inv, dfeat, st)
-                       : ra_gather<float, 2>(grid, dy, H, W, C, box, tab, R, Po, pw, inv, dfeat, st);
-    else h ? ra_gather<__half, 1>(grid, dy, H, W, C, box, tab, R, Po, pw, inv, dfeat, st)
-           : ra_gather<float, 1>(grid, dy, H, W, C, box, tab, R, Po, pw, inv, dfeat, st);
+    auto go = [&](auto kern, auto* dyp, auto* dxp) {
+        kern<<<grid, kRaBlk * kRaBlk * 32, 0, st>>>(dyp, H, W, C, w.box, w.tab, R, Po, pw, inv, dxp, w.tl_cnt,
+                                                   w.tl_nseg, w.seg_start, w.tl, w.seg, w.nseg_total, w.slot, w.ticket,
+                                                   w.part);
+    };
+    if (V == 4) h ? go(roialign_bwd_gather_kernel<__half, 4>, cp<__half>(dy), static_cast<__half*>(dfeat))
+                  : go(roialign_bwd_gather_kernel<float, 4>, cp<float>(dy), static_cast<float*>(dfeat));
+    else if (V == 2) h ? go(roialign_bwd_gather_kernel<__half, 2>, cp<__half>(dy), static_cast<__half*>(dfeat))
+                       : go(roialign_bwd_gather_kernel<float, 2>, cp<float>(dy), static_cast<float*>(dfeat));
+    else h ? go(roialign_bwd_gather_kernel<__half, 1>, cp<__half>(dy), static_cast<__half*>(dfeat))
+           : go(roialign_bwd_gather_kernel<float, 1>, cp<float>(dy), static_cast<float*>(dfeat));
     return cudaGetLastError();
 }
 
