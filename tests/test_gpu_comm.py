@@ -134,3 +134,17 @@ def test_sync_bn_needs_bn_mode():
     from paper_1903_05831_b200 import detector as D
     with pytest.raises(ParamError):
         D.Detector(D.preset("c2", img_h=128, img_w=128, extra={"sync_bn": 1}))
+
+
+def test_concurrent_shortcut_branch_is_bit_identical(monkeypatch):
+    """the downsampling blocks' shortcut (down conv + its InPlace-ABN) runs on a
+    second stream next to conv1-conv3 inside the captured step; the step must
+    not change a bit against the sequential schedule (SDB_NO_BRANCH)"""
+    from paper_1903_05831_b200 import detector as D
+    p = D.preset("c2", img_h=128, img_w=128)
+    t0, w0, v0 = _run(p, 3, False)
+    monkeypatch.setenv("SDB_NO_BRANCH", "1")
+    t1, w1, v1 = _run(p, 3, False)
+    assert [t[0] for t in t0] == [t[0] for t in t1]
+    assert np.array_equal(w0.view(np.uint32), w1.view(np.uint32))
+    assert np.array_equal(v0.view(np.uint32), v1.view(np.uint32))
