@@ -793,6 +793,54 @@ __global__ void maxpool_bwd_kernel(const T* __restrict__ dy, const uint8_t* __re
     }
 }
 
+// the ResNet stem pool (k 3, s 2, p 1): input row ih lies in window row ih/2
+// (tap 1) when even, in window rows (ih-1)/2 (tap 2) and (ih+1)/2 (tap 0) when
+// odd -- same for columns; one CTA row per input row, no division chains.
+// Same window order (oh, ow ascending) and fp32 sums as the generic kernel.
+template <class T>
+__global__ void __launch_bounds__(256) maxpool_bwd_k3s2_kernel(const T* __restrict__ dy, const uint8_t* __restrict__ am,
+                                                               int H, int W, int C8, int Ho, int Wo,
+                                                               T* __restrict__ dx) {
+    const int row = blockIdx.y;  // n * H + ih
+    const int n = row / H, ih = row - n * H;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int iw = t / C8, c8 = t - iw * C8;
+    if (iw >= W) return;
+    int ohs[2], rs[2], nh = 0, ows[2], qs[2], nw = 0;
+    if (ih & 1) {
+        ohs[0] = (ih - 1) >> 1; rs[0] = 2;
+        ohs[1] = (ih + 1) >> 1; rs[1] = 0;
+        nh = ohs[1] < Ho ? 2 : 1;
+    } else {
+        ohs[0] = ih >> 1; rs[0] = 1; nh = ohs[0] < Ho ? 1 : 0;
+    }
+    if (iw & 1) {
+        ows[0] = (iw - 1) >> 1; qs[0] = 2;
+        ows[1] = (iw + 1) >> 1; qs[1] = 0;
+        nw = ows[1] < Wo ? 2 : 1;
+    } else {
+        ows[0] = iw >> 1; qs[0] = 1; nw = ows[0] < Wo ? 1 : 0;
+    }
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+        if (a >= nh) break;
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+            if (b >= nw) break;
+            const int64_t oe = ((static_cast<int64_t>(n) * Ho + ohs[a]) * Wo + ows[b]) * C8 + c8;
+            const uint64_t pk = __ldg(reinterpret_cast<const uint64_t*>(am) + oe);
+            float g[8];
+            ld8<T>(dy + oe * 8, g);
+            const int tap = rs[a] * 3 + qs[b];
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (static_cast<int>((pk >> (8 * j)) & 0xff) == tap) acc[j] += g[j];
+        }
+    }
+    st8<T>(dx + ((static_cast<int64_t>(row) * W + iw) * C8 + c8) * 8, acc);
+}
+
 template <class T>
 __global__ void avgpool_fwd_kernel(const T* __restrict__ x, int N, int HW, int C, T* __restrict__ y) {
     const int C8 = C / 8;
@@ -1453,6 +1501,17 @@ cudaError_t maxpool_bwd(int dtype, const void* dy, const uint8_t* argmax, int N,
                         int p, void* dx, cudaStream_t st) {
     const int Ho = (H + 2 * p - k) / s + 1, Wo = (W + 2 * p - k) / s + 1;
     const int64_t total = static_cast<int64_t>(N) * H * W * (C / 8);
+    static const bool generic = std::getenv("SDB_MAXPOOL_GENERIC") != nullptr;  // A/B switch
+    if (k == 3 && s == 2 && p == 1 && static_cast<int64_t>(N) * H < 65536 && !generic) {
+        const dim3 grid((W * (C / 8) + 255) / 256, N * H);
+        if (dtype == kF16)
+            maxpool_bwd_k3s2_kernel<__half><<<grid, 256, 0, st>>>(cp<__half>(dy), argmax, H, W, C / 8, Ho, Wo,
+                                                                  static_cast<__half*>(dx));
+        else
+            maxpool_bwd_k3s2_kernel<float><<<grid, 256, 0, st>>>(cp<float>(dy), argmax, H, W, C / 8, Ho, Wo,
+                                                                 static_cast<float*>(dx));
+        return cudaGetLastError();
+    }
     if (dtype == kF16)
         launch_idx(total, [&](auto idx) {
             maxpool_bwd_kernel<__half, decltype(idx)><<<grid_for(total), 256, 0, st>>>(
