@@ -230,6 +230,11 @@ struct sdb_det {
     cudaStream_t bst = nullptr;
     cudaEvent_t ev_b_fork = nullptr, ev_b_join = nullptr;
     ConvStats cst2{};
+    // backward twin: the shortcut's norm backward + dgrad on bst (dz into dzb,
+    // whose wgrad on the side stream must finish before the next reuse: ev_dzb)
+    void* dzb = nullptr;
+    cudaEvent_t ev_b2_fork = nullptr, ev_dzb = nullptr;
+    bool dzb_busy = false;
     void* drpn_side = nullptr;
     cudaEvent_t dzr_ev[kDzRing] = {};
     bool dzr_busy[kDzRing] = {};
@@ -892,7 +897,29 @@ void block_bwd(Bwd& B, Block& b, const void* dS, void* dx, void* s1, void* s2, c
     const float neg = d->cfg.mode == 0 ? 0.0f : d->cfg.slope;
     // shortcut first (its params come last in the block's pack order)
     void* z;
-    if (b.has_down) {
+    const bool branch = b.has_down && d->bst && d->dzb && B.side && d->cfg.mode == 1;
+    if (branch) {
+        // on d->bst, next to the conv3..conv1 chain: the shortcut's IABN backward
+        // (statistics pass), its wgrad (side stream) and its dgrad into dx; the
+        // chain's final dgrad accumulates onto dx after the join
+        cudaStream_t bs = d->bst;
+        CK(cudaEventRecord(d->ev_b_fork, d->ctx->stream));
+        CK(cudaStreamWaitEvent(bs, d->ev_b_fork, 0));
+        if (d->dzb_busy) CK(cudaStreamWaitEvent(bs, d->ev_dzb, 0));
+        const int64_t rows = static_cast<int64_t>(b.zd.n) * b.zd.h * b.zd.w;
+        CK(iabn_backward(d->dt, dS, b.d.p, d->bnp(b.nd.pg), d->bnp(b.nd.pb), b.nd.mean, b.nd.invstd, d->dzb,
+                         d->bngp(b.nd.pg), d->bngp(b.nd.pb), rows, b.nd.C, b.nd.slope, d->ws2, bs));
+        CK(cudaEventRecord(d->ev_b2_fork, bs));
+        CK(cudaStreamWaitEvent(d->wst, d->ev_b2_fork, 0));
+        WgradJob job{};
+        CK(conv_wgrad_deferred(b.down.g, d->dt, b.in.p, d->dzb, d->gptr(b.down.p), d->wg_arena + d->wg_off.at(b.down.p),
+                               conv_wgrad_workspace(b.down.g, d->dt), d->wst, &job));
+        CK(cudaEventRecord(d->ev_dzb, d->wst));
+        d->dzb_busy = true;
+        job_issued(d, b.down.p, job, d->wst);
+        CK(conv_dgrad(b.down.g, d->dt, d->dzb, d->wdev_ptr(b.down.p), dx, 0, bs));
+        CK(cudaEventRecord(d->ev_b_join, bs));
+    } else if (b.has_down) {
         z = dz_buf(B, s1);
         norm_bwd(d, b.nd, b.zd, b.d, dS, z);
         conv_wgrad_to(B, b.down, b.in, z);
@@ -911,6 +938,7 @@ void block_bwd(Bwd& B, Block& b, const void* dS, void* dx, void* s1, void* s2, c
     conv_wgrad_to(B, b.c1, b.in, z);
     // residual fan-in in the dgrad epilogue: dx = conv1^T(dz1) + (down-path dx | identity dS),
     // then the previous block's activation mask
+    if (branch) CK(cudaStreamWaitEvent(d->ctx->stream, d->ev_b_join, 0));
     if (b.has_down) dgrad(d, b.c1, z, dx, 1, nullptr, in_mask, neg, in_bits);
     else dgrad(d, b.c1, z, dx, 1, dS, in_mask, neg, in_bits);
 }
@@ -1068,6 +1096,7 @@ void run_step(sdb_det* d) {
     Bwd B{d, 0, 0};
     B.side = d->side_wgrad && !d->prof.on;
     for (bool& bz : d->dzr_busy) bz = false;  // the previous step joined the side stream
+    d->dzb_busy = false;
     // fc layers (bbox then cls: reverse pack order)
     void* dpool = d->gbuf[2];
     conv_wgrad_to(B, d->fc_bbox, d->pooled, g1);
@@ -1477,6 +1506,16 @@ int sdb_det_create(sdb_ctx* ctx, const sdb_det_config* cfgp, sdb_det** out) {
             for (auto& bl : d->head)
                 if (bl.has_down) m2 = std::max(m2, norm_workspace_bytes(static_cast<int64_t>(bl.zd.n) * bl.zd.h * bl.zd.w, bl.zd.c));
             d->ws2 = d->alloc(std::max<size_t>(m2, 256));
+            int64_t zmax = 0;
+            for (auto& bl : d->backbone)
+                if (bl.has_down) zmax = std::max(zmax, bl.zd.numel());
+            for (auto& bl : d->head)
+                if (bl.has_down) zmax = std::max(zmax, bl.zd.numel());
+            if (std::getenv("SDB_NO_BRANCH_BWD") == nullptr) {
+                d->dzb = d->alloc(static_cast<size_t>(std::max<int64_t>(zmax, 1)) * d->es);
+                CK(cudaEventCreateWithFlags(&d->ev_b2_fork, cudaEventDisableTiming));
+                CK(cudaEventCreateWithFlags(&d->ev_dzb, cudaEventDisableTiming));
+            }
         }
         if (d->side_wgrad) {
             int lo = 0, hi = 0;
@@ -1584,6 +1623,8 @@ int sdb_det_destroy(sdb_det* d) {
     if (d->bst) {
         cudaEventDestroy(d->ev_b_fork);
         cudaEventDestroy(d->ev_b_join);
+        if (d->ev_b2_fork) cudaEventDestroy(d->ev_b2_fork);
+        if (d->ev_dzb) cudaEventDestroy(d->ev_dzb);
         cudaStreamDestroy(d->bst);
     }
     for (auto e : d->bucket_ev) cudaEventDestroy(e);
