@@ -1017,15 +1017,17 @@ SDB_DEV void tma_im2col_4d(uint32_t dst, const void* map, uint64_t* bar, int c, 
 }
 
 // BN = 256: 8 epilogue warps (two per TMEM lane quadrant, 128 columns each,
-// 32-column steps); BN <= 128: 4 warps, 16-column steps (two CTAs per SM).
-// EPI 1 (dgrad residual + bitmask epilogue, BN = 256): per epilogue warp two
-// output staging boxes and a two-slot addend ring (4 x 2 KB)
-template <int MODE, int BN, int ST, int EPI = 0>
+// 32-column steps) -- or EW = 16 (four per quadrant, 64 columns each) for the
+// fprops whose epilogue also reduces the norm statistics, which is then the
+// longer half of the tile pipeline; BN <= 128: 4 warps, 16-column steps (two
+// CTAs per SM).  EPI 1 (dgrad residual + bitmask epilogue, BN = 256): per
+// epilogue warp two output staging boxes and a two-slot addend ring (4 x 2 KB)
+template <int MODE, int BN, int ST, int EPI = 0, int EW = (BN == 256 ? 8 : 4)>
 struct TmaCfg {
     static constexpr int kABytes = kBM * kBK * 2;
     static constexpr int kBBytes = BN * kBK * 2;
     static constexpr int kStage = kABytes + kBBytes;
-    static constexpr int kEpiWarps = BN == 256 ? 8 : 4;
+    static constexpr int kEpiWarps = EW;
     static constexpr int kSC = BN == 256 ? 32 : 16;
     // EPI 1: 2 output boxes + 2 addend slots per warp; EPI 2: 1 output box + 2 y slots
     static constexpr int kStaging = EPI == 1 ? kEpiWarps * 4 * 32 * kSC * 2
@@ -1035,10 +1037,10 @@ struct TmaCfg {
     static constexpr int kPerSM = BN <= 128 ? 2 : 1;
 };
 
-template <int MODE, int BN, int ST, int EPI = 0>
-__global__ void __launch_bounds__(TmaCfg<MODE, BN, ST, EPI>::kThreads, (BN <= 128) ? 2 : 1)
+template <int MODE, int BN, int ST, int EPI = 0, int EW = (BN == 256 ? 8 : 4)>
+__global__ void __launch_bounds__(TmaCfg<MODE, BN, ST, EPI, EW>::kThreads, (BN <= 128) ? 2 : 1)
     conv_tma_kernel(ConvArgs a, int tiles_m, int tiles_n, int n_tiles, const __grid_constant__ TmaPair tm) {
-    using Cfg = TmaCfg<MODE, BN, ST, EPI>;
+    using Cfg = TmaCfg<MODE, BN, ST, EPI, EW>;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
@@ -1772,12 +1774,12 @@ static bool tma_ok(const ConvArgs& a, int mode) {
     return (a.C % 64) == 0;
 }
 
-template <int MODE, int BN, int ST, int EPI = 0>
+template <int MODE, int BN, int ST, int EPI = 0, int EW = (BN == 256 ? 8 : 4)>
 static cudaError_t launch_tma(ConvArgs a, int splits, cudaStream_t st, ConvStats* cst = nullptr) {
-    using Cfg = TmaCfg<MODE, BN, ST, EPI>;
+    using Cfg = TmaCfg<MODE, BN, ST, EPI, EW>;
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(conv_tma_kernel<MODE, BN, ST, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(conv_tma_kernel<MODE, BN, ST, EPI, EW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              Cfg::kSmem);
         configured = true;
     }
@@ -1888,7 +1890,7 @@ static cudaError_t launch_tma(ConvArgs a, int splits, cudaStream_t st, ConvStats
             cst->bn = BN;
         }
         if (!ok) return cudaErrorInvalidValue;
-        return launch_pdl(conv_tma_kernel<MODE, BN, ST, EPI>, dim3(grid), dim3(Cfg::kThreads), Cfg::kSmem, st, a,
+        return launch_pdl(conv_tma_kernel<MODE, BN, ST, EPI, EW>, dim3(grid), dim3(Cfg::kThreads), Cfg::kSmem, st, a,
                           tiles_m, tiles_n, n_tiles, tm);
     }
     if (!ok) return cudaErrorInvalidValue;
@@ -1906,7 +1908,7 @@ static cudaError_t launch_tma(ConvArgs a, int splits, cudaStream_t st, ConvStats
             cst->bn = BN;
         }
     }
-    return launch_pdl(conv_tma_kernel<MODE, BN, ST, EPI>, dim3(grid), dim3(Cfg::kThreads), Cfg::kSmem, st, a, tiles_m,
+    return launch_pdl(conv_tma_kernel<MODE, BN, ST, EPI, EW>, dim3(grid), dim3(Cfg::kThreads), Cfg::kSmem, st, a, tiles_m,
                       tiles_n, n_tiles, tm);
 }
 
@@ -1930,7 +1932,16 @@ static int tma_bn(const ConvArgs& a, int mode = WGRAD) {
 template <int MODE>
 static cudaError_t launch_tma_pick(const ConvArgs& a, int splits, cudaStream_t st, ConvStats* cst = nullptr) {
     switch (tma_bn(a, MODE)) {
-        case 256: return launch_tma<MODE, 256, 4>(a, splits, st, cst);
+        case 256: {
+            // fprop with fused norm statistics and a short reduction (<= 16 k-blocks):
+            // the epilogue is the longer half of the tile pipeline -> 16 epilogue warps
+            // (3 stages fit beside their staging; the res5 1x1 512 -> 2048 fprop with
+            // statistics 130 -> 121 us; at 32 k-blocks the 4th stage matters more)
+            static const bool ew16 = std::getenv("SDB_NO_EPI16") == nullptr;
+            if (MODE == FPROP && cst && ew16 && a.KG <= 16 * kBK)
+                return launch_tma<MODE, 256, 3, 0, 16>(a, splits, st, cst);
+            return launch_tma<MODE, 256, 4>(a, splits, st, cst);
+        }
         case 128: return launch_tma<MODE, 128, 3>(a, splits, st, cst);
         default: return launch_tma<MODE, 64, 4>(a, splits, st, cst);
     }
