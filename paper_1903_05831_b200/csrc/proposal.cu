@@ -408,10 +408,36 @@ __global__ void __launch_bounds__(kTopkPassT) topk_compact_kernel(TopkMC m, int 
     }
 }
 
+// decode candidate `key` (score key << 32 | anchor index) into sorted slot r
+// (orc_decode with unit weights)
+SDB_DEV void topk_decode_into(const TopkArgs& a, int img, unsigned long long key, int r) {
+    const int k = a.k;
+    const int ai = static_cast<int>(key & 0xffffffffu);
+    const int loc = ai / a.A, an = ai - loc * a.A;
+    const float* an4 = a.anchors + static_cast<int64_t>(ai) * 4;
+    const int64_t dbase = (static_cast<int64_t>(img) * a.n_loc + loc) * 4 * a.A_pad + 4 * an;
+    const float dx = load_val(a.deltas, a.dtype, dbase + 0), dy = load_val(a.deltas, a.dtype, dbase + 1);
+    const float dw = fminf(load_val(a.deltas, a.dtype, dbase + 2), a.clip_dw);
+    const float dh = fminf(load_val(a.deltas, a.dtype, dbase + 3), a.clip_dw);
+    const float aw = __fsub_rn(an4[2], an4[0]), ah = __fsub_rn(an4[3], an4[1]);
+    const float acx = __fadd_rn(an4[0], __fmul_rn(0.5f, aw)), acy = __fadd_rn(an4[1], __fmul_rn(0.5f, ah));
+    const float pcx = __fadd_rn(__fmul_rn(dx, aw), acx), pcy = __fadd_rn(__fmul_rn(dy, ah), acy);
+    const float pw = __fmul_rn(portable_expf(dw), aw), ph = __fmul_rn(portable_expf(dh), ah);
+    float* o = a.boxes + (static_cast<int64_t>(img) * k + r) * 4;
+    o[0] = fminf(fmaxf(__fsub_rn(pcx, __fmul_rn(0.5f, pw)), 0.0f), a.img_w);
+    o[1] = fminf(fmaxf(__fsub_rn(pcy, __fmul_rn(0.5f, ph)), 0.0f), a.img_h);
+    o[2] = fminf(fmaxf(__fadd_rn(pcx, __fmul_rn(0.5f, pw)), 0.0f), a.img_w);
+    o[3] = fminf(fmaxf(__fadd_rn(pcy, __fmul_rn(0.5f, ph)), 0.0f), a.img_h);
+    a.order[static_cast<int64_t>(img) * k + r] = ai;
+    a.scores[static_cast<int64_t>(img) * k + r] =
+        load_val(a.logits, a.dtype, (static_cast<int64_t>(img) * a.n_loc + loc) * a.A_pad + an);
+}
+
 constexpr int kRankKeys = 128;   // keys per CTA (4 per lane)
-__global__ void __launch_bounds__(256) topk_rank_decode_kernel(TopkMC m) {
+__global__ void __launch_bounds__(256) topk_rank_decode_kernel(TopkMC m, const int* __restrict__ only_if) {
     __shared__ int part[8][kRankKeys];
     const int img = blockIdx.y;
+    if (only_if && !only_if[img]) return;  // the bucket kernel ranked this image
     const TopkArgs& a = m.a;
     const int k = a.k;
     const unsigned long long* S = m.sel + static_cast<int64_t>(img) * k;
@@ -447,26 +473,131 @@ __global__ void __launch_bounds__(256) topk_rank_decode_kernel(TopkMC m) {
         int r = 0;
 #pragma unroll
         for (int w = 0; w < 8; ++w) r += part[w][u * 32 + lane];
-        // decode the candidate into slot r (orc_decode with unit weights)
-        const int ai = static_cast<int>(mine[u] & 0xffffffffu);
-        const int loc = ai / a.A, an = ai - loc * a.A;
-        const float* an4 = a.anchors + static_cast<int64_t>(ai) * 4;
-        const int64_t dbase = (static_cast<int64_t>(img) * a.n_loc + loc) * 4 * a.A_pad + 4 * an;
-        const float dx = load_val(a.deltas, a.dtype, dbase + 0), dy = load_val(a.deltas, a.dtype, dbase + 1);
-        const float dw = fminf(load_val(a.deltas, a.dtype, dbase + 2), a.clip_dw);
-        const float dh = fminf(load_val(a.deltas, a.dtype, dbase + 3), a.clip_dw);
-        const float aw = __fsub_rn(an4[2], an4[0]), ah = __fsub_rn(an4[3], an4[1]);
-        const float acx = __fadd_rn(an4[0], __fmul_rn(0.5f, aw)), acy = __fadd_rn(an4[1], __fmul_rn(0.5f, ah));
-        const float pcx = __fadd_rn(__fmul_rn(dx, aw), acx), pcy = __fadd_rn(__fmul_rn(dy, ah), acy);
-        const float pw = __fmul_rn(portable_expf(dw), aw), ph = __fmul_rn(portable_expf(dh), ah);
-        float* o = a.boxes + (static_cast<int64_t>(img) * k + r) * 4;
-        o[0] = fminf(fmaxf(__fsub_rn(pcx, __fmul_rn(0.5f, pw)), 0.0f), a.img_w);
-        o[1] = fminf(fmaxf(__fsub_rn(pcy, __fmul_rn(0.5f, ph)), 0.0f), a.img_h);
-        o[2] = fminf(fmaxf(__fadd_rn(pcx, __fmul_rn(0.5f, pw)), 0.0f), a.img_w);
-        o[3] = fminf(fmaxf(__fadd_rn(pcy, __fmul_rn(0.5f, ph)), 0.0f), a.img_h);
-        a.order[static_cast<int64_t>(img) * k + r] = ai;
-        a.scores[static_cast<int64_t>(img) * k + r] =
-            load_val(a.logits, a.dtype, (static_cast<int64_t>(img) * a.n_loc + loc) * a.A_pad + an);
+        topk_decode_into(a, img, mine[u], r);
+    }
+}
+
+// One CTA per image, the same total order (the unique 64-bit keys) as the
+// counting kernel above in O(k): keys are bucketed by the high bits of their
+// score key over the selected range (4096 buckets), the buckets laid out by an
+// exclusive scan, and each key's rank is its bucket's start plus the number of
+// smaller keys in its bucket.  Bit-identical output to topk_rank_decode_kernel.
+// Ties pile up in one bucket (fp16 scores of a trained RPN repeat often): when
+// a bucket holds more than kBucketMaxOcc keys the image is left to the
+// counting kernel (flag), which then runs for it and exits for the others.
+constexpr int kBucketMaxOcc = 48;
+constexpr int kBucketThreads = 1024;
+constexpr int kBuckets = 4096;
+constexpr int kBucketKeysMax = 16384;
+
+__global__ void __launch_bounds__(kBucketThreads) topk_bucket_rank_kernel(TopkMC m, int* __restrict__ fallback) {
+    extern __shared__ unsigned long long bk_keys[];  // [k] keys in bucket order
+    __shared__ unsigned int hist[kBuckets];
+    __shared__ unsigned int start[kBuckets];
+    __shared__ unsigned int wmin[32], wmax[32];
+    __shared__ unsigned int s_lo, s_shift;
+    const int img = blockIdx.x;
+    const TopkArgs& a = m.a;
+    const int k = a.k;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int KPT = kBucketKeysMax / kBucketThreads;
+    const unsigned long long* S = m.sel + static_cast<int64_t>(img) * k;
+    unsigned long long key[KPT];
+    unsigned int lo = 0xffffffffu, hi = 0u;
+#pragma unroll
+    for (int u = 0; u < KPT; ++u) {
+        const int i = u * kBucketThreads + tid;
+        key[u] = i < k ? S[i] : ~0ull;
+        if (i < k) {
+            const unsigned int h = static_cast<unsigned int>(key[u] >> 32);
+            lo = min(lo, h);
+            hi = max(hi, h);
+        }
+    }
+    for (int b = tid; b < kBuckets; b += kBucketThreads) hist[b] = 0u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if (lane == 0) {
+        wmin[warp] = lo;
+        wmax[warp] = hi;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        unsigned int l2 = 0xffffffffu, h2 = 0u;
+        for (int w = 0; w < kBucketThreads / 32; ++w) {
+            l2 = min(l2, wmin[w]);
+            h2 = max(h2, wmax[w]);
+        }
+        const unsigned int range = h2 >= l2 ? h2 - l2 : 0u;
+        int bits = 0;
+        while (bits < 32 && (range >> bits) >= static_cast<unsigned int>(kBuckets)) ++bits;
+        s_lo = l2;
+        s_shift = static_cast<unsigned int>(bits);
+    }
+    __syncthreads();
+    const unsigned int blo = s_lo, sh = s_shift;
+    int bkt[KPT];
+#pragma unroll
+    for (int u = 0; u < KPT; ++u) {
+        const int i = u * kBucketThreads + tid;
+        bkt[u] = i < k ? static_cast<int>((static_cast<unsigned int>(key[u] >> 32) - blo) >> sh) : -1;
+        if (bkt[u] >= 0) atomicAdd(&hist[bkt[u]], 1u);
+    }
+    __syncthreads();
+    // the largest bucket decides the path (uniform over the CTA)
+    unsigned int mx = 0;
+    for (int b = tid; b < kBuckets; b += kBucketThreads) mx = max(mx, hist[b]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) wmax[warp] = mx;
+    __syncthreads();
+    if (tid == 0) {
+        unsigned int m2 = 0;
+        for (int w = 0; w < kBucketThreads / 32; ++w) m2 = max(m2, wmax[w]);
+        s_shift = m2 > static_cast<unsigned int>(kBucketMaxOcc) ? 0xffffffffu : sh;
+        fallback[img] = m2 > static_cast<unsigned int>(kBucketMaxOcc);
+    }
+    __syncthreads();
+    if (s_shift == 0xffffffffu) return;  // the counting kernel takes this image
+    // exclusive scan of the 4096 counts: 4 per thread, then the 1024 thread sums
+    unsigned int c4[4], t4 = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        c4[j] = hist[tid * 4 + j];
+        t4 += c4[j];
+    }
+    unsigned int incl = t4;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) wmin[warp] = incl;
+    __syncthreads();
+    unsigned int off = 0;
+    for (int w = 0; w < warp; ++w) off += wmin[w];
+    unsigned int run = off + incl - t4;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        start[tid * 4 + j] = run;
+        run += c4[j];
+        hist[tid * 4 + j] = 0u;  // reused as the fill counters
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < KPT; ++u)
+        if (bkt[u] >= 0) bk_keys[start[bkt[u]] + atomicAdd(&hist[bkt[u]], 1u)] = key[u];
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < KPT; ++u) {
+        if (bkt[u] < 0) continue;
+        const unsigned int b0 = start[bkt[u]], n = hist[bkt[u]];
+        int r = static_cast<int>(b0);
+        for (unsigned int q = 0; q < n; ++q) r += bk_keys[b0 + q] < key[u];
+        topk_decode_into(a, img, key[u], r);
     }
 }
 
@@ -1240,7 +1371,19 @@ cudaError_t rpn_proposals(const ProposalArgs& p, void* ws, cudaStream_t st) {
     if (!select_all)
         for (int pass = 0; pass < 8; ++pass) topk_pass_kernel<<<dim3(kTopkG, p.n_img), kTopkPassT, 0, st>>>(m, pass);
     topk_compact_kernel<<<dim3(kTopkG, p.n_img), kTopkPassT, 0, st>>>(m, select_all ? 1 : 0);
-    topk_rank_decode_kernel<<<dim3((k + kRankKeys - 1) / kRankKeys, p.n_img), 256, 0, st>>>(m);
+    static const bool count_rank = std::getenv("SDB_TOPK_COUNT") != nullptr;  // A/B switch
+    if (k <= kBucketKeysMax && !count_rank) {
+        const int smem = k * 8;
+        static int configured = 0;
+        if (smem > configured) {
+            cudaFuncSetAttribute(topk_bucket_rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            configured = smem;
+        }
+        topk_bucket_rank_kernel<<<p.n_img, kBucketThreads, smem, st>>>(m, done);
+        topk_rank_decode_kernel<<<dim3((k + kRankKeys - 1) / kRankKeys, p.n_img), 256, 0, st>>>(m, done);
+    } else {
+        topk_rank_decode_kernel<<<dim3((k + kRankKeys - 1) / kRankKeys, p.n_img), 256, 0, st>>>(m, nullptr);
+    }
     if (p.topk_order_out) {
         cudaMemcpyAsync(p.topk_order_out, order, static_cast<size_t>(p.n_img) * k * 4, cudaMemcpyDeviceToDevice, st);
     }
