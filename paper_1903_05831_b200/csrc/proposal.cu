@@ -434,10 +434,9 @@ SDB_DEV void topk_decode_into(const TopkArgs& a, int img, unsigned long long key
 }
 
 constexpr int kRankKeys = 128;   // keys per CTA (4 per lane)
-__global__ void __launch_bounds__(256) topk_rank_decode_kernel(TopkMC m, const int* __restrict__ only_if) {
+__global__ void __launch_bounds__(256) topk_rank_decode_kernel(TopkMC m) {
     __shared__ int part[8][kRankKeys];
     const int img = blockIdx.y;
-    if (only_if && !only_if[img]) return;  // the bucket kernel ranked this image
     const TopkArgs& a = m.a;
     const int k = a.k;
     const unsigned long long* S = m.sel + static_cast<int64_t>(img) * k;
@@ -477,28 +476,33 @@ __global__ void __launch_bounds__(256) topk_rank_decode_kernel(TopkMC m, const i
     }
 }
 
-// One CTA per image, the same total order (the unique 64-bit keys) as the
-// counting kernel above in O(k): keys are bucketed by the high bits of their
-// score key over the selected range (4096 buckets), the buckets laid out by an
-// exclusive scan, and each key's rank is its bucket's start plus the number of
-// smaller keys in its bucket.  Bit-identical output to topk_rank_decode_kernel.
-// Ties pile up in one bucket (fp16 scores of a trained RPN repeat often): when
-// a bucket holds more than kBucketMaxOcc keys the image is left to the
-// counting kernel (flag), which then runs for it and exits for the others.
-constexpr int kBucketMaxOcc = 48;
+// The same total order (the unique 64-bit keys) as the counting kernel above,
+// in about O(k): topk_bucket_kernel (one CTA per image) buckets the selected
+// keys by the high bits of their score key over the selected range (4096
+// buckets) and lays them out bucket by bucket (exclusive scan) in global
+// scratch; topk_bucket_rank_kernel (one thread per key) ranks a key as its
+// bucket's start plus the number of smaller keys in its bucket.  Bucket sizes
+// follow the score distribution: the trained C4 RPN's fp16 scores tie in
+// groups of hundreds (still ~30x less work than counting against all k); only
+// if every score tied would it cost as much.  Bit-identical output.
 constexpr int kBucketThreads = 1024;
 constexpr int kBuckets = 4096;
 constexpr int kBucketKeysMax = 16384;
 
-__global__ void __launch_bounds__(kBucketThreads) topk_bucket_rank_kernel(TopkMC m, int* __restrict__ fallback) {
-    extern __shared__ unsigned long long bk_keys[];  // [k] keys in bucket order
+struct TopkBuckets {
+    unsigned long long* keys;  // [img][k] in bucket order
+    unsigned int* start;       // [img][kBuckets]
+    unsigned int* count;       // [img][kBuckets]
+    unsigned int* param;       // [img][2]: score-key base, shift
+};
+
+__global__ void __launch_bounds__(kBucketThreads) topk_bucket_kernel(TopkMC m, TopkBuckets tb) {
     __shared__ unsigned int hist[kBuckets];
-    __shared__ unsigned int start[kBuckets];
+    __shared__ unsigned int fill[kBuckets];
     __shared__ unsigned int wmin[32], wmax[32];
     __shared__ unsigned int s_lo, s_shift;
     const int img = blockIdx.x;
-    const TopkArgs& a = m.a;
-    const int k = a.k;
+    const int k = m.a.k;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int KPT = kBucketKeysMax / kBucketThreads;
     const unsigned long long* S = m.sel + static_cast<int64_t>(img) * k;
@@ -514,7 +518,7 @@ __global__ void __launch_bounds__(kBucketThreads) topk_bucket_rank_kernel(TopkMC
             hi = max(hi, h);
         }
     }
-    for (int b = tid; b < kBuckets; b += kBucketThreads) hist[b] = 0u;
+    for (int b = tid; b < kBuckets; b += kBucketThreads) hist[b] = fill[b] = 0u;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
@@ -536,6 +540,8 @@ __global__ void __launch_bounds__(kBucketThreads) topk_bucket_rank_kernel(TopkMC
         while (bits < 32 && (range >> bits) >= static_cast<unsigned int>(kBuckets)) ++bits;
         s_lo = l2;
         s_shift = static_cast<unsigned int>(bits);
+        tb.param[2 * img] = l2;
+        tb.param[2 * img + 1] = static_cast<unsigned int>(bits);
     }
     __syncthreads();
     const unsigned int blo = s_lo, sh = s_shift;
@@ -547,22 +553,7 @@ __global__ void __launch_bounds__(kBucketThreads) topk_bucket_rank_kernel(TopkMC
         if (bkt[u] >= 0) atomicAdd(&hist[bkt[u]], 1u);
     }
     __syncthreads();
-    // the largest bucket decides the path (uniform over the CTA)
-    unsigned int mx = 0;
-    for (int b = tid; b < kBuckets; b += kBucketThreads) mx = max(mx, hist[b]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if (lane == 0) wmax[warp] = mx;
-    __syncthreads();
-    if (tid == 0) {
-        unsigned int m2 = 0;
-        for (int w = 0; w < kBucketThreads / 32; ++w) m2 = max(m2, wmax[w]);
-        s_shift = m2 > static_cast<unsigned int>(kBucketMaxOcc) ? 0xffffffffu : sh;
-        fallback[img] = m2 > static_cast<unsigned int>(kBucketMaxOcc);
-    }
-    __syncthreads();
-    if (s_shift == 0xffffffffu) return;  // the counting kernel takes this image
-    // exclusive scan of the 4096 counts: 4 per thread, then the 1024 thread sums
+    // exclusive scan of the 4096 counts: 4 per thread, then the thread sums
     unsigned int c4[4], t4 = 0;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -580,25 +571,59 @@ __global__ void __launch_bounds__(kBucketThreads) topk_bucket_rank_kernel(TopkMC
     unsigned int off = 0;
     for (int w = 0; w < warp; ++w) off += wmin[w];
     unsigned int run = off + incl - t4;
+    unsigned int* gs = tb.start + static_cast<int64_t>(img) * kBuckets;
+    unsigned int* gc = tb.count + static_cast<int64_t>(img) * kBuckets;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-        start[tid * 4 + j] = run;
+        gs[tid * 4 + j] = run;
+        gc[tid * 4 + j] = c4[j];
+        hist[tid * 4 + j] = run;  // now the bucket starts
         run += c4[j];
-        hist[tid * 4 + j] = 0u;  // reused as the fill counters
     }
     __syncthreads();
+    unsigned long long* gk = tb.keys + static_cast<int64_t>(img) * k;
 #pragma unroll
     for (int u = 0; u < KPT; ++u)
-        if (bkt[u] >= 0) bk_keys[start[bkt[u]] + atomicAdd(&hist[bkt[u]], 1u)] = key[u];
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < KPT; ++u) {
-        if (bkt[u] < 0) continue;
-        const unsigned int b0 = start[bkt[u]], n = hist[bkt[u]];
-        int r = static_cast<int>(b0);
-        for (unsigned int q = 0; q < n; ++q) r += bk_keys[b0 + q] < key[u];
-        topk_decode_into(a, img, key[u], r);
+        if (bkt[u] >= 0) gk[hist[bkt[u]] + atomicAdd(&fill[bkt[u]], 1u)] = key[u];
+}
+
+// one thread per key in BUCKET order: a CTA's 256 keys share few buckets, so
+// the union of their buckets is staged in shared memory once and each thread's
+// scan of its bucket reads broadcast words
+__global__ void __launch_bounds__(256) topk_bucket_rank_kernel(TopkMC m, TopkBuckets tb) {
+    extern __shared__ unsigned long long sk[];
+    __shared__ unsigned int s_lo, s_hi;
+    const int img = blockIdx.y;
+    const int k = m.a.k;
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    const unsigned long long* gk = tb.keys + static_cast<int64_t>(img) * k;
+    const unsigned int blo = tb.param[2 * img], sh = tb.param[2 * img + 1];
+    unsigned long long key = ~0ull;
+    unsigned int b0 = 0xffffffffu, n = 0;
+    if (q < k) {
+        key = gk[q];
+        const int b = static_cast<int>((static_cast<unsigned int>(key >> 32) - blo) >> sh);
+        b0 = tb.start[static_cast<int64_t>(img) * kBuckets + b];
+        n = tb.count[static_cast<int64_t>(img) * kBuckets + b];
     }
+    if (threadIdx.x == 0) {
+        s_lo = 0xffffffffu;
+        s_hi = 0u;
+    }
+    __syncthreads();
+    if (q < k) {
+        atomicMin(&s_lo, b0);
+        atomicMax(&s_hi, b0 + n);
+    }
+    __syncthreads();
+    const unsigned int lo = s_lo, hi = s_hi;
+    for (unsigned int j = lo + threadIdx.x; j < hi; j += blockDim.x) sk[j - lo] = gk[j];
+    __syncthreads();
+    if (q >= k) return;
+    int r = static_cast<int>(b0);
+    const unsigned long long* mine = sk + (b0 - lo);
+    for (unsigned int j = 0; j < n; ++j) r += mine[j] < key;
+    topk_decode_into(m.a, img, key, r);
 }
 
 // ---------------------------------------------------------------- NMS
@@ -1372,17 +1397,31 @@ cudaError_t rpn_proposals(const ProposalArgs& p, void* ws, cudaStream_t st) {
         for (int pass = 0; pass < 8; ++pass) topk_pass_kernel<<<dim3(kTopkG, p.n_img), kTopkPassT, 0, st>>>(m, pass);
     topk_compact_kernel<<<dim3(kTopkG, p.n_img), kTopkPassT, 0, st>>>(m, select_all ? 1 : 0);
     static const bool count_rank = std::getenv("SDB_TOPK_COUNT") != nullptr;  // A/B switch
-    if (k <= kBucketKeysMax && !count_rank) {
+    const size_t mask_bytes = static_cast<size_t>(p.n_img) * k * nwords * 8;
+    const size_t bucket_bytes = ((static_cast<size_t>(p.n_img) * k * 8 + 255) & ~size_t(255)) +
+                                static_cast<size_t>(p.n_img) * kBuckets * 8 + static_cast<size_t>(p.n_img) * 8;
+    if (k <= kBucketKeysMax && !count_rank && bucket_bytes <= mask_bytes) {
+        // bucket scratch in the NMS mask region (written only after the ranking)
+        TopkBuckets tb{};
+        uint8_t* bw = reinterpret_cast<uint8_t*>(mask);
+        tb.keys = reinterpret_cast<unsigned long long*>(bw);
+        bw += (static_cast<size_t>(p.n_img) * k * 8 + 255) & ~size_t(255);
+        tb.start = reinterpret_cast<unsigned int*>(bw);
+        bw += static_cast<size_t>(p.n_img) * kBuckets * 4;
+        tb.count = reinterpret_cast<unsigned int*>(bw);
+        bw += static_cast<size_t>(p.n_img) * kBuckets * 4;
+        tb.param = reinterpret_cast<unsigned int*>(bw);
+        topk_bucket_kernel<<<p.n_img, kBucketThreads, 0, st>>>(m, tb);
+        // staging: the union of a CTA's buckets, at most all k keys
         const int smem = k * 8;
         static int configured = 0;
         if (smem > configured) {
             cudaFuncSetAttribute(topk_bucket_rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
             configured = smem;
         }
-        topk_bucket_rank_kernel<<<p.n_img, kBucketThreads, smem, st>>>(m, done);
-        topk_rank_decode_kernel<<<dim3((k + kRankKeys - 1) / kRankKeys, p.n_img), 256, 0, st>>>(m, done);
+        topk_bucket_rank_kernel<<<dim3((k + 255) / 256, p.n_img), 256, smem, st>>>(m, tb);
     } else {
-        topk_rank_decode_kernel<<<dim3((k + kRankKeys - 1) / kRankKeys, p.n_img), 256, 0, st>>>(m, nullptr);
+        topk_rank_decode_kernel<<<dim3((k + kRankKeys - 1) / kRankKeys, p.n_img), 256, 0, st>>>(m);
     }
     if (p.topk_order_out) {
         cudaMemcpyAsync(p.topk_order_out, order, static_cast<size_t>(p.n_img) * k * 4, cudaMemcpyDeviceToDevice, st);
