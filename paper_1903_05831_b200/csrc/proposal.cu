@@ -171,23 +171,63 @@ SDB_DEV uint64_t block_radix_select(int n, int k, KeyFn keyfn, int* hist /*256*/
             if (f && (key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255], 1);
         }
         __syncthreads();
-        // find the digit where the cumulative count reaches kk (single thread; 256 bins)
-        if (threadIdx.x == 0) {
-            int acc = 0, d = 0;
-            for (d = 0; d < 256; ++d) {
-                if (acc + hist[d] >= kk) break;
-                acc += hist[d];
+        // the digit where the cumulative count reaches kk: warp 0, 8 bins per lane
+        // and an inclusive shuffle scan (was a 256-step loop on one thread)
+        if (threadIdx.x < 32) {
+            const int lane = threadIdx.x;
+            int c[8], tot = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                c[j] = hist[lane * 8 + j];
+                tot += c[j];
             }
-            sh[0] = d;
-            sh[1] = acc;
+            int incl = tot;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const int excl = incl - tot;
+            // the lane whose range holds the kk-th element picks its digit
+            if (excl < kk && incl >= kk) {
+                int acc = excl, d = lane * 8;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    if (acc + c[j] >= kk) {
+                        d = lane * 8 + j;
+                        break;
+                    }
+                    acc += c[j];
+                }
+                sh[0] = d;
+                sh[1] = acc;
+                sh[2] = hist[d];
+            }
         }
         __syncthreads();
-        const int d = sh[0], acc = sh[1];
+        const int d = sh[0], acc = sh[1], in_bin = sh[2];
         __syncthreads();
         kk -= acc;
         below += acc;
         prefix |= static_cast<uint64_t>(d) << shift;
         mask |= 0xffull << shift;
+        if (in_bin == 1 && pass < 7) {
+            // the kk-th key is the only one left with this prefix: fetch it whole
+            for (int i = threadIdx.x; i < n; i += NT) {
+                bool f;
+                const uint64_t key = keyfn(i, f);
+                if (f && (key & mask) == prefix) {
+                    sh[3] = static_cast<int>(key & 0xffffffffu);
+                    sh[4] = static_cast<int>(key >> 32);
+                }
+            }
+            __syncthreads();
+            const uint64_t full = (static_cast<uint64_t>(static_cast<uint32_t>(sh[4])) << 32) |
+                                  static_cast<uint32_t>(sh[3]);
+            __syncthreads();
+            *n_lt_out = below;
+            return full;
+        }
     }
     *n_lt_out = below;
     return prefix;
