@@ -839,28 +839,47 @@ __global__ void __launch_bounds__(kScanThreads) nms_scan_kernel(const float* __r
 }
 
 // Pipelined keep scan.  The greedy decision for 64-box chunk c needs only
-// removed[c]; it reads the chunk's diagonal words diag[c] (its rows' word c)
-// and, for the kept rows, their word c+1 (sdiag[c]) -- both preloaded into
-// shared memory for every chunk, so the decision warp never waits on global
-// memory.  The kept rows' words >= c+2 are ORed into removed[] by two worker
-// groups (even / odd chunks) that run one to two chunks behind: the decision
-// for chunk c only needs the bulk OR of chunks <= c-2, so the L2 round trips
-// of the bulk OR overlap the following decisions instead of serialising them.
-// Same greedy order, same keep list as nms_scan_kernel (deterministic:
-// atomicOr is order-independent).
-constexpr int kScan2GW = 15;     // warps per worker group
-constexpr int kScan2Warps = 1 + 2 * kScan2GW;  // warp 0: decisions; then the even-chunk and odd-chunk groups
+// removed[c].  For every chunk of the band the words c .. c+G-1 of its 64
+// rows are preloaded into shared memory (pre[j][c], j < G), so the decision
+// warp never waits on global memory: it walks the chunk with pre[0] (the
+// diagonal word) and ORs pre[j] of the kept rows into removed[c+j].  The kept
+// rows' words >= c+G are ORed into removed[] by G worker groups (chunk c goes
+// to group c mod G) running behind the decisions: the decision for chunk c
+// only needs the bulk OR of chunks <= c-G, so G-1 decisions overlap each bulk
+// OR's L2 round trip.  Same greedy order, same keep list as nms_scan_kernel
+// (deterministic: OR is order-independent).
+// G = 3 measured best at the C4 step (one band: 2 groups 73 us, 3 -> 61,
+// 4 -> 65, 5 -> 74, 6 -> 105; beyond 3 the decision warp's extra words cost
+// more than the shorter wait)
+constexpr int kScan2G = 3;                    // worker groups = preloaded words per row
+constexpr int kScan2GW = 10;                  // warps per worker group
+constexpr int kScan2Warps = 1 + kScan2G * kScan2GW;  // warp 0: decisions
 constexpr int kScan2Threads = 32 * kScan2Warps;
 constexpr int kScan2MaxWords = 192;
+constexpr int kScan2BandChunks = 64;  // chunks one launch scans (the band width)
+constexpr int kScan2KeepCap = 4096;   // kept positions staged in shared memory per launch
 
-// Two-phase use (nchunks < nwords): the first launch scans the leading block
-// only (mask words < nchunks computed, c0 = 0); it sets done_out[img] = 1 and
-// writes the outputs when post_k boxes are kept inside the block, else
-// done_out[img] = 0 and kept_io[img] = the boxes kept so far (their positions
-// are in keep_pos).  The second launch (after the rest of the mask, nchunks =
-// nwords, c0 = the leading block's chunk count) resumes unless done_in[img]:
-// it rebuilds removed[] for words >= c0 from the kept rows and continues the
-// greedy scan at chunk c0.  The keep decisions of the leading block never
+// OR into a shared-memory 64-bit word as two native 32-bit atomics (a 64-bit
+// shared atomicOr compiles to a compare-and-swap spin loop, which contends badly)
+SDB_DEV void smem_or64(uint64_t* p, uint64_t v) {
+    unsigned int* h = reinterpret_cast<unsigned int*>(p);
+    const unsigned int lo = static_cast<unsigned int>(v), hi = static_cast<unsigned int>(v >> 32);
+    if (lo) atomicOr(h, lo);
+    if (hi) atomicOr(h + 1, hi);
+}
+
+SDB_DEV uint64_t warp_or64(uint64_t v) {
+    return static_cast<uint64_t>(__reduce_or_sync(0xffffffffu, static_cast<unsigned int>(v))) |
+           (static_cast<uint64_t>(__reduce_or_sync(0xffffffffu, static_cast<unsigned int>(v >> 32))) << 32);
+}
+
+// Banded use: launch b scans chunks [c0, nchunks) (at most kScan2BandChunks)
+// with the mask words < nchunks computed.  It sets done_out[img] = 1 and
+// writes the outputs when post_k boxes are kept, or when the band reaches the
+// last word; else done_out[img] = 0 and kept_io[img] = the boxes kept so far
+// (their positions are in keep_pos).  The next launch resumes unless
+// done_in[img]: it rebuilds removed[] for words >= c0 from the kept rows and
+// continues the greedy scan at chunk c0.  The keep decisions of a band never
 // depend on words beyond it, so the result equals the full scan.
 __global__ void __launch_bounds__(kScan2Threads) nms_scan2_kernel(const float* __restrict__ boxes,
                                                                   const uint64_t* __restrict__ mask,
@@ -871,40 +890,38 @@ __global__ void __launch_bounds__(kScan2Threads) nms_scan2_kernel(const float* _
                                                                   int32_t* __restrict__ count, int nchunks, int c0,
                                                                   int* __restrict__ done_out,
                                                                   int* __restrict__ kept_io,
-                                                                  const int* __restrict__ done_in) {
+                                                                  const int* __restrict__ done_in, int kcap) {
+    constexpr int G = kScan2G;
     extern __shared__ uint64_t sm2[];
     const int img = blockIdx.x;
-    if (done_in && done_in[img]) return;  // the leading-block scan already finished this image
-    uint64_t* diag = sm2;                              // [nchunks][64]
-    uint64_t* sdiag = diag + nchunks * 64;             // [nchunks][64]
-    uint64_t* removed = sdiag + nchunks * 64;          // [nchunks]
-    __shared__ int rows[2][64];
-    __shared__ int nrows[2];
-    __shared__ uint64_t rows_ready[2], or_done[2];
+    if (done_in && done_in[img]) return;  // an earlier band already finished this image
+    const int nb = nchunks - c0;                       // chunks in this band
+    uint64_t* pre = sm2;                               // [G][nb][64]: words c+j of chunk c's rows
+    uint64_t* removed = pre + G * nb * 64;             // [nchunks]
+    // positions kept by this launch, [kcap]: global stores ahead of the
+    // decision warp's mbarrier arrive would make every arrive wait for them
+    int* kbuf = reinterpret_cast<int*>(removed + nchunks);
+    __shared__ int rows[G][64];
+    __shared__ int nrows[G];
+    __shared__ uint64_t rows_ready[G], or_done[G];
     __shared__ int kept_total, complete;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint64_t* M = mask + static_cast<int64_t>(img) * k * nwords;
-    // preload: diagonal and super-diagonal words of every chunk >= c0
-    // (8 independent loads in flight per thread)
-    for (int e0 = c0 * 64 + tid; e0 < nchunks * 64; e0 += 4 * kScan2Threads) {
-        uint64_t dv[4], sv[4];
+    // preload (8 independent loads in flight per thread)
+    const int npre = G * nb * 64;
+    for (int e0 = tid; e0 < npre; e0 += 8 * kScan2Threads) {
+        uint64_t v[8];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 8; ++u) {
             const int e = e0 + u * kScan2Threads;
-            const int c = e >> 6, r = c * 64 + (e & 63);
-            dv[u] = sv[u] = 0;
-            if (e < nchunks * 64 && r < k) {
-                dv[u] = __ldg(M + static_cast<int64_t>(r) * nwords + c);
-                if (c + 1 < nchunks) sv[u] = __ldg(M + static_cast<int64_t>(r) * nwords + c + 1);
-            }
+            const int j = e / (nb * 64), rem = e - j * nb * 64;
+            const int c = c0 + (rem >> 6), r = c * 64 + (rem & 63);
+            v[u] = (e < npre && r < k && c + j < nchunks) ? __ldg(M + static_cast<int64_t>(r) * nwords + c + j) : 0ull;
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 8; ++u) {
             const int e = e0 + u * kScan2Threads;
-            if (e < nchunks * 64) {
-                diag[e] = dv[u];
-                sdiag[e] = sv[u];
-            }
+            if (e < npre) pre[e] = v[u];
         }
     }
     for (int w = tid; w < nchunks; w += kScan2Threads) removed[w] = 0;
@@ -912,7 +929,7 @@ __global__ void __launch_bounds__(kScan2Threads) nms_scan2_kernel(const float* _
     if (kc0 > 0) {
         // resume: every word >= c0 of the rows kept in chunks < c0
         __syncthreads();
-        const int nrem = nchunks - c0, total = kc0 * nrem;
+        const int total = kc0 * nb;
         const int32_t* kp = keep_pos + static_cast<int64_t>(img) * post_k;
         for (int e0 = tid; e0 < total; e0 += 8 * kScan2Threads) {
             uint64_t v[8];
@@ -923,19 +940,17 @@ __global__ void __launch_bounds__(kScan2Threads) nms_scan2_kernel(const float* _
                 v[u] = 0;
                 wi[u] = 0;
                 if (e < total) {
-                    const int r = e / nrem;
-                    wi[u] = c0 + (e - r * nrem);
+                    const int r = e / nb;
+                    wi[u] = c0 + (e - r * nb);
                     v[u] = __ldg(M + static_cast<int64_t>(kp[r]) * nwords + wi[u]);
                 }
             }
 #pragma unroll
-            for (int u = 0; u < 8; ++u)
-                if (v[u]) atomicOr(reinterpret_cast<unsigned long long*>(&removed[wi[u]]),
-                                   static_cast<unsigned long long>(v[u]));
+            for (int u = 0; u < 8; ++u) smem_or64(&removed[wi[u]], v[u]);
         }
     }
     if (tid == 0) {
-        for (int g = 0; g < 2; ++g) {
+        for (int g = 0; g < G; ++g) {
             mbar_init(&rows_ready[g], 1);
             mbar_init(&or_done[g], kScan2GW);
         }
@@ -943,45 +958,85 @@ __global__ void __launch_bounds__(kScan2Threads) nms_scan2_kernel(const float* _
     }
     __syncthreads();
     if (warp == 0) {
-        // ------------------------------------------------ decisions (lane 0)
-        if (lane == 0) {
-            int kc = kc0;
-            for (int c = c0; c < nchunks; ++c) {
-                const int rel = c - c0, g = rel & 1, it = rel >> 1;
-                // bulk OR of chunk c-2 (same worker group) must be in removed[]
-                if (rel >= 2) mbar_wait_spin(&or_done[g], (it - 1) & 1);
-                const int lim = min(64, k - c * 64);
-                const uint64_t valid = lim >= 64 ? ~0ull : ((1ull << lim) - 1ull);
-                uint64_t w = atomicOr(reinterpret_cast<unsigned long long*>(&removed[c]), 0ull);
-                uint64_t nxt = 0;
-                int nr = 0;
-                uint64_t cand = ~w & valid;
-                while (cand && kc < post_k) {
-                    const int b = __ffsll(static_cast<long long>(cand)) - 1;
-                    keep_pos[static_cast<int64_t>(img) * post_k + kc] = c * 64 + b;
-                    ++kc;
-                    rows[g][nr++] = c * 64 + b;
-                    w |= diag[c * 64 + b];
-                    nxt |= sdiag[c * 64 + b];
-                    cand = ~w & valid & ~((2ull << b) - 1ull);
-                }
-                if (c + 1 < nchunks && nxt) atomicOr(reinterpret_cast<unsigned long long*>(&removed[c + 1]), nxt);
-                const bool finished = kc >= post_k || c + 1 >= nchunks;
+        // ------------------------------------------------ decisions (whole warp)
+        // Lane l holds candidates l and l+32 of the chunk.  Only the potential
+        // suppressors P (candidates whose diagonal word hits another candidate)
+        // need the sequential greedy walk; every other candidate is kept iff no
+        // kept suppressor removed it, which is known once P has been walked
+        // (the mask holds j > i only, so a row never touches an earlier box).
+        int kc = kc0;
+        for (int c = c0; c < nchunks; ++c) {
+            const int rel = c - c0, g = rel % G, it = rel / G;
+            // bulk OR of chunk c-G (same worker group) must be in removed[]
+            if (rel >= G) mbar_wait_spin(&or_done[g], (it - 1) & 1);
+            const int lim = min(64, k - c * 64);
+            const uint64_t valid = lim >= 64 ? ~0ull : ((1ull << lim) - 1ull);
+            uint64_t w = 0;
+            if (lane == 0) w = *reinterpret_cast<volatile uint64_t*>(&removed[c]);
+            w = __shfl_sync(0xffffffffu, w, 0);
+            const uint64_t cand = ~w & valid;
+            const uint64_t* dg = pre + rel * 64;
+            const uint64_t d0 = dg[lane], d1 = dg[32 + lane];
+            const uint64_t P = static_cast<uint64_t>(__ballot_sync(0xffffffffu, ((cand >> lane) & 1) && (d0 & cand))) |
+                               (static_cast<uint64_t>(__ballot_sync(0xffffffffu,
+                                                                    ((cand >> (lane + 32)) & 1) && (d1 & cand)))
+                                << 32);
+            uint64_t q = P;
+            while (q) {  // warp-uniform
+                const int b = __ffsll(static_cast<long long>(q)) - 1;
+                w |= dg[b];
+                q = P & ~w & ~((2ull << b) - 1ull);
+            }
+            uint64_t kept = cand & ~w;
+            int nr = __popcll(kept);
+            if (kc + nr > post_k) {
+                // keep only the first post_k - kc (rows past the cut never touch earlier boxes)
+                for (int drop = kc + nr - post_k; drop > 0; --drop)
+                    kept &= ~(1ull << (63 - __clzll(static_cast<long long>(kept))));
+                nr = post_k - kc;
+            }
+            const bool k0 = (kept >> lane) & 1, k1 = (kept >> (lane + 32)) & 1;
+            auto put = [&](int r, int pos) {
+                const int j = kc - kc0 + r;
+                if (j < kcap) kbuf[j] = pos;
+                else keep_pos[static_cast<int64_t>(img) * post_k + kc + r] = pos;
+                rows[g][r] = pos;
+            };
+            if (k0) put(__popcll(kept & ((1ull << lane) - 1ull)), c * 64 + lane);
+            if (k1) put(__popcll(kept & ((1ull << (lane + 32)) - 1ull)), c * 64 + 32 + lane);
+            // words c+1 .. c+G-1 of the kept rows (warp OR, redux.sync)
+            uint64_t nx[G - 1];
+#pragma unroll
+            for (int j = 1; j < G; ++j) {
+                const uint64_t* pj = pre + (j * nb + rel) * 64;
+                nx[j - 1] = warp_or64((k0 ? pj[lane] : 0ull) | (k1 ? pj[32 + lane] : 0ull));
+            }
+            kc += nr;
+            const bool finished = kc >= post_k || c + 1 >= nchunks;
+            __threadfence_block();  // rows[g] of every lane before lane 0's arrive
+            __syncwarp();
+            if (lane == 0) {
+#pragma unroll
+                for (int j = 1; j < G; ++j)
+                    if (c + j < nchunks && nx[j - 1]) smem_or64(&removed[c + j], nx[j - 1]);
                 nrows[g] = finished ? -1 - nr : nr;  // negative: last chunk (workers stop after it)
                 mbar_arrive(&rows_ready[g]);
                 if (finished) {
-                    // release the other group, waiting for chunk c + 1, once it has
-                    // finished chunk c - 1
-                    const int g2 = g ^ 1, r2 = rel + 1;
-                    if (r2 >= 2) mbar_wait_spin(&or_done[g2], ((r2 >> 1) - 1) & 1);
-                    nrows[g2] = -1;
-                    mbar_arrive(&rows_ready[g2]);
-                    break;
+                    // release the other groups, each waiting for its next chunk
+                    // rel + j, once it has finished its previous one (rel + j - G)
+                    for (int j = 1; j < G; ++j) {
+                        const int r2 = rel + j, g2 = r2 % G;
+                        if (r2 >= G) mbar_wait_spin(&or_done[g2], ((r2 / G) - 1) & 1);
+                        nrows[g2] = -1;
+                        mbar_arrive(&rows_ready[g2]);
+                    }
                 }
             }
+            if (finished) break;
+        }
+        if (lane == 0) {
             kept_total = kc;
-            // a leading-block scan is conclusive when it kept post_k boxes or
-            // when the block holds every candidate
+            // conclusive when post_k boxes are kept or the band reaches the last word
             complete = kc >= post_k || nchunks == nwords;
             if (done_out) {
                 done_out[img] = complete;
@@ -990,35 +1045,38 @@ __global__ void __launch_bounds__(kScan2Threads) nms_scan2_kernel(const float* _
         }
     } else {
         // ------------------------------------------------ bulk OR workers
-        const int g = (warp - 1) / kScan2GW;     // 0: even chunks, 1: odd chunks
+        const int g = (warp - 1) / kScan2GW;     // chunks c0 + g, c0 + g + G, ...
         constexpr int GT = 32 * kScan2GW;        // threads per group
         const int wt = tid - 32 - g * GT;        // 0..GT-1 within the group
-        for (int c = c0 + g, it = 0;; c += 2, ++it) {
-            mbar_wait_spin(&rows_ready[g], it & 1);
+        for (int c = c0 + g, it = 0;; c += G, ++it) {
+            mbar_wait(&rows_ready[g], it & 1);  // sleeping wait: leaves issue slots to the decision warp
             int nr = nrows[g];
             const bool last = nr < 0;
             if (last) nr = -1 - nr;
-            const int w0 = c + 2, nrem = nchunks - w0;
+            const int w0 = c + G, nrem = nchunks - w0;
             if (nr > 0 && nrem > 0) {
-                const int total = nr * nrem;
-                for (int e0 = wt; e0 < total; e0 += 8 * GT) {
-                    uint64_t v[8];
-                    int wi[8];
+                // tpw threads per word (a row's words are read by consecutive
+                // threads), each ORs its share of the rows in registers: one
+                // shared-memory atomic per thread and word instead of per row
+                const int tpw = max(1, GT / nrem);
+                const int slots = GT / tpw;
+                const int ws = wt % slots, sub = wt / slots;
+                if (sub < tpw) {
+                    for (int wj = ws; wj < nrem; wj += slots) {
+                        const uint64_t* col = M + w0 + wj;
+                        uint64_t acc = 0;
+                        for (int r0 = sub; r0 < nr; r0 += 8 * tpw) {
+                            uint64_t v[8];
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const int e = e0 + u * GT;
-                        v[u] = 0;
-                        wi[u] = 0;
-                        if (e < total) {
-                            const int r = e / nrem;
-                            wi[u] = w0 + (e - r * nrem);
-                            v[u] = __ldg(M + static_cast<int64_t>(rows[g][r]) * nwords + wi[u]);
+                            for (int u = 0; u < 8; ++u) {
+                                const int r = r0 + u * tpw;
+                                v[u] = r < nr ? __ldg(col + static_cast<int64_t>(rows[g][r]) * nwords) : 0ull;
+                            }
+#pragma unroll
+                            for (int u = 0; u < 8; ++u) acc |= v[u];
                         }
+                        smem_or64(&removed[w0 + wj], acc);
                     }
-#pragma unroll
-                    for (int u = 0; u < 8; ++u)
-                        if (v[u]) atomicOr(reinterpret_cast<unsigned long long*>(&removed[wi[u]]),
-                                           static_cast<unsigned long long>(v[u]));
                 }
             }
             __syncwarp();
@@ -1027,8 +1085,11 @@ __global__ void __launch_bounds__(kScan2Threads) nms_scan2_kernel(const float* _
         }
     }
     __syncthreads();
-    if (!complete) return;  // the resume launch finishes this image
     const int nk = kept_total;
+    for (int j = tid; j < min(nk - kc0, kcap); j += kScan2Threads)
+        keep_pos[static_cast<int64_t>(img) * post_k + kc0 + j] = kbuf[j];
+    __syncthreads();
+    if (!complete) return;  // a later band finishes this image
     for (int j = tid; j < post_k; j += kScan2Threads) {
         float* o = rois + (static_cast<int64_t>(img) * post_k + j) * 4;
         if (j < nk) {
@@ -1388,7 +1449,7 @@ size_t proposal_workspace_bytes(int n_img, int n_anchors, int pre_k) {
 // 12000^2 / 2 pair mask is ~25x more than the greedy scan reads; while the C4
 // RPN trains, the depth of the 2000th kept box wanders between ~2000 and all
 // 12000 (tools/nms_depth.py), hence bands that resume rather than one lead
-constexpr int kNmsLeadWords = 64;  // band width: 4096 candidates
+constexpr int kNmsLeadWords = kScan2BandChunks;  // band width: 4096 candidates
 
 cudaError_t rpn_proposals(const ProposalArgs& p, void* ws, cudaStream_t st) {
     const int nA = p.n_loc * p.A;
@@ -1471,21 +1532,23 @@ cudaError_t rpn_proposals(const ProposalArgs& p, void* ws, cudaStream_t st) {
         const int g = std::max(1, std::min((tiles + 3) / 4, 4 * kNumSMs / std::max(1, p.n_img)));
         nms_mask2_kernel<<<dim3(g, p.n_img), 256, 0, st>>>(boxes, k, nwords, p.iou_thr, mask, w_lo, w_hi, dn);
     };
-    static const bool no_lead = std::getenv("SDB_NMS_FULL_MASK") != nullptr;
     if (nwords <= kScan2MaxWords) {
-        // leading block first; the rest of the mask and a second scan run only
-        // for images whose leading block did not fill post_k (device flag)
+        // leading band first; the next band's mask and scan run only for
+        // images whose earlier bands did not fill post_k (device flag)
         cudaFuncSetAttribute(nms_scan2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(static_cast<size_t>(nwords) * (2 * 64 + 1) * 8));
+                             static_cast<int>(static_cast<size_t>(kScan2G) * kScan2BandChunks * 64 * 8 +
+                                              kScan2MaxWords * 8 + kScan2KeepCap * 4));
         // bands [0, 64), [64, 128), [128, nwords) words: each band's mask is
         // computed, and its scan resumed, only for images not yet complete
         int lo = 0;
         for (int band = 0; lo < nwords; ++band) {
-            const int hi = no_lead ? nwords : std::min(nwords, (band + 1) * kNmsLeadWords);
+            const int hi = std::min(nwords, (band + 1) * kNmsLeadWords);
             mask_band(lo, hi, band ? done : nullptr);
-            nms_scan2_kernel<<<p.n_img, kScan2Threads, static_cast<size_t>(hi) * (2 * 64 + 1) * 8, st>>>(
+            const int kcap = std::min(std::min(p.post_k, (hi - lo) * 64), kScan2KeepCap);
+            const size_t smem = static_cast<size_t>(kScan2G) * (hi - lo) * 64 * 8 + static_cast<size_t>(hi) * 8 + kcap * 4;
+            nms_scan2_kernel<<<p.n_img, kScan2Threads, smem, st>>>(
                 boxes, mask, scores, k, nwords, p.post_k, p.rois, p.roi_scores, p.keep_pos, p.count, hi, lo,
-                hi < nwords ? done : nullptr, kept, band ? done : nullptr);
+                hi < nwords ? done : nullptr, kept, band ? done : nullptr, kcap);
             lo = hi;
         }
     } else {
