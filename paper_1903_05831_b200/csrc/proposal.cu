@@ -671,18 +671,29 @@ __global__ void __launch_bounds__(256) topk_bucket_rank_kernel(TopkMC m, TopkBuc
 // per 256-thread CTA, tiles strided over a grid of a few CTAs per SM (the
 // (nwords x nwords x img) grid of 64-thread blocks spent most of its time
 // launching and retiring blocks, half of which exited at once).
-// Column band [w_lo, w_hi) of the triangle (tiles rb <= cb, w_lo <= cb < w_hi,
-// column-block major): the first launch covers the leading band of the sorted
-// candidates; each later band is computed only if the scans so far did not
-// fill post_k (done[img] == 0 -- skipped otherwise).
+// Column band [w_lo, w_hi) of the triangle (rows rb <= cb, w_lo <= cb < w_hi):
+// the first launch covers the leading band of the sorted candidates; each
+// later band is computed only if the scans so far did not fill post_k
+// (done[img] == 0 -- skipped otherwise).  In a later band the rows of earlier
+// bands are needed only where the scan kept them (the resume ORs the kept
+// rows; a removed row is never read), so those tiles run over the kept list
+// (kept[img] positions in keep_pos, 64 per tile) instead of every row:
+// tiles [0, TA) = kept-row blocks x band columns, then the band's own
+// triangle (rows w_lo <= rb <= cb, column-block major).
 __global__ void __launch_bounds__(256) nms_mask2_kernel(const float* __restrict__ boxes, int k, int nwords, double thr,
                                                        uint64_t* __restrict__ mask, int w_lo, int w_hi,
-                                                       const int* __restrict__ done) {
+                                                       const int* __restrict__ done,
+                                                       const int32_t* __restrict__ keep_pos, int post_k,
+                                                       const int* __restrict__ kept) {
     __shared__ float4 cbox[4][64];
     const int img = blockIdx.y;
     if (done && done[img]) return;
     auto tri = [](int n) { return n * (n + 1) / 2; };
-    const int T = tri(w_hi) - tri(w_lo);
+    const int nb = w_hi - w_lo;
+    const int nkept = kept ? kept[img] : 0;
+    const int32_t* kp = keep_pos + static_cast<int64_t>(img) * post_k;
+    const int TA = kept ? ((nkept + 63) / 64) * nb : 0;
+    const int T = TA + (kept ? tri(nb) : tri(w_hi) - tri(w_lo));
     const int grp = threadIdx.x >> 6, t = threadIdx.x & 63;
     const float4* B = reinterpret_cast<const float4*>(boxes + static_cast<int64_t>(img) * k * 4);
     // fp32 screen: inter_f and uni_f are within ~2e-6 (relative) of the exact
@@ -695,22 +706,42 @@ __global__ void __launch_bounds__(256) nms_mask2_kernel(const float* __restrict_
     for (int pass = 0; pass < n_pass; ++pass) {
         const int tile = pass * tiles_per_pass + blockIdx.x * 4 + grp;
         const bool live = tile < T;
-        int rb = 0, cb = 0;
+        int rb = 0, cb = 0, i = k;
         if (live) {
-            // column block cb: tiles of columns [w_lo, cb) come first, tri(cb) - tri(w_lo) <= tile
-            int lo = w_lo, hi = w_hi - 1;
-            while (lo < hi) {
-                const int mid = (lo + hi + 1) >> 1;
-                if (tri(mid) - tri(w_lo) <= tile) lo = mid;
-                else hi = mid - 1;
+            if (tile < TA) {
+                // kept rows of earlier bands: block tile / nb of the kept list
+                const int kb = tile / nb;
+                cb = w_lo + (tile - kb * nb);
+                const int r = kb * 64 + t;
+                i = r < nkept ? kp[r] : k;
+            } else if (kept) {
+                // the band's own triangle: rows w_lo <= rb <= cb
+                const int tl = tile - TA;
+                int lo = 0, hi = nb - 1;
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (tri(mid) <= tl) lo = mid;
+                    else hi = mid - 1;
+                }
+                cb = w_lo + lo;
+                rb = w_lo + (tl - tri(lo));
+                i = rb * 64 + t;
+            } else {
+                // column block cb: tiles of columns [w_lo, cb) come first, tri(cb) - tri(w_lo) <= tile
+                int lo = w_lo, hi = w_hi - 1;
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (tri(mid) - tri(w_lo) <= tile) lo = mid;
+                    else hi = mid - 1;
+                }
+                cb = lo;
+                rb = tile - (tri(cb) - tri(w_lo));
+                i = rb * 64 + t;
             }
-            cb = lo;
-            rb = tile - (tri(cb) - tri(w_lo));
             const int jt = cb * 64 + t;
             if (jt < k) cbox[grp][t] = __ldg(B + jt);
         }
         asm volatile("bar.sync %0, 64;" ::"r"(grp + 1) : "memory");
-        const int i = rb * 64 + t;
         if (live && i < k) {
             const float4 bi = __ldg(B + i);
             const float ai = __fmul_rn(__fsub_rn(bi.z, bi.x), __fsub_rn(bi.w, bi.y));
@@ -1527,10 +1558,15 @@ cudaError_t rpn_proposals(const ProposalArgs& p, void* ws, cudaStream_t st) {
     if (p.topk_order_out) {
         cudaMemcpyAsync(p.topk_order_out, order, static_cast<size_t>(p.n_img) * k * 4, cudaMemcpyDeviceToDevice, st);
     }
-    auto mask_band = [&](int w_lo, int w_hi, const int* dn) {
-        const int tiles = w_hi * (w_hi + 1) / 2 - w_lo * (w_lo + 1) / 2;
+    // kept: boxes kept by the earlier bands (device counts, positions in
+    // keep_pos) -- a later band's mask needs only those of the earlier rows
+    auto mask_band = [&](int w_lo, int w_hi, const int* dn, const int* kept_rows) {
+        const int nb = w_hi - w_lo;
+        const int tiles = kept_rows ? ((p.post_k + 63) / 64) * nb + nb * (nb + 1) / 2
+                                    : w_hi * (w_hi + 1) / 2 - w_lo * (w_lo + 1) / 2;
         const int g = std::max(1, std::min((tiles + 3) / 4, 4 * kNumSMs / std::max(1, p.n_img)));
-        nms_mask2_kernel<<<dim3(g, p.n_img), 256, 0, st>>>(boxes, k, nwords, p.iou_thr, mask, w_lo, w_hi, dn);
+        nms_mask2_kernel<<<dim3(g, p.n_img), 256, 0, st>>>(boxes, k, nwords, p.iou_thr, mask, w_lo, w_hi, dn,
+                                                            p.keep_pos, p.post_k, kept_rows);
     };
     if (nwords <= kScan2MaxWords) {
         // leading band first; the next band's mask and scan run only for
@@ -1543,7 +1579,7 @@ cudaError_t rpn_proposals(const ProposalArgs& p, void* ws, cudaStream_t st) {
         int lo = 0;
         for (int band = 0; lo < nwords; ++band) {
             const int hi = std::min(nwords, (band + 1) * kNmsLeadWords);
-            mask_band(lo, hi, band ? done : nullptr);
+            mask_band(lo, hi, band ? done : nullptr, band ? kept : nullptr);
             const int kcap = std::min(std::min(p.post_k, (hi - lo) * 64), kScan2KeepCap);
             const size_t smem = static_cast<size_t>(kScan2G) * (hi - lo) * 64 * 8 + static_cast<size_t>(hi) * 8 + kcap * 4;
             nms_scan2_kernel<<<p.n_img, kScan2Threads, smem, st>>>(
@@ -1552,7 +1588,7 @@ cudaError_t rpn_proposals(const ProposalArgs& p, void* ws, cudaStream_t st) {
             lo = hi;
         }
     } else {
-        mask_band(0, nwords, nullptr);
+        mask_band(0, nwords, nullptr, nullptr);
         nms_scan_kernel<<<p.n_img, kScanThreads, static_cast<size_t>(nwords) * 8, st>>>(
             boxes, mask, scores, k, nwords, p.post_k, p.rois, p.roi_scores, p.keep_pos, p.count);
     }

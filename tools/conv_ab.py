@@ -11,6 +11,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1903_05831_b200 import simdet as sd  # noqa: E402
 
 SHAPES = [  # (N, H, W, C, K, R, stride)
+    (1024, 7, 7, 512, 2048, 1, 1),
+    (1024, 7, 7, 2048, 512, 1, 1),
+    (2, 200, 334, 64, 256, 1, 1),
     (2, 50, 84, 256, 256, 3, 1),
     (2, 100, 167, 128, 128, 3, 1),
     (2, 200, 334, 64, 64, 3, 1),
@@ -52,7 +55,8 @@ for (N, H, W, C, K, R, s) in SHAPES:
     dy = torch.randn_like(y)
     flop = 2.0 * y.numel() * C * R * R
     tf = timeit(lambda: sd.conv_fprop_nhwc(x, w, s, R // 2))
+    ts = timeit(lambda: sd.conv_fprop_stats_nhwc(x, w, s, R // 2, iabn=True))
     td = timeit(lambda: sd.conv_dgrad_nhwc(dy, w, x.shape, s, R // 2))
     tw = timeit(lambda: sd.conv_wgrad_nhwc(x, dy, w.shape, s, R // 2))
-    print(f"N{N} H{H} W{W} C{C} K{K} R{R}: fprop {tf:6.1f} us ({flop / tf / 1e6:5.0f} TF/s)  "
+    print(f"N{N} H{H} W{W} C{C} K{K} R{R}: fprop {tf:6.1f} us ({flop / tf / 1e6:5.0f} TF/s)  +stats {ts:6.1f}  "
           f"dgrad {td:6.1f} us ({flop / td / 1e6:5.0f})  wgrad {tw:6.1f} us ({flop / tw / 1e6:5.0f})")
