@@ -214,7 +214,6 @@ struct sdb_det {
     // only after the wgrad that read them has finished
     static constexpr int kDzRing = 6;
     bool side_wgrad = false;
-    bool pool_fuse = true;  // stem max-pool backward folded into the stem norm backward
     cudaStream_t wst = nullptr;
     cudaEvent_t wev_fork = nullptr, wev_join = nullptr;
     void* dzr[kDzRing] = {};
@@ -1179,22 +1178,10 @@ void run_step(sdb_det* d) {
         std::swap(cur, spare);
     }
     // maxpool, stem norm, stem wgrad (the image gradient is not needed)
+    { PScope ps(d, P_POOL, 0, d->es * (2.0 * d->stem_a.numel() + d->pool.numel()));
+    CK(maxpool_bwd(d->dt, cur, d->pool_arg, d->stem_a.n, d->stem_a.h, d->stem_a.w, d->stem_a.c, 3, 2, 1, spare, st)); }
     void* dstem = dz_buf(B, d->gbuf[0]);
-    if (cf.mode != 0 && !d->stem_n.agg && d->pool_fuse) {
-        // InPlace-ABN backward with the max-pool backward folded in (dy gathered
-        // from the pooled gradient; no dx of the pool written and re-read)
-        const Act& a = d->stem_a;
-        const int64_t rows = static_cast<int64_t>(a.n) * a.h * a.w;
-        PScope ps(d, P_NORM_B, 0, d->es * (2.0 * a.numel() + 1.5 * d->pool.numel()), 3);
-        CK(iabn_backward_pool(d->dt, cur, d->pool_arg, a.h, a.w, d->pool.h, d->pool.w, a.p, d->bnp(d->stem_n.pg),
-                              d->bnp(d->stem_n.pb), d->stem_n.invstd, dstem, d->bngp(d->stem_n.pg),
-                              d->bngp(d->stem_n.pb), rows, d->stem_n.C, d->stem_n.slope, d->ws, st));
-    } else {
-        { PScope ps(d, P_POOL, 0, d->es * (2.0 * d->stem_a.numel() + d->pool.numel()));
-        CK(maxpool_bwd(d->dt, cur, d->pool_arg, d->stem_a.n, d->stem_a.h, d->stem_a.w, d->stem_a.c, 3, 2, 1, spare,
-                       st)); }
-        norm_bwd(d, d->stem_n, d->stem_z, d->stem_a, spare, dstem);
-    }
+    norm_bwd(d, d->stem_n, d->stem_z, d->stem_a, spare, dstem);
     if (d->stem_gemm) {
         // dW' = X'^T dZ as a 1x1 wgrad; folded back to [64][7][7][8] once reduced
         ConvL c2 = d->stem2;
@@ -1505,7 +1492,6 @@ int sdb_det_create(sdb_ctx* ctx, const sdb_det_config* cfgp, sdb_det** out) {
             d->wg_arena = static_cast<uint8_t*>(d->alloc(off));
             d->side_wgrad = std::getenv("SDB_NO_SIDE_WGRAD") == nullptr;
         }
-        d->pool_fuse = std::getenv("SDB_NO_POOL_FUSE") == nullptr;  // A/B switch
         if (d->dt == kF16 && cf.mode == 1 && std::getenv("SDB_NO_BRANCH") == nullptr) {
             int lo = 0, hi = 0;
             CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));

@@ -71,61 +71,6 @@ SDB_DEV void store8<float>(float* p, const float (&v)[8]) {
 // KIND 0: (x, x^2)             forward statistics
 // KIND 1: (dz, dz*xhat) BN     xhat = (x-mean)*invstd (float), dz = relu mask ? dy : 0
 // KIND 2: (dz, dz*xhat) IABN   recompute from y
-// KIND 3: as KIND 2 with dy gathered from the 3x3/2 max-pool backward (PoolSrc)
-//
-// The max-pool backward folded into the next norm backward (the ResNet stem:
-// IABN -> max-pool 3x3/2 pad 1): dy of input pixel (n, ih, iw) is the sum, in
-// window order (oh, ow ascending), of the pooled gradients whose recorded tap
-// is this pixel -- the same fp32 sums, rounded to T, as maxpool_bwd_k3s2
-// stores, so the statistics and dx are those of the separate passes.
-struct PoolSrc {
-    const void* dy;       // pooled gradient [N][Ho][Wo][C]
-    const uint8_t* am;    // recorded taps, one byte per element
-    int H, W, Ho, Wo;
-};
-
-template <class T>
-SDB_DEV void pool_gather8(const PoolSrc& ps, int64_t row, int C, int c0, float (&d)[8]) {
-    const int C8 = C / 8, c8 = c0 / 8;
-    const int64_t nh = row / ps.W;
-    const int iw = static_cast<int>(row - nh * ps.W);
-    const int n = static_cast<int>(nh / ps.H), ih = static_cast<int>(nh - static_cast<int64_t>(n) * ps.H);
-    int ohs[2], rs[2], nho = 0, ows[2], qs[2], nwo = 0;
-    if (ih & 1) {
-        ohs[0] = (ih - 1) >> 1; rs[0] = 2;
-        ohs[1] = (ih + 1) >> 1; rs[1] = 0;
-        nho = ohs[1] < ps.Ho ? 2 : 1;
-    } else {
-        ohs[0] = ih >> 1; rs[0] = 1; nho = ohs[0] < ps.Ho ? 1 : 0;
-    }
-    if (iw & 1) {
-        ows[0] = (iw - 1) >> 1; qs[0] = 2;
-        ows[1] = (iw + 1) >> 1; qs[1] = 0;
-        nwo = ows[1] < ps.Wo ? 2 : 1;
-    } else {
-        ows[0] = iw >> 1; qs[0] = 1; nwo = ows[0] < ps.Wo ? 1 : 0;
-    }
-    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-#pragma unroll
-    for (int a = 0; a < 2; ++a) {
-        if (a >= nho) break;
-#pragma unroll
-        for (int b = 0; b < 2; ++b) {
-            if (b >= nwo) break;
-            const int64_t oe = ((static_cast<int64_t>(n) * ps.Ho + ohs[a]) * ps.Wo + ows[b]) * C8 + c8;
-            const uint64_t pk = __ldg(reinterpret_cast<const uint64_t*>(ps.am) + oe);
-            float g[8];
-            load8<T>(static_cast<const T*>(ps.dy) + oe * 8, g);
-            const int tap = rs[a] * 3 + qs[b];
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-                if (static_cast<int>((pk >> (8 * j)) & 0xff) == tap) acc[j] += g[j];
-        }
-    }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) d[j] = to_f<T>(from_f<T>(acc[j]));
-}
-
 struct StatArgs {
     const void* a;  // x (KIND 0/1) or y (KIND 2)
     const void* dy;
@@ -137,7 +82,6 @@ struct StatArgs {
     int64_t rows_per_block;
     double* partial;
     int keep_l2;  // operands small enough to stay in L2 for the apply pass
-    PoolSrc pool;  // KIND 3
 };
 
 // Bulk-copy pipeline: a producer lane streams contiguous row tiles (16 KB per
@@ -228,8 +172,8 @@ __global__ void __launch_bounds__(kStatThreads, 2) stats_kernel(StatArgs p) {
                 g[j] = p.gamma[c0 + j];
                 is[j] = p.invstd[c0 + j];
                 mu[j] = KIND == 1 ? p.mean[c0 + j] : 0.f;
-                b[j] = KIND >= 2 ? p.beta[c0 + j] : 0.f;
-                if (KIND >= 2) g[j] = 1.0f / g[j];  // xhat = (z - beta) * (1/gamma)
+                b[j] = KIND == 2 ? p.beta[c0 + j] : 0.f;
+                if (KIND == 2) g[j] = 1.0f / g[j];  // xhat = (z - beta) * (1/gamma)
             }
         }
         const float inv_slope = 1.0f / p.slope;
@@ -252,8 +196,7 @@ __global__ void __launch_bounds__(kStatThreads, 2) stats_kernel(StatArgs p) {
                 const int off = rr * C + c0;
                 float v[8], dd[8], ym[8];
                 load8<T>(ta + off, v);
-                if (KIND == 3) pool_gather8<T>(p.pool, r0 + rr, C, c0, dd);
-                else if (KIND != 0) load8<T>(td + off, dd);
+                if (KIND != 0) load8<T>(td + off, dd);
                 if (NIN == 3) load8<T>(tm + off, ym);
                 if (KIND == 0) {
 #pragma unroll
@@ -420,8 +363,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const double* __r
 }
 
 // ---------------------------------------------------------------- apply
-// KIND 0: BN fwd (+act relu when act==1), 1: IABN fwd, 2: BN bwd, 3: IABN bwd,
-// 5: IABN bwd with dy gathered from the max-pool backward (PoolSrc)
+// KIND 0: BN fwd (+act relu when act==1), 1: IABN fwd, 2: BN bwd, 3: IABN bwd
 struct ApplyArgs {
     const void* a;   // x or y
     const void* dy;
@@ -440,7 +382,6 @@ struct ApplyArgs {
     // optional sign bitmap of the stored out2 (bit j of byte [row][c/8] = out2 > 0),
     // what the dgrad epilogue of the next layer needs of it
     uint8_t* bits;
-    PoolSrc pool;  // KIND 5 (IABN bwd, dy gathered from the max-pool backward)
 };
 
 SDB_DEV void ldf8(const float* p, float (&v)[8]) {
@@ -489,7 +430,7 @@ __global__ void __launch_bounds__(kStatThreads, 2) apply_kernel(ApplyArgs p, int
     float g[8], b[8], mu[8], is[8], k1[8], k2[8];
     ldf8(p.gamma + c0, g);
     ldf8(p.invstd + c0, is);
-    if (KIND != 3 && KIND != 5) ldf8(p.mean + c0, mu);
+    if (KIND != 3) ldf8(p.mean + c0, mu);
     if (KIND != 2) ldf8(p.beta + c0, b);
     if (KIND >= 2) {
         ldf8(p.coef + c0, k1);
@@ -544,8 +485,7 @@ __global__ void __launch_bounds__(kStatThreads, 2) apply_kernel(ApplyArgs p, int
                 }
             } else {
                 float d[8];
-                if (KIND == 5) pool_gather8<T>(p.pool, r0 + rr, C, c0, d);
-                else load8<T>(td + off, d);
+                load8<T>(td + off, d);
                 if (KIND == 2) {
                     if (NIN == 3) {
                         float yv[8];
@@ -840,26 +780,6 @@ cudaError_t iabn_backward(int dtype, const void* dy, const void* y, const float*
     aa.a = y; aa.dy = dy; aa.out = dx; aa.gamma = gamma; aa.beta = beta; aa.invstd = invstd; aa.coef = coef;
     aa.slope = slope; aa.n8 = rows * C / 8; aa.C = C;
     return dtype == kF16 ? run_apply<__half, 3, 2>(aa, rows, pl, st) : run_apply<float, 3, 2>(aa, rows, pl, st);
-}
-
-cudaError_t iabn_backward_pool(int dtype, const void* dpool, const uint8_t* argmax, int H, int W, int Ho, int Wo,
-                               const void* y, const float* gamma, const float* beta, const float* invstd, void* dx,
-                               float* dgamma, float* dbeta, int64_t rows, int C, float slope, void* ws,
-                               cudaStream_t st) {
-    const Plan pl = plan_for(rows, C, dtype == kF16 ? 2 : 4);
-    double* partial = static_cast<double*>(ws);
-    float* coef = reinterpret_cast<float*>(partial + static_cast<int64_t>(pl.nblocks) * 2 * C);
-    const PoolSrc ps{dpool, argmax, H, W, Ho, Wo};
-    StatArgs sa{};
-    sa.a = y; sa.gamma = gamma; sa.beta = beta; sa.invstd = invstd; sa.slope = slope;
-    sa.rows = rows; sa.C = C; sa.partial = partial; sa.pool = ps;
-    cudaError_t e = dtype == kF16 ? run_stats<__half, 3, 1>(sa, pl, st) : run_stats<float, 3, 1>(sa, pl, st);
-    if (e != cudaSuccess) return e;
-    finalize(partial, pl, C, rows, 0.f, 3, nullptr, nullptr, dgamma, dbeta, coef, st);
-    ApplyArgs aa{};
-    aa.a = y; aa.out = dx; aa.gamma = gamma; aa.beta = beta; aa.invstd = invstd; aa.coef = coef;
-    aa.slope = slope; aa.n8 = rows * C / 8; aa.C = C; aa.pool = ps;
-    return dtype == kF16 ? run_apply<__half, 5, 1>(aa, rows, pl, st) : run_apply<float, 5, 1>(aa, rows, pl, st);
 }
 
 // ---------------------------------------------------------------- fused statistics

@@ -118,13 +118,6 @@ cudaError_t iabn_backward_conv_stats(int dtype, const void* dy, const void* y, c
 cudaError_t iabn_backward(int dtype, const void* dy, const void* y, const float* gamma, const float* beta,
                           const float* mean, const float* invstd, void* dx, float* dgamma, float* dbeta,
                           int64_t rows, int C, float slope, void* ws, cudaStream_t st);
-// iabn_backward of a layer followed by a 3x3/2 pad-1 max-pool, with the pool's
-// backward folded in: dy gathered from the pooled gradient and the recorded
-// taps (as maxpool_bwd stores it) inside the statistics and apply passes
-cudaError_t iabn_backward_pool(int dtype, const void* dpool, const uint8_t* argmax, int H, int W, int Ho, int Wo,
-                               const void* y, const float* gamma, const float* beta, const float* invstd, void* dx,
-                               float* dgamma, float* dbeta, int64_t rows, int C, float slope, void* ws,
-                               cudaStream_t st);
 
 // ---- optim.cu
 cudaError_t nonfinite_check(int gdtype, const void* g, int64_t n, int* flag, cudaStream_t st);

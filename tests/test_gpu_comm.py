@@ -149,17 +149,3 @@ def test_concurrent_shortcut_branch_is_bit_identical(monkeypatch):
     assert np.array_equal(w0.view(np.uint32), w1.view(np.uint32))
     assert np.array_equal(v0.view(np.uint32), v1.view(np.uint32))
 
-
-@pytest.mark.parametrize("preset,h,w", [("c2", 128, 192), ("c2", 130, 202), ("c5", 128, 192)])
-def test_pool_backward_fusion_is_bit_identical(monkeypatch, preset, h, w):
-    """the stem max-pool backward folded into the stem InPlace-ABN backward (dy
-    gathered inside the statistics and apply passes) must equal the separate
-    max-pool backward + norm backward bit for bit (SDB_NO_POOL_FUSE)"""
-    from paper_1903_05831_b200 import detector as D
-    p = D.preset(preset, img_h=h, img_w=w)
-    t0, w0, v0 = _run(p, 3, False)
-    monkeypatch.setenv("SDB_NO_POOL_FUSE", "1")
-    t1, w1, v1 = _run(p, 3, False)
-    assert [t[0] for t in t0] == [t[0] for t in t1]
-    assert np.array_equal(w0.view(np.uint32), w1.view(np.uint32))
-    assert np.array_equal(v0.view(np.uint32), v1.view(np.uint32))
