@@ -111,9 +111,11 @@ cudaError_t maxpool_bwd(int dtype, const void* dy, const uint8_t* argmax, int N,
                         int p, void* dx, cudaStream_t st);
 cudaError_t avgpool_fwd(int dtype, const void* x, int N, int HW, int C, void* y, cudaStream_t st);
 // act_y (optional): fuse the backward of the activation that produced the pooled
-// tensor (out = act_y > 0 ? g : neg * g on the rounded pooling gradient)
+// tensor (out = act_y > 0 ? g : neg * g on the rounded pooling gradient);
+// act_bits (optional, instead of act_y): its sign bitmap (bit j of byte
+// [pixel][c/8] = act_y > 0)
 cudaError_t avgpool_bwd(int dtype, const void* dy, int N, int HW, int C, void* dx, cudaStream_t st,
-                        const void* act_y = nullptr, float neg = 0.0f);
+                        const void* act_y = nullptr, float neg = 0.0f, const uint8_t* act_bits = nullptr);
 // out = act(a + b); act: 0 none, 1 relu, 2 leaky(slope)
 cudaError_t add_act(int dtype, const void* a, const void* b, void* out, int64_t n, int act, float slope,
                     cudaStream_t st);

@@ -214,6 +214,9 @@ struct sdb_det {
     // only after the wgrad that read them has finished
     static constexpr int kDzRing = 6;
     bool side_wgrad = false;
+    // the last RoI-head block's output is average-pooled inside its apply pass
+    // and never stored (only its sign bitmap); head_out is then not materialised
+    bool head_pool_fuse = false;
     cudaStream_t wst = nullptr;
     cudaEvent_t wev_fork = nullptr, wev_join = nullptr;
     void* dzr[kDzRing] = {};
@@ -703,6 +706,12 @@ void block_fwd(sdb_det* d, Block& b) {
             ps.label = "norm_apply_add rows " + std::to_string(rows) + " C " + std::to_string(b.n3.C);
             ps.bytes_ = 4.0 * d->es * b.out.numel();
         }
+        if (d->head_pool_fuse && &b == &d->head.back()) {
+            CK(bn_apply_add_act_pool(d->dt, b.z3.p, d->bnp(b.n3.pg), d->bnp(b.n3.pb), b.n3.mean, b.n3.invstd, b.b3.p,
+                                     sc->p, d->pooled.p, b.out.h * b.out.w, rows, b.n3.C, b.n3.slope, 2,
+                                     d->cfg.slope, d->ctx->stream, b.obits));
+            return;
+        }
         CK(bn_apply_add_act(d->dt, b.z3.p, d->bnp(b.n3.pg), d->bnp(b.n3.pb), b.n3.mean, b.n3.invstd, b.b3.p, sc->p,
                             b.out.p, rows, b.n3.C, b.n3.slope, 2, d->cfg.slope, d->ctx->stream, b.obits));
         return;
@@ -1066,8 +1075,10 @@ void run_step(sdb_det* d) {
     CK(roialign_fwd(d->dt, d->c4.p, d->c4.n, d->c4.h, d->c4.w, d->c4.c, d->rois, d->R, d->P, sscale,
                     cf.sampling_ratio, d->roi_feat.p, st, d->roi_step)); }
     for (auto& b : d->head) block_fwd(d, b);
-    { PScope ps(d, P_POOL, 0, static_cast<double>(d->es) * d->head_out.numel());
-    CK(avgpool_fwd(d->dt, d->head_out.p, d->R, d->head_out.h * d->head_out.w, d->feat_c, d->pooled.p, st)); }
+    if (!d->head_pool_fuse) {
+        PScope ps(d, P_POOL, 0, static_cast<double>(d->es) * d->head_out.numel());
+        CK(avgpool_fwd(d->dt, d->head_out.p, d->R, d->head_out.h * d->head_out.w, d->feat_c, d->pooled.p, st));
+    }
     conv_fwd(d, d->fc_cls, d->pooled, d->cls_logits);
     conv_fwd(d, d->fc_bbox, d->pooled, d->bbox_pred);
     // ---- losses (scale folded into backward)
@@ -1113,7 +1124,8 @@ void run_step(sdb_det* d) {
         // fused in; inner block boundaries are masked in the dgrad epilogues
         PScope ps(d, P_POOL, 0, static_cast<double>(d->es) * 2.0 * d->head_out.numel());
         CK(avgpool_bwd(d->dt, dpool, d->R, d->head_out.h * d->head_out.w, d->feat_c, dhead, st,
-                       d->head.empty() ? nullptr : d->head_out.p, neg));
+                       d->head.empty() || d->head_pool_fuse ? nullptr : d->head_out.p, neg,
+                       d->head_pool_fuse ? d->head.back().obits : nullptr));
     }
     for (int i = static_cast<int>(d->head.size()) - 1; i >= 0; --i) {
         const void* in_mask = i > 0 ? d->head[i - 1].out.p : nullptr;  // head[0].in = RoIAlign output (linear)
@@ -1403,6 +1415,9 @@ int sdb_det_create(sdb_ctx* ctx, const sdb_det_config* cfgp, sdb_det** out) {
             d->head_out = d->roi_feat;
         }
         d->pooled = d->act(d->R, 1, 1, d->feat_c);
+        d->head_pool_fuse = !d->head.empty() && d->dt == kF16 && cf.mode == 1 && d->head.back().n3.act == 2 &&
+                            d->head.back().obits != nullptr && d->feat_c == 2048 &&
+                            std::getenv("SDB_NO_HEAD_POOL_FUSE") == nullptr;
         setg(d->fc_cls, d->pooled);
         setg(d->fc_bbox, d->pooled);
         d->fc_cls.g.C = d->feat_c; d->fc_cls.g.K = d->ncls_pad; d->fc_cls.g.R = d->fc_cls.g.S = 1;
@@ -2100,7 +2115,11 @@ int sdb_det_export(sdb_det* d, int what, void* host, int64_t cap, int64_t* bytes
         case 16: src = d->wdev; n = d->n_w * d->es; break;
         case 17: src = d->w32; n = d->n_w * 4; break;
         case 18: src = d->roi_feat.p; n = d->roi_feat.numel() * d->es; break;
-        case 19: src = d->head_out.p; n = d->head_out.numel() * d->es; break;
+        case 19:
+            if (d->head_pool_fuse)
+                return det_fail(SDB_PARAM, "head_out is pooled inside the last head block and not stored "
+                                           "(build the detector with SDB_NO_HEAD_POOL_FUSE=1 to export it)");
+            src = d->head_out.p; n = d->head_out.numel() * d->es; break;
         case 20: src = d->pooled.p; n = d->pooled.numel() * d->es; break;
         case 21: src = d->cls_logits.p; n = d->cls_logits.numel() * d->es; break;
         case 22: src = d->bbox_pred.p; n = d->bbox_pred.numel() * d->es; break;

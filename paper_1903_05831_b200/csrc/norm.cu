@@ -363,7 +363,8 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const double* __r
 }
 
 // ---------------------------------------------------------------- apply
-// KIND 0: BN fwd (+act relu when act==1), 1: IABN fwd, 2: BN bwd, 3: IABN bwd
+// KIND 0: BN fwd (+act relu when act==1), 1: IABN fwd, 2: BN bwd, 3: IABN bwd,
+// 4: IABN fwd + residual add + act, 6: 4 + average pool (out2 not stored)
 struct ApplyArgs {
     const void* a;   // x or y
     const void* dy;
@@ -382,6 +383,12 @@ struct ApplyArgs {
     // optional sign bitmap of the stored out2 (bit j of byte [row][c/8] = out2 > 0),
     // what the dgrad epilogue of the next layer needs of it
     uint8_t* bits;
+    // KIND 6 (KIND 4 closing the RoI head, C/8 == kThreads): out2 is not
+    // stored; its rows are average-pooled per group of pool_hw rows into
+    // pooled [rows / pool_hw][C] (fp32 sums in row order, / pool_hw, rounded:
+    // avgpool_fwd's arithmetic) and only its sign bitmap is kept
+    void* pooled;
+    int pool_hw;
 };
 
 SDB_DEV void ldf8(const float* p, float (&v)[8]) {
@@ -444,6 +451,7 @@ __global__ void __launch_bounds__(kStatThreads, 2) apply_kernel(ApplyArgs p, int
     }
     const float inv_slope = 1.0f / p.slope;
     T* out = static_cast<T*>(p.out);
+    float pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // KIND 6: this thread's channels, rows in order
     for (int i = 0; i < ntiles; ++i) {
         const int st = i % ST;
         mbar_wait(&full[st], (i / ST) & 1);
@@ -456,7 +464,7 @@ __global__ void __launch_bounds__(kStatThreads, 2) apply_kernel(ApplyArgs p, int
             const int off = rr * C + c0;
             float v[8], o[8];
             load8<T>(ta + off, v);
-            if (KIND == 0 || KIND == 1 || KIND == 4) {
+            if (KIND == 0 || KIND == 1 || KIND == 4 || KIND == 6) {
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     // gamma*(x-mean)*invstd + beta, evaluated like the reference (no contraction)
@@ -464,7 +472,7 @@ __global__ void __launch_bounds__(kStatThreads, 2) apply_kernel(ApplyArgs p, int
                     if (KIND == 0) o[j] = (p.act && !(z > 0.f)) ? 0.f : z;
                     else o[j] = z > 0.f ? z : __fmul_rn(p.slope, z);
                 }
-                if (KIND == 4) {
+                if (KIND == 4 || KIND == 6) {
                     // residual node: s = round(round(y) + shortcut) (src/tensor.cpp:125), then
                     // relu / leaky, exactly as the separate add_act pass
                     float sc[8], o2[8];
@@ -475,7 +483,22 @@ __global__ void __launch_bounds__(kStatThreads, 2) apply_kernel(ApplyArgs p, int
                         const float sr = to_f<T>(from_f<T>(__fadd_rn(yr, sc[j])));
                         o2[j] = p.act2 == 0 ? sr : (sr > 0.f ? sr : (p.act2 == 1 ? 0.f : __fmul_rn(p.slope2, sr)));
                     }
-                    store8<T>(static_cast<T*>(p.out2) + (r0 + rr) * C + c0, o2);
+                    if (KIND == 4) {
+                        store8<T>(static_cast<T*>(p.out2) + (r0 + rr) * C + c0, o2);
+                    } else {
+                        // rpi == 1: this thread sees every row of its pooling groups in order
+                        const int64_t row = r0 + rr;
+                        const int64_t grp = row / p.pool_hw;
+                        const int ig = static_cast<int>(row - grp * p.pool_hw);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) pacc[j] = (ig == 0 ? 0.f : pacc[j]) + to_f<T>(from_f<T>(o2[j]));
+                        if (ig == p.pool_hw - 1) {
+                            float pm[8];
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) pm[j] = pacc[j] / static_cast<float>(p.pool_hw);
+                            store8<T>(static_cast<T*>(p.pooled) + grp * C + c0, pm);
+                        }
+                    }
                     if (p.bits) {
                         uint32_t bm = 0;
 #pragma unroll
@@ -739,6 +762,29 @@ cudaError_t bn_apply_add_act(int dtype, const void* x, const float* gamma, const
     aa.slope = slope; aa.act = 2; aa.n8 = rows * C / 8; aa.C = C;
     aa.out2 = out; aa.act2 = act2; aa.slope2 = slope2;
     return dtype == kF16 ? run_apply<__half, 4, 2>(aa, rows, pl, st) : run_apply<float, 4, 2>(aa, rows, pl, st);
+}
+
+cudaError_t bn_apply_add_act_pool(int dtype, const void* x, const float* gamma, const float* beta, const float* mean,
+                                  const float* invstd, void* y, const void* shortcut, void* pooled, int pool_hw,
+                                  int64_t rows, int C, float slope, int act2, float slope2, cudaStream_t st,
+                                  uint8_t* out_bits) {
+    const int eb = dtype == kF16 ? 2 : 4;
+    if (C / 8 != kThreads || pool_hw < 1 || rows % pool_hw != 0 || !out_bits) return cudaErrorInvalidValue;
+    // rows per CTA: whole pooling groups and whole tiles
+    const int64_t tr = kTileBytes / (static_cast<int64_t>(C) * eb);
+    int64_t a = tr, b = pool_hw;
+    while (b) { const int64_t t = a % b; a = b; b = t; }
+    const int64_t unit = tr / a * pool_hw;
+    const int64_t units = (rows + unit - 1) / unit;
+    Plan pl;
+    pl.rpb = ((units + kMaxBlocks - 1) / kMaxBlocks) * unit;
+    pl.nblocks = static_cast<int>((rows + pl.rpb - 1) / pl.rpb);
+    ApplyArgs aa{};
+    aa.bits = out_bits;
+    aa.a = x; aa.dy = shortcut; aa.out = y; aa.gamma = gamma; aa.beta = beta; aa.mean = mean; aa.invstd = invstd;
+    aa.slope = slope; aa.act = 2; aa.n8 = rows * C / 8; aa.C = C;
+    aa.act2 = act2; aa.slope2 = slope2; aa.pooled = pooled; aa.pool_hw = pool_hw;
+    return dtype == kF16 ? run_apply<__half, 6, 2>(aa, rows, pl, st) : run_apply<float, 6, 2>(aa, rows, pl, st);
 }
 
 cudaError_t bn_backward(int dtype, const void* dy, const void* x, const void* y_mask, const float* gamma,

@@ -866,7 +866,7 @@ __global__ void avgpool_fwd_kernel(const T* __restrict__ x, int N, int HW, int C
 // in, exactly as the separate act_bwd pass on the rounded pooling gradient
 template <class T, class I>
 __global__ void avgpool_bwd_kernel(const T* __restrict__ dy, int N, int HW, int C, float inv, T* __restrict__ dx,
-                                   const T* __restrict__ y, float neg) {
+                                   const T* __restrict__ y, float neg, const uint8_t* __restrict__ ybits) {
     const int C8 = C / 8;
     const I total = static_cast<I>(N) * HW * C8;
     for (I e = blockIdx.x * static_cast<I>(blockDim.x) + threadIdx.x; e < total;
@@ -877,7 +877,15 @@ __global__ void avgpool_bwd_kernel(const T* __restrict__ dy, int N, int HW, int 
         ld8<T>(dy + (static_cast<int64_t>(n) * C8 + c8) * 8, g);
 #pragma unroll
         for (int j = 0; j < 8; ++j) g[j] = g[j] * inv;
-        if (y) {
+        if (ybits) {
+            // the activation's sign bitmap (bit j = y > 0) in place of y itself
+            const unsigned int bm = ybits[e];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const float r = to_f<T>(from_f<T>(g[j]));
+                g[j] = ((bm >> j) & 1u) ? r : neg * r;
+            }
+        } else if (y) {
             float v[8];
             ld8<T>(y + static_cast<int64_t>(e) * 8, v);
 #pragma unroll
@@ -1535,18 +1543,18 @@ cudaError_t avgpool_fwd(int dtype, const void* x, int N, int HW, int C, void* y,
 }
 
 cudaError_t avgpool_bwd(int dtype, const void* dy, int N, int HW, int C, void* dx, cudaStream_t st, const void* act_y,
-                        float neg) {
+                        float neg, const uint8_t* act_bits) {
     const int64_t total = static_cast<int64_t>(N) * HW * (C / 8);
     const float inv = static_cast<float>(1.0 / static_cast<double>(HW));  // src/autograd.cpp:381-384
     if (dtype == kF16)
         launch_idx(total, [&](auto idx) {
             avgpool_bwd_kernel<__half, decltype(idx)><<<grid_for(total), 256, 0, st>>>(
-                cp<__half>(dy), N, HW, C, inv, static_cast<__half*>(dx), cp<__half>(act_y), neg);
+                cp<__half>(dy), N, HW, C, inv, static_cast<__half*>(dx), cp<__half>(act_y), neg, act_bits);
         });
     else
         launch_idx(total, [&](auto idx) {
             avgpool_bwd_kernel<float, decltype(idx)><<<grid_for(total), 256, 0, st>>>(
-                cp<float>(dy), N, HW, C, inv, static_cast<float*>(dx), cp<float>(act_y), neg);
+                cp<float>(dy), N, HW, C, inv, static_cast<float*>(dx), cp<float>(act_y), neg, act_bits);
         });
     return cudaGetLastError();
 }

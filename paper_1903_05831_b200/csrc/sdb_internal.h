@@ -82,6 +82,13 @@ cudaError_t bn_forward(int dtype, const void* x, const float* gamma, const float
 // recomputes from it)
 cudaError_t bn_forward_stats(int dtype, const void* x, float* mean, float* invstd, int64_t rows, int C, float eps,
                              int act, void* ws, cudaStream_t st);
+// bn_apply_add_act closing the RoI head (C == 2048 fp16 / the CTA width x 8):
+// the block output is average-pooled per pool_hw rows in the same pass and
+// only its sign bitmap is stored (avgpool_fwd's arithmetic, bit-identical)
+cudaError_t bn_apply_add_act_pool(int dtype, const void* x, const float* gamma, const float* beta, const float* mean,
+                                  const float* invstd, void* y, const void* shortcut, void* pooled, int pool_hw,
+                                  int64_t rows, int C, float slope, int act2, float slope2, cudaStream_t st,
+                                  uint8_t* out_bits);
 cudaError_t bn_apply_add_act(int dtype, const void* x, const float* gamma, const float* beta, const float* mean,
                              const float* invstd, void* y, const void* shortcut, void* out, int64_t rows, int C,
                              float slope, int act2, float slope2, cudaStream_t st, uint8_t* out_bits = nullptr);

@@ -149,3 +149,19 @@ def test_concurrent_shortcut_branch_is_bit_identical(monkeypatch):
     assert np.array_equal(w0.view(np.uint32), w1.view(np.uint32))
     assert np.array_equal(v0.view(np.uint32), v1.view(np.uint32))
 
+
+
+@pytest.mark.parametrize("steps", [3])
+def test_head_pool_fusion_is_bit_identical(monkeypatch, steps):
+    """the last RoI-head block's apply pass average-pools the block output
+    itself (not stored; the backward masks with its sign bitmap): the step
+    must equal the separate avgpool_fwd / masked avgpool_bwd bit for bit
+    (SDB_NO_HEAD_POOL_FUSE)"""
+    from paper_1903_05831_b200 import detector as D
+    p = D.preset("c5", img_h=160, img_w=224)
+    t0, w0, v0 = _run(p, steps, False)
+    monkeypatch.setenv("SDB_NO_HEAD_POOL_FUSE", "1")
+    t1, w1, v1 = _run(p, steps, False)
+    assert [t[0] for t in t0] == [t[0] for t in t1]
+    assert np.array_equal(w0.view(np.uint32), w1.view(np.uint32))
+    assert np.array_equal(v0.view(np.uint32), v1.view(np.uint32))

@@ -1,6 +1,7 @@
 """Diagnostic (not a test): per-tensor gradient errors of one C4 step against
 the torch checker, with the fp32 noise floor (torch32 vs torch64) and, for the
 fp16 graph, the fp16 floor (torch16 vs torch32).  Prints a table."""
+import os
 import sys
 
 import numpy as np
@@ -14,6 +15,7 @@ from tests.util import norm_rel  # noqa: E402
 
 torch.backends.cuda.matmul.allow_tf32 = False
 torch.backends.cudnn.allow_tf32 = False
+os.environ["SDB_NO_HEAD_POOL_FUSE"] = "1"  # head_out is exported below (not stored when pooled in place)
 mode = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 at_step = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 det = D.Detector(D.preset("c4", mode=mode, scale_init=1.0 if mode != 1 else 128.0))
