@@ -217,6 +217,7 @@ struct sdb_det {
     // the last RoI-head block's output is average-pooled inside its apply pass
     // and never stored (only its sign bitmap); head_out is then not materialised
     bool head_pool_fuse = false;
+    const void* dpool_cur = nullptr;  // this step's pooled gradient (head_pool_fuse)
     cudaStream_t wst = nullptr;
     cudaEvent_t wev_fork = nullptr, wev_join = nullptr;
     void* dzr[kDzRing] = {};
@@ -935,7 +936,18 @@ void block_bwd(Bwd& B, Block& b, const void* dS, void* dx, void* s1, void* s2, c
         dgrad(d, b.down, z, dx, 0);
     }
     z = dz_buf(B, s1);
-    norm_bwd(d, b.n3, b.z3, b.b3, dS, z);
+    if (d->head_pool_fuse && &b == &d->head.back() && !b.has_down) {
+        // dS is the masked average-pool gradient: formed inside bn3's statistics
+        // pass from the pooled gradient and the sign bitmap (and stored there
+        // for the residual fan-in below), again inside the apply pass
+        const int64_t rows = static_cast<int64_t>(b.z3.n) * b.z3.h * b.z3.w;
+        PScope ps(d, P_NORM_B, 0, d->es * (4.0 * b.z3.numel()) + b.z3.numel() / 4.0, 3);
+        CK(iabn_backward_pooled(d->dt, d->dpool_cur, b.obits, b.z3.h * b.z3.w, neg, b.b3.p, d->bnp(b.n3.pg),
+                                d->bnp(b.n3.pb), b.n3.invstd, const_cast<void*>(dS), z, d->bngp(b.n3.pg),
+                                d->bngp(b.n3.pb), rows, b.n3.C, b.n3.slope, d->ws, d->ctx->stream));
+    } else {
+        norm_bwd(d, b.n3, b.z3, b.b3, dS, z);
+    }
     conv_wgrad_to(B, b.c3, b.a2, z);
     dgrad(d, b.c3, z, s2, 0, nullptr, nullptr, 0.0f, nullptr, bstats_for(d, b.n2, b.a2));
     z = dz_buf(B, s1);
@@ -1119,9 +1131,11 @@ void run_step(sdb_det* d) {
     void* cur = dhead;
     void* spare = d->gbuf[2];
     const float neg = cf.mode == 0 ? 0.0f : cf.slope;
-    {
+    d->dpool_cur = dpool;
+    if (!d->head_pool_fuse || d->head.back().has_down) {
         // avgpool backward with the last head block's output activation (its dS)
         // fused in; inner block boundaries are masked in the dgrad epilogues
+        // (with head_pool_fuse the last block's bn3 backward forms dS itself)
         PScope ps(d, P_POOL, 0, static_cast<double>(d->es) * 2.0 * d->head_out.numel());
         CK(avgpool_bwd(d->dt, dpool, d->R, d->head_out.h * d->head_out.w, d->feat_c, dhead, st,
                        d->head.empty() || d->head_pool_fuse ? nullptr : d->head_out.p, neg,

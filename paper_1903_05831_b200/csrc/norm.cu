@@ -82,7 +82,28 @@ struct StatArgs {
     int64_t rows_per_block;
     double* partial;
     int keep_l2;  // operands small enough to stay in L2 for the apply pass
+    // KIND 4: dy is the average-pool backward of pooled [rows / pool_hw][C],
+    // masked by the sign bitmap in the `dy` slot (C / 8 bytes per row):
+    // dy = rn(bit ? rn(g * inv) : neg * rn(g * inv)) exactly as avgpool_bwd
+    // stores it, which this pass also writes to dy_out
+    const void* pooled;
+    float pool_inv, pool_neg;
+    int pool_hw;
+    void* dy_out;
 };
+
+// the masked average-pool gradient of one row's 8 channels (avgpool_bwd's arithmetic)
+template <class T>
+SDB_DEV void pooled_dy8(const T* pooled, int64_t row, int pool_hw, int C, int c0, float inv, float neg,
+                        unsigned int bm, float (&d)[8]) {
+    float g[8];
+    load8<T>(pooled + (row / pool_hw) * C + c0, g);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const float r = to_f<T>(from_f<T>(g[j] * inv));
+        d[j] = to_f<T>(from_f<T>(((bm >> j) & 1u) ? r : neg * r));
+    }
+}
 
 // Bulk-copy pipeline: a producer lane streams contiguous row tiles (16 KB per
 // operand) into a ring of shared-memory stages with cp.async.bulk (completion
@@ -108,22 +129,29 @@ SDB_DEV int tile_rows_for(int C) {
 // producer lane: stream row tiles [r_begin, r_end) of up to three operands
 // into the stage ring
 // hint: 0 default, 1 evict_last (a second pass follows), 2 evict_first (last read)
+// rowb1 > 0: operand 1 has rowb1 bytes per row (a sign bitmap) instead of C x T
 template <class T, int NIN, int ST>
 SDB_DEV void stream_tiles(uint32_t sbase, uint64_t* full, uint64_t* empty, const void* a, const void* b,
-                          const void* c, int64_t r_begin, int64_t r_end, int ntiles, int TR, int C, int hint = 0) {
-    const T* src[3] = {static_cast<const T*>(a), static_cast<const T*>(b), static_cast<const T*>(c)};
+                          const void* c, int64_t r_begin, int64_t r_end, int ntiles, int TR, int C, int hint = 0,
+                          int rowb1 = 0) {
+    const uint8_t* src[3] = {static_cast<const uint8_t*>(a), static_cast<const uint8_t*>(b),
+                             static_cast<const uint8_t*>(c)};
+    const int64_t rb = static_cast<int64_t>(C) * sizeof(T);
     const uint64_t pol = hint == 1 ? l2_evict_last_policy() : (hint == 2 ? l2_evict_first_policy() : 0ull);
     for (int i = 0; i < ntiles; ++i) {
         const int s = i % ST;
         if (i >= ST) mbar_wait(&empty[s], ((i / ST) - 1) & 1);
         const int64_t r0 = r_begin + static_cast<int64_t>(i) * TR;
         const int nr = static_cast<int>(min(static_cast<int64_t>(TR), r_end - r0));
-        const uint32_t bytes = static_cast<uint32_t>(nr) * C * sizeof(T);
-        mbar_arrive_expect_tx(&full[s], bytes * NIN);
+        const uint32_t bytes = static_cast<uint32_t>(nr * rb);
+        const uint32_t bytes1 = rowb1 ? static_cast<uint32_t>(nr) * rowb1 : bytes;
+        mbar_arrive_expect_tx(&full[s], bytes * NIN + (NIN > 1 ? bytes1 - bytes : 0u));
 #pragma unroll
         for (int j = 0; j < NIN; ++j) {
-            if (hint) bulk_load_hint(sbase + (s * NIN + j) * kTileBytes, src[j] + r0 * C, bytes, &full[s], pol);
-            else bulk_load(sbase + (s * NIN + j) * kTileBytes, src[j] + r0 * C, bytes, &full[s]);
+            const int64_t rbj = (j == 1 && rowb1) ? rowb1 : rb;
+            const uint32_t by = j == 1 ? bytes1 : bytes;
+            if (hint) bulk_load_hint(sbase + (s * NIN + j) * kTileBytes, src[j] + r0 * rbj, by, &full[s], pol);
+            else bulk_load(sbase + (s * NIN + j) * kTileBytes, src[j] + r0 * rbj, by, &full[s]);
         }
     }
 }
@@ -162,7 +190,7 @@ __global__ void __launch_bounds__(kStatThreads, 2) stats_kernel(StatArgs p) {
         // ------------------------------------------------ producer
         if (lane == 0)
             stream_tiles<T, NIN, ST>(sbase, full, empty, p.a, p.dy, p.y, r_begin, r_end, ntiles, TR, C,
-                                     p.keep_l2 ? 1 : 0);
+                                     p.keep_l2 ? 1 : 0, KIND == 4 ? C / 8 : 0);
     } else {
         // ------------------------------------------------ consumers
         float g[8], b[8], mu[8], is[8];
@@ -172,8 +200,8 @@ __global__ void __launch_bounds__(kStatThreads, 2) stats_kernel(StatArgs p) {
                 g[j] = p.gamma[c0 + j];
                 is[j] = p.invstd[c0 + j];
                 mu[j] = KIND == 1 ? p.mean[c0 + j] : 0.f;
-                b[j] = KIND == 2 ? p.beta[c0 + j] : 0.f;
-                if (KIND == 2) g[j] = 1.0f / g[j];  // xhat = (z - beta) * (1/gamma)
+                b[j] = KIND >= 2 ? p.beta[c0 + j] : 0.f;
+                if (KIND >= 2) g[j] = 1.0f / g[j];  // xhat = (z - beta) * (1/gamma)
             }
         }
         const float inv_slope = 1.0f / p.slope;
@@ -196,7 +224,14 @@ __global__ void __launch_bounds__(kStatThreads, 2) stats_kernel(StatArgs p) {
                 const int off = rr * C + c0;
                 float v[8], dd[8], ym[8];
                 load8<T>(ta + off, v);
-                if (KIND != 0) load8<T>(td + off, dd);
+                if (KIND == 4) {
+                    const unsigned int bm = reinterpret_cast<const uint8_t*>(td)[rr * (C / 8) + cg];
+                    pooled_dy8<T>(static_cast<const T*>(p.pooled), r0 + rr, p.pool_hw, C, c0, p.pool_inv,
+                                  p.pool_neg, bm, dd);
+                    store8<T>(static_cast<T*>(p.dy_out) + (r0 + rr) * C + c0, dd);
+                } else if (KIND != 0) {
+                    load8<T>(td + off, dd);
+                }
                 if (NIN == 3) load8<T>(tm + off, ym);
                 if (KIND == 0) {
 #pragma unroll
@@ -389,6 +424,9 @@ struct ApplyArgs {
     // avgpool_fwd's arithmetic) and only its sign bitmap is kept
     void* pooled;
     int pool_hw;
+    // KIND 7 (IABN bwd, dy = the masked average-pool gradient as in KIND 4 of
+    // the statistics pass; the sign bitmap streams in the `dy` slot)
+    float pool_inv, pool_neg;
 };
 
 SDB_DEV void ldf8(const float* p, float (&v)[8]) {
@@ -427,7 +465,8 @@ __global__ void __launch_bounds__(kStatThreads, 2) apply_kernel(ApplyArgs p, int
     pdl_trigger();
     if (warp == kThreads / 32) {
         if (lane == 0)
-            stream_tiles<T, NIN, ST>(smem_u32(sm), full, empty, p.a, p.dy, p.y, r_begin, r_end, ntiles, TR, C, 2);
+            stream_tiles<T, NIN, ST>(smem_u32(sm), full, empty, p.a, p.dy, p.y, r_begin, r_end, ntiles, TR, C, 2,
+                                     KIND == 7 ? C / 8 : 0);
         return;
     }
     const int tpr = C / 8;
@@ -437,7 +476,7 @@ __global__ void __launch_bounds__(kStatThreads, 2) apply_kernel(ApplyArgs p, int
     float g[8], b[8], mu[8], is[8], k1[8], k2[8];
     ldf8(p.gamma + c0, g);
     ldf8(p.invstd + c0, is);
-    if (KIND != 3) ldf8(p.mean + c0, mu);
+    if (KIND != 3 && KIND != 7) ldf8(p.mean + c0, mu);
     if (KIND != 2) ldf8(p.beta + c0, b);
     if (KIND >= 2) {
         ldf8(p.coef + c0, k1);
@@ -508,7 +547,13 @@ __global__ void __launch_bounds__(kStatThreads, 2) apply_kernel(ApplyArgs p, int
                 }
             } else {
                 float d[8];
-                load8<T>(td + off, d);
+                if (KIND == 7) {
+                    const unsigned int bm = reinterpret_cast<const uint8_t*>(td)[rr * (C / 8) + cg];
+                    pooled_dy8<T>(static_cast<const T*>(p.pooled), r0 + rr, p.pool_hw, C, c0, p.pool_inv, p.pool_neg,
+                                  bm, d);
+                } else {
+                    load8<T>(td + off, d);
+                }
                 if (KIND == 2) {
                     if (NIN == 3) {
                         float yv[8];
@@ -785,6 +830,29 @@ cudaError_t bn_apply_add_act_pool(int dtype, const void* x, const float* gamma, 
     aa.slope = slope; aa.act = 2; aa.n8 = rows * C / 8; aa.C = C;
     aa.act2 = act2; aa.slope2 = slope2; aa.pooled = pooled; aa.pool_hw = pool_hw;
     return dtype == kF16 ? run_apply<__half, 6, 2>(aa, rows, pl, st) : run_apply<float, 6, 2>(aa, rows, pl, st);
+}
+
+cudaError_t iabn_backward_pooled(int dtype, const void* pooled, const uint8_t* bits, int pool_hw, float neg,
+                                 const void* y, const float* gamma, const float* beta, const float* invstd,
+                                 void* dy_out, void* dx, float* dgamma, float* dbeta, int64_t rows, int C, float slope,
+                                 void* ws, cudaStream_t st) {
+    if (C / 8 != kThreads || pool_hw < 1 || rows % pool_hw != 0) return cudaErrorInvalidValue;
+    const Plan pl = plan_for(rows, C, dtype == kF16 ? 2 : 4);
+    double* partial = static_cast<double*>(ws);
+    float* coef = reinterpret_cast<float*>(partial + static_cast<int64_t>(pl.nblocks) * 2 * C);
+    const float inv = static_cast<float>(1.0 / static_cast<double>(pool_hw));  // as avgpool_bwd
+    StatArgs sa{};
+    sa.a = y; sa.dy = bits; sa.gamma = gamma; sa.beta = beta; sa.invstd = invstd; sa.slope = slope;
+    sa.rows = rows; sa.C = C; sa.partial = partial;
+    sa.pooled = pooled; sa.pool_inv = inv; sa.pool_neg = neg; sa.pool_hw = pool_hw; sa.dy_out = dy_out;
+    cudaError_t e = dtype == kF16 ? run_stats<__half, 4, 2>(sa, pl, st) : run_stats<float, 4, 2>(sa, pl, st);
+    if (e != cudaSuccess) return e;
+    finalize(partial, pl, C, rows, 0.f, 3, nullptr, nullptr, dgamma, dbeta, coef, st);
+    ApplyArgs aa{};
+    aa.a = y; aa.dy = bits; aa.out = dx; aa.gamma = gamma; aa.beta = beta; aa.invstd = invstd; aa.coef = coef;
+    aa.slope = slope; aa.n8 = rows * C / 8; aa.C = C;
+    aa.pooled = const_cast<void*>(pooled); aa.pool_hw = pool_hw; aa.pool_inv = inv; aa.pool_neg = neg;
+    return dtype == kF16 ? run_apply<__half, 7, 2>(aa, rows, pl, st) : run_apply<float, 7, 2>(aa, rows, pl, st);
 }
 
 cudaError_t bn_backward(int dtype, const void* dy, const void* x, const void* y_mask, const float* gamma,

@@ -122,6 +122,15 @@ cudaError_t syncbn_backward_finish(int dtype, const void* dy, const void* x, con
 cudaError_t iabn_backward_conv_stats(int dtype, const void* dy, const void* y, const float* gamma, const float* beta,
                                      const float* invstd, void* dx, float* dgamma, float* dbeta, int64_t rows, int C,
                                      float slope, const ConvStats& cs, float* coef, cudaStream_t st);
+// iabn_backward of the layer whose dy is the masked average-pool backward
+// (the last RoI-head block's bn3 when its output was pooled in place): dy is
+// formed from the pooled gradient and the output's sign bitmap inside the
+// statistics pass (written once to dy_out for the residual consumer) and again
+// inside the apply pass, never read back as a tensor
+cudaError_t iabn_backward_pooled(int dtype, const void* pooled, const uint8_t* bits, int pool_hw, float neg,
+                                 const void* y, const float* gamma, const float* beta, const float* invstd,
+                                 void* dy_out, void* dx, float* dgamma, float* dbeta, int64_t rows, int C, float slope,
+                                 void* ws, cudaStream_t st);
 cudaError_t iabn_backward(int dtype, const void* dy, const void* y, const float* gamma, const float* beta,
                           const float* mean, const float* invstd, void* dx, float* dgamma, float* dbeta,
                           int64_t rows, int C, float slope, void* ws, cudaStream_t st);
