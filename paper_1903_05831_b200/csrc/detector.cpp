@@ -218,6 +218,7 @@ struct sdb_det {
     // and never stored (only its sign bitmap); head_out is then not materialised
     bool head_pool_fuse = false;
     const void* dpool_cur = nullptr;  // this step's pooled gradient (head_pool_fuse)
+    bool head_pool_bwd = false;       // the last block's bn3 backward forms the pool gradient itself
     cudaStream_t wst = nullptr;
     cudaEvent_t wev_fork = nullptr, wev_join = nullptr;
     void* dzr[kDzRing] = {};
@@ -936,7 +937,7 @@ void block_bwd(Bwd& B, Block& b, const void* dS, void* dx, void* s1, void* s2, c
         dgrad(d, b.down, z, dx, 0);
     }
     z = dz_buf(B, s1);
-    if (d->head_pool_fuse && &b == &d->head.back() && !b.has_down) {
+    if (d->head_pool_bwd && &b == &d->head.back()) {
         // dS is the masked average-pool gradient: formed inside bn3's statistics
         // pass from the pooled gradient and the sign bitmap (and stored there
         // for the residual fan-in below), again inside the apply pass
@@ -1132,7 +1133,7 @@ void run_step(sdb_det* d) {
     void* spare = d->gbuf[2];
     const float neg = cf.mode == 0 ? 0.0f : cf.slope;
     d->dpool_cur = dpool;
-    if (!d->head_pool_fuse || d->head.back().has_down) {
+    if (!d->head_pool_bwd) {
         // avgpool backward with the last head block's output activation (its dS)
         // fused in; inner block boundaries are masked in the dgrad epilogues
         // (with head_pool_fuse the last block's bn3 backward forms dS itself)
@@ -1432,6 +1433,8 @@ int sdb_det_create(sdb_ctx* ctx, const sdb_det_config* cfgp, sdb_det** out) {
         d->head_pool_fuse = !d->head.empty() && d->dt == kF16 && cf.mode == 1 && d->head.back().n3.act == 2 &&
                             d->head.back().obits != nullptr && d->feat_c == 2048 &&
                             std::getenv("SDB_NO_HEAD_POOL_FUSE") == nullptr;
+        d->head_pool_bwd = d->head_pool_fuse && !d->head.back().has_down &&
+                           std::getenv("SDB_NO_HEAD_POOL_BWD") == nullptr;
         setg(d->fc_cls, d->pooled);
         setg(d->fc_bbox, d->pooled);
         d->fc_cls.g.C = d->feat_c; d->fc_cls.g.K = d->ncls_pad; d->fc_cls.g.R = d->fc_cls.g.S = 1;

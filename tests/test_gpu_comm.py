@@ -159,6 +159,10 @@ def test_head_pool_fusion_is_bit_identical(monkeypatch, steps):
     (SDB_NO_HEAD_POOL_FUSE)"""
     from paper_1903_05831_b200 import detector as D
     p = D.preset("c5", img_h=160, img_w=224)
+    det = D.Detector(p)
+    with pytest.raises(Exception):  # the fused path is the one under test: head_out is not stored
+        det.export(19, np.float16)
+    det.close()
     t0, w0, v0 = _run(p, steps, False)
     monkeypatch.setenv("SDB_NO_HEAD_POOL_FUSE", "1")
     t1, w1, v1 = _run(p, steps, False)
