@@ -96,20 +96,37 @@ struct StatArgs {
 // the masked average-pool gradient of one row's 8 channels (avgpool_bwd's
 // arithmetic); the scaled pooled values are cached per pooling group (a
 // thread walks consecutive rows, 49 per RoI)
-struct PooledCache {
+// Row -> (group, index in group) without a 64-bit division per row: the
+// callers (C / 8 == threads, one thread per 8 channels) visit every row of
+// their range in order, so the position advances by one per call.
+struct GroupPos {
     int64_t grp = -1;
+    int ig = 0;
+    SDB_DEV void next(int64_t row, int hw) {
+        if (grp < 0) {
+            grp = row / hw;
+            ig = static_cast<int>(row - grp * hw);
+        } else if (++ig == hw) {
+            ig = 0;
+            ++grp;
+        }
+    }
+};
+struct PooledCache {
+    GroupPos pos;
+    int64_t loaded = -1;
     float r[8];
 };
 template <class T>
 SDB_DEV void pooled_dy8(const T* pooled, int64_t row, int pool_hw, int C, int c0, float inv, float neg,
                         unsigned int bm, PooledCache& pc, float (&d)[8]) {
-    const int64_t grp = row / pool_hw;
-    if (grp != pc.grp) {
+    pc.pos.next(row, pool_hw);
+    if (pc.pos.grp != pc.loaded) {
         float g[8];
-        load8<T>(pooled + grp * C + c0, g);
+        load8<T>(pooled + pc.pos.grp * C + c0, g);
 #pragma unroll
         for (int j = 0; j < 8; ++j) pc.r[j] = to_f<T>(from_f<T>(g[j] * inv));
-        pc.grp = grp;
+        pc.loaded = pc.pos.grp;
     }
 #pragma unroll
     for (int j = 0; j < 8; ++j) d[j] = to_f<T>(from_f<T>(((bm >> j) & 1u) ? pc.r[j] : neg * pc.r[j]));
@@ -503,6 +520,7 @@ __global__ void __launch_bounds__(kStatThreads, 2) apply_kernel(ApplyArgs p, int
     T* out = static_cast<T*>(p.out);
     float pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // KIND 6: this thread's channels, rows in order
     PooledCache pcache;                        // KIND 7
+    GroupPos ppos;                             // KIND 6
     for (int i = 0; i < ntiles; ++i) {
         const int st = i % ST;
         mbar_wait(&full[st], (i / ST) & 1);
@@ -538,9 +556,9 @@ __global__ void __launch_bounds__(kStatThreads, 2) apply_kernel(ApplyArgs p, int
                         store8<T>(static_cast<T*>(p.out2) + (r0 + rr) * C + c0, o2);
                     } else {
                         // rpi == 1: this thread sees every row of its pooling groups in order
-                        const int64_t row = r0 + rr;
-                        const int64_t grp = row / p.pool_hw;
-                        const int ig = static_cast<int>(row - grp * p.pool_hw);
+                        ppos.next(r0 + rr, p.pool_hw);
+                        const int64_t grp = ppos.grp;
+                        const int ig = ppos.ig;
 #pragma unroll
                         for (int j = 0; j < 8; ++j) pacc[j] = (ig == 0 ? 0.f : pacc[j]) + to_f<T>(from_f<T>(o2[j]));
                         if (ig == p.pool_hw - 1) {
