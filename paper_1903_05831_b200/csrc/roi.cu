@@ -763,6 +763,46 @@ __global__ void maxpool_fwd_kernel(const T* __restrict__ x, int N, int H, int W,
     }
 }
 
+// the stem pool forward (k 3, s 2, p 1): one CTA row per output row (n, oh),
+// threads over (ow, 8-channel group) -- no per-element division chains; the
+// same window order and tie rule as maxpool_fwd_kernel (first maximum in
+// (r, q) order, padding taps skipped)
+template <class T>
+__global__ void __launch_bounds__(256) maxpool_fwd_k3s2_kernel(const T* __restrict__ x, int H, int W, int C8, int Ho,
+                                                               int Wo, T* __restrict__ y, uint8_t* __restrict__ am) {
+    const int orow = blockIdx.y;  // n * Ho + oh
+    const int n = orow / Ho, oh = orow - n * Ho;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int ow = t / C8, c8 = t - ow * C8;
+    if (ow >= Wo) return;
+    float m[8];
+    int at[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { m[j] = -INFINITY; at[j] = -1; }
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+        const int ih = 2 * oh - 1 + r;
+        if (ih < 0 || ih >= H) continue;
+        const T* xr = x + (static_cast<int64_t>(n) * H + ih) * W * C8 * 8;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            const int iw = 2 * ow - 1 + q;
+            if (iw < 0 || iw >= W) continue;
+            float v[8];
+            ld8<T>(xr + (static_cast<int64_t>(iw) * C8 + c8) * 8, v);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (at[j] < 0 || v[j] > m[j]) { m[j] = v[j]; at[j] = r * 3 + q; }
+        }
+    }
+    const int64_t e = (static_cast<int64_t>(orow) * Wo + ow) * C8 + c8;
+    st8<T>(y + e * 8, m);
+    uint64_t pk = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) pk |= static_cast<uint64_t>(at[j] & 0xff) << (8 * j);
+    reinterpret_cast<uint64_t*>(am)[e] = pk;
+}
+
 template <class T, class I>
 __global__ void maxpool_bwd_kernel(const T* __restrict__ dy, const uint8_t* __restrict__ am, int N, int H, int W, int C,
                                    int k, int s, int p, int Ho, int Wo, T* __restrict__ dx) {
@@ -1492,6 +1532,17 @@ cudaError_t maxpool_fwd(int dtype, const void* x, int N, int H, int W, int C, in
                         uint8_t* argmax, cudaStream_t st) {
     const int Ho = (H + 2 * p - k) / s + 1, Wo = (W + 2 * p - k) / s + 1;
     const int64_t total = static_cast<int64_t>(N) * Ho * Wo * (C / 8);
+    static const bool generic = std::getenv("SDB_MAXPOOL_GENERIC") != nullptr;  // A/B switch
+    if (k == 3 && s == 2 && p == 1 && static_cast<int64_t>(N) * Ho < 65536 && !generic) {
+        const dim3 grid((Wo * (C / 8) + 255) / 256, N * Ho);
+        if (dtype == kF16)
+            maxpool_fwd_k3s2_kernel<__half><<<grid, 256, 0, st>>>(cp<__half>(x), H, W, C / 8, Ho, Wo,
+                                                                  static_cast<__half*>(y), argmax);
+        else
+            maxpool_fwd_k3s2_kernel<float><<<grid, 256, 0, st>>>(cp<float>(x), H, W, C / 8, Ho, Wo,
+                                                                 static_cast<float*>(y), argmax);
+        return cudaGetLastError();
+    }
     if (dtype == kF16)
         launch_idx(total, [&](auto idx) {
             maxpool_fwd_kernel<__half, decltype(idx)><<<grid_for(total), 256, 0, st>>>(
