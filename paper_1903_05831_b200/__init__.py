@@ -14,7 +14,8 @@ import os
 import re
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsdb.so")
+# SDB_LIB: diagnostic override (A/B of two builds, tools/step_digest.py)
+LIB_PATH = os.environ.get("SDB_LIB") or os.path.join(_HERE, "libsdb.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "sdb.h")
 
 F32 = 0

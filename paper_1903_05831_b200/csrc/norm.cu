@@ -52,6 +52,43 @@ SDB_DEV void load8<float>(const float* p, float (&v)[8]) {
     const float4 b = *reinterpret_cast<const float4*>(p + 4);
     v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
 }
+// Packed fp32 pairs (sm_100 add/mul.rn.f32x2): each lane is exactly the scalar
+// round-to-nearest operation, so the IABN expressions below stay bit-identical
+// to their scalar forms (a - b is issued as a + (-b), x * k2 subtracted as
+// x * (-k2): both exact sign identities) at half the FP32 instruction count.
+// ptxas (12.9) contracts a packed multiply feeding a packed add into FFMA2
+// (one rounding instead of two) even for explicit mul.rn/add.rn.f32x2 PTX and
+// -fmad=false; a packed product feeding SCALAR add.rn stays two roundings.
+// So: add2 only where no product feeds it, add2s (two scalar adds) after a
+// product.
+SDB_DEV float2 mul2(float2 a, float2 b) {
+    uint64_t r;
+    asm("mul.rn.f32x2 %0, %1, %2;"
+        : "=l"(r)
+        : "l"(*reinterpret_cast<const uint64_t*>(&a)), "l"(*reinterpret_cast<const uint64_t*>(&b)));
+    return *reinterpret_cast<const float2*>(&r);
+}
+SDB_DEV float2 add2(float2 a, float2 b) {
+    uint64_t r;
+    asm("add.rn.f32x2 %0, %1, %2;"
+        : "=l"(r)
+        : "l"(*reinterpret_cast<const uint64_t*>(&a)), "l"(*reinterpret_cast<const uint64_t*>(&b)));
+    return *reinterpret_cast<const float2*>(&r);
+}
+SDB_DEV float2 add2s(float2 a, float2 b) { return make_float2(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y)); }
+SDB_DEV float2 pair(const float (&v)[8], int j) { return make_float2(v[j], v[j + 1]); }
+
+// InPlace-ABN backward for channels j, j+1 of one row (memopt.cpp:278-327):
+// z = y >= 0 ? y : y / slope (as y * (1/slope)), dz = dy * (y > 0 ? 1 : slope),
+// xhat = (z - beta) * (1/gamma)
+SDB_DEV void iabn_bwd_pair(const float (&y)[8], const float (&dy)[8], int j, float2 inv_slope2, float slope,
+                           float2 nbeta, float2 igamma, float2& dz, float2& xh) {
+    const float2 ys = mul2(pair(y, j), inv_slope2);
+    const float2 z = make_float2(y[j] >= 0.f ? y[j] : ys.x, y[j + 1] >= 0.f ? y[j + 1] : ys.y);
+    dz = mul2(pair(dy, j), make_float2(y[j] > 0.f ? 1.f : slope, y[j + 1] > 0.f ? 1.f : slope));
+    xh = mul2(add2(z, nbeta), igamma);
+}
+
 template <class T>
 SDB_DEV void store8(T* p, const float (&v)[8]);
 template <>
@@ -227,11 +264,12 @@ __global__ void __launch_bounds__(kStatThreads, 2) stats_kernel(StatArgs p) {
                 g[j] = p.gamma[c0 + j];
                 is[j] = p.invstd[c0 + j];
                 mu[j] = KIND == 1 ? p.mean[c0 + j] : 0.f;
-                b[j] = KIND >= 2 ? p.beta[c0 + j] : 0.f;
-                if (KIND >= 2) g[j] = 1.0f / g[j];  // xhat = (z - beta) * (1/gamma)
+                b[j] = KIND >= 2 ? -p.beta[c0 + j] : 0.f;  // negated: z + (-beta)
+                if (KIND >= 2) g[j] = 1.0f / g[j];          // xhat = (z - beta) * (1/gamma)
             }
         }
         const float inv_slope = 1.0f / p.slope;
+        const float2 inv_slope2 = make_float2(inv_slope, inv_slope);
         PooledCache pcache;  // KIND 4
         // Every element is accumulated in fp64 exactly as the reference does
         // (syncbn.cpp:29-39, memopt.cpp:250-258 / 305-314): the float value
@@ -278,13 +316,13 @@ __global__ void __launch_bounds__(kStatThreads, 2) stats_kernel(StatArgs p) {
                     }
                 } else {
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        const float yv = v[j];
-                        const float z = yv >= 0.f ? yv : __fmul_rn(yv, inv_slope);
-                        const float dz = __fmul_rn(dd[j], yv > 0.f ? 1.f : p.slope);
-                        const float xh = __fmul_rn(__fsub_rn(z, b[j]), g[j]);
-                        S[j] = __dadd_rn(S[j], static_cast<double>(dz));
-                        Q[j] = __fma_rn(static_cast<double>(dz), static_cast<double>(xh), Q[j]);
+                    for (int j = 0; j < 8; j += 2) {
+                        float2 dz, xh;
+                        iabn_bwd_pair(v, dd, j, inv_slope2, p.slope, pair(b, j), pair(g, j), dz, xh);
+                        S[j] = __dadd_rn(S[j], static_cast<double>(dz.x));
+                        Q[j] = __fma_rn(static_cast<double>(dz.x), static_cast<double>(xh.x), Q[j]);
+                        S[j + 1] = __dadd_rn(S[j + 1], static_cast<double>(dz.y));
+                        Q[j + 1] = __fma_rn(static_cast<double>(dz.y), static_cast<double>(xh.y), Q[j + 1]);
                     }
                 }
             }
@@ -510,13 +548,19 @@ __global__ void __launch_bounds__(kStatThreads, 2) apply_kernel(ApplyArgs p, int
         ldf8(p.coef + c0, k1);
         ldf8(p.coef + C + c0, k2);
     }
-    float ig[8], gis[8];
+    float ig[8], gis[8], nmu[8], nb[8], nk1[8], nk2[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
         ig[j] = 1.0f / g[j];
         gis[j] = __fmul_rn(g[j], is[j]);
+        nmu[j] = KIND != 3 && KIND != 7 ? -mu[j] : 0.f;
+        nb[j] = KIND != 2 ? -b[j] : 0.f;
+        nk1[j] = KIND >= 2 ? -k1[j] : 0.f;
+        nk2[j] = KIND >= 2 ? -k2[j] : 0.f;
     }
     const float inv_slope = 1.0f / p.slope;
+    const float2 inv_slope2 = make_float2(inv_slope, inv_slope);
+    const float2 slope2 = make_float2(p.slope, p.slope);
     T* out = static_cast<T*>(p.out);
     float pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // KIND 6: this thread's channels, rows in order
     PooledCache pcache;                        // KIND 7
@@ -535,11 +579,18 @@ __global__ void __launch_bounds__(kStatThreads, 2) apply_kernel(ApplyArgs p, int
             load8<T>(ta + off, v);
             if (KIND == 0 || KIND == 1 || KIND == 4 || KIND == 6) {
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
+                for (int j = 0; j < 8; j += 2) {
                     // gamma*(x-mean)*invstd + beta, evaluated like the reference (no contraction)
-                    const float z = __fadd_rn(__fmul_rn(__fmul_rn(g[j], __fsub_rn(v[j], mu[j])), is[j]), b[j]);
-                    if (KIND == 0) o[j] = (p.act && !(z > 0.f)) ? 0.f : z;
-                    else o[j] = z > 0.f ? z : __fmul_rn(p.slope, z);
+                    const float2 z =
+                        add2s(mul2(mul2(pair(g, j), add2(pair(v, j), pair(nmu, j))), pair(is, j)), pair(b, j));
+                    if (KIND == 0) {
+                        o[j] = (p.act && !(z.x > 0.f)) ? 0.f : z.x;
+                        o[j + 1] = (p.act && !(z.y > 0.f)) ? 0.f : z.y;
+                    } else {
+                        const float2 zs = mul2(slope2, z);
+                        o[j] = z.x > 0.f ? z.x : zs.x;
+                        o[j + 1] = z.y > 0.f ? z.y : zs.y;
+                    }
                 }
                 if (KIND == 4 || KIND == 6) {
                     // residual node: s = round(round(y) + shortcut) (src/tensor.cpp:125), then
@@ -599,12 +650,14 @@ __global__ void __launch_bounds__(kStatThreads, 2) apply_kernel(ApplyArgs p, int
                     }
                 } else {
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        const float yv = v[j];
-                        const float z = yv >= 0.f ? yv : __fmul_rn(yv, inv_slope);
-                        const float dz = __fmul_rn(d[j], yv > 0.f ? 1.f : p.slope);
-                        const float xh = __fmul_rn(__fsub_rn(z, b[j]), ig[j]);
-                        o[j] = __fmul_rn(gis[j], __fsub_rn(__fsub_rn(dz, k1[j]), __fmul_rn(xh, k2[j])));
+                    for (int j = 0; j < 8; j += 2) {
+                        // gis * ((dz - s1) - xh * s2) (memopt.cpp:318-322), no contraction
+                        float2 dz, xh;
+                        iabn_bwd_pair(v, d, j, inv_slope2, p.slope, pair(nb, j), pair(ig, j), dz, xh);
+                        const float2 r =
+                            mul2(pair(gis, j), add2s(add2s(dz, pair(nk1, j)), mul2(xh, pair(nk2, j))));
+                        o[j] = r.x;
+                        o[j + 1] = r.y;
                     }
                 }
             }
