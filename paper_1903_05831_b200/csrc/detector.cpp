@@ -212,7 +212,8 @@ struct sdb_det {
     // the deferred wgrads run on a side stream, overlapping the dgrad -> norm
     // backward chain; each takes its dz from a ring whose slots are recycled
     // only after the wgrad that read them has finished
-    static constexpr int kDzRing = 6;
+    static constexpr int kDzRing = 64;  // capacity; dzr_n slots in use
+    int dzr_n = 6;
     bool side_wgrad = false;
     // the last RoI-head block's output is average-pooled inside its apply pass
     // and never stored (only its sign bitmap); head_out is then not materialised
@@ -767,7 +768,7 @@ void* dz_buf(Bwd& B, void* fallback) {
     sdb_det* d = B.d;
     if (!B.side) return fallback;
     const int k = d->dzr_next;
-    d->dzr_next = (k + 1) % sdb_det::kDzRing;
+    d->dzr_next = (k + 1) % d->dzr_n;
     if (d->dzr_busy[k]) CK(cudaStreamWaitEvent(d->ctx->stream, d->dzr_ev[k], 0));
     d->dzr_busy[k] = false;
     B.slot = k;
@@ -1562,7 +1563,8 @@ int sdb_det_create(sdb_ctx* ctx, const sdb_det_config* cfgp, sdb_det** out) {
             CK(cudaEventCreateWithFlags(&d->ev_rpn_join, cudaEventDisableTiming));
             d->drpn_side = d->alloc(static_cast<size_t>(d->rpn_a.numel()) * d->es);
             d->ws_at = d->alloc(anchor_target_workspace_bytes(cf.batch, d->nA, cf.max_gt));
-            for (int k = 0; k < sdb_det::kDzRing; ++k) {
+            if (const char* e = std::getenv("SDB_DZ_RING")) d->dzr_n = std::max(2, std::min(sdb_det::kDzRing, std::atoi(e)));
+            for (int k = 0; k < d->dzr_n; ++k) {
                 d->dzr[k] = d->alloc(static_cast<size_t>(d->gbuf_elems) * d->es);
                 CK(cudaEventCreateWithFlags(&d->dzr_ev[k], cudaEventDisableTiming));
             }
@@ -1661,7 +1663,8 @@ int sdb_det_destroy(sdb_det* d) {
     }
     for (auto e : d->bucket_ev) cudaEventDestroy(e);
     if (d->wst) {
-        for (auto e : d->dzr_ev) cudaEventDestroy(e);
+        for (auto e : d->dzr_ev)
+            if (e) cudaEventDestroy(e);
         cudaEventDestroy(d->wev_fork);
         cudaEventDestroy(d->wev_join);
         cudaEventDestroy(d->ev_at_fork);
