@@ -21,6 +21,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+
+#include <nvtx3/nvToolsExt.h>
 #include <fstream>
 #include <stdexcept>
 #include <string>
@@ -393,6 +395,7 @@ struct PScope {
     }
     ~PScope() {
         if (!e0) return;
+        if (nvtx) nvtxRangePop();
         cudaEvent_t e1 = d->prof.get();
         cudaEventRecord(e1, d->ctx->stream);
         d->prof.recs.push_back({cat, {e0, e1}});
@@ -400,8 +403,19 @@ struct PScope {
         d->prof.rec_flops.push_back(flops_);
         d->prof.rec_bytes.push_back(bytes_);
     }
+    // the record's label; while profiling it also names an NVTX range around
+    // the scope's launches (ncu --nvtx --print-nvtx-rename kernel: per-layer
+    // counters, tools/ncu_conv_pipe.py)
+    void set(std::string l) {
+        label = std::move(l);
+        if (e0 && !nvtx) {
+            nvtxRangePushA(label.c_str());
+            nvtx = true;
+        }
+    }
     std::string label;
     double flops_ = 0, bytes_ = 0;
+    bool nvtx = false;
 };
 
 std::string shape_label(const char* what, const ConvShape& g) {
@@ -577,7 +591,7 @@ size_t max_ws(sdb_det* d) {
 // ------------------------------------------------------------------ forward helpers
 void conv_fwd(sdb_det* d, const ConvL& c, const Act& x, const Act& y, bool want_stats = false) {
     PScope ps(d, P_FPROP, conv_flops(c.g));
-    if (d->prof.on) { ps.label = shape_label("fprop", c.g); ps.flops_ = conv_flops(c.g); }
+    if (d->prof.on) { ps.set(shape_label("fprop", c.g)); ps.flops_ = conv_flops(c.g); }
     CK(conv_fprop(c.g, d->dt, x.p, d->wdev_ptr(c.p), y.p, d->ctx->stream,
                   want_stats && d->cst.buf ? &d->cst : nullptr));
     if (!(want_stats && d->cst.buf)) d->cst.produced = 0;
@@ -589,7 +603,7 @@ void norm_fwd(sdb_det* d, const NormL& n, const Act& z, const Act& a) {
         // statistics came out of the producing fprop's epilogue: finalize + apply
         PScope ps(d, P_NORM_F, 0, 2.0 * d->es * z.numel(), 2);
         if (d->prof.on && std::getenv("SDB_PROFILE_VERBOSE")) {
-            ps.label = "norm_fwd(fused stats) rows " + std::to_string(rows) + " C " + std::to_string(n.C);
+            ps.set("norm_fwd(fused stats) rows " + std::to_string(rows) + " C " + std::to_string(n.C));
             ps.bytes_ = 2.0 * d->es * z.numel();
         }
         CK(bn_forward_conv_stats(d->dt, z.p, d->bnp(n.pg), d->bnp(n.pb), a.p, n.mean, n.invstd, rows, n.C, d->cfg.eps,
@@ -599,7 +613,7 @@ void norm_fwd(sdb_det* d, const NormL& n, const Act& z, const Act& a) {
     }
     PScope ps(d, P_NORM_F, 0, 2.0 * d->es * z.numel(), 3);
     if (d->prof.on && std::getenv("SDB_PROFILE_VERBOSE")) {
-        ps.label = "norm_fwd rows " + std::to_string(rows) + " C " + std::to_string(n.C);
+        ps.set("norm_fwd rows " + std::to_string(rows) + " C " + std::to_string(n.C));
         ps.bytes_ = 3.0 * d->es * z.numel();
     }
     if (n.agg) {
@@ -620,7 +634,7 @@ void norm_bwd(sdb_det* d, const NormL& n, const Act& z, const Act& a, const void
     const int64_t rows = static_cast<int64_t>(z.n) * z.h * z.w;
     PScope ps(d, P_NORM_B, 0, 3.0 * d->es * z.numel(), 3);
     if (d->prof.on && std::getenv("SDB_PROFILE_VERBOSE")) {
-        ps.label = "norm_bwd rows " + std::to_string(rows) + " C " + std::to_string(n.C);
+        ps.set("norm_bwd rows " + std::to_string(rows) + " C " + std::to_string(n.C));
         ps.bytes_ = 5.0 * d->es * z.numel();
     }
     if (n.agg) {
@@ -681,8 +695,8 @@ void block_fwd(sdb_det* d, Block& b) {
         {
             PScope ps(d, P_NORM_F, 0, 1.0 * d->es * b.z3.numel(), 2);
             if (d->prof.on && std::getenv("SDB_PROFILE_VERBOSE")) {
-                ps.label = std::string(d->cst.produced ? "norm_stats3(fused) rows " : "norm_stats3 rows ") +
-                           std::to_string(rows) + " C " + std::to_string(b.n3.C);
+                ps.set(std::string(d->cst.produced ? "norm_stats3(fused) rows " : "norm_stats3 rows ") +
+                       std::to_string(rows) + " C " + std::to_string(b.n3.C));
                 ps.bytes_ = 1.0 * d->es * b.z3.numel();
             }
             if (d->cst.produced) {
@@ -706,7 +720,7 @@ void block_fwd(sdb_det* d, Block& b) {
         }
         PScope ps(d, P_NORM_F, 0, 4.0 * d->es * b.out.numel());
         if (d->prof.on && std::getenv("SDB_PROFILE_VERBOSE")) {
-            ps.label = "norm_apply_add rows " + std::to_string(rows) + " C " + std::to_string(b.n3.C);
+            ps.set("norm_apply_add rows " + std::to_string(rows) + " C " + std::to_string(b.n3.C));
             ps.bytes_ = 4.0 * d->es * b.out.numel();
         }
         if (d->head_pool_fuse && &b == &d->head.back()) {
@@ -736,7 +750,7 @@ void dgrad(sdb_det* d, const ConvL& c, const void* dy, void* dx, int accumulate,
            ConvStats* bstats = nullptr) {
     PScope ps(d, P_DGRAD, conv_flops(c.g), 0, c.g.stride * c.g.stride);
     if (d->prof.on) {
-        ps.label = shape_label(mask_bits ? "dgrad+res" : (bstats ? "dgrad+bstats" : "dgrad"), c.g);
+        ps.set(shape_label(mask_bits ? "dgrad+res" : (bstats ? "dgrad+bstats" : "dgrad"), c.g));
         ps.flops_ = conv_flops(c.g);
     }
     CK(conv_dgrad(c.g, d->dt, dy, d->wdev_ptr(c.p), dx, accumulate, d->ctx->stream, addend, mask, mask_neg,
@@ -858,7 +872,7 @@ void conv_wgrad_to(Bwd& B, const ConvL& c, const Act& x, const void* dy, void* d
     void* dwp = dw_override ? dw_override : d->gptr(c.p);
     {
     PScope ps(d, P_WGRAD, conv_flops(c.g), 0, 2);
-    if (d->prof.on) { ps.label = shape_label("wgrad", c.g); ps.flops_ = conv_flops(c.g); }
+    if (d->prof.on) { ps.set(shape_label("wgrad", c.g)); ps.flops_ = conv_flops(c.g); }
     if (d->defer_wgrad) {
         auto it = d->wg_off.find(c.p);
         if (it == d->wg_off.end()) throw std::runtime_error("wgrad arena: unknown conv");
@@ -1028,13 +1042,13 @@ void run_step(sdb_det* d) {
     if (d->stem_gemm) {
         {
             PScope ps(d, P_ELEM, 0, 2.0 * (d->img.numel() + static_cast<double>(d->stem2.g.W) * 192), 3);
-            if (d->prof.on) ps.label = "stem im2col + weight pack";
+            if (d->prof.on) ps.set("stem im2col + weight pack");
             CK(stem_weights(d->wdev_ptr(d->stem.p), 64, 8, d->stem_w2, 0, st));
             CK(stem_im2col(d->img.p, d->img.n, d->img.h, d->img.w, 8, d->stem_z.h, d->stem_z.w, 2, 3, d->stem_x2,
                            st));
         }
         PScope ps(d, P_FPROP, conv_flops(d->stem2.g));
-        if (d->prof.on) { ps.label = shape_label("fprop(stem gemm)", d->stem2.g); ps.flops_ = conv_flops(d->stem2.g); }
+        if (d->prof.on) { ps.set(shape_label("fprop(stem gemm)", d->stem2.g)); ps.flops_ = conv_flops(d->stem2.g); }
         CK(conv_fprop(d->stem2.g, d->dt, d->stem_x2, d->stem_w2, d->stem_z.p, st, d->cst.buf ? &d->cst : nullptr));
     } else {
         conv_fwd(d, d->stem, d->img, d->stem_z, true);
