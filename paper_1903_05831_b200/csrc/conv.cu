@@ -1016,19 +1016,6 @@ SDB_DEV void tma_im2col_4d(uint32_t dst, const void* map, uint64_t* bar, int c, 
         : "memory");
 }
 
-// multicast twin: the box lands at `dst` (and completes the mbarrier at the
-// same offset) in every CTA of the cluster named by `mask`
-SDB_DEV void tma_im2col_4d_mc(uint32_t dst, const void* map, uint64_t* bar, int c, int w, int h, int n, int off_w,
-                              int off_h, uint16_t mask) {
-    const uint16_t ow = static_cast<uint16_t>(off_w), oh = static_cast<uint16_t>(off_h);
-    asm volatile(
-        "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes.multicast::cluster [%0], "
-        "[%1, {%3, %4, %5, %6}], [%2], {%7, %8}, %9;" ::"r"(dst),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c), "r"(w), "r"(h), "r"(n), "h"(ow), "h"(oh),
-        "h"(mask)
-        : "memory");
-}
-
 // BN = 256: 8 epilogue warps (two per TMEM lane quadrant, 128 columns each,
 // 32-column steps) -- or EW = 16 (four per quadrant, 64 columns each) for the
 // fprops whose epilogue also reduces the norm statistics, which is then the
@@ -1050,11 +1037,7 @@ struct TmaCfg {
     static constexpr int kPerSM = BN <= 128 ? 2 : 1;
 };
 
-// MC = 2 (fprop / dgrad): a cluster of two CTAs on the two column tiles of one
-// row tile shares the activation operand -- each CTA loads half of the A box
-// and multicasts it into both, so a k-block costs each SM half an A box plus
-// its own B box; both MMA warps release a stage to both producers.
-template <int MODE, int BN, int ST, int EPI = 0, int EW = (BN == 256 ? 8 : 4), int MC = 1>
+template <int MODE, int BN, int ST, int EPI = 0, int EW = (BN == 256 ? 8 : 4)>
 __global__ void __launch_bounds__(TmaCfg<MODE, BN, ST, EPI, EW>::kThreads, (BN <= 128) ? 2 : 1)
     conv_tma_kernel(ConvArgs a, int tiles_m, int tiles_n, int n_tiles, const __grid_constant__ TmaPair tm) {
     using Cfg = TmaCfg<MODE, BN, ST, EPI, EW>;
@@ -1079,7 +1062,7 @@ __global__ void __launch_bounds__(TmaCfg<MODE, BN, ST, EPI, EW>::kThreads, (BN <
         if (EPI) prefetch_tmap(&tm.r);
         for (int s = 0; s < ST; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], MC);
+            mbar_init(&empty[s], 1);
         }
         for (int i = 0; i < (EPI ? 2 * Cfg::kEpiWarps : 0); ++i) mbar_init(&rbar[i], 1);
         for (int i = 0; i < 2; ++i) {
@@ -1091,7 +1074,6 @@ __global__ void __launch_bounds__(TmaCfg<MODE, BN, ST, EPI, EW>::kThreads, (BN <
     if (warp == 1) tmem_alloc(tmem_slot, 2 * BN);
     tc_fence_before();
     __syncthreads();
-    if constexpr (MC > 1) cluster_sync();  // the peer's barriers exist before any multicast reaches them
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     // everything above overlapped the previous kernel's tail (PDL)
@@ -1132,23 +1114,20 @@ __global__ void __launch_bounds__(TmaCfg<MODE, BN, ST, EPI, EW>::kThreads, (BN <
             const int HoWo = a.Ho * a.Wo;
             // wgrad: a k-block is 64 consecutive output pixels; 64 = dn*HoWo + doh*Wo + dow
             const int dn = kBK / HoWo, drem = kBK - dn * HoWo, doh = drem / a.Wo, dow = drem - doh * a.Wo;
-            const int crank = MC > 1 ? static_cast<int>(cluster_ctarank()) : 0;
-            constexpr uint32_t kAHalf = Cfg::kABytes / MC;  // this CTA's slice of the A box
             int it = 0;
             for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
                 int m0, n0, kb0, nk;
                 tile_coords(t, m0, n0, kb0, nk);
                 // im2col base of the tile's first output pixel (fprop / dgrad)
                 int bw = 0, bh = 0, bn = 0;
-                const int mA = m0 + crank * (kBM / MC);  // first row of this CTA's A slice
                 if (MODE == FPROP) {
-                    const int n = mA / HoWo, rem = mA - n * HoWo, oh = rem / a.Wo, ow = rem - oh * a.Wo;
+                    const int n = m0 / HoWo, rem = m0 - n * HoWo, oh = rem / a.Wo, ow = rem - oh * a.Wo;
                     bn = n;
                     bh = oh * a.stride - a.pad;
                     bw = ow * a.stride - a.pad;
                 } else if (MODE == DGRAD) {
                     const int HpWp = a.Hp * a.Wp;
-                    const int n = mA / HpWp, rem = mA - n * HpWp, i2 = rem / a.Wp, j2 = rem - i2 * a.Wp;
+                    const int n = m0 / HpWp, rem = m0 - n * HpWp, i2 = rem / a.Wp, j2 = rem - i2 * a.Wp;
                     bn = n;
                     // DY row of phase pixel i2 for tap ti: i2 + cy - ti; base shifted by (nr-1) so the
                     // per-tap offset (nr-1-ti) is non-negative
@@ -1185,13 +1164,8 @@ __global__ void __launch_bounds__(TmaCfg<MODE, BN, ST, EPI, EW>::kThreads, (BN <
                     const int kg0 = (kb0 + k) * kBK;
                     mbar_arrive_expect_tx(&full[s], Cfg::kStage);
                     if (MODE == FPROP) {
-                        if constexpr (MC > 1) {
-                            if (a.plain) tma_load_2d_mc(sa + crank * kAHalf, &tm.a, &full[s], kg0, mA, 3);
-                            else tma_im2col_4d_mc(sa + crank * kAHalf, &tm.a, &full[s], c0, bw, bh, bn, t1, t0, 3);
-                        } else {
-                            if (a.plain) tma_load_2d(sa, &tm.a, &full[s], kg0, m0);
-                            else tma_im2col_4d(sa, &tm.a, &full[s], c0, bw, bh, bn, t1, t0);
-                        }
+                        if (a.plain) tma_load_2d(sa, &tm.a, &full[s], kg0, m0);
+                        else tma_im2col_4d(sa, &tm.a, &full[s], c0, bw, bh, bn, t1, t0);
                         tma_load_2d(sb, &tm.b, &full[s], kg0, n0);
                         // next (r, q, c): c += 64 with carries into q then r
                         c0 += kBK;
@@ -1204,15 +1178,8 @@ __global__ void __launch_bounds__(TmaCfg<MODE, BN, ST, EPI, EW>::kThreads, (BN <
                         }
                     } else if (MODE == DGRAD) {
                         // (t0, t1) = (ti, tq), c0 = kout
-                        if constexpr (MC > 1) {
-                            if (a.plain) tma_load_2d_mc(sa + crank * kAHalf, &tm.a, &full[s], c0, mA, 3);
-                            else
-                                tma_im2col_4d_mc(sa + crank * kAHalf, &tm.a, &full[s], c0, bw, bh, bn, a.nq - 1 - t1,
-                                                 a.nr - 1 - t0, 3);
-                        } else {
-                            if (a.plain) tma_load_2d(sa, &tm.a, &full[s], c0, m0);
-                            else tma_im2col_4d(sa, &tm.a, &full[s], c0, bw, bh, bn, a.nq - 1 - t1, a.nr - 1 - t0);
-                        }
+                        if (a.plain) tma_load_2d(sa, &tm.a, &full[s], c0, m0);
+                        else tma_im2col_4d(sa, &tm.a, &full[s], c0, bw, bh, bn, a.nq - 1 - t1, a.nr - 1 - t0);
                         const int r2 = a.r0 + a.stride * t0, q2 = a.q0 + a.stride * t1;
 #pragma unroll
                         for (int g = 0; g < BN / 64; ++g)
@@ -1279,8 +1246,7 @@ __global__ void __launch_bounds__(TmaCfg<MODE, BN, ST, EPI, EW>::kThreads, (BN <
                                                  : umma_desc_sw128(sb + kk * 32, 16, 1024);
                         umma_f16(dcol, ad, bd, idesc, (k > 0 || kk > 0) ? 1u : 0u);
                     }
-                    if constexpr (MC > 1) umma_commit_mc(&empty[s], 3);
-                    else umma_commit(&empty[s]);
+                    umma_commit(&empty[s]);
                 }
                 umma_commit(&tfull[acc]);
             }
@@ -1386,7 +1352,6 @@ __global__ void __launch_bounds__(TmaCfg<MODE, BN, ST, EPI, EW>::kThreads, (BN <
     }
     tc_fence_before();
     __syncthreads();
-    if constexpr (MC > 1) cluster_sync();  // no CTA leaves while its peer may still signal it
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc(tmem, 2 * BN);
@@ -1809,44 +1774,18 @@ static bool tma_ok(const ConvArgs& a, int mode) {
     return (a.C % 64) == 0;
 }
 
-template <int MODE, int BN, int ST, int EPI = 0, int EW = (BN == 256 ? 8 : 4), int MC = 1>
+template <int MODE, int BN, int ST, int EPI = 0, int EW = (BN == 256 ? 8 : 4)>
 static cudaError_t launch_tma(ConvArgs a, int splits, cudaStream_t st, ConvStats* cst = nullptr) {
     using Cfg = TmaCfg<MODE, BN, ST, EPI, EW>;
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(conv_tma_kernel<MODE, BN, ST, EPI, EW, MC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(conv_tma_kernel<MODE, BN, ST, EPI, EW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              Cfg::kSmem);
         configured = true;
     }
     const int tiles_m = (a.M + kBM - 1) / kBM, tiles_n = (a.NG + BN - 1) / BN;
     const int n_tiles = tiles_m * tiles_n * splits;
     int grid = std::min(n_tiles, Cfg::kPerSM * kNumSMs);
-    // CTA pairs: the two column tiles of a row tile on the two CTAs of a cluster
-    // (n-fastest tiles, even grid: CTA 2c+r always holds column tiles of parity r)
-    if (MC > 1 && (tiles_n % MC != 0 || MODE == WGRAD)) return cudaErrorInvalidValue;
-    if (MC > 1) {
-        // persistent CTAs: only as many pairs as can be resident at once (a
-        // GPC's odd SM is left out), else the surplus pairs would run after
-        static const int max_pairs = [] {
-            cudaLaunchConfig_t cfg = {};
-            cfg.gridDim = dim3(2 * kNumSMs);
-            cfg.blockDim = dim3(Cfg::kThreads);
-            cfg.dynamicSmemBytes = Cfg::kSmem;
-            cudaLaunchAttribute attr[1];
-            attr[0].id = cudaLaunchAttributeClusterDimension;
-            attr[0].val.clusterDim.x = MC;
-            attr[0].val.clusterDim.y = 1;
-            attr[0].val.clusterDim.z = 1;
-            cfg.attrs = attr;
-            cfg.numAttrs = 1;
-            int n = 0;
-            if (cudaOccupancyMaxActiveClusters(&n, conv_tma_kernel<MODE, BN, ST, EPI, EW, MC>, &cfg) != cudaSuccess)
-                n = Cfg::kPerSM * kNumSMs / MC;
-            return n;
-        }();
-        grid = std::min(grid, max_pairs * MC);
-        grid -= grid % MC;
-    }
     // fused output statistics need every CTA on one column block (grid a
     // multiple of tiles_n): e.g. the res5 expansion convs (tiles_n = 8) give up
     // 4 of 148 CTAs (< 3% of a ~80 us GEMM) to save a 50 us statistics pass
@@ -1869,9 +1808,9 @@ static cudaError_t launch_tma(ConvArgs a, int splits, cudaStream_t st, ConvStats
         return make_tmap(m, p, 2, dims, strides, box);
     };
     if (MODE == FPROP) {
-        ok = a.plain ? plain_map(&tm.a, a.x, static_cast<int64_t>(a.N) * a.H * a.W, a.C, kBM / MC)
+        ok = a.plain ? plain_map(&tm.a, a.x, static_cast<int64_t>(a.N) * a.H * a.W, a.C, kBM)
                      : make_im2col(&tm.a, a.x, a.N, a.H, a.W, a.C, -a.pad, -a.pad, a.pad - (a.R - 1),
-                                   a.pad - (a.S - 1), a.stride, kBM / MC);
+                                   a.pad - (a.S - 1), a.stride, kBM);
         const uint64_t dims[2] = {static_cast<uint64_t>(a.KG), static_cast<uint64_t>(a.NG)};
         const uint64_t strides[1] = {static_cast<uint64_t>(a.KG) * 2};
         const uint32_t box[2] = {64, static_cast<uint32_t>(BN)};
@@ -1880,9 +1819,8 @@ static cudaError_t launch_tma(ConvArgs a, int splits, cudaStream_t st, ConvStats
         // DY over the phase grid: Hp x Wp output positions, base shifted by (nr-1, nq-1)
         const int lh = (a.ph + a.pad - a.r0) / a.stride - (a.nr - 1);
         const int lw = (a.pw + a.pad - a.q0) / a.stride - (a.nq - 1);
-        ok = a.plain ? plain_map(&tm.a, a.x, static_cast<int64_t>(a.N) * a.Ho * a.Wo, a.K, kBM / MC)
-                     : make_im2col(&tm.a, a.x, a.N, a.Ho, a.Wo, a.K, lh, lw, a.Hp - a.Ho + lh, a.Wp - a.Wo + lw, 1,
-                                   kBM / MC);
+        ok = a.plain ? plain_map(&tm.a, a.x, static_cast<int64_t>(a.N) * a.Ho * a.Wo, a.K, kBM)
+                     : make_im2col(&tm.a, a.x, a.N, a.Ho, a.Wo, a.K, lh, lw, a.Hp - a.Ho + lh, a.Wp - a.Wo + lw, 1, kBM);
         const uint64_t dims[3] = {static_cast<uint64_t>(a.C), static_cast<uint64_t>(a.R) * a.S, static_cast<uint64_t>(a.K)};
         const uint64_t strides[2] = {static_cast<uint64_t>(a.C) * 2, static_cast<uint64_t>(a.R) * a.S * a.C * 2};
         const uint32_t box[3] = {64, 1, 64};
@@ -1952,11 +1890,8 @@ static cudaError_t launch_tma(ConvArgs a, int splits, cudaStream_t st, ConvStats
             cst->bn = BN;
         }
         if (!ok) return cudaErrorInvalidValue;
-        if (MC > 1)
-            return launch_pdl_cluster(conv_tma_kernel<MODE, BN, ST, EPI, EW, MC>, dim3(grid), dim3(Cfg::kThreads),
-                                      Cfg::kSmem, st, MC, a, tiles_m, tiles_n, n_tiles, tm);
-        return launch_pdl(conv_tma_kernel<MODE, BN, ST, EPI, EW, MC>, dim3(grid), dim3(Cfg::kThreads), Cfg::kSmem, st,
-                          a, tiles_m, tiles_n, n_tiles, tm);
+        return launch_pdl(conv_tma_kernel<MODE, BN, ST, EPI, EW>, dim3(grid), dim3(Cfg::kThreads), Cfg::kSmem, st, a,
+                          tiles_m, tiles_n, n_tiles, tm);
     }
     if (!ok) return cudaErrorInvalidValue;
     a.stats = nullptr;
@@ -1973,11 +1908,8 @@ static cudaError_t launch_tma(ConvArgs a, int splits, cudaStream_t st, ConvStats
             cst->bn = BN;
         }
     }
-    if (MC > 1)
-        return launch_pdl_cluster(conv_tma_kernel<MODE, BN, ST, EPI, EW, MC>, dim3(grid), dim3(Cfg::kThreads),
-                                  Cfg::kSmem, st, MC, a, tiles_m, tiles_n, n_tiles, tm);
-    return launch_pdl(conv_tma_kernel<MODE, BN, ST, EPI, EW, MC>, dim3(grid), dim3(Cfg::kThreads), Cfg::kSmem, st, a,
-                      tiles_m, tiles_n, n_tiles, tm);
+    return launch_pdl(conv_tma_kernel<MODE, BN, ST, EPI, EW>, dim3(grid), dim3(Cfg::kThreads), Cfg::kSmem, st, a, tiles_m,
+                      tiles_n, n_tiles, tm);
 }
 
 // tile width: 256 when the GEMM N is wide enough (one CTA per SM, 2 x 256 TMEM
@@ -1997,14 +1929,6 @@ static int tma_bn(const ConvArgs& a, int mode = WGRAD) {
     return a.NG > 64 ? 128 : 64;
 }
 
-// CTA pairs sharing the activation operand (conv_tma_kernel MC = 2): fprop /
-// dgrad with an even number of column tiles
-template <int MODE>
-static bool pair_pays(const ConvArgs& a, int bn) {
-    static const bool on = std::getenv("SDB_CONV_MC") != nullptr;
-    return on && MODE != WGRAD && ((a.NG + bn - 1) / bn) % 2 == 0;
-}
-
 template <int MODE>
 static cudaError_t launch_tma_pick(const ConvArgs& a, int splits, cudaStream_t st, ConvStats* cst = nullptr) {
     switch (tma_bn(a, MODE)) {
@@ -2015,14 +1939,10 @@ static cudaError_t launch_tma_pick(const ConvArgs& a, int splits, cudaStream_t s
             // statistics 130 -> 121 us; at 32 k-blocks the 4th stage matters more)
             static const bool ew16 = std::getenv("SDB_NO_EPI16") == nullptr;
             if (MODE == FPROP && cst && ew16 && a.KG <= 16 * kBK)
-                return pair_pays<MODE>(a, 256) ? launch_tma<MODE, 256, 3, 0, 16, 2>(a, splits, st, cst)
-                                               : launch_tma<MODE, 256, 3, 0, 16>(a, splits, st, cst);
-            return pair_pays<MODE>(a, 256) ? launch_tma<MODE, 256, 4, 0, 8, 2>(a, splits, st, cst)
-                                           : launch_tma<MODE, 256, 4>(a, splits, st, cst);
+                return launch_tma<MODE, 256, 3, 0, 16>(a, splits, st, cst);
+            return launch_tma<MODE, 256, 4>(a, splits, st, cst);
         }
-        case 128:
-            return pair_pays<MODE>(a, 128) ? launch_tma<MODE, 128, 3, 0, 4, 2>(a, splits, st, cst)
-                                           : launch_tma<MODE, 128, 3>(a, splits, st, cst);
+        case 128: return launch_tma<MODE, 128, 3>(a, splits, st, cst);
         default: return launch_tma<MODE, 64, 4>(a, splits, st, cst);
     }
 }
@@ -2181,14 +2101,11 @@ cudaError_t conv_dgrad(const ConvShape& g, int dtype, const void* dy, const void
                     // BN <= 128 only: the 256-wide tile cannot keep its 4 mainloop stages
                     // next to the y ring, and 3 stages cost the res5 dgrads more than
                     // the statistics pass they save (measured)
-                    if (tma_bn(a, DGRAD) == 128)
-                        e = pair_pays<DGRAD>(a, 128) ? launch_tma<DGRAD, 128, 3, 2, 4, 2>(a, 1, st, bstats)
-                                                     : launch_tma<DGRAD, 128, 3, 2>(a, 1, st, bstats);
+                    if (tma_bn(a, DGRAD) == 128) e = launch_tma<DGRAD, 128, 3, 2>(a, 1, st, bstats);
                     else e = launch_tma<DGRAD, 64, 4, 2>(a, 1, st, bstats);
                 } else if (tma_ok(a, DGRAD) && a.mbits && a.accumulate && sd == 1 && tma_bn(a, DGRAD) == 256 &&
                            (g.C % 32) == 0 && !no_resid)
-                    e = pair_pays<DGRAD>(a, 256) ? launch_tma<DGRAD, 256, 3, 1, 8, 2>(a, 1, st)
-                                                 : launch_tma<DGRAD, 256, 3, 1>(a, 1, st);
+                    e = launch_tma<DGRAD, 256, 3, 1>(a, 1, st);
                 else
                     e = tma_ok(a, DGRAD) ? launch_tma_pick<DGRAD>(a, 1, st) : launch_tc_pick<DGRAD>(a, 1, st);
             } else {
