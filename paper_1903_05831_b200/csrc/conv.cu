@@ -1915,15 +1915,18 @@ static cudaError_t launch_tma(ConvArgs a, int splits, cudaStream_t st, ConvStats
 // tile width: 256 when the GEMM N is wide enough (one CTA per SM, 2 x 256 TMEM
 // columns), else 128 / 64 (two CTAs per SM)
 // fprop/dgrad: when 128x256 tiles would leave more than half of the 148 SMs
-// idle (small-M res4 layers with N = 256: 66 tiles), 128x128 tiles put one CTA
-// on twice as many SMs (measured 1.08-1.1x: the narrow tile needs 1.33x the
-// operand bytes per FLOP, so L2 bandwidth caps the gain; with 132 tiles it is a
-// loss).  wgrad fills the machine with split-K instead.
+// idle (small-M res4 layers with N = 256: 66 tiles), 128x64 tiles (264, two
+// CTAs per SM) -- these one-tile-per-CTA layers are latency-bound, not
+// L2-bound: two independent tile pipelines per SM hide each other's fill and
+// drain (ncu: 128x128 -> 128x64 0.78x on the fprops, 0.71x on the dgrads with
+// fused statistics; SDB_CONV_NARROW128 restores 128).  wgrad fills the machine
+// with split-K instead.
 static int tma_bn(const ConvArgs& a, int mode = WGRAD) {
     if (a.NG >= 256) {
         const int64_t tiles256 = static_cast<int64_t>((a.M + kBM - 1) / kBM) * ((a.NG + 255) / 256);
         static const bool no_narrow = std::getenv("SDB_CONV_NO_NARROW") != nullptr;
-        if (mode != WGRAD && 2 * tiles256 <= kNumSMs && !no_narrow) return 128;
+        static const bool bn128 = std::getenv("SDB_CONV_NARROW128") != nullptr;
+        if (mode != WGRAD && 2 * tiles256 <= kNumSMs && !no_narrow) return bn128 ? 128 : 64;
         return 256;
     }
     return a.NG > 64 ? 128 : 64;
